@@ -1,0 +1,270 @@
+// The event-driven dispatch contract, shared by the virtual-time simulator
+// (drop-in for the reference simulate()) and the CUDA executor.
+//
+// Reference: proj/src/simulator.cpp:108-344 (Dispatcher) and
+// proj/include/memplan/simulator.hpp:22-61 (profile, policy, trace types).
+// A vertex dispatches once every memgraph predecessor finished and its
+// resources are free (simulator.cpp:167-177):
+//   kernel   -> a free stream on its device + the device's compute token
+//   transfer -> a free stream on the destination device
+//   offload  -> a free stream + the device's host_out (D2H) channel
+//   reload   -> a free stream + the device's host_in (H2D) channel
+//   input    -> nothing (reference) | stream + host_in when the executor
+//               materialises inputs from pinned host memory (SURVEY hard part 3)
+// The ready list is re-ordered before every dispatch by the tie-break
+// (simulator.cpp:200-219) and the sweep restarts after each dispatch.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "types.hpp"
+
+namespace tn {
+
+enum class NoiseKind : std::uint8_t { None, Uniform, Lognormal };
+struct NoiseSpec {
+    NoiseKind kind = NoiseKind::None;
+    double param = 0.0;
+};
+
+struct DeviceProfile {
+    std::int32_t streams_per_device = 5;
+    double kernel_multiplier = 1.0;
+    double d2d_bandwidth = 1.0;
+    double host_link_bandwidth = 1.0;
+    double link_latency = 0.0;
+    NoiseSpec noise;
+    std::uint64_t seed = 0;
+};
+
+enum class SchedulerKind : std::uint8_t { EventDriven, FixedOrder };
+enum class TieBreak : std::uint8_t { Fifo, SeededRandom, LowestId };
+
+struct SchedulerPolicy {
+    SchedulerKind kind = SchedulerKind::EventDriven;
+    TieBreak tie_break = TieBreak::Fifo;
+};
+
+TieBreak tie_break_from_string(const std::string& s);
+SchedulerKind scheduler_kind_from_string(const std::string& s);
+
+struct TraceRow {
+    VertexId vertex = 0;
+    double start = 0.0;
+    double end = 0.0;
+    DeviceId device = 0;
+    std::int32_t stream = -1;
+};
+
+struct ExecutionTrace {
+    std::vector<TraceRow> rows;  // dispatch order
+    double makespan = 0.0;
+    std::vector<double> busy_time;
+    std::vector<double> idle_time;
+    std::vector<std::int64_t> peak_live;
+    std::int64_t host_bytes_transferred = 0;
+    std::string to_json() const;
+    std::string to_csv() const;
+};
+
+std::uint64_t mix64(std::uint64_t x);
+
+// Fills makespan / busy / idle / peak_live / host bytes from rows
+// (simulator.cpp:274-343).
+void finalize_trace(const MemGraph& m, const MemoryMap& map, ExecutionTrace& t);
+
+// Resource model (simulator.cpp:115-197) with two executor knobs:
+// `compute_tokens` (reference: 1) and `inputs_use_host_in`.
+class Resources {
+  public:
+    Resources(int devices, int streams_per_device, int compute_tokens, bool inputs_use_host_in)
+        : streams_(streams_per_device), inputs_(inputs_use_host_in), devs_(devices) {
+        for (auto& d : devs_) {
+            d.free_mask.assign((streams_per_device + 63) / 64, 0);
+            for (int i = 0; i < streams_per_device; ++i) d.free_mask[i / 64] |= 1ULL << (i % 64);
+            d.nfree = streams_per_device;
+            d.compute = compute_tokens;
+        }
+    }
+    bool holds_nothing(const MemVertex& v) const { return v.op == MemOpKind::Input && !inputs_; }
+    bool free(const MemVertex& v) const {
+        const Dev& d = devs_[v.device];
+        switch (v.op) {
+            case MemOpKind::Input: return !inputs_ || (d.nfree > 0 && d.host_in);
+            case MemOpKind::Kernel: return d.nfree > 0 && d.compute > 0;
+            case MemOpKind::Transfer: return d.nfree > 0;
+            case MemOpKind::Offload: return d.nfree > 0 && d.host_out;
+            case MemOpKind::Reload: return d.nfree > 0 && d.host_in;
+        }
+        return false;
+    }
+    std::int32_t acquire(const MemVertex& v) {
+        if (holds_nothing(v)) return -1;
+        Dev& d = devs_[v.device];
+        std::int32_t s = -1;
+        for (size_t w = 0; w < d.free_mask.size(); ++w)
+            if (d.free_mask[w]) {
+                int b = __builtin_ctzll(d.free_mask[w]);
+                d.free_mask[w] &= ~(1ULL << b);
+                s = static_cast<std::int32_t>(w * 64 + b);
+                break;
+            }
+        d.nfree--;
+        if (v.op == MemOpKind::Kernel) d.compute--;
+        if (v.op == MemOpKind::Offload) d.host_out = false;
+        if (v.op == MemOpKind::Reload || v.op == MemOpKind::Input) d.host_in = false;
+        return s;
+    }
+    void release(const MemVertex& v, std::int32_t s) {
+        if (holds_nothing(v)) return;
+        Dev& d = devs_[v.device];
+        d.free_mask[s / 64] |= 1ULL << (s % 64);
+        d.nfree++;
+        if (v.op == MemOpKind::Kernel) d.compute++;
+        if (v.op == MemOpKind::Offload) d.host_out = true;
+        if (v.op == MemOpKind::Reload || v.op == MemOpKind::Input) d.host_in = true;
+    }
+
+  private:
+    struct Dev {
+        std::vector<std::uint64_t> free_mask;
+        int nfree = 0;
+        int compute = 1;
+        bool host_out = true, host_in = true;
+    };
+    int streams_;
+    bool inputs_;
+    std::vector<Dev> devs_;
+};
+
+// Ready list + tie-break (simulator.cpp:135-219). FIFO entries arrive with
+// non-decreasing ready time and increasing arrival, so the list is always
+// FIFO-sorted and the reference's per-dispatch sort is the identity;
+// LowestId keeps the list id-sorted on insert; SeededRandom re-sorts by id and
+// reshuffles with the run's mt19937_64 before every sweep, exactly like the
+// reference, because the shuffle consumes the shared generator.
+class ReadyList {
+  public:
+    struct Entry {
+        double ready_time;
+        std::int64_t arrival;
+        VertexId vertex;
+        std::int32_t vidx;
+    };
+    ReadyList(TieBreak tb, std::uint64_t seed) : tb_(tb), rng_(mix64(seed)) {}
+    void push(VertexId id, std::int32_t vidx, double t) {
+        Entry e{t, arrivals_++, id, vidx};
+        if (tb_ == TieBreak::LowestId) {
+            auto it = std::upper_bound(v_.begin(), v_.end(), e,
+                                       [](const Entry& a, const Entry& b) { return a.vertex < b.vertex; });
+            v_.insert(it, e);
+        } else {
+            v_.push_back(e);
+        }
+    }
+    // Reorders for a sweep; returns true when a restart from 0 is required
+    // after every dispatch (SeededRandom).
+    bool sort() {
+        if (tb_ != TieBreak::SeededRandom) return false;
+        std::sort(v_.begin(), v_.end(), [](const Entry& a, const Entry& b) { return a.vertex < b.vertex; });
+        std::shuffle(v_.begin(), v_.end(), rng_);
+        return true;
+    }
+    std::vector<Entry>& entries() { return v_; }
+    void erase(size_t i) { v_.erase(v_.begin() + static_cast<std::ptrdiff_t>(i)); }
+    bool empty() const { return v_.empty(); }
+    size_t size() const { return v_.size(); }
+
+  private:
+    TieBreak tb_;
+    std::mt19937_64 rng_;
+    std::vector<Entry> v_;
+    std::int64_t arrivals_ = 0;
+};
+
+// Successor CSR and in-degrees of a memgraph, by vertex index.
+struct GraphIndex {
+    std::vector<std::int32_t> indeg, succ_start, succ;
+    explicit GraphIndex(const MemGraph& m);
+};
+
+// The dispatch loop. Backend provides:
+//   void launch(std::int32_t vidx, std::int32_t stream, double now);
+//   bool idle() const;                       // nothing in flight
+//   std::int32_t wait_next(double& now);      // blocks for one completion
+template <class Backend>
+void dispatch_loop(const MemGraph& m, Resources& res, ReadyList& ready, Backend& be) {
+    GraphIndex gi(m);
+    const size_t V = m.vertices.size();
+    std::vector<std::int32_t> pending = gi.indeg;
+    std::vector<std::int32_t> held(V, -1);
+    for (size_t i = 0; i < V; ++i)
+        if (pending[i] == 0) ready.push(m.vertices[i].id, static_cast<std::int32_t>(i), 0.0);
+    double now = 0.0;
+    size_t done = 0;
+    while (done < V) {
+        // Dispatch greedily until nothing fits.
+        size_t i = 0;
+        bool restart = ready.sort();
+        while (i < ready.size()) {
+            auto& e = ready.entries()[i];
+            const MemVertex& v = m.vertices[e.vidx];
+            if (!res.free(v)) {
+                ++i;
+                continue;
+            }
+            std::int32_t vidx = e.vidx;
+            std::int32_t s = res.acquire(v);
+            held[vidx] = s;
+            ready.erase(i);
+            be.launch(vidx, s, now);
+            if (restart) {
+                ready.sort();
+                i = 0;
+            }
+        }
+        if (be.idle()) {
+            std::string msg = "simulation deadlock: " + std::to_string(ready.size()) +
+                              " vertices ready but blocked, none in flight; frontier:";
+            for (const auto& r : ready.entries()) msg += " " + std::to_string(r.vertex);
+            throw DeadlockError(msg);
+        }
+        std::int32_t vidx = be.wait_next(now);
+        res.release(m.vertices[vidx], held[vidx]);
+        done++;
+        for (std::int32_t a = gi.succ_start[vidx]; a < gi.succ_start[vidx + 1]; ++a) {
+            std::int32_t w = gi.succ[a];
+            if (--pending[w] == 0) ready.push(m.vertices[w].id, w, now);
+        }
+    }
+}
+
+// --- virtual-time simulator (drop-in for the reference) ------------------------
+double sample_duration(const MemVertex& v, const DeviceProfile& p, std::uint64_t draw_seed);
+MemGraph make_fixed_order(const MemGraph& m);
+MemGraph make_fixed_order(const MemGraph& m, const std::vector<VertexId>& order);
+ExecutionTrace simulate(const MemGraph& m, const MemoryMap& map, const DeviceProfile& p,
+                        const SchedulerPolicy& policy, std::uint64_t seed);
+
+struct PolicyStats {
+    double mean = 0.0, ci_low = 0.0, ci_high = 0.0;
+    std::vector<double> makespans;
+};
+struct ComparisonSummary {
+    PolicyStats event_driven, fixed_order;
+    double speedup_mean = 0.0, speedup_ci_low = 0.0, speedup_ci_high = 0.0;
+    std::int64_t trials = 0;
+    std::string to_json() const;
+};
+PolicyStats bootstrap_stats(const std::vector<double>& samples, std::uint64_t seed);
+ComparisonSummary compare_policies(const MemGraph& m, const MemoryMap& map, const DeviceProfile& p,
+                                   std::int64_t trials, std::uint64_t seed);
+
+std::string serialize_profile(const DeviceProfile& p);
+DeviceProfile parse_profile(const std::string& text);
+
+}  // namespace tn
