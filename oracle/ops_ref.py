@@ -1,0 +1,190 @@
+"""CPU restatement of the op payload semantics in fp32 (numpy).
+
+TEST INFRASTRUCTURE ONLY — the checker, never the product: only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline leg may import this.
+
+Parity status: the reference has no tensor math at all (vertices are opaque
+tasks; "real GPU execution, CUDA/cuTensor
+kernels" out of scope), so tensor values are "parity unpinned":
+these functions DEFINE the op semantics of our payload schema
+(paper_2405_16283_b200/csrc/exec/ops.hpp) and the GPU kernels are checked
+against them within stated tolerances. Every op reduces in fp32 and rounds
+once to the output dtype (bf16 round-to-nearest-even), like the kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+DT = {"bf16": 2, "f32": 4, "i32": 4}
+
+
+# ---------------------------------------------------------------- bf16 ---
+def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
+    return (u16.astype(np.uint32) << 16).view(np.float32)
+
+
+def f32_to_bf16(x: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u >> 16) & 1) + np.uint32(0x7FFF)
+    return ((u + r) >> 16).astype(np.uint16)
+
+
+def load(buf: np.ndarray, dtype: str, count: int, off_elems: int = 0) -> np.ndarray:
+    """Reads `count` elements of `dtype` from a uint8 buffer as fp32 (or int32)."""
+    es = DT[dtype]
+    raw = buf[off_elems * es:(off_elems + count) * es]
+    if dtype == "bf16":
+        return bf16_to_f32(raw.view(np.uint16))
+    if dtype == "f32":
+        return raw.view(np.float32).astype(np.float32)
+    return raw.view(np.int32)
+
+
+def store(buf: np.ndarray, dtype: str, values: np.ndarray, off_elems: int = 0) -> None:
+    es = DT[dtype]
+    v = np.ascontiguousarray(values).reshape(-1)
+    if dtype == "bf16":
+        b = f32_to_bf16(v.astype(np.float32)).view(np.uint8)
+    elif dtype == "f32":
+        b = v.astype(np.float32).view(np.uint8)
+    else:
+        b = v.astype(np.int32).view(np.uint8)
+    buf[off_elems * es:off_elems * es + b.size] = b
+
+
+def typed(buf: np.ndarray, dtype: str) -> np.ndarray:
+    es = DT[dtype]
+    raw = buf[: (buf.size // es) * es]
+    return raw.view({"bf16": np.uint16, "f32": np.float32, "i32": np.int32}[dtype])
+
+
+def strided(buf, dtype, off, batch, bs, rows, ld, cols):
+    """[batch, rows, cols] fp32 copy of an element-strided region."""
+    t = typed(buf, dtype)
+    span = off + (batch - 1) * bs + (rows - 1) * ld + cols
+    if span > t.size:
+        raise ValueError(f"strided view needs {span} elements, region has {t.size}")
+    es = t.itemsize
+    v = np.lib.stride_tricks.as_strided(t[off:], shape=(batch, rows, cols), strides=(bs * es, ld * es, es))
+    return bf16_to_f32(v) if dtype == "bf16" else v.astype(np.float32)
+
+
+def scatter(buf, dtype, off, bs, ld, values, mask=None):
+    """Writes values[batch, rows, cols] into an element-strided region."""
+    t = typed(buf, dtype)
+    Bn, R, Cc = values.shape
+    es = t.itemsize
+    v = np.lib.stride_tricks.as_strided(t[off:], shape=(Bn, R, Cc), strides=(bs * es, ld * es, es),
+                                        writeable=True)
+    conv = f32_to_bf16(values) if dtype == "bf16" else values.astype(t.dtype)
+    if mask is None:
+        v[...] = conv
+    else:
+        np.copyto(v, conv, where=mask)
+
+
+# ------------------------------------------------------------------ ops ---
+def op_gemm(op, args, out):
+    """C[b] = alpha * A[b] @ B[b]^T (+ R[b]); causal 1 = only j <= i is
+    defined (upper triangle left untouched), causal 2 = only k <= i used."""
+    M, N, K, B = op["M"], op["N"], op["K"], op.get("batch", 1)
+    lda, ldb, ldc = op.get("lda") or K, op.get("ldb") or K, op.get("ldc") or N
+    ind, outd = op.get("in_dtype", "bf16"), op.get("out_dtype", "bf16")
+    A = strided(args[0], ind, op.get("a_off", 0), B, op.get("sa", 0), M, lda, K)
+    Bm = strided(args[1], ind, op.get("b_off", 0), B, op.get("sb", 0), N, ldb, K)
+    causal = op.get("causal", 0)
+    if causal == 2:
+        mask = (np.arange(K)[None, :] <= np.arange(M)[:, None]).astype(np.float32)
+        A = A * mask[None]
+    C = np.matmul(A, np.transpose(Bm, (0, 2, 1))) * np.float32(op.get("alpha", 1.0))
+    if len(args) == 3:
+        C = C + strided(args[2], outd, op.get("r_off", 0), B, op.get("sc", 0), M, ldc, N)
+    mask = None
+    if causal == 1:
+        mask = np.broadcast_to((np.arange(N)[None, :] <= np.arange(M)[:, None])[None], C.shape)
+    scatter(out, outd, op.get("c_off", 0), op.get("sc", 0), ldc, C.astype(np.float32), mask)
+
+
+def op_rmsnorm(op, args, out):
+    R, Cc, eps = op["rows"], op["cols"], op.get("eps", 1e-5)
+    x = load(args[0], "bf16", R * Cc).reshape(R, Cc)
+    w = load(args[1], "bf16", Cc)
+    ms = np.mean(x * x, axis=1, keepdims=True, dtype=np.float32)
+    y = x * (1.0 / np.sqrt(ms + np.float32(eps))).astype(np.float32) * w[None, :]
+    store(out, "bf16", y)
+
+
+def op_softmax(op, args, out):
+    B, R, Cc, scale, causal = op.get("batch", 1), op["rows"], op["cols"], op.get("scale", 1.0), op.get("causal", 0)
+    S = load(args[0], "f32", B * R * Cc).reshape(B, R, Cc) * np.float32(scale)
+    if causal:
+        mask = np.arange(Cc)[None, :] <= np.arange(R)[:, None]
+        S = np.where(mask[None], S, -np.inf)
+    mx = np.max(S, axis=2, keepdims=True)
+    e = np.exp(S - mx)
+    if causal:
+        e = np.where(mask[None], e, 0.0)
+    P = e / np.sum(e, axis=2, keepdims=True, dtype=np.float32)
+    store(out, "bf16", P.astype(np.float32))
+
+
+def op_rope(op, args, out):
+    S, ld, co, H, hd = op["seq"], op["ld"], op.get("col_off", 0), op["heads"], op["hd"]
+    half = hd // 2
+    x = strided(args[0], "bf16", co, 1, 0, S, ld, H * hd)[0].reshape(S, H, hd)
+    tab = load(args[1], "f32", S * half * 2).reshape(S, half, 2)
+    c, s = tab[:, None, :, 0], tab[:, None, :, 1]
+    a, b = x[..., :half], x[..., half:]
+    y = np.concatenate([a * c - b * s, b * c + a * s], axis=-1)  # [S, H, hd]
+    store(out, "bf16", np.transpose(y, (1, 0, 2)))
+
+
+def op_transpose_heads(op, args, out):
+    S, ld, co, H, hd = op["seq"], op["ld"], op.get("col_off", 0), op["heads"], op["hd"]
+    x = strided(args[0], "bf16", co, 1, 0, S, ld, H * hd)[0].reshape(S, H, hd)
+    store(out, "bf16", np.transpose(x, (1, 2, 0)))
+
+
+def op_silu_mul(op, args, out):
+    R, Cc = op["rows"], op["cols"]
+    gu = load(args[0], "bf16", R * 2 * Cc).reshape(R, 2 * Cc)
+    g, u = gu[:, :Cc], gu[:, Cc:]
+    store(out, "bf16", g / (1.0 + np.exp(-g)) * u)
+
+
+def op_sum(op, args, out):
+    n, ind, outd = op["count"], op.get("in_dtype", "bf16"), op.get("out_dtype", "bf16")
+    acc = load(args[0], ind, n).astype(np.float32).copy()
+    for a in args[1:]:
+        acc += load(a, ind, n)
+    store(out, outd, acc)
+
+
+def op_embedding(op, args, out):
+    S, Dm, V = op["seq"], op["dim"], op["vocab"]
+    tok = np.clip(load(args[0], "i32", S), 0, V - 1)
+    tab = args[1][: V * Dm * 2].view(np.uint16).reshape(V, Dm)
+    out[: S * Dm * 2] = tab[tok].reshape(-1).view(np.uint8)
+
+
+def op_cast(op, args, out):
+    n = op["count"]
+    store(out, op.get("out_dtype", "bf16"), load(args[0], op.get("in_dtype", "f32"), n))
+
+
+OPS = {
+    "gemm": op_gemm,
+    "rmsnorm": op_rmsnorm,
+    "softmax": op_softmax,
+    "rope": op_rope,
+    "transpose_heads": op_transpose_heads,
+    "silu_mul": op_silu_mul,
+    "sum": op_sum,
+    "embedding": op_embedding,
+    "cast": op_cast,
+}
+
+
+def gemm_flops(op) -> float:
+    f = 2.0 * op["M"] * op["N"] * op["K"] * op.get("batch", 1)
+    return f * 0.5 * (1 + 1 / op["M"]) if op.get("causal", 0) else f

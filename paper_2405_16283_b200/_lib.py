@@ -66,16 +66,12 @@ def lib():
             "tn_exec_destroy": (None, [c_void_p]),
         }
         for name, (res, args) in {**sig, **exec_sig}.items():
-            fn = getattr(L, name, None)
-            if fn is None:
-                continue
+            fn = getattr(L, name)  # AttributeError: the library lacks a declared symbol
             fn.restype = res
             fn.argtypes = args
         # char** outputs must be freed with tn_free, so read them as raw pointers.
         for name in list(sig) + list(exec_sig):
-            fn = getattr(L, name, None)
-            if fn is None:
-                continue
+            fn = getattr(L, name)
             fn.argtypes = [c_void_p if a is P else a for a in fn.argtypes]
         _lib = L
     return _lib

@@ -1,0 +1,700 @@
+// The CUDA executor: runs a memgraph for real on B200s, behind the same
+// dispatch contract as the reference simulator (proj/src/simulator.cpp:108-344).
+//
+// Layout: one cudaMalloc arena of exactly capacities[d] bytes per memgraph
+// device; every placement is arena[d] + offset (no allocation while running,
+// PAPER.md:175). Offload/reload slots and input tensors live in a pinned host
+// pool (cudaHostAlloc). Per device: `streams_per_device` non-blocking streams
+// (reference default 5, simulator.hpp:23); copy engines are picked by the
+// driver from the copy direction.
+//
+// Event loop (dispatch_loop in core/dispatch.hpp): a vertex dispatches when
+// all memgraph predecessors have completed and its resources are free. Each
+// launch is followed by cudaLaunchHostFunc; the callback (driver thread, no
+// CUDA calls) pushes the vertex into a completion queue that wakes the loop.
+// Per-vertex start/end cudaEvents give the trace times.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <unordered_map>
+#include <unordered_set>
+
+#include <nlohmann/json.hpp>
+
+#include "../core/dispatch.hpp"
+#include "../core/planner.hpp"
+#include "../kernels/kernels.hpp"
+#include "executor.hpp"
+#include "ops.hpp"
+
+namespace tn {
+
+using json = nlohmann::json;
+
+#define TN_CUDA(call)                                                                                     \
+    do {                                                                                                  \
+        cudaError_t e_ = (call);                                                                          \
+        if (e_ != cudaSuccess)                                                                            \
+            throw CudaError(std::string(#call) + " failed: " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                            std::to_string(__LINE__) + ")");                                              \
+    } while (0)
+
+namespace {
+
+struct HostBuf {
+    void* p = nullptr;
+    std::size_t bytes = 0;
+};
+
+void* pinned_alloc(std::size_t bytes) {
+    void* p = nullptr;
+    TN_CUDA(cudaHostAlloc(&p, std::max<std::size_t>(bytes, 1), cudaHostAllocPortable));
+    return p;
+}
+
+}  // namespace
+
+struct Executor::Impl {
+    // --- inputs ----------------------------------------------------------------
+    MemGraph m;
+    MemoryMap map;
+    TaskGraph tg;
+    std::unordered_map<VertexId, OpDesc> ops;
+    ExecConfig cfg;
+
+    // --- device state ----------------------------------------------------------
+    int D = 1;
+    std::vector<int> ordinal;       // logical device -> CUDA ordinal
+    std::vector<int> num_sms;
+    std::vector<char*> arena;       // per logical device
+    std::vector<std::vector<cudaStream_t>> streams;
+    std::vector<cudaEvent_t> t0;    // per logical device
+    std::vector<cudaEvent_t> ev_start, ev_end;  // per memgraph vertex index
+
+    // --- host pool ---------------------------------------------------------------
+    std::unordered_map<VertexId, HostBuf> inputs;  // taskgraph input id -> pinned bytes
+    std::unordered_map<VertexId, HostBuf> slots;   // evicted root id -> pinned slot
+
+    // --- per-vertex launch programs ------------------------------------------------
+    struct Instr {
+        MemOpKind op = MemOpKind::Kernel;
+        int dev = 0;
+        int src_dev = 0;
+        char* dst = nullptr;
+        const char* src = nullptr;
+        void* host = nullptr;  // offload/reload slot, input buffer
+        std::size_t bytes = 0;
+        VertexId input_id = -1;
+        const OpDesc* op_desc = nullptr;
+        std::vector<const char*> argp;  // resolved argument pointers
+        std::unique_ptr<k::GemmPlan> gemm;
+    };
+    std::vector<Instr> prog;
+
+    // --- completion queue ------------------------------------------------------------
+    struct CbCtx {
+        Impl* self;
+        std::int32_t vidx;
+    };
+    std::vector<CbCtx> cb;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::int32_t> completed;
+    std::atomic<int> callback_errors{0};
+
+    // --- per run ---------------------------------------------------------------------
+    std::vector<std::int32_t> dispatched;  // vidx in dispatch order
+    std::vector<std::int32_t> stream_of;
+    RunStats last;
+    int cur_dev = -1;
+
+    void set_device(int logical) {
+        int o = ordinal[logical];
+        if (o != cur_dev) {
+            TN_CUDA(cudaSetDevice(o));
+            cur_dev = o;
+        }
+    }
+
+    char* ptr_of(VertexId mem_id) {
+        auto it = map.placements.find(mem_id);
+        if (it == map.placements.end())
+            throw Error("memgraph vertex " + std::to_string(mem_id) + " has no placement");
+        const Placement& p = it->second;
+        if (p.device < 0 || p.device >= D) throw Error("placement of " + std::to_string(mem_id) + " names unknown device");
+        return arena[p.device] + p.offset;
+    }
+    std::int64_t size_of(VertexId mem_id) const { return map.placements.at(mem_id).size; }
+
+    static void CUDART_CB on_done(void* data) {
+        auto* c = static_cast<CbCtx*>(data);
+        {
+            std::lock_guard<std::mutex> g(c->self->mu);
+            c->self->completed.push_back(c->vidx);
+        }
+        c->self->cv.notify_one();
+    }
+
+    void build();
+    void prepare_kernel(Instr& in, const MemVertex& v, const std::vector<std::pair<VertexId, VertexId>>& data_in);
+    void launch(std::int32_t vidx, std::int32_t stream);
+    void run(const SchedulerPolicy& pol, std::uint64_t seed, ExecutionTrace* trace);
+    ~Impl();
+};
+
+// ------------------------------------------------------------------ build ---
+void Executor::Impl::build() {
+    if (map.mode != MemoryMode::Byte) throw Error("the CUDA executor needs a byte-mode memgraph");
+    D = m.device_count;
+    if (static_cast<int>(map.capacities.size()) != D) throw Error("capacities must list one entry per device");
+    int ngpu = 0;
+    TN_CUDA(cudaGetDeviceCount(&ngpu));
+    if (ngpu < 1) throw CudaError("no CUDA device visible");
+    ordinal.resize(D);
+    for (int d = 0; d < D; ++d) {
+        ordinal[d] = d < static_cast<int>(cfg.devices.size()) ? cfg.devices[d] : d % ngpu;
+        if (ordinal[d] < 0 || ordinal[d] >= ngpu) throw Error("device map names CUDA ordinal out of range");
+    }
+    num_sms.resize(D);
+    arena.assign(D, nullptr);
+    streams.resize(D);
+    t0.resize(D);
+    for (int d = 0; d < D; ++d) {
+        set_device(d);
+        TN_CUDA(cudaDeviceGetAttribute(&num_sms[d], cudaDevAttrMultiProcessorCount, ordinal[d]));
+        TN_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena[d]), std::max<std::int64_t>(map.capacities[d], 256)));
+        streams[d].resize(cfg.streams_per_device);
+        for (auto& s : streams[d]) TN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        TN_CUDA(cudaEventCreate(&t0[d]));
+    }
+    // Peer access for every pair of distinct GPUs a transfer connects.
+    for (const auto& v : m.vertices) {
+        if (v.op != MemOpKind::Transfer) continue;
+        if (v.src_device < 0 || v.src_device >= D) throw Error("transfer with unknown src_device");
+        int a = ordinal[v.device], b = ordinal[v.src_device];
+        if (a == b) continue;
+        int can = 0;
+        TN_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
+        if (can) {
+            TN_CUDA(cudaSetDevice(a));
+            cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) TN_CUDA(e);
+            cudaGetLastError();
+            cur_dev = a;
+        }
+    }
+
+    // Data in-edges per vertex, edge order.
+    std::unordered_map<VertexId, std::vector<std::pair<VertexId, VertexId>>> data_in;  // to -> (from, root)
+    for (const auto& e : m.edges) {
+        if (e.kind != EdgeKind::Data) continue;
+        const MemVertex& f = m.at(e.from);
+        data_in[e.to].push_back({e.from, f.origin.ref});
+    }
+    // Placement bounds.
+    for (const auto& [id, p] : map.placements) {
+        if (p.device < 0 || p.device >= D || p.offset < 0 || p.size < 0 || p.offset + p.size > map.capacities[p.device])
+            throw Error("placement of " + std::to_string(id) + " exceeds its device arena");
+    }
+
+    const size_t V = m.vertices.size();
+    prog.resize(V);
+    cb.resize(V);
+    ev_start.resize(V);
+    ev_end.resize(V);
+    for (size_t i = 0; i < V; ++i) {
+        const MemVertex& v = m.vertices[i];
+        Instr& in = prog[i];
+        cb[i] = {this, static_cast<std::int32_t>(i)};
+        in.op = v.op;
+        in.dev = v.device;
+        if (v.device < 0 || v.device >= D) throw Error("vertex " + std::to_string(v.id) + " on unknown device");
+        set_device(v.device);
+        TN_CUDA(cudaEventCreate(&ev_start[i]));
+        TN_CUDA(cudaEventCreate(&ev_end[i]));
+        const auto& din = data_in[v.id];
+        switch (v.op) {
+            case MemOpKind::Input: {
+                in.dst = ptr_of(v.id);
+                in.bytes = static_cast<std::size_t>(size_of(v.id));
+                in.input_id = v.origin.ref;
+                break;
+            }
+            case MemOpKind::Offload: {
+                if (din.size() != 1) throw Error("offload " + std::to_string(v.id) + " needs exactly one data source");
+                in.src = ptr_of(din[0].first);
+                in.bytes = static_cast<std::size_t>(v.size);
+                HostBuf& s = slots[v.origin.ref];
+                s.bytes = std::max(s.bytes, in.bytes);
+                break;
+            }
+            case MemOpKind::Reload: {
+                in.dst = ptr_of(v.id);
+                in.bytes = static_cast<std::size_t>(std::min<std::int64_t>(v.size, size_of(v.id)));
+                HostBuf& s = slots[v.origin.ref];
+                s.bytes = std::max(s.bytes, in.bytes);
+                break;
+            }
+            case MemOpKind::Transfer: {
+                if (din.size() != 1) throw Error("transfer " + std::to_string(v.id) + " needs exactly one data source");
+                in.src = ptr_of(din[0].first);
+                in.src_dev = map.placements.at(din[0].first).device;
+                in.dst = ptr_of(v.id);
+                in.bytes = static_cast<std::size_t>(std::min(size_of(v.id), size_of(din[0].first)));
+                break;
+            }
+            case MemOpKind::Kernel: prepare_kernel(in, v, din); break;
+        }
+    }
+    // Pinned offload slots (one per evicted root, reused across generations:
+    // generation g+1's offload data-depends on generation g's reload,
+    // compiler.cpp:353-361).
+    for (auto& [root, s] : slots) s.p = pinned_alloc(s.bytes);
+    for (size_t i = 0; i < V; ++i) {
+        const MemVertex& v = m.vertices[i];
+        if (v.op == MemOpKind::Offload || v.op == MemOpKind::Reload) prog[i].host = slots.at(v.origin.ref).p;
+    }
+}
+
+void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
+                                    const std::vector<std::pair<VertexId, VertexId>>& din) {
+    auto it = ops.find(v.origin.ref);
+    if (it == ops.end()) throw Error("kernel vertex " + std::to_string(v.id) + " has no op payload");
+    const OpDesc& op = it->second;
+    in.op_desc = &op;
+    in.dst = ptr_of(v.id);
+    const std::int64_t out_bytes = size_of(v.id);
+    std::vector<std::int64_t> arg_bytes;
+    for (VertexId a : op.args) {
+        const char* p = nullptr;
+        std::int64_t sz = 0;
+        for (const auto& [src, root] : din)
+            if (root == a) {
+                p = ptr_of(src);
+                sz = size_of(src);
+                break;
+            }
+        if (!p)
+            throw Error("kernel " + std::to_string(v.id) + ": argument " + std::to_string(a) +
+                        " is not a data predecessor in the memgraph");
+        in.argp.push_back(p);
+        arg_bytes.push_back(sz);
+    }
+    auto need_args = [&](size_t lo, size_t hi) {
+        if (op.args.size() < lo || op.args.size() > hi)
+            throw Error("kernel " + std::to_string(v.id) + " (" + to_string(op.type) + "): wrong argument count");
+    };
+    auto fits = [&](std::int64_t bytes, std::int64_t cap, const char* what) {
+        if (bytes < 0 || bytes > cap)
+            throw Error("kernel " + std::to_string(v.id) + " (" + to_string(op.type) + "): " + what +
+                        " extent " + std::to_string(bytes) + " exceeds its region of " + std::to_string(cap) + " bytes");
+    };
+    auto es = [](int dt) { return static_cast<std::int64_t>(k::dtype_size(dt)); };
+    switch (op.type) {
+        case OpType::Gemm: {
+            need_args(2, 3);
+            k::GemmArgs g;
+            g.M = static_cast<int>(op.M);
+            g.N = static_cast<int>(op.N);
+            g.K = static_cast<int>(op.K);
+            g.batch = static_cast<int>(op.batch);
+            g.lda = op.lda ? op.lda : op.K;
+            g.ldb = op.ldb ? op.ldb : op.K;
+            g.ldc = op.ldc ? op.ldc : op.N;
+            g.sa = op.sa;
+            g.sb = op.sb;
+            g.sc = op.sc;
+            g.alpha = static_cast<float>(op.alpha);
+            g.in_dtype = op.in_dtype;
+            g.out_dtype = op.out_dtype;
+            g.causal = op.causal;
+            if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) throw Error("gemm with empty shape");
+            const std::int64_t ei = es(op.in_dtype), eo = es(op.out_dtype);
+            auto extent = [](std::int64_t off, int batch, std::int64_t bs, std::int64_t rows, std::int64_t ld,
+                             std::int64_t cols) { return off + (batch - 1) * bs + (rows - 1) * ld + cols; };
+            fits(extent(op.a_off, g.batch, g.sa, g.M, g.lda, g.K) * ei, arg_bytes[0], "A");
+            fits(extent(op.b_off, g.batch, g.sb, g.N, g.ldb, g.K) * ei, arg_bytes[1], "B");
+            fits(extent(op.c_off, g.batch, g.sc, g.M, g.ldc, g.N) * eo, out_bytes, "C");
+            g.A = in.argp[0] + op.a_off * ei;
+            g.B = in.argp[1] + op.b_off * ei;
+            g.C = in.dst + op.c_off * eo;
+            if (op.args.size() == 3) {
+                fits(extent(op.r_off, g.batch, g.sc, g.M, g.ldc, g.N) * eo, arg_bytes[2], "R");
+                g.R = in.argp[2] + op.r_off * eo;
+            }
+            in.gemm = std::make_unique<k::GemmPlan>();
+            TN_CUDA(k::gemm_prepare(g, in.gemm.get(), num_sms[v.device]));
+            break;
+        }
+        case OpType::RmsNorm:
+            need_args(2, 2);
+            fits(op.rows * op.cols * 2, arg_bytes[0], "x");
+            fits(op.cols * 2, arg_bytes[1], "w");
+            fits(op.rows * op.cols * 2, out_bytes, "y");
+            break;
+        case OpType::Softmax:
+            need_args(1, 1);
+            fits(op.batch * op.rows * op.cols * 4, arg_bytes[0], "S");
+            fits(op.batch * op.rows * op.cols * 2, out_bytes, "P");
+            break;
+        case OpType::Rope:
+            need_args(2, 2);
+            if (op.hd % 2) throw Error("rope needs an even head dim");
+            fits(((op.seq - 1) * op.ld + op.col_off + op.heads * op.hd) * 2, arg_bytes[0], "src");
+            fits(op.seq * (op.hd / 2) * 2 * 4, arg_bytes[1], "table");
+            fits(op.heads * op.seq * op.hd * 2, out_bytes, "out");
+            break;
+        case OpType::TransposeHeads:
+            need_args(1, 1);
+            fits(((op.seq - 1) * op.ld + op.col_off + op.heads * op.hd) * 2, arg_bytes[0], "src");
+            fits(op.heads * op.seq * op.hd * 2, out_bytes, "out");
+            break;
+        case OpType::SiluMul:
+            need_args(1, 1);
+            fits(op.rows * op.cols * 2 * 2, arg_bytes[0], "gu");
+            fits(op.rows * op.cols * 2, out_bytes, "out");
+            break;
+        case OpType::Sum:
+            need_args(1, 16);
+            for (size_t i = 0; i < op.args.size(); ++i) fits(op.count * es(op.in_dtype), arg_bytes[i], "part");
+            fits(op.count * es(op.out_dtype), out_bytes, "out");
+            break;
+        case OpType::Embedding:
+            need_args(2, 2);
+            fits(op.seq * 4, arg_bytes[0], "tokens");
+            fits(op.vocab * op.dim * 2, arg_bytes[1], "table");
+            fits(op.seq * op.dim * 2, out_bytes, "out");
+            break;
+        case OpType::Cast:
+            need_args(1, 1);
+            fits(op.count * es(op.in_dtype), arg_bytes[0], "x");
+            fits(op.count * es(op.out_dtype), out_bytes, "out");
+            break;
+    }
+}
+
+// ----------------------------------------------------------------- launch ---
+void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream) {
+    Instr& in = prog[vidx];
+    set_device(in.dev);
+    cudaStream_t s = streams[in.dev][stream < 0 ? 0 : stream];  // inputs hold no stream when not materialised
+    TN_CUDA(cudaEventRecord(ev_start[vidx], s));
+    switch (in.op) {
+        case MemOpKind::Input: {
+            auto it = inputs.find(in.input_id);
+            if (it == inputs.end() || !it->second.p)
+                throw Error("input " + std::to_string(in.input_id) + " has no data (tn_exec_set_input)");
+            TN_CUDA(cudaMemcpyAsync(in.dst, it->second.p, std::min(in.bytes, it->second.bytes), cudaMemcpyHostToDevice, s));
+            last.h2d_bytes += static_cast<std::int64_t>(std::min(in.bytes, it->second.bytes));
+            break;
+        }
+        case MemOpKind::Offload:
+            TN_CUDA(cudaMemcpyAsync(in.host, in.src, in.bytes, cudaMemcpyDeviceToHost, s));
+            last.d2h_bytes += static_cast<std::int64_t>(in.bytes);
+            break;
+        case MemOpKind::Reload:
+            TN_CUDA(cudaMemcpyAsync(in.dst, in.host, in.bytes, cudaMemcpyHostToDevice, s));
+            last.h2d_bytes += static_cast<std::int64_t>(in.bytes);
+            break;
+        case MemOpKind::Transfer:
+            if (ordinal[in.src_dev] == ordinal[in.dev]) {
+                TN_CUDA(cudaMemcpyAsync(in.dst, in.src, in.bytes, cudaMemcpyDeviceToDevice, s));
+                last.d2d_bytes += static_cast<std::int64_t>(in.bytes);
+            } else {
+                TN_CUDA(cudaMemcpyPeerAsync(in.dst, ordinal[in.dev], in.src, ordinal[in.src_dev], in.bytes, s));
+                last.p2p_bytes += static_cast<std::int64_t>(in.bytes);
+            }
+            break;
+        case MemOpKind::Kernel: {
+            const OpDesc& op = *in.op_desc;
+            const auto& a = in.argp;
+            switch (op.type) {
+                case OpType::Gemm:
+                    TN_CUDA(k::gemm_launch(*in.gemm, s));
+                    last.flops += k::gemm_flops(in.gemm->args);
+                    break;
+                case OpType::RmsNorm:
+                    TN_CUDA(k::rmsnorm(a[0], a[1], in.dst, static_cast<int>(op.rows), static_cast<int>(op.cols),
+                                       static_cast<float>(op.eps), s));
+                    break;
+                case OpType::Softmax:
+                    TN_CUDA(k::softmax(a[0], in.dst, static_cast<int>(op.batch), static_cast<int>(op.rows),
+                                       static_cast<int>(op.cols), static_cast<float>(op.scale), op.causal, s));
+                    break;
+                case OpType::Rope:
+                    TN_CUDA(k::rope(a[0], a[1], in.dst, static_cast<int>(op.seq), op.ld, op.col_off,
+                                    static_cast<int>(op.heads), static_cast<int>(op.hd), s));
+                    break;
+                case OpType::TransposeHeads:
+                    TN_CUDA(k::transpose_heads(a[0], in.dst, static_cast<int>(op.seq), op.ld, op.col_off,
+                                               static_cast<int>(op.heads), static_cast<int>(op.hd), s));
+                    break;
+                case OpType::SiluMul:
+                    TN_CUDA(k::silu_mul(a[0], in.dst, static_cast<int>(op.rows), static_cast<int>(op.cols), s));
+                    break;
+                case OpType::Sum: {
+                    std::vector<const void*> ps(a.begin(), a.end());
+                    TN_CUDA(k::sum_n(ps.data(), static_cast<int>(ps.size()), op.in_dtype, in.dst, op.out_dtype,
+                                     op.count, s));
+                    break;
+                }
+                case OpType::Embedding:
+                    TN_CUDA(k::embedding(a[0], a[1], in.dst, static_cast<int>(op.seq), static_cast<int>(op.dim),
+                                         static_cast<int>(op.vocab), s));
+                    break;
+                case OpType::Cast:
+                    TN_CUDA(k::cast(a[0], op.in_dtype, in.dst, op.out_dtype, op.count, s));
+                    break;
+            }
+            last.kernel_launches++;
+            break;
+        }
+    }
+    TN_CUDA(cudaEventRecord(ev_end[vidx], s));
+    TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
+}
+
+// -------------------------------------------------------------------- run ---
+namespace {
+
+class CudaBackend {
+  public:
+    explicit CudaBackend(Executor::Impl& x) : x_(x), start_(std::chrono::steady_clock::now()) {}
+    void launch(std::int32_t vidx, std::int32_t stream, double) {
+        x_.launch(vidx, stream);
+        x_.dispatched.push_back(vidx);
+        x_.stream_of[vidx] = stream;
+        in_flight_++;
+    }
+    bool idle() const { return in_flight_ == 0; }
+    std::int32_t wait_next(double& now) {
+        std::unique_lock<std::mutex> lk(x_.mu);
+        if (x_.completed.empty()) {
+            if (!x_.cv.wait_for(lk, std::chrono::seconds(x_.cfg.timeout_s), [&] { return !x_.completed.empty(); }))
+                throw CudaError("executor timed out waiting for a completion (" + std::to_string(in_flight_) +
+                                " vertices in flight)");
+        }
+        std::int32_t v = x_.completed.front();
+        x_.completed.pop_front();
+        lk.unlock();
+        in_flight_--;
+        now = std::chrono::duration<double>(std::chrono::steady_clock::now() - start_).count();
+        return v;
+    }
+
+  private:
+    Executor::Impl& x_;
+    std::chrono::steady_clock::time_point start_;
+    int in_flight_ = 0;
+};
+
+}  // namespace
+
+void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, ExecutionTrace* trace) {
+    const MemGraph* g = &m;
+    MemGraph fixed;
+    if (pol.kind == SchedulerKind::FixedOrder) {
+        fixed = make_fixed_order(m);
+        fixed.reindex();
+        g = &fixed;
+    }
+    last = RunStats{};
+    dispatched.clear();
+    dispatched.reserve(g->vertices.size());
+    stream_of.assign(g->vertices.size(), -1);
+    completed.clear();
+    for (int d = 0; d < D; ++d) {
+        set_device(d);
+        TN_CUDA(cudaDeviceSynchronize());
+        TN_CUDA(cudaEventRecord(t0[d], streams[d][0]));
+    }
+    auto wall0 = std::chrono::steady_clock::now();
+    Resources res(D, cfg.streams_per_device, cfg.compute_tokens, cfg.materialize_inputs);
+    ReadyList ready(pol.tie_break, seed);
+    CudaBackend be(*this);
+    try {
+        dispatch_loop(*g, res, ready, be);
+    } catch (...) {
+        for (int d = 0; d < D; ++d) {
+            cudaSetDevice(ordinal[d]);
+            cudaDeviceSynchronize();
+        }
+        cur_dev = -1;
+        throw;
+    }
+    for (int d = 0; d < D; ++d) {
+        set_device(d);
+        TN_CUDA(cudaDeviceSynchronize());
+    }
+    last.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+
+    // Trace from device timestamps (seconds since the device's t0 event).
+    ExecutionTrace t;
+    t.rows.reserve(dispatched.size());
+    double kernel_s = 0, copy_s = 0;
+    std::vector<std::vector<std::pair<double, double>>> kspans(D), cspans(D);
+    for (std::int32_t vidx : dispatched) {
+        const MemVertex& v = g->vertices[vidx];
+        float a = 0, b = 0;
+        TN_CUDA(cudaEventElapsedTime(&a, t0[v.device], ev_start[vidx]));
+        TN_CUDA(cudaEventElapsedTime(&b, t0[v.device], ev_end[vidx]));
+        double s = a * 1e-3, e = std::max(a, b) * 1e-3;
+        t.rows.push_back({v.id, s, e, v.device, stream_of[vidx]});
+        if (v.op == MemOpKind::Kernel) {
+            kernel_s += e - s;
+            kspans[v.device].push_back({s, e});
+        } else {
+            copy_s += e - s;
+            cspans[v.device].push_back({s, e});
+        }
+    }
+    finalize_trace(*g, map, t);
+    // Exposed transfer time: instants where a copy runs on a device and no
+    // kernel does (union arithmetic per device).
+    auto unite = [](std::vector<std::pair<double, double>>& sp) {
+        std::sort(sp.begin(), sp.end());
+        std::vector<std::pair<double, double>> out;
+        for (auto& x : sp) {
+            if (!out.empty() && x.first <= out.back().second) out.back().second = std::max(out.back().second, x.second);
+            else out.push_back(x);
+        }
+        return out;
+    };
+    double exposed = 0, busy_k = 0;
+    for (int d = 0; d < D; ++d) {
+        auto K = unite(kspans[d]), C = unite(cspans[d]);
+        for (auto& kk : K) busy_k += kk.second - kk.first;
+        size_t j = 0;
+        for (auto& c : C) {
+            double covered = 0;
+            while (j < K.size() && K[j].second <= c.first) ++j;
+            for (size_t q = j; q < K.size() && K[q].first < c.second; ++q)
+                covered += std::min(c.second, K[q].second) - std::max(c.first, K[q].first);
+            exposed += (c.second - c.first) - covered;
+        }
+    }
+    last.makespan_s = t.makespan;
+    last.kernel_time_s = kernel_s;
+    last.copy_time_s = copy_s;
+    last.kernel_busy_s = busy_k;
+    last.exposed_transfer_s = exposed;
+    last.vertices = static_cast<std::int64_t>(dispatched.size());
+    if (trace) *trace = std::move(t);
+}
+
+Executor::Impl::~Impl() {
+    for (int d = 0; d < D && d < static_cast<int>(ordinal.size()); ++d) {
+        cudaSetDevice(ordinal[d]);
+        cudaDeviceSynchronize();
+    }
+    for (size_t i = 0; i < ev_start.size(); ++i) {
+        if (ev_start[i]) cudaEventDestroy(ev_start[i]);
+        if (ev_end[i]) cudaEventDestroy(ev_end[i]);
+    }
+    for (auto e : t0)
+        if (e) cudaEventDestroy(e);
+    for (auto& ss : streams)
+        for (auto s : ss)
+            if (s) cudaStreamDestroy(s);
+    for (auto p : arena)
+        if (p) cudaFree(p);
+    for (auto& [id, b] : inputs)
+        if (b.p) cudaFreeHost(b.p);
+    for (auto& [id, b] : slots)
+        if (b.p) cudaFreeHost(b.p);
+}
+
+// ------------------------------------------------------------- public API ---
+Executor::Executor(const std::string& memgraph_json, const std::string& taskgraph_json, const ExecConfig& cfg)
+    : impl_(std::make_unique<Impl>()) {
+    auto [m, map] = parse_memgraph(memgraph_json);
+    impl_->m = std::move(m);
+    impl_->map = std::move(map);
+    impl_->tg = parse_taskgraph(taskgraph_json);
+    impl_->ops = parse_ops(taskgraph_json);
+    impl_->cfg = cfg;
+    if (cfg.streams_per_device < 1) throw Error("streams_per_device must be >= 1");
+    if (cfg.compute_tokens < 1) throw Error("compute_tokens must be >= 1");
+    impl_->build();
+}
+
+Executor::~Executor() = default;
+
+void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool from_device) {
+    const TaskVertex* v = impl_->tg.find(id);
+    if (!v || v->kind != VertexKind::Input) throw Error("vertex " + std::to_string(id) + " is not a taskgraph input");
+    if (bytes > static_cast<std::size_t>(v->output_size))
+        throw Error("input " + std::to_string(id) + ": " + std::to_string(bytes) + " bytes exceed output_size " +
+                    std::to_string(v->output_size));
+    HostBuf& b = impl_->inputs[id];
+    if (!b.p || b.bytes != bytes) {
+        if (b.p) cudaFreeHost(b.p);
+        b.p = pinned_alloc(bytes);
+        b.bytes = bytes;
+    }
+    if (from_device) TN_CUDA(cudaMemcpy(b.p, host, bytes, cudaMemcpyDeviceToHost));
+    else std::memcpy(b.p, host, bytes);
+}
+
+ExecutionTrace Executor::run(const SchedulerPolicy& pol, std::uint64_t seed) {
+    ExecutionTrace t;
+    impl_->run(pol, seed, &t);
+    return t;
+}
+
+void Executor::get_output(VertexId id, void* host, std::size_t bytes) {
+    auto it = impl_->map.placements.find(id);
+    if (it == impl_->map.placements.end()) throw Error("vertex " + std::to_string(id) + " has no placement");
+    if (bytes > static_cast<std::size_t>(it->second.size))
+        throw Error("requested " + std::to_string(bytes) + " bytes from a region of " + std::to_string(it->second.size));
+    impl_->set_device(it->second.device);
+    TN_CUDA(cudaMemcpy(host, impl_->arena[it->second.device] + it->second.offset, bytes, cudaMemcpyDeviceToHost));
+}
+
+void* Executor::placement_ptr(VertexId id) { return impl_->ptr_of(id); }
+
+const RunStats& Executor::stats() const { return impl_->last; }
+
+std::string RunStats::to_json() const {
+    json j;
+    j["vertices"] = vertices;
+    j["kernel_launches"] = kernel_launches;
+    j["h2d_bytes"] = h2d_bytes;
+    j["d2h_bytes"] = d2h_bytes;
+    j["p2p_bytes"] = p2p_bytes;
+    j["d2d_bytes"] = d2d_bytes;
+    j["flops"] = flops;
+    j["makespan_s"] = makespan_s;
+    j["wall_s"] = wall_s;
+    j["kernel_time_s"] = kernel_time_s;
+    j["kernel_busy_s"] = kernel_busy_s;
+    j["copy_time_s"] = copy_time_s;
+    j["exposed_transfer_s"] = exposed_transfer_s;
+    return j.dump();
+}
+
+ExecConfig parse_exec_config(const std::string& text) {
+    ExecConfig c;
+    if (text.empty()) return c;
+    json j;
+    try {
+        j = json::parse(text);
+        if (j.contains("devices")) c.devices = j["devices"].get<std::vector<int>>();
+        c.streams_per_device = j.value("streams_per_device", c.streams_per_device);
+        c.compute_tokens = j.value("compute_tokens", c.compute_tokens);
+        c.materialize_inputs = j.value("materialize_inputs", c.materialize_inputs);
+        c.timeout_s = j.value("timeout_s", c.timeout_s);
+    } catch (const json::exception& e) {
+        throw ParseError(std::string("invalid executor config: ") + e.what());
+    }
+    return c;
+}
+
+}  // namespace tn

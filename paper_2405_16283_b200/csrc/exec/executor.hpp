@@ -1,0 +1,45 @@
+// CUDA executor for memgraphs: the real-hardware slot of the reference
+// simulate() (proj/include/memplan/simulator.hpp:67-68). See executor.cpp.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../core/dispatch.hpp"
+
+namespace tn {
+
+struct ExecConfig {
+    std::vector<int> devices;        // memgraph device -> CUDA ordinal (default d % gpus)
+    int streams_per_device = 5;      // simulator.hpp:23
+    int compute_tokens = 1;          // concurrent kernels per device (reference: 1)
+    bool materialize_inputs = true;  // Input = H2D copy on the host_in channel
+    int timeout_s = 600;             // completion watchdog
+};
+ExecConfig parse_exec_config(const std::string& text);
+
+struct RunStats {
+    std::int64_t vertices = 0, kernel_launches = 0;
+    std::int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_bytes = 0, d2d_bytes = 0;
+    double flops = 0, makespan_s = 0, wall_s = 0;
+    double kernel_time_s = 0, kernel_busy_s = 0, copy_time_s = 0, exposed_transfer_s = 0;
+    std::string to_json() const;
+};
+
+class Executor {
+  public:
+    Executor(const std::string& memgraph_json, const std::string& taskgraph_json, const ExecConfig& cfg);
+    ~Executor();
+    void set_input(VertexId id, const void* src, std::size_t bytes, bool from_device);
+    ExecutionTrace run(const SchedulerPolicy& pol, std::uint64_t seed);
+    void get_output(VertexId id, void* host, std::size_t bytes);
+    void* placement_ptr(VertexId id);
+    const RunStats& stats() const;
+    struct Impl;
+
+  private:
+    std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace tn

@@ -1,0 +1,103 @@
+// Parser for the per-vertex "op" payload (schema in ops.hpp).
+#include "ops.hpp"
+
+#include <nlohmann/json.hpp>
+
+#include "../kernels/kernels.hpp"
+
+namespace tn {
+
+const char* to_string(OpType t) {
+    switch (t) {
+        case OpType::Gemm: return "gemm";
+        case OpType::RmsNorm: return "rmsnorm";
+        case OpType::Softmax: return "softmax";
+        case OpType::Rope: return "rope";
+        case OpType::TransposeHeads: return "transpose_heads";
+        case OpType::SiluMul: return "silu_mul";
+        case OpType::Sum: return "sum";
+        case OpType::Embedding: return "embedding";
+        case OpType::Cast: return "cast";
+    }
+    return "?";
+}
+
+namespace {
+
+int dtype_of(const std::string& s) {
+    if (s == "bf16") return k::BF16;
+    if (s == "f32") return k::F32;
+    if (s == "i32") return k::I32;
+    throw ParseError("unknown dtype '" + s + "'");
+}
+
+OpType type_of(const std::string& s) {
+    if (s == "gemm") return OpType::Gemm;
+    if (s == "rmsnorm") return OpType::RmsNorm;
+    if (s == "softmax") return OpType::Softmax;
+    if (s == "rope") return OpType::Rope;
+    if (s == "transpose_heads") return OpType::TransposeHeads;
+    if (s == "silu_mul") return OpType::SiluMul;
+    if (s == "sum") return OpType::Sum;
+    if (s == "embedding") return OpType::Embedding;
+    if (s == "cast") return OpType::Cast;
+    throw ParseError("unknown op type '" + s + "'");
+}
+
+}  // namespace
+
+std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
+    std::unordered_map<VertexId, OpDesc> out;
+    nlohmann::json j;
+    try {
+        j = nlohmann::json::parse(text);
+    } catch (const nlohmann::json::parse_error& e) {
+        throw ParseError(std::string("invalid JSON: ") + e.what());
+    }
+    try {
+        for (const auto& jv : j.at("vertices")) {
+            if (!jv.contains("op") || jv["op"].is_null()) continue;
+            const auto& o = jv["op"];
+            OpDesc d;
+            d.type = type_of(o.at("type").get<std::string>());
+            d.args = o.value("args", std::vector<VertexId>{});
+            auto I = [&](const char* k, std::int64_t dflt) { return o.value(k, dflt); };
+            d.M = I("M", 0);
+            d.N = I("N", 0);
+            d.K = I("K", 0);
+            d.batch = I("batch", 1);
+            d.lda = I("lda", 0);
+            d.ldb = I("ldb", 0);
+            d.ldc = I("ldc", 0);
+            d.sa = I("sa", 0);
+            d.sb = I("sb", 0);
+            d.sc = I("sc", 0);
+            d.a_off = I("a_off", 0);
+            d.b_off = I("b_off", 0);
+            d.c_off = I("c_off", 0);
+            d.r_off = I("r_off", 0);
+            d.rows = I("rows", 0);
+            d.cols = I("cols", 0);
+            d.seq = I("seq", 0);
+            d.ld = I("ld", 0);
+            d.col_off = I("col_off", 0);
+            d.heads = I("heads", 0);
+            d.hd = I("hd", 0);
+            d.count = I("count", 0);
+            d.dim = I("dim", 0);
+            d.vocab = I("vocab", 0);
+            d.causal = static_cast<int>(I("causal", 0));
+            d.in_dtype = dtype_of(o.value("in_dtype", std::string("bf16")));
+            d.out_dtype = dtype_of(o.value("out_dtype", std::string("bf16")));
+            d.alpha = o.value("alpha", 1.0);
+            d.eps = o.value("eps", 1e-5);
+            d.scale = o.value("scale", 1.0);
+            out[jv.at("id").get<VertexId>()] = std::move(d);
+        }
+    } catch (const nlohmann::json::exception& e) {
+        throw ParseError(std::string("invalid op payload: ") + e.what());
+    }
+    return out;
+}
+
+}  // namespace tn

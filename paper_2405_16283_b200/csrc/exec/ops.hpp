@@ -1,0 +1,54 @@
+// Op payload schema: the extra per-vertex "op" key a generator puts on
+// taskgraph vertices. The reference parser ignores unknown keys
+// (proj/src/taskgraph.cpp:375-389), so a taskgraph carrying payloads is still
+// a valid reference input and builds a bit-identical memgraph.
+//
+//   {"type": "gemm", "args": [A, B (, R)], "M":..,"N":..,"K":.., "batch":1,
+//    "lda","ldb","ldc","sa","sb","sc", "a_off","b_off","c_off","r_off",
+//    "alpha":1.0, "in_dtype":"bf16"|"f32", "out_dtype":"bf16"|"f32",
+//    "causal":0|1|2}
+//   {"type": "rmsnorm", "args": [x, w], "rows", "cols", "eps"}
+//   {"type": "softmax", "args": [S], "batch", "rows", "cols", "scale", "causal"}
+//   {"type": "rope", "args": [src, table], "seq", "ld", "col_off", "heads", "hd"}
+//   {"type": "transpose_heads", "args": [src], "seq", "ld", "col_off", "heads", "hd"}
+//   {"type": "silu_mul", "args": [gu], "rows", "cols"}
+//   {"type": "sum", "args": [p0, p1, ...], "count", "in_dtype", "out_dtype"}
+//   {"type": "embedding", "args": [tokens, table], "seq", "dim", "vocab"}
+//   {"type": "cast", "args": [x], "count", "in_dtype", "out_dtype"}
+// `args` are taskgraph producer ids; every arg must be a taskgraph edge into
+// the vertex. Offsets/strides are in elements. Semantics are restated in fp32
+// by oracle/ops_ref.py (the CPU oracle).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../core/types.hpp"
+
+namespace tn {
+
+enum class OpType : std::uint8_t { Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast };
+
+struct OpDesc {
+    OpType type = OpType::Gemm;
+    std::vector<VertexId> args;
+    // integer and float parameters (absent keys default to 0 / listed defaults)
+    std::int64_t M = 0, N = 0, K = 0, batch = 1;
+    std::int64_t lda = 0, ldb = 0, ldc = 0, sa = 0, sb = 0, sc = 0;
+    std::int64_t a_off = 0, b_off = 0, c_off = 0, r_off = 0;
+    std::int64_t rows = 0, cols = 0, seq = 0, ld = 0, col_off = 0, heads = 0, hd = 0, count = 0, dim = 0,
+                 vocab = 0;
+    int causal = 0;
+    int in_dtype = 0, out_dtype = 0;  // k::DType
+    double alpha = 1.0, eps = 1e-5, scale = 1.0;
+};
+
+// Parses the "op" payloads of a taskgraph JSON document (vertices without an
+// "op" key are skipped).
+std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& taskgraph_json);
+
+const char* to_string(OpType t);
+
+}  // namespace tn

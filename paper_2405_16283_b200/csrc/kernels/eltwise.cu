@@ -1,0 +1,264 @@
+// Elementwise / layout tasks: RoPE, per-head V
+// transpose, SiLU·mul, fixed-order sum of partials, embedding gather, casts.
+// HBM-bound: 128-bit coalesced loads/stores, grid-stride loops sized to the
+// SM count, fp32 math with one round-to-nearest-even per output.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace tn::k {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 x = __bfloat1622float2(h[i]);
+        f[2 * i] = x.x;
+        f[2 * i + 1] = x.y;
+    }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return u;
+}
+
+unsigned grid_for(std::int64_t work, int per_block = kThreads) {
+    std::int64_t b = (work + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return static_cast<unsigned>(b);
+}
+
+// One thread = 8 consecutive rotation pairs (i, i + hd/2) of one (t, h).
+__global__ void rope_vec(const __nv_bfloat16* __restrict__ src, const float* __restrict__ table,
+                         __nv_bfloat16* __restrict__ out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
+                         int hd) {
+    const int half = hd / 2, groups = half / 8;
+    const std::int64_t total = static_cast<std::int64_t>(seq) * heads * groups;
+    for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(w % groups);
+        const int h = static_cast<int>((w / groups) % heads);
+        const int t = static_cast<int>(w / (static_cast<std::int64_t>(groups) * heads));
+        const __nv_bfloat16* x = src + t * ld + col_off + static_cast<std::int64_t>(h) * hd;
+        float a[8], b[8];
+        unpack8(*reinterpret_cast<const uint4*>(x + g * 8), a);
+        unpack8(*reinterpret_cast<const uint4*>(x + half + g * 8), b);
+        const float4* cs = reinterpret_cast<const float4*>(table + (static_cast<std::int64_t>(t) * half + g * 8) * 2);
+        float lo[8], hi[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float4 q = cs[j];  // (cos_j0, sin_j0, cos_j1, sin_j1)
+            lo[2 * j] = a[2 * j] * q.x - b[2 * j] * q.y;
+            hi[2 * j] = b[2 * j] * q.x + a[2 * j] * q.y;
+            lo[2 * j + 1] = a[2 * j + 1] * q.z - b[2 * j + 1] * q.w;
+            hi[2 * j + 1] = b[2 * j + 1] * q.z + a[2 * j + 1] * q.w;
+        }
+        __nv_bfloat16* o = out + (static_cast<std::int64_t>(h) * seq + t) * hd;
+        *reinterpret_cast<uint4*>(o + g * 8) = pack8(lo);
+        *reinterpret_cast<uint4*>(o + half + g * 8) = pack8(hi);
+    }
+}
+
+__global__ void rope_scalar(const __nv_bfloat16* __restrict__ src, const float* __restrict__ table,
+                            __nv_bfloat16* __restrict__ out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
+                            int hd) {
+    const int half = hd / 2;
+    const std::int64_t total = static_cast<std::int64_t>(seq) * heads * half;
+    for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(w % half);
+        const int h = static_cast<int>((w / half) % heads);
+        const int t = static_cast<int>(w / (static_cast<std::int64_t>(half) * heads));
+        const __nv_bfloat16* x = src + t * ld + col_off + static_cast<std::int64_t>(h) * hd;
+        const float a = __bfloat162float(x[i]), b = __bfloat162float(x[i + half]);
+        const float c = table[(static_cast<std::int64_t>(t) * half + i) * 2];
+        const float s = table[(static_cast<std::int64_t>(t) * half + i) * 2 + 1];
+        __nv_bfloat16* o = out + (static_cast<std::int64_t>(h) * seq + t) * hd;
+        o[i] = __float2bfloat16_rn(a * c - b * s);
+        o[i + half] = __float2bfloat16_rn(b * c + a * s);
+    }
+}
+
+// 32x32 smem tile transpose per head: src[t][col_off + h*hd + d] -> out[h][d][t].
+__global__ void transpose_heads_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out, int seq,
+                                       std::int64_t ld, std::int64_t col_off, int heads, int hd) {
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int h = blockIdx.z;
+    const int t0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        int t = t0 + r, d = d0 + threadIdx.x;
+        if (t < seq && d < hd) tile[r][threadIdx.x] = src[t * ld + col_off + static_cast<std::int64_t>(h) * hd + d];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        int d = d0 + r, t = t0 + threadIdx.x;
+        if (t < seq && d < hd) out[(static_cast<std::int64_t>(h) * hd + d) * seq + t] = tile[threadIdx.x][r];
+    }
+}
+
+__global__ void silu_mul_vec(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int rows,
+                             int cols) {
+    const int nv = cols / 8;
+    const std::int64_t total = static_cast<std::int64_t>(rows) * nv;
+    for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t r = w / nv, c = w % nv;
+        const uint4* row = reinterpret_cast<const uint4*>(gu + r * 2 * cols);
+        float g[8], u[8];
+        unpack8(row[c], g);
+        unpack8(row[nv + c], u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) g[j] = g[j] / (1.0f + __expf(-g[j])) * u[j];
+        reinterpret_cast<uint4*>(out + r * cols)[c] = pack8(g);
+    }
+}
+
+__global__ void silu_mul_scalar(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int rows,
+                                int cols) {
+    const std::int64_t total = static_cast<std::int64_t>(rows) * cols;
+    for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t r = w / cols, c = w % cols;
+        float g = __bfloat162float(gu[r * 2 * cols + c]), u = __bfloat162float(gu[r * 2 * cols + cols + c]);
+        out[w] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+    }
+}
+
+constexpr int kMaxSum = 16;
+struct SumArgs {
+    const void* in[kMaxSum];
+    int n;
+};
+
+__device__ __forceinline__ float ld_as_float(const void* p, std::int64_t i, int dt) {
+    return dt == BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]) : static_cast<const float*>(p)[i];
+}
+
+__global__ void sum_kernel(SumArgs a, int in_dt, void* __restrict__ out, int out_dt, std::int64_t count) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        float acc = ld_as_float(a.in[0], i, in_dt);
+        for (int k = 1; k < a.n; ++k) acc += ld_as_float(a.in[k], i, in_dt);
+        if (out_dt == BF16) static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(acc);
+        else static_cast<float*>(out)[i] = acc;
+    }
+}
+
+// fp32 partial tiles, 4 elements per thread (the fp32 matmul-chain combine).
+__global__ void sum_f32_vec(SumArgs a, float* __restrict__ out, std::int64_t count4) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count4;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        float4 acc = static_cast<const float4*>(a.in[0])[i];
+        for (int k = 1; k < a.n; ++k) {
+            float4 x = static_cast<const float4*>(a.in[k])[i];
+            acc.x += x.x;
+            acc.y += x.y;
+            acc.z += x.z;
+            acc.w += x.w;
+        }
+        reinterpret_cast<float4*>(out)[i] = acc;
+    }
+}
+
+__global__ void embedding_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
+                                 __nv_bfloat16* __restrict__ out, int dim, int vocab, int vec) {
+    const int t = blockIdx.x;
+    int id = tok[t];
+    id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
+    const __nv_bfloat16* src = table + static_cast<std::int64_t>(id) * dim;
+    __nv_bfloat16* dst = out + static_cast<std::int64_t>(t) * dim;
+    if (vec) {
+        for (int c = threadIdx.x; c < dim / 8; c += blockDim.x)
+            reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(src)[c];
+    } else {
+        for (int c = threadIdx.x; c < dim; c += blockDim.x) dst[c] = src[c];
+    }
+}
+
+__global__ void cast_kernel(const void* __restrict__ in, int in_dt, void* __restrict__ out, int out_dt,
+                            std::int64_t count) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        float x = ld_as_float(in, i, in_dt);
+        if (out_dt == BF16) static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(x);
+        else static_cast<float*>(out)[i] = x;
+    }
+}
+
+bool al16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+cudaError_t rope(const void* src, const void* table, void* out, int seq, std::int64_t ld, std::int64_t col_off,
+                 int heads, int hd, cudaStream_t s) {
+    auto S = static_cast<const __nv_bfloat16*>(src);
+    auto T = static_cast<const float*>(table);
+    auto O = static_cast<__nv_bfloat16*>(out);
+    if (hd % 16 == 0 && ld % 8 == 0 && col_off % 8 == 0 && al16(src) && al16(table) && al16(out)) {
+        std::int64_t work = static_cast<std::int64_t>(seq) * heads * (hd / 16);
+        rope_vec<<<grid_for(work), kThreads, 0, s>>>(S, T, O, seq, ld, col_off, heads, hd);
+    } else {
+        std::int64_t work = static_cast<std::int64_t>(seq) * heads * (hd / 2);
+        rope_scalar<<<grid_for(work), kThreads, 0, s>>>(S, T, O, seq, ld, col_off, heads, hd);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t transpose_heads(const void* src, void* out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
+                            int hd, cudaStream_t s) {
+    dim3 grid((seq + 31) / 32, (hd + 31) / 32, heads), block(32, 8);
+    transpose_heads_kernel<<<grid, block, 0, s>>>(static_cast<const __nv_bfloat16*>(src),
+                                                  static_cast<__nv_bfloat16*>(out), seq, ld, col_off, heads, hd);
+    return cudaGetLastError();
+}
+
+cudaError_t silu_mul(const void* gu, void* out, int rows, int cols, cudaStream_t s) {
+    auto G = static_cast<const __nv_bfloat16*>(gu);
+    auto O = static_cast<__nv_bfloat16*>(out);
+    if (cols % 8 == 0 && al16(gu) && al16(out))
+        silu_mul_vec<<<grid_for(static_cast<std::int64_t>(rows) * cols / 8), kThreads, 0, s>>>(G, O, rows, cols);
+    else
+        silu_mul_scalar<<<grid_for(static_cast<std::int64_t>(rows) * cols), kThreads, 0, s>>>(G, O, rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t sum_n(const void* const* ins, int n, int in_dtype, void* out, int out_dtype, std::int64_t count,
+                  cudaStream_t s) {
+    if (n < 1 || n > kMaxSum) return cudaErrorInvalidValue;
+    SumArgs a{};
+    a.n = n;
+    bool aligned = al16(out);
+    for (int i = 0; i < n; ++i) {
+        a.in[i] = ins[i];
+        aligned = aligned && al16(ins[i]);
+    }
+    if (in_dtype == F32 && out_dtype == F32 && count % 4 == 0 && aligned)
+        sum_f32_vec<<<grid_for(count / 4), kThreads, 0, s>>>(a, static_cast<float*>(out), count / 4);
+    else
+        sum_kernel<<<grid_for(count), kThreads, 0, s>>>(a, in_dtype, out, out_dtype, count);
+    return cudaGetLastError();
+}
+
+cudaError_t embedding(const void* tokens, const void* table, void* out, int seq, int dim, int vocab, cudaStream_t s) {
+    int vec = dim % 8 == 0 && al16(table) && al16(out);
+    embedding_kernel<<<seq, 128, 0, s>>>(static_cast<const int*>(tokens), static_cast<const __nv_bfloat16*>(table),
+                                        static_cast<__nv_bfloat16*>(out), dim, vocab, vec);
+    return cudaGetLastError();
+}
+
+cudaError_t cast(const void* in, int in_dtype, void* out, int out_dtype, std::int64_t count, cudaStream_t s) {
+    cast_kernel<<<grid_for(count), kThreads, 0, s>>>(in, in_dtype, out, out_dtype, count);
+    return cudaGetLastError();
+}
+
+}  // namespace tn::k

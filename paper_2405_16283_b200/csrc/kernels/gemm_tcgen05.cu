@@ -1,0 +1,497 @@
+// Contraction tasks: C = alpha * A·Bᵀ (+ R), batched, on
+// the 5th-gen tensor cores.
+//
+// Persistent warp-specialised kernel, one CTA per SM:
+//   warp 0   TMA producer   — 4-stage ring of 128-byte-swizzled K-major A/B
+//                             tiles (cp.async.bulk.tensor + mbarrier tx count)
+//   warp 1   MMA issuer     — one thread issues tcgen05.mma (M=128, N=BN,
+//                             K=32 bytes per instruction) into a TMEM
+//                             accumulator, double-buffered (2*BN columns) so
+//                             the epilogue of tile i overlaps the MMAs of i+1
+//   warps 2-5 epilogue      — tcgen05.ld 32x32b → fp32 regs → alpha,
+//                             residual add, bf16/fp32 pack → 16-byte stores
+// bf16 inputs use kind::f16, fp32 inputs kind::tf32 (same byte geometry:
+// a K block is always one 128-byte swizzle atom).
+// Deterministic: each output element is accumulated by one CTA in K order.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace tn::k {
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kStages = 4;
+constexpr int kAtom = 128;  // bytes of one K block row (SWIZZLE_128B span)
+constexpr int kThreads = 32 * 6;
+
+struct Params {
+    void* C;
+    const void* R;
+    int M, N, K, batch;
+    int tiles_m, tiles_n;
+    std::int64_t ldc, sc;
+    float alpha;
+    int out_dtype;
+    int causal;
+    int in_bytes;
+    int a_batched, b_batched;
+};
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint32_t bar, std::uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint32_t bar, std::uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(std::uint32_t bar, std::uint32_t parity) {
+    std::uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_3d(std::uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            std::uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(std::uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(std::uint32_t d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                       std::uint32_t accum, bool tf32) {
+    if (tf32) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accum)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accum)
+            : "memory");
+    }
+}
+// K-major operand in a SWIZZLE_128B layout: rows of 128 B, 8-row groups
+// 1024 B apart (SBO), LBO unused, descriptor version 1 (sm_100).
+__device__ __forceinline__ std::uint64_t sdesc(std::uint32_t saddr) {
+    std::uint64_t d = 0;
+    d |= static_cast<std::uint64_t>((saddr & 0x3FFFF) >> 4);
+    d |= static_cast<std::uint64_t>(1) << 16;
+    d |= static_cast<std::uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<std::uint64_t>(1) << 46;
+    d |= static_cast<std::uint64_t>(2) << 61;
+    return d;
+}
+
+#define TN_LD32(taddr, r)                                                                                     \
+    asm volatile(                                                                                             \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                   \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),     \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),            \
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),          \
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),          \
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                               \
+        : "r"(taddr))
+
+__device__ __forceinline__ bool tile_skipped(const Params& p, int mb, int nb, int bn) {
+    return p.causal == 1 && nb * bn > mb * kBM + kBM - 1;
+}
+
+__device__ __forceinline__ void decode(const Params& p, int t, int& b, int& mb, int& nb) {
+    int per = p.tiles_m * p.tiles_n;
+    b = t / per;
+    int r = t - b * per;
+    mb = r / p.tiles_n;
+    nb = r - mb * p.tiles_n;
+}
+
+__device__ __forceinline__ int kblocks(const Params& p, int mb, int bk) {
+    int kb = (p.K + bk - 1) / bk;
+    if (p.causal == 2) kb = min(kb, ((mb + 1) * kBM + bk - 1) / bk);
+    return kb;
+}
+
+__device__ __forceinline__ std::uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<std::uint32_t*>(&v);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
+    constexpr int A_BYTES = kBM * kAtom;
+    constexpr int B_BYTES = BN * kAtom;
+    constexpr int STAGE = A_BYTES + B_BYTES;
+    constexpr std::uint32_t TMEM_COLS = 2 * BN;
+
+    extern __shared__ std::uint8_t smem_raw[];
+    const std::uint32_t raw = smem_u32(smem_raw);
+    const std::uint32_t pad = ((raw + 1023) & ~1023u) - raw;
+    std::uint8_t* smem = smem_raw + pad;
+    const std::uint32_t sbase = raw + pad;
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStages * STAGE);
+    const std::uint32_t full = smem_u32(bars), empty = full + 8 * kStages;
+    const std::uint32_t tfull = empty + 8 * kStages, tempty = tfull + 16;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 4);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int bk = kAtom / p.in_bytes;
+    const bool tf32 = p.in_bytes == 4;
+    const int tiles = p.batch * p.tiles_m * p.tiles_n;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&ta)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tb)) : "memory");
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full + 8 * s, 1);
+            mbar_init(empty + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + 8 * a, 1);
+            mbar_init(tempty + 8 * a, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const std::uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            std::uint32_t phase = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int b, mb, nb;
+                decode(p, t, b, mb, nb);
+                if (tile_skipped(p, mb, nb, BN)) continue;
+                const int nk = kblocks(p, mb, bk);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(empty + 8 * stage, phase ^ 1);
+                    const std::uint32_t fb = full + 8 * stage;
+                    mbar_expect_tx(fb, STAGE);
+                    const std::uint32_t sa = sbase + stage * STAGE;
+                    tma_load_3d(sa, &ta, kb * bk, mb * kBM, p.a_batched ? b : 0, fb);
+                    tma_load_3d(sa + A_BYTES, &tb, kb * bk, nb * BN, p.b_batched ? b : 0, fb);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const std::uint32_t fmt = tf32 ? 2u : 1u;
+            const std::uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
+                                        (static_cast<std::uint32_t>(BN >> 3) << 17) |
+                                        (static_cast<std::uint32_t>(kBM >> 4) << 24);
+            int stage = 0, acc = 0;
+            std::uint32_t phase = 0, acc_phase = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int b, mb, nb;
+                decode(p, t, b, mb, nb);
+                if (tile_skipped(p, mb, nb, BN)) continue;
+                const int nk = kblocks(p, mb, bk);
+                mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
+                tc_fence_after();
+                const std::uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(full + 8 * stage, phase);
+                    tc_fence_after();
+                    const std::uint32_t sa = sbase + stage * STAGE;
+                    const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + A_BYTES);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)  // 4 x 32 bytes of K per 128-byte block
+                        tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                    tc_commit(empty + 8 * stage);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(tfull + 8 * acc);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // Epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (its subpartition).
+        const int lane_base = (warp % 4) * 32;
+        int acc = 0;
+        std::uint32_t acc_phase = 0;
+        const int ob = p.out_dtype == BF16 ? 2 : 4;
+        const bool vec_ok = (p.N % 32 == 0) && ((p.ldc * ob) % 16 == 0) && ((p.sc * ob) % 16 == 0) &&
+                            ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
+                            ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            int b, mb, nb;
+            decode(p, t, b, mb, nb);
+            if (tile_skipped(p, mb, nb, BN)) continue;
+            mbar_wait(tfull + 8 * acc, acc_phase);
+            tc_fence_after();
+            const int row = mb * kBM + lane_base + lane;
+            const bool row_ok = row < p.M;
+            const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                std::uint32_t r[32];
+                const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN + c0;
+                TN_LD32(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int n0 = nb * BN + c0;
+                if (!row_ok || n0 >= p.N) continue;
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+                if (vec_ok) {
+                    if (p.out_dtype == BF16) {
+                        __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off + n0;
+                        if (p.R) {
+                            const uint4* rr = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.R) + off + n0);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                uint4 x = rr[q];
+                                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&x);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) v[q * 8 + j] += __bfloat162float(h[j]);
+                            }
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(c);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            dst[q] = make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                                pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+                    } else {
+                        float* c = static_cast<float*>(p.C) + off + n0;
+                        if (p.R) {
+                            const float4* rr = reinterpret_cast<const float4*>(static_cast<const float*>(p.R) + off + n0);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                float4 x = rr[q];
+                                v[q * 4 + 0] += x.x;
+                                v[q * 4 + 1] += x.y;
+                                v[q * 4 + 2] += x.z;
+                                v[q * 4 + 3] += x.w;
+                            }
+                        }
+                        float4* dst = reinterpret_cast<float4*>(c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+                    }
+                } else {
+                    for (int j = 0; j < 32 && n0 + j < p.N; ++j) {
+                        float x = v[j];
+                        if (p.out_dtype == BF16) {
+                            __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off + n0 + j;
+                            if (p.R) x += __bfloat162float(static_cast<const __nv_bfloat16*>(p.R)[off + n0 + j]);
+                            *c = __float2bfloat16_rn(x);
+                        } else {
+                            float* c = static_cast<float*>(p.C) + off + n0 + j;
+                            if (p.R) x += static_cast<const float*>(p.R)[off + n0 + j];
+                            *c = x;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + 8 * acc);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+}
+
+// --- SIMT fallback: one warp per output element, fp32 accumulate in K order.
+// Used for tiny M (GEMV-like last-token heads) or shapes TMA cannot describe.
+__global__ void gemm_simt_kernel(GemmArgs a) {
+    const std::int64_t gw = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
+    const std::int64_t total = static_cast<std::int64_t>(a.batch) * a.M * a.N;
+    if (gw >= total) return;
+    const int n = static_cast<int>(gw % a.N);
+    const int m = static_cast<int>((gw / a.N) % a.M);
+    const int b = static_cast<int>(gw / (static_cast<std::int64_t>(a.N) * a.M));
+    if (a.causal == 1 && n > m) return;
+    int kend = a.K;
+    if (a.causal == 2) kend = min(kend, m + 1);
+    float acc = 0.f;
+    if (a.in_dtype == BF16) {
+        const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
+        const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B) + b * a.sb + static_cast<std::int64_t>(n) * a.ldb;
+        for (int k = lane; k < kend; k += 32) acc += __bfloat162float(A[k]) * __bfloat162float(B[k]);
+    } else {
+        const float* A = static_cast<const float*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
+        const float* B = static_cast<const float*>(a.B) + b * a.sb + static_cast<std::int64_t>(n) * a.ldb;
+        for (int k = lane; k < kend; k += 32) acc += A[k] * B[k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane != 0) return;
+    acc *= a.alpha;
+    const std::int64_t off = b * a.sc + static_cast<std::int64_t>(m) * a.ldc + n;
+    if (a.out_dtype == BF16) {
+        if (a.R) acc += __bfloat162float(static_cast<const __nv_bfloat16*>(a.R)[off]);
+        static_cast<__nv_bfloat16*>(a.C)[off] = __float2bfloat16_rn(acc);
+    } else {
+        if (a.R) acc += static_cast<const float*>(a.R)[off];
+        static_cast<float*>(a.C)[off] = acc;
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    }
+    return fn;
+}
+
+bool encode(CUtensorMap* map, const void* base, int esize, std::int64_t K, std::int64_t rows, std::int64_t ld,
+            int batch, std::int64_t bstride, int box_rows) {
+    EncodeFn fn = get_encode();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
+    std::int64_t bs = batch > 1 ? bstride : rows * ld;
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * esize), static_cast<cuuint64_t>(bs * esize)};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(kAtom / esize), static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN>
+int smem_bytes() {
+    return kStages * (kBM + BN) * kAtom + 256 + 1024;
+}
+
+}  // namespace
+
+double gemm_flops(const GemmArgs& a) {
+    double mnk = 2.0 * a.M * static_cast<double>(a.N) * a.K * a.batch;
+    if (a.causal) mnk *= 0.5 * (1.0 + 1.0 / std::max(1, a.M));  // lower triangle incl. diagonal
+    return mnk;
+}
+
+cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
+    plan->args = a;
+    const int es = dtype_size(a.in_dtype);
+    auto al16 = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
+    const int bn = a.N <= 128 ? 128 : 256;
+    bool ok = a.M >= kBM && a.N >= bn && a.K * es >= kAtom && al16(a.A) && al16(a.B) && (a.lda * es) % 16 == 0 &&
+              (a.ldb * es) % 16 == 0 && (a.batch == 1 || ((a.sa * es) % 16 == 0 && (a.sb * es) % 16 == 0)) &&
+              (a.in_dtype == BF16 || a.in_dtype == F32);
+    if (ok) {
+        const bool ab = a.batch > 1 && a.sa != 0, bb = a.batch > 1 && a.sb != 0;
+        ok = encode(&plan->ta, a.A, es, a.K, a.M, a.lda, ab ? a.batch : 1, a.sa, kBM) &&
+             encode(&plan->tb, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, bn);
+    }
+    plan->path = ok ? 0 : 1;
+    plan->bn = bn;
+    const int tm = (a.M + kBM - 1) / kBM, tn = (a.N + bn - 1) / bn;
+    plan->tiles = a.batch * tm * tn;
+    plan->grid = std::min(plan->tiles, std::max(1, num_sms));
+    if (ok) {
+        static unsigned long long attr_set = 0;  // per CUDA device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!((attr_set >> dev) & 1ULL)) {
+            cudaFuncSetAttribute(gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
+            cudaFuncSetAttribute(gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>());
+            attr_set |= 1ULL << dev;
+        }
+    }
+    return cudaSuccess;
+}
+
+cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
+    const GemmArgs& a = plan.args;
+    if (plan.path == 1) {
+        const std::int64_t warps = static_cast<std::int64_t>(a.batch) * a.M * a.N;
+        const int threads = 256;
+        const std::int64_t blocks = (warps * 32 + threads - 1) / threads;
+        gemm_simt_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
+    Params p;
+    p.C = a.C;
+    p.R = a.R;
+    p.M = a.M;
+    p.N = a.N;
+    p.K = a.K;
+    p.batch = a.batch;
+    p.tiles_m = (a.M + kBM - 1) / kBM;
+    p.tiles_n = (a.N + plan.bn - 1) / plan.bn;
+    p.ldc = a.ldc;
+    p.sc = a.sc;
+    p.alpha = a.alpha;
+    p.out_dtype = a.out_dtype;
+    p.causal = a.causal;
+    p.in_bytes = dtype_size(a.in_dtype);
+    p.a_batched = a.batch > 1 && a.sa != 0;
+    p.b_batched = a.batch > 1 && a.sb != 0;
+    if (plan.bn == 128)
+        gemm_kernel<128><<<plan.grid, kThreads, smem_bytes<128>(), s>>>(plan.ta, plan.tb, p);
+    else
+        gemm_kernel<256><<<plan.grid, kThreads, smem_bytes<256>(), s>>>(plan.ta, plan.tb, p);
+    return cudaGetLastError();
+}
+
+}  // namespace tn::k

@@ -1,0 +1,83 @@
+// Host-side launch interface of the sm_100a task kernels. Every memgraph
+// Kernel vertex maps to exactly one of these launches (op payload types in
+// exec/ops.hpp). All kernels are deterministic: fixed reduction order, no
+// atomics, so a vertex's output does not depend on the dispatch schedule.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tn::k {
+
+enum DType : int { BF16 = 0, F32 = 1, I32 = 2 };
+
+inline int dtype_size(int dt) { return dt == BF16 ? 2 : 4; }
+
+// C[b][m][n] = alpha * sum_k A[b][m][k] * B[b][n][k] (+ R[b][m][n])
+// A, B K-major (row-major [M,K] and [N,K]); C, R row-major with ldc.
+// causal: 0 none; 1 "scores" (tiles strictly above the diagonal are
+// skipped — their values are never read by a causal softmax); 2 "probs"
+// (the K loop stops at the diagonal; P is zero beyond it).
+struct GemmArgs {
+    const void* A = nullptr;
+    const void* B = nullptr;
+    const void* R = nullptr;
+    void* C = nullptr;
+    int M = 0, N = 0, K = 0, batch = 1;
+    std::int64_t lda = 0, ldb = 0, ldc = 0;
+    std::int64_t sa = 0, sb = 0, sc = 0;  // batch strides (elements)
+    float alpha = 1.0f;
+    int in_dtype = BF16;   // BF16 -> kind::f16, F32 -> kind::tf32
+    int out_dtype = BF16;
+    int causal = 0;
+};
+
+struct alignas(64) GemmPlan {
+    CUtensorMap ta;  // A: (K, M, batch)
+    CUtensorMap tb;  // B: (K, N, batch)
+    GemmArgs args;
+    int path = 0;    // 0 tcgen05/TMA, 1 SIMT fallback (small or unaligned shapes)
+    int bn = 256;    // N tile of the tcgen05 path
+    int tiles = 0;   // output tiles (all batches)
+    int grid = 0;
+};
+
+// Encodes TMA descriptors (needs a CUDA context on the target device).
+cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms);
+cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s);
+double gemm_flops(const GemmArgs& a);  // algorithmic FLOPs (causal-aware)
+
+// y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w        (bf16 in/out, fp32 math)
+cudaError_t rmsnorm(const void* x, const void* w, void* y, int rows, int cols, float eps, cudaStream_t s);
+
+// P[b][i][j] = softmax_j(scale * S[b][i][j]) over j <= i (causal) or all j;
+// masked entries are written as exact zeros. S fp32, P bf16.
+cudaError_t softmax(const void* S, void* P, int batch, int rows, int cols, float scale, int causal,
+                    cudaStream_t s);
+
+// Rotate-half RoPE: src [seq, ld] bf16, head h at columns col_off + h*hd;
+// table fp32 [seq, hd/2, 2] = (cos, sin); out [H, seq, hd] bf16 (head-major).
+cudaError_t rope(const void* src, const void* table, void* out, int seq, std::int64_t ld, std::int64_t col_off,
+                 int heads, int hd, cudaStream_t s);
+
+// out[h][d][t] = src[t][col_off + h*hd + d]  (V^T per head, bf16)
+cudaError_t transpose_heads(const void* src, void* out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
+                            int hd, cudaStream_t s);
+
+// out[r][c] = silu(gu[r][c]) * gu[r][cols + c]   (bf16, fp32 math)
+cudaError_t silu_mul(const void* gu, void* out, int rows, int cols, cudaStream_t s);
+
+// out = sum_i in[i] in argument order, fp32 accumulate; dtypes per tensor.
+cudaError_t sum_n(const void* const* ins, int n, int in_dtype, void* out, int out_dtype, std::int64_t count,
+                  cudaStream_t s);
+
+// out[t][:] = table[tokens[t]][:]   (tokens int32, table bf16 [vocab, dim])
+cudaError_t embedding(const void* tokens, const void* table, void* out, int seq, int dim, int vocab,
+                      cudaStream_t s);
+
+// Elementwise dtype cast (bf16 <-> f32), RNE.
+cudaError_t cast(const void* in, int in_dtype, void* out, int out_dtype, std::int64_t count, cudaStream_t s);
+
+}  // namespace tn::k

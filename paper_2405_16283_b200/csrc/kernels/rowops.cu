@@ -1,0 +1,213 @@
+// Row-reduction tasks: RMSNorm and (causal) softmax.
+// One CTA per row; 128-bit coalesced loads, the row is kept in registers,
+// warp-shuffle + shared-memory reductions in a fixed tree order (the result
+// is independent of the schedule and of other rows).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace tn::k {
+namespace {
+
+constexpr int kRowThreads = 256;
+
+template <bool kMax>
+__device__ __forceinline__ float block_reduce(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o /= 2) {
+        float w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = kMax ? fmaxf(v, w) : v + w;
+    }
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    __syncthreads();  // red[] reuse across calls
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float r = red[0];
+    for (int i = 1; i < kRowThreads / 32; ++i) r = kMax ? fmaxf(r, red[i]) : r + red[i];
+    return r;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 x = __bfloat1622float2(h[i]);
+        f[2 * i] = x.x;
+        f[2 * i + 1] = x.y;
+    }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return u;
+}
+
+// cols % 8 == 0, <= kRowThreads * 8 * kMaxVec
+template <int kMaxVec>
+__global__ void __launch_bounds__(kRowThreads) rmsnorm_vec(const __nv_bfloat16* __restrict__ x,
+                                                           const __nv_bfloat16* __restrict__ w,
+                                                           __nv_bfloat16* __restrict__ y, int cols, float eps) {
+    __shared__ float red[kRowThreads / 32];
+    const std::int64_t row = blockIdx.x;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+    const int nv = cols / 8;
+    float v[kMaxVec][8];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+        int c = threadIdx.x + i * kRowThreads;
+        if (c < nv) {
+            unpack8(xr[c], v[i]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss += v[i][j] * v[i][j];
+        }
+    }
+    ss = block_reduce<false>(ss, red);
+    const float inv = rsqrtf(ss / static_cast<float>(cols) + eps);
+    const uint4* wr = reinterpret_cast<const uint4*>(w);
+    uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+        int c = threadIdx.x + i * kRowThreads;
+        if (c < nv) {
+            float g[8];
+            unpack8(wr[c], g);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[i][j] = v[i][j] * inv * g[j];
+            yr[c] = pack8(v[i]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kRowThreads) rmsnorm_scalar(const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ w,
+                                                              __nv_bfloat16* __restrict__ y, int cols, float eps) {
+    __shared__ float red[kRowThreads / 32];
+    const std::int64_t row = blockIdx.x;
+    float ss = 0.f;
+    for (int c = threadIdx.x; c < cols; c += kRowThreads) {
+        float a = __bfloat162float(x[row * cols + c]);
+        ss += a * a;
+    }
+    ss = block_reduce<false>(ss, red);
+    const float inv = rsqrtf(ss / static_cast<float>(cols) + eps);
+    for (int c = threadIdx.x; c < cols; c += kRowThreads)
+        y[row * cols + c] = __float2bfloat16_rn(__bfloat162float(x[row * cols + c]) * inv * __bfloat162float(w[c]));
+}
+
+// Causal/full softmax of fp32 scores into bf16 probabilities, row in
+// registers (cols % 4 == 0, cols <= kRowThreads * 4 * kMaxVec).
+template <int kMaxVec>
+__global__ void __launch_bounds__(kRowThreads) softmax_vec(const float* __restrict__ S, __nv_bfloat16* __restrict__ P,
+                                                           int rows, int cols, float scale_log2, int causal) {
+    __shared__ float red[kRowThreads / 32];
+    const std::int64_t r = blockIdx.x;  // over batch*rows
+    const int i = static_cast<int>(r % rows);
+    const int valid = causal ? min(cols, i + 1) : cols;
+    const float4* sr = reinterpret_cast<const float4*>(S + r * cols);
+    const int nv = cols / 4;
+    float v[kMaxVec][4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < kMaxVec; ++q) {
+        int c = threadIdx.x + q * kRowThreads;
+        if (c < nv && c * 4 < valid) {
+            float4 a = sr[c];
+            v[q][0] = a.x * scale_log2;
+            v[q][1] = a.y * scale_log2;
+            v[q][2] = a.z * scale_log2;
+            v[q][3] = a.w * scale_log2;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (c * 4 + j < valid) mx = fmaxf(mx, v[q][j]);
+        }
+    }
+    mx = block_reduce<true>(mx, red);
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < kMaxVec; ++q) {
+        int c = threadIdx.x + q * kRowThreads;
+        if (c < nv) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float e = (c * 4 + j < valid) ? exp2f(v[q][j] - mx) : 0.f;
+                v[q][j] = e;
+                sum += e;
+            }
+        }
+    }
+    sum = block_reduce<false>(sum, red);
+    const float inv = 1.0f / sum;
+    uint2* pr = reinterpret_cast<uint2*>(P + r * cols);
+#pragma unroll
+    for (int q = 0; q < kMaxVec; ++q) {
+        int c = threadIdx.x + q * kRowThreads;
+        if (c < nv) {
+            uint2 u;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+            h[0] = __floats2bfloat162_rn(v[q][0] * inv, v[q][1] * inv);
+            h[1] = __floats2bfloat162_rn(v[q][2] * inv, v[q][3] * inv);
+            pr[c] = u;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kRowThreads) softmax_scalar(const float* __restrict__ S, __nv_bfloat16* __restrict__ P,
+                                                              int rows, int cols, float scale_log2, int causal) {
+    __shared__ float red[kRowThreads / 32];
+    const std::int64_t r = blockIdx.x;
+    const int i = static_cast<int>(r % rows);
+    const int valid = causal ? min(cols, i + 1) : cols;
+    const float* s = S + r * cols;
+    float mx = -INFINITY;
+    for (int c = threadIdx.x; c < valid; c += kRowThreads) mx = fmaxf(mx, s[c] * scale_log2);
+    mx = block_reduce<true>(mx, red);
+    float sum = 0.f;
+    for (int c = threadIdx.x; c < valid; c += kRowThreads) sum += exp2f(s[c] * scale_log2 - mx);
+    sum = block_reduce<false>(sum, red);
+    const float inv = 1.0f / sum;
+    for (int c = threadIdx.x; c < cols; c += kRowThreads)
+        P[r * cols + c] = __float2bfloat16_rn(c < valid ? exp2f(s[c] * scale_log2 - mx) * inv : 0.f);
+}
+
+bool al16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+cudaError_t rmsnorm(const void* x, const void* w, void* y, int rows, int cols, float eps, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    auto X = static_cast<const __nv_bfloat16*>(x);
+    auto W = static_cast<const __nv_bfloat16*>(w);
+    auto Y = static_cast<__nv_bfloat16*>(y);
+    if (cols % 8 == 0 && al16(x) && al16(w) && al16(y) && cols <= kRowThreads * 8 * 8) {
+        if (cols <= kRowThreads * 8 * 2) rmsnorm_vec<2><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
+        else if (cols <= kRowThreads * 8 * 4) rmsnorm_vec<4><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
+        else rmsnorm_vec<8><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
+    } else {
+        rmsnorm_scalar<<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t softmax(const void* S, void* P, int batch, int rows, int cols, float scale, int causal, cudaStream_t s) {
+    const std::int64_t n = static_cast<std::int64_t>(batch) * rows;
+    if (n <= 0) return cudaSuccess;
+    const float sl2 = scale * 1.4426950408889634f;
+    auto Sp = static_cast<const float*>(S);
+    auto Pp = static_cast<__nv_bfloat16*>(P);
+    if (cols % 4 == 0 && al16(S) && (reinterpret_cast<std::uintptr_t>(P) & 7) == 0 && cols <= kRowThreads * 4 * 16) {
+        if (cols <= kRowThreads * 4 * 4) softmax_vec<4><<<static_cast<unsigned>(n), kRowThreads, 0, s>>>(Sp, Pp, rows, cols, sl2, causal);
+        else if (cols <= kRowThreads * 4 * 8) softmax_vec<8><<<static_cast<unsigned>(n), kRowThreads, 0, s>>>(Sp, Pp, rows, cols, sl2, causal);
+        else softmax_vec<16><<<static_cast<unsigned>(n), kRowThreads, 0, s>>>(Sp, Pp, rows, cols, sl2, causal);
+    } else {
+        softmax_scalar<<<static_cast<unsigned>(n), kRowThreads, 0, s>>>(Sp, Pp, rows, cols, sl2, causal);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace tn::k

@@ -1,0 +1,315 @@
+"""Taskgraph generators with op payloads.
+
+The reference generators (proj/src/taskgraph.cpp:418-616) emit unit-sized
+opaque tasks. These emit byte-sized, device-assigned taskgraphs whose kernel
+vertices carry an "op" payload (schema: csrc/exec/ops.hpp); the reference
+parser ignores the extra key (taskgraph.cpp:375-389), so every graph here is
+also a valid input of the reference memplan and builds a bit-identical
+memgraph there.
+
+Sizes are padded to a multiple of ALIGN bytes so the planner's first-fit
+offsets (prefix sums of sizes, compiler.cpp:205-216) stay 1 KiB aligned for
+TMA and 128-bit access (SURVEY hard part 4).
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+ALIGN = 1024
+DSIZE = {"bf16": 2, "f32": 4, "i32": 4}
+# cost_hint model (abstract seconds) for the virtual-time simulator only.
+_PEAK_FLOPS = 1.4e15
+_HBM = 6.5e12
+
+
+def _pad(n: int) -> int:
+    return max(ALIGN, (n + ALIGN - 1) // ALIGN * ALIGN)
+
+
+@dataclass
+class Tensor:
+    id: int
+    name: str
+    shape: tuple
+    dtype: str
+    device: int
+    init: tuple | None = None  # inputs: ("normal", std) | ("uniform", lo, hi) | ("tokens", vocab) | ("rope", theta)
+
+    @property
+    def nbytes(self) -> int:
+        return int(np.prod(self.shape)) * DSIZE[self.dtype]
+
+
+@dataclass
+class GraphBuilder:
+    device_count: int = 1
+    vertices: list = field(default_factory=list)
+    edges: list = field(default_factory=list)
+    tensors: dict = field(default_factory=dict)
+    flops: float = 0.0
+
+    def _add(self, kind, name, shape, dtype, device, cost, op=None, src_device=-1, init=None):
+        vid = len(self.vertices)
+        t = Tensor(vid, name, tuple(shape), dtype, device, init)
+        v = {"id": vid, "kind": kind, "device": device}
+        if kind == "transfer":
+            v["src_device"] = src_device
+        v["output_size"] = _pad(t.nbytes)
+        v["cost_hint"] = float(cost)
+        if op is not None:
+            v["op"] = op
+        self.vertices.append(v)
+        self.tensors[vid] = t
+        return vid
+
+    def input(self, name, shape, dtype="bf16", device=0, init=("normal", 0.02)):
+        return self._add("input", name, shape, dtype, device, 0.0, init=init)
+
+    def kernel(self, name, op, shape, dtype, device=0, cost=None):
+        for a in op["args"]:
+            if self.tensors[a].device != device:
+                raise ValueError(f"{name}: argument {a} lives on device {self.tensors[a].device}")
+        if cost is None:
+            cost = self._cost(op, shape, dtype)
+        vid = self._add("kernel", name, shape, dtype, device, cost, op=op)
+        for a in dict.fromkeys(op["args"]):
+            self.edges.append([a, vid])
+        return vid
+
+    def transfer(self, src, device, name=None):
+        t = self.tensors[src]
+        vid = self._add("transfer", name or f"{t.name}@{device}", t.shape, t.dtype, device,
+                        t.nbytes / 7.7e11, src_device=t.device)
+        self.edges.append([src, vid])
+        return vid
+
+    def _cost(self, op, shape, dtype):
+        if op["type"] == "gemm":
+            f = 2.0 * op["M"] * op["N"] * op["K"] * op.get("batch", 1) * (0.5 if op.get("causal") else 1.0)
+            self.flops += f
+            return f / _PEAK_FLOPS
+        byts = sum(self.tensors[a].nbytes for a in op["args"]) + int(np.prod(shape)) * DSIZE[dtype]
+        return byts / _HBM
+
+    # --- ops -----------------------------------------------------------------
+    def gemm(self, name, a, b, M, N, K, *, r=None, out_dtype="bf16", in_dtype="bf16", device=0, **kw):
+        op = {"type": "gemm", "args": [a, b] + ([r] if r is not None else []), "M": M, "N": N, "K": K,
+              "in_dtype": in_dtype, "out_dtype": out_dtype}
+        op.update({k: v for k, v in kw.items() if v is not None and k != "out_shape"})
+        shape = kw.get("out_shape") or (op.get("batch", 1), M, N)
+        return self.kernel(name, op, shape, out_dtype, device)
+
+    def to_json(self) -> str:
+        return json.dumps({"device_count": self.device_count, "vertices": self.vertices, "edges": self.edges})
+
+    def meta(self) -> dict:
+        return {vid: {"name": t.name, "shape": list(t.shape), "dtype": t.dtype, "device": t.device,
+                      "init": list(t.init) if t.init else None} for vid, t in self.tensors.items()}
+
+    def inputs(self):
+        return [t for t in self.tensors.values() if t.init is not None]
+
+    def outputs(self):
+        consumed = {p for p, _ in self.edges}
+        return [vid for vid in self.tensors if vid not in consumed]
+
+
+# ------------------------------------------------------------ input data ---
+def make_input(t: Tensor, seed: int) -> np.ndarray:
+    """Deterministic synthetic bytes for an input tensor (host numpy)."""
+    rng = np.random.default_rng([seed, t.id])
+    n = int(np.prod(t.shape))
+    kind = t.init[0]
+    if kind == "tokens":
+        return rng.integers(0, t.init[1], size=n, dtype=np.int32)
+    if kind == "rope":
+        S, half = t.shape[0], t.shape[1]
+        theta = float(t.init[1])
+        inv = theta ** (-np.arange(half, dtype=np.float64) * 2.0 / (2 * half))
+        ang = np.arange(S, dtype=np.float64)[:, None] * inv[None, :]
+        tab = np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+        return tab
+    if kind == "ones":
+        x = np.ones(n, dtype=np.float32)
+    elif kind == "normal":
+        x = rng.standard_normal(n, dtype=np.float32) * np.float32(t.init[1])
+    elif kind == "uniform":
+        x = rng.uniform(t.init[1], t.init[2], size=n).astype(np.float32)
+    else:
+        raise ValueError(kind)
+    if t.dtype == "bf16":
+        u = x.view(np.uint32)
+        return (((u + (((u >> 16) & 1) + 0x7FFF)) >> 16).astype(np.uint16))
+    return x
+
+
+# ---------------------------------------------------------------- LLaMA ---
+@dataclass
+class LlamaConfig:
+    dim: int = 4096
+    layers: int = 32
+    heads: int = 32
+    ffn: int = 11008
+    vocab: int = 32000
+    eps: float = 1e-5
+    theta: float = 10000.0
+
+    @property
+    def hd(self) -> int:
+        return self.dim // self.heads
+
+
+LLAMA_7B = LlamaConfig()
+LLAMA_65B = LlamaConfig(dim=8192, layers=80, heads=64, ffn=22016)
+
+
+def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device: int = 0,
+                  std: float = 0.02) -> GraphBuilder:
+    """One forward prefill over `seq` tokens (causal), single device.
+
+    Per layer: rmsnorm -> QKV gemm -> rope(q), rope(k), Vᵀ -> batched causal
+    QKᵀ (fp32 scores, upper tiles skipped) -> causal softmax (bf16 P) ->
+    batched P·V written straight into [seq, dim] -> O-proj gemm with fused
+    residual -> rmsnorm -> gate/up gemm -> silu·mul -> down gemm + residual.
+    Head: final rmsnorm -> last-token logits (fp32). Weights are graph inputs
+    (cold in host RAM, materialised by H2D at dispatch).
+    """
+    L = cfg.layers if layers is None else layers
+    d, H, hd, f, V, S = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, cfg.vocab, seq
+    g = GraphBuilder(device_count=1)
+    dev = device
+    tok = g.input("tokens", (S,), "i32", dev, init=("tokens", V))
+    emb = g.input("tok_embeddings", (V, d), "bf16", dev, init=("normal", std))
+    rope_tab = g.input("rope_table", (S, hd // 2, 2), "f32", dev, init=("rope", cfg.theta))
+    x = g.kernel("embed", {"type": "embedding", "args": [tok, emb], "seq": S, "dim": d, "vocab": V}, (S, d), "bf16", dev)
+    for l in range(L):
+        p = f"layers.{l}."
+        wn1 = g.input(p + "attention_norm", (d,), "bf16", dev, init=("normal", 1.0))
+        wqkv = g.input(p + "wqkv", (3 * d, d), "bf16", dev, init=("normal", std))
+        wo = g.input(p + "wo", (d, d), "bf16", dev, init=("normal", std))
+        wn2 = g.input(p + "ffn_norm", (d,), "bf16", dev, init=("normal", 1.0))
+        w13 = g.input(p + "w13", (2 * f, d), "bf16", dev, init=("normal", std))
+        w2 = g.input(p + "w2", (d, f), "bf16", dev, init=("normal", std))
+        h = g.kernel(p + "attn_norm_out", {"type": "rmsnorm", "args": [x, wn1], "rows": S, "cols": d, "eps": cfg.eps},
+                     (S, d), "bf16", dev)
+        qkv = g.gemm(p + "qkv", h, wqkv, S, 3 * d, d, out_shape=(S, 3 * d), device=dev)
+        q = g.kernel(p + "q_rope", {"type": "rope", "args": [qkv, rope_tab], "seq": S, "ld": 3 * d, "col_off": 0,
+                                    "heads": H, "hd": hd}, (H, S, hd), "bf16", dev)
+        k = g.kernel(p + "k_rope", {"type": "rope", "args": [qkv, rope_tab], "seq": S, "ld": 3 * d, "col_off": d,
+                                    "heads": H, "hd": hd}, (H, S, hd), "bf16", dev)
+        vt = g.kernel(p + "v_t", {"type": "transpose_heads", "args": [qkv], "seq": S, "ld": 3 * d, "col_off": 2 * d,
+                                  "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
+        sc = g.gemm(p + "scores", q, k, S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S, out_dtype="f32",
+                    causal=1, out_shape=(H, S, S), device=dev)
+        pr = g.kernel(p + "probs", {"type": "softmax", "args": [sc], "batch": H, "rows": S, "cols": S,
+                                    "scale": 1.0 / math.sqrt(hd), "causal": 1}, (H, S, S), "bf16", dev)
+        o = g.gemm(p + "attn", pr, vt, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                   causal=2, out_shape=(S, d), device=dev)
+        x = g.gemm(p + "attn_out", o, wo, S, d, d, r=x, out_shape=(S, d), device=dev)
+        h2 = g.kernel(p + "ffn_norm_out", {"type": "rmsnorm", "args": [x, wn2], "rows": S, "cols": d, "eps": cfg.eps},
+                      (S, d), "bf16", dev)
+        gu = g.gemm(p + "gate_up", h2, w13, S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
+        a = g.kernel(p + "act", {"type": "silu_mul", "args": [gu], "rows": S, "cols": f}, (S, f), "bf16", dev)
+        x = g.gemm(p + "ffn_out", a, w2, S, d, f, r=x, out_shape=(S, d), device=dev)
+    wn = g.input("norm", (d,), "bf16", dev, init=("normal", 1.0))
+    wout = g.input("output", (V, d), "bf16", dev, init=("normal", std))
+    hn = g.kernel("final_norm", {"type": "rmsnorm", "args": [x, wn], "rows": S, "cols": d, "eps": cfg.eps},
+                  (S, d), "bf16", dev)
+    g.gemm("logits", hn, wout, 1, V, d, a_off=(S - 1) * d, out_dtype="f32", out_shape=(1, V), device=dev)
+    return g
+
+
+def prefill_flops(cfg: LlamaConfig, seq: int, layers: int | None = None) -> float:
+    """Algorithmic FLOPs of llama_prefill (causal attention counted as half)."""
+    L = cfg.layers if layers is None else layers
+    d, f, S, hd, H = cfg.dim, cfg.ffn, seq, cfg.hd, cfg.heads
+    lin = 2.0 * S * (3 * d * d + d * d + 2 * f * d + f * d)
+    attn = 2 * (2.0 * S * S * hd * H) * 0.5 * (1 + 1 / S)
+    return L * (lin + attn) + 2.0 * cfg.vocab * d
+
+
+# ------------------------------------------------- tiled matmul chain (cfg 1) ---
+def matmul_chain(n: int = 4096, tile: int = 1024, chain: int = 4, devices: int = 2,
+                 dtype: str = "f32") -> GraphBuilder:
+    """Config 1: X·W1·W2·…·WL, n×n fp32, tiled `tile`×`tile`.
+
+    Row panels of X are split over devices; each device holds its own copy of
+    every weight tile (inputs), computes per-tile partial products (one gemm
+    vertex per (i, j, k)) and a fixed-order combine (`sum` of the k partials,
+    so the reduction order never depends on the schedule). Between links the
+    activation row panels are exchanged with Transfer vertices (all-gather of
+    panels), which exercises the move path across devices.
+    Weights are stored transposed per tile (B operand is K-major)."""
+    T = n // tile
+    g = GraphBuilder(device_count=devices)
+    rows_per_dev = [list(range(d * T // devices, (d + 1) * T // devices)) for d in range(devices)]
+    owner = {i: d for d in range(devices) for i in rows_per_dev[d]}
+    X = {(i, k): g.input(f"X[{i},{k}]", (tile, tile), dtype, owner[i], init=("uniform", -1 / 64, 1 / 64))
+         for i in range(T) for k in range(T)}
+    cur = X
+    for l in range(chain):
+        Wt = {}
+        for d in range(devices):
+            for j in range(T):
+                for k in range(T):
+                    Wt[(d, j, k)] = g.input(f"W{l}T[{j},{k}]@{d}", (tile, tile), dtype, d,
+                                            init=("uniform", -1 / 64, 1 / 64))
+        nxt = {}
+        for i in range(T):
+            d = owner[i]
+            for j in range(T):
+                parts = []
+                for k in range(T):
+                    parts.append(g.gemm(f"P{l}[{i},{j},{k}]", cur[(i, k)], Wt[(d, j, k)], tile, tile, tile,
+                                        in_dtype=dtype, out_dtype="f32", out_shape=(tile, tile), device=d))
+                nxt[(i, j)] = g.kernel(f"Y{l}[{i},{j}]", {"type": "sum", "args": parts, "count": tile * tile,
+                                                          "in_dtype": "f32", "out_dtype": dtype},
+                                       (tile, tile), dtype, d)
+        if l + 1 < chain and devices > 1:
+            # Row panels stay with their owner; nothing moves for X·W. To
+            # exercise NVLink moves, rotate panel ownership each link.
+            moved = {}
+            new_owner = {i: (owner[i] + 1) % devices for i in range(T)}
+            for (i, j), vid in nxt.items():
+                moved[(i, j)] = g.transfer(vid, new_owner[i])
+            owner = new_owner
+            nxt = moved
+        cur = nxt
+    return g
+
+
+# ------------------------------------------------------------- memgraph ---
+def plan(g: GraphBuilder, capacity, *, alloc_horizon="greedy", victim_policy="farthest-next-use",
+         order_policy="as-listed", seed=0, keep_superfluous=True):
+    """Builds the memgraph with this package's bit-exact planner."""
+    from . import memplan
+
+    caps = capacity if isinstance(capacity, (list, tuple)) else [int(capacity)] * g.device_count
+    return memplan.build_memgraph(g.to_json(), list(caps), mode="byte", order_policy=order_policy,
+                                  victim_policy=victim_policy, seed=seed, alloc_horizon=alloc_horizon,
+                                  keep_superfluous=keep_superfluous)
+
+
+def working_set_floor(g: GraphBuilder) -> list[int]:
+    """Per-device lower bound for a plan: permanent outputs plus the largest
+    single working set (a vertex's output + same-device inputs), like
+    tests/test_helpers.hpp:55-74 in byte mode (without its 1.5x slack)."""
+    cons = {}
+    prods = {v["id"]: [] for v in g.vertices}
+    for p, c in g.edges:
+        cons[p] = cons.get(p, 0) + 1
+        prods[c].append(p)
+    size = {v["id"]: v["output_size"] for v in g.vertices}
+    dev = {v["id"]: v["device"] for v in g.vertices}
+    outs = [0] * g.device_count
+    ws = [0] * g.device_count
+    for v in g.vertices:
+        if cons.get(v["id"], 0) == 0:
+            outs[v["device"]] += v["output_size"]
+        w = v["output_size"] + sum(size[p] for p in prods[v["id"]] if dev[p] == v["device"])
+        ws[v["device"]] = max(ws[v["device"]], w)
+    return [o + w for o, w in zip(outs, ws)]

@@ -1,0 +1,87 @@
+"""Shared fixtures: small op-payload graphs, their inputs and comparisons."""
+import json
+
+import numpy as np
+
+from oracle import ops_ref
+from oracle.cpu_executor import CpuExecutor, linear_extension
+from paper_2405_16283_b200 import workloads as W
+
+SMALL = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=1024, vocab=1000)
+
+
+def small_llama(seq=256, layers=2, cap_factor=1.5, hz="lazy"):
+    g = W.llama_prefill(SMALL, seq, layers=layers)
+    cap = int(W.working_set_floor(g)[0] * cap_factor) // 1024 * 1024
+    mg, stats = W.plan(g, cap, alloc_horizon=hz)
+    return g, mg, stats
+
+
+def inputs_of(g, seed=0):
+    return {t.id: W.make_input(t, seed) for t in g.inputs()}
+
+
+def as_f32(raw: bytes, dtype: str, n: int) -> np.ndarray:
+    b = np.frombuffer(raw, dtype=np.uint8)
+    return ops_ref.load(b, dtype, n).astype(np.float32)
+
+
+def out_values(g, vid, raw):
+    t = g.tensors[vid]
+    return as_f32(raw, t.dtype, int(np.prod(t.shape)))
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def oracle_outputs(g, mg, inputs, schedule="total_order", seed=0):
+    ex = CpuExecutor(mg, g.to_json())
+    for vid, a in inputs.items():
+        ex.set_input(vid, a)
+    sched = linear_extension(json.loads(mg), schedule, seed)
+    return ex.run(sched, outputs=g.outputs())
+
+
+def direct_forward(g, inputs):
+    """Evaluates the taskgraph straight (no memgraph, no arena reuse)."""
+    bufs = {}
+    for v in g.vertices:
+        vid = v["id"]
+        out = np.zeros(v["output_size"], dtype=np.uint8)
+        if v["kind"] == "input":
+            b = np.frombuffer(inputs[vid].tobytes(), dtype=np.uint8)
+            out[: b.size] = b
+        elif v["kind"] == "transfer":
+            (src,) = [p for p, c in g.edges if c == vid]
+            out[:] = bufs[src][: out.size]
+        else:
+            op = v["op"]
+            ops_ref.OPS[op["type"]](op, [bufs[a] for a in op["args"]], out)
+        bufs[vid] = out
+    return {o: bufs[o].tobytes() for o in g.outputs()}
+
+
+def replay_capacity(mg_json, order):
+    """Restates verifier.cpp:198-288 check_capacity for an arbitrary order."""
+    m = json.loads(mg_json)
+    pos = {v: i for i, v in enumerate(order)}
+    readers = {}
+    for e in m["edges"]:
+        if e["kind"] == "data":
+            readers.setdefault(e["from"], []).append(e["to"])
+    iv = []
+    for k, p in m["placement"].items():
+        vid = int(k)
+        rs = readers.get(vid, [])
+        end = max(pos[r] for r in rs) if rs else None
+        iv.append((vid, p["device"], p["offset"], p["size"], pos[vid], end))
+    for i in range(len(iv)):
+        for j in range(i + 1, len(iv)):
+            a, b = iv[i], iv[j]
+            if a[1] != b[1] or not (a[2] < b[2] + b[3] and b[2] < a[2] + a[3]):
+                continue
+            disjoint = (a[5] is not None and a[5] < b[4]) or (b[5] is not None and b[5] < a[4])
+            assert disjoint, f"regions of {a[0]} and {b[0]} overlap while both live"
