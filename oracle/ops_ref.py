@@ -85,17 +85,18 @@ def scatter(buf, dtype, off, bs, ld, values, mask=None):
 
 # ------------------------------------------------------------------ ops ---
 def op_gemm(op, args, out):
-    """C[b] = alpha * A[b] @ B[b]^T (+ R[b]); causal 1 = only j <= i is
-    defined (upper triangle left untouched), causal 2 = only k <= i used."""
+    """C[b] = alpha * A[b] @ B[b]^T (+ R[b]).
+
+    causal 1: only C[b][i][j<=i] is defined (the upper triangle is left
+    untouched; a causal softmax never reads it). causal 2: A is lower
+    triangular (A[b][i][k>i] == 0, e.g. causal softmax probabilities), which
+    lets the kernel skip the all-zero K blocks; the product is the plain one."""
     M, N, K, B = op["M"], op["N"], op["K"], op.get("batch", 1)
     lda, ldb, ldc = op.get("lda") or K, op.get("ldb") or K, op.get("ldc") or N
     ind, outd = op.get("in_dtype", "bf16"), op.get("out_dtype", "bf16")
     A = strided(args[0], ind, op.get("a_off", 0), B, op.get("sa", 0), M, lda, K)
     Bm = strided(args[1], ind, op.get("b_off", 0), B, op.get("sb", 0), N, ldb, K)
     causal = op.get("causal", 0)
-    if causal == 2:
-        mask = (np.arange(K)[None, :] <= np.arange(M)[:, None]).astype(np.float32)
-        A = A * mask[None]
     C = np.matmul(A, np.transpose(Bm, (0, 2, 1))) * np.float32(op.get("alpha", 1.0))
     if len(args) == 3:
         C = C + strided(args[2], outd, op.get("r_off", 0), B, op.get("sc", 0), M, ldc, N)
@@ -114,18 +115,37 @@ def op_rmsnorm(op, args, out):
     store(out, "bf16", y)
 
 
+def _pool():
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=os.cpu_count() or 1)
+    return _POOL
+
+
+_POOL = None
+
+
 def op_softmax(op, args, out):
+    """Row softmax of scale*S over j <= i (causal) or all j; masked entries
+    are exact zeros. Heads run on a thread pool (numpy ufuncs drop the GIL)."""
     B, R, Cc, scale, causal = op.get("batch", 1), op["rows"], op["cols"], op.get("scale", 1.0), op.get("causal", 0)
-    S = load(args[0], "f32", B * R * Cc).reshape(B, R, Cc) * np.float32(scale)
-    if causal:
-        mask = np.arange(Cc)[None, :] <= np.arange(R)[:, None]
-        S = np.where(mask[None], S, -np.inf)
-    mx = np.max(S, axis=2, keepdims=True)
-    e = np.exp(S - mx)
-    if causal:
-        e = np.where(mask[None], e, 0.0)
-    P = e / np.sum(e, axis=2, keepdims=True, dtype=np.float32)
-    store(out, "bf16", P.astype(np.float32))
+    S = typed(args[0], "f32")[: B * R * Cc].reshape(B, R, Cc)
+    P = typed(out, "bf16")[: B * R * Cc].reshape(B, R, Cc)
+    keep = (np.arange(Cc)[None, :] <= np.arange(R)[:, None]) if causal else None
+
+    def one(b):
+        x = S[b] * np.float32(scale)
+        if keep is not None:
+            np.copyto(x, np.float32(-np.inf), where=~keep)
+        x -= x.max(axis=1, keepdims=True)
+        np.exp(x, out=x)
+        x /= x.sum(axis=1, keepdims=True, dtype=np.float32)
+        P[b] = f32_to_bf16(x)
+
+    list(_pool().map(one, range(B)))
 
 
 def op_rope(op, args, out):

@@ -9,8 +9,9 @@
 //   transfer -> a free stream on the destination device
 //   offload  -> a free stream + the device's host_out (D2H) channel
 //   reload   -> a free stream + the device's host_in (H2D) channel
-//   input    -> nothing (reference) | stream + host_in when the executor
-//               materialises inputs from pinned host memory (SURVEY hard part 3)
+//   input    -> nothing (reference) | a stream when the executor materialises
+//               inputs, plus host_in when they come from pinned host memory
+//               (SURVEY hard part 3)
 // The ready list is re-ordered before every dispatch by the tie-break
 // (simulator.cpp:200-219) and the sweep restarts after each dispatch.
 #pragma once
@@ -81,8 +82,10 @@ void finalize_trace(const MemGraph& m, const MemoryMap& map, ExecutionTrace& t);
 // `compute_tokens` (reference: 1) and `inputs_use_host_in`.
 class Resources {
   public:
-    Resources(int devices, int streams_per_device, int compute_tokens, bool inputs_use_host_in)
-        : streams_(streams_per_device), inputs_(inputs_use_host_in), devs_(devices) {
+    Resources(int devices, int streams_per_device, int compute_tokens, bool inputs_take_stream,
+              bool inputs_use_host_in = true)
+        : streams_(streams_per_device), inputs_(inputs_take_stream), inputs_host_(inputs_use_host_in),
+          devs_(devices) {
         for (auto& d : devs_) {
             d.free_mask.assign((streams_per_device + 63) / 64, 0);
             for (int i = 0; i < streams_per_device; ++i) d.free_mask[i / 64] |= 1ULL << (i % 64);
@@ -94,7 +97,7 @@ class Resources {
     bool free(const MemVertex& v) const {
         const Dev& d = devs_[v.device];
         switch (v.op) {
-            case MemOpKind::Input: return !inputs_ || (d.nfree > 0 && d.host_in);
+            case MemOpKind::Input: return !inputs_ || (d.nfree > 0 && (!inputs_host_ || d.host_in));
             case MemOpKind::Kernel: return d.nfree > 0 && d.compute > 0;
             case MemOpKind::Transfer: return d.nfree > 0;
             case MemOpKind::Offload: return d.nfree > 0 && d.host_out;
@@ -116,7 +119,7 @@ class Resources {
         d.nfree--;
         if (v.op == MemOpKind::Kernel) d.compute--;
         if (v.op == MemOpKind::Offload) d.host_out = false;
-        if (v.op == MemOpKind::Reload || v.op == MemOpKind::Input) d.host_in = false;
+        if (v.op == MemOpKind::Reload || (v.op == MemOpKind::Input && inputs_host_)) d.host_in = false;
         return s;
     }
     void release(const MemVertex& v, std::int32_t s) {
@@ -126,7 +129,7 @@ class Resources {
         d.nfree++;
         if (v.op == MemOpKind::Kernel) d.compute++;
         if (v.op == MemOpKind::Offload) d.host_out = true;
-        if (v.op == MemOpKind::Reload || v.op == MemOpKind::Input) d.host_in = true;
+        if (v.op == MemOpKind::Reload || (v.op == MemOpKind::Input && inputs_host_)) d.host_in = true;
     }
 
   private:
@@ -137,7 +140,7 @@ class Resources {
         bool host_out = true, host_in = true;
     };
     int streams_;
-    bool inputs_;
+    bool inputs_, inputs_host_;
     std::vector<Dev> devs_;
 };
 

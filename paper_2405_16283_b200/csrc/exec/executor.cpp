@@ -80,6 +80,7 @@ struct Executor::Impl {
 
     // --- host pool ---------------------------------------------------------------
     std::unordered_map<VertexId, HostBuf> inputs;  // taskgraph input id -> pinned bytes
+    std::unordered_map<VertexId, HostBuf> staged;  // input id -> HBM staging copy (device residency)
     std::unordered_map<VertexId, HostBuf> slots;   // evicted root id -> pinned slot
 
     // --- per-vertex launch programs ------------------------------------------------
@@ -388,6 +389,15 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream) {
     TN_CUDA(cudaEventRecord(ev_start[vidx], s));
     switch (in.op) {
         case MemOpKind::Input: {
+            if (cfg.inputs_on_device) {
+                auto it = staged.find(in.input_id);
+                if (it == staged.end() || !it->second.p)
+                    throw Error("input " + std::to_string(in.input_id) + " has no data (tn_exec_set_input)");
+                const std::size_t n = std::min(in.bytes, it->second.bytes);
+                TN_CUDA(cudaMemcpyAsync(in.dst, it->second.p, n, cudaMemcpyDeviceToDevice, s));
+                last.d2d_bytes += static_cast<std::int64_t>(n);
+                break;
+            }
             auto it = inputs.find(in.input_id);
             if (it == inputs.end() || !it->second.p)
                 throw Error("input " + std::to_string(in.input_id) + " has no data (tn_exec_set_input)");
@@ -516,7 +526,7 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
         TN_CUDA(cudaEventRecord(t0[d], streams[d][0]));
     }
     auto wall0 = std::chrono::steady_clock::now();
-    Resources res(D, cfg.streams_per_device, cfg.compute_tokens, cfg.materialize_inputs);
+    Resources res(D, cfg.streams_per_device, cfg.compute_tokens, cfg.materialize_inputs, !cfg.inputs_on_device);
     ReadyList ready(pol.tie_break, seed);
     CudaBackend be(*this);
     try {
@@ -607,6 +617,8 @@ Executor::Impl::~Impl() {
         if (p) cudaFree(p);
     for (auto& [id, b] : inputs)
         if (b.p) cudaFreeHost(b.p);
+    for (auto& [id, b] : staged)
+        if (b.p) cudaFree(b.p);
     for (auto& [id, b] : slots)
         if (b.p) cudaFreeHost(b.p);
 }
@@ -633,6 +645,18 @@ void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool 
     if (bytes > static_cast<std::size_t>(v->output_size))
         throw Error("input " + std::to_string(id) + ": " + std::to_string(bytes) + " bytes exceed output_size " +
                     std::to_string(v->output_size));
+    if (impl_->cfg.inputs_on_device) {
+        HostBuf& b = impl_->staged[id];
+        impl_->set_device(v->device);
+        if (!b.p || b.bytes != bytes) {
+            if (b.p) cudaFree(b.p);
+            b.p = nullptr;
+            TN_CUDA(cudaMalloc(&b.p, std::max<std::size_t>(bytes, 1)));
+            b.bytes = bytes;
+        }
+        TN_CUDA(cudaMemcpy(b.p, host, bytes, from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+        return;
+    }
     HostBuf& b = impl_->inputs[id];
     if (!b.p || b.bytes != bytes) {
         if (b.p) cudaFreeHost(b.p);
@@ -691,6 +715,9 @@ ExecConfig parse_exec_config(const std::string& text) {
         c.compute_tokens = j.value("compute_tokens", c.compute_tokens);
         c.materialize_inputs = j.value("materialize_inputs", c.materialize_inputs);
         c.timeout_s = j.value("timeout_s", c.timeout_s);
+        const std::string res = j.value("input_residency", std::string("host"));
+        if (res != "host" && res != "device") throw ParseError("input_residency must be host or device");
+        c.inputs_on_device = res == "device";
     } catch (const json::exception& e) {
         throw ParseError(std::string("invalid executor config: ") + e.what());
     }

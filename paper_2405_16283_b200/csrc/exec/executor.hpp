@@ -14,7 +14,10 @@ struct ExecConfig {
     std::vector<int> devices;        // memgraph device -> CUDA ordinal (default d % gpus)
     int streams_per_device = 5;      // simulator.hpp:23
     int compute_tokens = 1;          // concurrent kernels per device (reference: 1)
-    bool materialize_inputs = true;  // Input = H2D copy on the host_in channel
+    bool materialize_inputs = true;  // Input = a copy into its placement at dispatch
+    bool inputs_on_device = false;   // "input_residency": "device" -> D2D from an HBM
+                                     // staging copy (stream only); "host" -> H2D from the
+                                     // pinned pool (stream + host_in channel)
     int timeout_s = 600;             // completion watchdog
 };
 ExecConfig parse_exec_config(const std::string& text);

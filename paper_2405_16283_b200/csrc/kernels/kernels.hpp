@@ -19,7 +19,8 @@ inline int dtype_size(int dt) { return dt == BF16 ? 2 : 4; }
 // A, B K-major (row-major [M,K] and [N,K]); C, R row-major with ldc.
 // causal: 0 none; 1 "scores" (tiles strictly above the diagonal are
 // skipped — their values are never read by a causal softmax); 2 "probs"
-// (the K loop stops at the diagonal; P is zero beyond it).
+// (A must be lower triangular, A[b][m][k>m] == 0 as a causal softmax writes
+// it, so the K loop stops at the diagonal block).
 struct GemmArgs {
     const void* A = nullptr;
     const void* B = nullptr;

@@ -57,6 +57,11 @@ def test_gemm_parity(shape):
     g = gemm_graph(**shape)
     mg, _ = W.plan(g, 1 << 30)
     inp = inputs_of(g, seed=11)
+    if shape.get("causal") == 2:  # A must be lower triangular (causal probabilities)
+        a_id = g.inputs()[0].id
+        B, M, K = g.tensors[a_id].shape
+        tri = (np.arange(K)[None, :] <= np.arange(M)[:, None])[None]
+        inp[a_id] = np.where(np.broadcast_to(tri, (B, M, K)).reshape(-1), inp[a_id], 0).astype(inp[a_id].dtype)
     _, got = run_gpu(g, mg, inp)
     want = oracle_outputs(g, mg, inp)
     (o,) = g.outputs()
