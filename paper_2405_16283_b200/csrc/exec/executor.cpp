@@ -468,7 +468,7 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream) {
         }
     }
     TN_CUDA(cudaEventRecord(ev_end[vidx], s));
-    TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
+    if (!cfg.poll) TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
 }
 
 // -------------------------------------------------------------------- run ---
@@ -482,9 +482,11 @@ class CudaBackend {
         x_.dispatched.push_back(vidx);
         x_.stream_of[vidx] = stream;
         in_flight_++;
+        if (x_.cfg.poll) flying_.push_back(vidx);
     }
     bool idle() const { return in_flight_ == 0; }
     std::int32_t wait_next(double& now) {
+        if (x_.cfg.poll) return poll_next(now);
         std::unique_lock<std::mutex> lk(x_.mu);
         if (x_.completed.empty()) {
             if (!x_.cv.wait_for(lk, std::chrono::seconds(x_.cfg.timeout_s), [&] { return !x_.completed.empty(); }))
@@ -500,9 +502,33 @@ class CudaBackend {
     }
 
   private:
+    // Spins over the in-flight vertices' end events (oldest first) until one
+    // has completed; lower latency than a host-function round trip.
+    std::int32_t poll_next(double& now) {
+        const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(x_.cfg.timeout_s);
+        for (std::uint64_t spin = 0;; ++spin) {
+            for (size_t i = 0; i < flying_.size(); ++i) {
+                const std::int32_t v = flying_[i];
+                const int dev = x_.prog[v].dev;
+                if (x_.ordinal[dev] != x_.cur_dev) x_.set_device(dev);
+                cudaError_t e = cudaEventQuery(x_.ev_end[v]);
+                if (e == cudaErrorNotReady) continue;
+                if (e != cudaSuccess) throw CudaError(std::string("vertex failed on the device: ") + cudaGetErrorString(e));
+                flying_.erase(flying_.begin() + static_cast<std::ptrdiff_t>(i));
+                in_flight_--;
+                now = std::chrono::duration<double>(std::chrono::steady_clock::now() - start_).count();
+                return v;
+            }
+            if ((spin & 1023) == 1023 && std::chrono::steady_clock::now() > deadline)
+                throw CudaError("executor timed out waiting for a completion (" + std::to_string(in_flight_) +
+                                " vertices in flight)");
+        }
+    }
+
     Executor::Impl& x_;
     std::chrono::steady_clock::time_point start_;
     int in_flight_ = 0;
+    std::vector<std::int32_t> flying_;
 };
 
 }  // namespace
@@ -715,6 +741,9 @@ ExecConfig parse_exec_config(const std::string& text) {
         c.compute_tokens = j.value("compute_tokens", c.compute_tokens);
         c.materialize_inputs = j.value("materialize_inputs", c.materialize_inputs);
         c.timeout_s = j.value("timeout_s", c.timeout_s);
+        const std::string comp = j.value("completion", std::string("poll"));
+        if (comp != "poll" && comp != "callback") throw ParseError("completion must be poll or callback");
+        c.poll = comp == "poll";
         const std::string res = j.value("input_residency", std::string("host"));
         if (res != "host" && res != "device") throw ParseError("input_residency must be host or device");
         c.inputs_on_device = res == "device";

@@ -19,6 +19,8 @@ struct ExecConfig {
                                      // staging copy (stream only); "host" -> H2D from the
                                      // pinned pool (stream + host_in channel)
     int timeout_s = 600;             // completion watchdog
+    bool poll = true;                // "completion": "poll" (spin on cudaEventQuery) | "callback"
+                                     // (cudaLaunchHostFunc -> queue -> condition variable)
 };
 ExecConfig parse_exec_config(const std::string& text);
 
