@@ -1,0 +1,26 @@
+"""Summarises an ncu --metrics gpu__time_duration.sum launch list (CSV)."""
+import collections, csv, re, sys
+rows = list(csv.reader(open(sys.argv[1])))
+for i, r in enumerate(rows):
+    if r and r[0] == "ID":
+        hdr, start = r, i + 1
+        break
+ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+agg = collections.defaultdict(lambda: [0, 0.0])
+for r in rows[start:]:
+    if len(r) <= vi:
+        continue
+    name = r[ki]
+    if not name.startswith(("tn::", "void tn::")):
+        continue  # torch kernels of the input generator run before the step
+    name = re.sub(r"\(anonymous namespace\)::", "", name.replace("void ", ""))
+    name = re.sub(r"\(.*$", "", name)
+    v = float(r[vi].replace(",", ""))
+    v = {"ns": v / 1e3, "nsecond": v / 1e3, "ms": v * 1e3, "msecond": v * 1e3}.get(r[ui], v)  # -> microseconds
+    agg[name][0] += 1
+    agg[name][1] += v
+tot = sum(x[1] for x in agg.values())
+print(f"{'kernel':45s} {'launches':>8s} {'total ms':>9s} {'share':>6s} {'avg us':>9s}")
+for k, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"{k:45s} {n:8d} {us / 1e3:9.2f} {100 * us / tot:5.1f}% {us / n:9.1f}")
+print(f"{'total':45s} {sum(x[0] for x in agg.values()):8d} {tot / 1e3:9.2f}")
