@@ -216,7 +216,7 @@ def cpu_sample(cfg, seq, layers_full):
     from paper_2405_16283_b200 import workloads as W
 
     g = W.llama_prefill(cfg, seq, layers=1)
-    mg, _ = W.plan(g, 1 << 40)
+    mg, _ = W.plan(g, 16 << 30)  # the bench cap; numpy arenas are calloc-backed (lazy)
     ex = CpuExecutor(mg, g.to_json())
     for t in g.inputs():
         ex.set_input(t.id, W.make_input(t, 0))

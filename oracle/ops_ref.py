@@ -148,6 +148,30 @@ def op_softmax(op, args, out):
     list(_pool().map(one, range(B)))
 
 
+def op_attention(op, args, out):
+    """O[i, h*hd:(h+1)*hd] = softmax_j(scale * q_i . k_j, j <= i if causal) @ v,
+    fp32 throughout (the fused GPU kernel rounds P to bf16 for its MMA)."""
+    H, S, hd, scale, causal = op["heads"], op["seq"], op["hd"], op.get("scale", 1.0), op.get("causal", 1)
+    ldo = op.get("ldo") or H * hd
+    q = load(args[0], "bf16", H * S * hd).reshape(H, S, hd)
+    k = load(args[1], "bf16", H * S * hd).reshape(H, S, hd)
+    vt = load(args[2], "bf16", H * hd * S).reshape(H, hd, S)
+    keep = (np.arange(S)[None, :] <= np.arange(S)[:, None]) if causal else None
+    O = np.empty((S, H, hd), dtype=np.float32)
+
+    def one(h):
+        s = (q[h] @ k[h].T) * np.float32(scale)
+        if keep is not None:
+            np.copyto(s, np.float32(-np.inf), where=~keep)
+        s -= s.max(axis=1, keepdims=True)
+        np.exp(s, out=s)
+        s /= s.sum(axis=1, keepdims=True, dtype=np.float32)
+        O[:, h, :] = s @ vt[h].T
+
+    list(_pool().map(one, range(H)))
+    scatter(out, "bf16", 0, 0, ldo, O.reshape(1, S, H * hd))
+
+
 def op_rope(op, args, out):
     S, ld, co, H, hd = op["seq"], op["ld"], op.get("col_off", 0), op["heads"], op["hd"]
     half = hd // 2
@@ -202,6 +226,7 @@ OPS = {
     "sum": op_sum,
     "embedding": op_embedding,
     "cast": op_cast,
+    "attention": op_attention,
 }
 
 

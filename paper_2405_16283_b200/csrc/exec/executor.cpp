@@ -96,6 +96,7 @@ struct Executor::Impl {
         const OpDesc* op_desc = nullptr;
         std::vector<const char*> argp;  // resolved argument pointers
         std::unique_ptr<k::GemmPlan> gemm;
+        std::unique_ptr<k::AttnPlan> attn;
     };
     std::vector<Instr> prog;
 
@@ -378,6 +379,29 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             fits(op.count * es(op.in_dtype), arg_bytes[0], "x");
             fits(op.count * es(op.out_dtype), out_bytes, "out");
             break;
+        case OpType::Attention: {
+            need_args(3, 3);
+            if (op.hd <= 0 || op.hd > 256 || op.seq <= 0 || op.heads <= 0) throw Error("attention: bad shape");
+            const std::int64_t ldo = op.ldo ? op.ldo : op.heads * op.hd;
+            fits(op.heads * op.seq * op.hd * 2, arg_bytes[0], "q");
+            fits(op.heads * op.seq * op.hd * 2, arg_bytes[1], "k");
+            fits(op.heads * op.seq * op.hd * 2, arg_bytes[2], "vt");
+            fits(((op.seq - 1) * ldo + op.heads * op.hd) * 2, out_bytes, "out");
+            k::AttnArgs aa;
+            aa.q = in.argp[0];
+            aa.k = in.argp[1];
+            aa.vt = in.argp[2];
+            aa.out = in.dst;
+            aa.heads = static_cast<int>(op.heads);
+            aa.seq = static_cast<int>(op.seq);
+            aa.hd = static_cast<int>(op.hd);
+            aa.ldo = ldo;
+            aa.scale = static_cast<float>(op.scale);
+            aa.causal = op.causal;
+            in.attn = std::make_unique<k::AttnPlan>();
+            TN_CUDA(k::attention_prepare(aa, in.attn.get()));
+            break;
+        }
     }
 }
 
@@ -461,6 +485,10 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream) {
                     break;
                 case OpType::Cast:
                     TN_CUDA(k::cast(a[0], op.in_dtype, in.dst, op.out_dtype, op.count, s));
+                    break;
+                case OpType::Attention:
+                    TN_CUDA(k::attention_launch(*in.attn, s));
+                    last.flops += k::attention_flops(in.attn->args);
                     break;
             }
             last.kernel_launches++;

@@ -18,6 +18,7 @@ const char* to_string(OpType t) {
         case OpType::Sum: return "sum";
         case OpType::Embedding: return "embedding";
         case OpType::Cast: return "cast";
+        case OpType::Attention: return "attention";
     }
     return "?";
 }
@@ -41,6 +42,7 @@ OpType type_of(const std::string& s) {
     if (s == "sum") return OpType::Sum;
     if (s == "embedding") return OpType::Embedding;
     if (s == "cast") return OpType::Cast;
+    if (s == "attention") return OpType::Attention;
     throw ParseError("unknown op type '" + s + "'");
 }
 
@@ -86,6 +88,7 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
             d.count = I("count", 0);
             d.dim = I("dim", 0);
             d.vocab = I("vocab", 0);
+            d.ldo = I("ldo", 0);
             d.causal = static_cast<int>(I("causal", 0));
             d.in_dtype = dtype_of(o.value("in_dtype", std::string("bf16")));
             d.out_dtype = dtype_of(o.value("out_dtype", std::string("bf16")));

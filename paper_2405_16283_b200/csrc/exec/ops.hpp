@@ -15,6 +15,8 @@
 //   {"type": "sum", "args": [p0, p1, ...], "count", "in_dtype", "out_dtype"}
 //   {"type": "embedding", "args": [tokens, table], "seq", "dim", "vocab"}
 //   {"type": "cast", "args": [x], "count", "in_dtype", "out_dtype"}
+//   {"type": "attention", "args": [q, k, vt], "heads", "seq", "hd", "ldo", "scale",
+//    "causal"}   q,k [H,seq,hd], vt [H,hd,seq] -> out [seq, ldo] (head h at col h*hd)
 // `args` are taskgraph producer ids; every arg must be a taskgraph edge into
 // the vertex. Offsets/strides are in elements. Semantics are restated in fp32
 // by oracle/ops_ref.py (the CPU oracle).
@@ -29,7 +31,9 @@
 
 namespace tn {
 
-enum class OpType : std::uint8_t { Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast };
+enum class OpType : std::uint8_t {
+    Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast, Attention
+};
 
 struct OpDesc {
     OpType type = OpType::Gemm;
@@ -39,7 +43,7 @@ struct OpDesc {
     std::int64_t lda = 0, ldb = 0, ldc = 0, sa = 0, sb = 0, sc = 0;
     std::int64_t a_off = 0, b_off = 0, c_off = 0, r_off = 0;
     std::int64_t rows = 0, cols = 0, seq = 0, ld = 0, col_off = 0, heads = 0, hd = 0, count = 0, dim = 0,
-                 vocab = 0;
+                 vocab = 0, ldo = 0;
     int causal = 0;
     int in_dtype = 0, out_dtype = 0;  // k::DType
     double alpha = 1.0, eps = 1e-5, scale = 1.0;

@@ -45,10 +45,36 @@ struct alignas(64) GemmPlan {
     int grid = 0;
 };
 
+// 3-D tiled TMA descriptor (inner, rows, batch), 128-byte swizzle.
+bool encode_tma_3d(CUtensorMap* map, const void* base, int esize, std::int64_t inner, std::int64_t rows,
+                   std::int64_t ld, int batch, std::int64_t bstride, int box_inner, int box_rows);
+
 // Encodes TMA descriptors (needs a CUDA context on the target device).
 cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms);
 cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s);
 double gemm_flops(const GemmArgs& a);  // algorithmic FLOPs (causal-aware)
+
+// Fused causal attention: q, k [H, seq, hd] bf16, vt [H, hd, seq] bf16,
+// out [seq, ldo] bf16 with head h at columns h*hd. Online softmax in fp32,
+// P rounded to bf16 for the P·V MMA. Fast path: hd == 128, seq % 128 == 0.
+struct AttnArgs {
+    const void* q = nullptr;
+    const void* k = nullptr;
+    const void* vt = nullptr;
+    void* out = nullptr;
+    int heads = 0, seq = 0, hd = 0;
+    std::int64_t ldo = 0;
+    float scale = 1.0f;
+    int causal = 1;
+};
+struct alignas(64) AttnPlan {
+    CUtensorMap tq, tk, tv;
+    AttnArgs args;
+    int path = 0;  // 0 tcgen05 fused, 1 SIMT fallback
+};
+cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan);
+cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s);
+double attention_flops(const AttnArgs& a);
 
 // y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w        (bf16 in/out, fp32 math)
 cudaError_t rmsnorm(const void* x, const void* w, void* y, int rows, int cols, float eps, cudaStream_t s);

@@ -168,13 +168,16 @@ LLAMA_65B = LlamaConfig(dim=8192, layers=80, heads=64, ffn=22016)
 
 
 def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device: int = 0,
-                  std: float = 0.02) -> GraphBuilder:
+                  std: float = 0.02, fused_attention: bool = True) -> GraphBuilder:
     """One forward prefill over `seq` tokens (causal), single device.
 
-    Per layer: rmsnorm -> QKV gemm -> rope(q), rope(k), Vᵀ -> batched causal
-    QKᵀ (fp32 scores, upper tiles skipped) -> causal softmax (bf16 P) ->
-    batched P·V written straight into [seq, dim] -> O-proj gemm with fused
-    residual -> rmsnorm -> gate/up gemm -> silu·mul -> down gemm + residual.
+    Per layer: rmsnorm -> QKV gemm -> rope(q), rope(k), Vᵀ -> attention ->
+    O-proj gemm with fused residual -> rmsnorm -> gate/up gemm -> silu·mul ->
+    down gemm + residual. Attention is one fused blockwise vertex
+    (`fused_attention`, S/P stay on chip) or three vertices with the n²
+    intermediates materialised (batched causal QKᵀ in fp32 with the upper
+    tiles skipped -> causal softmax to bf16 P -> batched P·V into [seq, dim]),
+    which the planner may offload.
     Head: final rmsnorm -> last-token logits (fp32). Weights are graph inputs
     (cold in host RAM, materialised by H2D at dispatch).
     """
@@ -203,12 +206,18 @@ def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device:
                                     "heads": H, "hd": hd}, (H, S, hd), "bf16", dev)
         vt = g.kernel(p + "v_t", {"type": "transpose_heads", "args": [qkv], "seq": S, "ld": 3 * d, "col_off": 2 * d,
                                   "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
-        sc = g.gemm(p + "scores", q, k, S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S, out_dtype="f32",
-                    causal=1, out_shape=(H, S, S), device=dev)
-        pr = g.kernel(p + "probs", {"type": "softmax", "args": [sc], "batch": H, "rows": S, "cols": S,
-                                    "scale": 1.0 / math.sqrt(hd), "causal": 1}, (H, S, S), "bf16", dev)
-        o = g.gemm(p + "attn", pr, vt, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
-                   causal=2, out_shape=(S, d), device=dev)
+        if fused_attention:
+            op = {"type": "attention", "args": [q, k, vt], "heads": H, "seq": S, "hd": hd, "ldo": d,
+                  "scale": 1.0 / math.sqrt(hd), "causal": 1}
+            o = g.kernel(p + "attn", op, (S, d), "bf16", dev, cost=2.0 * S * S * hd * H / _PEAK_FLOPS)
+            g.flops += 2.0 * S * S * hd * H * (1 + 1 / S)
+        else:
+            sc = g.gemm(p + "scores", q, k, S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S, out_dtype="f32",
+                        causal=1, out_shape=(H, S, S), device=dev)
+            pr = g.kernel(p + "probs", {"type": "softmax", "args": [sc], "batch": H, "rows": S, "cols": S,
+                                        "scale": 1.0 / math.sqrt(hd), "causal": 1}, (H, S, S), "bf16", dev)
+            o = g.gemm(p + "attn", pr, vt, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                       causal=2, out_shape=(S, d), device=dev)
         x = g.gemm(p + "attn_out", o, wo, S, d, d, r=x, out_shape=(S, d), device=dev)
         h2 = g.kernel(p + "ffn_norm_out", {"type": "rmsnorm", "args": [x, wn2], "rows": S, "cols": d, "eps": cfg.eps},
                       (S, d), "bf16", dev)

@@ -116,6 +116,35 @@ def test_rowops_and_eltwise_parity():
         assert rel_err(x_, y_) <= (0 if exact else 1e-2), g.tensors[o].name
 
 
+@pytest.mark.parametrize("seq,hd,causal", [(256, 128, 1), (512, 128, 1), (256, 128, 0), (200, 64, 1)])
+def test_fused_attention_parity(seq, hd, causal):
+    H = 4
+    g = W.GraphBuilder()
+    q = g.input("q", (H, seq, hd), "bf16", init=("normal", 1.0))
+    k = g.input("k", (H, seq, hd), "bf16", init=("normal", 1.0))
+    vt = g.input("vt", (H, hd, seq), "bf16", init=("normal", 1.0))
+    o = g.kernel("o", {"type": "attention", "args": [q, k, vt], "heads": H, "seq": seq, "hd": hd, "ldo": H * hd,
+                       "scale": hd ** -0.5, "causal": causal}, (seq, H * hd), "bf16")
+    mg, _ = W.plan(g, 1 << 30)
+    inp = inputs_of(g, seed=13)
+    _, got = run_gpu(g, mg, inp)
+    want = oracle_outputs(g, mg, inp)
+    assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 1e-2
+
+
+def test_unfused_attention_pipeline_matches_fused():
+    """Materialised S/P (scores gemm -> softmax -> P·V gemm) vs the fused vertex."""
+    from helpers import SMALL
+    outs = []
+    for fused in (True, False):
+        g = W.llama_prefill(SMALL, 256, layers=2, fused_attention=fused)
+        mg, _ = W.plan(g, int(W.working_set_floor(g)[0] * 2))
+        _, got = run_gpu(g, mg, inputs_of(g, seed=8))
+        (o,) = g.outputs()
+        outs.append(out_values(g, o, got[o]))
+    assert rel_err(outs[0], outs[1]) < 3e-2
+
+
 def test_llama_small_parity_with_offloads():
     g, mg, stats = small_llama(seq=256, layers=2)
     assert stats["offloads"] > 0

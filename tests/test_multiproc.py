@@ -1,0 +1,53 @@
+"""The bench's multi-rank plumbing (barrier + max-over-ranks) on CPU with gloo,
+world_size 2 — the same code path torchrun drives with NCCL on GPUs."""
+import os
+import socket
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r"""
+import os, sys, json
+sys.path.insert(0, %r)
+import torch.distributed as dist
+import bench
+world, rank, local = bench.dist_setup()
+t = bench.max_over_ranks(0.5 + rank, world)
+bench.barrier(world)
+# each rank plans its own replica of a small memgraph: identical plans
+from paper_2405_16283_b200 import workloads as W
+g = W.llama_prefill(W.LlamaConfig(dim=256, layers=1, heads=2, ffn=512, vocab=300), 128)
+mg, st = W.plan(g, 64 << 20)
+import hashlib
+h = hashlib.sha256(mg.encode()).hexdigest()
+import torch
+obj = [None] * world
+dist.all_gather_object(obj, h)
+print(json.dumps({"rank": rank, "max": t, "same_plan": len(set(obj)) == 1}))
+dist.destroy_process_group()
+"""
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_rank_gloo():
+    port = free_port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, WORLD_SIZE="2", RANK=str(r), LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), CUDA_VISIBLE_DEVICES="")
+        procs.append(subprocess.Popen([sys.executable, "-c", WORKER % ROOT], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=240) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-2000:]
+    import json
+    res = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
+    assert all(r["max"] == 1.5 and r["same_plan"] for r in res)

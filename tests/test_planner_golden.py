@@ -150,9 +150,14 @@ def test_large_llama_plan_matches_reference(ref_memplan):
     ignores) plans identically; the reference takes seconds, we take less."""
     from paper_2405_16283_b200 import workloads as W
 
-    g = W.llama_prefill(W.LlamaConfig(dim=1024, layers=6, heads=8, ffn=2816, vocab=4000), 512).to_json()
+    g = W.llama_prefill(W.LlamaConfig(dim=1024, layers=6, heads=8, ffn=2816, vocab=4000), 512,
+                        fused_attention=False).to_json()
     for caps, hz, spills in (([54 << 20], "greedy", False), ([26 << 20], "lazy", True), ([35 << 20], "lazy", True)):
         a = ref_memplan.build_memgraph(g, caps, mode="byte", alloc_horizon=hz)
         b = memplan.build_memgraph(g, caps, mode="byte", alloc_horizon=hz)
         assert a == b
         assert (a[1]["offloads"] > 0) == spills
+    gf = W.llama_prefill(W.LlamaConfig(dim=1024, layers=6, heads=8, ffn=2816, vocab=4000), 512).to_json()
+    for caps, hz in (([20 << 20], "lazy"), ([40 << 20], "greedy")):
+        assert ref_memplan.build_memgraph(gf, caps, mode="byte", alloc_horizon=hz) == \
+            memplan.build_memgraph(gf, caps, mode="byte", alloc_horizon=hz)
