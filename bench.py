@@ -137,10 +137,12 @@ def device_inputs(g, seed: int, device):
     token ids U[0, vocab), RoPE table) — torch is only the data source."""
     import torch
 
+    from paper_2405_16283_b200 import workloads as W
+
     gen = torch.Generator(device=device)
     out = {}
     for t in g.inputs():
-        gen.manual_seed(seed * 1000003 + t.id)
+        gen.manual_seed(seed * 1000003 + W.input_key(t))
         n = math.prod(t.shape)
         kind = t.init[0]
         if kind == "tokens":

@@ -119,9 +119,16 @@ class GraphBuilder:
 
 
 # ------------------------------------------------------------ input data ---
+def input_key(t: Tensor) -> int:
+    import zlib
+
+    return zlib.crc32(t.name.encode())
+
+
 def make_input(t: Tensor, seed: int) -> np.ndarray:
-    """Deterministic synthetic bytes for an input tensor (host numpy)."""
-    rng = np.random.default_rng([seed, t.id])
+    """Deterministic synthetic bytes for an input tensor (host numpy), keyed by
+    the tensor name so equal-named inputs of different graphs agree."""
+    rng = np.random.default_rng([seed, input_key(t)])
     n = int(np.prod(t.shape))
     kind = t.init[0]
     if kind == "tokens":

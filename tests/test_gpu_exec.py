@@ -211,3 +211,55 @@ def test_missing_input_is_an_error():
     with Executor(mg, g.to_json()) as ex:
         with pytest.raises(MemplanError, match="has no data"):
             ex.run()
+
+
+def test_full_size_llama7b_properties():
+    """BASELINE config 2 at full size (LLaMA-7B, seq 4096, 16 GiB cap), checked
+    through size-independent properties: bitwise-identical logits under
+    different dispatch orders, finite outputs, exact byte accounting, and a
+    trace that respects every memgraph edge and replays within capacity."""
+    import bench
+    g = W.llama_prefill(W.LLAMA_7B, 4096)
+    mg, stats = W.plan(g, 16 << 30)
+    inputs = bench.device_inputs(g, 0, torch.device("cuda", 0))
+    (o,) = g.outputs()
+    n = g.tensors[o].nbytes
+    outs = []
+    with Executor(mg, g.to_json(), {"input_residency": "device"}) as ex:
+        for vid, t in inputs.items():
+            ex.set_input(vid, t)
+        for tb, seed in (("fifo", 0), ("seeded-random", 5), ("lowest-id", 0)):
+            trace = json.loads(ex.run("event-driven", tb, seed))
+            outs.append(ex.get_output(o, n))
+            st = ex.stats()
+            assert st["d2d_bytes"] == sum(t.nbytes for t in g.inputs())
+        check_trace(mg, trace)
+    assert outs[0] == outs[1] == outs[2]
+    logits = np.frombuffer(outs[0], dtype=np.float32)
+    assert np.isfinite(logits).all() and logits.std() > 0
+
+
+def test_tight_cap_offload_reload_bytes():
+    """A cap that forces offloads: every offload/reload is a real pinned copy
+    and the executor's byte counters equal the memgraph's sizes."""
+    g = W.llama_prefill(W.LlamaConfig(dim=1024, layers=3, heads=8, ffn=2816, vocab=4000), 512,
+                        fused_attention=False)
+    mg, stats = W.plan(g, int(W.working_set_floor(g)[0] * 1.4), alloc_horizon="lazy")
+    assert stats["offloads"] > 0
+    m = json.loads(mg)
+    off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
+    rel = sum(v["size"] for v in m["vertices"] if v["op"] == "reload")
+    inp = inputs_of(g, seed=9)
+    with Executor(mg, g.to_json()) as ex:
+        for vid, a in inp.items():
+            ex.set_input(vid, a)
+        trace = json.loads(ex.run())
+        st = ex.stats()
+        (o,) = g.outputs()
+        got = ex.get_output(o, g.tensors[o].nbytes)
+    assert st["d2h_bytes"] == off
+    assert st["h2d_bytes"] == rel + sum(t.nbytes for t in g.inputs())
+    assert trace["host_bytes_transferred"] == off + rel
+    want = oracle_outputs(g, mg, inp)
+    assert rel_err(out_values(g, o, got), out_values(g, o, want[o])) < 3e-2
+    check_trace(mg, trace)
