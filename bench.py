@@ -295,19 +295,19 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    traces = []
+    makespans = []
     with Clocks(local) as clk:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for _ in range(args.steps):
-            traces.append(exv.run())
+            exv.run(trace=False)  # per-vertex CUDA events are recorded; no host trace work in the loop
         e.record()
         torch.cuda.synchronize()
     barrier(world)
     t_value = max_over_ranks(s.elapsed_time(e) * 1e-3, world)
+    last = json.loads(exv.last_trace())  # the last timed step, from its own CUDA events
     st_v = exv.stats()
-    last = json.loads(traces[-1])
-    makespans = [json.loads(t)["makespan"] for t in traces]
+    makespans.append(last["makespan"])
     exv.close()
     del exv
 
@@ -325,14 +325,14 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s2.record()
-    e2e_traces = []
     for _ in range(args.steps):
-        e2e_traces.append(exe.run())
+        exe.run(trace=False)
         exe.get_output(logits, logits_bytes)
     e2.record()
     torch.cuda.synchronize()
     barrier(world)
     t_e2e = max_over_ranks(s2.elapsed_time(e2) * 1e-3, world)
+    exe.last_trace()  # fills the exposed-transfer stats of the last timed step
     st_e = exe.stats()
     exe.close()
 
@@ -371,7 +371,7 @@ def run_ours(args, world, rank, local):
             "value_frac_of_compute_roofline": round(step_compute / (t_value / args.steps), 4),
             "e2e_frac_of_step_roofline": round(max(step_compute, step_pcie) / e2e_step, 4)},
         "device_time_by_op_s": {k: round(v, 5) for k, v in sorted(by_type.items(), key=lambda kv: -kv[1])},
-        "value_run": {"makespans_s": [round(x, 5) for x in makespans], "exposed_transfer_s":
+        "value_run": {"last_step_makespan_s": [round(x, 5) for x in makespans], "exposed_transfer_s":
                       round(st_v["exposed_transfer_s"], 5), "d2d_input_bytes": st_v["d2d_bytes"]},
         "clocks": clk.summary(),
         "peaks": {k: pk.get(k) for k in ("bf16_tflops", "bf16_tflops_sustained", "hbm_gbs")},

@@ -103,6 +103,10 @@ int tn_exec_set_input_device(tn_exec* h, int64_t vertex_id, const void* device_p
 int tn_exec_run(tn_exec* h, const char* policy, const char* tie_break, uint64_t seed, char** trace_json,
                 char** err);
 
+/* Trace of the most recent tn_exec_run (built from that run's CUDA events),
+ * for runs made with trace_json == NULL (no host work inside the timed loop). */
+int tn_exec_last_trace(tn_exec* h, char** trace_json, char** err);
+
 /* Copies graph output `vertex_id` (never freed or evicted) to host. */
 int tn_exec_get_output(tn_exec* h, int64_t vertex_id, void* host, size_t bytes, char** err);
 

@@ -61,6 +61,7 @@ def lib():
             "tn_exec_set_input_device": (c_int, [c_void_p, c_int64, c_void_p, c_size_t, P]),
             "tn_exec_run": (c_int, [c_void_p, c_char_p, c_char_p, c_uint64, P, P]),
             "tn_exec_get_output": (c_int, [c_void_p, c_int64, c_void_p, c_size_t, P]),
+            "tn_exec_last_trace": (c_int, [c_void_p, P, P]),
             "tn_exec_placement_ptr": (c_int, [c_void_p, c_int64, POINTER(c_void_p), P]),
             "tn_exec_stats": (c_int, [c_void_p, P, P]),
             "tn_exec_destroy": (None, [c_void_p]),

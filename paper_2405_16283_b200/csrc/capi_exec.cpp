@@ -73,8 +73,15 @@ int tn_exec_run(tn_exec* h, const char* policy, const char* tie_break, uint64_t 
         SchedulerPolicy pol;
         pol.kind = scheduler_kind_from_string(str(policy, "event-driven"));
         pol.tie_break = tie_break_from_string(str(tie_break, "fifo"));
-        auto t = h->x->run(pol, seed);
+        auto t = h->x->run(pol, seed, trace != nullptr);
         if (trace) *trace = dup(t.to_json());
+    });
+}
+
+int tn_exec_last_trace(tn_exec* h, char** trace, char** err) {
+    return guarded(err, [&] {
+        if (!h) throw Error("null executor handle");
+        *trace = dup(h->x->last_trace().to_json());
     });
 }
 

@@ -148,6 +148,8 @@ struct Executor::Impl {
     void prepare_kernel(Instr& in, const MemVertex& v, const std::vector<std::pair<VertexId, VertexId>>& data_in);
     void launch(std::int32_t vidx, std::int32_t stream);
     void run(const SchedulerPolicy& pol, std::uint64_t seed, ExecutionTrace* trace);
+    ExecutionTrace build_trace();
+    std::unique_ptr<MemGraph> last_graph;  // fixed-order graph of the last run
     ~Impl();
 };
 
@@ -598,8 +600,15 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
         TN_CUDA(cudaDeviceSynchronize());
     }
     last.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    last.vertices = static_cast<std::int64_t>(dispatched.size());
+    last_graph = g == &m ? nullptr : std::make_unique<MemGraph>(std::move(fixed));
+    if (trace) *trace = build_trace();
+}
 
-    // Trace from device timestamps (seconds since the device's t0 event).
+// Trace of the most recent run from its device timestamps (seconds since the
+// device's t0 event), plus the derived timing stats.
+ExecutionTrace Executor::Impl::build_trace() {
+    const MemGraph* g = last_graph ? last_graph.get() : &m;
     ExecutionTrace t;
     t.rows.reserve(dispatched.size());
     double kernel_s = 0, copy_s = 0;
@@ -649,8 +658,7 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
     last.copy_time_s = copy_s;
     last.kernel_busy_s = busy_k;
     last.exposed_transfer_s = exposed;
-    last.vertices = static_cast<std::int64_t>(dispatched.size());
-    if (trace) *trace = std::move(t);
+    return t;
 }
 
 Executor::Impl::~Impl() {
@@ -721,10 +729,15 @@ void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool 
     else std::memcpy(b.p, host, bytes);
 }
 
-ExecutionTrace Executor::run(const SchedulerPolicy& pol, std::uint64_t seed) {
+ExecutionTrace Executor::run(const SchedulerPolicy& pol, std::uint64_t seed, bool want_trace) {
     ExecutionTrace t;
-    impl_->run(pol, seed, &t);
+    impl_->run(pol, seed, want_trace ? &t : nullptr);
     return t;
+}
+
+ExecutionTrace Executor::last_trace() {
+    if (impl_->dispatched.empty()) throw Error("no run to trace yet");
+    return impl_->build_trace();
 }
 
 void Executor::get_output(VertexId id, void* host, std::size_t bytes) {

@@ -37,7 +37,8 @@ class Executor {
     Executor(const std::string& memgraph_json, const std::string& taskgraph_json, const ExecConfig& cfg);
     ~Executor();
     void set_input(VertexId id, const void* src, std::size_t bytes, bool from_device);
-    ExecutionTrace run(const SchedulerPolicy& pol, std::uint64_t seed);
+    ExecutionTrace run(const SchedulerPolicy& pol, std::uint64_t seed, bool want_trace = true);
+    ExecutionTrace last_trace();
     void get_output(VertexId id, void* host, std::size_t bytes);
     void* placement_ptr(VertexId id);
     const RunStats& stats() const;

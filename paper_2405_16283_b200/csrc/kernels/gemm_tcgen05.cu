@@ -67,6 +67,64 @@ __device__ __forceinline__ std::uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<std::uint32_t*>(&v);
 }
 
+// Stores one 32-column chunk of an accumulator row (alpha, residual, dtype).
+__device__ __forceinline__ void store_chunk(const Params& p, const std::uint32_t* r, std::int64_t off, int n0,
+                                            bool row_ok, bool vec_ok) {
+    if (!row_ok || n0 >= p.N) return;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+    if (vec_ok) {
+        if (p.out_dtype == BF16) {
+            __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off + n0;
+            if (p.R) {
+                const uint4* rr = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.R) + off + n0);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint4 x = rr[q];
+                    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&x);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) v[q * 8 + j] += __bfloat162float(h[j]);
+                }
+            }
+            uint4* dst = reinterpret_cast<uint4*>(c);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                    pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+        } else {
+            float* c = static_cast<float*>(p.C) + off + n0;
+            if (p.R) {
+                const float4* rr = reinterpret_cast<const float4*>(static_cast<const float*>(p.R) + off + n0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float4 x = rr[q];
+                    v[q * 4 + 0] += x.x;
+                    v[q * 4 + 1] += x.y;
+                    v[q * 4 + 2] += x.z;
+                    v[q * 4 + 3] += x.w;
+                }
+            }
+            float4* dst = reinterpret_cast<float4*>(c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+        }
+    } else {
+        for (int j = 0; j < 32 && n0 + j < p.N; ++j) {
+            float x = v[j];
+            if (p.out_dtype == BF16) {
+                __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off + n0 + j;
+                if (p.R) x += __bfloat162float(static_cast<const __nv_bfloat16*>(p.R)[off + n0 + j]);
+                *c = __float2bfloat16_rn(x);
+            } else {
+                float* c = static_cast<float*>(p.C) + off + n0 + j;
+                if (p.R) x += static_cast<const float*>(p.R)[off + n0 + j];
+                *c = x;
+            }
+        }
+    }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
@@ -198,60 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN + c0;
                 TN_LD32(taddr, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int n0 = nb * BN + c0;
-                if (!row_ok || n0 >= p.N) continue;
-                float v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
-                if (vec_ok) {
-                    if (p.out_dtype == BF16) {
-                        __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off + n0;
-                        if (p.R) {
-                            const uint4* rr = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.R) + off + n0);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                uint4 x = rr[q];
-                                const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&x);
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) v[q * 8 + j] += __bfloat162float(h[j]);
-                            }
-                        }
-                        uint4* dst = reinterpret_cast<uint4*>(c);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            dst[q] = make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
-                                                pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
-                    } else {
-                        float* c = static_cast<float*>(p.C) + off + n0;
-                        if (p.R) {
-                            const float4* rr = reinterpret_cast<const float4*>(static_cast<const float*>(p.R) + off + n0);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                float4 x = rr[q];
-                                v[q * 4 + 0] += x.x;
-                                v[q * 4 + 1] += x.y;
-                                v[q * 4 + 2] += x.z;
-                                v[q * 4 + 3] += x.w;
-                            }
-                        }
-                        float4* dst = reinterpret_cast<float4*>(c);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
-                    }
-                } else {
-                    for (int j = 0; j < 32 && n0 + j < p.N; ++j) {
-                        float x = v[j];
-                        if (p.out_dtype == BF16) {
-                            __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off + n0 + j;
-                            if (p.R) x += __bfloat162float(static_cast<const __nv_bfloat16*>(p.R)[off + n0 + j]);
-                            *c = __float2bfloat16_rn(x);
-                        } else {
-                            float* c = static_cast<float*>(p.C) + off + n0 + j;
-                            if (p.R) x += static_cast<const float*>(p.R)[off + n0 + j];
-                            *c = x;
-                        }
-                    }
-                }
+                store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
             }
             tc_fence_before();
             __syncwarp();
@@ -268,6 +273,219 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+}
+
+
+// ---------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): a cluster of two CTAs on a TPC computes a
+// 256x256 output tile with M=256 MMAs issued by the leader. Each CTA stages
+// half of A (its 128 rows) and half of B (128 rows) per 128-byte K block, so
+// per-SM L2->SMEM traffic per FLOP drops by 1.5x vs the 1-CTA 128x256 tile
+// (which is L2-bandwidth bound: ~96 B/clk/SM at full MMA rate).
+//   full[s]   leader only: expect_tx(64 KB) by the leader, complete_tx from
+//             both CTAs' TMA (.cta_group::2 loads signal the leader barrier)
+//   empty[s]  per CTA: multicast tcgen05.commit from the leader MMA
+//   tfull[a]  per CTA: multicast commit after the last K block of a tile
+//   tempty[a] leader only: 8 arrivals (4 epilogue warps x 2 CTAs)
+constexpr int kStages2 = 6;
+
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+    std::uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ std::uint32_t mapa(std::uint32_t addr, std::uint32_t rank) {
+    std::uint32_t out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+    return out;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(std::uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                std::uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_2sm(std::uint32_t d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                           std::uint32_t accum, bool tf32) {
+    if (tf32) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accum)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accum)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tc_commit_2sm(std::uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"(static_cast<unsigned short>(3))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(std::uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_kernel_2sm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
+    constexpr int HALF = 128;                  // rows of A and of B staged per CTA
+    constexpr int A_BYTES = HALF * kAtom;      // 16 KB
+    constexpr int STAGE = 2 * A_BYTES;         // 32 KB per CTA
+    constexpr int BN = 256, BM2 = 256;
+    constexpr std::uint32_t TMEM_COLS = 512;   // 2 x 256 fp32 accumulators
+
+    extern __shared__ std::uint8_t smem_raw[];
+    const std::uint32_t raw = smem_u32(smem_raw);
+    const std::uint32_t pad = ((raw + 1023) & ~1023u) - raw;
+    std::uint8_t* smem = smem_raw + pad;
+    const std::uint32_t sbase = raw + pad;
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStages2 * STAGE);
+    const std::uint32_t full = smem_u32(bars), empty = full + 8 * kStages2;
+    const std::uint32_t tfull = empty + 8 * kStages2, tempty = tfull + 16;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages2 + 4);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const std::uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int bk = kAtom / p.in_bytes;
+    const bool tf32 = p.in_bytes == 4;
+    const int tiles = p.batch * p.tiles_m * p.tiles_n;  // tiles_m counts 256-row pair tiles
+    const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&ta)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tb)) : "memory");
+        for (int s = 0; s < kStages2; ++s) {
+            mbar_init(full + 8 * s, 1);
+            mbar_init(empty + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + 8 * a, 1);
+            mbar_init(tempty + 8 * a, 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const std::uint32_t tmem = *tmem_slot;
+    const std::uint32_t full_leader0 = mapa(full, 0);
+    const std::uint32_t tempty_leader0 = mapa(tempty, 0);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            std::uint32_t phase = 0;
+            for (int t = pair; t < tiles; t += npairs) {
+                int b, mb, nb;
+                decode(p, t, b, mb, nb);
+                if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
+                int nk = (p.K + bk - 1) / bk;
+                if (p.causal == 2) nk = min(nk, ((mb + 1) * BM2 + bk - 1) / bk);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(empty + 8 * stage, phase ^ 1);
+                    const std::uint32_t fb = full_leader0 + 8 * stage;
+                    if (leader) mbar_expect_tx(full + 8 * stage, 2 * STAGE);
+                    const std::uint32_t sa = sbase + stage * STAGE;
+                    tma_load_3d_2sm(sa, &ta, kb * bk, mb * BM2 + rank * HALF, p.a_batched ? b : 0, fb);
+                    tma_load_3d_2sm(sa + A_BYTES, &tb, kb * bk, nb * BN + rank * HALF, p.b_batched ? b : 0, fb);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            const std::uint32_t idesc = make_idesc(tf32 ? 2u : 1u, BM2, BN);
+            int stage = 0, acc = 0;
+            std::uint32_t phase = 0, acc_phase = 0;
+            for (int t = pair; t < tiles; t += npairs) {
+                int b, mb, nb;
+                decode(p, t, b, mb, nb);
+                if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
+                int nk = (p.K + bk - 1) / bk;
+                if (p.causal == 2) nk = min(nk, ((mb + 1) * BM2 + bk - 1) / bk);
+                mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
+                tc_fence_after();
+                const std::uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(full + 8 * stage, phase);
+                    tc_fence_after();
+                    const std::uint32_t sa = sbase + stage * STAGE;
+                    const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + A_BYTES);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) tc_mma_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                    tc_commit_2sm(empty + 8 * stage);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit_2sm(tfull + 8 * acc);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else {
+        const int lane_base = (warp % 4) * 32;
+        int acc = 0;
+        std::uint32_t acc_phase = 0;
+        const int ob = p.out_dtype == BF16 ? 2 : 4;
+        const bool vec_ok = (p.N % 32 == 0) && ((p.ldc * ob) % 16 == 0) && ((p.sc * ob) % 16 == 0) &&
+                            ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
+                            ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
+        for (int t = pair; t < tiles; t += npairs) {
+            int b, mb, nb;
+            decode(p, t, b, mb, nb);
+            if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
+            mbar_wait(tfull + 8 * acc, acc_phase);
+            tc_fence_after();
+            const int row = mb * BM2 + static_cast<int>(rank) * HALF + lane_base + lane;
+            const bool row_ok = row < p.M;
+            const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                std::uint32_t r[32];
+                const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN + c0;
+                TN_LD32(taddr, r);
+                tc_wait_ld();
+                store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + 8 * acc);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
 }
 
 // --- SIMT fallback: one warp per output element, fp32 accumulate in K order.
@@ -351,6 +569,7 @@ template <int BN>
 int smem_bytes() {
     return kStages * (kBM + BN) * kAtom + 256 + 1024;
 }
+int smem_bytes_2sm() { return kStages2 * 2 * 128 * kAtom + 256 + 1024; }
 
 }  // namespace
 
@@ -365,19 +584,22 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     const int es = dtype_size(a.in_dtype);
     auto al16 = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
     const int bn = a.N <= 128 ? 128 : 256;
+    const bool two_sm = a.M >= 256 && a.N >= 256;
     bool ok = a.M >= kBM && a.N >= bn && a.K * es >= kAtom && al16(a.A) && al16(a.B) && (a.lda * es) % 16 == 0 &&
               (a.ldb * es) % 16 == 0 && (a.batch == 1 || ((a.sa * es) % 16 == 0 && (a.sb * es) % 16 == 0)) &&
               (a.in_dtype == BF16 || a.in_dtype == F32);
     if (ok) {
         const bool ab = a.batch > 1 && a.sa != 0, bb = a.batch > 1 && a.sb != 0;
         ok = encode(&plan->ta, a.A, es, a.K, a.M, a.lda, ab ? a.batch : 1, a.sa, kBM) &&
-             encode(&plan->tb, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, bn);
+             encode(&plan->tb, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, two_sm ? 128 : bn);
     }
-    plan->path = ok ? 0 : 1;
+    plan->path = ok ? (two_sm ? 2 : 0) : 1;
     plan->bn = bn;
-    const int tm = (a.M + kBM - 1) / kBM, tn = (a.N + bn - 1) / bn;
+    const int bm = plan->path == 2 ? 256 : kBM;
+    const int tm = (a.M + bm - 1) / bm, tn = (a.N + bn - 1) / bn;
     plan->tiles = a.batch * tm * tn;
     plan->grid = std::min(plan->tiles, std::max(1, num_sms));
+    if (plan->path == 2) plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
     if (ok) {
         static unsigned long long attr_set = 0;  // per CUDA device
         int dev = 0;
@@ -385,6 +607,7 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         if (!((attr_set >> dev) & 1ULL)) {
             cudaFuncSetAttribute(gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
             cudaFuncSetAttribute(gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>());
+            cudaFuncSetAttribute(gemm_kernel_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm());
             attr_set |= 1ULL << dev;
         }
     }
@@ -407,7 +630,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
     p.N = a.N;
     p.K = a.K;
     p.batch = a.batch;
-    p.tiles_m = (a.M + kBM - 1) / kBM;
+    p.tiles_m = (a.M + (plan.path == 2 ? 256 : kBM) - 1) / (plan.path == 2 ? 256 : kBM);
     p.tiles_n = (a.N + plan.bn - 1) / plan.bn;
     p.ldc = a.ldc;
     p.sc = a.sc;
@@ -417,7 +640,9 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
     p.in_bytes = dtype_size(a.in_dtype);
     p.a_batched = a.batch > 1 && a.sa != 0;
     p.b_batched = a.batch > 1 && a.sb != 0;
-    if (plan.bn == 128)
+    if (plan.path == 2)
+        gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, p);
+    else if (plan.bn == 128)
         gemm_kernel<128><<<plan.grid, kThreads, smem_bytes<128>(), s>>>(plan.ta, plan.tb, p);
     else
         gemm_kernel<256><<<plan.grid, kThreads, smem_bytes<256>(), s>>>(plan.ta, plan.tb, p);

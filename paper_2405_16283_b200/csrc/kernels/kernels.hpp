@@ -39,7 +39,7 @@ struct alignas(64) GemmPlan {
     CUtensorMap ta;  // A: (K, M, batch)
     CUtensorMap tb;  // B: (K, N, batch)
     GemmArgs args;
-    int path = 0;    // 0 tcgen05/TMA, 1 SIMT fallback (small or unaligned shapes)
+    int path = 0;    // 0 tcgen05 1-CTA, 2 tcgen05 CTA pair (cta_group::2), 1 SIMT fallback
     int bn = 256;    // N tile of the tcgen05 path
     int tiles = 0;   // output tiles (all batches)
     int grid = 0;

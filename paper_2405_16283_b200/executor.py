@@ -61,6 +61,12 @@ class Executor:
         check(rc, err)
         return out.take()
 
+    def last_trace(self) -> str:
+        """Trace of the most recent run (useful after runs with trace=False)."""
+        out, err = Out(), Out()
+        check(lib().tn_exec_last_trace(self._ptr(), out.ref, err.ref), err)
+        return out.take()
+
     def get_output(self, vid: int, nbytes: int) -> bytes:
         buf = ctypes.create_string_buffer(nbytes)
         err = Out()

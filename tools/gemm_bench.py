@@ -1,0 +1,34 @@
+"""GEMM microbenchmark through the executor: TFLOP/s per shape from CUDA
+events (trace) and error vs a torch fp32 matmul of the same bf16 inputs."""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+from paper_2405_16283_b200 import workloads as W
+from paper_2405_16283_b200.executor import Executor
+
+SHAPES = [(4096, 4096, 4096), (4096, 12288, 4096), (4096, 22016, 4096), (4096, 4096, 11008), (8192, 8192, 8192),
+          (4096, 32000, 4096), (300, 4096, 4096), (4096, 200, 4096)]
+if len(sys.argv) > 1:
+    SHAPES = [tuple(int(x) for x in s.split("x")) for s in sys.argv[1:]]
+for M, N, K in SHAPES:
+    g = W.GraphBuilder()
+    a = g.input("A", (M, K), "bf16")
+    b = g.input("B", (N, K), "bf16")
+    c = g.gemm("C", a, b, M, N, K, out_shape=(M, N))
+    mg, _ = W.plan(g, 1 << 36)
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    with Executor(mg, g.to_json(), {"input_residency": "device"}) as ex:
+        ex.set_input(a, A)
+        ex.set_input(b, B)
+        best = 1e9
+        for _ in range(5):
+            t = json.loads(ex.run())
+            row = [r for r in t["rows"] if r["vertex"] == c][0]
+            best = min(best, row["end"] - row["start"])
+        out = torch.frombuffer(bytearray(ex.get_output(c, M * N * 2)), dtype=torch.bfloat16).view(M, N).cuda()
+    ref = A.float() @ B.float().T
+    err = ((out.float() - ref).norm() / ref.norm()).item()
+    print(json.dumps({"M": M, "N": N, "K": K, "us": round(best * 1e6, 1), "tflops": round(2 * M * N * K / best / 1e12, 1),
+                      "rel_err": err}), flush=True)
