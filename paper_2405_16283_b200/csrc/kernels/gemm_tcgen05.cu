@@ -48,12 +48,21 @@ __device__ __forceinline__ bool tile_skipped(const Params& p, int mb, int nb, in
     return p.causal == 1 && nb * bn > mb * kBM + kBM - 1;
 }
 
+// Grouped rasterisation: within a group of up to 16 M-tiles the M index runs
+// fastest, so the ~74-148 tiles in flight share a few B column panels and a
+// group's A rows stay L2-resident (B is streamed from DRAM about once instead
+// of once per M-tile row).
 __device__ __forceinline__ void decode(const Params& p, int t, int& b, int& mb, int& nb) {
-    int per = p.tiles_m * p.tiles_n;
+    constexpr int G = 16;
+    const int per = p.tiles_m * p.tiles_n;
     b = t / per;
-    int r = t - b * per;
-    mb = r / p.tiles_n;
-    nb = r - mb * p.tiles_n;
+    const int r = t - b * per;
+    const int group = r / (G * p.tiles_n);
+    const int m0 = group * G;
+    const int gsz = min(G, p.tiles_m - m0);
+    const int local = r - group * G * p.tiles_n;
+    mb = m0 + local % gsz;
+    nb = local / gsz;
 }
 
 __device__ __forceinline__ int kblocks(const Params& p, int mb, int bk) {
@@ -583,7 +592,7 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     plan->args = a;
     const int es = dtype_size(a.in_dtype);
     auto al16 = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
-    const int bn = a.N <= 128 ? 128 : 256;
+    const int bn = a.N >= 256 ? 256 : a.N >= 128 ? 128 : 64;
     const bool two_sm = a.M >= 256 && a.N >= 256;
     bool ok = a.M >= kBM && a.N >= bn && a.K * es >= kAtom && al16(a.A) && al16(a.B) && (a.lda * es) % 16 == 0 &&
               (a.ldb * es) % 16 == 0 && (a.batch == 1 || ((a.sa * es) % 16 == 0 && (a.sb * es) % 16 == 0)) &&
@@ -605,6 +614,7 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (!((attr_set >> dev) & 1ULL)) {
+            cudaFuncSetAttribute(gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>());
             cudaFuncSetAttribute(gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
             cudaFuncSetAttribute(gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>());
             cudaFuncSetAttribute(gemm_kernel_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm());
@@ -644,6 +654,8 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
         gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, p);
     else if (plan.bn == 128)
         gemm_kernel<128><<<plan.grid, kThreads, smem_bytes<128>(), s>>>(plan.ta, plan.tb, p);
+    else if (plan.bn == 64)
+        gemm_kernel<64><<<plan.grid, kThreads, smem_bytes<64>(), s>>>(plan.ta, plan.tb, p);
     else
         gemm_kernel<256><<<plan.grid, kThreads, smem_bytes<256>(), s>>>(plan.ta, plan.tb, p);
     return cudaGetLastError();

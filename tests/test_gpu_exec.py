@@ -51,6 +51,9 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=256, N=256, K=128, batch=3, out_dtype="f32", causal=1),
     dict(M=256, N=128, K=256, batch=2, causal=2),
     dict(M=512, N=1024, K=512, alpha=0.5),
+    dict(M=640, N=200, K=256),                       # 1-CTA BN=128, ragged N, scalar epilogue
+    dict(M=256, N=64, K=192, out_dtype="f32"),       # BN=64
+    dict(M=1000, N=520, K=320, residual=True),       # CTA-pair path with ragged M/N tiles
 ])
 def test_gemm_parity(shape):
     shape = dict(shape)
