@@ -172,6 +172,43 @@ def op_attention(op, args, out):
     scatter(out, "bf16", 0, 0, ldo, O.reshape(1, S, H * hd))
 
 
+def _valid_mask(rows, cols, causal):
+    return (np.arange(cols)[None, :] <= np.arange(rows)[:, None]) if causal else np.ones((rows, cols), bool)
+
+
+def op_rowstats(op, args, out):
+    """(m, l) per row of a bf16 score tile: m = max_j s_ij, l = sum_j exp(s_ij - m)
+    over valid j (j <= i on a causal diagonal tile)."""
+    R, Cc, causal = op["rows"], op["cols"], op.get("causal", 0)
+    S = load(args[0], "bf16", R * Cc).reshape(R, Cc)
+    keep = _valid_mask(R, Cc, causal)
+    x = np.where(keep, S, -np.inf)
+    m = x.max(axis=1)
+    l = np.exp(x - m[:, None]).sum(axis=1, dtype=np.float32)
+    store(out, "f32", np.stack([m, l], axis=1).astype(np.float32))
+
+
+def op_stats_combine(op, args, out):
+    """Folds per-tile (m, l) in argument order: m = max, l = sum l_k exp(m_k - m)."""
+    R = op["rows"]
+    acc = load(args[0], "f32", 2 * R).reshape(R, 2).copy()
+    for a in args[1:]:
+        x = load(a, "f32", 2 * R).reshape(R, 2)
+        m = np.maximum(acc[:, 0], x[:, 0])
+        acc[:, 1] = acc[:, 1] * np.exp(acc[:, 0] - m) + x[:, 1] * np.exp(x[:, 0] - m)
+        acc[:, 0] = m
+    store(out, "f32", acc)
+
+
+def op_softmax_apply(op, args, out):
+    """P = exp(S - m) / l (bf16), masked entries 0."""
+    R, Cc, causal = op["rows"], op["cols"], op.get("causal", 0)
+    S = load(args[0], "bf16", R * Cc).reshape(R, Cc)
+    st = load(args[1], "f32", 2 * R).reshape(R, 2)
+    P = np.exp(S - st[:, :1]) / st[:, 1:]
+    store(out, "bf16", np.where(_valid_mask(R, Cc, causal), P, 0.0).astype(np.float32))
+
+
 def op_rope(op, args, out):
     S, ld, co, H, hd = op["seq"], op["ld"], op.get("col_off", 0), op["heads"], op["hd"]
     half = hd // 2
@@ -227,6 +264,9 @@ OPS = {
     "embedding": op_embedding,
     "cast": op_cast,
     "attention": op_attention,
+    "rowstats": op_rowstats,
+    "stats_combine": op_stats_combine,
+    "softmax_apply": op_softmax_apply,
 }
 
 

@@ -381,6 +381,22 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             fits(op.count * es(op.in_dtype), arg_bytes[0], "x");
             fits(op.count * es(op.out_dtype), out_bytes, "out");
             break;
+        case OpType::RowStats:
+            need_args(1, 1);
+            fits(op.rows * op.cols * 2, arg_bytes[0], "S");
+            fits(op.rows * 8, out_bytes, "stats");
+            break;
+        case OpType::StatsCombine:
+            need_args(1, 64);
+            for (size_t i = 0; i < op.args.size(); ++i) fits(op.rows * 8, arg_bytes[i], "stats");
+            fits(op.rows * 8, out_bytes, "stats");
+            break;
+        case OpType::SoftmaxApply:
+            need_args(2, 2);
+            fits(op.rows * op.cols * 2, arg_bytes[0], "S");
+            fits(op.rows * 8, arg_bytes[1], "stats");
+            fits(op.rows * op.cols * 2, out_bytes, "P");
+            break;
         case OpType::Attention: {
             need_args(3, 3);
             if (op.hd <= 0 || op.hd > 256 || op.seq <= 0 || op.heads <= 0) throw Error("attention: bad shape");
@@ -487,6 +503,18 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream) {
                     break;
                 case OpType::Cast:
                     TN_CUDA(k::cast(a[0], op.in_dtype, in.dst, op.out_dtype, op.count, s));
+                    break;
+                case OpType::RowStats:
+                    TN_CUDA(k::rowstats(a[0], in.dst, static_cast<int>(op.rows), static_cast<int>(op.cols), op.causal, s));
+                    break;
+                case OpType::StatsCombine: {
+                    std::vector<const void*> ps(a.begin(), a.end());
+                    TN_CUDA(k::stats_combine(ps.data(), static_cast<int>(ps.size()), in.dst, static_cast<int>(op.rows), s));
+                    break;
+                }
+                case OpType::SoftmaxApply:
+                    TN_CUDA(k::softmax_apply(a[0], a[1], in.dst, static_cast<int>(op.rows), static_cast<int>(op.cols),
+                                             op.causal, s));
                     break;
                 case OpType::Attention:
                     TN_CUDA(k::attention_launch(*in.attn, s));

@@ -19,6 +19,9 @@ const char* to_string(OpType t) {
         case OpType::Embedding: return "embedding";
         case OpType::Cast: return "cast";
         case OpType::Attention: return "attention";
+        case OpType::RowStats: return "rowstats";
+        case OpType::StatsCombine: return "stats_combine";
+        case OpType::SoftmaxApply: return "softmax_apply";
     }
     return "?";
 }
@@ -43,6 +46,9 @@ OpType type_of(const std::string& s) {
     if (s == "embedding") return OpType::Embedding;
     if (s == "cast") return OpType::Cast;
     if (s == "attention") return OpType::Attention;
+    if (s == "rowstats") return OpType::RowStats;
+    if (s == "stats_combine") return OpType::StatsCombine;
+    if (s == "softmax_apply") return OpType::SoftmaxApply;
     throw ParseError("unknown op type '" + s + "'");
 }
 

@@ -17,6 +17,9 @@
 //   {"type": "cast", "args": [x], "count", "in_dtype", "out_dtype"}
 //   {"type": "attention", "args": [q, k, vt], "heads", "seq", "hd", "ldo", "scale",
 //    "causal"}   q,k [H,seq,hd], vt [H,hd,seq] -> out [seq, ldo] (head h at col h*hd)
+//   {"type": "rowstats", "args": [S], "rows", "cols", "causal"}      bf16 S -> f32 (m,l) rows
+//   {"type": "stats_combine", "args": [st0, st1, ...], "rows"}        fold (m,l) in arg order
+//   {"type": "softmax_apply", "args": [S, st], "rows", "cols", "causal"}  P = exp(S-m)/l, bf16
 // `args` are taskgraph producer ids; every arg must be a taskgraph edge into
 // the vertex. Offsets/strides are in elements. Semantics are restated in fp32
 // by oracle/ops_ref.py (the CPU oracle).
@@ -32,7 +35,8 @@
 namespace tn {
 
 enum class OpType : std::uint8_t {
-    Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast, Attention
+    Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast, Attention,
+    RowStats, StatsCombine, SoftmaxApply
 };
 
 struct OpDesc {

@@ -84,6 +84,12 @@ cudaError_t rmsnorm(const void* x, const void* w, void* y, int rows, int cols, f
 cudaError_t softmax(const void* S, void* P, int batch, int rows, int cols, float scale, int causal,
                     cudaStream_t s);
 
+// Two-pass blockwise softmax over bf16 score tiles (stats in natural-log
+// units, fp32 float2 (m, l) per row; `causal` = diagonal tile, j <= i valid).
+cudaError_t rowstats(const void* S, void* st, int rows, int cols, int causal, cudaStream_t s);
+cudaError_t stats_combine(const void* const* parts, int n, void* out, int rows, cudaStream_t s);
+cudaError_t softmax_apply(const void* S, const void* st, void* P, int rows, int cols, int causal, cudaStream_t s);
+
 // Rotate-half RoPE: src [seq, ld] bf16, head h at columns col_off + h*hd;
 // table fp32 [seq, hd/2, 2] = (cos, sin); out [H, seq, hd] bf16 (head-major).
 cudaError_t rope(const void* src, const void* table, void* out, int seq, std::int64_t ld, std::int64_t col_off,

@@ -175,6 +175,101 @@ __global__ void __launch_bounds__(kRowThreads) softmax_scalar(const float* __res
         P[r * cols + c] = __float2bfloat16_rn(c < valid ? exp2f(s[c] * scale_log2 - mx) * inv : 0.f);
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-pass blockwise softmax over materialised score tiles (config 5: the
+// n^2 intermediates live in memgraph vertices the planner may offload).
+// Statistics are (m, l) per row in natural-log units: m = max_j s_j,
+// l = sum_j exp(s_j - m). `causal` marks a diagonal tile: column j of row i
+// is valid iff j <= i.
+
+// st[r] = (m, l) of one bf16 score-tile row.
+__global__ void __launch_bounds__(kRowThreads) rowstats_kernel(const __nv_bfloat16* __restrict__ S,
+                                                               float2* __restrict__ st, int cols, int causal) {
+    __shared__ float red[kRowThreads / 32];
+    const std::int64_t r = blockIdx.x;
+    const int valid = causal ? min(cols, static_cast<int>(r) + 1) : cols;
+    const __nv_bfloat16* s = S + r * cols;
+    constexpr float L2E = 1.4426950408889634f;
+    float mx = -INFINITY;
+    const bool vec = (cols % 8 == 0) && ((reinterpret_cast<std::uintptr_t>(S) & 15) == 0);
+    if (vec) {
+        for (int c = threadIdx.x * 8; c < valid; c += kRowThreads * 8) {
+            float f[8];
+            unpack8(*reinterpret_cast<const uint4*>(s + c), f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c + j < valid) mx = fmaxf(mx, f[j]);
+        }
+    } else {
+        for (int c = threadIdx.x; c < valid; c += kRowThreads) mx = fmaxf(mx, __bfloat162float(s[c]));
+    }
+    mx = block_reduce<true>(mx, red);
+    float sum = 0.f;
+    if (vec) {
+        for (int c = threadIdx.x * 8; c < valid; c += kRowThreads * 8) {
+            float f[8];
+            unpack8(*reinterpret_cast<const uint4*>(s + c), f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c + j < valid) sum += exp2f((f[j] - mx) * L2E);
+        }
+    } else {
+        for (int c = threadIdx.x; c < valid; c += kRowThreads) sum += exp2f((__bfloat162float(s[c]) - mx) * L2E);
+    }
+    sum = block_reduce<false>(sum, red);
+    if (threadIdx.x == 0) st[r] = make_float2(mx, sum);
+}
+
+constexpr int kMaxParts = 64;
+struct Parts {
+    const float2* p[kMaxParts];
+    int n;
+};
+
+// (m, l) of the union of k column ranges, folded in argument order.
+__global__ void stats_combine_kernel(Parts a, float2* __restrict__ out, int rows) {
+    constexpr float L2E = 1.4426950408889634f;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        float2 acc = a.p[0][r];
+        for (int k = 1; k < a.n; ++k) {
+            const float2 x = a.p[k][r];
+            const float m = fmaxf(acc.x, x.x);
+            acc.y = acc.y * exp2f((acc.x - m) * L2E) + x.y * exp2f((x.x - m) * L2E);
+            acc.x = m;
+        }
+        out[r] = acc;
+    }
+}
+
+// P = exp(S - m) / l (bf16), masked (diagonal tile) entries exactly zero.
+__global__ void __launch_bounds__(kRowThreads) softmax_apply_kernel(const __nv_bfloat16* __restrict__ S,
+                                                                    const float2* __restrict__ st,
+                                                                    __nv_bfloat16* __restrict__ P, int cols,
+                                                                    int causal) {
+    const std::int64_t r = blockIdx.x;
+    const int valid = causal ? min(cols, static_cast<int>(r) + 1) : cols;
+    constexpr float L2E = 1.4426950408889634f;
+    const float2 ml = st[r];
+    const float inv = 1.0f / ml.y, moff = ml.x * L2E;
+    const __nv_bfloat16* s = S + r * cols;
+    __nv_bfloat16* p = P + r * cols;
+    const bool vec = (cols % 8 == 0) && ((reinterpret_cast<std::uintptr_t>(S) & 15) == 0) &&
+                     ((reinterpret_cast<std::uintptr_t>(P) & 15) == 0);
+    if (vec) {
+        for (int c = threadIdx.x * 8; c < cols; c += kRowThreads * 8) {
+            float f[8];
+            unpack8(*reinterpret_cast<const uint4*>(s + c), f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = (c + j < valid) ? exp2f(f[j] * L2E - moff) * inv : 0.f;
+            *reinterpret_cast<uint4*>(p + c) = pack8(f);
+        }
+    } else {
+        for (int c = threadIdx.x; c < cols; c += kRowThreads)
+            p[c] = __float2bfloat16_rn(c < valid ? exp2f(__bfloat162float(s[c]) * L2E - moff) * inv : 0.f);
+    }
+}
+
 bool al16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -207,6 +302,30 @@ cudaError_t softmax(const void* S, void* P, int batch, int rows, int cols, float
     } else {
         softmax_scalar<<<static_cast<unsigned>(n), kRowThreads, 0, s>>>(Sp, Pp, rows, cols, sl2, causal);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t rowstats(const void* S, void* st, int rows, int cols, int causal, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    rowstats_kernel<<<rows, kRowThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(S), static_cast<float2*>(st), cols,
+                                                 causal);
+    return cudaGetLastError();
+}
+
+cudaError_t stats_combine(const void* const* parts, int n, void* out, int rows, cudaStream_t s) {
+    if (n < 1 || n > kMaxParts) return cudaErrorInvalidValue;
+    Parts a{};
+    a.n = n;
+    for (int i = 0; i < n; ++i) a.p[i] = static_cast<const float2*>(parts[i]);
+    stats_combine_kernel<<<(rows + 255) / 256, 256, 0, s>>>(a, static_cast<float2*>(out), rows);
+    return cudaGetLastError();
+}
+
+cudaError_t softmax_apply(const void* S, const void* st, void* P, int rows, int cols, int causal, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    softmax_apply_kernel<<<rows, kRowThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(S),
+                                                      static_cast<const float2*>(st), static_cast<__nv_bfloat16*>(P),
+                                                      cols, causal);
     return cudaGetLastError();
 }
 

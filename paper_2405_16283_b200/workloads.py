@@ -248,6 +248,57 @@ def prefill_flops(cfg: LlamaConfig, seq: int, layers: int | None = None) -> floa
     return L * (lin + attn) + 2.0 * cfg.vocab * d
 
 
+# ------------------------------------------ long-context blockwise attention (cfg 5) ---
+def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: int = 4096,
+                        device: int = 0) -> GraphBuilder:
+    """Config 5: causal attention over `seq` tokens with the n^2 score tiles
+    materialised as vertices and kept live across a two-pass softmax, so a
+    capped plan must offload them to host RAM.
+
+    Pass 1, for every head h and query block i, key block j <= i:
+        S_hij = scale * Q_hi K_hjᵀ (bf16 tile)      st_hij = rowstats(S_hij)
+    then m/l per (h, i) = stats_combine(st_hi0..st_hii) in fixed j order.
+    Pass 2 (after ALL of pass 1, as listed):
+        P_hij = softmax_apply(S_hij, ml_hi); O_hi = P_hi0 V_h0 + ... (a chain of
+        gemms with fused fp32 residual, j ascending); out_hi = bf16(O_hi).
+    Q/K/Vᵀ blocks are graph inputs (cold in host RAM)."""
+    assert seq % tile == 0
+    nb = seq // tile
+    T = tile
+    g = GraphBuilder(device_count=1)
+    dev = device
+    scale = 1.0 / math.sqrt(hd)
+    q = {(h, i): g.input(f"q[{h},{i}]", (T, hd), "bf16", dev, init=("normal", 1.0)) for h in range(heads) for i in range(nb)}
+    k = {(h, j): g.input(f"k[{h},{j}]", (T, hd), "bf16", dev, init=("normal", 1.0)) for h in range(heads) for j in range(nb)}
+    vt = {(h, j): g.input(f"vt[{h},{j}]", (hd, T), "bf16", dev, init=("normal", 1.0)) for h in range(heads) for j in range(nb)}
+    S, ml = {}, {}
+    for h in range(heads):
+        for i in range(nb):
+            parts = []
+            for j in range(i + 1):
+                S[(h, i, j)] = g.gemm(f"S[{h},{i},{j}]", q[(h, i)], k[(h, j)], T, T, hd, alpha=scale,
+                                      out_shape=(T, T), device=dev)
+                parts.append(g.kernel(f"st[{h},{i},{j}]", {"type": "rowstats", "args": [S[(h, i, j)]], "rows": T,
+                                                            "cols": T, "causal": int(i == j)}, (T, 2), "f32", dev))
+            ml[(h, i)] = g.kernel(f"ml[{h},{i}]", {"type": "stats_combine", "args": parts, "rows": T}, (T, 2), "f32", dev)
+    for h in range(heads):
+        for i in range(nb):
+            acc = None
+            for j in range(i + 1):
+                P = g.kernel(f"P[{h},{i},{j}]", {"type": "softmax_apply", "args": [S[(h, i, j)], ml[(h, i)]], "rows": T,
+                                                 "cols": T, "causal": int(i == j)}, (T, T), "bf16", dev)
+                acc = g.gemm(f"O[{h},{i},{j}]", P, vt[(h, j)], T, hd, T, r=acc, out_dtype="f32", out_shape=(T, hd),
+                             device=dev)
+            g.kernel(f"out[{h},{i}]", {"type": "cast", "args": [acc], "count": T * hd, "in_dtype": "f32",
+                                       "out_dtype": "bf16"}, (T, hd), "bf16", dev)
+    return g
+
+
+def blockwise_attention_flops(seq, heads, hd, tile):
+    nb = seq // tile
+    return heads * (nb * (nb + 1) // 2) * 2 * (2.0 * tile * tile * hd)
+
+
 # ------------------------------------------------- tiled matmul chain (cfg 1) ---
 def matmul_chain(n: int = 4096, tile: int = 1024, chain: int = 4, devices: int = 2,
                  dtype: str = "f32") -> GraphBuilder:

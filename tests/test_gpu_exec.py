@@ -266,3 +266,27 @@ def test_tight_cap_offload_reload_bytes():
     want = oracle_outputs(g, mg, inp)
     assert rel_err(out_values(g, o, got), out_values(g, o, want[o])) < 3e-2
     check_trace(mg, trace)
+
+
+def test_blockwise_attention_offloaded_tiles_parity():
+    """Config 5 at small scale: score tiles offloaded/reloaded through pinned
+    host memory, GPU == oracle, bitwise stable across dispatch orders."""
+    g = W.blockwise_attention(seq=2048, heads=2, hd=128, tile=256)
+    mg, stats = W.plan(g, 3 << 20, alloc_horizon="lazy")
+    assert stats["offloads"] > 10
+    inp = inputs_of(g, seed=22)
+    outs = g.outputs()
+    want = oracle_outputs(g, mg, inp)
+    res = []
+    with Executor(mg, g.to_json()) as ex:
+        for vid, a in inp.items():
+            ex.set_input(vid, a)
+        for tb, seed in (("fifo", 0), ("seeded-random", 4)):
+            trace = json.loads(ex.run("event-driven", tb, seed))
+            res.append({o: ex.get_output(o, g.tensors[o].nbytes) for o in outs})
+            check_trace(mg, trace)
+        st = ex.stats()
+    assert res[0] == res[1]
+    for o in outs:
+        assert rel_err(out_values(g, o, res[0][o]), out_values(g, o, want[o])) < 2e-2
+    assert st["d2h_bytes"] > 0 and trace["host_bytes_transferred"] > 0
