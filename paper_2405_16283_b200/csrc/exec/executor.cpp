@@ -176,7 +176,16 @@ void Executor::Impl::build() {
         TN_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena[d]), std::max<std::int64_t>(map.capacities[d], 256)));
         streams[d].resize(cfg.streams_per_device);
         for (auto& s : streams[d]) TN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        TN_CUDA(cudaEventCreate(&t0[d]));
+        // One time origin per physical GPU: memgraph devices that share a GPU
+        // share t0, so cross-device edges compare on one clock.
+        int first = d;
+        for (int e = 0; e < d; ++e)
+            if (ordinal[e] == ordinal[d]) {
+                first = e;
+                break;
+            }
+        if (first == d) TN_CUDA(cudaEventCreate(&t0[d]));
+        else t0[d] = t0[first];
     }
     // Peer access for every pair of distinct GPUs a transfer connects.
     for (const auto& v : m.vertices) {
@@ -607,7 +616,9 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
     for (int d = 0; d < D; ++d) {
         set_device(d);
         TN_CUDA(cudaDeviceSynchronize());
-        TN_CUDA(cudaEventRecord(t0[d], streams[d][0]));
+        bool owner = true;
+        for (int e = 0; e < d; ++e) owner = owner && ordinal[e] != ordinal[d];
+        if (owner) TN_CUDA(cudaEventRecord(t0[d], streams[d][0]));
     }
     auto wall0 = std::chrono::steady_clock::now();
     Resources res(D, cfg.streams_per_device, cfg.compute_tokens, cfg.materialize_inputs, !cfg.inputs_on_device);
@@ -698,8 +709,11 @@ Executor::Impl::~Impl() {
         if (ev_start[i]) cudaEventDestroy(ev_start[i]);
         if (ev_end[i]) cudaEventDestroy(ev_end[i]);
     }
-    for (auto e : t0)
-        if (e) cudaEventDestroy(e);
+    for (int d = 0; d < static_cast<int>(t0.size()); ++d) {
+        bool owner = true;
+        for (int e = 0; e < d; ++e) owner = owner && t0[e] != t0[d];
+        if (t0[d] && owner) cudaEventDestroy(t0[d]);
+    }
     for (auto& ss : streams)
         for (auto s : ss)
             if (s) cudaStreamDestroy(s);

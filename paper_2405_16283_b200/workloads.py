@@ -250,7 +250,7 @@ def prefill_flops(cfg: LlamaConfig, seq: int, layers: int | None = None) -> floa
 
 # ------------------------------------------ long-context blockwise attention (cfg 5) ---
 def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: int = 4096,
-                        device: int = 0) -> GraphBuilder:
+                        device: int = 0, lag: int | None = None) -> GraphBuilder:
     """Config 5: causal attention over `seq` tokens with the n^2 score tiles
     materialised as vertices and kept live across a two-pass softmax, so a
     capped plan must offload them to host RAM.
@@ -261,7 +261,13 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
     Pass 2 (after ALL of pass 1, as listed):
         P_hij = softmax_apply(S_hij, ml_hi); O_hi = P_hi0 V_h0 + ... (a chain of
         gemms with fused fp32 residual, j ascending); out_hi = bf16(O_hi).
-    Q/K/Vᵀ blocks are graph inputs (cold in host RAM)."""
+    Q/K/Vᵀ blocks are graph inputs (cold in host RAM).
+
+    `lag` (default: all heads) is the listing distance between a head's pass 1
+    and its pass 2: pass 2 of head h is listed right after pass 1 of head
+    h + lag, so `lag` heads of score tiles are live at once — enough to force
+    offloads under a cap while letting the D2H of new tiles overlap the H2D of
+    old ones (duplex PCIe)."""
     assert seq % tile == 0
     nb = seq // tile
     T = tile
@@ -272,7 +278,9 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
     k = {(h, j): g.input(f"k[{h},{j}]", (T, hd), "bf16", dev, init=("normal", 1.0)) for h in range(heads) for j in range(nb)}
     vt = {(h, j): g.input(f"vt[{h},{j}]", (hd, T), "bf16", dev, init=("normal", 1.0)) for h in range(heads) for j in range(nb)}
     S, ml = {}, {}
-    for h in range(heads):
+    lag = heads if lag is None else max(0, min(lag, heads))
+
+    def pass1(h):
         for i in range(nb):
             parts = []
             for j in range(i + 1):
@@ -281,7 +289,8 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
                 parts.append(g.kernel(f"st[{h},{i},{j}]", {"type": "rowstats", "args": [S[(h, i, j)]], "rows": T,
                                                             "cols": T, "causal": int(i == j)}, (T, 2), "f32", dev))
             ml[(h, i)] = g.kernel(f"ml[{h},{i}]", {"type": "stats_combine", "args": parts, "rows": T}, (T, 2), "f32", dev)
-    for h in range(heads):
+
+    def pass2(h):
         for i in range(nb):
             acc = None
             for j in range(i + 1):
@@ -291,6 +300,12 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
                              device=dev)
             g.kernel(f"out[{h},{i}]", {"type": "cast", "args": [acc], "count": T * hd, "in_dtype": "f32",
                                        "out_dtype": "bf16"}, (T, hd), "bf16", dev)
+
+    for step in range(heads + lag):
+        if step < heads:
+            pass1(step)
+        if step - lag >= 0:
+            pass2(step - lag)
     return g
 
 

@@ -17,9 +17,10 @@ ap.add_argument("--tile", type=int, default=4096)
 ap.add_argument("--cap-gib", type=float, default=16)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--policy", default="event-driven")
+ap.add_argument("--lag", type=int, default=None)
 a = ap.parse_args()
 t0 = time.time()
-g = W.blockwise_attention(a.seq, a.heads, 128, a.tile)
+g = W.blockwise_attention(a.seq, a.heads, 128, a.tile, lag=a.lag)
 mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon="lazy")
 m = json.loads(mg)
 off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
@@ -44,7 +45,7 @@ stt = ex.stats()
 flops = W.blockwise_attention_flops(a.seq, a.heads, 128, a.tile)
 roof = max(stt["h2d_bytes"] / (pcie * 1e9), stt["d2h_bytes"] / (pcie * 1e9), flops / (pk["bf16_tflops_sustained"] * 1e12))
 best = min(times)
-print(json.dumps({"workload": f"blockwise_attention_seq{a.seq}_h{a.heads}_tile{a.tile}_cap{a.cap_gib}GiB",
+print(json.dumps({"workload": f"blockwise_attention_seq{a.seq}_h{a.heads}_tile{a.tile}_lag{a.lag}_cap{a.cap_gib}GiB",
                   "memgraph_vertices": len(m["vertices"]), "plan": st, "plan_s": round(plan_s, 2),
                   "setup_s": round(setup_s, 1), "offload_gb": round(off / 1e9, 2), "reload_gb": round(rel / 1e9, 2),
                   "input_gb": round(inb / 1e9, 2), "step_s": [round(x, 4) for x in times],
