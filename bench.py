@@ -132,33 +132,37 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # ------------------------------------------------------------------ inputs ---
-def device_inputs(g, seed: int, device):
-    """Synthetic inputs generated on the GPU (random-init weights ~N(0, 0.02),
-    token ids U[0, vocab), RoPE table) — torch is only the data source."""
+def device_inputs_one(t, seed: int, device):
     import torch
 
     from paper_2405_16283_b200 import workloads as W
 
     gen = torch.Generator(device=device)
+    gen.manual_seed(seed * 1000003 + W.input_key(t))
+    n = math.prod(t.shape)
+    kind = t.init[0]
+    if kind == "tokens":
+        x = torch.randint(0, t.init[1], (n,), generator=gen, device=device, dtype=torch.int32)
+    elif kind == "rope":
+        S, half = t.shape[0], t.shape[1]
+        inv = float(t.init[1]) ** (-torch.arange(half, device=device, dtype=torch.float64) * 2.0 / (2 * half))
+        ang = torch.arange(S, device=device, dtype=torch.float64)[:, None] * inv[None, :]
+        x = torch.stack([ang.cos(), ang.sin()], dim=-1).float().reshape(-1)
+    elif kind == "normal":
+        x = torch.randn(n, generator=gen, device=device, dtype=torch.float32).mul_(float(t.init[1]))
+        x = x.to(torch.bfloat16) if t.dtype == "bf16" else x
+    else:
+        x = torch.empty(n, device=device, dtype=torch.float32).uniform_(t.init[1], t.init[2], generator=gen)
+        x = x.to(torch.bfloat16) if t.dtype == "bf16" else x
+    return {t.id: x}
+
+
+def device_inputs(g, seed: int, device):
+    """Synthetic inputs generated on the GPU (random-init weights ~N(0, 0.02),
+    token ids U[0, vocab), RoPE table) — torch is only the data source."""
     out = {}
     for t in g.inputs():
-        gen.manual_seed(seed * 1000003 + W.input_key(t))
-        n = math.prod(t.shape)
-        kind = t.init[0]
-        if kind == "tokens":
-            x = torch.randint(0, t.init[1], (n,), generator=gen, device=device, dtype=torch.int32)
-        elif kind == "rope":
-            S, half = t.shape[0], t.shape[1]
-            inv = float(t.init[1]) ** (-torch.arange(half, device=device, dtype=torch.float64) * 2.0 / (2 * half))
-            ang = torch.arange(S, device=device, dtype=torch.float64)[:, None] * inv[None, :]
-            x = torch.stack([ang.cos(), ang.sin()], dim=-1).float().reshape(-1)
-        elif kind == "normal":
-            x = torch.randn(n, generator=gen, device=device, dtype=torch.float32).mul_(float(t.init[1]))
-            x = x.to(torch.bfloat16) if t.dtype == "bf16" else x
-        else:
-            x = torch.empty(n, device=device, dtype=torch.float32).uniform_(t.init[1], t.init[2], generator=gen)
-            x = x.to(torch.bfloat16) if t.dtype == "bf16" else x
-        out[t.id] = x
+        out.update(device_inputs_one(t, seed, device))
     return out
 
 

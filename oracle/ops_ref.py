@@ -234,11 +234,20 @@ def op_silu_mul(op, args, out):
 
 
 def op_sum(op, args, out):
+    """out = sum_i in_i[offs_i : offs_i + count], fp32, argument order."""
     n, ind, outd = op["count"], op.get("in_dtype", "bf16"), op.get("out_dtype", "bf16")
-    acc = load(args[0], ind, n).astype(np.float32).copy()
-    for a in args[1:]:
-        acc += load(a, ind, n)
+    offs = op.get("offs") or [0] * len(args)
+    acc = load(args[0], ind, n, offs[0]).astype(np.float32).copy()
+    for a, o in zip(args[1:], offs[1:]):
+        acc += load(a, ind, n, o)
     store(out, outd, acc)
+
+
+def op_concat(op, args, out):
+    """out = args[0] ++ args[1] ++ ... (count elements of out_dtype each)."""
+    nb = op["count"] * DT[op.get("out_dtype", "bf16")]
+    for i, a in enumerate(args):
+        out[i * nb:(i + 1) * nb] = a[:nb]
 
 
 def op_embedding(op, args, out):
@@ -267,6 +276,7 @@ OPS = {
     "rowstats": op_rowstats,
     "stats_combine": op_stats_combine,
     "softmax_apply": op_softmax_apply,
+    "concat": op_concat,
 }
 
 

@@ -376,8 +376,18 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             break;
         case OpType::Sum:
             need_args(1, 16);
-            for (size_t i = 0; i < op.args.size(); ++i) fits(op.count * es(op.in_dtype), arg_bytes[i], "part");
+            if (!op.offs.empty() && op.offs.size() != op.args.size()) throw Error("sum: offs must list one offset per arg");
+            for (size_t i = 0; i < op.args.size(); ++i) {
+                const std::int64_t off = op.offs.empty() ? 0 : op.offs[i];
+                fits((off + op.count) * es(op.in_dtype), arg_bytes[i], "part");
+                in.argp[i] += off * es(op.in_dtype);
+            }
             fits(op.count * es(op.out_dtype), out_bytes, "out");
+            break;
+        case OpType::Concat:
+            need_args(1, 64);
+            for (size_t i = 0; i < op.args.size(); ++i) fits(op.count * es(op.out_dtype), arg_bytes[i], "part");
+            fits(static_cast<std::int64_t>(op.args.size()) * op.count * es(op.out_dtype), out_bytes, "out");
             break;
         case OpType::Embedding:
             need_args(2, 2);
@@ -513,6 +523,12 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream) {
                 case OpType::Cast:
                     TN_CUDA(k::cast(a[0], op.in_dtype, in.dst, op.out_dtype, op.count, s));
                     break;
+                case OpType::Concat: {
+                    std::vector<const void*> ps(a.begin(), a.end());
+                    TN_CUDA(k::concat(ps.data(), static_cast<int>(ps.size()), op.count * k::dtype_size(op.out_dtype),
+                                      in.dst, s));
+                    break;
+                }
                 case OpType::RowStats:
                     TN_CUDA(k::rowstats(a[0], in.dst, static_cast<int>(op.rows), static_cast<int>(op.cols), op.causal, s));
                     break;

@@ -22,6 +22,7 @@ const char* to_string(OpType t) {
         case OpType::RowStats: return "rowstats";
         case OpType::StatsCombine: return "stats_combine";
         case OpType::SoftmaxApply: return "softmax_apply";
+        case OpType::Concat: return "concat";
     }
     return "?";
 }
@@ -49,6 +50,7 @@ OpType type_of(const std::string& s) {
     if (s == "rowstats") return OpType::RowStats;
     if (s == "stats_combine") return OpType::StatsCombine;
     if (s == "softmax_apply") return OpType::SoftmaxApply;
+    if (s == "concat") return OpType::Concat;
     throw ParseError("unknown op type '" + s + "'");
 }
 
@@ -95,6 +97,7 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
             d.dim = I("dim", 0);
             d.vocab = I("vocab", 0);
             d.ldo = I("ldo", 0);
+            d.offs = o.value("offs", std::vector<std::int64_t>{});
             d.causal = static_cast<int>(I("causal", 0));
             d.in_dtype = dtype_of(o.value("in_dtype", std::string("bf16")));
             d.out_dtype = dtype_of(o.value("out_dtype", std::string("bf16")));

@@ -12,7 +12,9 @@
 //   {"type": "rope", "args": [src, table], "seq", "ld", "col_off", "heads", "hd"}
 //   {"type": "transpose_heads", "args": [src], "seq", "ld", "col_off", "heads", "hd"}
 //   {"type": "silu_mul", "args": [gu], "rows", "cols"}
-//   {"type": "sum", "args": [p0, p1, ...], "count", "in_dtype", "out_dtype"}
+//   {"type": "sum", "args": [p0, p1, ...], "count", "in_dtype", "out_dtype",
+//    "offs": [element offset per arg] (optional)}
+//   {"type": "concat", "args": [t0, t1, ...], "count" (elements per part), "out_dtype"}
 //   {"type": "embedding", "args": [tokens, table], "seq", "dim", "vocab"}
 //   {"type": "cast", "args": [x], "count", "in_dtype", "out_dtype"}
 //   {"type": "attention", "args": [q, k, vt], "heads", "seq", "hd", "ldo", "scale",
@@ -36,7 +38,7 @@ namespace tn {
 
 enum class OpType : std::uint8_t {
     Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast, Attention,
-    RowStats, StatsCombine, SoftmaxApply
+    RowStats, StatsCombine, SoftmaxApply, Concat
 };
 
 struct OpDesc {
@@ -51,6 +53,7 @@ struct OpDesc {
     int causal = 0;
     int in_dtype = 0, out_dtype = 0;  // k::DType
     double alpha = 1.0, eps = 1e-5, scale = 1.0;
+    std::vector<std::int64_t> offs;  // sum: per-argument element offsets
 };
 
 // Parses the "op" payloads of a taskgraph JSON document (vertices without an

@@ -140,6 +140,30 @@ struct SumArgs {
     int n;
 };
 
+constexpr int kMaxParts = 64;
+struct CatArgs {
+    const void* in[kMaxParts];
+    int n;
+};
+
+// out = in[0] ++ in[1] ++ ... (equal-sized parts, bytes), 16-byte vectors.
+__global__ void concat_kernel(CatArgs a, uint4* __restrict__ out, std::int64_t part_vec) {
+    const std::int64_t total = part_vec * a.n;
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int p = static_cast<int>(i / part_vec);
+        out[i] = static_cast<const uint4*>(a.in[p])[i - p * part_vec];
+    }
+}
+__global__ void concat_bytes_kernel(CatArgs a, std::uint8_t* __restrict__ out, std::int64_t part_bytes) {
+    const std::int64_t total = part_bytes * a.n;
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const int p = static_cast<int>(i / part_bytes);
+        out[i] = static_cast<const std::uint8_t*>(a.in[p])[i - p * part_bytes];
+    }
+}
+
 __device__ __forceinline__ float ld_as_float(const void* p, std::int64_t i, int dt) {
     return dt == BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]) : static_cast<const float*>(p)[i];
 }
@@ -246,6 +270,22 @@ cudaError_t sum_n(const void* const* ins, int n, int in_dtype, void* out, int ou
         sum_f32_vec<<<grid_for(count / 4), kThreads, 0, s>>>(a, static_cast<float*>(out), count / 4);
     else
         sum_kernel<<<grid_for(count), kThreads, 0, s>>>(a, in_dtype, out, out_dtype, count);
+    return cudaGetLastError();
+}
+
+cudaError_t concat(const void* const* parts, int n, std::int64_t part_bytes, void* out, cudaStream_t s) {
+    if (n < 1 || n > kMaxParts) return cudaErrorInvalidValue;
+    CatArgs a{};
+    a.n = n;
+    bool aligned = al16(out) && part_bytes % 16 == 0;
+    for (int i = 0; i < n; ++i) {
+        a.in[i] = parts[i];
+        aligned = aligned && al16(parts[i]);
+    }
+    if (aligned)
+        concat_kernel<<<grid_for(part_bytes / 16 * n), kThreads, 0, s>>>(a, static_cast<uint4*>(out), part_bytes / 16);
+    else
+        concat_bytes_kernel<<<grid_for(part_bytes * n), kThreads, 0, s>>>(a, static_cast<std::uint8_t*>(out), part_bytes);
     return cudaGetLastError();
 }
 

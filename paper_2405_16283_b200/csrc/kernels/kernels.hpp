@@ -106,6 +106,9 @@ cudaError_t silu_mul(const void* gu, void* out, int rows, int cols, cudaStream_t
 cudaError_t sum_n(const void* const* ins, int n, int in_dtype, void* out, int out_dtype, std::int64_t count,
                   cudaStream_t s);
 
+// out = parts[0] ++ parts[1] ++ ... (n equal parts of part_bytes bytes).
+cudaError_t concat(const void* const* parts, int n, std::int64_t part_bytes, void* out, cudaStream_t s);
+
 // out[t][:] = table[tokens[t]][:]   (tokens int32, table bf16 [vocab, dim])
 cudaError_t embedding(const void* tokens, const void* table, void* out, int seq, int dim, int vocab,
                       cudaStream_t s);

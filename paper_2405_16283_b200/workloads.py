@@ -239,6 +239,99 @@ def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device:
     return g
 
 
+def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = None,
+                     std: float = 0.02) -> GraphBuilder:
+    """Config 3: tensor-parallel prefill over `tp` memgraph devices (Megatron
+    layout). QKV / gate-up are column-parallel (each device owns
+    heads / ffn columns), O / down are row-parallel and produce per-device
+    partial sums. The all-reduce is explicit memgraph vertices — no NCCL:
+      reduce-scatter: device r receives row block r of every other device's
+        partial (Transfer, NVLink peer copy) and adds them in fixed device
+        order plus its residual rows (`sum` with per-arg offsets);
+      all-gather: every device receives the other reduced row blocks
+        (Transfer) and concatenates them (`concat`) into its replica of x.
+    The residual stream x is replicated; weights are per-device inputs
+    (host-resident, sliced exactly like a TP checkpoint shard). The final norm
+    and last-token logits run on device 0."""
+    L = cfg.layers if layers is None else layers
+    d, H, hd, f, V, S = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, cfg.vocab, seq
+    assert H % tp == 0 and f % tp == 0 and S % tp == 0
+    Hl, fl, Sb = H // tp, f // tp, S // tp
+    dl = Hl * hd
+    g = GraphBuilder(device_count=tp)
+    x = {}
+    tab = {}
+    for r in range(tp):
+        tok = g.input(f"tokens@{r}", (S,), "i32", r, init=("tokens", V))
+        emb = g.input(f"tok_embeddings@{r}", (V, d), "bf16", r, init=("normal", std))
+        tab[r] = g.input(f"rope_table@{r}", (S, hd // 2, 2), "f32", r, init=("rope", cfg.theta))
+        x[r] = g.kernel(f"embed@{r}", {"type": "embedding", "args": [tok, emb], "seq": S, "dim": d, "vocab": V},
+                        (S, d), "bf16", r)
+
+    def allreduce(name, partial, resid, need=None):
+        """partial[r][b]: [Sb, d] row block b of device r's partial sum;
+        `need`: devices that receive the gathered result (default all)."""
+        red = {}
+        for b in range(tp):
+            args = [partial[r][b] if r == b else g.transfer(partial[r][b], b, f"{name}.rs[{r}->{b}]") for r in range(tp)]
+            args.append(resid[b])
+            red[b] = g.kernel(f"{name}.reduced[{b}]", {"type": "sum", "args": args, "count": Sb * d,
+                                                        "offs": [0] * tp + [b * Sb * d], "in_dtype": "bf16",
+                                                        "out_dtype": "bf16"}, (Sb, d), "bf16", b)
+        out = {}
+        for r in (range(tp) if need is None else need):
+            parts = [red[b] if b == r else g.transfer(red[b], r, f"{name}.ag[{b}->{r}]") for b in range(tp)]
+            out[r] = g.kernel(f"{name}.x@{r}", {"type": "concat", "args": parts, "count": Sb * d, "out_dtype": "bf16"},
+                              (S, d), "bf16", r)
+        return out
+
+    for l in range(L):
+        p = f"layers.{l}."
+        o = {}
+        for r in range(tp):
+            wn1 = g.input(p + f"attention_norm@{r}", (d,), "bf16", r, init=("normal", 1.0))
+            wqkv = g.input(p + f"wqkv@{r}", (3 * dl, d), "bf16", r, init=("normal", std))
+            h = g.kernel(p + f"attn_norm_out@{r}", {"type": "rmsnorm", "args": [x[r], wn1], "rows": S, "cols": d,
+                                                     "eps": cfg.eps}, (S, d), "bf16", r)
+            qkv = g.gemm(p + f"qkv@{r}", h, wqkv, S, 3 * dl, d, out_shape=(S, 3 * dl), device=r)
+            q = g.kernel(p + f"q_rope@{r}", {"type": "rope", "args": [qkv, tab[r]], "seq": S, "ld": 3 * dl, "col_off": 0,
+                                             "heads": Hl, "hd": hd}, (Hl, S, hd), "bf16", r)
+            k = g.kernel(p + f"k_rope@{r}", {"type": "rope", "args": [qkv, tab[r]], "seq": S, "ld": 3 * dl,
+                                             "col_off": dl, "heads": Hl, "hd": hd}, (Hl, S, hd), "bf16", r)
+            vt = g.kernel(p + f"v_t@{r}", {"type": "transpose_heads", "args": [qkv], "seq": S, "ld": 3 * dl,
+                                           "col_off": 2 * dl, "heads": Hl, "hd": hd}, (Hl, hd, S), "bf16", r)
+            o[r] = g.kernel(p + f"attn@{r}", {"type": "attention", "args": [q, k, vt], "heads": Hl, "seq": S, "hd": hd,
+                                              "ldo": dl, "scale": 1.0 / math.sqrt(hd), "causal": 1}, (S, dl), "bf16", r,
+                            cost=2.0 * S * S * hd * Hl / _PEAK_FLOPS)
+            g.flops += 2.0 * S * S * hd * Hl * (1 + 1 / S)
+        partial = {}
+        for r in range(tp):
+            wo = g.input(p + f"wo@{r}", (d, dl), "bf16", r, init=("normal", std))
+            partial[r] = {b: g.gemm(p + f"attn_out_partial@{r}[{b}]", o[r], wo, Sb, d, dl, a_off=b * Sb * dl,
+                                    out_shape=(Sb, d), device=r) for b in range(tp)}
+        x = allreduce(p + "attn_ar", partial, x)
+        a = {}
+        for r in range(tp):
+            wn2 = g.input(p + f"ffn_norm@{r}", (d,), "bf16", r, init=("normal", 1.0))
+            w13 = g.input(p + f"w13@{r}", (2 * fl, d), "bf16", r, init=("normal", std))
+            h2 = g.kernel(p + f"ffn_norm_out@{r}", {"type": "rmsnorm", "args": [x[r], wn2], "rows": S, "cols": d,
+                                                     "eps": cfg.eps}, (S, d), "bf16", r)
+            gu = g.gemm(p + f"gate_up@{r}", h2, w13, S, 2 * fl, d, out_shape=(S, 2 * fl), device=r)
+            a[r] = g.kernel(p + f"act@{r}", {"type": "silu_mul", "args": [gu], "rows": S, "cols": fl}, (S, fl), "bf16", r)
+        partial = {}
+        for r in range(tp):
+            w2 = g.input(p + f"w2@{r}", (d, fl), "bf16", r, init=("normal", std))
+            partial[r] = {b: g.gemm(p + f"ffn_out_partial@{r}[{b}]", a[r], w2, Sb, d, fl, a_off=b * Sb * fl,
+                                    out_shape=(Sb, d), device=r) for b in range(tp)}
+        x = allreduce(p + "ffn_ar", partial, x, need=[0] if l == L - 1 else None)
+    wn = g.input("norm", (d,), "bf16", 0, init=("normal", 1.0))
+    wout = g.input("output", (V, d), "bf16", 0, init=("normal", std))
+    hn = g.kernel("final_norm", {"type": "rmsnorm", "args": [x[0], wn], "rows": S, "cols": d, "eps": cfg.eps},
+                  (S, d), "bf16", 0)
+    g.gemm("logits", hn, wout, 1, V, d, a_off=(S - 1) * d, out_dtype="f32", out_shape=(1, V), device=0)
+    return g
+
+
 def prefill_flops(cfg: LlamaConfig, seq: int, layers: int | None = None) -> float:
     """Algorithmic FLOPs of llama_prefill (causal attention counted as half)."""
     L = cfg.layers if layers is None else layers

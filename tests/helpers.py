@@ -85,3 +85,29 @@ def replay_capacity(mg_json, order):
                 continue
             disjoint = (a[5] is not None and a[5] < b[4]) or (b[5] is not None and b[5] < a[4])
             assert disjoint, f"regions of {a[0]} and {b[0]} overlap while both live"
+
+
+def tp_inputs_from_full(g_tp, g_full, full_inputs, cfg, tp):
+    """Shards single-device LLaMA inputs into the TP graph's per-device inputs
+    (Megatron slicing: QKV / gate-up rows by head / ffn column, O / down by K)."""
+    by_name = {g_full.tensors[v].name: a for v, a in full_inputs.items()}
+    d, hd, f = cfg.dim, cfg.hd, cfg.ffn
+    Hl, fl = cfg.heads // tp, f // tp
+    dl = Hl * hd
+    out = {}
+    for t in g_tp.inputs():
+        base, _, dev = t.name.partition("@")
+        r = int(dev) if dev else 0
+        a = by_name[base]
+        if base.endswith("wqkv"):
+            w = a.reshape(3 * d, d)
+            a = np.concatenate([w[j * d + r * dl: j * d + (r + 1) * dl] for j in range(3)])
+        elif base.endswith("w13"):
+            w = a.reshape(2 * f, d)
+            a = np.concatenate([w[r * fl:(r + 1) * fl], w[f + r * fl: f + (r + 1) * fl]])
+        elif base.endswith(".wo"):
+            a = a.reshape(d, d)[:, r * dl:(r + 1) * dl]
+        elif base.endswith(".w2"):
+            a = a.reshape(d, f)[:, r * fl:(r + 1) * fl]
+        out[t.id] = np.ascontiguousarray(a).reshape(-1)
+    return out

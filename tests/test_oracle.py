@@ -76,3 +76,25 @@ def test_blockwise_two_pass_equals_direct_attention():
 
 def _id(g, name):
     return next(t.id for t in g.tensors.values() if t.name == name)
+
+
+def test_tensor_parallel_graph_equals_single_device():
+    """Config-3 structure: the TP memgraph (column/row-parallel GEMMs, explicit
+    reduce-scatter/all-gather as Transfer + fixed-order sum + concat) computes
+    the same logits as the single-device graph from the same (sharded) weights."""
+    from helpers import tp_inputs_from_full
+    cfg = W.LlamaConfig(dim=256, layers=2, heads=4, ffn=512, vocab=300)
+    g1 = W.llama_prefill(cfg, 128)
+    mg1, _ = W.plan(g1, 1 << 30)
+    full = inputs_of(g1, seed=31)
+    (o1,) = g1.outputs()
+    want = out_values(g1, o1, oracle_outputs(g1, mg1, full)[o1])
+    gt = W.llama_prefill_tp(cfg, 128, tp=4)
+    caps = [int(c * 1.5) for c in W.working_set_floor(gt)]
+    mgt, st = W.plan(gt, caps, alloc_horizon="lazy")
+    m = json.loads(mgt)
+    assert sum(v["op"] == "transfer" for v in m["vertices"]) == 2 * 2 * (4 * 3 + 4 * 3) - 3 * 3
+    tin = tp_inputs_from_full(gt, g1, full, cfg, 4)
+    (ot,) = gt.outputs()
+    got = out_values(gt, ot, oracle_outputs(gt, mgt, tin, "random", 2)[ot])
+    assert rel_err(got, want) < 2e-2
