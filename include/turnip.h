@@ -73,6 +73,18 @@ int tn_simulate(const char* memgraph_json, const char* profile_json, const char*
 int tn_compare_policies(const char* memgraph_json, const char* profile_json, int64_t trials,
                         uint64_t seed, char** summary_json, char** err);
 
+/* replaces bindings.cpp:87-93 verify(graph_json, memgraph_json,
+ * schedule_limit) -> report JSON (verifier.cpp:474-492 format, same witnesses;
+ * scalable pair/reachability algorithms so large plans can be certified). */
+int tn_verify(const char* graph_json, const char* memgraph_json, int64_t schedule_limit, char** report_json,
+              char** err);
+
+/* replaces verifier.hpp:47-48 check_capacity(m, map, order): replays an
+ * arbitrary order (e.g. an executor trace's completion order) against the
+ * placement lifetimes. out: {"passed": bool[, "witness": str]}. */
+int tn_check_capacity(const char* memgraph_json, const int64_t* order, size_t norder, char** result_json,
+                      char** err);
+
 /* replaces simulator.hpp:72-73 make_fixed_order(m): memgraph JSON in/out. */
 int tn_make_fixed_order(const char* memgraph_json, char** memgraph_out, char** err);
 

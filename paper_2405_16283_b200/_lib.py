@@ -54,6 +54,8 @@ def lib():
             "tn_simulate": (c_int, [c_char_p, c_char_p, c_char_p, c_char_p, c_uint64, c_char_p, P, P]),
             "tn_compare_policies": (c_int, [c_char_p, c_char_p, c_int64, c_uint64, P, P]),
             "tn_make_fixed_order": (c_int, [c_char_p, P, P]),
+            "tn_verify": (c_int, [c_char_p, c_char_p, c_int64, P, P]),
+            "tn_check_capacity": (c_int, [c_char_p, POINTER(c_int64), c_size_t, P, P]),
         }
         exec_sig = {
             "tn_exec_create": (c_int, [c_char_p, c_char_p, c_char_p, POINTER(c_void_p), P]),

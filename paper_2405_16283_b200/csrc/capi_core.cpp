@@ -10,6 +10,7 @@
 #include "../../include/turnip.h"
 #include "core/dispatch.hpp"
 #include "core/planner.hpp"
+#include "core/verify.hpp"
 
 using namespace tn;
 
@@ -123,6 +124,26 @@ int tn_compare_policies(const char* memgraph_json, const char* profile_json, int
         DeviceProfile p;
         if (profile_json && *profile_json) p = parse_profile(profile_json);
         *out = dup(compare_policies(m, map, p, trials, seed).to_json());
+    });
+}
+
+int tn_verify(const char* graph_json, const char* memgraph_json, int64_t schedule_limit, char** out, char** err) {
+    return guarded(err, [&] {
+        auto g = parse_taskgraph(str(graph_json));
+        auto [m, map] = parse_memgraph(str(memgraph_json));
+        *out = dup(verify_all(g, m, map, schedule_limit).to_json());
+    });
+}
+
+int tn_check_capacity(const char* memgraph_json, const int64_t* order, size_t norder, char** out, char** err) {
+    return guarded(err, [&] {
+        auto [m, map] = parse_memgraph(str(memgraph_json));
+        std::vector<VertexId> o(order, order + norder);
+        auto r = check_capacity(m, map, o);
+        nlohmann::ordered_json j;
+        j["passed"] = r.passed;
+        if (!r.passed) j["witness"] = r.witness;
+        *out = dup(j.dump());
     });
 }
 

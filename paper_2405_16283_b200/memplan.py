@@ -26,6 +26,8 @@ __all__ = [
     "taskgraph_to_dot",
     "topological_order",
     "validate_taskgraph",
+    "verify",
+    "check_capacity",
 ]
 
 
@@ -86,6 +88,17 @@ def build_memgraph(
         nout=2,
     )
     return mg, json.loads(stats)
+
+
+def verify(graph_json: str, memgraph_json: str, schedule_limit: int = 0) -> str:
+    """bindings.cpp:87-93: every verifier check; returns the report as JSON."""
+    return call("tn_verify", enc(graph_json), enc(memgraph_json), int(schedule_limit))
+
+
+def check_capacity(memgraph_json: str, order) -> dict:
+    """verifier.hpp:47-48 (C++-only in the reference): replays `order`."""
+    arr, n = i64_array(order)
+    return json.loads(call("tn_check_capacity", enc(memgraph_json), arr, n))
 
 
 def simulate(memgraph_json: str, profile_json: str = "", policy: str = "event-driven",

@@ -39,6 +39,15 @@ def main():
             continue
         entry["memgraph_sha256"] = h(mg)
         entry["stats"] = stats
+        entry["verify_sha256"] = h(ref.verify(g, mg, 0) + ref.verify(g, mg, 200))
+        m = json.loads(mg)
+        req = [i for i, e in enumerate(m["edges"]) if e["kind"] == "memory" and not e["superfluous"]][:2]
+        mut = []
+        for i in req:  # racing mutants (acceptance_main.cpp:236-259)
+            mm = dict(m)
+            mm["edges"] = m["edges"][:i] + m["edges"][i + 1:]
+            mut.append(h(ref.verify(g, json.dumps(mm), 50)))
+        entry["mutant_verify_sha256"] = mut
         if case.get("simulate"):
             sims = {}
             for pol, tb, prof in case["simulate"]:
@@ -53,6 +62,9 @@ def main():
                                          alloc_horizon="lazy")[0],
         "five_slots_trace_seed7": ref.simulate(ref.build_memgraph(g, [5, 5, 5])[0], seed=7),
     }
+    cyc = json.loads(worked["five_slots"])
+    cyc["edges"].append({"from": 14, "to": 0, "kind": "memory", "superfluous": False})
+    worked["cyclic_verify"] = ref.verify(g, json.dumps(cyc), 0)
     out = {"generator": "tests/golden/make_golden.py (reference: oracle/_ref/_memplan)", "cases": cases,
            "worked": worked}
     with open(os.path.join(HERE, "planner_corpus.json"), "w") as f:

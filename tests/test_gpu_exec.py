@@ -193,7 +193,9 @@ def check_trace(mg, trace):
         for (s0, e0), (s1, e1) in zip(spans, spans[1:]):
             assert e0 <= s1 + 1e-6
     order = [r["vertex"] for r in sorted(trace["rows"], key=lambda r: (r["end"], r["start"]))]
-    replay_capacity(mg, order)
+    from paper_2405_16283_b200 import memplan
+    res = memplan.check_capacity(mg, order)  # verifier.cpp:198-288 on the completion order
+    assert res["passed"], res
 
 
 def test_multi_device_graph_on_one_gpu_tf32():

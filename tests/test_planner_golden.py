@@ -42,6 +42,15 @@ def test_golden_corpus_bit_exact():
         for key, hsum in want.get("simulate_sha256", {}).items():
             pol, tb, prof = key.split("|", 2)
             assert sha(memplan.simulate(mg, prof, pol, tb, case["kw"]["seed"])) == hsum, (case, key)
+        assert sha(memplan.verify(g, mg, 0) + memplan.verify(g, mg, 200)) == want["verify_sha256"], case
+        m = json.loads(mg)
+        req = [i for i, e in enumerate(m["edges"]) if e["kind"] == "memory" and not e["superfluous"]][:2]
+        for i, hsum in zip(req, want["mutant_verify_sha256"]):
+            mm = dict(m)
+            mm["edges"] = m["edges"][:i] + m["edges"][i + 1:]
+            rep = memplan.verify(g, json.dumps(mm), 50)
+            assert sha(rep) == hsum, case
+            assert json.loads(rep)["all_passed"] is False  # every required memory edge matters
         if "compare_sha256" in want:
             assert sha(memplan.compare_policies(mg, "", 4, case["kw"]["seed"])) == want["compare_sha256"]
     assert n_err > 50  # the corpus deliberately includes wedged / too-small capacities
@@ -73,6 +82,12 @@ def test_worked_example_four_slots():
     assert off[0]["origin"]["ref"] == 0 and rel[0]["origin"]["ref"] == 0
     mem = {(e["from"], e["to"]) for e in m["edges"] if e["kind"] == "memory"}
     assert (off[0]["id"], 13) in mem and (13, rel[0]["id"]) in mem
+
+
+def test_verifier_cycle_witness():
+    cyc = json.loads(GOLD["worked"]["five_slots"])
+    cyc["edges"].append({"from": 14, "to": 0, "kind": "memory", "superfluous": False})
+    assert memplan.verify(memplan.gen_matmul(3), json.dumps(cyc), 0) == GOLD["worked"]["cyclic_verify"]
 
 
 def test_byte_mode_first_fit_offsets():
@@ -161,3 +176,17 @@ def test_large_llama_plan_matches_reference(ref_memplan):
     for caps, hz in (([20 << 20], "lazy"), ([40 << 20], "greedy")):
         assert ref_memplan.build_memgraph(gf, caps, mode="byte", alloc_horizon=hz) == \
             memplan.build_memgraph(gf, caps, mode="byte", alloc_horizon=hz)
+
+
+def test_verifier_certifies_large_plans():
+    """The scalable verifier certifies BASELINE-size plans the reference's
+    O(P^2 * BFS) checks cannot finish."""
+    import time
+    from paper_2405_16283_b200 import workloads as W
+    for g, cap, hz in ((W.llama_prefill(W.LLAMA_7B, 4096), 16 << 30, "greedy"),
+                       (W.blockwise_attention(65536, 32, 128, 8192, lag=8), 16 << 30, "lazy")):
+        mg, st = W.plan(g, cap, alloc_horizon=hz)
+        t0 = time.time()
+        rep = json.loads(memplan.verify(g.to_json(), mg, 0))
+        assert rep["all_passed"], rep
+        assert time.time() - t0 < 30
