@@ -246,6 +246,139 @@ void dispatch_loop(const MemGraph& m, Resources& res, ReadyList& ready, Backend&
     }
 }
 
+// Lookahead variant for hardware backends (executor config "lookahead": 1).
+// A kernel whose not-yet-completed predecessors are all kernels of its own
+// device that are already running or queued on that device's compute token
+// is dispatched immediately behind them (device-side event wait) instead of
+// after a host round trip; at most `lookahead` kernels wait per device. The
+// compute token still serialises kernels per device (reference semantics,
+// simulator.cpp:171,184), every other op dispatches exactly as in
+// dispatch_loop, and the GPU enforces every edge, so outputs are unchanged.
+// Backend additionally provides:
+//   void launch_after(std::int32_t vidx, std::int32_t stream, std::int32_t after, double now);
+template <class Backend>
+void dispatch_loop_lookahead(const MemGraph& m, Resources& res, ReadyList& ready, Backend& be, int lookahead) {
+    GraphIndex gi(m);
+    const size_t V = m.vertices.size();
+    const int D = m.device_count;
+    std::vector<std::int32_t> npc = gi.indeg, npd = gi.indeg;  // not completed / not dispatched preds
+    std::vector<std::int32_t> held(V, -1);
+    std::vector<char> queued_in_ready(V, 0), dispatched(V, 0);
+    std::vector<std::int32_t> holder(D, -1);          // kernel owning the compute token
+    std::vector<std::vector<std::int32_t>> waiting(D);  // kernels dispatched behind the holder
+    // preds by vertex (for the early-dispatch check)
+    std::vector<std::int32_t> pstart(V + 1, 0), preds;
+    for (size_t u = 0; u < V; ++u)
+        for (std::int32_t a = gi.succ_start[u]; a < gi.succ_start[u + 1]; ++a) pstart[gi.succ[a] + 1]++;
+    for (size_t i = 0; i < V; ++i) pstart[i + 1] += pstart[i];
+    preds.resize(gi.succ.size());
+    {
+        std::vector<std::int32_t> fill(pstart.begin(), pstart.end() - 1);
+        for (size_t u = 0; u < V; ++u)
+            for (std::int32_t a = gi.succ_start[u]; a < gi.succ_start[u + 1]; ++a)
+                preds[fill[gi.succ[a]]++] = static_cast<std::int32_t>(u);
+    }
+    std::vector<char> done(V, 0);
+    auto tail_of = [&](int d) { return waiting[d].empty() ? holder[d] : waiting[d].back(); };
+    auto can_chain = [&](std::int32_t v) {
+        const MemVertex& x = m.vertices[v];
+        if (x.op != MemOpKind::Kernel || holder[x.device] < 0) return false;
+        if (static_cast<int>(waiting[x.device].size()) >= lookahead) return false;
+        for (std::int32_t k = pstart[v]; k < pstart[v + 1]; ++k) {
+            const std::int32_t p = preds[k];
+            if (done[p]) continue;
+            const MemVertex& y = m.vertices[p];
+            if (!dispatched[p] || y.op != MemOpKind::Kernel || y.device != x.device) return false;
+        }
+        return true;
+    };
+    auto push = [&](std::int32_t w, double t) {
+        if (queued_in_ready[w]) return;
+        queued_in_ready[w] = 1;
+        ready.push(m.vertices[w].id, w, t);
+    };
+    for (size_t i = 0; i < V; ++i)
+        if (npc[i] == 0) push(static_cast<std::int32_t>(i), 0.0);
+    double now = 0.0;
+    size_t ndone = 0;
+    while (ndone < V) {
+        size_t i = 0;
+        bool restart = ready.sort();
+        while (i < ready.size()) {
+            auto& e = ready.entries()[i];
+            const std::int32_t v = e.vidx;
+            const MemVertex& x = m.vertices[v];
+            bool go = false, chain = false;
+            if (npc[v] == 0) {
+                if (x.op == MemOpKind::Kernel) go = holder[x.device] < 0 && res.free(x);
+                else go = res.free(x);
+            } else {
+                chain = can_chain(v) && res.free(x);
+                go = chain;
+            }
+            if (!go) {
+                ++i;
+                continue;
+            }
+            const std::int32_t s = res.acquire(x);
+            held[v] = s;
+            dispatched[v] = 1;
+            ready.erase(i);
+            if (x.op == MemOpKind::Kernel && !chain) {
+                holder[x.device] = v;
+                be.launch(v, s, now);
+            } else if (chain) {
+                const std::int32_t after = tail_of(x.device);
+                waiting[x.device].push_back(v);
+                be.launch_after(v, s, after, now);
+            } else {
+                be.launch(v, s, now);
+            }
+            for (std::int32_t a = gi.succ_start[v]; a < gi.succ_start[v + 1]; ++a) {
+                const std::int32_t w = gi.succ[a];
+                if (--npd[w] == 0 && npc[w] > 0 && m.vertices[w].op == MemOpKind::Kernel) push(w, now);
+            }
+            if (restart) {
+                ready.sort();
+                i = 0;
+            }
+        }
+        if (be.idle()) {
+            std::string msg = "simulation deadlock: " + std::to_string(ready.size()) +
+                              " vertices ready but blocked, none in flight; frontier:";
+            for (const auto& r : ready.entries()) msg += " " + std::to_string(r.vertex);
+            throw DeadlockError(msg);
+        }
+        const std::int32_t u = be.wait_next(now);
+        const MemVertex& y = m.vertices[u];
+        res.release(y, held[u]);
+        done[u] = 1;
+        ndone++;
+        if (y.op == MemOpKind::Kernel) {
+            auto& wq = waiting[y.device];
+            if (holder[y.device] == u) {
+                // hand the token down the chain (skipping kernels already seen done)
+                holder[y.device] = -1;
+                while (!wq.empty()) {
+                    const std::int32_t nx = wq.front();
+                    wq.erase(wq.begin());
+                    if (!done[nx]) {
+                        holder[y.device] = nx;
+                        break;
+                    }
+                }
+            } else {
+                auto it = std::find(wq.begin(), wq.end(), u);
+                if (it != wq.end()) wq.erase(it);
+            }
+        }
+        for (std::int32_t a = gi.succ_start[u]; a < gi.succ_start[u + 1]; ++a) {
+            const std::int32_t w = gi.succ[a];
+            if (--npc[w] == 0 && !dispatched[w]) push(w, now);
+        }
+    }
+}
+
 // --- virtual-time simulator (drop-in for the reference) ------------------------
 double sample_duration(const MemVertex& v, const DeviceProfile& p, std::uint64_t draw_seed);
 MemGraph make_fixed_order(const MemGraph& m);

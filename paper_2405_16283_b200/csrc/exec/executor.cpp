@@ -146,7 +146,7 @@ struct Executor::Impl {
 
     void build();
     void prepare_kernel(Instr& in, const MemVertex& v, const std::vector<std::pair<VertexId, VertexId>>& data_in);
-    void launch(std::int32_t vidx, std::int32_t stream);
+    void launch(std::int32_t vidx, std::int32_t stream, std::int32_t after = -1);
     void run(const SchedulerPolicy& pol, std::uint64_t seed, ExecutionTrace* trace);
     ExecutionTrace build_trace();
     std::unique_ptr<MemGraph> last_graph;  // fixed-order graph of the last run
@@ -443,10 +443,11 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
 }
 
 // ----------------------------------------------------------------- launch ---
-void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream) {
+void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t after) {
     Instr& in = prog[vidx];
     set_device(in.dev);
     cudaStream_t s = streams[in.dev][stream < 0 ? 0 : stream];  // inputs hold no stream when not materialised
+    if (after >= 0) TN_CUDA(cudaStreamWaitEvent(s, ev_end[after], 0));  // lookahead: run behind `after`
     TN_CUDA(cudaEventRecord(ev_start[vidx], s));
     switch (in.op) {
         case MemOpKind::Input: {
@@ -567,6 +568,13 @@ class CudaBackend {
         in_flight_++;
         if (x_.cfg.poll) flying_.push_back(vidx);
     }
+    void launch_after(std::int32_t vidx, std::int32_t stream, std::int32_t after, double) {
+        x_.launch(vidx, stream, after);
+        x_.dispatched.push_back(vidx);
+        x_.stream_of[vidx] = stream;
+        in_flight_++;
+        if (x_.cfg.poll) flying_.push_back(vidx);
+    }
     bool idle() const { return in_flight_ == 0; }
     std::int32_t wait_next(double& now) {
         if (x_.cfg.poll) return poll_next(now);
@@ -637,11 +645,14 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
         if (owner) TN_CUDA(cudaEventRecord(t0[d], streams[d][0]));
     }
     auto wall0 = std::chrono::steady_clock::now();
-    Resources res(D, cfg.streams_per_device, cfg.compute_tokens, cfg.materialize_inputs, !cfg.inputs_on_device);
+    const bool chain = cfg.lookahead > 0 && cfg.compute_tokens == 1;
+    Resources res(D, cfg.streams_per_device, chain ? (1 << 30) : cfg.compute_tokens, cfg.materialize_inputs,
+                  !cfg.inputs_on_device);
     ReadyList ready(pol.tie_break, seed);
     CudaBackend be(*this);
     try {
-        dispatch_loop(*g, res, ready, be);
+        if (chain) dispatch_loop_lookahead(*g, res, ready, be, cfg.lookahead);
+        else dispatch_loop(*g, res, ready, be);
     } catch (...) {
         for (int d = 0; d < D; ++d) {
             cudaSetDevice(ordinal[d]);
@@ -838,6 +849,7 @@ ExecConfig parse_exec_config(const std::string& text) {
         if (j.contains("devices")) c.devices = j["devices"].get<std::vector<int>>();
         c.streams_per_device = j.value("streams_per_device", c.streams_per_device);
         c.compute_tokens = j.value("compute_tokens", c.compute_tokens);
+        c.lookahead = j.value("lookahead", c.lookahead);
         c.materialize_inputs = j.value("materialize_inputs", c.materialize_inputs);
         c.timeout_s = j.value("timeout_s", c.timeout_s);
         const std::string comp = j.value("completion", std::string("poll"));

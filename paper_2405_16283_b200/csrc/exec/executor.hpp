@@ -14,6 +14,8 @@ struct ExecConfig {
     std::vector<int> devices;        // memgraph device -> CUDA ordinal (default d % gpus)
     int streams_per_device = 5;      // simulator.hpp:23
     int compute_tokens = 1;          // concurrent kernels per device (reference: 1)
+    int lookahead = 1;               // kernels queued behind the running one on the GPU
+                                     // (0 = reference dispatch: only after host-observed completion)
     bool materialize_inputs = true;  // Input = a copy into its placement at dispatch
     bool inputs_on_device = false;   // "input_residency": "device" -> D2D from an HBM
                                      // staging copy (stream only); "host" -> H2D from the
