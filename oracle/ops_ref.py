@@ -98,6 +98,28 @@ def op_gemm(op, args, out):
     Bm = strided(args[1], ind, op.get("b_off", 0), B, op.get("sb", 0), N, ldb, K)
     causal = op.get("causal", 0)
     C = np.matmul(A, np.transpose(Bm, (0, 2, 1))) * np.float32(op.get("alpha", 1.0))
+    if op.get("epilogue", "none") == "qkv_rope":
+        # packed [rope(q) (H,M,128) | rope(k) | vT (H,128,M)] from C = x W^T
+        H, Mm = op["heads"], op["M"]
+        tab = load(args[2], "f32", Mm * 64 * 2).reshape(Mm, 64, 2)
+        c, s_ = tab[:, None, :, 0], tab[:, None, :, 1]
+        X = C[0].reshape(Mm, 3, H, 128)
+
+        def rope(x):  # x [M, H, 128]
+            a, b = x[..., :64], x[..., 64:]
+            return np.concatenate([a * c - b * s_, b * c + a * s_], axis=-1).transpose(1, 0, 2)
+
+        packed = np.concatenate([rope(X[:, 0]).reshape(-1), rope(X[:, 1]).reshape(-1),
+                                 X[:, 2].transpose(1, 2, 0).reshape(-1)])
+        store(out, "bf16", packed)
+        return
+    if op.get("epilogue", "none") == "swiglu":
+        # out[:, 128b + j] = silu(C[:, 256b + j]) * C[:, 256b + 128 + j]
+        Bn, Mm, Nn = C.shape
+        blk = C.reshape(Bn, Mm, Nn // 256, 2, 128)
+        g, u = blk[:, :, :, 0, :], blk[:, :, :, 1, :]
+        C = (g / (1.0 + np.exp(-g)) * u).reshape(Bn, Mm, Nn // 2)
+        ldc = op.get("ldc") or Nn // 2
     if len(args) == 3:
         C = C + strided(args[2], outd, op.get("r_off", 0), B, op.get("sc", 0), M, ldc, N)
     mask = None
@@ -153,9 +175,11 @@ def op_attention(op, args, out):
     fp32 throughout (the fused GPU kernel rounds P to bf16 for its MMA)."""
     H, S, hd, scale, causal = op["heads"], op["seq"], op["hd"], op.get("scale", 1.0), op.get("causal", 1)
     ldo = op.get("ldo") or H * hd
-    q = load(args[0], "bf16", H * S * hd).reshape(H, S, hd)
-    k = load(args[1], "bf16", H * S * hd).reshape(H, S, hd)
-    vt = load(args[2], "bf16", H * hd * S).reshape(H, hd, S)
+    n = H * S * hd
+    aq, ak, av = (args[0], args[1], args[2]) if len(args) == 3 else (args[0], args[0], args[0])
+    q = load(aq, "bf16", n, op.get("q_off", 0)).reshape(H, S, hd)
+    k = load(ak, "bf16", n, op.get("k_off", 0)).reshape(H, S, hd)
+    vt = load(av, "bf16", n, op.get("v_off", 0)).reshape(H, hd, S)
     keep = (np.arange(S)[None, :] <= np.arange(S)[:, None]) if causal else None
     O = np.empty((S, H, hd), dtype=np.float32)
 

@@ -320,7 +320,13 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             g.batch = static_cast<int>(op.batch);
             g.lda = op.lda ? op.lda : op.K;
             g.ldb = op.ldb ? op.ldb : op.K;
-            g.ldc = op.ldc ? op.ldc : op.N;
+            const std::int64_t n_out = op.epilogue == 1 ? op.N / 2 : op.N;
+            g.ldc = op.ldc ? op.ldc : n_out;
+            g.epi = op.epilogue;
+            if (op.epilogue == 1 && (op.N % 256 != 0 || op.args.size() != 2))
+                throw Error("gemm swiglu epilogue needs N % 256 == 0 and no residual");
+            if (op.epilogue == 2 && (op.N != 3 * op.heads * 128 || op.args.size() != 3 || op.batch != 1))
+                throw Error("gemm qkv_rope epilogue needs N = 3*heads*128, args [x, w, rope_table], batch 1");
             g.sa = op.sa;
             g.sb = op.sb;
             g.sc = op.sc;
@@ -334,16 +340,23 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
                              std::int64_t cols) { return off + (batch - 1) * bs + (rows - 1) * ld + cols; };
             fits(extent(op.a_off, g.batch, g.sa, g.M, g.lda, g.K) * ei, arg_bytes[0], "A");
             fits(extent(op.b_off, g.batch, g.sb, g.N, g.ldb, g.K) * ei, arg_bytes[1], "B");
-            fits(extent(op.c_off, g.batch, g.sc, g.M, g.ldc, g.N) * eo, out_bytes, "C");
+            if (op.epilogue == 2) fits(3 * op.heads * 128 * op.M * 2, out_bytes, "C (packed q|k|vT)");
+            else fits(extent(op.c_off, g.batch, g.sc, g.M, g.ldc, n_out) * eo, out_bytes, "C");
             g.A = in.argp[0] + op.a_off * ei;
             g.B = in.argp[1] + op.b_off * ei;
             g.C = in.dst + op.c_off * eo;
-            if (op.args.size() == 3) {
+            if (op.epilogue == 2) {
+                fits(op.M * 64 * 2 * 4, arg_bytes[2], "rope_table");
+                g.rope = in.argp[2];
+                g.heads = static_cast<int>(op.heads);
+            } else if (op.args.size() == 3) {
                 fits(extent(op.r_off, g.batch, g.sc, g.M, g.ldc, g.N) * eo, arg_bytes[2], "R");
                 g.R = in.argp[2] + op.r_off * eo;
             }
             in.gemm = std::make_unique<k::GemmPlan>();
             TN_CUDA(k::gemm_prepare(g, in.gemm.get(), num_sms[v.device]));
+            if (op.epilogue == 2 && in.gemm->path == 1)
+                throw Error("gemm qkv_rope epilogue needs a tcgen05-eligible shape (M >= 128, aligned operands)");
             break;
         }
         case OpType::RmsNorm:
@@ -417,17 +430,19 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             fits(op.rows * op.cols * 2, out_bytes, "P");
             break;
         case OpType::Attention: {
-            need_args(3, 3);
+            need_args(1, 3);
             if (op.hd <= 0 || op.hd > 256 || op.seq <= 0 || op.heads <= 0) throw Error("attention: bad shape");
             const std::int64_t ldo = op.ldo ? op.ldo : op.heads * op.hd;
-            fits(op.heads * op.seq * op.hd * 2, arg_bytes[0], "q");
-            fits(op.heads * op.seq * op.hd * 2, arg_bytes[1], "k");
-            fits(op.heads * op.seq * op.hd * 2, arg_bytes[2], "vt");
+            const std::int64_t sec = op.heads * op.seq * op.hd;
+            const size_t iq = 0, ik = op.args.size() == 3 ? 1 : 0, iv = op.args.size() == 3 ? 2 : 0;
+            fits((op.q_off + sec) * 2, arg_bytes[iq], "q");
+            fits((op.k_off + sec) * 2, arg_bytes[ik], "k");
+            fits((op.v_off + sec) * 2, arg_bytes[iv], "vt");
             fits(((op.seq - 1) * ldo + op.heads * op.hd) * 2, out_bytes, "out");
             k::AttnArgs aa;
-            aa.q = in.argp[0];
-            aa.k = in.argp[1];
-            aa.vt = in.argp[2];
+            aa.q = in.argp[iq] + op.q_off * 2;
+            aa.k = in.argp[ik] + op.k_off * 2;
+            aa.vt = in.argp[iv] + op.v_off * 2;
             aa.out = in.dst;
             aa.heads = static_cast<int>(op.heads);
             aa.seq = static_cast<int>(op.seq);

@@ -98,7 +98,17 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
             d.vocab = I("vocab", 0);
             d.ldo = I("ldo", 0);
             d.offs = o.value("offs", std::vector<std::int64_t>{});
+            d.q_off = I("q_off", 0);
+            d.k_off = I("k_off", 0);
+            d.v_off = I("v_off", 0);
             d.causal = static_cast<int>(I("causal", 0));
+            {
+                const std::string ep = o.value("epilogue", std::string("none"));
+                if (ep == "none") d.epilogue = 0;
+                else if (ep == "swiglu") d.epilogue = 1;
+                else if (ep == "qkv_rope") d.epilogue = 2;
+                else throw ParseError("unknown gemm epilogue '" + ep + "'");
+            }
             d.in_dtype = dtype_of(o.value("in_dtype", std::string("bf16")));
             d.out_dtype = dtype_of(o.value("out_dtype", std::string("bf16")));
             d.alpha = o.value("alpha", 1.0);

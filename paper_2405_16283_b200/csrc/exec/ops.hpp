@@ -6,7 +6,11 @@
 //   {"type": "gemm", "args": [A, B (, R)], "M":..,"N":..,"K":.., "batch":1,
 //    "lda","ldb","ldc","sa","sb","sc", "a_off","b_off","c_off","r_off",
 //    "alpha":1.0, "in_dtype":"bf16"|"f32", "out_dtype":"bf16"|"f32",
-//    "causal":0|1|2}
+//    "causal":0|1|2, "epilogue": "none"|"swiglu"}   swiglu: out [M, N/2] with
+//    out[:, 128b+j] = silu(C[:, 256b+j]) * C[:, 256b+128+j] (gate/up rows interleaved in 128-row blocks)
+//    "qkv_rope": args [x, wqkv, rope_table], "heads", hd 128, N = 3*heads*128 -> out packed
+//    [rope(q) (H,M,128) | rope(k) (H,M,128) | vᵀ (H,128,M)]
+//   attention may take one packed arg [qkv] with "q_off", "k_off", "v_off" (elements)
 //   {"type": "rmsnorm", "args": [x, w], "rows", "cols", "eps"}
 //   {"type": "softmax", "args": [S], "batch", "rows", "cols", "scale", "causal"}
 //   {"type": "rope", "args": [src, table], "seq", "ld", "col_off", "heads", "hd"}
@@ -51,9 +55,11 @@ struct OpDesc {
     std::int64_t rows = 0, cols = 0, seq = 0, ld = 0, col_off = 0, heads = 0, hd = 0, count = 0, dim = 0,
                  vocab = 0, ldo = 0;
     int causal = 0;
+    int epilogue = 0;  // gemm: 0 none, 1 swiglu
     int in_dtype = 0, out_dtype = 0;  // k::DType
     double alpha = 1.0, eps = 1e-5, scale = 1.0;
     std::vector<std::int64_t> offs;  // sum: per-argument element offsets
+    std::int64_t q_off = 0, k_off = 0, v_off = 0;  // attention on a packed qkv tensor
 };
 
 // Parses the "op" payloads of a taskgraph JSON document (vertices without an

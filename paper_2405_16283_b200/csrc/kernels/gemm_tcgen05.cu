@@ -42,6 +42,9 @@ struct Params {
     int causal;
     int in_bytes;
     int a_batched, b_batched;
+    int epi;  // 0 plain, 1 swiglu (out[:, 128b + j] = silu(C[:, 256b + j]) * C[:, 256b + 128 + j]), 2 qkv_rope
+    const float* rope;  // qkv_rope: [seq, 64, 2] (cos, sin)
+    int heads;          // qkv_rope: heads per q/k/v section (hd = 128)
 };
 
 __device__ __forceinline__ bool tile_skipped(const Params& p, int mb, int nb, int bn) {
@@ -129,6 +132,95 @@ __device__ __forceinline__ void store_chunk(const Params& p, const std::uint32_t
                 float* c = static_cast<float*>(p.C) + off + n0 + j;
                 if (p.R) x += static_cast<const float*>(p.R)[off + n0 + j];
                 *c = x;
+            }
+        }
+    }
+}
+
+// SwiGLU epilogue: the N tile holds 128-column gate/up block pairs (the
+// weight rows are interleaved that way), so each output column needs two
+// TMEM columns of the same row: out = silu(alpha*g) * (alpha*u).
+template <int BN>
+__device__ __forceinline__ void epilogue_swiglu(const Params& p, std::uint32_t tbase, std::int64_t off, int nb,
+                                                bool row_ok) {
+    Params q = p;
+    q.N = p.N / 2;
+    q.alpha = 1.0f;
+    q.R = nullptr;
+    const int ob = p.out_dtype == BF16 ? 2 : 4;
+    const bool vec_ok = (q.N % 32 == 0) && ((q.ldc * ob) % 16 == 0) && ((reinterpret_cast<std::uintptr_t>(q.C) & 15) == 0);
+    constexpr int H = BN / 2;
+#pragma unroll 1
+    for (int c0 = 0; c0 < H; c0 += 32) {
+        std::uint32_t g[32], u[32];
+        TN_LD32(tbase + c0, g);
+        TN_LD32(tbase + H + c0, u);
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float x = __uint_as_float(g[j]) * p.alpha, y = __uint_as_float(u[j]) * p.alpha;
+            g[j] = __float_as_uint(x / (1.0f + __expf(-x)) * y);
+        }
+        store_chunk(q, g, off, nb * H + c0, row_ok, vec_ok);
+    }
+}
+
+// QKV epilogue (hd = 128, BN = 256 = two heads per N tile): rotate-half
+// RoPE for the q and k sections written head-major [H, seq, 128], and the v
+// section written transposed [H, 128, seq] (lanes hold consecutive tokens, so
+// the transposed stores coalesce across the warp). Output = packed
+// [q | k | vᵀ], each H*seq*128 elements.
+__device__ __forceinline__ void epilogue_qkv_rope(const Params& p, std::uint32_t tbase, int row, int nb,
+                                                  bool row_ok) {
+    constexpr int HD = 128;
+    const std::int64_t sec = static_cast<std::int64_t>(p.heads) * p.M * HD;
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.C);
+#pragma unroll 1
+    for (int hb = 0; hb < 256; hb += HD) {
+        const int col = nb * 256 + hb;  // first column of this head in [0, 3*H*HD)
+        const int which = col / (p.heads * HD), h = (col % (p.heads * HD)) / HD;
+        if (which < 2) {
+            __nv_bfloat16* dst = out + which * sec + (static_cast<std::int64_t>(h) * p.M + row) * HD;
+#pragma unroll 1
+            for (int c0 = 0; c0 < HD / 2; c0 += 32) {
+                std::uint32_t lo[32], hi[32];
+                TN_LD32(tbase + hb + c0, lo);
+                TN_LD32(tbase + hb + HD / 2 + c0, hi);
+                tc_wait_ld();
+                if (!row_ok) continue;
+                const float4* cs = reinterpret_cast<const float4*>(p.rope + (static_cast<std::int64_t>(row) * (HD / 2) + c0) * 2);
+                float a[32], b[32];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const float4 q = cs[j];  // (cos_2j, sin_2j, cos_2j+1, sin_2j+1)
+                    const float x0 = __uint_as_float(lo[2 * j]), y0 = __uint_as_float(hi[2 * j]);
+                    const float x1 = __uint_as_float(lo[2 * j + 1]), y1 = __uint_as_float(hi[2 * j + 1]);
+                    a[2 * j] = x0 * q.x - y0 * q.y;
+                    b[2 * j] = y0 * q.x + x0 * q.y;
+                    a[2 * j + 1] = x1 * q.z - y1 * q.w;
+                    b[2 * j + 1] = y1 * q.z + x1 * q.w;
+                }
+                uint4* d0 = reinterpret_cast<uint4*>(dst + c0);
+                uint4* d1 = reinterpret_cast<uint4*>(dst + HD / 2 + c0);
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd) {
+                    d0[qd] = make_uint4(pack_bf16(a[qd * 8], a[qd * 8 + 1]), pack_bf16(a[qd * 8 + 2], a[qd * 8 + 3]),
+                                        pack_bf16(a[qd * 8 + 4], a[qd * 8 + 5]), pack_bf16(a[qd * 8 + 6], a[qd * 8 + 7]));
+                    d1[qd] = make_uint4(pack_bf16(b[qd * 8], b[qd * 8 + 1]), pack_bf16(b[qd * 8 + 2], b[qd * 8 + 3]),
+                                        pack_bf16(b[qd * 8 + 4], b[qd * 8 + 5]), pack_bf16(b[qd * 8 + 6], b[qd * 8 + 7]));
+                }
+            }
+        } else {
+            __nv_bfloat16* dst = out + 2 * sec + static_cast<std::int64_t>(h) * HD * p.M + row;
+#pragma unroll 1
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                std::uint32_t v[32];
+                TN_LD32(tbase + hb + c0, v);
+                tc_wait_ld();
+                if (!row_ok) continue;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    dst[static_cast<std::int64_t>(c0 + j) * p.M] = __float2bfloat16_rn(__uint_as_float(v[j]));
             }
         }
     }
@@ -259,13 +351,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row = mb * kBM + lane_base + lane;
             const bool row_ok = row < p.M;
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+            const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
+            if (p.epi == 1) {
+                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+            } else if (p.epi == 2) {
+                epilogue_qkv_rope(p, tbase, row, nb, row_ok);
+            } else {
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                std::uint32_t r[32];
-                const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN + c0;
-                TN_LD32(taddr, r);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    std::uint32_t r[32];
+                    TN_LD32(tbase + c0, r);
+                    tc_wait_ld();
+                    store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -472,13 +570,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int row = mb * BM2 + static_cast<int>(rank) * HALF + lane_base + lane;
             const bool row_ok = row < p.M;
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+            const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
+            if (p.epi == 1) {
+                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+            } else if (p.epi == 2) {
+                epilogue_qkv_rope(p, tbase, row, nb, row_ok);
+            } else {
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                std::uint32_t r[32];
-                const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN + c0;
-                TN_LD32(taddr, r);
-                tc_wait_ld();
-                store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    std::uint32_t r[32];
+                    TN_LD32(tbase + c0, r);
+                    tc_wait_ld();
+                    store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -502,29 +606,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 __global__ void gemm_simt_kernel(GemmArgs a) {
     const std::int64_t gw = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
     const int lane = threadIdx.x % 32;
-    const std::int64_t total = static_cast<std::int64_t>(a.batch) * a.M * a.N;
+    const int Nout = a.epi == 1 ? a.N / 2 : a.N;
+    const std::int64_t total = static_cast<std::int64_t>(a.batch) * a.M * Nout;
     if (gw >= total) return;
-    const int n = static_cast<int>(gw % a.N);
-    const int m = static_cast<int>((gw / a.N) % a.M);
-    const int b = static_cast<int>(gw / (static_cast<std::int64_t>(a.N) * a.M));
+    const int nout = static_cast<int>(gw % Nout);
+    const int m = static_cast<int>((gw / Nout) % a.M);
+    const int b = static_cast<int>(gw / (static_cast<std::int64_t>(Nout) * a.M));
+    // swiglu: gate column 256*(j/128) + j%128, up column + 128
+    const int n = a.epi == 1 ? 256 * (nout / 128) + nout % 128 : nout;
     if (a.causal == 1 && n > m) return;
     int kend = a.K;
     if (a.causal == 2) kend = min(kend, m + 1);
-    float acc = 0.f;
-    if (a.in_dtype == BF16) {
-        const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
-        const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B) + b * a.sb + static_cast<std::int64_t>(n) * a.ldb;
-        for (int k = lane; k < kend; k += 32) acc += __bfloat162float(A[k]) * __bfloat162float(B[k]);
-    } else {
-        const float* A = static_cast<const float*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
-        const float* B = static_cast<const float*>(a.B) + b * a.sb + static_cast<std::int64_t>(n) * a.ldb;
-        for (int k = lane; k < kend; k += 32) acc += A[k] * B[k];
-    }
+    auto dot = [&](int col) {
+        float acc = 0.f;
+        if (a.in_dtype == BF16) {
+            const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
+            const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B) + b * a.sb + static_cast<std::int64_t>(col) * a.ldb;
+            for (int k = lane; k < kend; k += 32) acc += __bfloat162float(A[k]) * __bfloat162float(B[k]);
+        } else {
+            const float* A = static_cast<const float*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
+            const float* B = static_cast<const float*>(a.B) + b * a.sb + static_cast<std::int64_t>(col) * a.ldb;
+            for (int k = lane; k < kend; k += 32) acc += A[k] * B[k];
+        }
 #pragma unroll
-    for (int o = 16; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        for (int o = 16; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        return acc * a.alpha;
+    };
+    float acc = dot(n);
+    if (a.epi == 1) {
+        const float up = dot(n + 128);
+        acc = acc / (1.0f + __expf(-acc)) * up;
+    }
     if (lane != 0) return;
-    acc *= a.alpha;
-    const std::int64_t off = b * a.sc + static_cast<std::int64_t>(m) * a.ldc + n;
+    const std::int64_t off = b * a.sc + static_cast<std::int64_t>(m) * a.ldc + nout;
     if (a.out_dtype == BF16) {
         if (a.R) acc += __bfloat162float(static_cast<const __nv_bfloat16*>(a.R)[off]);
         static_cast<__nv_bfloat16*>(a.C)[off] = __float2bfloat16_rn(acc);
@@ -594,7 +708,8 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     auto al16 = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
     const int bn = a.N >= 256 ? 256 : a.N >= 128 ? 128 : 64;
     const bool two_sm = a.M >= 256 && a.N >= 256;
-    bool ok = a.M >= kBM && a.N >= bn && a.K * es >= kAtom && al16(a.A) && al16(a.B) && (a.lda * es) % 16 == 0 &&
+    bool ok = (a.epi == 0 || (a.N % 256 == 0 && bn == 256 && a.R == nullptr)) &&
+              (a.epi != 2 || (a.batch == 1 && (reinterpret_cast<std::uintptr_t>(a.rope) & 15) == 0)) && a.M >= kBM && a.N >= bn && a.K * es >= kAtom && al16(a.A) && al16(a.B) && (a.lda * es) % 16 == 0 &&
               (a.ldb * es) % 16 == 0 && (a.batch == 1 || ((a.sa * es) % 16 == 0 && (a.sb * es) % 16 == 0)) &&
               (a.in_dtype == BF16 || a.in_dtype == F32);
     if (ok) {
@@ -626,8 +741,9 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
 
 cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
     const GemmArgs& a = plan.args;
+    if (plan.path == 1 && a.epi == 2) return cudaErrorNotSupported;  // rejected at prepare time
     if (plan.path == 1) {
-        const std::int64_t warps = static_cast<std::int64_t>(a.batch) * a.M * a.N;
+        const std::int64_t warps = static_cast<std::int64_t>(a.batch) * a.M * (a.epi == 1 ? a.N / 2 : a.N);
         const int threads = 256;
         const std::int64_t blocks = (warps * 32 + threads - 1) / threads;
         gemm_simt_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(a);
@@ -650,6 +766,9 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
     p.in_bytes = dtype_size(a.in_dtype);
     p.a_batched = a.batch > 1 && a.sa != 0;
     p.b_batched = a.batch > 1 && a.sb != 0;
+    p.epi = a.epi;
+    p.rope = static_cast<const float*>(a.rope);
+    p.heads = a.heads;
     if (plan.path == 2)
         gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, p);
     else if (plan.bn == 128)

@@ -33,6 +33,10 @@ struct GemmArgs {
     int in_dtype = BF16;   // BF16 -> kind::f16, F32 -> kind::tf32
     int out_dtype = BF16;
     int causal = 0;
+    int epi = 0;  // 1: SwiGLU epilogue, out [M, N/2]: out[:, 128b+j] = silu(C[:, 256b+j]) * C[:, 256b+128+j]
+                  // 2: QKV + RoPE epilogue (hd 128): out = [rope(q) (H,M,128) | rope(k) | vᵀ (H,128,M)]
+    const void* rope = nullptr;  // epi 2: fp32 [M, 64, 2] (cos, sin)
+    int heads = 0;               // epi 2: heads per section, N = 3 * heads * 128
 };
 
 struct alignas(64) GemmPlan {

@@ -175,7 +175,8 @@ LLAMA_65B = LlamaConfig(dim=8192, layers=80, heads=64, ffn=22016)
 
 
 def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device: int = 0,
-                  std: float = 0.02, fused_attention: bool = True) -> GraphBuilder:
+                  std: float = 0.02, fused_attention: bool = True, fused_swiglu: bool = True,
+                  fused_qkv: bool = True) -> GraphBuilder:
     """One forward prefill over `seq` tokens (causal), single device.
 
     Per layer: rmsnorm -> QKV gemm -> rope(q), rope(k), Vᵀ -> attention ->
@@ -184,7 +185,13 @@ def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device:
     (`fused_attention`, S/P stay on chip) or three vertices with the n²
     intermediates materialised (batched causal QKᵀ in fp32 with the upper
     tiles skipped -> causal softmax to bf16 P -> batched P·V into [seq, dim]),
-    which the planner may offload.
+    which the planner may offload. With `fused_swiglu` the gate/up weight
+    rows are stored interleaved in 128-row blocks (gate_b, up_b, ...) and the
+    gate_up GEMM's epilogue applies silu(g)*u, so the [seq, 2*ffn]
+    intermediate never reaches HBM (requires ffn % 128 == 0). With
+    `fused_qkv` (hd 128, fused attention) the QKV GEMM's epilogue applies RoPE
+    to q/k and transposes v, writing one packed [q | k | vᵀ] tensor that the
+    attention vertex reads by offset.
     Head: final rmsnorm -> last-token logits (fp32). Weights are graph inputs
     (cold in host RAM, materialised by H2D at dispatch).
     """
@@ -206,6 +213,19 @@ def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device:
         w2 = g.input(p + "w2", (d, f), "bf16", dev, init=("normal", std))
         h = g.kernel(p + "attn_norm_out", {"type": "rmsnorm", "args": [x, wn1], "rows": S, "cols": d, "eps": cfg.eps},
                      (S, d), "bf16", dev)
+        if fused_qkv and fused_attention and hd == 128:
+            qkv = g.gemm(p + "qkv_rope", h, wqkv, S, 3 * d, d, r=rope_tab, epilogue="qkv_rope", heads=H,
+                         out_shape=(3, H, S, hd), device=dev)
+            sec = H * S * hd
+            op = {"type": "attention", "args": [qkv], "q_off": 0, "k_off": sec, "v_off": 2 * sec, "heads": H,
+                  "seq": S, "hd": hd, "ldo": d, "scale": 1.0 / math.sqrt(hd), "causal": 1}
+            o = g.kernel(p + "attn", op, (S, d), "bf16", dev, cost=2.0 * S * S * hd * H / _PEAK_FLOPS)
+            g.flops += 2.0 * S * S * hd * H * (1 + 1 / S)
+            x = g.gemm(p + "attn_out", o, wo, S, d, d, r=x, out_shape=(S, d), device=dev)
+            h2 = g.kernel(p + "ffn_norm_out", {"type": "rmsnorm", "args": [x, wn2], "rows": S, "cols": d,
+                                               "eps": cfg.eps}, (S, d), "bf16", dev)
+            x = _ffn(g, p, h2, w13, w2, x, S, d, f, dev, fused_swiglu)
+            continue
         qkv = g.gemm(p + "qkv", h, wqkv, S, 3 * d, d, out_shape=(S, 3 * d), device=dev)
         q = g.kernel(p + "q_rope", {"type": "rope", "args": [qkv, rope_tab], "seq": S, "ld": 3 * d, "col_off": 0,
                                     "heads": H, "hd": hd}, (H, S, hd), "bf16", dev)
@@ -228,15 +248,22 @@ def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device:
         x = g.gemm(p + "attn_out", o, wo, S, d, d, r=x, out_shape=(S, d), device=dev)
         h2 = g.kernel(p + "ffn_norm_out", {"type": "rmsnorm", "args": [x, wn2], "rows": S, "cols": d, "eps": cfg.eps},
                       (S, d), "bf16", dev)
-        gu = g.gemm(p + "gate_up", h2, w13, S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
-        a = g.kernel(p + "act", {"type": "silu_mul", "args": [gu], "rows": S, "cols": f}, (S, f), "bf16", dev)
-        x = g.gemm(p + "ffn_out", a, w2, S, d, f, r=x, out_shape=(S, d), device=dev)
+        x = _ffn(g, p, h2, w13, w2, x, S, d, f, dev, fused_swiglu)
     wn = g.input("norm", (d,), "bf16", dev, init=("normal", 1.0))
     wout = g.input("output", (V, d), "bf16", dev, init=("normal", std))
     hn = g.kernel("final_norm", {"type": "rmsnorm", "args": [x, wn], "rows": S, "cols": d, "eps": cfg.eps},
                   (S, d), "bf16", dev)
     g.gemm("logits", hn, wout, 1, V, d, a_off=(S - 1) * d, out_dtype="f32", out_shape=(1, V), device=dev)
     return g
+
+
+def _ffn(g, p, h2, w13, w2, x, S, d, f, dev, fused_swiglu):
+    if fused_swiglu and f % 128 == 0:
+        a = g.gemm(p + "act", h2, w13, S, 2 * f, d, epilogue="swiglu", out_shape=(S, f), device=dev)
+    else:
+        gu = g.gemm(p + "gate_up", h2, w13, S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
+        a = g.kernel(p + "act", {"type": "silu_mul", "args": [gu], "rows": S, "cols": f}, (S, f), "bf16", dev)
+    return g.gemm(p + "ffn_out", a, w2, S, d, f, r=x, out_shape=(S, d), device=dev)
 
 
 def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = None,

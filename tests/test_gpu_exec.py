@@ -36,8 +36,9 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     a = g.input("A", (batch, M, K), in_dtype, init=("normal", 1.0))
     b = g.input("B", (batch, N, K), in_dtype, init=("normal", 1.0))
     r = g.input("R", (batch, M, N), out_dtype, init=("normal", 1.0)) if residual else None
-    g.gemm("C", a, b, M, N, K, r=r, batch=batch, sa=sa, sb=sb, sc=M * N if batch > 1 else 0, in_dtype=in_dtype,
-           out_dtype=out_dtype, causal=causal, out_shape=(batch, M, N), **kw)
+    n_out = N // 2 if kw.get("epilogue") == "swiglu" else N
+    g.gemm("C", a, b, M, N, K, r=r, batch=batch, sa=sa, sb=sb, sc=M * n_out if batch > 1 else 0, in_dtype=in_dtype,
+           out_dtype=out_dtype, causal=causal, out_shape=(batch, M, n_out), **kw)
     return g
 
 
@@ -54,6 +55,9 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=640, N=200, K=256),                       # 1-CTA BN=128, ragged N, scalar epilogue
     dict(M=256, N=64, K=192, out_dtype="f32"),       # BN=64
     dict(M=1000, N=520, K=320, residual=True),       # CTA-pair path with ragged M/N tiles
+    dict(M=512, N=1024, K=256, epilogue="swiglu"),   # fused SwiGLU, CTA pair
+    dict(M=128, N=512, K=128, epilogue="swiglu"),    # fused SwiGLU, 1-CTA
+    dict(M=8, N=512, K=128, epilogue="swiglu"),      # fused SwiGLU, SIMT
 ])
 def test_gemm_parity(shape):
     shape = dict(shape)

@@ -38,6 +38,46 @@ def test_oracle_matches_direct_forward():
     assert np.isfinite(logits).all() and np.abs(logits).max() > 0
 
 
+def test_fused_swiglu_equals_unfused():
+    """gemm epilogue "swiglu" == gate/up gemm + silu_mul with the same weights
+    (interleaved 128-row gate/up blocks vs stacked halves)."""
+    from oracle import ops_ref as R
+    cfg = W.LlamaConfig(dim=256, layers=1, heads=2, ffn=512, vocab=300)
+    gf, gu = W.llama_prefill(cfg, 128, fused_swiglu=True), W.llama_prefill(cfg, 128, fused_swiglu=False)
+    inp_u = inputs_of(gu, seed=41)
+    name_u = {gu.tensors[v].name: a for v, a in inp_u.items()}
+    inp_f = {}
+    for t in gf.inputs():
+        a = name_u[t.name]
+        if t.name.endswith("w13"):  # stacked [gate; up] -> interleaved 128-row blocks
+            w = a.reshape(2 * cfg.ffn, cfg.dim)
+            blocks = [np.concatenate([w[128 * b:128 * (b + 1)], w[cfg.ffn + 128 * b: cfg.ffn + 128 * (b + 1)]])
+                      for b in range(cfg.ffn // 128)]
+            a = np.concatenate(blocks).reshape(-1)
+        inp_f[t.id] = a
+    of, ou = gf.outputs()[0], gu.outputs()[0]
+    mf, _ = W.plan(gf, 1 << 28)
+    mu, _ = W.plan(gu, 1 << 28)
+    yf = out_values(gf, of, oracle_outputs(gf, mf, inp_f)[of])
+    yu = out_values(gu, ou, oracle_outputs(gu, mu, inp_u)[ou])
+    assert rel_err(yf, yu) < 1e-2
+
+
+def test_fused_qkv_rope_equals_unfused():
+    """gemm epilogue "qkv_rope" + packed-offset attention == qkv gemm -> rope(q),
+    rope(k), vᵀ -> attention, with identical weights."""
+    cfg = W.LlamaConfig(dim=256, layers=2, heads=2, ffn=512, vocab=300)
+    ga, gb = W.llama_prefill(cfg, 128, fused_qkv=True), W.llama_prefill(cfg, 128, fused_qkv=False)
+    assert any(v.get("op", {}).get("epilogue") == "qkv_rope" for v in ga.vertices)
+    ia, ib = inputs_of(ga, seed=43), inputs_of(gb, seed=43)  # name-keyed: same weights
+    oa, ob = ga.outputs()[0], gb.outputs()[0]
+    ma, _ = W.plan(ga, 1 << 28)
+    mb, _ = W.plan(gb, 1 << 28)
+    ya = out_values(ga, oa, oracle_outputs(ga, ma, ia)[oa])
+    yb = out_values(gb, ob, oracle_outputs(gb, mb, ib)[ob])
+    assert rel_err(ya, yb) < 1e-2
+
+
 def test_matmul_chain_oracle_multi_device():
     g = W.matmul_chain(n=256, tile=128, chain=2, devices=2)
     cap = [int(c * 1.6) for c in W.working_set_floor(g)]
@@ -84,7 +124,7 @@ def test_tensor_parallel_graph_equals_single_device():
     the same logits as the single-device graph from the same (sharded) weights."""
     from helpers import tp_inputs_from_full
     cfg = W.LlamaConfig(dim=256, layers=2, heads=4, ffn=512, vocab=300)
-    g1 = W.llama_prefill(cfg, 128)
+    g1 = W.llama_prefill(cfg, 128, fused_swiglu=False)  # TP shards use stacked [gate; up] rows
     mg1, _ = W.plan(g1, 1 << 30)
     full = inputs_of(g1, seed=31)
     (o1,) = g1.outputs()
