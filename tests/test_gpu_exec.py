@@ -145,7 +145,7 @@ def test_unfused_attention_pipeline_matches_fused():
     outs = []
     for fused in (True, False):
         g = W.llama_prefill(SMALL, 256, layers=2, fused_attention=fused)
-        mg, _ = W.plan(g, int(W.working_set_floor(g)[0] * 2))
+        mg, _ = W.plan(g, int(W.working_set_floor(g)[0] * 2), alloc_horizon="lazy")
         _, got = run_gpu(g, mg, inputs_of(g, seed=8))
         (o,) = g.outputs()
         outs.append(out_values(g, o, got[o]))
