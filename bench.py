@@ -148,6 +148,15 @@ def device_inputs_one(t, seed: int, device):
         inv = float(t.init[1]) ** (-torch.arange(half, device=device, dtype=torch.float64) * 2.0 / (2 * half))
         ang = torch.arange(S, device=device, dtype=torch.float64)[:, None] * inv[None, :]
         x = torch.stack([ang.cos(), ang.sin()], dim=-1).float().reshape(-1)
+    elif kind in ("lora_a", "lora_b"):
+        rows, cols = t.shape
+        x = torch.randn(rows, cols, generator=gen, device=device, dtype=torch.float32).mul_(float(t.init[1]))
+        r = int(t.init[2])
+        if kind == "lora_a":
+            x[r:, :] = 0
+        else:
+            x[:, r:] = 0
+        x = x.reshape(-1).to(torch.bfloat16)
     elif kind == "normal":
         x = torch.randn(n, generator=gen, device=device, dtype=torch.float32).mul_(float(t.init[1]))
         x = x.to(torch.bfloat16) if t.dtype == "bf16" else x

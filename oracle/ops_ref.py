@@ -234,14 +234,78 @@ def op_softmax_apply(op, args, out):
 
 
 def op_rope(op, args, out):
+    """Rotate-half RoPE; "inverse" rotates by -theta (the backward), "tokens_out"
+    writes [seq, heads*hd] instead of head-major [heads, seq, hd]."""
     S, ld, co, H, hd = op["seq"], op["ld"], op.get("col_off", 0), op["heads"], op["hd"]
     half = hd // 2
     x = strided(args[0], "bf16", co, 1, 0, S, ld, H * hd)[0].reshape(S, H, hd)
     tab = load(args[1], "f32", S * half * 2).reshape(S, half, 2)
-    c, s = tab[:, None, :, 0], tab[:, None, :, 1]
+    sgn = np.float32(-1.0 if op.get("inverse", 0) else 1.0)
+    c, s = tab[:, None, :, 0], sgn * tab[:, None, :, 1]
     a, b = x[..., :half], x[..., half:]
     y = np.concatenate([a * c - b * s, b * c + a * s], axis=-1)  # [S, H, hd]
-    store(out, "bf16", np.transpose(y, (1, 0, 2)))
+    store(out, "bf16", y if op.get("tokens_out", 0) else np.transpose(y, (1, 0, 2)))
+
+
+def op_transpose(op, args, out):
+    Bn, R, Cc, dt = op.get("batch", 1), op["rows"], op["cols"], op.get("out_dtype", "bf16")
+    t = typed(args[0], dt)[: Bn * R * Cc].reshape(Bn, R, Cc)
+    o = typed(out, dt)
+    o[: Bn * R * Cc] = np.transpose(t, (0, 2, 1)).reshape(-1)
+
+
+def op_rmsnorm_bwd(op, args, out):
+    """dx = r (w.dy) - x r^3 mean((w.dy).x), r = 1/sqrt(mean(x^2) + eps)."""
+    R, Cc, eps = op["rows"], op["cols"], op.get("eps", 1e-5)
+    x = load(args[0], "bf16", R * Cc).reshape(R, Cc)
+    w = load(args[1], "bf16", Cc)
+    dy = load(args[2], "bf16", R * Cc).reshape(R, Cc)
+    r = (1.0 / np.sqrt(np.mean(x * x, axis=1, keepdims=True, dtype=np.float32) + np.float32(eps))).astype(np.float32)
+    g = w[None, :] * dy
+    k = r ** 3 * np.mean(g * x, axis=1, keepdims=True, dtype=np.float32)
+    store(out, "bf16", r * g - x * k)
+
+
+def op_swiglu_bwd(op, args, out):
+    R, Cc = op["rows"], op["cols"]
+    gu = load(args[0], "bf16", R * 2 * Cc).reshape(R, 2 * Cc)
+    da = load(args[1], "bf16", R * Cc).reshape(R, Cc)
+    g, u = gu[:, :Cc], gu[:, Cc:]
+    sg = 1.0 / (1.0 + np.exp(-g))
+    store(out, "bf16", np.concatenate([da * u * sg * (1.0 + g * (1.0 - sg)), da * g * sg], axis=1))
+
+
+def op_softmax_bwd(op, args, out):
+    Bn, R, Cc, causal = op.get("batch", 1), op["rows"], op["cols"], op.get("causal", 0)
+    P = load(args[0], "bf16", Bn * R * Cc).reshape(Bn, R, Cc)
+    dP = load(args[1], op.get("in_dtype", "f32"), Bn * R * Cc).reshape(Bn, R, Cc)
+    keep = _valid_mask(R, Cc, causal)[None]
+    P = np.where(keep, P, 0.0)
+    dot = np.sum(P * np.where(keep, dP, 0.0), axis=2, keepdims=True, dtype=np.float32)
+    store(out, "bf16", np.where(keep, P * (dP - dot), 0.0).astype(np.float32))
+
+
+def _xent_parts(op, args):
+    R, V = op["rows"], op["vocab"]
+    lg = load(args[0], op.get("in_dtype", "bf16"), R * V).reshape(R, V)
+    t = np.clip(load(args[1], "i32", R), 0, V - 1)
+    mx = lg.max(axis=1, keepdims=True)
+    e = np.exp(lg - mx)
+    ssum = e.sum(axis=1, keepdims=True, dtype=np.float32)
+    return lg, t, mx, e, ssum
+
+
+def op_xent_grad(op, args, out):
+    lg, t, mx, e, ssum = _xent_parts(op, args)
+    g = e / ssum
+    g[np.arange(len(t)), t] -= 1.0
+    store(out, op.get("out_dtype", "bf16"), g * np.float32(op.get("scale", 1.0)))
+
+
+def op_xent_loss(op, args, out):
+    lg, t, mx, e, ssum = _xent_parts(op, args)
+    rows = (mx[:, 0] + np.log(ssum[:, 0]) - lg[np.arange(len(t)), t]) * np.float32(op.get("scale", 1.0))
+    store(out, "f32", np.array([np.sum(rows, dtype=np.float32)], dtype=np.float32))
 
 
 def op_transpose_heads(op, args, out):
@@ -301,6 +365,12 @@ OPS = {
     "stats_combine": op_stats_combine,
     "softmax_apply": op_softmax_apply,
     "concat": op_concat,
+    "transpose": op_transpose,
+    "rmsnorm_bwd": op_rmsnorm_bwd,
+    "swiglu_bwd": op_swiglu_bwd,
+    "softmax_bwd": op_softmax_bwd,
+    "xent_grad": op_xent_grad,
+    "xent_loss": op_xent_loss,
 }
 
 

@@ -97,6 +97,7 @@ struct Executor::Impl {
         std::vector<const char*> argp;  // resolved argument pointers
         std::unique_ptr<k::GemmPlan> gemm;
         std::unique_ptr<k::AttnPlan> attn;
+        void* scratch = nullptr;  // per-vertex device scratch (xent_loss row losses), outside the arena
     };
     std::vector<Instr> prog;
 
@@ -377,6 +378,43 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             fits(op.seq * (op.hd / 2) * 2 * 4, arg_bytes[1], "table");
             fits(op.heads * op.seq * op.hd * 2, out_bytes, "out");
             break;
+        case OpType::Transpose:
+            need_args(1, 1);
+            fits(op.batch * op.rows * op.cols * es(op.out_dtype), arg_bytes[0], "x");
+            fits(op.batch * op.rows * op.cols * es(op.out_dtype), out_bytes, "out");
+            break;
+        case OpType::RmsNormBwd:
+            need_args(3, 3);
+            fits(op.rows * op.cols * 2, arg_bytes[0], "x");
+            fits(op.cols * 2, arg_bytes[1], "w");
+            fits(op.rows * op.cols * 2, arg_bytes[2], "dy");
+            fits(op.rows * op.cols * 2, out_bytes, "dx");
+            break;
+        case OpType::SwigluBwd:
+            need_args(2, 2);
+            fits(op.rows * op.cols * 4, arg_bytes[0], "gu");
+            fits(op.rows * op.cols * 2, arg_bytes[1], "da");
+            fits(op.rows * op.cols * 4, out_bytes, "dgu");
+            break;
+        case OpType::SoftmaxBwd:
+            need_args(2, 2);
+            fits(op.batch * op.rows * op.cols * 2, arg_bytes[0], "P");
+            fits(op.batch * op.rows * op.cols * es(op.in_dtype), arg_bytes[1], "dP");
+            fits(op.batch * op.rows * op.cols * 2, out_bytes, "dS");
+            break;
+        case OpType::XentGrad:
+        case OpType::XentLoss:
+            need_args(2, 2);
+            fits(op.rows * op.vocab * es(op.in_dtype), arg_bytes[0], "logits");
+            fits(op.rows * 4, arg_bytes[1], "targets");
+            if (op.type == OpType::XentGrad) {
+                fits(op.rows * op.vocab * es(op.out_dtype), out_bytes, "grad");
+            } else {
+                fits(4, out_bytes, "loss");
+                set_device(v.device);
+                TN_CUDA(cudaMalloc(&in.scratch, static_cast<size_t>(op.rows) * 4 + 256));
+            }
+            break;
         case OpType::TransposeHeads:
             need_args(1, 1);
             fits(((op.seq - 1) * op.ld + op.col_off + op.heads * op.hd) * 2, arg_bytes[0], "src");
@@ -517,7 +555,30 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
                     break;
                 case OpType::Rope:
                     TN_CUDA(k::rope(a[0], a[1], in.dst, static_cast<int>(op.seq), op.ld, op.col_off,
-                                    static_cast<int>(op.heads), static_cast<int>(op.hd), s));
+                                    static_cast<int>(op.heads), static_cast<int>(op.hd), s, op.inverse, op.tokens_out));
+                    break;
+                case OpType::Transpose:
+                    TN_CUDA(k::transpose(a[0], in.dst, static_cast<int>(op.batch), static_cast<int>(op.rows),
+                                         static_cast<int>(op.cols), k::dtype_size(op.out_dtype), s));
+                    break;
+                case OpType::RmsNormBwd:
+                    TN_CUDA(k::rmsnorm_bwd(a[0], a[1], a[2], in.dst, static_cast<int>(op.rows), static_cast<int>(op.cols),
+                                           static_cast<float>(op.eps), s));
+                    break;
+                case OpType::SwigluBwd:
+                    TN_CUDA(k::swiglu_bwd(a[0], a[1], in.dst, static_cast<int>(op.rows), static_cast<int>(op.cols), s));
+                    break;
+                case OpType::SoftmaxBwd:
+                    TN_CUDA(k::softmax_bwd(a[0], a[1], op.in_dtype, in.dst, static_cast<int>(op.batch),
+                                           static_cast<int>(op.rows), static_cast<int>(op.cols), op.causal, s));
+                    break;
+                case OpType::XentGrad:
+                    TN_CUDA(k::xent(a[0], op.in_dtype, a[1], in.dst, op.out_dtype, static_cast<int>(op.rows),
+                                    static_cast<int>(op.vocab), static_cast<float>(op.scale), 1, nullptr, s));
+                    break;
+                case OpType::XentLoss:
+                    TN_CUDA(k::xent(a[0], op.in_dtype, a[1], in.dst, k::F32, static_cast<int>(op.rows),
+                                    static_cast<int>(op.vocab), static_cast<float>(op.scale), 0, in.scratch, s));
                     break;
                 case OpType::TransposeHeads:
                     TN_CUDA(k::transpose_heads(a[0], in.dst, static_cast<int>(op.seq), op.ld, op.col_off,
@@ -765,6 +826,8 @@ Executor::Impl::~Impl() {
         if (b.p) cudaFreeHost(b.p);
     for (auto& [id, b] : staged)
         if (b.p) cudaFree(b.p);
+    for (auto& in : prog)
+        if (in.scratch) cudaFree(in.scratch);
     for (auto& [id, b] : slots)
         if (b.p) cudaFreeHost(b.p);
 }

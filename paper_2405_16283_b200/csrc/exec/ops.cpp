@@ -23,6 +23,12 @@ const char* to_string(OpType t) {
         case OpType::StatsCombine: return "stats_combine";
         case OpType::SoftmaxApply: return "softmax_apply";
         case OpType::Concat: return "concat";
+        case OpType::Transpose: return "transpose";
+        case OpType::RmsNormBwd: return "rmsnorm_bwd";
+        case OpType::SwigluBwd: return "swiglu_bwd";
+        case OpType::SoftmaxBwd: return "softmax_bwd";
+        case OpType::XentGrad: return "xent_grad";
+        case OpType::XentLoss: return "xent_loss";
     }
     return "?";
 }
@@ -51,6 +57,12 @@ OpType type_of(const std::string& s) {
     if (s == "stats_combine") return OpType::StatsCombine;
     if (s == "softmax_apply") return OpType::SoftmaxApply;
     if (s == "concat") return OpType::Concat;
+    if (s == "transpose") return OpType::Transpose;
+    if (s == "rmsnorm_bwd") return OpType::RmsNormBwd;
+    if (s == "swiglu_bwd") return OpType::SwigluBwd;
+    if (s == "softmax_bwd") return OpType::SoftmaxBwd;
+    if (s == "xent_grad") return OpType::XentGrad;
+    if (s == "xent_loss") return OpType::XentLoss;
     throw ParseError("unknown op type '" + s + "'");
 }
 
@@ -98,6 +110,8 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
             d.vocab = I("vocab", 0);
             d.ldo = I("ldo", 0);
             d.offs = o.value("offs", std::vector<std::int64_t>{});
+            d.inverse = static_cast<int>(I("inverse", 0));
+            d.tokens_out = static_cast<int>(I("tokens_out", 0));
             d.q_off = I("q_off", 0);
             d.k_off = I("k_off", 0);
             d.v_off = I("v_off", 0);

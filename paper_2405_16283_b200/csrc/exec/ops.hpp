@@ -11,6 +11,14 @@
 //    "qkv_rope": args [x, wqkv, rope_table], "heads", hd 128, N = 3*heads*128 -> out packed
 //    [rope(q) (H,M,128) | rope(k) (H,M,128) | vᵀ (H,128,M)]
 //   attention may take one packed arg [qkv] with "q_off", "k_off", "v_off" (elements)
+//   rope: optional "inverse": 1 (rotate by -theta), "tokens_out": 1 (write [seq, heads*hd])
+// training (LoRA step) tasks:
+//   {"type": "transpose", "args": [x], "batch", "rows", "cols", "out_dtype"}   out[b][c][r] = x[b][r][c]
+//   {"type": "rmsnorm_bwd", "args": [x, w, dy], "rows", "cols", "eps"}
+//   {"type": "swiglu_bwd", "args": [gu, da], "rows", "cols"}   gu = [g | u] rows of 2*cols
+//   {"type": "softmax_bwd", "args": [P, dP], "batch", "rows", "cols", "causal", "in_dtype" (dP)}
+//   {"type": "xent_grad", "args": [logits, targets], "rows", "vocab", "scale", "in_dtype", "out_dtype"}
+//   {"type": "xent_loss", "args": [logits, targets], "rows", "vocab", "scale", "in_dtype"} -> f32 scalar
 //   {"type": "rmsnorm", "args": [x, w], "rows", "cols", "eps"}
 //   {"type": "softmax", "args": [S], "batch", "rows", "cols", "scale", "causal"}
 //   {"type": "rope", "args": [src, table], "seq", "ld", "col_off", "heads", "hd"}
@@ -42,7 +50,8 @@ namespace tn {
 
 enum class OpType : std::uint8_t {
     Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast, Attention,
-    RowStats, StatsCombine, SoftmaxApply, Concat
+    RowStats, StatsCombine, SoftmaxApply, Concat,
+    Transpose, RmsNormBwd, SwigluBwd, SoftmaxBwd, XentGrad, XentLoss
 };
 
 struct OpDesc {
@@ -55,7 +64,8 @@ struct OpDesc {
     std::int64_t rows = 0, cols = 0, seq = 0, ld = 0, col_off = 0, heads = 0, hd = 0, count = 0, dim = 0,
                  vocab = 0, ldo = 0;
     int causal = 0;
-    int epilogue = 0;  // gemm: 0 none, 1 swiglu
+    int epilogue = 0;  // gemm: 0 none, 1 swiglu, 2 qkv_rope
+    int inverse = 0, tokens_out = 0;  // rope
     int in_dtype = 0, out_dtype = 0;  // k::DType
     double alpha = 1.0, eps = 1e-5, scale = 1.0;
     std::vector<std::int64_t> offs;  // sum: per-argument element offsets

@@ -41,7 +41,7 @@ unsigned grid_for(std::int64_t work, int per_block = kThreads) {
 // One thread = 8 consecutive rotation pairs (i, i + hd/2) of one (t, h).
 __global__ void rope_vec(const __nv_bfloat16* __restrict__ src, const float* __restrict__ table,
                          __nv_bfloat16* __restrict__ out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
-                         int hd) {
+                         int hd, float sgn, int tokens_out) {
     const int half = hd / 2, groups = half / 8;
     const std::int64_t total = static_cast<std::int64_t>(seq) * heads * groups;
     for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
@@ -57,13 +57,16 @@ __global__ void rope_vec(const __nv_bfloat16* __restrict__ src, const float* __r
         float lo[8], hi[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            float4 q = cs[j];  // (cos_j0, sin_j0, cos_j1, sin_j1)
+            float4 q = cs[j];  // (cos_j0, sin_j0, cos_j1, sin_j1); sgn = -1 rotates back
+            q.y *= sgn;
+            q.w *= sgn;
             lo[2 * j] = a[2 * j] * q.x - b[2 * j] * q.y;
             hi[2 * j] = b[2 * j] * q.x + a[2 * j] * q.y;
             lo[2 * j + 1] = a[2 * j + 1] * q.z - b[2 * j + 1] * q.w;
             hi[2 * j + 1] = b[2 * j + 1] * q.z + a[2 * j + 1] * q.w;
         }
-        __nv_bfloat16* o = out + (static_cast<std::int64_t>(h) * seq + t) * hd;
+        __nv_bfloat16* o = tokens_out ? out + static_cast<std::int64_t>(t) * heads * hd + static_cast<std::int64_t>(h) * hd
+                                      : out + (static_cast<std::int64_t>(h) * seq + t) * hd;
         *reinterpret_cast<uint4*>(o + g * 8) = pack8(lo);
         *reinterpret_cast<uint4*>(o + half + g * 8) = pack8(hi);
     }
@@ -71,7 +74,7 @@ __global__ void rope_vec(const __nv_bfloat16* __restrict__ src, const float* __r
 
 __global__ void rope_scalar(const __nv_bfloat16* __restrict__ src, const float* __restrict__ table,
                             __nv_bfloat16* __restrict__ out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
-                            int hd) {
+                            int hd, float sgn, int tokens_out) {
     const int half = hd / 2;
     const std::int64_t total = static_cast<std::int64_t>(seq) * heads * half;
     for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
@@ -82,8 +85,9 @@ __global__ void rope_scalar(const __nv_bfloat16* __restrict__ src, const float* 
         const __nv_bfloat16* x = src + t * ld + col_off + static_cast<std::int64_t>(h) * hd;
         const float a = __bfloat162float(x[i]), b = __bfloat162float(x[i + half]);
         const float c = table[(static_cast<std::int64_t>(t) * half + i) * 2];
-        const float s = table[(static_cast<std::int64_t>(t) * half + i) * 2 + 1];
-        __nv_bfloat16* o = out + (static_cast<std::int64_t>(h) * seq + t) * hd;
+        const float s = sgn * table[(static_cast<std::int64_t>(t) * half + i) * 2 + 1];
+        __nv_bfloat16* o = tokens_out ? out + static_cast<std::int64_t>(t) * heads * hd + static_cast<std::int64_t>(h) * hd
+                                      : out + (static_cast<std::int64_t>(h) * seq + t) * hd;
         o[i] = __float2bfloat16_rn(a * c - b * s);
         o[i + half] = __float2bfloat16_rn(b * c + a * s);
     }
@@ -224,16 +228,17 @@ bool al16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 
 }  // namespace
 
 cudaError_t rope(const void* src, const void* table, void* out, int seq, std::int64_t ld, std::int64_t col_off,
-                 int heads, int hd, cudaStream_t s) {
+                 int heads, int hd, cudaStream_t s, int inverse, int tokens_out) {
+    const float sgn = inverse ? -1.0f : 1.0f;
     auto S = static_cast<const __nv_bfloat16*>(src);
     auto T = static_cast<const float*>(table);
     auto O = static_cast<__nv_bfloat16*>(out);
     if (hd % 16 == 0 && ld % 8 == 0 && col_off % 8 == 0 && al16(src) && al16(table) && al16(out)) {
         std::int64_t work = static_cast<std::int64_t>(seq) * heads * (hd / 16);
-        rope_vec<<<grid_for(work), kThreads, 0, s>>>(S, T, O, seq, ld, col_off, heads, hd);
+        rope_vec<<<grid_for(work), kThreads, 0, s>>>(S, T, O, seq, ld, col_off, heads, hd, sgn, tokens_out);
     } else {
         std::int64_t work = static_cast<std::int64_t>(seq) * heads * (hd / 2);
-        rope_scalar<<<grid_for(work), kThreads, 0, s>>>(S, T, O, seq, ld, col_off, heads, hd);
+        rope_scalar<<<grid_for(work), kThreads, 0, s>>>(S, T, O, seq, ld, col_off, heads, hd, sgn, tokens_out);
     }
     return cudaGetLastError();
 }

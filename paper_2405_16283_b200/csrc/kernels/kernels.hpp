@@ -96,8 +96,9 @@ cudaError_t softmax_apply(const void* S, const void* st, void* P, int rows, int 
 
 // Rotate-half RoPE: src [seq, ld] bf16, head h at columns col_off + h*hd;
 // table fp32 [seq, hd/2, 2] = (cos, sin); out [H, seq, hd] bf16 (head-major).
+// inverse: rotate by -theta (RoPE backward); tokens_out: write [seq, heads*hd].
 cudaError_t rope(const void* src, const void* table, void* out, int seq, std::int64_t ld, std::int64_t col_off,
-                 int heads, int hd, cudaStream_t s);
+                 int heads, int hd, cudaStream_t s, int inverse = 0, int tokens_out = 0);
 
 // out[h][d][t] = src[t][col_off + h*hd + d]  (V^T per head, bf16)
 cudaError_t transpose_heads(const void* src, void* out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
@@ -116,6 +117,22 @@ cudaError_t concat(const void* const* parts, int n, std::int64_t part_bytes, voi
 // out[t][:] = table[tokens[t]][:]   (tokens int32, table bf16 [vocab, dim])
 cudaError_t embedding(const void* tokens, const void* table, void* out, int seq, int dim, int vocab,
                       cudaStream_t s);
+
+// --- training (LoRA step) tasks ---------------------------------------------
+// out[b][c][r] = in[b][r][c], esize 2 or 4 bytes.
+cudaError_t transpose(const void* in, void* out, int batch, int rows, int cols, int esize, cudaStream_t s);
+// dx = r*(w.dy) - x r^3 mean((w.dy).x), r = rsqrt(mean(x^2)+eps) (bf16).
+cudaError_t rmsnorm_bwd(const void* x, const void* w, const void* dy, void* dx, int rows, int cols, float eps,
+                        cudaStream_t s);
+// gu = [g | u] per row; dgu = [da*u*silu'(g) | da*silu(g)] (bf16).
+cudaError_t swiglu_bwd(const void* gu, const void* da, void* dgu, int rows, int cols, cudaStream_t s);
+// dS = P * (dP - rowsum(P*dP)), causal-masked entries 0 (P bf16, dS bf16).
+cudaError_t softmax_bwd(const void* P, const void* dP, int dp_dtype, void* dS, int batch, int rows, int cols,
+                        int causal, cudaStream_t s);
+// Cross entropy: want_grad -> out = (softmax - onehot) * scale [rows, vocab];
+// else out = fp32 scalar sum_r (lse_r - l_r,t) * scale (scratch: rows floats).
+cudaError_t xent(const void* logits, int lg_dtype, const void* targets, void* out, int out_dtype, int rows, int vocab,
+                 float scale, int want_grad, void* scratch, cudaStream_t s);
 
 // Elementwise dtype cast (bf16 <-> f32), RNE.
 cudaError_t cast(const void* in, int in_dtype, void* out, int out_dtype, std::int64_t count, cudaStream_t s);

@@ -140,7 +140,18 @@ def make_input(t: Tensor, seed: int) -> np.ndarray:
         ang = np.arange(S, dtype=np.float64)[:, None] * inv[None, :]
         tab = np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
         return tab
-    if kind == "ones":
+    if kind in ("lora_a", "lora_b"):
+        # rank-`r` adapter stored padded to the tensor's full rank dimension
+        # (rows >= r of A and columns >= r of B are exactly zero)
+        rows, cols = t.shape
+        x = (rng.standard_normal(n, dtype=np.float32) * np.float32(t.init[1])).reshape(rows, cols)
+        r = int(t.init[2])
+        if kind == "lora_a":
+            x[r:, :] = 0
+        else:
+            x[:, r:] = 0
+        x = x.reshape(-1)
+    elif kind == "ones":
         x = np.ones(n, dtype=np.float32)
     elif kind == "normal":
         x = rng.standard_normal(n, dtype=np.float32) * np.float32(t.init[1])
@@ -356,6 +367,192 @@ def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = N
     hn = g.kernel("final_norm", {"type": "rmsnorm", "args": [x[0], wn], "rows": S, "cols": d, "eps": cfg.eps},
                   (S, d), "bf16", 0)
     g.gemm("logits", hn, wout, 1, V, d, a_off=(S - 1) * d, out_dtype="f32", out_shape=(1, V), device=0)
+    return g
+
+
+def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank: int = 16, rank_pad: int = 64,
+                    lora_alpha: float = 16.0, std: float = 0.02, device: int = 0) -> GraphBuilder:
+    """Config 4: one LoRA fine-tuning step (forward + backward) of a LLaMA
+    model over `seq` tokens, rank-`rank` adapters on the fused QKV projection
+    and on both FFN projections ("rank 16 on Q,K,V,FFN"), frozen
+    base weights, mean token cross-entropy. Every activation the backward
+    needs is a vertex output that stays live from the forward to the
+    backward, so under an HBM cap the planner offloads it to host RAM and
+    reloads it (activation offload). Outputs: the loss and dA/dB of every
+    adapter. Adapters are stored zero-padded to `rank_pad` (the tensor-core
+    K atom); padding rows/columns are exactly zero.
+
+    Backward GEMMs need transposed operands (dX = dY·W, dW = dYᵀ·X); they
+    are expressed as explicit `transpose` vertices feeding the K-major GEMM
+    task, and the attention backward as dP = dO·Vᵀ -> softmax_bwd ->
+    dQ = dS·K, dK = dSᵀ·Q, dV = Pᵀ·dO (materialised n² tiles)."""
+    L = cfg.layers if layers is None else layers
+    d, H, hd, f, V, S = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, cfg.vocab, seq
+    R, sc = rank_pad, lora_alpha / rank
+    scale = 1.0 / math.sqrt(hd)
+    g = GraphBuilder(device_count=1)
+    dev = device
+
+    def tr(name, x, rows, cols, batch=1, dt="bf16"):
+        return g.kernel(name, {"type": "transpose", "args": [x], "batch": batch, "rows": rows, "cols": cols,
+                               "out_dtype": dt}, (batch, cols, rows), dt, dev)
+
+    def rms(name, x, w):
+        return g.kernel(name, {"type": "rmsnorm", "args": [x, w], "rows": S, "cols": d, "eps": cfg.eps}, (S, d),
+                        "bf16", dev)
+
+    def rms_bwd(name, x, w, dy):
+        return g.kernel(name, {"type": "rmsnorm_bwd", "args": [x, w, dy], "rows": S, "cols": d, "eps": cfg.eps},
+                        (S, d), "bf16", dev)
+
+    def add(name, a, b):
+        return g.kernel(name, {"type": "sum", "args": [a, b], "count": S * d, "in_dtype": "bf16",
+                               "out_dtype": "bf16"}, (S, d), "bf16", dev)
+
+    tok = g.input("tokens", (S,), "i32", dev, init=("tokens", V))
+    tgt = g.input("targets", (S,), "i32", dev, init=("tokens", V))
+    emb = g.input("tok_embeddings", (V, d), "bf16", dev, init=("normal", std))
+    rope_tab = g.input("rope_table", (S, hd // 2, 2), "f32", dev, init=("rope", cfg.theta))
+    x = g.kernel("embed", {"type": "embedding", "args": [tok, emb], "seq": S, "dim": d, "vocab": V}, (S, d), "bf16", dev)
+
+    saved = []
+    for l in range(L):
+        p = f"layers.{l}."
+        w = {
+            "wn1": g.input(p + "attention_norm", (d,), "bf16", dev, init=("normal", 1.0)),
+            "wqkv": g.input(p + "wqkv", (3 * d, d), "bf16", dev, init=("normal", std)),
+            "wo": g.input(p + "wo", (d, d), "bf16", dev, init=("normal", std)),
+            "wn2": g.input(p + "ffn_norm", (d,), "bf16", dev, init=("normal", 1.0)),
+            "w13": g.input(p + "w13", (2 * f, d), "bf16", dev, init=("normal", std)),
+            "w2": g.input(p + "w2", (d, f), "bf16", dev, init=("normal", std)),
+            "A1": g.input(p + "lora_qkv.A", (R, d), "bf16", dev, init=("lora_a", std, rank)),
+            "B1": g.input(p + "lora_qkv.B", (3 * d, R), "bf16", dev, init=("lora_b", std, rank)),
+            "A2": g.input(p + "lora_w13.A", (R, d), "bf16", dev, init=("lora_a", std, rank)),
+            "B2": g.input(p + "lora_w13.B", (2 * f, R), "bf16", dev, init=("lora_b", std, rank)),
+            "A3": g.input(p + "lora_w2.A", (R, f), "bf16", dev, init=("lora_a", std, rank)),
+            "B3": g.input(p + "lora_w2.B", (d, R), "bf16", dev, init=("lora_b", std, rank)),
+        }
+        a = {"x": x}
+        a["h"] = rms(p + "attn_norm_out", x, w["wn1"])
+        base = g.gemm(p + "qkv_base", a["h"], w["wqkv"], S, 3 * d, d, out_shape=(S, 3 * d), device=dev)
+        a["U1"] = g.gemm(p + "lora_qkv.U", a["h"], w["A1"], S, R, d, out_shape=(S, R), device=dev)
+        a["qkv"] = g.gemm(p + "qkv", a["U1"], w["B1"], S, 3 * d, R, r=base, alpha=sc, out_shape=(S, 3 * d), device=dev)
+        a["q"] = g.kernel(p + "q_rope", {"type": "rope", "args": [a["qkv"], rope_tab], "seq": S, "ld": 3 * d,
+                                         "col_off": 0, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev)
+        a["k"] = g.kernel(p + "k_rope", {"type": "rope", "args": [a["qkv"], rope_tab], "seq": S, "ld": 3 * d,
+                                         "col_off": d, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev)
+        vt = g.kernel(p + "v_t", {"type": "transpose_heads", "args": [a["qkv"]], "seq": S, "ld": 3 * d,
+                                  "col_off": 2 * d, "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
+        scr = g.gemm(p + "scores", a["q"], a["k"], S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S,
+                     out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
+        a["P"] = g.kernel(p + "probs", {"type": "softmax", "args": [scr], "batch": H, "rows": S, "cols": S,
+                                        "scale": scale, "causal": 1}, (H, S, S), "bf16", dev)
+        o = g.gemm(p + "attn", a["P"], vt, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                   causal=2, out_shape=(S, d), device=dev)
+        a["x1"] = g.gemm(p + "attn_out", o, w["wo"], S, d, d, r=x, out_shape=(S, d), device=dev)
+        a["h2"] = rms(p + "ffn_norm_out", a["x1"], w["wn2"])
+        gub = g.gemm(p + "gate_up_base", a["h2"], w["w13"], S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
+        a["U2"] = g.gemm(p + "lora_w13.U", a["h2"], w["A2"], S, R, d, out_shape=(S, R), device=dev)
+        a["gu"] = g.gemm(p + "gate_up", a["U2"], w["B2"], S, 2 * f, R, r=gub, alpha=sc, out_shape=(S, 2 * f), device=dev)
+        a["act"] = g.kernel(p + "act", {"type": "silu_mul", "args": [a["gu"]], "rows": S, "cols": f}, (S, f), "bf16", dev)
+        y0 = g.gemm(p + "ffn_base", a["act"], w["w2"], S, d, f, r=a["x1"], out_shape=(S, d), device=dev)
+        a["U3"] = g.gemm(p + "lora_w2.U", a["act"], w["A3"], S, R, f, out_shape=(S, R), device=dev)
+        x = g.gemm(p + "ffn_out", a["U3"], w["B3"], S, d, R, r=y0, alpha=sc, out_shape=(S, d), device=dev)
+        saved.append((p, w, a))
+    wn = g.input("norm", (d,), "bf16", dev, init=("normal", 1.0))
+    wout = g.input("output", (V, d), "bf16", dev, init=("normal", std))
+    xL = x
+    hn = rms("final_norm", xL, wn)
+    logits = g.gemm("logits", hn, wout, S, V, d, out_shape=(S, V), device=dev)
+    g.kernel("loss", {"type": "xent_loss", "args": [logits, tgt], "rows": S, "vocab": V, "scale": 1.0 / S,
+                      "in_dtype": "bf16"}, (1,), "f32", dev)
+    dlog = g.kernel("dlogits", {"type": "xent_grad", "args": [logits, tgt], "rows": S, "vocab": V, "scale": 1.0 / S,
+                                "in_dtype": "bf16", "out_dtype": "bf16"}, (S, V), "bf16", dev)
+    woutT = tr("output.T", wout, V, d)
+    dhn = g.gemm("d_final_norm_out", dlog, woutT, S, d, V, out_shape=(S, d), device=dev)
+    dx = rms_bwd("d_x_final", xL, wn, dhn)
+
+    def lora_grads(p, nm, dY, n_out, k_in, U, X, A, B):
+        """dY [S, n_out] of Y = X Wᵀ + s U Bᵀ with U = X Aᵀ: returns V = dY·B and emits
+        dB = s dYᵀU [n_out, R], dA = s VᵀX [R, k_in] as graph outputs."""
+        BT = tr(p + nm + ".B.T", B, n_out, R)
+        Vv = g.gemm(p + nm + ".V", dY, BT, S, R, n_out, out_shape=(S, R), device=dev)
+        dYT = tr(p + nm + ".dY.T", dY, S, n_out)
+        UT = tr(p + nm + ".U.T", U, S, R)
+        g.gemm(p + nm + ".dB", dYT, UT, n_out, R, S, alpha=sc, out_shape=(n_out, R), device=dev)
+        VT = tr(p + nm + ".V.T", Vv, S, R)
+        XT = tr(p + nm + ".X.T", X, S, k_in)
+        # dAᵀ = s·Xᵀ·V keeps M = k_in on the tensor cores (R rows would be a GEMV)
+        dAT = g.gemm(p + nm + ".dA.T", XT, VT, k_in, R, S, alpha=sc, out_shape=(k_in, R), device=dev)
+        tr(p + nm + ".dA", dAT, k_in, R)
+        return Vv
+
+    for l in reversed(range(L)):
+        p, w, a = saved[l]
+        dy = dx  # gradient of x_{l+1}
+        # x_{l+1} = act·W2ᵀ + s·U3·B3ᵀ + x1
+        V3 = lora_grads(p, "lora_w2", dy, d, f, a["U3"], a["act"], w["A3"], w["B3"])
+        w2T = tr(p + "w2.T", w["w2"], d, f)
+        A3T = tr(p + "lora_w2.A.T", w["A3"], R, f)
+        da0 = g.gemm(p + "d_act_base", dy, w2T, S, f, d, out_shape=(S, f), device=dev)
+        da = g.gemm(p + "d_act", V3, A3T, S, f, R, r=da0, alpha=sc, out_shape=(S, f), device=dev)
+        dgu = g.kernel(p + "d_gate_up", {"type": "swiglu_bwd", "args": [a["gu"], da], "rows": S, "cols": f},
+                       (S, 2 * f), "bf16", dev)
+        V2 = lora_grads(p, "lora_w13", dgu, 2 * f, d, a["U2"], a["h2"], w["A2"], w["B2"])
+        w13T = tr(p + "w13.T", w["w13"], 2 * f, d)
+        A2T = tr(p + "lora_w13.A.T", w["A2"], R, d)
+        dh2_0 = g.gemm(p + "d_ffn_norm_out_base", dgu, w13T, S, d, 2 * f, out_shape=(S, d), device=dev)
+        dh2 = g.gemm(p + "d_ffn_norm_out", V2, A2T, S, d, R, r=dh2_0, alpha=sc, out_shape=(S, d), device=dev)
+        dx1 = add(p + "d_x1", dy, rms_bwd(p + "d_x1_norm", a["x1"], w["wn2"], dh2))
+        # x1 = o·Woᵀ + x ; o[:, head h] = P_h·V_h
+        woT = tr(p + "wo.T", w["wo"], d, d)
+        do = g.gemm(p + "d_attn", dx1, woT, S, d, d, out_shape=(S, d), device=dev)
+        dP = g.gemm(p + "d_probs", do, a["qkv"], S, S, hd, batch=H, lda=d, sa=hd, ldb=3 * d, b_off=2 * d, sb=hd,
+                    sc=S * S, out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
+        dS = g.kernel(p + "d_scores", {"type": "softmax_bwd", "args": [a["P"], dP], "batch": H, "rows": S, "cols": S,
+                                       "causal": 1, "in_dtype": "f32"}, (H, S, S), "bf16", dev)
+        kT = tr(p + "k.T", a["k"], S, hd, batch=H)
+        dq_r = g.gemm(p + "d_q_rot", dS, kT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                      alpha=scale, causal=2, out_shape=(S, d), device=dev)
+        dST = tr(p + "d_scores.T", dS, S, S, batch=H)
+        qT = tr(p + "q.T", a["q"], S, hd, batch=H)
+        dk_r = g.gemm(p + "d_k_rot", dST, qT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                      alpha=scale, out_shape=(S, d), device=dev)
+        PT = tr(p + "probs.T", a["P"], S, S, batch=H)
+        doT = g.kernel(p + "d_attn.T", {"type": "transpose_heads", "args": [do], "seq": S, "ld": d, "col_off": 0,
+                                        "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
+        dv = g.gemm(p + "d_v", PT, doT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                    out_shape=(S, d), device=dev)
+        dq = g.kernel(p + "d_q", {"type": "rope", "args": [dq_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
+                                  "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
+        dk = g.kernel(p + "d_k", {"type": "rope", "args": [dk_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
+                                  "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
+        # qkv = h·Wqkvᵀ + s·U1·B1ᵀ with dqkv = [dq | dk | dv]
+        B1T = tr(p + "lora_qkv.B.T", w["B1"], 3 * d, R)
+        V1 = None
+        dBs = []
+        U1T = tr(p + "lora_qkv.U.T", a["U1"], S, R)
+        for j, dpart in enumerate((dq, dk, dv)):
+            V1 = g.gemm(p + f"lora_qkv.V{j}", dpart, B1T, S, R, d, ldb=3 * d, b_off=j * d, r=V1,
+                        out_shape=(S, R), device=dev)
+            dT = tr(p + f"lora_qkv.dY{j}.T", dpart, S, d)
+            dBs.append(g.gemm(p + f"lora_qkv.dB{j}", dT, U1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev))
+        g.kernel(p + "lora_qkv.dB", {"type": "concat", "args": dBs, "count": d * R, "out_dtype": "bf16"},
+                 (3 * d, R), "bf16", dev)
+        V1T = tr(p + "lora_qkv.V.T", V1, S, R)
+        hT = tr(p + "lora_qkv.X.T", a["h"], S, d)
+        dA1T = g.gemm(p + "lora_qkv.dA.T", hT, V1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev)
+        tr(p + "lora_qkv.dA", dA1T, d, R)
+        if l == 0:
+            break  # no gradient is needed below the first layer
+        wqkvT = tr(p + "wqkv.T", w["wqkv"], 3 * d, d)
+        A1T = tr(p + "lora_qkv.A.T", w["A1"], R, d)
+        dh = None
+        for j, dpart in enumerate((dq, dk, dv)):
+            dh = g.gemm(p + f"d_attn_norm_out{j}", dpart, wqkvT, S, d, d, ldb=3 * d, b_off=j * d, r=dh,
+                        out_shape=(S, d), device=dev)
+        dh = g.gemm(p + "d_attn_norm_out", V1, A1T, S, d, R, r=dh, alpha=sc, out_shape=(S, d), device=dev)
+        dx = add(p + "d_x", dx1, rms_bwd(p + "d_x_norm", a["x"], w["wn1"], dh))
     return g
 
 

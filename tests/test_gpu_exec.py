@@ -325,3 +325,79 @@ def test_tensor_parallel_on_one_gpu_four_memgraph_devices():
     assert res[0] == res[1]
     assert st["d2d_bytes"] > 0
     assert rel_err(out_values(g, o, res[0]), out_values(g, o, want[o])) < 3e-2
+
+
+@pytest.mark.parametrize("shape", [dict(batch=1, rows=200, cols=72, dt="bf16"), dict(batch=3, rows=256, cols=128, dt="bf16"),
+                                   dict(batch=2, rows=64, cols=96, dt="f32")])
+def test_transpose_parity(shape):
+    g = W.GraphBuilder()
+    x = g.input("x", (shape["batch"], shape["rows"], shape["cols"]), shape["dt"], init=("normal", 1.0))
+    o = g.kernel("t", {"type": "transpose", "args": [x], "batch": shape["batch"], "rows": shape["rows"],
+                       "cols": shape["cols"], "out_dtype": shape["dt"]},
+                 (shape["batch"], shape["cols"], shape["rows"]), shape["dt"])
+    mg, _ = W.plan(g, 1 << 26)
+    inp = inputs_of(g, seed=60)
+    _, got = run_gpu(g, mg, inp)
+    want = oracle_outputs(g, mg, inp)
+    assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) == 0.0
+
+
+def test_training_rowops_parity():
+    S, d, f, H, V = 256, 512, 384, 2, 1000
+    g = W.GraphBuilder()
+    x = g.input("x", (S, d), "bf16", init=("normal", 1.0))
+    w = g.input("w", (d,), "bf16", init=("normal", 1.0))
+    dy = g.input("dy", (S, d), "bf16", init=("normal", 1.0))
+    gu = g.input("gu", (S, 2 * f), "bf16", init=("normal", 2.0))
+    da = g.input("da", (S, f), "bf16", init=("normal", 1.0))
+    sc = g.input("sc", (H, S, S), "f32", init=("normal", 2.0))
+    dp = g.input("dp", (H, S, S), "f32", init=("normal", 1.0))
+    lg = g.input("lg", (S, V), "bf16", init=("normal", 3.0))
+    tg = g.input("tg", (S,), "i32", init=("tokens", V))
+    tab = g.input("tab", (S, 64, 2), "f32", init=("rope", 10000.0))
+    qr = g.input("qr", (S, d), "bf16", init=("normal", 1.0))
+    P = g.kernel("P", {"type": "softmax", "args": [sc], "batch": H, "rows": S, "cols": S, "scale": 0.3, "causal": 1},
+                 (H, S, S), "bf16")
+    outs = [
+        g.kernel("rb", {"type": "rmsnorm_bwd", "args": [x, w, dy], "rows": S, "cols": d, "eps": 1e-5}, (S, d), "bf16"),
+        g.kernel("sb", {"type": "swiglu_bwd", "args": [gu, da], "rows": S, "cols": f}, (S, 2 * f), "bf16"),
+        g.kernel("smb", {"type": "softmax_bwd", "args": [P, dp], "batch": H, "rows": S, "cols": S, "causal": 1,
+                         "in_dtype": "f32"}, (H, S, S), "bf16"),
+        g.kernel("xg", {"type": "xent_grad", "args": [lg, tg], "rows": S, "vocab": V, "scale": 1.0 / S,
+                        "in_dtype": "bf16", "out_dtype": "bf16"}, (S, V), "bf16"),
+        g.kernel("xl", {"type": "xent_loss", "args": [lg, tg], "rows": S, "vocab": V, "scale": 1.0 / S,
+                        "in_dtype": "bf16"}, (1,), "f32"),
+        g.kernel("ri", {"type": "rope", "args": [qr, tab], "seq": S, "ld": d, "col_off": 0, "heads": 4, "hd": 128,
+                        "inverse": 1, "tokens_out": 1}, (S, d), "bf16"),
+    ]
+    mg, _ = W.plan(g, 1 << 30)
+    inp = inputs_of(g, seed=61)
+    _, got = run_gpu(g, mg, inp)
+    want = oracle_outputs(g, mg, inp)
+    for o in outs:
+        assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 1e-2, g.tensors[o].name
+
+
+def test_lora_step_parity_with_activation_offload():
+    """Config 4 at small scale: the LoRA fwd+bwd memgraph, activations
+    offloaded between forward and backward, GPU == oracle for the loss and
+    every adapter gradient, bitwise stable across dispatch orders."""
+    cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=512, vocab=1000)
+    g = W.llama_lora_step(cfg, 256)
+    mg, st = W.plan(g, int(W.working_set_floor(g)[0] * 2.0), alloc_horizon="lazy")
+    assert st["offloads"] > 0
+    inp = inputs_of(g, seed=62)
+    want = oracle_outputs(g, mg, inp)
+    res = []
+    with Executor(mg, g.to_json()) as ex:
+        for vid, a in inp.items():
+            ex.set_input(vid, a)
+        for tb, seed in (("fifo", 0), ("seeded-random", 3)):
+            trace = json.loads(ex.run("event-driven", tb, seed))
+            res.append({o: ex.get_output(o, g.tensors[o].nbytes) for o in g.outputs()})
+            check_trace(mg, trace)
+        st2 = ex.stats()
+    assert res[0] == res[1]
+    assert st2["d2h_bytes"] > 0
+    for o in g.outputs():
+        assert rel_err(out_values(g, o, res[0][o]), out_values(g, o, want[o])) < 5e-2, g.tensors[o].name

@@ -138,3 +138,81 @@ def test_tensor_parallel_graph_equals_single_device():
     (ot,) = gt.outputs()
     got = out_values(gt, ot, oracle_outputs(gt, mgt, tin, "random", 2)[ot])
     assert rel_err(got, want) < 2e-2
+
+
+def _lora_torch_reference(g, inp, cfg, seq, rank_pad=64, rank=16, lora_alpha=16.0):
+    """fp32 torch autograd of the same LoRA step (weights from the graph inputs)."""
+    import torch
+    from oracle import ops_ref as R
+    byname = {g.tensors[v].name: (g.tensors[v], a) for v, a in inp.items()}
+
+    def T(name):
+        t, a = byname[name]
+        if t.dtype == "bf16":
+            return torch.tensor(R.bf16_to_f32(a).reshape(t.shape))
+        if t.dtype == "i32":
+            return torch.tensor(a.astype(np.int64).reshape(t.shape))
+        return torch.tensor(a.reshape(t.shape))
+
+    d, H, hd, f, S = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, seq
+    s = lora_alpha / rank
+    tab = T("rope_table")
+    cos, sin = tab[..., 0], tab[..., 1]
+
+    def rope(x):  # x [S, H, hd]
+        a, b = x[..., : hd // 2], x[..., hd // 2:]
+        return torch.cat([a * cos[:, None] - b * sin[:, None], b * cos[:, None] + a * sin[:, None]], -1)
+
+    def rms(x, w):
+        return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + cfg.eps) * w
+
+    params = {}
+    x = T("tok_embeddings")[T("tokens")]
+    mask = torch.tril(torch.ones(S, S, dtype=torch.bool))
+    for l in range(cfg.layers):
+        p = f"layers.{l}."
+        for nm in ("lora_qkv", "lora_w13", "lora_w2"):
+            for ab in ("A", "B"):
+                params[p + nm + ".d" + ab] = T(p + nm + "." + ab).requires_grad_(True)
+        A1, B1 = params[p + "lora_qkv.dA"], params[p + "lora_qkv.dB"]
+        A2, B2 = params[p + "lora_w13.dA"], params[p + "lora_w13.dB"]
+        A3, B3 = params[p + "lora_w2.dA"], params[p + "lora_w2.dB"]
+        h = rms(x, T(p + "attention_norm"))
+        qkv = h @ T(p + "wqkv").T + s * (h @ A1.T) @ B1.T
+        q = rope(qkv[:, :d].reshape(S, H, hd)).permute(1, 0, 2)
+        k = rope(qkv[:, d:2 * d].reshape(S, H, hd)).permute(1, 0, 2)
+        v = qkv[:, 2 * d:].reshape(S, H, hd).permute(1, 0, 2)
+        sc = (q @ k.transpose(1, 2)) / hd ** 0.5
+        P = torch.softmax(sc.masked_fill(~mask, float("-inf")), -1)
+        o = (P @ v).permute(1, 0, 2).reshape(S, d)
+        x1 = o @ T(p + "wo").T + x
+        h2 = rms(x1, T(p + "ffn_norm"))
+        gu = h2 @ T(p + "w13").T + s * (h2 @ A2.T) @ B2.T
+        a = torch.nn.functional.silu(gu[:, :f]) * gu[:, f:]
+        x = a @ T(p + "w2").T + s * (a @ A3.T) @ B3.T + x1
+    logits = rms(x, T("norm")) @ T("output").T
+    loss = torch.nn.functional.cross_entropy(logits, T("targets"))
+    loss.backward()
+    return float(loss), {k: v.grad.numpy() for k, v in params.items()}
+
+
+def test_lora_step_gradients_match_torch_autograd():
+    """Config-4 semantics: the LoRA fwd+bwd memgraph (transposes, rmsnorm/
+    swiglu/softmax backward, inverse RoPE, cross entropy), executed by the
+    oracle under an offloading plan, reproduces fp32 autograd's loss and
+    adapter gradients (bf16 activations: 5e-2 normwise)."""
+    cfg = W.LlamaConfig(dim=256, layers=2, heads=2, ffn=256, vocab=300)
+    S = 128
+    g = W.llama_lora_step(cfg, S)
+    fl = W.working_set_floor(g)[0]
+    mg, st = W.plan(g, int(fl * 2.0), alloc_horizon="lazy")
+    assert st["offloads"] > 0  # activations are offloaded between forward and backward
+    inp = inputs_of(g, seed=51)
+    got = oracle_outputs(g, mg, inp, "random", 5)
+    loss_ref, grads = _lora_torch_reference(g, inp, cfg, S)
+    name = {g.tensors[o].name: o for o in g.outputs()}
+    loss = out_values(g, name["loss"], got[name["loss"]])[0]
+    assert abs(loss - loss_ref) / abs(loss_ref) < 1e-2
+    for k, ref in grads.items():
+        o = name[k]
+        assert rel_err(out_values(g, o, got[o]), ref.reshape(-1)) < 5e-2, k
