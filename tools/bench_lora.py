@@ -1,0 +1,56 @@
+"""Config 4: LLaMA-7B LoRA fine-tuning step (fwd + bwd, seq 4096) with
+activation offload under an HBM cap, one B200. Reports step time, host
+traffic, the step roofline max(FLOP/peak, H2D/PCIe, D2H/PCIe) and the
+event-driven vs fixed-order comparison on hardware."""
+import argparse, json, os, sys, time
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import bench
+from paper_2405_16283_b200 import workloads as W
+from paper_2405_16283_b200.executor import Executor
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--seq", type=int, default=4096)
+ap.add_argument("--layers", type=int, default=None)
+ap.add_argument("--cap-gib", type=float, default=16)
+ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--residency", default="host")
+ap.add_argument("--compare", action="store_true")
+a = ap.parse_args()
+t0 = time.time()
+g = W.llama_lora_step(W.LLAMA_7B, a.seq, layers=a.layers)
+mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon="lazy")
+m = json.loads(mg)
+off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
+plan_s = time.time() - t0
+dev = torch.device("cuda", 0)
+inputs = bench.device_inputs(g, 0, dev)
+ex = Executor(mg, g.to_json(), {"input_residency": a.residency})
+for k, v in inputs.items():
+    ex.set_input(k, v)
+del inputs
+pcie = bench.measure_pcie(dev)
+pk = bench.peaks()
+ts = []
+for s in range(a.steps):
+    ts.append(json.loads(ex.run("event-driven", "fifo", s))["makespan"])
+stt = ex.stats()
+loss_id = next(o for o in g.outputs() if g.tensors[o].name == "loss")
+import struct
+loss = struct.unpack("<f", ex.get_output(loss_id, 4))[0]
+res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency}", "memgraph_vertices": len(m["vertices"]),
+       "plan": st, "plan_s": round(plan_s, 2), "offload_gb": round(off / 1e9, 1), "step_s": [round(x, 4) for x in ts],
+       "loss": loss, "tokens_per_s": round(a.seq / min(ts), 1), "flops": stt["flops"],
+       "h2d_gb": round(stt["h2d_bytes"] / 1e9, 2), "d2h_gb": round(stt["d2h_bytes"] / 1e9, 2),
+       "pcie_h2d_measured_gbs": round(pcie, 1), "kernel_busy_s": round(stt["kernel_busy_s"], 4),
+       "exposed_transfer_s": round(stt["exposed_transfer_s"], 4)}
+roof = max(stt["flops"] / (pk["bf16_tflops_sustained"] * 1e12), stt["h2d_bytes"] / (pcie * 1e9),
+           stt["d2h_bytes"] / (pcie * 1e9))
+res["roofline_s"] = round(roof, 4)
+res["frac_of_roofline"] = round(roof / min(ts), 4)
+if a.compare:
+    fx = [json.loads(ex.run("fixed-order", "fifo", s))["makespan"] for s in range(a.steps)]
+    res["fixed_order_step_s"] = [round(x, 4) for x in fx]
+    res["event_driven_speedup"] = round((min(fx) - min(ts)) / min(fx), 4)
+print(json.dumps(res), flush=True)
