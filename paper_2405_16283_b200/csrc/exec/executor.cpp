@@ -92,7 +92,8 @@ struct Executor::Impl {
         const char* src = nullptr;
         void* host = nullptr;  // offload/reload slot, input buffer
         std::size_t bytes = 0;
-        VertexId input_id = -1;
+        VertexId input_id = -1;   // Input vertices, and offload/reload of an evicted input root
+        bool elided = false;      // offload of an unmodified input: no copy
         const OpDesc* op_desc = nullptr;
         std::vector<const char*> argp;  // resolved argument pointers
         std::unique_ptr<k::GemmPlan> gemm;
@@ -270,10 +271,25 @@ void Executor::Impl::build() {
     // Pinned offload slots (one per evicted root, reused across generations:
     // generation g+1's offload data-depends on generation g's reload,
     // compiler.cpp:353-361).
+    // Evicted inputs: their bytes are the input tensor itself, so the offload
+    // copies nothing and the reload reads the input's host / staging copy.
+    if (cfg.elide_input_offloads && cfg.materialize_inputs) {
+        for (size_t i = 0; i < V; ++i) {
+            const MemVertex& v = m.vertices[i];
+            if (v.op != MemOpKind::Offload && v.op != MemOpKind::Reload) continue;
+            const TaskVertex* root = tg.find(v.origin.ref);
+            if (!root || root->kind != VertexKind::Input) continue;
+            prog[i].input_id = v.origin.ref;
+            prog[i].elided = v.op == MemOpKind::Offload;
+        }
+        for (size_t i = 0; i < V; ++i)
+            if (prog[i].input_id >= 0 && m.vertices[i].op != MemOpKind::Input) slots.erase(m.vertices[i].origin.ref);
+    }
     for (auto& [root, s] : slots) s.p = pinned_alloc(s.bytes);
     for (size_t i = 0; i < V; ++i) {
         const MemVertex& v = m.vertices[i];
-        if (v.op == MemOpKind::Offload || v.op == MemOpKind::Reload) prog[i].host = slots.at(v.origin.ref).p;
+        if ((v.op == MemOpKind::Offload || v.op == MemOpKind::Reload) && prog[i].input_id < 0)
+            prog[i].host = slots.at(v.origin.ref).p;
     }
 }
 
@@ -521,10 +537,25 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
             break;
         }
         case MemOpKind::Offload:
+            if (in.elided) {
+                last.d2h_elided_bytes += static_cast<std::int64_t>(in.bytes);
+                break;
+            }
             TN_CUDA(cudaMemcpyAsync(in.host, in.src, in.bytes, cudaMemcpyDeviceToHost, s));
             last.d2h_bytes += static_cast<std::int64_t>(in.bytes);
             break;
         case MemOpKind::Reload:
+            if (in.input_id >= 0) {  // reload of an evicted input: from its own copy
+                const bool dev_copy = cfg.inputs_on_device;
+                auto& pool = dev_copy ? staged : inputs;
+                auto it = pool.find(in.input_id);
+                if (it == pool.end() || !it->second.p)
+                    throw Error("input " + std::to_string(in.input_id) + " has no data (tn_exec_set_input)");
+                const std::size_t n = std::min(in.bytes, it->second.bytes);
+                TN_CUDA(cudaMemcpyAsync(in.dst, it->second.p, n, dev_copy ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+                (dev_copy ? last.d2d_bytes : last.h2d_bytes) += static_cast<std::int64_t>(n);
+                break;
+            }
             TN_CUDA(cudaMemcpyAsync(in.dst, in.host, in.bytes, cudaMemcpyHostToDevice, s));
             last.h2d_bytes += static_cast<std::int64_t>(in.bytes);
             break;
@@ -906,6 +937,7 @@ std::string RunStats::to_json() const {
     j["kernel_launches"] = kernel_launches;
     j["h2d_bytes"] = h2d_bytes;
     j["d2h_bytes"] = d2h_bytes;
+    j["d2h_elided_bytes"] = d2h_elided_bytes;
     j["p2p_bytes"] = p2p_bytes;
     j["d2d_bytes"] = d2d_bytes;
     j["flops"] = flops;
@@ -928,6 +960,7 @@ ExecConfig parse_exec_config(const std::string& text) {
         c.streams_per_device = j.value("streams_per_device", c.streams_per_device);
         c.compute_tokens = j.value("compute_tokens", c.compute_tokens);
         c.lookahead = j.value("lookahead", c.lookahead);
+        c.elide_input_offloads = j.value("elide_input_offloads", c.elide_input_offloads);
         c.materialize_inputs = j.value("materialize_inputs", c.materialize_inputs);
         c.timeout_s = j.value("timeout_s", c.timeout_s);
         const std::string comp = j.value("completion", std::string("poll"));

@@ -21,6 +21,8 @@ struct ExecConfig {
                                      // staging copy (stream only); "host" -> H2D from the
                                      // pinned pool (stream + host_in channel)
     int timeout_s = 600;             // completion watchdog
+    bool elide_input_offloads = true;  // an evicted *input* is never modified: skip its D2H and
+                                       // reload from the input's own host (or HBM staging) copy
     bool poll = true;                // "completion": "poll" (spin on cudaEventQuery) | "callback"
                                      // (cudaLaunchHostFunc -> queue -> condition variable)
 };
@@ -28,7 +30,7 @@ ExecConfig parse_exec_config(const std::string& text);
 
 struct RunStats {
     std::int64_t vertices = 0, kernel_launches = 0;
-    std::int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_bytes = 0, d2d_bytes = 0;
+    std::int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_bytes = 0, d2d_bytes = 0, d2h_elided_bytes = 0;
     double flops = 0, makespan_s = 0, wall_s = 0;
     double kernel_time_s = 0, kernel_busy_s = 0, copy_time_s = 0, exposed_transfer_s = 0;
     std::string to_json() const;

@@ -270,7 +270,7 @@ def test_tight_cap_offload_reload_bytes():
         st = ex.stats()
         (o,) = g.outputs()
         got = ex.get_output(o, g.tensors[o].nbytes)
-    assert st["d2h_bytes"] == off
+    assert st["d2h_bytes"] + st["d2h_elided_bytes"] == off  # evicted inputs are not copied out again
     assert st["h2d_bytes"] == rel + sum(t.nbytes for t in g.inputs())
     assert trace["host_bytes_transferred"] == off + rel
     want = oracle_outputs(g, mg, inp)
@@ -376,6 +376,25 @@ def test_training_rowops_parity():
     want = oracle_outputs(g, mg, inp)
     for o in outs:
         assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 1e-2, g.tensors[o].name
+
+
+def test_input_offload_elision_is_exact():
+    """Elided offloads of evicted (never modified) inputs reload the input's own
+    copy: outputs are bitwise identical to copying them out."""
+    cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=512, vocab=1000)
+    g = W.llama_lora_step(cfg, 256)
+    mg, st = W.plan(g, int(W.working_set_floor(g)[0] * 2.0), alloc_horizon="lazy")
+    inp = inputs_of(g, seed=63)
+    outs = []
+    for elide in (True, False):
+        with Executor(mg, g.to_json(), {"elide_input_offloads": elide}) as ex:
+            for vid, a in inp.items():
+                ex.set_input(vid, a)
+            ex.run()
+            outs.append({o: ex.get_output(o, g.tensors[o].nbytes) for o in g.outputs()})
+            stt = ex.stats()
+            assert (stt["d2h_elided_bytes"] > 0) == elide
+    assert outs[0] == outs[1]
 
 
 def test_lora_step_parity_with_activation_offload():
