@@ -182,7 +182,7 @@ def test_dispatch_order_independence_bitwise(cfg):
             check_trace(mg, trace)
         st = ex.stats()
     assert all(r == results[0] for r in results)
-    assert st["kernel_launches"] > 0 and st["d2h_bytes"] > 0
+    assert st["kernel_launches"] > 0 and st["d2h_bytes"] + st["d2h_elided_bytes"] > 0
     want = oracle_outputs(g, mg, inp)
     assert rel_err(out_values(g, o, results[0]), out_values(g, o, want[o])) < 3e-2
 
