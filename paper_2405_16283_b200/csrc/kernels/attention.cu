@@ -54,15 +54,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ std::uint8_t smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = (raw + 1023) & ~1023u;
-    const std::uint32_t sQ = base, sP = base + kTile;
-    const std::uint32_t sK[2] = {base + 2 * kTile, base + 3 * kTile};
-    const std::uint32_t sV[2] = {base + 4 * kTile, base + 5 * kTile};
+    // P is double-buffered so the softmax of block j+1 overlaps the P·V MMA of
+    // block j (p_full / o_done are per-buffer barriers: each completes every
+    // other block, so no waiter can fall two phases behind).
+    const std::uint32_t sQ = base;
+    const std::uint32_t sP[2] = {base + kTile, base + 2 * kTile};
+    const std::uint32_t sK[2] = {base + 3 * kTile, base + 4 * kTile};
+    const std::uint32_t sV[2] = {base + 5 * kTile, base + 6 * kTile};
     std::uint8_t* gen_base = smem_raw + (base - raw);
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + 6 * kTile);
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + 7 * kTile);
     const std::uint32_t b0 = smem_u32(bars);
     const std::uint32_t q_full = b0, kv_full = b0 + 8, kv_empty = b0 + 24, s_full = b0 + 40, s_free = b0 + 48,
-                        p_full = b0 + 56, o_done = b0 + 64;
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 10);
+                        p_full = b0 + 56, o_done = b0 + 72;  // p_full[2], o_done[2]
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 12);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     // Heavy (late) query blocks first: blockIdx.x enumerates (qb desc, head).
@@ -82,7 +86,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(s_full, 1);
         mbar_init(s_free, 4);
         mbar_init(p_full, 4);
+        mbar_init(p_full + 8, 4);
         mbar_init(o_done, 1);
+        mbar_init(o_done + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 256);
@@ -123,15 +129,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue_s(0);
             for (int j = 0; j < nkv; ++j) {
                 if (j + 1 < nkv) issue_s(j + 1);
-                mbar_wait(p_full, j & 1);
+                const int pb = j & 1;
+                mbar_wait(p_full + 8 * pb, (j >> 1) & 1);
                 tc_fence_after();
                 const int st = j & 1;
 #pragma unroll
                 for (int kk = 0; kk < kB / 16; ++kk) {
                     const std::uint32_t off = (kk >> 2) * kAtomB + (kk & 3) * 32;
-                    tc_mma(tO, sdesc(sP + off), sdesc(sV[st] + off), idesc, (j | kk) != 0, false);
+                    tc_mma(tO, sdesc(sP[pb] + off), sdesc(sV[st] + off), idesc, (j | kk) != 0, false);
                 }
-                tc_commit(o_done);
+                tc_commit(o_done + 8 * pb);
                 tc_commit(kv_empty + 8 * st);
             }
         }
@@ -176,10 +183,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool grew = mx > m;
             m = mx;
 
-            if (j > 0) {
-                mbar_wait(o_done, (j - 1) & 1);  // P_{j-1}·V done: O stable, P tile free
+            const int pb = j & 1;
+            if (j >= 2) mbar_wait(o_done + 8 * pb, ((j - 2) >> 1) & 1);  // P_{j-2}·V done: buffer pb free
+            if (j > 0 && __any_sync(0xffffffffu, grew)) {
+                mbar_wait(o_done + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1);  // P_{j-1}·V done: O stable
                 tc_fence_after();
-                if (__any_sync(0xffffffffu, grew)) {
+                {
 #pragma unroll 1
                     for (int c = 0; c < kB; c += 32) {
                         std::uint32_t u[32];
@@ -198,17 +207,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) hv[i] = __floats2bfloat162_rn(s[c + 2 * i], s[c + 2 * i + 1]);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(p_chunk_addr(sP, r, c)), "r"(v.x),
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(p_chunk_addr(sP[pb], r, c)), "r"(v.x),
                              "r"(v.y), "r"(v.z), "r"(v.w)
                              : "memory");
             }
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
+            if (lane == 0) mbar_arrive(p_full + 8 * pb);
         }
         // Epilogue: O / l -> bf16 rows of the [seq, heads*hd] output.
-        mbar_wait(o_done, (nkv - 1) & 1);
+        mbar_wait(o_done + 8 * ((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
         tc_fence_after();
         const float inv = 1.0f / l;
         __nv_bfloat16* orow = p.O + static_cast<std::int64_t>(qb * kB + r) * p.ldo + static_cast<std::int64_t>(h) * kHd;
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tmem_free(tmem, 256);
 }
 
-constexpr int kSmem = 6 * kTile + 128 + 1024;
+constexpr int kSmem = 7 * kTile + 128 + 1024;
 
 // --- SIMT fallback (any seq / head dim): one warp per query row, fp32 online
 // softmax over all keys in order. Slow; only for shapes the fused path rejects.
