@@ -164,21 +164,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(s_free);
 
             const bool diag = p.causal && j == qb;
-            float mx = m;
+            // 8 independent max / sum chains (a fixed tree, so still
+            // deterministic): one warp per SMSP cannot hide a 128-long chain.
+            constexpr int kW = 8;
+            float pm[kW];
+#pragma unroll
+            for (int w = 0; w < kW; ++w) pm[w] = m;
 #pragma unroll
             for (int c = 0; c < kB; ++c) {
                 float x = s[c] * p.scale_log2;
                 if (diag && c > r) x = -INFINITY;
                 s[c] = x;
-                mx = fmaxf(mx, x);
+                pm[c % kW] = fmaxf(pm[c % kW], x);
             }
+#pragma unroll
+            for (int w = kW / 2; w > 0; w /= 2)
+#pragma unroll
+                for (int i = 0; i < w; ++i) pm[i] = fmaxf(pm[i], pm[i + w]);
+            const float mx = pm[0];
             const float corr = exp2f(m - mx);  // 0 on the first block (m = -inf)
-            float sum = 0.f;
+            float ps[kW];
+#pragma unroll
+            for (int w = 0; w < kW; ++w) ps[w] = 0.f;
 #pragma unroll
             for (int c = 0; c < kB; ++c) {
                 s[c] = exp2f(s[c] - mx);
-                sum += s[c];
+                ps[c % kW] += s[c];
             }
+#pragma unroll
+            for (int w = kW / 2; w > 0; w /= 2)
+#pragma unroll
+                for (int i = 0; i < w; ++i) ps[i] += ps[i + w];
+            const float sum = ps[0];
             l = l * corr + sum;
             const bool grew = mx > m;
             m = mx;
