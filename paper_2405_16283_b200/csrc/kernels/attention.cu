@@ -166,29 +166,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool diag = p.causal && j == qb;
             // 8 independent max / sum chains (a fixed tree, so still
             // deterministic): one warp per SMSP cannot hide a 128-long chain.
+            // Max is taken on raw scores (scale > 0), then p = 2^(s*scale - m)
+            // is one FFMA + one MUFU.EX2 per element.
             constexpr int kW = 8;
             float pm[kW];
 #pragma unroll
-            for (int w = 0; w < kW; ++w) pm[w] = m;
+            for (int w = 0; w < kW; ++w) pm[w] = -INFINITY;
+            if (diag) {
 #pragma unroll
-            for (int c = 0; c < kB; ++c) {
-                float x = s[c] * p.scale_log2;
-                if (diag && c > r) x = -INFINITY;
-                s[c] = x;
-                pm[c % kW] = fmaxf(pm[c % kW], x);
+                for (int c = 0; c < kB; ++c) {
+                    if (c > r) s[c] = -INFINITY;
+                    pm[c % kW] = fmaxf(pm[c % kW], s[c]);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < kB; ++c) pm[c % kW] = fmaxf(pm[c % kW], s[c]);
             }
 #pragma unroll
             for (int w = kW / 2; w > 0; w /= 2)
 #pragma unroll
                 for (int i = 0; i < w; ++i) pm[i] = fmaxf(pm[i], pm[i + w]);
-            const float mx = pm[0];
-            const float corr = exp2f(m - mx);  // 0 on the first block (m = -inf)
+            const float mx = fmaxf(m, pm[0] * p.scale_log2);
+            const float corr = ex2(m - mx);  // 0 on the first block (m = -inf)
             float ps[kW];
 #pragma unroll
             for (int w = 0; w < kW; ++w) ps[w] = 0.f;
 #pragma unroll
             for (int c = 0; c < kB; ++c) {
-                s[c] = exp2f(s[c] - mx);
+                s[c] = ex2(fmaf(s[c], p.scale_log2, -mx));
                 ps[c % kW] += s[c];
             }
 #pragma unroll
