@@ -420,3 +420,64 @@ def test_lora_step_parity_with_activation_offload():
     assert st2["d2h_bytes"] > 0
     for o in g.outputs():
         assert rel_err(out_values(g, o, res[0][o]), out_values(g, o, want[o])) < 5e-2, g.tensors[o].name
+
+
+def test_executor_rejects_bad_payloads_without_crashing():
+    """Malformed op payloads fail at create time with a MemplanError (code 2),
+    never a device fault: extents are checked against every placement."""
+    from paper_2405_16283_b200.memplan import MemplanError
+    g = W.GraphBuilder()
+    a = g.input("A", (128, 64), "bf16")
+    b = g.input("B", (128, 64), "bf16")
+    g.gemm("C", a, b, 128, 128, 64, out_shape=(128, 128))
+    tj = json.loads(g.to_json())
+    mg, _ = W.plan(g, 1 << 24)
+    bad = json.loads(json.dumps(tj))
+    bad["vertices"][2]["op"]["K"] = 4096  # reads past A's region
+    with pytest.raises(MemplanError, match="exceeds its region") as e:
+        Executor(mg, json.dumps(bad))
+    assert e.value.code == 2
+    bad = json.loads(json.dumps(tj))
+    bad["vertices"][2]["op"]["type"] = "nope"
+    with pytest.raises(MemplanError, match="unknown op type"):
+        Executor(mg, json.dumps(bad))
+    bad = json.loads(json.dumps(tj))
+    del bad["vertices"][2]["op"]
+    with pytest.raises(MemplanError, match="no op payload"):
+        Executor(mg, json.dumps(bad))
+    slot_mg, _ = memplan_build_slot(g)
+    with pytest.raises(MemplanError, match="byte-mode"):
+        Executor(slot_mg, g.to_json())
+
+
+def memplan_build_slot(g):
+    from paper_2405_16283_b200 import memplan
+    return memplan.build_memgraph(g.to_json(), [8], mode="slot")
+
+
+def test_empty_and_input_only_graphs():
+    g = W.GraphBuilder()
+    x = g.input("x", (1000,), "f32", init=("normal", 1.0))  # output = the input itself
+    mg, _ = W.plan(g, 1 << 20)
+    inp = inputs_of(g, seed=70)
+    trace, got = run_gpu(g, mg, inp)
+    assert np.array_equal(out_values(g, x, got[x]), inp[x])
+    assert len(trace["rows"]) == 1
+
+
+def test_executor_reuse_many_runs_and_inputs_update():
+    """One executor, many runs: new input bytes take effect on the next run."""
+    g = W.GraphBuilder()
+    a = g.input("A", (256, 128), "bf16", init=("normal", 1.0))
+    b = g.input("B", (256, 128), "bf16", init=("normal", 1.0))
+    c = g.gemm("C", a, b, 256, 256, 128, out_shape=(256, 256))
+    mg, _ = W.plan(g, 1 << 24)
+    with Executor(mg, g.to_json()) as ex:
+        outs = []
+        for seed in (1, 2, 1):
+            for vid, arr in inputs_of(g, seed=seed).items():
+                ex.set_input(vid, arr)
+            ex.run(trace=False)
+            outs.append(ex.get_output(c, 256 * 256 * 2))
+        assert json.loads(ex.last_trace())["rows"]
+    assert outs[0] == outs[2] and outs[0] != outs[1]
