@@ -1,11 +1,13 @@
 // Fused blockwise causal attention task: for one head and
 // one 128-query block, O = softmax(scale · Q Kᵀ) V with an online softmax over
-// 128-key blocks — the S/P tiles never leave the SM.
+// 64-key blocks — the S/P tiles never leave the SM. 96 KB of smem and 256
+// TMEM columns per CTA, two CTAs per SM.
 //
-//   warp 0     TMA: Q once, then K_j / Vᵀ_j into a 2-stage ring
-//   warp 1     one thread issues tcgen05.mma: S_j = Q·K_jᵀ into TMEM cols
-//              [0,128), O += P_j·V_j into TMEM cols [128,256); S_{j+1} is issued
-//              as soon as the softmax warps have pulled S_j into registers
+//   warp 0     TMA: Q once, then K_j (2-stage ring) and Vᵀ_j
+//   warp 1     one thread issues tcgen05.mma: S_j = Q·K_jᵀ (M=128, N=64) into
+//              TMEM cols [0,64), O += P_j·V_j (M=128, N=128, K=64) into cols
+//              [128,256); S_{j+1} is issued as soon as the softmax warps have
+//              pulled S_j into registers
 //   warps 2-5  softmax/correction, one query row per thread: tcgen05.ld S_j,
 //              running max/sum in fp32 (exp2 with log2e-folded scale), rescale O
 //              in TMEM when the row max grows, P_j as bf16 into a 128B-swizzled
@@ -22,11 +24,15 @@
 namespace tn::k {
 namespace {
 
-constexpr int kB = 128;      // query rows / keys per block
-constexpr int kHd = 128;     // head dim of the fused path
-constexpr int kAtomB = 16384;  // one 128-row x 128-byte swizzle atom
-constexpr int kTile = 2 * kAtomB;  // 128 x 128 bf16 = two atoms along K
+constexpr int kB = 128;          // query rows per CTA
+constexpr int kN = 64;           // keys per KV block
+constexpr int kHd = 128;         // head dim of the fused path
 constexpr int kThreads = 192;
+// smem (bytes): Q 128x128 (2 atoms of 16 KB), K 2 stages x 64x128 (2 atoms of
+// 8 KB each), V 1 stage 128(hd)x64(keys) (1 atom, 16 KB), P 128x64 (1 atom,
+// 16 KB): 96 KB, so two CTAs share an SM and interleave their MMA and
+// softmax phases (the softmax of one hides the MMAs / loads of the other).
+constexpr int kQ = 32768, kKst = 16384, kV = 16384, kP = 16384;
 
 struct AttnParams {
     __nv_bfloat16* O;
@@ -36,59 +42,46 @@ struct AttnParams {
     int causal;
 };
 
-__device__ __forceinline__ void load_tile(std::uint32_t dst, const CUtensorMap* map, int inner0, int row0, int h,
-                                          std::uint32_t bar) {
-    tma_load_3d(dst, map, inner0, row0, h, bar);
-    tma_load_3d(dst + kAtomB, map, inner0 + 64, row0, h, bar);
-}
-
-// P row r, keys [c0, c0+8) as one 16-byte chunk into the swizzled K-major tile.
+// P row r, keys [key, key+8) as one 16-byte chunk of the 128B-swizzled
+// K-major tile (one 64-key atom, rows of 128 bytes).
 __device__ __forceinline__ std::uint32_t p_chunk_addr(std::uint32_t base, int r, int key) {
-    const int atom = key >> 6, chunk = (key & 63) >> 3;
-    return base + atom * kAtomB + r * 128 + ((chunk ^ (r & 7)) << 4);
+    return base + r * 128 + ((((key >> 3) ^ (r & 7))) << 4);
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                      const __grid_constant__ CUtensorMap tv, const AttnParams p) {
     extern __shared__ std::uint8_t smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = (raw + 1023) & ~1023u;
-    // P is double-buffered so the softmax of block j+1 overlaps the P·V MMA of
-    // block j (p_full / o_done are per-buffer barriers: each completes every
-    // other block, so no waiter can fall two phases behind).
-    const std::uint32_t sQ = base;
-    const std::uint32_t sP[2] = {base + kTile, base + 2 * kTile};
-    const std::uint32_t sK[2] = {base + 3 * kTile, base + 4 * kTile};
-    const std::uint32_t sV[2] = {base + 5 * kTile, base + 6 * kTile};
+    const std::uint32_t sQ = base, sK0 = base + kQ, sV = sK0 + 2 * kKst, sP = sV + kV;
     std::uint8_t* gen_base = smem_raw + (base - raw);
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + 7 * kTile);
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + kQ + 2 * kKst + kV + kP);
     const std::uint32_t b0 = smem_u32(bars);
-    const std::uint32_t q_full = b0, kv_full = b0 + 8, kv_empty = b0 + 24, s_full = b0 + 40, s_free = b0 + 48,
-                        p_full = b0 + 56, o_done = b0 + 72;  // p_full[2], o_done[2]
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 12);
+    const std::uint32_t q_full = b0, k_full = b0 + 8, k_empty = b0 + 24, v_full = b0 + 40, v_empty = b0 + 48,
+                        s_full = b0 + 56, s_free = b0 + 64, p_full = b0 + 72, o_done = b0 + 80;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 11);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    // Heavy (late) query blocks first: blockIdx.x enumerates (qb desc, head).
     const int h = blockIdx.x % p.heads;
-    const int qb = p.nblk - 1 - static_cast<int>(blockIdx.x / p.heads);
-    const int nkv = p.causal ? qb + 1 : p.nblk;
+    const int qb = p.nblk - 1 - static_cast<int>(blockIdx.x / p.heads);  // heavy blocks first
+    const int nkv = p.causal ? (qb + 1) * (kB / kN) : p.nblk * (kB / kN);
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tq)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tk)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tv)) : "memory");
         mbar_init(q_full, 1);
-        mbar_init(kv_full, 1);
-        mbar_init(kv_full + 8, 1);
-        mbar_init(kv_empty, 1);
-        mbar_init(kv_empty + 8, 1);
+        mbar_init(k_full, 1);
+        mbar_init(k_full + 8, 1);
+        mbar_init(k_empty, 1);
+        mbar_init(k_empty + 8, 1);
+        mbar_init(v_full, 1);
+        mbar_init(v_empty, 1);
         mbar_init(s_full, 1);
         mbar_init(s_free, 4);
         mbar_init(p_full, 4);
-        mbar_init(p_full + 8, 4);
         mbar_init(o_done, 1);
-        mbar_init(o_done + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 256);
@@ -96,63 +89,69 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const std::uint32_t tmem = *tmem_slot;
-    const std::uint32_t tS = tmem, tO = tmem + 128;
+    const std::uint32_t tS = tmem, tO = tmem + 128;  // S uses 64 columns
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(q_full, kTile);
-            load_tile(sQ, &tq, 0, qb * kB, h, q_full);
+            mbar_expect_tx(q_full, kQ);
+            tma_load_3d(sQ, &tq, 0, qb * kB, h, q_full);
+            tma_load_3d(sQ + kQ / 2, &tq, 64, qb * kB, h, q_full);
             for (int j = 0; j < nkv; ++j) {
                 const int st = j & 1;
-                mbar_wait(kv_empty + 8 * st, ((j >> 1) & 1) ^ 1);
-                mbar_expect_tx(kv_full + 8 * st, 2 * kTile);
-                load_tile(sK[st], &tk, 0, j * kB, h, kv_full + 8 * st);
-                load_tile(sV[st], &tv, j * kB, 0, h, kv_full + 8 * st);
+                mbar_wait(k_empty + 8 * st, ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(k_full + 8 * st, kKst);
+                const std::uint32_t dk = sK0 + st * kKst;
+                tma_load_3d(dk, &tk, 0, j * kN, h, k_full + 8 * st);
+                tma_load_3d(dk + kKst / 2, &tk, 64, j * kN, h, k_full + 8 * st);
+                mbar_wait(v_empty, (j & 1) ^ 1);
+                mbar_expect_tx(v_full, kV);
+                tma_load_3d(sV, &tv, j * kN, 0, h, v_full);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const std::uint32_t idesc = make_idesc(1u, kB, kB);
+            const std::uint32_t idesc_s = make_idesc(1u, kB, kN);
+            const std::uint32_t idesc_o = make_idesc(1u, kB, kHd);
             auto issue_s = [&](int j) {
                 const int st = j & 1;
-                mbar_wait(kv_full + 8 * st, (j >> 1) & 1);
-                if (j > 0) mbar_wait(s_free, (j - 1) & 1);  // softmax pulled S_{j-1}
+                mbar_wait(k_full + 8 * st, (j >> 1) & 1);
+                if (j > 0) mbar_wait(s_free, (j - 1) & 1);  // softmax pulled S_{j-1} into registers
                 tc_fence_after();
+                const std::uint32_t dk = sK0 + st * kKst;
 #pragma unroll
-                for (int kk = 0; kk < kHd / 16; ++kk) {
-                    const std::uint32_t off = (kk >> 2) * kAtomB + (kk & 3) * 32;
-                    tc_mma(tS, sdesc(sQ + off), sdesc(sK[st] + off), idesc, kk != 0, false);
-                }
+                for (int kk = 0; kk < kHd / 16; ++kk)
+                    tc_mma(tS, sdesc(sQ + (kk >> 2) * (kQ / 2) + (kk & 3) * 32),
+                           sdesc(dk + (kk >> 2) * (kKst / 2) + (kk & 3) * 32), idesc_s, kk != 0, false);
                 tc_commit(s_full);
+                tc_commit(k_empty + 8 * st);
             };
             mbar_wait(q_full, 0);
             issue_s(0);
             for (int j = 0; j < nkv; ++j) {
                 if (j + 1 < nkv) issue_s(j + 1);
-                const int pb = j & 1;
-                mbar_wait(p_full + 8 * pb, (j >> 1) & 1);
+                mbar_wait(p_full, j & 1);
+                mbar_wait(v_full, j & 1);
                 tc_fence_after();
-                const int st = j & 1;
 #pragma unroll
-                for (int kk = 0; kk < kB / 16; ++kk) {
-                    const std::uint32_t off = (kk >> 2) * kAtomB + (kk & 3) * 32;
-                    tc_mma(tO, sdesc(sP[pb] + off), sdesc(sV[st] + off), idesc, (j | kk) != 0, false);
-                }
-                tc_commit(o_done + 8 * pb);
-                tc_commit(kv_empty + 8 * st);
+                for (int kk = 0; kk < kN / 16; ++kk)
+                    tc_mma(tO, sdesc(sP + kk * 32), sdesc(sV + kk * 32), idesc_o, (j | kk) != 0, false);
+                tc_commit(o_done);
+                tc_commit(v_empty);
             }
         }
     } else {
         const int lane_base = (warp % 4) * 32;
         const int r = lane_base + lane;  // query row within the block
+        const int qrow = qb * kB + r;
         const std::uint32_t trow = static_cast<std::uint32_t>(lane_base) << 16;
         float m = -INFINITY, l = 0.f;
+        constexpr int kW = 8;
         for (int j = 0; j < nkv; ++j) {
             mbar_wait(s_full, j & 1);
             tc_fence_after();
-            float s[kB];
+            float s[kN];
 #pragma unroll
-            for (int c = 0; c < kB; c += 32) {
+            for (int c = 0; c < kN; c += 32) {
                 std::uint32_t u[32];
                 TN_LD32(tS + trow + c, u);
 #pragma unroll
@@ -163,36 +162,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(s_free);
 
-            const bool diag = p.causal && j == qb;
-            // 8 independent max / sum chains (a fixed tree, so still
-            // deterministic): one warp per SMSP cannot hide a 128-long chain.
-            // Max is taken on raw scores (scale > 0), then p = 2^(s*scale - m)
-            // is one FFMA + one MUFU.EX2 per element.
-            constexpr int kW = 8;
+            // masked keys: key index j*kN + c > query row (causal)
+            const int lim = p.causal ? qrow - j * kN : kN;  // keys c <= lim are valid
             float pm[kW];
 #pragma unroll
             for (int w = 0; w < kW; ++w) pm[w] = -INFINITY;
-            if (diag) {
+            if (lim < kN - 1) {
 #pragma unroll
-                for (int c = 0; c < kB; ++c) {
-                    if (c > r) s[c] = -INFINITY;
+                for (int c = 0; c < kN; ++c) {
+                    if (c > lim) s[c] = -INFINITY;
                     pm[c % kW] = fmaxf(pm[c % kW], s[c]);
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < kB; ++c) pm[c % kW] = fmaxf(pm[c % kW], s[c]);
+                for (int c = 0; c < kN; ++c) pm[c % kW] = fmaxf(pm[c % kW], s[c]);
             }
 #pragma unroll
             for (int w = kW / 2; w > 0; w /= 2)
 #pragma unroll
                 for (int i = 0; i < w; ++i) pm[i] = fmaxf(pm[i], pm[i + w]);
-            const float mx = fmaxf(m, pm[0] * p.scale_log2);
-            const float corr = ex2(m - mx);  // 0 on the first block (m = -inf)
+            const float mx = fmaxf(m, pm[0] * p.scale_log2);  // a fully masked block keeps m
+            const float corr = ex2(m - mx);
             float ps[kW];
 #pragma unroll
             for (int w = 0; w < kW; ++w) ps[w] = 0.f;
 #pragma unroll
-            for (int c = 0; c < kB; ++c) {
+            for (int c = 0; c < kN; ++c) {
                 s[c] = ex2(fmaf(s[c], p.scale_log2, -mx));
                 ps[c % kW] += s[c];
             }
@@ -200,19 +195,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int w = kW / 2; w > 0; w /= 2)
 #pragma unroll
                 for (int i = 0; i < w; ++i) ps[i] += ps[i + w];
-            const float sum = ps[0];
-            l = l * corr + sum;
+            l = l * corr + ps[0];
             const bool grew = mx > m;
             m = mx;
 
-            const int pb = j & 1;
-            if (j >= 2) mbar_wait(o_done + 8 * pb, ((j - 2) >> 1) & 1);  // P_{j-2}·V done: buffer pb free
-            if (j > 0 && __any_sync(0xffffffffu, grew)) {
-                mbar_wait(o_done + 8 * ((j - 1) & 1), ((j - 1) >> 1) & 1);  // P_{j-1}·V done: O stable
+            if (j > 0) {
+                mbar_wait(o_done, (j - 1) & 1);  // P_{j-1}·V done: O stable, P tile free
                 tc_fence_after();
-                {
+                if (__any_sync(0xffffffffu, grew)) {
 #pragma unroll 1
-                    for (int c = 0; c < kB; c += 32) {
+                    for (int c = 0; c < kHd; c += 32) {
                         std::uint32_t u[32];
                         TN_LD32(tO + trow + c, u);
                         tc_wait_ld();
@@ -224,25 +216,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
 #pragma unroll
-            for (int c = 0; c < kB; c += 8) {
+            for (int c = 0; c < kN; c += 8) {
                 uint4 v;
                 __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) hv[i] = __floats2bfloat162_rn(s[c + 2 * i], s[c + 2 * i + 1]);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(p_chunk_addr(sP[pb], r, c)), "r"(v.x),
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(p_chunk_addr(sP, r, c)), "r"(v.x),
                              "r"(v.y), "r"(v.z), "r"(v.w)
                              : "memory");
             }
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full + 8 * pb);
+            if (lane == 0) mbar_arrive(p_full);
         }
         // Epilogue: O / l -> bf16 rows of the [seq, heads*hd] output.
-        mbar_wait(o_done + 8 * ((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
+        mbar_wait(o_done, (nkv - 1) & 1);
         tc_fence_after();
         const float inv = 1.0f / l;
-        __nv_bfloat16* orow = p.O + static_cast<std::int64_t>(qb * kB + r) * p.ldo + static_cast<std::int64_t>(h) * kHd;
+        __nv_bfloat16* orow = p.O + static_cast<std::int64_t>(qrow) * p.ldo + static_cast<std::int64_t>(h) * kHd;
 #pragma unroll 1
         for (int c = 0; c < kHd; c += 32) {
             std::uint32_t u[32];
@@ -267,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tmem_free(tmem, 256);
 }
 
-constexpr int kSmem = 7 * kTile + 128 + 1024;
+constexpr int kSmem = kQ + 2 * kKst + kV + kP + 128 + 1024;
 
 // --- SIMT fallback (any seq / head dim): one warp per query row, fp32 online
 // softmax over all keys in order. Slow; only for shapes the fused path rejects.
@@ -314,7 +306,7 @@ cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan) {
         ok = encode_tma_3d(&plan->tq, a.q, 2, a.hd, a.seq, a.hd, a.heads, static_cast<std::int64_t>(a.seq) * a.hd, 64,
                            kB) &&
              encode_tma_3d(&plan->tk, a.k, 2, a.hd, a.seq, a.hd, a.heads, static_cast<std::int64_t>(a.seq) * a.hd, 64,
-                           kB) &&
+                           kN) &&
              encode_tma_3d(&plan->tv, a.vt, 2, a.seq, a.hd, a.seq, a.heads, static_cast<std::int64_t>(a.seq) * a.hd, 64,
                            kHd);
     plan->path = ok ? 0 : 1;
