@@ -29,9 +29,11 @@ constexpr int kN = 64;           // keys per KV block
 constexpr int kHd = 128;         // head dim of the fused path
 constexpr int kThreads = 192;
 // smem (bytes): Q 128x128 (2 atoms of 16 KB), K 2 stages x 64x128 (2 atoms of
-// 8 KB each), V 1 stage 128(hd)x64(keys) (1 atom, 16 KB), P 128x64 (1 atom,
-// 16 KB): 96 KB, so two CTAs share an SM and interleave their MMA and
+// 8 KB each), V 2 stages x 128(hd)x64(keys) (1 atom, 16 KB), P 128x64 (1 atom,
+// 16 KB): 112 KB, so two CTAs share an SM and interleave their MMA and
 // softmax phases (the softmax of one hides the MMAs / loads of the other).
+// Two CTAs only fit without alignment slack: the dynamic window starts on a
+// 1 KB boundary (the per-CTA system reservation precedes it), checked below.
 constexpr int kQ = 32768, kKst = 16384, kV = 16384, kP = 16384;
 
 struct AttnParams {
@@ -53,14 +55,15 @@ __global__ void __launch_bounds__(kThreads, 2)
                      const __grid_constant__ CUtensorMap tv, const AttnParams p) {
     extern __shared__ std::uint8_t smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
-    const std::uint32_t base = (raw + 1023) & ~1023u;
-    const std::uint32_t sQ = base, sK0 = base + kQ, sV = sK0 + 2 * kKst, sP = sV + kV;
+    if (raw & 1023u) __trap();  // SW128 tiles need 1 KB alignment
+    const std::uint32_t base = raw;
+    const std::uint32_t sQ = base, sK0 = base + kQ, sV = sK0 + 2 * kKst, sP = sV + 2 * kV;
     std::uint8_t* gen_base = smem_raw + (base - raw);
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + kQ + 2 * kKst + kV + kP);
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + kQ + 2 * kKst + 2 * kV + kP);
     const std::uint32_t b0 = smem_u32(bars);
-    const std::uint32_t q_full = b0, k_full = b0 + 8, k_empty = b0 + 24, v_full = b0 + 40, v_empty = b0 + 48,
-                        s_full = b0 + 56, s_free = b0 + 64, p_full = b0 + 72, o_done = b0 + 80;
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 11);
+    const std::uint32_t q_full = b0, k_full = b0 + 8, k_empty = b0 + 24, v_full = b0 + 40, v_empty = b0 + 56,
+                        s_full = b0 + 72, s_free = b0 + 80, p_full = b0 + 88, o_done = b0 + 96;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 13);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int h = blockIdx.x % p.heads;
@@ -77,7 +80,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(k_empty, 1);
         mbar_init(k_empty + 8, 1);
         mbar_init(v_full, 1);
+        mbar_init(v_full + 8, 1);
         mbar_init(v_empty, 1);
+        mbar_init(v_empty + 8, 1);
         mbar_init(s_full, 1);
         mbar_init(s_free, 4);
         mbar_init(p_full, 4);
@@ -103,9 +108,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const std::uint32_t dk = sK0 + st * kKst;
                 tma_load_3d(dk, &tk, 0, j * kN, h, k_full + 8 * st);
                 tma_load_3d(dk + kKst / 2, &tk, 64, j * kN, h, k_full + 8 * st);
-                mbar_wait(v_empty, (j & 1) ^ 1);
-                mbar_expect_tx(v_full, kV);
-                tma_load_3d(sV, &tv, j * kN, 0, h, v_full);
+                mbar_wait(v_empty + 8 * st, ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(v_full + 8 * st, kV);
+                tma_load_3d(sV + st * kV, &tv, j * kN, 0, h, v_full + 8 * st);
             }
         }
     } else if (warp == 1) {
@@ -130,13 +135,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int j = 0; j < nkv; ++j) {
                 if (j + 1 < nkv) issue_s(j + 1);
                 mbar_wait(p_full, j & 1);
-                mbar_wait(v_full, j & 1);
+                mbar_wait(v_full + 8 * (j & 1), (j >> 1) & 1);
                 tc_fence_after();
+                const std::uint32_t dv = sV + (j & 1) * kV;
 #pragma unroll
                 for (int kk = 0; kk < kN / 16; ++kk)
-                    tc_mma(tO, sdesc(sP + kk * 32), sdesc(sV + kk * 32), idesc_o, (j | kk) != 0, false);
+                    tc_mma(tO, sdesc(sP + kk * 32), sdesc(dv + kk * 32), idesc_o, (j | kk) != 0, false);
                 tc_commit(o_done);
-                tc_commit(v_empty);
+                tc_commit(v_empty + 8 * (j & 1));
             }
         }
     } else {
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (warp == 1) tmem_free(tmem, 256);
 }
 
-constexpr int kSmem = kQ + 2 * kKst + kV + kP + 128 + 1024;
+constexpr int kSmem = kQ + 2 * kKst + 2 * kV + kP + 128;
 
 // --- SIMT fallback (any seq / head dim): one warp per query row, fp32 online
 // softmax over all keys in order. Slow; only for shapes the fused path rejects.
