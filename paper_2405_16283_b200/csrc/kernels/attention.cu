@@ -187,7 +187,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int w = kW / 2; w > 0; w /= 2)
 #pragma unroll
                 for (int i = 0; i < w; ++i) pm[i] = fmaxf(pm[i], pm[i + w]);
-            const float mx = fmaxf(m, pm[0] * p.scale_log2);  // a fully masked block keeps m
+            // Lazy rescale: the running max only moves (and O is only
+            // rescaled) when the block max exceeds it by more than 2^8, so
+            // P <= 256 stays well inside bf16/fp32 range and most blocks skip
+            // the TMEM read-modify-write of O. Final O / l is unchanged.
+            const float cand = fmaxf(m, pm[0] * p.scale_log2);  // a fully masked block keeps m
+            const bool grew = cand > m + 8.0f;
+            const float mx = grew ? cand : m;
             const float corr = ex2(m - mx);
             float ps[kW];
 #pragma unroll
@@ -202,7 +208,6 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int i = 0; i < w; ++i) ps[i] += ps[i + w];
             l = l * corr + ps[0];
-            const bool grew = mx > m;
             m = mx;
 
             if (j > 0) {
