@@ -75,6 +75,7 @@ struct Executor::Impl {
     std::vector<int> num_sms;
     std::vector<char*> arena;       // per logical device
     std::vector<std::vector<cudaStream_t>> streams;
+    std::vector<cudaStream_t> marker;  // per logical device: timestamps of instant vertices
     std::vector<cudaEvent_t> t0;    // per logical device
     std::vector<cudaEvent_t> ev_start, ev_end;  // per memgraph vertex index
 
@@ -82,6 +83,8 @@ struct Executor::Impl {
     std::unordered_map<VertexId, HostBuf> inputs;  // taskgraph input id -> pinned bytes
     std::unordered_map<VertexId, HostBuf> staged;  // input id -> HBM staging copy (device residency)
     std::unordered_map<VertexId, HostBuf> slots;   // evicted root id -> pinned slot
+    std::unordered_map<VertexId, char*> alias;     // Input mem id -> its staging copy (aliased inputs)
+    bool aliased_inputs() const { return cfg.inputs_on_device && cfg.alias_device_inputs; }
 
     // --- per-vertex launch programs ------------------------------------------------
     struct Instr {
@@ -94,6 +97,7 @@ struct Executor::Impl {
         std::size_t bytes = 0;
         VertexId input_id = -1;   // Input vertices, and offload/reload of an evicted input root
         bool elided = false;      // offload of an unmodified input: no copy
+        bool instant = false;     // aliased Input: completes at dispatch, no stream, no copy
         const OpDesc* op_desc = nullptr;
         std::vector<const char*> argp;  // resolved argument pointers
         std::unique_ptr<k::GemmPlan> gemm;
@@ -128,6 +132,10 @@ struct Executor::Impl {
     }
 
     char* ptr_of(VertexId mem_id) {
+        if (!alias.empty()) {
+            auto a = alias.find(mem_id);
+            if (a != alias.end()) return a->second;
+        }
         auto it = map.placements.find(mem_id);
         if (it == map.placements.end())
             throw Error("memgraph vertex " + std::to_string(mem_id) + " has no placement");
@@ -171,6 +179,7 @@ void Executor::Impl::build() {
     num_sms.resize(D);
     arena.assign(D, nullptr);
     streams.resize(D);
+    marker.assign(D, nullptr);
     t0.resize(D);
     for (int d = 0; d < D; ++d) {
         set_device(d);
@@ -178,6 +187,7 @@ void Executor::Impl::build() {
         TN_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena[d]), std::max<std::int64_t>(map.capacities[d], 256)));
         streams[d].resize(cfg.streams_per_device);
         for (auto& s : streams[d]) TN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        TN_CUDA(cudaStreamCreateWithFlags(&marker[d], cudaStreamNonBlocking));
         // One time origin per physical GPU: memgraph devices that share a GPU
         // share t0, so cross-device edges compare on one clock.
         int first = d;
@@ -219,6 +229,21 @@ void Executor::Impl::build() {
             throw Error("placement of " + std::to_string(id) + " exceeds its device arena");
     }
 
+    // Aliased device inputs: one HBM staging buffer per input, sized to its
+    // placement (tail zeroed), allocated up front so every reader's pointer
+    // (and TMA descriptor) is fixed at build time; tn_exec_set_input fills it.
+    if (aliased_inputs()) {
+        for (const auto& v : m.vertices) {
+            if (v.op != MemOpKind::Input) continue;
+            HostBuf& b = staged[v.origin.ref];
+            set_device(v.device);
+            b.bytes = static_cast<std::size_t>(std::max<std::int64_t>(size_of(v.id), 1));
+            TN_CUDA(cudaMalloc(&b.p, b.bytes));
+            TN_CUDA(cudaMemset(b.p, 0, b.bytes));
+            alias[v.id] = static_cast<char*>(b.p);
+        }
+    }
+
     const size_t V = m.vertices.size();
     prog.resize(V);
     cb.resize(V);
@@ -240,6 +265,7 @@ void Executor::Impl::build() {
                 in.dst = ptr_of(v.id);
                 in.bytes = static_cast<std::size_t>(size_of(v.id));
                 in.input_id = v.origin.ref;
+                in.instant = aliased_inputs();
                 break;
             }
             case MemOpKind::Offload: {
@@ -515,11 +541,12 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
 void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t after) {
     Instr& in = prog[vidx];
     set_device(in.dev);
-    cudaStream_t s = streams[in.dev][stream < 0 ? 0 : stream];  // inputs hold no stream when not materialised
+    cudaStream_t s = in.instant ? marker[in.dev] : streams[in.dev][stream < 0 ? 0 : stream];  // inputs hold no stream when not materialised
     if (after >= 0) TN_CUDA(cudaStreamWaitEvent(s, ev_end[after], 0));  // lookahead: run behind `after`
     TN_CUDA(cudaEventRecord(ev_start[vidx], s));
     switch (in.op) {
         case MemOpKind::Input: {
+            if (in.instant) break;  // readers use the staging copy in place
             if (cfg.inputs_on_device) {
                 auto it = staged.find(in.input_id);
                 if (it == staged.end() || !it->second.p)
@@ -673,7 +700,8 @@ class CudaBackend {
         x_.dispatched.push_back(vidx);
         x_.stream_of[vidx] = stream;
         in_flight_++;
-        if (x_.cfg.poll) flying_.push_back(vidx);
+        if (x_.prog[vidx].instant) instant_.push_back(vidx);
+        else if (x_.cfg.poll) flying_.push_back(vidx);
     }
     void launch_after(std::int32_t vidx, std::int32_t stream, std::int32_t after, double) {
         x_.launch(vidx, stream, after);
@@ -684,6 +712,13 @@ class CudaBackend {
     }
     bool idle() const { return in_flight_ == 0; }
     std::int32_t wait_next(double& now) {
+        if (!instant_.empty()) {  // aliased inputs complete at dispatch
+            const std::int32_t v = instant_.front();
+            instant_.pop_front();
+            in_flight_--;
+            now = std::chrono::duration<double>(std::chrono::steady_clock::now() - start_).count();
+            return v;
+        }
         if (x_.cfg.poll) return poll_next(now);
         std::unique_lock<std::mutex> lk(x_.mu);
         if (x_.completed.empty()) {
@@ -727,6 +762,7 @@ class CudaBackend {
     std::chrono::steady_clock::time_point start_;
     int in_flight_ = 0;
     std::vector<std::int32_t> flying_;
+    std::deque<std::int32_t> instant_;
 };
 
 }  // namespace
@@ -753,8 +789,8 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
     }
     auto wall0 = std::chrono::steady_clock::now();
     const bool chain = cfg.lookahead > 0 && cfg.compute_tokens == 1;
-    Resources res(D, cfg.streams_per_device, chain ? (1 << 30) : cfg.compute_tokens, cfg.materialize_inputs,
-                  !cfg.inputs_on_device);
+    Resources res(D, cfg.streams_per_device, chain ? (1 << 30) : cfg.compute_tokens,
+                  cfg.materialize_inputs && !aliased_inputs(), !cfg.inputs_on_device);
     ReadyList ready(pol.tie_break, seed);
     CudaBackend be(*this);
     try {
@@ -851,6 +887,8 @@ Executor::Impl::~Impl() {
     for (auto& ss : streams)
         for (auto s : ss)
             if (s) cudaStreamDestroy(s);
+    for (auto s : marker)
+        if (s) cudaStreamDestroy(s);
     for (auto p : arena)
         if (p) cudaFree(p);
     for (auto& [id, b] : inputs)
@@ -885,6 +923,13 @@ void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool 
     if (bytes > static_cast<std::size_t>(v->output_size))
         throw Error("input " + std::to_string(id) + ": " + std::to_string(bytes) + " bytes exceed output_size " +
                     std::to_string(v->output_size));
+    if (impl_->aliased_inputs()) {
+        HostBuf& b = impl_->staged.at(id);  // fixed at build: readers hold its address
+        if (bytes > b.bytes) throw Error("input " + std::to_string(id) + " exceeds its placement");
+        impl_->set_device(v->device);
+        TN_CUDA(cudaMemcpy(b.p, host, bytes, from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+        return;
+    }
     if (impl_->cfg.inputs_on_device) {
         HostBuf& b = impl_->staged[id];
         impl_->set_device(v->device);
@@ -924,7 +969,7 @@ void Executor::get_output(VertexId id, void* host, std::size_t bytes) {
     if (bytes > static_cast<std::size_t>(it->second.size))
         throw Error("requested " + std::to_string(bytes) + " bytes from a region of " + std::to_string(it->second.size));
     impl_->set_device(it->second.device);
-    TN_CUDA(cudaMemcpy(host, impl_->arena[it->second.device] + it->second.offset, bytes, cudaMemcpyDeviceToHost));
+    TN_CUDA(cudaMemcpy(host, impl_->ptr_of(id), bytes, cudaMemcpyDeviceToHost));
 }
 
 void* Executor::placement_ptr(VertexId id) { return impl_->ptr_of(id); }
@@ -969,6 +1014,9 @@ ExecConfig parse_exec_config(const std::string& text) {
         const std::string res = j.value("input_residency", std::string("host"));
         if (res != "host" && res != "device") throw ParseError("input_residency must be host or device");
         c.inputs_on_device = res == "device";
+        const std::string di = j.value("device_inputs", std::string("alias"));
+        if (di != "alias" && di != "copy") throw ParseError("device_inputs must be alias or copy");
+        c.alias_device_inputs = di == "alias";
     } catch (const json::exception& e) {
         throw ParseError(std::string("invalid executor config: ") + e.what());
     }

@@ -25,6 +25,10 @@ struct ExecConfig {
                                        // reload from the input's own host (or HBM staging) copy
     bool poll = true;                // "completion": "poll" (spin on cudaEventQuery) | "callback"
                                      // (cudaLaunchHostFunc -> queue -> condition variable)
+    bool alias_device_inputs = true;  // "device_inputs": "alias" -> with device residency the
+                                      // Input vertex is zero-cost (reference: simulator.cpp:66-67):
+                                      // generation-0 readers use the HBM staging copy in place;
+                                      // "copy" -> a D2D copy into the placement at dispatch
 };
 ExecConfig parse_exec_config(const std::string& text);
 
