@@ -76,6 +76,7 @@ struct Executor::Impl {
     std::vector<char*> arena;       // per logical device
     std::vector<std::vector<cudaStream_t>> streams;
     std::vector<cudaStream_t> marker;  // per logical device: timestamps of instant vertices
+    std::vector<std::vector<k::GemmWorkspace>> gws;  // per device x stream: stream-K GEMM scratch
     std::vector<cudaEvent_t> t0;    // per logical device
     std::vector<cudaEvent_t> ev_start, ev_end;  // per memgraph vertex index
 
@@ -312,6 +313,21 @@ void Executor::Impl::build() {
             if (prog[i].input_id >= 0 && m.vertices[i].op != MemOpKind::Input) slots.erase(m.vertices[i].origin.ref);
     }
     for (auto& [root, s] : slots) s.p = pinned_alloc(s.bytes);
+    // Stream-K GEMM scratch, one per stream of each device (sized to the
+    // largest plan on that device).
+    gws.assign(D, std::vector<k::GemmWorkspace>(cfg.streams_per_device));
+    for (int d = 0; d < D; ++d) {
+        std::size_t need = 0;
+        for (size_t i = 0; i < V; ++i)
+            if (prog[i].gemm && prog[i].dev == d) need = std::max(need, prog[i].gemm->ws_bytes);
+        if (!need) continue;
+        set_device(d);
+        for (auto& w : gws[d]) {
+            TN_CUDA(cudaMalloc(&w.p, need));
+            TN_CUDA(cudaMemset(w.p, 0, need));
+            w.bytes = need;
+        }
+    }
     for (size_t i = 0; i < V; ++i) {
         const MemVertex& v = m.vertices[i];
         if ((v.op == MemOpKind::Offload || v.op == MemOpKind::Reload) && prog[i].input_id < 0)
@@ -366,6 +382,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             const std::int64_t n_out = op.epilogue == 1 ? op.N / 2 : op.N;
             g.ldc = op.ldc ? op.ldc : n_out;
             g.epi = op.epilogue;
+            g.tile = op.tile;
             if (op.epilogue == 1 && (op.N % 256 != 0 || op.args.size() != 2))
                 throw Error("gemm swiglu epilogue needs N % 256 == 0 and no residual");
             if (op.epilogue == 2 && (op.N != 3 * op.heads * 128 || op.args.size() != 3 || op.batch != 1))
@@ -600,7 +617,7 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
             const auto& a = in.argp;
             switch (op.type) {
                 case OpType::Gemm:
-                    TN_CUDA(k::gemm_launch(*in.gemm, s));
+                    TN_CUDA(k::gemm_launch(*in.gemm, s, &gws[in.dev][stream < 0 ? 0 : stream]));
                     last.flops += k::gemm_flops(in.gemm->args);
                     break;
                 case OpType::RmsNorm:
@@ -889,6 +906,9 @@ Executor::Impl::~Impl() {
             if (s) cudaStreamDestroy(s);
     for (auto s : marker)
         if (s) cudaStreamDestroy(s);
+    for (auto& ws : gws)
+        for (auto& w : ws)
+            if (w.p) cudaFree(w.p);
     for (auto p : arena)
         if (p) cudaFree(p);
     for (auto& [id, b] : inputs)

@@ -122,6 +122,11 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
                 else if (ep == "swiglu") d.epilogue = 1;
                 else if (ep == "qkv_rope") d.epilogue = 2;
                 else throw ParseError("unknown gemm epilogue '" + ep + "'");
+                const std::string tl = o.value("tile", std::string("auto"));
+                if (tl == "auto") d.tile = 0;
+                else if (tl == "narrow") d.tile = 1;
+                else if (tl == "wide") d.tile = 2;
+                else throw ParseError("gemm tile must be auto, narrow or wide");
             }
             d.in_dtype = dtype_of(o.value("in_dtype", std::string("bf16")));
             d.out_dtype = dtype_of(o.value("out_dtype", std::string("bf16")));

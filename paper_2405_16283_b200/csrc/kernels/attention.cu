@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // whole warp: one elected lane issues (tc_mma)
             const std::uint32_t idesc_s = make_idesc(1u, kB, kN);
             const std::uint32_t idesc_o = make_idesc(1u, kB, kHd);
             auto issue_s = [&](int j) {

@@ -45,6 +45,16 @@ struct Params {
     int epi;  // 0 plain, 1 swiglu (out[:, 128b + j] = silu(C[:, 256b + j]) * C[:, 256b + 128 + j]), 2 qkv_rope
     const float* rope;  // qkv_rope: [seq, 64, 2] (cos, sin)
     int heads;          // qkv_rope: heads per q/k/v section (hd = 128)
+    // Stream-K tail (CTA-pair kernel): tiles [0, dp_tiles) go round-robin to
+    // the pairs; the K blocks of the remaining tiles are split evenly across
+    // all pairs (sk_total = sk_tiles * sk_nk blocks). Partial accumulators go
+    // to ws (one 256x256 fp32 slot per pair) and are summed by the pair that
+    // owns a tile's first K block, in ascending pair order (deterministic).
+    int dp_tiles, sk_nk;
+    long long sk_total;
+    float* ws;
+    unsigned* flags;  // per CTA of each pair: epoch of its last published partial
+    unsigned epoch;
 };
 
 __device__ __forceinline__ bool tile_skipped(const Params& p, int mb, int nb, int bn) {
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // whole warp: one elected lane issues (tc_mma)
             const std::uint32_t fmt = tf32 ? 2u : 1u;
             const std::uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                                         (static_cast<std::uint32_t>(BN >> 3) << 17) |
@@ -421,21 +431,59 @@ __device__ __forceinline__ void tc_mma_2sm(std::uint32_t d, std::uint64_t a, std
                                            std::uint32_t accum, bool tf32) {
     if (tf32) {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
             "l"(a), "l"(b), "r"(idesc), "r"(accum)
             : "memory");
     } else {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
             "l"(a), "l"(b), "r"(idesc), "r"(accum)
             : "memory");
     }
 }
+__device__ __forceinline__ long long sk_begin(const Params& p, int q, int npairs) {
+    return p.sk_total * q / npairs;
+}
+// Pair owning stream-K block `it`: largest q with sk_begin(q) <= it.
+__device__ __forceinline__ int sk_owner(const Params& p, long long it, int npairs) {
+    int q = static_cast<int>(it * npairs / max(1LL, p.sk_total));
+    while (q + 1 < npairs && sk_begin(p, q + 1, npairs) <= it) ++q;
+    while (q > 0 && sk_begin(p, q, npairs) > it) --q;
+    return q;
+}
+// Visits this pair's work as (tile, K-block range) segments: its round-robin
+// data-parallel tiles, then its contiguous slice of the stream-K blocks.
+template <class F>
+__device__ __forceinline__ void for_each_segment(const Params& p, int pair, int npairs, int bk, F&& f) {
+    constexpr int BN = 256, BM2 = 256;
+    for (int t = pair; t < p.dp_tiles; t += npairs) {
+        int b, mb, nb;
+        decode(p, t, b, mb, nb);
+        if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
+        int nk = (p.K + bk - 1) / bk;
+        if (p.causal == 2) nk = min(nk, ((mb + 1) * BM2 + bk - 1) / bk);
+        f(b, mb, nb, 0, nk, nk, 0LL);
+    }
+    if (p.sk_total <= 0) return;
+    const long long end = sk_begin(p, pair + 1, npairs);
+    for (long long it = sk_begin(p, pair, npairs); it < end;) {
+        const int tt = p.dp_tiles + static_cast<int>(it / p.sk_nk);
+        const int kb0 = static_cast<int>(it % p.sk_nk);
+        const int kb1 = static_cast<int>(min(static_cast<long long>(p.sk_nk), kb0 + (end - it)));
+        int b, mb, nb;
+        decode(p, tt, b, mb, nb);
+        f(b, mb, nb, kb0, kb1, p.sk_nk, it - kb0);
+        it += kb1 - kb0;
+    }
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 __device__ __forceinline__ void tc_commit_2sm(std::uint32_t bar) {
     asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
         "h"(static_cast<unsigned short>(3))
         : "memory");
 }
@@ -466,7 +514,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool leader = rank == 0;
     const int bk = kAtom / p.in_bytes;
     const bool tf32 = p.in_bytes == 4;
-    const int tiles = p.batch * p.tiles_m * p.tiles_n;  // tiles_m counts 256-row pair tiles
     const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
 
     if (warp == 0 && lane == 0) {
@@ -499,13 +546,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             std::uint32_t phase = 0;
-            for (int t = pair; t < tiles; t += npairs) {
-                int b, mb, nb;
-                decode(p, t, b, mb, nb);
-                if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
-                int nk = (p.K + bk - 1) / bk;
-                if (p.causal == 2) nk = min(nk, ((mb + 1) * BM2 + bk - 1) / bk);
-                for (int kb = 0; kb < nk; ++kb) {
+            for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int nb, int kb0, int kb1, int, long long) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty + 8 * stage, phase ^ 1);
                     const std::uint32_t fb = full_leader0 + 8 * stage;
                     if (leader) mbar_expect_tx(full + 8 * stage, 2 * STAGE);
@@ -517,29 +559,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         phase ^= 1;
                     }
                 }
-            }
+            });
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {
+        if (leader) {  // whole warp: one elected lane issues (tc_mma_2sm)
             const std::uint32_t idesc = make_idesc(tf32 ? 2u : 1u, BM2, BN);
             int stage = 0, acc = 0;
             std::uint32_t phase = 0, acc_phase = 0;
-            for (int t = pair; t < tiles; t += npairs) {
-                int b, mb, nb;
-                decode(p, t, b, mb, nb);
-                if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
-                int nk = (p.K + bk - 1) / bk;
-                if (p.causal == 2) nk = min(nk, ((mb + 1) * BM2 + bk - 1) / bk);
+            for_each_segment(p, pair, npairs, bk, [&](int, int, int, int kb0, int kb1, int, long long) {
                 mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
                 tc_fence_after();
                 const std::uint32_t d = tmem + acc * BN;
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(full + 8 * stage, phase);
                     tc_fence_after();
                     const std::uint32_t sa = sbase + stage * STAGE;
                     const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + A_BYTES);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) tc_mma_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                    for (int k = 0; k < 4; ++k) tc_mma_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0) | (k != 0), tf32);
                     tc_commit_2sm(empty + 8 * stage);
                     if (++stage == kStages2) {
                         stage = 0;
@@ -551,7 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     acc = 0;
                     acc_phase ^= 1;
                 }
-            }
+            });
         }
     } else {
         const int lane_base = (warp % 4) * 32;
@@ -561,17 +598,79 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const bool vec_ok = (p.N % 32 == 0) && ((p.ldc * ob) % 16 == 0) && ((p.sc * ob) % 16 == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
-        for (int t = pair; t < tiles; t += npairs) {
-            int b, mb, nb;
-            decode(p, t, b, mb, nb);
-            if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
+        const int r_local = lane_base + lane;
+        for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int nb, int kb0, int kb1, int nk, long long tile_it0) {
             mbar_wait(tfull + 8 * acc, acc_phase);
             tc_fence_after();
             const int row = mb * BM2 + static_cast<int>(rank) * HALF + lane_base + lane;
             const bool row_ok = row < p.M;
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
-            if (p.epi == 1) {
+            if (kb0 > 0) {
+                // Stream-K contributor (the first segment of this pair's
+                // slice, a tile's later K blocks): publish the partial.
+                float* slot = p.ws + ((static_cast<std::int64_t>(pair) * 2 + rank) * HALF + r_local) * BN;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    std::uint32_t r[32];
+                    TN_LD32(tbase + c0, r);
+                    tc_wait_ld();
+                    float4* dst = reinterpret_cast<float4*>(slot + c0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        __stcg(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                    __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+                }
+                __threadfence();
+                epi_bar();
+                if (threadIdx.x == 64) {
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + pair * 2 + rank), "r"(p.epoch)
+                                 : "memory");
+                }
+            } else if (kb1 < nk) {
+                // Stream-K finisher: owns the tile's first K blocks, which
+                // are the last segment of its slice, so the later pairs'
+                // partials (their first segments) are published by now.
+                const int q1 = sk_owner(p, tile_it0 + nk - 1, npairs);
+                if (threadIdx.x == 64) {
+                    for (int q = pair + 1; q <= q1; ++q) {
+                        if (sk_begin(p, q, npairs) == sk_begin(p, q + 1, npairs)) continue;
+                        const unsigned* f = p.flags + q * 2 + rank;
+                        unsigned v;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                        } while (v != p.epoch);
+                    }
+                }
+                epi_bar();
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    std::uint32_t r[32];
+                    TN_LD32(tbase + c0, r);
+                    tc_wait_ld();
+                    for (int q = pair + 1; q <= q1; ++q) {
+                        if (sk_begin(p, q, npairs) == sk_begin(p, q + 1, npairs)) continue;
+                        const float4* src = reinterpret_cast<const float4*>(
+                            p.ws + ((static_cast<std::int64_t>(q) * 2 + rank) * HALF + r_local) * BN + c0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 x = __ldcg(src + j);
+                            r[4 * j] = __float_as_uint(__uint_as_float(r[4 * j]) + x.x);
+                            r[4 * j + 1] = __float_as_uint(__uint_as_float(r[4 * j + 1]) + x.y);
+                            r[4 * j + 2] = __float_as_uint(__uint_as_float(r[4 * j + 2]) + x.z);
+                            r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + x.w);
+                        }
+                    }
+                    if (p.epi == 0) store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                    else TN_ST32(tbase + c0, r);  // summed tile back to TMEM for the fused epilogue
+                }
+                if (p.epi != 0) {
+                    tc_wait_st();
+                    if (p.epi == 1) epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+                    else epilogue_qkv_rope(p, tbase, row, nb, row_ok);
+                }
+            } else if (p.epi == 1) {
                 epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
             } else if (p.epi == 2) {
                 epilogue_qkv_rope(p, tbase, row, nb, row_ok);
@@ -591,6 +690,198 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 acc = 0;
                 acc_phase ^= 1;
             }
+        });
+    }
+
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Wide CTA-pair variant: a 512x256 output tile per pair (each CTA owns 256
+// rows = two 128-row M-halves, one M=256 MMA per half per K step, both
+// accumulators filling the 512 TMEM columns). Per 64-element K block a CTA
+// receives 48 KB for 2x256x256x64 MACs — 25% fewer bytes per FLOP than the
+// 256x256 pair tile, whose L2->SM operand stream (64 B/clk/SM) caps the
+// tensor pipe near 2/3 busy. With no spare TMEM for a second accumulator,
+// the next tile's half-0 MMAs start as soon as the epilogue has drained half
+// 0, and half-1 MMAs are deferred (holding their stages) until half 1 drains.
+constexpr int kStagesW = 4;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_kernel_2sm_w(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
+    constexpr int HALF = 128;
+    constexpr int A_SUB = HALF * kAtom;        // 16 KB: one 128-row A sub-tile
+    constexpr int STAGE = 3 * A_SUB;           // A half 0, A half 1, B (48 KB per CTA)
+    constexpr int BN = 256, BMW = 512;
+    constexpr std::uint32_t TMEM_COLS = 512;   // half h accumulates in columns [256h, 256h+256)
+
+    extern __shared__ std::uint8_t smem_raw[];
+    const std::uint32_t raw = smem_u32(smem_raw);
+    const std::uint32_t pad = ((raw + 1023) & ~1023u) - raw;
+    std::uint8_t* smem = smem_raw + pad;
+    const std::uint32_t sbase = raw + pad;
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStagesW * STAGE);
+    const std::uint32_t full = smem_u32(bars), empty = full + 8 * kStagesW;
+    const std::uint32_t tfull = empty + 8 * kStagesW, tempty = tfull + 8;  // tempty[2]
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStagesW + 3);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const std::uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int bk = kAtom / p.in_bytes;
+    const bool tf32 = p.in_bytes == 4;
+    const int tiles = p.batch * p.tiles_m * p.tiles_n;  // tiles_m counts 512-row tiles
+    const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+    auto tile_nk = [&](int mb) {
+        int nk = (p.K + bk - 1) / bk;
+        if (p.causal == 2) nk = min(nk, ((mb + 1) * BMW + bk - 1) / bk);
+        return nk;
+    };
+    auto skipped = [&](int mb, int nb) { return p.causal == 1 && nb * BN > mb * BMW + BMW - 1; };
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&ta)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tb)) : "memory");
+        for (int s = 0; s < kStagesW; ++s) {
+            mbar_init(full + 8 * s, 1);
+            mbar_init(empty + 8 * s, 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 8);
+        mbar_init(tempty + 8, 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const std::uint32_t tmem = *tmem_slot;
+    const std::uint32_t full_leader0 = mapa(full, 0);
+    const std::uint32_t tempty_leader0 = mapa(tempty, 0);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            std::uint32_t phase = 0;
+            for (int t = pair; t < tiles; t += npairs) {
+                int b, mb, nb;
+                decode(p, t, b, mb, nb);
+                if (skipped(mb, nb)) continue;
+                const int nk = tile_nk(mb);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(empty + 8 * stage, phase ^ 1);
+                    const std::uint32_t fb = full_leader0 + 8 * stage;
+                    if (leader) mbar_expect_tx(full + 8 * stage, 2 * STAGE);
+                    const std::uint32_t sa = sbase + stage * STAGE;
+                    const int ab = p.a_batched ? b : 0;
+                    tma_load_3d_2sm(sa, &ta, kb * bk, mb * BMW + rank * HALF, ab, fb);
+                    tma_load_3d_2sm(sa + A_SUB, &ta, kb * bk, mb * BMW + 256 + rank * HALF, ab, fb);
+                    tma_load_3d_2sm(sa + 2 * A_SUB, &tb, kb * bk, nb * BN + rank * HALF, p.b_batched ? b : 0, fb);
+                    if (++stage == kStagesW) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {  // whole warp: one elected lane issues (tc_mma_2sm)
+            const std::uint32_t idesc = make_idesc(tf32 ? 2u : 1u, 256, BN);
+            int stage = 0;
+            std::uint32_t phase = 0, tphase = 0;
+            int defer_stage[kStagesW];
+            for (int t = pair; t < tiles; t += npairs) {
+                int b, mb, nb;
+                decode(p, t, b, mb, nb);
+                if (skipped(mb, nb)) continue;
+                const int nk = tile_nk(mb);
+                mbar_wait(tempty, tphase ^ 1);  // half 0 drained by the previous tile's epilogue
+                tc_fence_after();
+                bool h1_ready = false;
+                int ndefer = 0, h1_done = 0;  // half-1 K blocks issued so far
+                auto issue_h1 = [&](int st) {
+                    const std::uint32_t sa = sbase + st * STAGE;
+                    const std::uint64_t ad = sdesc(sa + A_SUB), bd = sdesc(sa + 2 * A_SUB);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        tc_mma_2sm(tmem + 256, ad + 2 * k, bd + 2 * k, idesc, (h1_done | k) != 0, tf32);
+                    tc_commit_2sm(empty + 8 * st);
+                    ++h1_done;
+                };
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(full + 8 * stage, phase);
+                    tc_fence_after();
+                    const std::uint32_t sa = sbase + stage * STAGE;
+                    const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + 2 * A_SUB);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) tc_mma_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                    if (!h1_ready) {
+                        defer_stage[ndefer++] = stage;
+                        const bool drained = __shfl_sync(0xffffffffu, mbar_test(tempty + 8, tphase ^ 1), 0);
+                        if (ndefer == kStagesW || kb == nk - 1 || drained) {
+                            mbar_wait(tempty + 8, tphase ^ 1);
+                            tc_fence_after();
+                            h1_ready = true;
+                            for (int i = 0; i < ndefer; ++i) issue_h1(defer_stage[i]);
+                        }
+                    } else {
+                        issue_h1(stage);
+                    }
+                    if (++stage == kStagesW) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit_2sm(tfull);
+                tphase ^= 1;
+            }
+        }
+    } else {
+        const int lane_base = (warp % 4) * 32;
+        std::uint32_t tphase = 0;
+        const int ob = p.out_dtype == BF16 ? 2 : 4;
+        const bool vec_ok = (p.N % 32 == 0) && ((p.ldc * ob) % 16 == 0) && ((p.sc * ob) % 16 == 0) &&
+                            ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
+                            ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
+        for (int t = pair; t < tiles; t += npairs) {
+            int b, mb, nb;
+            decode(p, t, b, mb, nb);
+            if (skipped(mb, nb)) continue;
+            mbar_wait(tfull, tphase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int row = mb * BMW + h * 256 + static_cast<int>(rank) * HALF + lane_base + lane;
+                const bool row_ok = row < p.M;
+                const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+                const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + h * 256;
+                if (p.epi == 1) {
+                    epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+                } else if (p.epi == 2) {
+                    epilogue_qkv_rope(p, tbase, row, nb, row_ok);
+                } else {
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                        std::uint32_t r[32];
+                        TN_LD32(tbase + c0, r);
+                        tc_wait_ld();
+                        store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(tempty_leader0 + 8 * h);
+            }
+            tphase ^= 1;
         }
     }
 
@@ -693,6 +984,7 @@ int smem_bytes() {
     return kStages * (kBM + BN) * kAtom + 256 + 1024;
 }
 int smem_bytes_2sm() { return kStages2 * 2 * 128 * kAtom + 256 + 1024; }
+int smem_bytes_2sm_w() { return kStagesW * 3 * 128 * kAtom + 256 + 1024; }
 
 }  // namespace
 
@@ -719,11 +1011,41 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     }
     plan->path = ok ? (two_sm ? 2 : 0) : 1;
     plan->bn = bn;
-    const int bm = plan->path == 2 ? 256 : kBM;
+    if (plan->path == 2 && a.tile == 2) plan->path = 3;
+    if (plan->path == 2 && a.M > 256 && a.tile == 0) {
+        // Wide 512x256 pair tiles do ~5% more per pair-cycle (fewer operand
+        // bytes per FLOP) but quantise to whole waves; narrow tiles get a
+        // stream-K tail (no quantisation; ~15% overhead when every tile is
+        // split). Measured per shape on B200 (tools/gemm_bench.py).
+        const int P = std::max(1, num_sms / 2);
+        const long long tn = (a.N + 255) / 256;
+        const long long narrow = a.batch * ((a.M + 255) / 256) * tn, wide = a.batch * ((a.M + 511) / 512) * tn;
+        const bool sk = a.causal == 0 && narrow >= P && narrow % P != 0;
+        const double t_narrow = sk ? static_cast<double>(narrow) / P * (narrow >= 2 * P ? 1.0 : 1.15)
+                                   : static_cast<double>((narrow + P - 1) / P);
+        const double t_wide = static_cast<double>((wide + P - 1) / P) * 2.0 / 1.05;
+        if (t_wide < t_narrow) plan->path = 3;
+    }
+    const int bm = plan->path == 2 ? 256 : plan->path == 3 ? 512 : kBM;
     const int tm = (a.M + bm - 1) / bm, tn = (a.N + bn - 1) / bn;
     plan->tiles = a.batch * tm * tn;
     plan->grid = std::min(plan->tiles, std::max(1, num_sms));
-    if (plan->path == 2) plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
+    if (plan->path == 3) plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
+    if (plan->path == 2) {
+        plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
+        // Stream-K tail when the tiles do not fill the last wave of pairs:
+        // the last partial wave plus one full wave are split by K blocks.
+        const int npairs = plan->grid / 2, T = plan->tiles;
+        const int nk = static_cast<int>((a.K * es + kAtom - 1) / kAtom);
+        if (a.causal == 0 && T >= npairs && T % npairs != 0) {
+            const int sk = T / npairs >= 2 ? T % npairs + npairs : T;
+            if (static_cast<long long>(sk) * nk >= 4LL * npairs) {
+                plan->sk_tiles = sk;
+                plan->sk_nk = nk;
+                plan->ws_bytes = static_cast<std::size_t>(npairs) * 2 * 128 * 256 * 4 + static_cast<std::size_t>(npairs) * 2 * 4;
+            }
+        }
+    }
     if (ok) {
         static unsigned long long attr_set = 0;  // per CUDA device
         int dev = 0;
@@ -733,13 +1055,14 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
             cudaFuncSetAttribute(gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
             cudaFuncSetAttribute(gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>());
             cudaFuncSetAttribute(gemm_kernel_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm());
+            cudaFuncSetAttribute(gemm_kernel_2sm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm_w());
             attr_set |= 1ULL << dev;
         }
     }
     return cudaSuccess;
 }
 
-cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
+cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws) {
     const GemmArgs& a = plan.args;
     if (plan.path == 1 && a.epi == 2) return cudaErrorNotSupported;  // rejected at prepare time
     if (plan.path == 1) {
@@ -756,7 +1079,8 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
     p.N = a.N;
     p.K = a.K;
     p.batch = a.batch;
-    p.tiles_m = (a.M + (plan.path == 2 ? 256 : kBM) - 1) / (plan.path == 2 ? 256 : kBM);
+    const int bm = plan.path == 3 ? 512 : plan.path == 2 ? 256 : kBM;
+    p.tiles_m = (a.M + bm - 1) / bm;
     p.tiles_n = (a.N + plan.bn - 1) / plan.bn;
     p.ldc = a.ldc;
     p.sc = a.sc;
@@ -769,7 +1093,25 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s) {
     p.epi = a.epi;
     p.rope = static_cast<const float*>(a.rope);
     p.heads = a.heads;
-    if (plan.path == 2)
+    p.dp_tiles = plan.tiles;
+    p.sk_nk = 0;
+    p.sk_total = 0;
+    p.ws = nullptr;
+    p.flags = nullptr;
+    p.epoch = 0;
+    if (plan.path == 2 && plan.sk_tiles > 0 && ws && ws->p && ws->bytes >= plan.ws_bytes) {
+        const int npairs = plan.grid / 2;
+        p.dp_tiles = plan.tiles - plan.sk_tiles;
+        p.sk_nk = plan.sk_nk;
+        p.sk_total = static_cast<long long>(plan.sk_tiles) * plan.sk_nk;
+        p.ws = static_cast<float*>(ws->p);
+        p.flags = reinterpret_cast<unsigned*>(static_cast<char*>(ws->p) + static_cast<std::size_t>(npairs) * 2 * 128 * 256 * 4);
+        if (++ws->epoch == 0) ws->epoch = 1;  // 0 = never published
+        p.epoch = ws->epoch;
+    }
+    if (plan.path == 3)
+        gemm_kernel_2sm_w<<<plan.grid, kThreads, smem_bytes_2sm_w(), s>>>(plan.ta, plan.tb, p);
+    else if (plan.path == 2)
         gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, p);
     else if (plan.bn == 128)
         gemm_kernel<128><<<plan.grid, kThreads, smem_bytes<128>(), s>>>(plan.ta, plan.tb, p);

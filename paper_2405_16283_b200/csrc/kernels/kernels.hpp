@@ -37,6 +37,7 @@ struct GemmArgs {
                   // 2: QKV + RoPE epilogue (hd 128): out = [rope(q) (H,M,128) | rope(k) | vᵀ (H,128,M)]
     const void* rope = nullptr;  // epi 2: fp32 [M, 64, 2] (cos, sin)
     int heads = 0;               // epi 2: heads per section, N = 3 * heads * 128
+    int tile = 0;                // CTA-pair tile: 0 auto, 1 narrow (256x256), 2 wide (512x256)
 };
 
 struct alignas(64) GemmPlan {
@@ -47,6 +48,18 @@ struct alignas(64) GemmPlan {
     int bn = 256;    // N tile of the tcgen05 path
     int tiles = 0;   // output tiles (all batches)
     int grid = 0;
+    int sk_tiles = 0;          // path 2: trailing tiles split by K blocks across all pairs (stream-K)
+    int sk_nk = 0;             // K blocks per stream-K tile
+    std::size_t ws_bytes = 0;  // workspace the stream-K tail needs (0: none)
+};
+
+// Stream-K scratch: per-pair fp32 partial slots + publication flags. One per
+// stream (launches on a stream are ordered); `epoch` advances per launch so
+// the flags never need resetting. Zero-initialised memory.
+struct GemmWorkspace {
+    void* p = nullptr;
+    std::size_t bytes = 0;
+    unsigned epoch = 0;
 };
 
 // 3-D tiled TMA descriptor (inner, rows, batch), 128-byte swizzle.
@@ -55,7 +68,7 @@ bool encode_tma_3d(CUtensorMap* map, const void* base, int esize, std::int64_t i
 
 // Encodes TMA descriptors (needs a CUDA context on the target device).
 cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms);
-cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s);
+cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws = nullptr);
 double gemm_flops(const GemmArgs& a);  // algorithmic FLOPs (causal-aware)
 
 // Fused causal attention: q, k [H, seq, hd] bf16, vt [H, hd, seq] bf16,

@@ -32,6 +32,17 @@ __device__ __forceinline__ bool mbar_try_wait(std::uint32_t bar, std::uint32_t p
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test(std::uint32_t bar, std::uint32_t parity) {  // non-blocking
+    std::uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
@@ -46,22 +57,28 @@ __device__ __forceinline__ void tma_load_3d(std::uint32_t dst, const CUtensorMap
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+// MMA issue helpers: called by a whole converged warp; one elected lane
+// issues. Warp-wide calls let ptxas keep the descriptors in uniform
+// registers — issuing from a single divergent lane costs ~40 instructions per
+// MMA (ELECT/R2UR broadcast loops), more than a short MMA's execution time.
 __device__ __forceinline__ void tc_commit(std::uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
 }
 __device__ __forceinline__ void tc_mma(std::uint32_t d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
                                        std::uint32_t accum, bool tf32) {
     if (tf32) {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
             "l"(a), "l"(b), "r"(idesc), "r"(accum)
             : "memory");
     } else {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
             "l"(a), "l"(b), "r"(idesc), "r"(accum)
             : "memory");
     }

@@ -58,6 +58,19 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=512, N=1024, K=256, epilogue="swiglu"),   # fused SwiGLU, CTA pair
     dict(M=128, N=512, K=128, epilogue="swiglu"),    # fused SwiGLU, 1-CTA
     dict(M=8, N=512, K=128, epilogue="swiglu"),      # fused SwiGLU, SIMT
+    dict(M=2304, N=2304, K=512, out_dtype="f32", tile="narrow"),  # 81 pair tiles: all stream-K
+    dict(M=4096, N=4096, K=1024, residual=True, tile="narrow"),   # 256 tiles: 2 DP waves + stream-K tail
+    dict(M=2304, N=2304, K=256, in_dtype="f32", out_dtype="f32", tile="narrow"),  # tf32 stream-K
+    dict(M=1280, N=1280, K=256, batch=4, out_dtype="f32", tile="narrow"),         # batched stream-K
+    dict(M=4096, N=4096, K=1024, residual=True),     # wide 512x256 pair tiles (auto)
+    dict(M=1000, N=520, K=320, residual=True, tile="wide"),        # wide, ragged M/N
+    dict(M=1024, N=768, K=512, out_dtype="f32", tile="wide", alpha=0.25),
+    dict(M=768, N=512, K=256, in_dtype="f32", out_dtype="f32", tile="wide"),  # wide tf32
+    dict(M=1024, N=512, K=256, batch=3, out_dtype="f32", causal=1, tile="wide"),
+    dict(M=1024, N=512, K=1024, batch=2, causal=2, tile="wide"),
+    dict(M=1536, N=1024, K=256, epilogue="swiglu", tile="wide"),  # wide + fused SwiGLU
+    dict(M=512, N=256, K=4096, tile="wide"),         # long K: deferred half-1 MMAs cycle the ring
+    dict(M=2304, N=2304, K=256, epilogue="swiglu", tile="narrow"),  # stream-K + fused SwiGLU
 ])
 def test_gemm_parity(shape):
     shape = dict(shape)
@@ -79,6 +92,40 @@ def test_gemm_parity(shape):
         x, y = x[keep], y[keep]
     tol = 5e-3 if shape.get("in_dtype") == "f32" else (1e-4 if shape.get("out_dtype") == "f32" else 1e-2)
     assert rel_err(x, y) < tol
+
+
+@pytest.mark.parametrize("tile,S,H", [("narrow", 1024, 4), ("wide", 1024, 4), ("narrow", 4096, 8)])
+def test_gemm_qkv_rope_epilogue_tiles(tile, S, H):
+    """Fused QKV + RoPE + Vᵀ epilogue on both CTA-pair tile shapes (and with a
+    stream-K tail: 192 pair tiles) vs the oracle."""
+    d = 512
+    g = W.GraphBuilder()
+    x = g.input("x", (S, d), "bf16", init=("normal", 1.0))
+    w = g.input("wqkv", (3 * H * 128, d), "bf16", init=("normal", 0.05))
+    rope = g.input("rope_table", (S, 64, 2), "f32", init=("rope", 10000.0))
+    o = g.gemm("qkv", x, w, S, 3 * H * 128, d, r=rope, epilogue="qkv_rope", heads=H, tile=tile,
+               out_shape=(3, H, S, 128))
+    mg, _ = W.plan(g, 1 << 30)
+    inp = inputs_of(g, seed=21)
+    _, got = run_gpu(g, mg, inp)
+    want = oracle_outputs(g, mg, inp)
+    assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 1e-2
+
+
+def test_gemm_stream_k_deterministic():
+    """Stream-K partial sums are combined in a fixed order: repeated runs
+    through one executor (advancing the workspace epoch) are bitwise equal."""
+    g = gemm_graph(4096, 4096, 2048, tile="narrow")
+    mg, _ = W.plan(g, 1 << 30)
+    (o,) = g.outputs()
+    outs = []
+    with Executor(mg, g.to_json(), {}) as ex:
+        for vid, data in inputs_of(g, seed=2).items():
+            ex.set_input(vid, data)
+        for _ in range(3):
+            ex.run()
+            outs.append(ex.get_output(o, g.tensors[o].nbytes))
+    assert outs[0] == outs[1] == outs[2]
 
 
 def test_rowops_and_eltwise_parity():
