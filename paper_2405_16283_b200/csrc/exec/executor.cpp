@@ -76,6 +76,8 @@ struct Executor::Impl {
     std::vector<char*> arena;       // per logical device
     std::vector<std::vector<cudaStream_t>> streams;
     std::vector<cudaStream_t> marker;  // per logical device: timestamps of instant vertices
+    std::vector<cudaStream_t> compute;  // per logical device: every kernel when compute_tokens == 1, so a
+                                        // lookahead chain is plain stream order (no cross-stream event wait)
     std::vector<std::vector<k::GemmWorkspace>> gws;  // per device x stream: stream-K GEMM scratch
     std::vector<cudaEvent_t> t0;    // per logical device
     std::vector<cudaEvent_t> ev_start, ev_end;  // per memgraph vertex index
@@ -99,6 +101,7 @@ struct Executor::Impl {
         VertexId input_id = -1;   // Input vertices, and offload/reload of an evicted input root
         bool elided = false;      // offload of an unmodified input: no copy
         bool instant = false;     // aliased Input: completes at dispatch, no stream, no copy
+        bool timeless = false;    // instant with no in-edges: no device timestamps (trace time 0)
         const OpDesc* op_desc = nullptr;
         std::vector<const char*> argp;  // resolved argument pointers
         std::unique_ptr<k::GemmPlan> gemm;
@@ -181,6 +184,7 @@ void Executor::Impl::build() {
     arena.assign(D, nullptr);
     streams.resize(D);
     marker.assign(D, nullptr);
+    compute.assign(D, nullptr);
     t0.resize(D);
     for (int d = 0; d < D; ++d) {
         set_device(d);
@@ -189,6 +193,7 @@ void Executor::Impl::build() {
         streams[d].resize(cfg.streams_per_device);
         for (auto& s : streams[d]) TN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         TN_CUDA(cudaStreamCreateWithFlags(&marker[d], cudaStreamNonBlocking));
+        TN_CUDA(cudaStreamCreateWithFlags(&compute[d], cudaStreamNonBlocking));
         // One time origin per physical GPU: memgraph devices that share a GPU
         // share t0, so cross-device edges compare on one clock.
         int first = d;
@@ -219,6 +224,8 @@ void Executor::Impl::build() {
 
     // Data in-edges per vertex, edge order.
     std::unordered_map<VertexId, std::vector<std::pair<VertexId, VertexId>>> data_in;  // to -> (from, root)
+    std::unordered_map<VertexId, bool> has_in_edge;
+    for (const auto& e : m.edges) has_in_edge[e.to] = true;
     for (const auto& e : m.edges) {
         if (e.kind != EdgeKind::Data) continue;
         const MemVertex& f = m.at(e.from);
@@ -267,6 +274,7 @@ void Executor::Impl::build() {
                 in.bytes = static_cast<std::size_t>(size_of(v.id));
                 in.input_id = v.origin.ref;
                 in.instant = aliased_inputs();
+                in.timeless = in.instant && !has_in_edge[v.id];
                 break;
             }
             case MemOpKind::Offload: {
@@ -558,8 +566,14 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
 void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t after) {
     Instr& in = prog[vidx];
     set_device(in.dev);
-    cudaStream_t s = in.instant ? marker[in.dev] : streams[in.dev][stream < 0 ? 0 : stream];  // inputs hold no stream when not materialised
-    if (after >= 0) TN_CUDA(cudaStreamWaitEvent(s, ev_end[after], 0));  // lookahead: run behind `after`
+    if (in.timeless) return;  // zero-cost input with nothing to wait for: trace time 0
+    const bool on_compute = in.op == MemOpKind::Kernel && cfg.compute_tokens == 1;
+    cudaStream_t s = in.instant ? marker[in.dev]
+                     : on_compute ? compute[in.dev]
+                                  : streams[in.dev][stream < 0 ? 0 : stream];  // inputs hold no stream when not materialised
+    // lookahead: run behind `after` (same stream when both are on the compute stream)
+    if (after >= 0 && !(on_compute && prog[after].op == MemOpKind::Kernel && prog[after].dev == in.dev))
+        TN_CUDA(cudaStreamWaitEvent(s, ev_end[after], 0));
     TN_CUDA(cudaEventRecord(ev_start[vidx], s));
     switch (in.op) {
         case MemOpKind::Input: {
@@ -842,8 +856,10 @@ ExecutionTrace Executor::Impl::build_trace() {
     for (std::int32_t vidx : dispatched) {
         const MemVertex& v = g->vertices[vidx];
         float a = 0, b = 0;
-        TN_CUDA(cudaEventElapsedTime(&a, t0[v.device], ev_start[vidx]));
-        TN_CUDA(cudaEventElapsedTime(&b, t0[v.device], ev_end[vidx]));
+        if (!prog[vidx].timeless) {
+            TN_CUDA(cudaEventElapsedTime(&a, t0[v.device], ev_start[vidx]));
+            TN_CUDA(cudaEventElapsedTime(&b, t0[v.device], ev_end[vidx]));
+        }
         double s = a * 1e-3, e = std::max(a, b) * 1e-3;
         t.rows.push_back({v.id, s, e, v.device, stream_of[vidx]});
         if (v.op == MemOpKind::Kernel) {
@@ -905,6 +921,8 @@ Executor::Impl::~Impl() {
         for (auto s : ss)
             if (s) cudaStreamDestroy(s);
     for (auto s : marker)
+        if (s) cudaStreamDestroy(s);
+    for (auto s : compute)
         if (s) cudaStreamDestroy(s);
     for (auto& ws : gws)
         for (auto& w : ws)
