@@ -29,12 +29,15 @@ constexpr int kN = 64;           // keys per KV block
 constexpr int kHd = 128;         // head dim of the fused path
 constexpr int kThreads = 192;
 // smem (bytes): Q 128x128 (2 atoms of 16 KB), K 2 stages x 64x128 (2 atoms of
-// 8 KB each), V 2 stages x 128(hd)x64(keys) (1 atom, 16 KB), P 128x64 (1 atom,
-// 16 KB): 112 KB, so two CTAs share an SM and interleave their MMA and
-// softmax phases (the softmax of one hides the MMAs / loads of the other).
-// Two CTAs only fit without alignment slack: the dynamic window starts on a
-// 1 KB boundary (the per-CTA system reservation precedes it), checked below.
-constexpr int kQ = 32768, kKst = 16384, kV = 16384, kP = 16384;
+// 8 KB each), V 2 stages x 128(hd)x64(keys) (1 atom, 16 KB): 96 KB, so two
+// CTAs share an SM and interleave their MMA and softmax phases (the softmax
+// of one hides the MMAs / loads of the other). P never touches shared
+// memory: the softmax warps write it as packed bf16 into TMEM and the P·V
+// MMA reads its A operand from there.
+// TMEM (256 columns per CTA): S [0, 64), P [64, 96), O [128, 256).
+// Two CTAs fit without alignment slack: the dynamic window starts on a 1 KB
+// boundary (the per-CTA system reservation precedes it), checked below.
+constexpr int kQ = 32768, kKst = 16384, kV = 16384;
 
 struct AttnParams {
     __nv_bfloat16* O;
@@ -44,12 +47,6 @@ struct AttnParams {
     int causal;
 };
 
-// P row r, keys [key, key+8) as one 16-byte chunk of the 128B-swizzled
-// K-major tile (one 64-key atom, rows of 128 bytes).
-__device__ __forceinline__ std::uint32_t p_chunk_addr(std::uint32_t base, int r, int key) {
-    return base + r * 128 + ((((key >> 3) ^ (r & 7))) << 4);
-}
-
 __global__ void __launch_bounds__(kThreads, 2)
     attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                      const __grid_constant__ CUtensorMap tv, const AttnParams p) {
@@ -57,9 +54,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     const std::uint32_t raw = smem_u32(smem_raw);
     if (raw & 1023u) __trap();  // SW128 tiles need 1 KB alignment
     const std::uint32_t base = raw;
-    const std::uint32_t sQ = base, sK0 = base + kQ, sV = sK0 + 2 * kKst, sP = sV + 2 * kV;
+    const std::uint32_t sQ = base, sK0 = base + kQ, sV = sK0 + 2 * kKst;
     std::uint8_t* gen_base = smem_raw + (base - raw);
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + kQ + 2 * kKst + 2 * kV + kP);
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + kQ + 2 * kKst + 2 * kV);
     const std::uint32_t b0 = smem_u32(bars);
     const std::uint32_t q_full = b0, k_full = b0 + 8, k_empty = b0 + 24, v_full = b0 + 40, v_empty = b0 + 56,
                         s_full = b0 + 72, s_free = b0 + 80, p_full = b0 + 88, o_done = b0 + 96;
@@ -94,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     tc_fence_after();
     const std::uint32_t tmem = *tmem_slot;
-    const std::uint32_t tS = tmem, tO = tmem + 128;  // S uses 64 columns
+    const std::uint32_t tS = tmem, tP = tmem + 64, tO = tmem + 128;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -140,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const std::uint32_t dv = sV + (j & 1) * kV;
 #pragma unroll
                 for (int kk = 0; kk < kN / 16; ++kk)
-                    tc_mma(tO, sdesc(sP + kk * 32), sdesc(dv + kk * 32), idesc_o, (j | kk) != 0, false);
+                    tc_mma_ts(tO, tP + kk * 8, sdesc(dv + kk * 32), idesc_o, (j | kk) != 0);
                 tc_commit(o_done);
                 tc_commit(v_empty + 8 * (j & 1));
             }
@@ -226,17 +223,16 @@ __global__ void __launch_bounds__(kThreads, 2)
                     tc_wait_st();
                 }
             }
+            {
+                std::uint32_t pw[kN / 2];
 #pragma unroll
-            for (int c = 0; c < kN; c += 8) {
-                uint4 v;
-                __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) hv[i] = __floats2bfloat162_rn(s[c + 2 * i], s[c + 2 * i + 1]);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(p_chunk_addr(sP, r, c)), "r"(v.x),
-                             "r"(v.y), "r"(v.z), "r"(v.w)
-                             : "memory");
+                for (int i = 0; i < kN / 2; ++i) {
+                    __nv_bfloat162 v2 = __floats2bfloat162_rn(s[2 * i], s[2 * i + 1]);
+                    pw[i] = *reinterpret_cast<std::uint32_t*>(&v2);
+                }
+                TN_ST32(tP + trow, pw);
+                tc_wait_st();
             }
-            fence_async_smem();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full);
@@ -270,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (warp == 1) tmem_free(tmem, 256);
 }
 
-constexpr int kSmem = kQ + 2 * kKst + 2 * kV + kP + 128;
+constexpr int kSmem = kQ + 2 * kKst + 2 * kV + 128;
 
 // --- SIMT fallback (any seq / head dim): one warp per query row, fp32 online
 // softmax over all keys in order. Slow; only for shapes the fused path rejects.

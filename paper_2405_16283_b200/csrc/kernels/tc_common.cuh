@@ -83,6 +83,16 @@ __device__ __forceinline__ void tc_mma(std::uint32_t d, std::uint64_t a, std::ui
             : "memory");
     }
 }
+// A operand from tensor memory (rows = lanes, K packed two 16-bit values per
+// 32-bit column), B from shared memory.
+__device__ __forceinline__ void tc_mma_ts(std::uint32_t d, std::uint32_t a_tmem, std::uint64_t b, std::uint32_t idesc,
+                                          std::uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum)
+        : "memory");
+}
 // K-major operand in a SWIZZLE_128B layout: rows of 128 B, 8-row groups
 // 1024 B apart (SBO), LBO unused, descriptor version 1 (sm_100).
 __device__ __forceinline__ std::uint64_t sdesc(std::uint32_t saddr) {
