@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.hpp"
 #include "tc_common.cuh"
@@ -1011,8 +1013,14 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     }
     plan->path = ok ? (two_sm ? 2 : 0) : 1;
     plan->bn = bn;
-    if (plan->path == 2 && a.tile == 2) plan->path = 3;
-    if (plan->path == 2 && a.M > 256 && a.tile == 0) {
+    int tile = a.tile;
+    if (tile == 0) {  // TN_GEMM_TILE=narrow|wide overrides the automatic choice (tuning experiments)
+        static const char* env = std::getenv("TN_GEMM_TILE");
+        if (env && std::strcmp(env, "narrow") == 0) tile = 1;
+        if (env && std::strcmp(env, "wide") == 0) tile = 2;
+    }
+    if (plan->path == 2 && tile == 2) plan->path = 3;
+    if (plan->path == 2 && a.M > 256 && tile == 0) {
         // Wide 512x256 pair tiles do ~5% more per pair-cycle (fewer operand
         // bytes per FLOP) but quantise to whole waves; narrow tiles get a
         // stream-K tail (no quantisation; ~15% overhead when every tile is
