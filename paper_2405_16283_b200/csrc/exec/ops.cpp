@@ -126,7 +126,8 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
                 if (tl == "auto") d.tile = 0;
                 else if (tl == "narrow") d.tile = 1;
                 else if (tl == "wide") d.tile = 2;
-                else throw ParseError("gemm tile must be auto, narrow or wide");
+                else if (tl == "streamk") d.tile = 3;
+                else throw ParseError("gemm tile must be auto, narrow, wide or streamk");
             }
             d.in_dtype = dtype_of(o.value("in_dtype", std::string("bf16")));
             d.out_dtype = dtype_of(o.value("out_dtype", std::string("bf16")));

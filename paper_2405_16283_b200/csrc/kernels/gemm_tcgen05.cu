@@ -54,6 +54,11 @@ struct Params {
     // owns a tile's first K block, in ascending pair order (deterministic).
     int dp_tiles, sk_nk;
     long long sk_total;
+    // Half-width tail (CTA-pair kernel, default): when the last wave of
+    // 256x256 tiles would leave more than half the pairs idle, its tiles are
+    // split into two 256x128 halves (N=128 MMAs, 64 B rows per CTA), so the
+    // tail costs half a tile-time. Tiles [dp_tiles, dp_tiles + half_tiles/2).
+    int half_tiles;
     float* ws;
     unsigned* flags;  // per CTA of each pair: epoch of its last published partial
     unsigned epoch;
@@ -182,14 +187,14 @@ __device__ __forceinline__ void epilogue_swiglu(const Params& p, std::uint32_t t
 // section written transposed [H, 128, seq] (lanes hold consecutive tokens, so
 // the transposed stores coalesce across the warp). Output = packed
 // [q | k | vᵀ], each H*seq*128 elements.
-__device__ __forceinline__ void epilogue_qkv_rope(const Params& p, std::uint32_t tbase, int row, int nb,
+__device__ __forceinline__ void epilogue_qkv_rope(const Params& p, std::uint32_t tbase, int row, int n0, int width,
                                                   bool row_ok) {
     constexpr int HD = 128;
     const std::int64_t sec = static_cast<std::int64_t>(p.heads) * p.M * HD;
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.C);
 #pragma unroll 1
-    for (int hb = 0; hb < 256; hb += HD) {
-        const int col = nb * 256 + hb;  // first column of this head in [0, 3*H*HD)
+    for (int hb = 0; hb < width; hb += HD) {
+        const int col = n0 + hb;  // first column of this head in [0, 3*H*HD)
         const int which = col / (p.heads * HD), h = (col % (p.heads * HD)) / HD;
         if (which < 2) {
             __nv_bfloat16* dst = out + which * sec + (static_cast<std::int64_t>(h) * p.M + row) * HD;
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.epi == 1) {
                 epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
             } else if (p.epi == 2) {
-                epilogue_qkv_rope(p, tbase, row, nb, row_ok);
+                epilogue_qkv_rope(p, tbase, row, nb * BN, BN, row_ok);
             } else {
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -455,8 +460,9 @@ __device__ __forceinline__ int sk_owner(const Params& p, long long it, int npair
     while (q > 0 && sk_begin(p, q, npairs) > it) --q;
     return q;
 }
-// Visits this pair's work as (tile, K-block range) segments: its round-robin
-// data-parallel tiles, then its contiguous slice of the stream-K blocks.
+// Visits this pair's work as (tile, K-block range, columns) segments: its
+// round-robin data-parallel tiles, then its half-width tail tiles, then its
+// contiguous slice of the stream-K blocks. f(b, mb, n0, width, kb0, kb1, nk, it0).
 template <class F>
 __device__ __forceinline__ void for_each_segment(const Params& p, int pair, int npairs, int bk, F&& f) {
     constexpr int BN = 256, BM2 = 256;
@@ -466,7 +472,13 @@ __device__ __forceinline__ void for_each_segment(const Params& p, int pair, int 
         if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
         int nk = (p.K + bk - 1) / bk;
         if (p.causal == 2) nk = min(nk, ((mb + 1) * BM2 + bk - 1) / bk);
-        f(b, mb, nb, 0, nk, nk, 0LL);
+        f(b, mb, nb * BN, BN, 0, nk, nk, 0LL);
+    }
+    for (int u = pair; u < p.half_tiles; u += npairs) {  // causal == 0 only
+        int b, mb, nb;
+        decode(p, p.dp_tiles + u / 2, b, mb, nb);
+        const int nk = (p.K + bk - 1) / bk;
+        f(b, mb, nb * BN + (u & 1) * (BN / 2), BN / 2, 0, nk, nk, 0LL);
     }
     if (p.sk_total <= 0) return;
     const long long end = sk_begin(p, pair + 1, npairs);
@@ -476,7 +488,7 @@ __device__ __forceinline__ void for_each_segment(const Params& p, int pair, int 
         const int kb1 = static_cast<int>(min(static_cast<long long>(p.sk_nk), kb0 + (end - it)));
         int b, mb, nb;
         decode(p, tt, b, mb, nb);
-        f(b, mb, nb, kb0, kb1, p.sk_nk, it - kb0);
+        f(b, mb, nb * BN, BN, kb0, kb1, p.sk_nk, it - kb0);
         it += kb1 - kb0;
     }
 }
@@ -494,7 +506,8 @@ __device__ __forceinline__ void mbar_arrive_remote(std::uint32_t cluster_addr) {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_kernel_2sm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
+    gemm_kernel_2sm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                    const __grid_constant__ CUtensorMap tbh, const Params p) {
     constexpr int HALF = 128;                  // rows of A and of B staged per CTA
     constexpr int A_BYTES = HALF * kAtom;      // 16 KB
     constexpr int STAGE = 2 * A_BYTES;         // 32 KB per CTA
@@ -521,6 +534,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&ta)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tb)) : "memory");
+        if (p.half_tiles > 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tbh)) : "memory");
         for (int s = 0; s < kStages2; ++s) {
             mbar_init(full + 8 * s, 1);
             mbar_init(empty + 8 * s, 1);
@@ -548,14 +562,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             std::uint32_t phase = 0;
-            for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int nb, int kb0, int kb1, int, long long) {
+            for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int n0, int w, int kb0, int kb1, int, long long) {
+                const int brows = w / 2;  // B rows staged per CTA
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty + 8 * stage, phase ^ 1);
                     const std::uint32_t fb = full_leader0 + 8 * stage;
-                    if (leader) mbar_expect_tx(full + 8 * stage, 2 * STAGE);
+                    if (leader) mbar_expect_tx(full + 8 * stage, 2 * (A_BYTES + brows * kAtom));
                     const std::uint32_t sa = sbase + stage * STAGE;
                     tma_load_3d_2sm(sa, &ta, kb * bk, mb * BM2 + rank * HALF, p.a_batched ? b : 0, fb);
-                    tma_load_3d_2sm(sa + A_BYTES, &tb, kb * bk, nb * BN + rank * HALF, p.b_batched ? b : 0, fb);
+                    tma_load_3d_2sm(sa + A_BYTES, w == BN ? &tb : &tbh, kb * bk, n0 + rank * brows,
+                                    p.b_batched ? b : 0, fb);
                     if (++stage == kStages2) {
                         stage = 0;
                         phase ^= 1;
@@ -565,10 +581,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (leader) {  // whole warp: one elected lane issues (tc_mma_2sm)
-            const std::uint32_t idesc = make_idesc(tf32 ? 2u : 1u, BM2, BN);
+            const std::uint32_t idesc_full = make_idesc(tf32 ? 2u : 1u, BM2, BN);
+            const std::uint32_t idesc_half = make_idesc(tf32 ? 2u : 1u, BM2, BN / 2);
             int stage = 0, acc = 0;
             std::uint32_t phase = 0, acc_phase = 0;
-            for_each_segment(p, pair, npairs, bk, [&](int, int, int, int kb0, int kb1, int, long long) {
+            for_each_segment(p, pair, npairs, bk, [&](int, int, int, int w, int kb0, int kb1, int, long long) {
+                const std::uint32_t idesc = w == BN ? idesc_full : idesc_half;
                 mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
                 tc_fence_after();
                 const std::uint32_t d = tmem + acc * BN;
@@ -601,7 +619,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
         const int r_local = lane_base + lane;
-        for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int nb, int kb0, int kb1, int nk, long long tile_it0) {
+        for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int n0, int w, int kb0, int kb1, int nk, long long tile_it0) {
+            const int nb = n0 / BN;
             mbar_wait(tfull + 8 * acc, acc_phase);
             tc_fence_after();
             const int row = mb * BM2 + static_cast<int>(rank) * HALF + lane_base + lane;
@@ -670,19 +689,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (p.epi != 0) {
                     tc_wait_st();
                     if (p.epi == 1) epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
-                    else epilogue_qkv_rope(p, tbase, row, nb, row_ok);
+                    else epilogue_qkv_rope(p, tbase, row, n0, BN, row_ok);
                 }
             } else if (p.epi == 1) {
-                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);  // never a half tile
             } else if (p.epi == 2) {
-                epilogue_qkv_rope(p, tbase, row, nb, row_ok);
+                epilogue_qkv_rope(p, tbase, row, n0, w, row_ok);
             } else {
 #pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
+                for (int c0 = 0; c0 < w; c0 += 32) {
                     std::uint32_t r[32];
                     TN_LD32(tbase + c0, r);
                     tc_wait_ld();
-                    store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                    store_chunk(p, r, off, n0 + c0, row_ok, vec_ok);
                 }
             }
             tc_fence_before();
@@ -711,9 +730,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // tensor pipe near 2/3 busy. With no spare TMEM for a second accumulator,
 // the next tile's half-0 MMAs start as soon as the epilogue has drained half
 // 0, and half-1 MMAs are deferred (holding their stages) until half 1 drains.
+// Two epilogue warpgroups (warps 2-5: half 0, warps 6-9: half 1) drain the
+// halves concurrently, so the accumulator is free again after one half's
+// drain time rather than two.
 constexpr int kStagesW = 4;
+constexpr int kThreadsW = 32 * 10;
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// Plain epilogue of one 128-row x BN accumulator slab: two 32-column TMEM
+// loads in flight per wait.
+template <int BN>
+__device__ __forceinline__ void epilogue_plain(const Params& p, std::uint32_t tbase, std::int64_t off, int n0,
+                                               bool row_ok, bool vec_ok) {
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 64) {
+        std::uint32_t r0[32], r1[32];
+        TN_LD32(tbase + c0, r0);
+        TN_LD32(tbase + c0 + 32, r1);
+        tc_wait_ld();
+        store_chunk(p, r0, off, n0 + c0, row_ok, vec_ok);
+        store_chunk(p, r1, off, n0 + c0 + 32, row_ok, vec_ok);
+    }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     gemm_kernel_2sm_w(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
     constexpr int HALF = 128;
     constexpr int A_SUB = HALF * kAtom;        // 16 KB: one 128-row A sub-tile
@@ -849,6 +888,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else {
         const int lane_base = (warp % 4) * 32;
+        const int h = (warp - 2) / 4;  // the accumulator half this warpgroup drains
         std::uint32_t tphase = 0;
         const int ob = p.out_dtype == BF16 ? 2 : 4;
         const bool vec_ok = (p.N % 32 == 0) && ((p.ldc * ob) % 16 == 0) && ((p.sc * ob) % 16 == 0) &&
@@ -860,29 +900,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (skipped(mb, nb)) continue;
             mbar_wait(tfull, tphase);
             tc_fence_after();
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-                const int row = mb * BMW + h * 256 + static_cast<int>(rank) * HALF + lane_base + lane;
-                const bool row_ok = row < p.M;
-                const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
-                const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + h * 256;
-                if (p.epi == 1) {
-                    epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
-                } else if (p.epi == 2) {
-                    epilogue_qkv_rope(p, tbase, row, nb, row_ok);
-                } else {
-#pragma unroll 1
-                    for (int c0 = 0; c0 < BN; c0 += 32) {
-                        std::uint32_t r[32];
-                        TN_LD32(tbase + c0, r);
-                        tc_wait_ld();
-                        store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_remote(tempty_leader0 + 8 * h);
+            const int row = mb * BMW + h * 256 + static_cast<int>(rank) * HALF + lane_base + lane;
+            const bool row_ok = row < p.M;
+            const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+            const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + h * 256;
+            if (p.epi == 1) {
+                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+            } else if (p.epi == 2) {
+                epilogue_qkv_rope(p, tbase, row, nb * BN, BN, row_ok);
+            } else {
+                epilogue_plain<BN>(p, tbase, off, nb * BN, row_ok, vec_ok);
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + 8 * h);
             tphase ^= 1;
         }
     }
@@ -1010,6 +1041,7 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         const bool ab = a.batch > 1 && a.sa != 0, bb = a.batch > 1 && a.sb != 0;
         ok = encode(&plan->ta, a.A, es, a.K, a.M, a.lda, ab ? a.batch : 1, a.sa, kBM) &&
              encode(&plan->tb, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, two_sm ? 128 : bn);
+        plan->tbh_ok = ok && two_sm && encode(&plan->tbh, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, 64);
     }
     plan->path = ok ? (two_sm ? 2 : 0) : 1;
     plan->bn = bn;
@@ -1021,17 +1053,17 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     }
     if (plan->path == 2 && tile == 2) plan->path = 3;
     if (plan->path == 2 && a.M > 256 && tile == 0) {
-        // Wide 512x256 pair tiles do ~5% more per pair-cycle (fewer operand
-        // bytes per FLOP) but quantise to whole waves; narrow tiles get a
-        // stream-K tail (no quantisation; ~15% overhead when every tile is
-        // split). Measured per shape on B200 (tools/gemm_bench.py).
+        // Wide 512x256 pair tiles do fewer operand bytes per FLOP but leave
+        // the epilogue exposed (no second accumulator): measured slower than
+        // narrow tiles on every 7B shape, so they are only picked when the
+        // narrow tiles quantise much worse (narrow tail: half a tile-time
+        // when the last wave fits in half-width tiles, else a full one).
         const int P = std::max(1, num_sms / 2);
         const long long tn = (a.N + 255) / 256;
         const long long narrow = a.batch * ((a.M + 255) / 256) * tn, wide = a.batch * ((a.M + 511) / 512) * tn;
-        const bool sk = a.causal == 0 && narrow >= P && narrow % P != 0;
-        const double t_narrow = sk ? static_cast<double>(narrow) / P * (narrow >= 2 * P ? 1.0 : 1.15)
-                                   : static_cast<double>((narrow + P - 1) / P);
-        const double t_wide = static_cast<double>((wide + P - 1) / P) * 2.0 / 1.05;
+        const long long rem = narrow % P;
+        const double t_narrow = static_cast<double>(narrow / P) + (rem == 0 ? 0.0 : 2 * rem <= P ? 0.5 : 1.0);
+        const double t_wide = static_cast<double>((wide + P - 1) / P) * 2.0 / 0.9;
         if (t_wide < t_narrow) plan->path = 3;
     }
     const int bm = plan->path == 2 ? 256 : plan->path == 3 ? 512 : kBM;
@@ -1041,17 +1073,30 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     if (plan->path == 3) plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
     if (plan->path == 2) {
         plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
-        // Stream-K tail when the tiles do not fill the last wave of pairs:
-        // the last partial wave plus one full wave are split by K blocks.
         const int npairs = plan->grid / 2, T = plan->tiles;
         const int nk = static_cast<int>((a.K * es + kAtom - 1) / kAtom);
-        if (a.causal == 0 && T >= npairs && T % npairs != 0) {
-            const int sk = T / npairs >= 2 ? T % npairs + npairs : T;
-            if (static_cast<long long>(sk) * nk >= 4LL * npairs) {
-                plan->sk_tiles = sk;
-                plan->sk_nk = nk;
-                plan->ws_bytes = static_cast<std::size_t>(npairs) * 2 * 128 * 256 * 4 + static_cast<std::size_t>(npairs) * 2 * 4;
+        // Tail of the last wave of pairs. Default: split its tiles into
+        // 256x128 halves when they fit in half the pairs (half a tile-time
+        // instead of a whole one). TN_GEMM_SK=1 selects the stream-K tail
+        // instead (last partial wave + one full wave split by K blocks);
+        // measured on B200 it never beat the plain or half-width tail
+        // (fix-up traffic + serialised finishers), so it is off by default.
+        static const char* sk_env = std::getenv("TN_GEMM_SK");
+        const bool sk_on = tile == 3 || (sk_env && std::strcmp(sk_env, "1") == 0);
+        const int P = std::max(1, num_sms / 2);
+        const int rem = T >= P ? T % P : T;
+        if (sk_on) {
+            if (a.causal == 0 && T >= npairs && T % npairs != 0) {
+                const int sk = T / npairs >= 2 ? T % npairs + npairs : T;
+                if (static_cast<long long>(sk) * nk >= 4LL * npairs) {
+                    plan->sk_tiles = sk;
+                    plan->sk_nk = nk;
+                    plan->ws_bytes = static_cast<std::size_t>(npairs) * 2 * 128 * 256 * 4 + static_cast<std::size_t>(npairs) * 2 * 4;
+                }
             }
+        } else if (a.causal == 0 && a.epi != 1 && rem > 0 && 2 * rem <= P && plan->tbh_ok) {
+            plan->half_tiles = 2 * rem;
+            plan->grid = 2 * std::min(P, T >= P ? P : 2 * rem);
         }
     }
     if (ok) {
@@ -1101,7 +1146,8 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
     p.epi = a.epi;
     p.rope = static_cast<const float*>(a.rope);
     p.heads = a.heads;
-    p.dp_tiles = plan.tiles;
+    p.dp_tiles = plan.tiles - plan.half_tiles / 2;
+    p.half_tiles = plan.half_tiles;
     p.sk_nk = 0;
     p.sk_total = 0;
     p.ws = nullptr;
@@ -1118,9 +1164,9 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
         p.epoch = ws->epoch;
     }
     if (plan.path == 3)
-        gemm_kernel_2sm_w<<<plan.grid, kThreads, smem_bytes_2sm_w(), s>>>(plan.ta, plan.tb, p);
+        gemm_kernel_2sm_w<<<plan.grid, kThreadsW, smem_bytes_2sm_w(), s>>>(plan.ta, plan.tb, p);
     else if (plan.path == 2)
-        gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, p);
+        gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, plan.tbh, p);
     else if (plan.bn == 128)
         gemm_kernel<128><<<plan.grid, kThreads, smem_bytes<128>(), s>>>(plan.ta, plan.tb, p);
     else if (plan.bn == 64)

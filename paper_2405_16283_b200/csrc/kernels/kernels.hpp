@@ -37,12 +37,14 @@ struct GemmArgs {
                   // 2: QKV + RoPE epilogue (hd 128): out = [rope(q) (H,M,128) | rope(k) | vᵀ (H,128,M)]
     const void* rope = nullptr;  // epi 2: fp32 [M, 64, 2] (cos, sin)
     int heads = 0;               // epi 2: heads per section, N = 3 * heads * 128
-    int tile = 0;                // CTA-pair tile: 0 auto, 1 narrow (256x256), 2 wide (512x256)
+    int tile = 0;                // CTA-pair tile: 0 auto, 1 narrow (256x256), 2 wide (512x256),
+                                 // 3 narrow with a stream-K tail (instead of half-width tail tiles)
 };
 
 struct alignas(64) GemmPlan {
     CUtensorMap ta;  // A: (K, M, batch)
     CUtensorMap tb;  // B: (K, N, batch)
+    CUtensorMap tbh; // B with 64-row boxes (half-width tail tiles of the CTA-pair path)
     GemmArgs args;
     int path = 0;    // 0 tcgen05 1-CTA, 2 tcgen05 CTA pair (cta_group::2), 1 SIMT fallback
     int bn = 256;    // N tile of the tcgen05 path
@@ -51,6 +53,8 @@ struct alignas(64) GemmPlan {
     int sk_tiles = 0;          // path 2: trailing tiles split by K blocks across all pairs (stream-K)
     int sk_nk = 0;             // K blocks per stream-K tile
     std::size_t ws_bytes = 0;  // workspace the stream-K tail needs (0: none)
+    int half_tiles = 0;        // path 2: trailing tiles run as 2 x 256x128 halves (count of halves)
+    bool tbh_ok = false;
 };
 
 // Stream-K scratch: per-pair fp32 partial slots + publication flags. One per

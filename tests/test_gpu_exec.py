@@ -58,10 +58,15 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=512, N=1024, K=256, epilogue="swiglu"),   # fused SwiGLU, CTA pair
     dict(M=128, N=512, K=128, epilogue="swiglu"),    # fused SwiGLU, 1-CTA
     dict(M=8, N=512, K=128, epilogue="swiglu"),      # fused SwiGLU, SIMT
-    dict(M=2304, N=2304, K=512, out_dtype="f32", tile="narrow"),  # 81 pair tiles: all stream-K
-    dict(M=4096, N=4096, K=1024, residual=True, tile="narrow"),   # 256 tiles: 2 DP waves + stream-K tail
-    dict(M=2304, N=2304, K=256, in_dtype="f32", out_dtype="f32", tile="narrow"),  # tf32 stream-K
-    dict(M=1280, N=1280, K=256, batch=4, out_dtype="f32", tile="narrow"),         # batched stream-K
+    dict(M=2304, N=2304, K=512, out_dtype="f32", tile="streamk"),  # 81 pair tiles: all stream-K
+    dict(M=4096, N=4096, K=1024, residual=True, tile="streamk"),   # 256 tiles: 2 DP waves + stream-K tail
+    dict(M=2304, N=2304, K=256, in_dtype="f32", out_dtype="f32", tile="streamk"),  # tf32 stream-K
+    dict(M=1280, N=1280, K=256, batch=4, out_dtype="f32", tile="streamk"),         # batched stream-K
+    dict(M=2304, N=2304, K=512, out_dtype="f32", tile="narrow"),   # 74 full tiles + 7 tiles as 14 halves
+    dict(M=4096, N=4096, K=1024, residual=True, tile="narrow"),    # 3 waves + 34 tiles as 68 halves
+    dict(M=2304, N=2304, K=256, in_dtype="f32", out_dtype="f32", tile="narrow"),  # tf32 half tail
+    dict(M=1280, N=1280, K=256, batch=4, out_dtype="f32", tile="narrow"),         # batched half tail
+    dict(M=1000, N=600, K=320, residual=True, tile="narrow"),      # all-half tiles, ragged M/N (N tail half OOB)
     dict(M=4096, N=4096, K=1024, residual=True),     # wide 512x256 pair tiles (auto)
     dict(M=1000, N=520, K=320, residual=True, tile="wide"),        # wide, ragged M/N
     dict(M=1024, N=768, K=512, out_dtype="f32", tile="wide", alpha=0.25),
@@ -70,7 +75,8 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=1024, N=512, K=1024, batch=2, causal=2, tile="wide"),
     dict(M=1536, N=1024, K=256, epilogue="swiglu", tile="wide"),  # wide + fused SwiGLU
     dict(M=512, N=256, K=4096, tile="wide"),         # long K: deferred half-1 MMAs cycle the ring
-    dict(M=2304, N=2304, K=256, epilogue="swiglu", tile="narrow"),  # stream-K + fused SwiGLU
+    dict(M=2304, N=2304, K=256, epilogue="swiglu", tile="streamk"),  # stream-K + fused SwiGLU
+    dict(M=2304, N=2304, K=256, epilogue="swiglu", tile="narrow"),  # SwiGLU never takes half tiles
 ])
 def test_gemm_parity(shape):
     shape = dict(shape)
@@ -94,10 +100,12 @@ def test_gemm_parity(shape):
     assert rel_err(x, y) < tol
 
 
-@pytest.mark.parametrize("tile,S,H", [("narrow", 1024, 4), ("wide", 1024, 4), ("narrow", 4096, 8)])
+@pytest.mark.parametrize("tile,S,H", [("narrow", 1024, 4), ("wide", 1024, 4), ("narrow", 4096, 8),
+                                     ("streamk", 4096, 8), ("narrow", 2048, 8)])
 def test_gemm_qkv_rope_epilogue_tiles(tile, S, H):
-    """Fused QKV + RoPE + Vᵀ epilogue on both CTA-pair tile shapes (and with a
-    stream-K tail: 192 pair tiles) vs the oracle."""
+    """Fused QKV + RoPE + Vᵀ epilogue on every CTA-pair tile shape vs the
+    oracle: S=1024,H=4 is 24 tiles, all run as one-head halves; S=2048,H=8 is
+    96 tiles, the last 22 as halves; streamk splits 192 tiles by K."""
     d = 512
     g = W.GraphBuilder()
     x = g.input("x", (S, d), "bf16", init=("normal", 1.0))
@@ -115,7 +123,7 @@ def test_gemm_qkv_rope_epilogue_tiles(tile, S, H):
 def test_gemm_stream_k_deterministic():
     """Stream-K partial sums are combined in a fixed order: repeated runs
     through one executor (advancing the workspace epoch) are bitwise equal."""
-    g = gemm_graph(4096, 4096, 2048, tile="narrow")
+    g = gemm_graph(4096, 4096, 2048, tile="streamk")
     mg, _ = W.plan(g, 1 << 30)
     (o,) = g.outputs()
     outs = []

@@ -1,19 +1,32 @@
-"""Summarises an ncu --metrics gpu__time_duration.sum launch list (CSV)."""
-import collections, csv, re, sys
-rows = list(csv.reader(open(sys.argv[1])))
+"""Summarises an ncu --metrics gpu__time_duration.sum launch list (CSV).
+
+    python tools/launches.py launches.csv [--last N] [--dump out.csv]
+--last N keeps only the last N tn:: launches (e.g. one step); --dump writes
+those rows (tn:: kernels only) as a compact CSV for profiles/."""
+import argparse, collections, csv, re
+
+ap = argparse.ArgumentParser()
+ap.add_argument("csv")
+ap.add_argument("--last", type=int, default=0)
+ap.add_argument("--dump", default=None)
+a = ap.parse_args()
+rows = list(csv.reader(open(a.csv)))
 for i, r in enumerate(rows):
     if r and r[0] == "ID":
         hdr, start = r, i + 1
         break
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+ours = [r for r in rows[start:] if len(r) > vi and r[ki].startswith(("tn::", "void tn::"))]
+if a.last:
+    ours = ours[-a.last:]  # torch kernels of the input generator run before the step
+if a.dump:
+    with open(a.dump, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(hdr)
+        w.writerows(ours)
 agg = collections.defaultdict(lambda: [0, 0.0])
-for r in rows[start:]:
-    if len(r) <= vi:
-        continue
-    name = r[ki]
-    if not name.startswith(("tn::", "void tn::")):
-        continue  # torch kernels of the input generator run before the step
-    name = re.sub(r"\(anonymous namespace\)::", "", name.replace("void ", ""))
+for r in ours:
+    name = re.sub(r"\(anonymous namespace\)::", "", r[ki].replace("void ", ""))
     name = re.sub(r"\(.*$", "", name)
     v = float(r[vi].replace(",", ""))
     v = {"ns": v / 1e3, "nsecond": v / 1e3, "ms": v * 1e3, "msecond": v * 1e3}.get(r[ui], v)  # -> microseconds
