@@ -215,10 +215,34 @@ def roofline_from_trace(g, trace, peak_tflops):
             dur += d
             launches += 1
     ach = fl / dur / 1e12 if dur > 0 else 0.0
+    alg_bytes = sum(gemm_bytes(g, ids[r["vertex"]]) for r in trace["rows"]
+                    if r["vertex"] in ids and (ids[r["vertex"]].get("op") or {}).get("type") == "gemm")
+    traffic, src = gemm_traffic()
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
-            "frac": round(ach / peak_tflops, 4), "traffic": None, "kernel": "gemm_tcgen05 (all GEMM tasks)",
+            "frac": round(ach / peak_tflops, 4), "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
+            "traffic_source": src, "algorithmic_bytes_per_launch": round(alg_bytes / max(1, launches)),
+            "kernel": "gemm_tcgen05 (all GEMM tasks)",
             "launches_per_step": launches, "algorithmic_flops_per_step": fl,
             "gemm_device_s_per_step": round(dur, 6)}, by_type
+
+
+def gemm_bytes(g, v) -> int:
+    """Algorithmic HBM bytes of one GEMM task: its operands and its output,
+    each touched once (A, B, optional residual/rope table, C)."""
+    ins = sum(g.tensors[a].nbytes for a in v["op"]["args"] if a in g.tensors)
+    return ins + g.tensors[v["id"]].nbytes
+
+
+def gemm_traffic():
+    """DRAM bytes per GEMM launch from the committed `ncu --set full` capture
+    of one layer's four GEMM classes (each class is 1/4 of the step's GEMM
+    launches, so the plain mean is the per-launch average)."""
+    p = os.path.join(ROOT, "profiles", "r1_ncu_gemm.json")
+    try:
+        ls = json.load(open(p))["launches"]
+        return round(sum(x["dram_bytes"] for x in ls) / len(ls)), "profiles/r1_ncu_gemm.json"
+    except Exception:
+        return None, None
 
 
 # --------------------------------------------------------------- CPU sample ---
