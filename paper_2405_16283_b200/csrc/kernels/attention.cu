@@ -195,10 +195,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             float ps[kW];
 #pragma unroll
             for (int w = 0; w < kW; ++w) ps[w] = 0.f;
+            // x = s*scale - mx, 2^x, per-column-class partial sums: packed
+            // FFMA2/FADD2 (bitwise the same as the scalar fmaf / += chain)
 #pragma unroll
-            for (int c = 0; c < kN; ++c) {
-                s[c] = ex2(fmaf(s[c], p.scale_log2, -mx));
-                ps[c % kW] += s[c];
+            for (int c = 0; c < kN; c += 2) {
+                fma2(s[c], s[c + 1], p.scale_log2, -mx);
+                s[c] = ex2(s[c]);
+                s[c + 1] = ex2(s[c + 1]);
+                add2(ps[c % kW], ps[c % kW + 1], s[c], s[c + 1]);
             }
 #pragma unroll
             for (int w = kW / 2; w > 0; w /= 2)

@@ -134,6 +134,21 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// Packed fp32 pairs (FFMA2 / FADD2, sm_100): each lane is rounded exactly
+// like the scalar fmaf / fadd, at half the issue cost.
+__device__ __forceinline__ void fma2(float& a, float& b, float m, float c) {  // a = a*m + c, b = b*m + c
+    asm("{\n\t.reg .b64 t, u, v;\n\tmov.b64 t, {%0, %1};\n\tmov.b64 u, {%2, %2};\n\tmov.b64 v, {%3, %3};\n\t"
+        "fma.rn.f32x2 t, t, u, v;\n\tmov.b64 {%0, %1}, t;\n\t}"
+        : "+f"(a), "+f"(b)
+        : "f"(m), "f"(c));
+}
+__device__ __forceinline__ void add2(float& a, float& b, float x, float y) {  // a += x, b += y
+    asm("{\n\t.reg .b64 t, u;\n\tmov.b64 t, {%0, %1};\n\tmov.b64 u, {%2, %3};\n\t"
+        "add.rn.f32x2 t, t, u;\n\tmov.b64 {%0, %1}, t;\n\t}"
+        : "+f"(a), "+f"(b)
+        : "f"(x), "f"(y));
+}
+
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
