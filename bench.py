@@ -398,6 +398,7 @@ def run_ours(args, world, rank, local):
         "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": st_e["h2d_bytes"],
                 "d2h_bytes_per_step": logits_bytes + st_e["d2h_bytes"], "ms_per_step": round(e2e_step * 1e3, 2),
                 "exposed_transfer_s": round(st_e["exposed_transfer_s"], 4),
+                "exposed_transfer_gpu_s": round(st_e.get("exposed_transfer_gpu_s", st_e["exposed_transfer_s"]), 4),
                 "pcie_h2d_gbs_measured": round(pcie, 1),
                 "achieved_h2d_gbs": round(st_e["h2d_bytes"] / e2e_step / 1e9, 1)},
         "gpu_launches": st_v["kernel_launches"] * args.steps,

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -882,24 +883,38 @@ ExecutionTrace Executor::Impl::build_trace() {
         }
         return out;
     };
-    double exposed = 0, busy_k = 0;
-    for (int d = 0; d < D; ++d) {
-        auto K = unite(kspans[d]), C = unite(cspans[d]);
-        for (auto& kk : K) busy_k += kk.second - kk.first;
+    auto exposed_of = [&](std::vector<std::pair<double, double>> ks, std::vector<std::pair<double, double>> cs,
+                          double* busy) {
+        auto K = unite(ks), C = unite(cs);
+        for (auto& kk : K) *busy += kk.second - kk.first;
+        double ex = 0;
         size_t j = 0;
         for (auto& c : C) {
             double covered = 0;
             while (j < K.size() && K[j].second <= c.first) ++j;
             for (size_t q = j; q < K.size() && K[q].first < c.second; ++q)
                 covered += std::min(c.second, K[q].second) - std::max(c.first, K[q].first);
-            exposed += (c.second - c.first) - covered;
+            ex += (c.second - c.first) - covered;
         }
+        return ex;
+    };
+    double exposed = 0, busy_k = 0, exposed_gpu = 0, busy_gpu = 0;
+    for (int d = 0; d < D; ++d) exposed += exposed_of(kspans[d], cspans[d], &busy_k);
+    // The same per physical GPU: memgraph devices sharing a GPU cover each
+    // other's copies (times share one origin per GPU).
+    std::map<int, std::pair<std::vector<std::pair<double, double>>, std::vector<std::pair<double, double>>>> per_gpu;
+    for (int d = 0; d < D; ++d) {
+        auto& pg = per_gpu[ordinal[d]];
+        pg.first.insert(pg.first.end(), kspans[d].begin(), kspans[d].end());
+        pg.second.insert(pg.second.end(), cspans[d].begin(), cspans[d].end());
     }
+    for (auto& [gpu, pg] : per_gpu) exposed_gpu += exposed_of(pg.first, pg.second, &busy_gpu);
     last.makespan_s = t.makespan;
     last.kernel_time_s = kernel_s;
     last.copy_time_s = copy_s;
     last.kernel_busy_s = busy_k;
     last.exposed_transfer_s = exposed;
+    last.exposed_transfer_gpu_s = exposed_gpu;
     return t;
 }
 
@@ -1030,6 +1045,7 @@ std::string RunStats::to_json() const {
     j["kernel_busy_s"] = kernel_busy_s;
     j["copy_time_s"] = copy_time_s;
     j["exposed_transfer_s"] = exposed_transfer_s;
+    j["exposed_transfer_gpu_s"] = exposed_transfer_gpu_s;
     return j.dump();
 }
 

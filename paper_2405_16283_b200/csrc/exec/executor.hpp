@@ -37,6 +37,7 @@ struct RunStats {
     std::int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_bytes = 0, d2d_bytes = 0, d2h_elided_bytes = 0;
     double flops = 0, makespan_s = 0, wall_s = 0;
     double kernel_time_s = 0, kernel_busy_s = 0, copy_time_s = 0, exposed_transfer_s = 0;
+    double exposed_transfer_gpu_s = 0;  // same, per physical GPU (devices sharing a GPU cover each other)
     std::string to_json() const;
 };
 
