@@ -216,3 +216,61 @@ def test_lora_step_gradients_match_torch_autograd():
     for k, ref in grads.items():
         o = name[k]
         assert rel_err(out_values(g, o, got[o]), ref.reshape(-1)) < 5e-2, k
+
+
+def test_llama_graph_matches_hf_transformers():
+    """Pins the LLaMA taskgraph semantics (rotate-half RoPE, RMSNorm, SwiGLU
+    with the interleaved gate/up rows of the fused epilogue, causal softmax
+    attention, last-token head) to an independent implementation: HF
+    transformers' LlamaForCausalLM in fp32 with the same (bf16-valued)
+    weights. The oracle stores every vertex output in bf16, HF keeps fp32
+    activations, so the logits agree to bf16 activation rounding (tol 2e-2)."""
+    import pytest
+    torch = pytest.importorskip("torch")
+    tr = pytest.importorskip("transformers")
+    from oracle import ops_ref as R
+    cfg, S, L = W.LlamaConfig(dim=256, layers=2, heads=2, ffn=512, vocab=300), 64, 2
+    g = W.llama_prefill(cfg, S, layers=L)
+    mg, _ = W.plan(g, 1 << 30)
+    inp = inputs_of(g, seed=7)
+    (o,) = g.outputs()
+    ours = out_values(g, o, oracle_outputs(g, mg, inp)[o])
+    byname = {g.tensors[v].name: (g.tensors[v], a) for v, a in inp.items()}
+
+    def T(name):
+        t, a = byname[name]
+        if t.dtype == "bf16":
+            return torch.tensor(R.bf16_to_f32(a).reshape(t.shape))
+        return torch.tensor(np.asarray(a).reshape(t.shape))
+
+    hc = tr.LlamaConfig(hidden_size=cfg.dim, intermediate_size=cfg.ffn, num_hidden_layers=L,
+                        num_attention_heads=cfg.heads, num_key_value_heads=cfg.heads, vocab_size=cfg.vocab,
+                        rms_norm_eps=cfg.eps, rope_theta=cfg.theta, max_position_embeddings=S,
+                        tie_word_embeddings=False, attention_bias=False, mlp_bias=False)
+    hc._attn_implementation = "eager"
+    m = tr.LlamaForCausalLM(hc).float().eval()
+    d, f = cfg.dim, cfg.ffn
+    idx = np.arange(2 * f).reshape(-1, 2, 128)  # w13 rows: (gate block b, up block b) interleaved by 128
+    gate_rows, up_rows = idx[:, 0].reshape(-1), idx[:, 1].reshape(-1)
+    with torch.no_grad():
+        m.model.embed_tokens.weight.copy_(T("tok_embeddings"))
+        for l, layer in enumerate(m.model.layers):
+            p = f"layers.{l}."
+            wqkv, w13 = T(p + "wqkv"), T(p + "w13")
+            layer.input_layernorm.weight.copy_(T(p + "attention_norm"))
+            layer.self_attn.q_proj.weight.copy_(wqkv[:d])
+            layer.self_attn.k_proj.weight.copy_(wqkv[d:2 * d])
+            layer.self_attn.v_proj.weight.copy_(wqkv[2 * d:])
+            layer.self_attn.o_proj.weight.copy_(T(p + "wo"))
+            layer.post_attention_layernorm.weight.copy_(T(p + "ffn_norm"))
+            layer.mlp.gate_proj.weight.copy_(w13[gate_rows])
+            layer.mlp.up_proj.weight.copy_(w13[up_rows])
+            layer.mlp.down_proj.weight.copy_(T(p + "w2"))
+        m.model.norm.weight.copy_(T("norm"))
+        m.lm_head.weight.copy_(T("output"))
+        tok = torch.tensor(np.asarray(byname["tokens"][1]).astype(np.int64).reshape(1, S))
+        ref = m(input_ids=tok).logits[0, -1].double().numpy()
+    err = rel_err(ours, ref)
+    print("oracle vs HF transformers fp32, last-token logits: rel err", err)
+    assert err < 2e-2
+    assert int(np.argmax(ours)) == int(np.argmax(ref))
