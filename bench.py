@@ -215,6 +215,20 @@ def roofline_from_trace(g, trace, peak_tflops):
             dur += d
             launches += 1
     ach = fl / dur / 1e12 if dur > 0 else 0.0
+    classes = {}
+    for r in trace["rows"]:
+        v = ids.get(r["vertex"])
+        op = (v or {}).get("op") or {}
+        if op.get("type") != "gemm":
+            continue
+        key = f"{op['M']}x{op['N']}x{op['K']}" + (f"/{op['epilogue']}" if op.get("epilogue") else "") + \
+              ("+res" if len(op["args"]) > 2 and not op.get("epilogue") else "")
+        c = classes.setdefault(key, [0, 0.0, 0.0])
+        c[0] += 1
+        c[1] += r["end"] - r["start"]
+        c[2] += gemm_flops(op)
+    by_class = {k: {"n": n, "ms": round(t * 1e3, 3), "tflops": round(f / t / 1e12, 1) if t > 0 else None}
+                for k, (n, t, f) in sorted(classes.items(), key=lambda kv: -kv[1][1])}
     alg_bytes = sum(gemm_bytes(g, ids[r["vertex"]]) for r in trace["rows"]
                     if r["vertex"] in ids and (ids[r["vertex"]].get("op") or {}).get("type") == "gemm")
     traffic, src = gemm_traffic()
@@ -223,7 +237,7 @@ def roofline_from_trace(g, trace, peak_tflops):
             "traffic_source": src, "algorithmic_bytes_per_launch": round(alg_bytes / max(1, launches)),
             "kernel": "gemm_tcgen05 (all GEMM tasks)",
             "launches_per_step": launches, "algorithmic_flops_per_step": fl,
-            "gemm_device_s_per_step": round(dur, 6)}, by_type
+            "gemm_device_s_per_step": round(dur, 6), "gemm_classes": by_class}, by_type
 
 
 def gemm_bytes(g, v) -> int:

@@ -54,11 +54,13 @@ struct Params {
     // owns a tile's first K block, in ascending pair order (deterministic).
     int dp_tiles, sk_nk;
     long long sk_total;
-    // Half-width tail (CTA-pair kernel, default): when the last wave of
-    // 256x256 tiles would leave more than half the pairs idle, its tiles are
-    // split into two 256x128 halves (N=128 MMAs, 64 B rows per CTA), so the
-    // tail costs half a tile-time. Tiles [dp_tiles, dp_tiles + half_tiles/2).
-    int half_tiles;
+    // Sliced tail (CTA-pair kernels, default): the tiles of the last, partial
+    // wave of pairs are each split into `tail_split` (2 or 4) N-slices of
+    // 256/tail_split accumulator columns (N=128/64 MMAs), so the tail costs
+    // 1/tail_split of a tile-time when the slices fit in one wave. Tiles
+    // [dp_tiles, dp_tiles + tail_units / tail_split).
+    int tail_split, tail_units;
+    int tma_c;  // 1: plain/SwiGLU epilogues store through smem staging + TMA (tensor map `tc`)
     float* ws;
     unsigned* flags;  // per CTA of each pair: epoch of its last published partial
     unsigned epoch;
@@ -154,19 +156,129 @@ __device__ __forceinline__ void store_chunk(const Params& p, const std::uint32_t
     }
 }
 
+// --- TMA-store epilogue ------------------------------------------------------
+// Each epilogue warp owns two 2 KB staging buffers, each one {64 B x 32 rows}
+// TMA box in the SWIZZLE_64B layout (16-byte chunk q of row r at
+// r*64 + ((q ^ ((r >> 1) & 3)) << 4): a warp's 16-byte stores hit 8 distinct
+// bank groups, i.e. the ideal 4 wavefronts per 512 B). A 32-column chunk of
+// accumulator rows (one row per lane) is packed into a buffer and one lane
+// issues cp.async.bulk.tensor: full-line global writes, asynchronous, so the
+// warp (and the TMEM columns it drained) is free as soon as the smem writes
+// are fenced. Replaces 32 scattered rows per store instruction.
+constexpr int kStgBuf = 2048;
+constexpr int kStgWarp = 2 * kStgBuf;
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, std::uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<std::uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(std::uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+struct Stager {
+    std::uint32_t base;  // this warp's two buffers
+    int n;               // boxes issued so far (buffer = n & 1)
+};
+
+// Alpha and residual of one 32-column chunk of this lane's row (vector path).
+__device__ __forceinline__ void chunk_values(const Params& p, const std::uint32_t* r, std::int64_t off, int n0,
+                                             bool row_ok, float* v) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+    if (!p.R || !row_ok || n0 >= p.N) return;
+    if (p.out_dtype == BF16) {
+        const uint4* rr = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.R) + off + n0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint4 x = rr[q];
+            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&x);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[q * 8 + j] += __bfloat162float(h[j]);
+        }
+    } else {
+        const float4* rr = reinterpret_cast<const float4*>(static_cast<const float*>(p.R) + off + n0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            float4 x = rr[q];
+            v[q * 4 + 0] += x.x;
+            v[q * 4 + 1] += x.y;
+            v[q * 4 + 2] += x.z;
+            v[q * 4 + 3] += x.w;
+        }
+    }
+}
+
+// Stages a 32-column chunk (values for rows row0 + lane, columns n0..n0+31 of
+// batch b) and stores it with TMA; out-of-range rows/columns are clipped by
+// the tensor map. bf16: one box; fp32: two 16-column boxes.
+__device__ __forceinline__ void stage_chunk(const Params& p, const CUtensorMap* tc, Stager& st, const float* v,
+                                            int row0, int n0, int b) {
+    const int lane = threadIdx.x % 32;
+    const std::uint32_t sw = static_cast<std::uint32_t>((lane >> 1) & 3);
+    const int nbox = p.out_dtype == BF16 ? 1 : 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (h >= nbox) break;
+        const std::uint32_t buf = st.base + static_cast<std::uint32_t>(st.n & 1) * kStgBuf;
+        if (lane == 0) bulk_wait_read1();  // the box issued from this buffer two boxes ago has been read
+        __syncwarp();
+        uint4 w[4];
+        if (p.out_dtype == BF16) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                w[q] = make_uint4(pack_bf16(v[q * 8 + 0], v[q * 8 + 1]), pack_bf16(v[q * 8 + 2], v[q * 8 + 3]),
+                                  pack_bf16(v[q * 8 + 4], v[q * 8 + 5]), pack_bf16(v[q * 8 + 6], v[q * 8 + 7]));
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                w[q] = make_uint4(__float_as_uint(v[h * 16 + q * 4 + 0]), __float_as_uint(v[h * 16 + q * 4 + 1]),
+                                  __float_as_uint(v[h * 16 + q * 4 + 2]), __float_as_uint(v[h * 16 + q * 4 + 3]));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st_shared_v4(buf + lane * 64 + ((static_cast<std::uint32_t>(q) ^ sw) << 4), w[q]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_3d(tc, buf, n0 + h * 16, row0, b);
+            bulk_commit();
+        }
+        ++st.n;
+    }
+}
+
+// Plain epilogue through the stager: 128-row x width accumulator slab.
+__device__ __forceinline__ void epilogue_plain_tma(const Params& p, const CUtensorMap* tc, Stager& st,
+                                                   std::uint32_t tbase, std::int64_t off, int row0, int n0, int width,
+                                                   int b, bool row_ok) {
+#pragma unroll 1
+    for (int c0 = 0; c0 < width; c0 += 32) {
+        std::uint32_t r[32];
+        TN_LD32(tbase + c0, r);
+        tc_wait_ld();
+        float v[32];
+        chunk_values(p, r, off, n0 + c0, row_ok, v);
+        stage_chunk(p, tc, st, v, row0, n0 + c0, b);
+    }
+}
+
 // SwiGLU epilogue: the N tile holds 128-column gate/up block pairs (the
 // weight rows are interleaved that way), so each output column needs two
 // TMEM columns of the same row: out = silu(alpha*g) * (alpha*u).
-template <int BN>
-__device__ __forceinline__ void epilogue_swiglu(const Params& p, std::uint32_t tbase, std::int64_t off, int nb,
-                                                bool row_ok) {
+__device__ __forceinline__ void epilogue_swiglu(const Params& p, std::uint32_t tbase, std::int64_t off, int H,
+                                                int out0, bool row_ok) {
     Params q = p;
     q.N = p.N / 2;
     q.alpha = 1.0f;
     q.R = nullptr;
     const int ob = p.out_dtype == BF16 ? 2 : 4;
     const bool vec_ok = (q.N % 32 == 0) && ((q.ldc * ob) % 16 == 0) && ((reinterpret_cast<std::uintptr_t>(q.C) & 15) == 0);
-    constexpr int H = BN / 2;
 #pragma unroll 1
     for (int c0 = 0; c0 < H; c0 += 32) {
         std::uint32_t g[32], u[32];
@@ -178,7 +290,26 @@ __device__ __forceinline__ void epilogue_swiglu(const Params& p, std::uint32_t t
             const float x = __uint_as_float(g[j]) * p.alpha, y = __uint_as_float(u[j]) * p.alpha;
             g[j] = __float_as_uint(x / (1.0f + __expf(-x)) * y);
         }
-        store_chunk(q, g, off, nb * H + c0, row_ok, vec_ok);
+        store_chunk(q, g, off, out0 + c0, row_ok, vec_ok);
+    }
+}
+
+// H: gate (= up) columns in the accumulator ([gate | up]); out0: first output column.
+__device__ __forceinline__ void epilogue_swiglu_tma(const Params& p, const CUtensorMap* tc, Stager& st,
+                                                    std::uint32_t tbase, int row0, int H, int out0, int b) {
+#pragma unroll 1
+    for (int c0 = 0; c0 < H; c0 += 32) {
+        std::uint32_t g[32], u[32];
+        TN_LD32(tbase + c0, g);
+        TN_LD32(tbase + H + c0, u);
+        tc_wait_ld();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float x = __uint_as_float(g[j]) * p.alpha, y = __uint_as_float(u[j]) * p.alpha;
+            v[j] = x / (1.0f + __expf(-x)) * y;
+        }
+        stage_chunk(p, tc, st, v, row0, out0 + c0, b);
     }
 }
 
@@ -370,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
             if (p.epi == 1) {
-                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+                epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok);
             } else if (p.epi == 2) {
                 epilogue_qkv_rope(p, tbase, row, nb * BN, BN, row_ok);
             } else {
@@ -460,9 +591,20 @@ __device__ __forceinline__ int sk_owner(const Params& p, long long it, int npair
     while (q > 0 && sk_begin(p, q, npairs) > it) --q;
     return q;
 }
-// Visits this pair's work as (tile, K-block range, columns) segments: its
-// round-robin data-parallel tiles, then its half-width tail tiles, then its
-// contiguous slice of the stream-K blocks. f(b, mb, n0, width, kb0, kb1, nk, it0).
+// B rows staged by CTA `rank` for slice k of s of N tile nb (256 accumulator
+// columns; each CTA of the pair stages half of the slice's B rows). A plain
+// tile's slice is GEMM columns [nb*256 + k*256/s, +256/s). A SwiGLU tile
+// (128 gate rows then the matching 128 up rows) keeps the pairing: rank 0
+// stages the slice's gate rows and rank 1 the matching up rows, so the
+// accumulator holds [gate | up] halves of 128/s columns each.
+__device__ __forceinline__ int slice_brow(const Params& p, int nb, int k, int s, int rank) {
+    const int w = 256 / s;
+    return p.epi == 1 ? nb * 256 + rank * 128 + k * (w / 2) : nb * 256 + k * w + rank * (w / 2);
+}
+
+// Visits this pair's work as (tile, N-slice, K-block range) segments: its
+// round-robin data-parallel tiles, then its share of the sliced tail, then
+// its contiguous slice of the stream-K blocks. f(b, mb, nb, k, s, kb0, kb1, nk, it0).
 template <class F>
 __device__ __forceinline__ void for_each_segment(const Params& p, int pair, int npairs, int bk, F&& f) {
     constexpr int BN = 256, BM2 = 256;
@@ -472,13 +614,13 @@ __device__ __forceinline__ void for_each_segment(const Params& p, int pair, int 
         if (p.causal == 1 && nb * BN > mb * BM2 + BM2 - 1) continue;
         int nk = (p.K + bk - 1) / bk;
         if (p.causal == 2) nk = min(nk, ((mb + 1) * BM2 + bk - 1) / bk);
-        f(b, mb, nb * BN, BN, 0, nk, nk, 0LL);
+        f(b, mb, nb, 0, 1, 0, nk, nk, 0LL);
     }
-    for (int u = pair; u < p.half_tiles; u += npairs) {  // causal == 0 only
+    for (int u = pair; u < p.tail_units; u += npairs) {  // causal == 0 only
         int b, mb, nb;
-        decode(p, p.dp_tiles + u / 2, b, mb, nb);
+        decode(p, p.dp_tiles + u / p.tail_split, b, mb, nb);
         const int nk = (p.K + bk - 1) / bk;
-        f(b, mb, nb * BN + (u & 1) * (BN / 2), BN / 2, 0, nk, nk, 0LL);
+        f(b, mb, nb, u % p.tail_split, p.tail_split, 0, nk, nk, 0LL);
     }
     if (p.sk_total <= 0) return;
     const long long end = sk_begin(p, pair + 1, npairs);
@@ -488,7 +630,7 @@ __device__ __forceinline__ void for_each_segment(const Params& p, int pair, int 
         const int kb1 = static_cast<int>(min(static_cast<long long>(p.sk_nk), kb0 + (end - it)));
         int b, mb, nb;
         decode(p, tt, b, mb, nb);
-        f(b, mb, nb * BN, BN, kb0, kb1, p.sk_nk, it - kb0);
+        f(b, mb, nb, 0, 1, kb0, kb1, p.sk_nk, it - kb0);
         it += kb1 - kb0;
     }
 }
@@ -507,7 +649,8 @@ __device__ __forceinline__ void mbar_arrive_remote(std::uint32_t cluster_addr) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel_2sm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                    const __grid_constant__ CUtensorMap tbh, const Params p) {
+                    const __grid_constant__ CUtensorMap tbh, const __grid_constant__ CUtensorMap tbq,
+                    const __grid_constant__ CUtensorMap tc, const Params p) {
     constexpr int HALF = 128;                  // rows of A and of B staged per CTA
     constexpr int A_BYTES = HALF * kAtom;      // 16 KB
     constexpr int STAGE = 2 * A_BYTES;         // 32 KB per CTA
@@ -519,7 +662,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const std::uint32_t pad = ((raw + 1023) & ~1023u) - raw;
     std::uint8_t* smem = smem_raw + pad;
     const std::uint32_t sbase = raw + pad;
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStages2 * STAGE);
+    const std::uint32_t stg = sbase + kStages2 * STAGE;  // 4 epilogue warps x kStgWarp
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStages2 * STAGE + 4 * kStgWarp);
     const std::uint32_t full = smem_u32(bars), empty = full + 8 * kStages2;
     const std::uint32_t tfull = empty + 8 * kStages2, tempty = tfull + 16;
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages2 + 4);
@@ -534,7 +678,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&ta)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tb)) : "memory");
-        if (p.half_tiles > 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tbh)) : "memory");
+        if (p.tail_units > 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(p.tail_split == 2 ? &tbh : &tbq))
+                         : "memory");
+        }
         for (int s = 0; s < kStages2; ++s) {
             mbar_init(full + 8 * s, 1);
             mbar_init(empty + 8 * s, 1);
@@ -562,16 +709,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             std::uint32_t phase = 0;
-            for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int n0, int w, int kb0, int kb1, int, long long) {
-                const int brows = w / 2;  // B rows staged per CTA
+            for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int nb, int k, int sl, int kb0, int kb1, int, long long) {
+                const int brows = BN / 2 / sl;  // B rows staged per CTA
+                const CUtensorMap* mb_map = sl == 1 ? &tb : sl == 2 ? &tbh : &tbq;
+                const int brow = slice_brow(p, nb, k, sl, static_cast<int>(rank));
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty + 8 * stage, phase ^ 1);
                     const std::uint32_t fb = full_leader0 + 8 * stage;
                     if (leader) mbar_expect_tx(full + 8 * stage, 2 * (A_BYTES + brows * kAtom));
                     const std::uint32_t sa = sbase + stage * STAGE;
                     tma_load_3d_2sm(sa, &ta, kb * bk, mb * BM2 + rank * HALF, p.a_batched ? b : 0, fb);
-                    tma_load_3d_2sm(sa + A_BYTES, w == BN ? &tb : &tbh, kb * bk, n0 + rank * brows,
-                                    p.b_batched ? b : 0, fb);
+                    tma_load_3d_2sm(sa + A_BYTES, mb_map, kb * bk, brow, p.b_batched ? b : 0, fb);
                     if (++stage == kStages2) {
                         stage = 0;
                         phase ^= 1;
@@ -581,12 +729,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (leader) {  // whole warp: one elected lane issues (tc_mma_2sm)
-            const std::uint32_t idesc_full = make_idesc(tf32 ? 2u : 1u, BM2, BN);
-            const std::uint32_t idesc_half = make_idesc(tf32 ? 2u : 1u, BM2, BN / 2);
+            const std::uint32_t fmt = tf32 ? 2u : 1u;
             int stage = 0, acc = 0;
             std::uint32_t phase = 0, acc_phase = 0;
-            for_each_segment(p, pair, npairs, bk, [&](int, int, int, int w, int kb0, int kb1, int, long long) {
-                const std::uint32_t idesc = w == BN ? idesc_full : idesc_half;
+            for_each_segment(p, pair, npairs, bk, [&](int, int, int, int, int sl, int kb0, int kb1, int, long long) {
+                const std::uint32_t idesc = make_idesc(fmt, BM2, BN / sl);
                 mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
                 tc_fence_after();
                 const std::uint32_t d = tmem + acc * BN;
@@ -619,8 +766,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
         const int r_local = lane_base + lane;
-        for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int n0, int w, int kb0, int kb1, int nk, long long tile_it0) {
-            const int nb = n0 / BN;
+        Stager st{stg + static_cast<std::uint32_t>(warp - 2) * kStgWarp, 0};
+        for_each_segment(p, pair, npairs, bk, [&](int b, int mb, int nb, int k, int sl, int kb0, int kb1, int nk, long long tile_it0) {
+            const int w = BN / sl;      // accumulator columns of this segment
+            const int n0 = nb * BN + k * w;  // first GEMM column (plain / qkv)
+            const int row0 = mb * BM2 + static_cast<int>(rank) * HALF + lane_base;
             mbar_wait(tfull + 8 * acc, acc_phase);
             tc_fence_after();
             const int row = mb * BM2 + static_cast<int>(rank) * HALF + lane_base + lane;
@@ -688,13 +838,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 if (p.epi != 0) {
                     tc_wait_st();
-                    if (p.epi == 1) epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+                    if (p.epi == 1) epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok);
                     else epilogue_qkv_rope(p, tbase, row, n0, BN, row_ok);
                 }
-            } else if (p.epi == 1) {
-                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);  // never a half tile
+            } else if (p.epi == 1) {  // [gate | up] halves of w/2 columns -> output columns nb*128 + k*w/2
+                if (p.tma_c) epilogue_swiglu_tma(p, &tc, st, tbase, row0, w / 2, nb * (BN / 2) + k * (w / 2), b);
+                else epilogue_swiglu(p, tbase, off, w / 2, nb * (BN / 2) + k * (w / 2), row_ok);
             } else if (p.epi == 2) {
                 epilogue_qkv_rope(p, tbase, row, n0, w, row_ok);
+            } else if (p.tma_c) {
+                epilogue_plain_tma(p, &tc, st, tbase, off, row0, n0, w, b, row_ok);
             } else {
 #pragma unroll 1
                 for (int c0 = 0; c0 < w; c0 += 32) {
@@ -712,6 +865,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         });
+        if (lane == 0) bulk_wait_all();  // staged TMA stores complete before the CTA exits
     }
 
     tc_fence_before();
@@ -738,11 +892,10 @@ constexpr int kThreadsW = 32 * 10;
 
 // Plain epilogue of one 128-row x BN accumulator slab: two 32-column TMEM
 // loads in flight per wait.
-template <int BN>
-__device__ __forceinline__ void epilogue_plain(const Params& p, std::uint32_t tbase, std::int64_t off, int n0,
+__device__ __forceinline__ void epilogue_plain(const Params& p, std::uint32_t tbase, std::int64_t off, int n0, int width,
                                                bool row_ok, bool vec_ok) {
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 64) {
+    for (int c0 = 0; c0 < width; c0 += 64) {
         std::uint32_t r0[32], r1[32];
         TN_LD32(tbase + c0, r0);
         TN_LD32(tbase + c0 + 32, r1);
@@ -753,7 +906,9 @@ __device__ __forceinline__ void epilogue_plain(const Params& p, std::uint32_t tb
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
-    gemm_kernel_2sm_w(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
+    gemm_kernel_2sm_w(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                      const __grid_constant__ CUtensorMap tbh, const __grid_constant__ CUtensorMap tbq,
+                      const __grid_constant__ CUtensorMap tc, const Params p) {
     constexpr int HALF = 128;
     constexpr int A_SUB = HALF * kAtom;        // 16 KB: one 128-row A sub-tile
     constexpr int STAGE = 3 * A_SUB;           // A half 0, A half 1, B (48 KB per CTA)
@@ -765,7 +920,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     const std::uint32_t pad = ((raw + 1023) & ~1023u) - raw;
     std::uint8_t* smem = smem_raw + pad;
     const std::uint32_t sbase = raw + pad;
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStagesW * STAGE);
+    const std::uint32_t stg = sbase + kStagesW * STAGE;  // 8 epilogue warps x kStgWarp
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStagesW * STAGE + 8 * kStgWarp);
     const std::uint32_t full = smem_u32(bars), empty = full + 8 * kStagesW;
     const std::uint32_t tfull = empty + 8 * kStagesW, tempty = tfull + 8;  // tempty[2]
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStagesW + 3);
@@ -775,7 +931,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     const bool leader = rank == 0;
     const int bk = kAtom / p.in_bytes;
     const bool tf32 = p.in_bytes == 4;
-    const int tiles = p.batch * p.tiles_m * p.tiles_n;  // tiles_m counts 512-row tiles
     const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
     auto tile_nk = [&](int mb) {
         int nk = (p.K + bk - 1) / bk;
@@ -783,10 +938,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
         return nk;
     };
     auto skipped = [&](int mb, int nb) { return p.causal == 1 && nb * BN > mb * BMW + BMW - 1; };
+    // This pair's work: round-robin full tiles, then its share of the sliced
+    // tail (slice k of sl of tile nb, see slice_brow). f(b, mb, nb, k, sl).
+    auto for_each_tile = [&](auto&& f) {
+        for (int t = pair; t < p.dp_tiles; t += npairs) {
+            int b, mb, nb;
+            decode(p, t, b, mb, nb);
+            if (!skipped(mb, nb)) f(b, mb, nb, 0, 1);
+        }
+        for (int u = pair; u < p.tail_units; u += npairs) {
+            int b, mb, nb;
+            decode(p, p.dp_tiles + u / p.tail_split, b, mb, nb);
+            f(b, mb, nb, u % p.tail_split, p.tail_split);
+        }
+    };
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&ta)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tb)) : "memory");
+        if (p.tail_units > 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(p.tail_split == 2 ? &tbh : &tbq))
+                         : "memory");
+        }
         for (int s = 0; s < kStagesW; ++s) {
             mbar_init(full + 8 * s, 1);
             mbar_init(empty + 8 * s, 1);
@@ -813,38 +986,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
         if (lane == 0) {
             int stage = 0;
             std::uint32_t phase = 0;
-            for (int t = pair; t < tiles; t += npairs) {
-                int b, mb, nb;
-                decode(p, t, b, mb, nb);
-                if (skipped(mb, nb)) continue;
+            for_each_tile([&](int b, int mb, int nb, int k, int sl) {
                 const int nk = tile_nk(mb);
+                const CUtensorMap* bmap = sl == 1 ? &tb : sl == 2 ? &tbh : &tbq;
+                const int brow = slice_brow(p, nb, k, sl, static_cast<int>(rank));
+                const std::uint32_t tx = 2 * (2 * A_SUB + (BN / 2 / sl) * kAtom);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(empty + 8 * stage, phase ^ 1);
                     const std::uint32_t fb = full_leader0 + 8 * stage;
-                    if (leader) mbar_expect_tx(full + 8 * stage, 2 * STAGE);
+                    if (leader) mbar_expect_tx(full + 8 * stage, tx);
                     const std::uint32_t sa = sbase + stage * STAGE;
                     const int ab = p.a_batched ? b : 0;
                     tma_load_3d_2sm(sa, &ta, kb * bk, mb * BMW + rank * HALF, ab, fb);
                     tma_load_3d_2sm(sa + A_SUB, &ta, kb * bk, mb * BMW + 256 + rank * HALF, ab, fb);
-                    tma_load_3d_2sm(sa + 2 * A_SUB, &tb, kb * bk, nb * BN + rank * HALF, p.b_batched ? b : 0, fb);
+                    tma_load_3d_2sm(sa + 2 * A_SUB, bmap, kb * bk, brow, p.b_batched ? b : 0, fb);
                     if (++stage == kStagesW) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-            }
+            });
         }
     } else if (warp == 1) {
         if (leader) {  // whole warp: one elected lane issues (tc_mma_2sm)
-            const std::uint32_t idesc = make_idesc(tf32 ? 2u : 1u, 256, BN);
+            const std::uint32_t fmt = tf32 ? 2u : 1u;
             int stage = 0;
             std::uint32_t phase = 0, tphase = 0;
             int defer_stage[kStagesW];
-            for (int t = pair; t < tiles; t += npairs) {
-                int b, mb, nb;
-                decode(p, t, b, mb, nb);
-                if (skipped(mb, nb)) continue;
+            for_each_tile([&](int, int mb, int, int, int sl) {
                 const int nk = tile_nk(mb);
+                const std::uint32_t idesc = make_idesc(fmt, 256, BN / sl);
                 mbar_wait(tempty, tphase ^ 1);  // half 0 drained by the previous tile's epilogue
                 tc_fence_after();
                 bool h1_ready = false;
@@ -884,38 +1055,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 }
                 tc_commit_2sm(tfull);
                 tphase ^= 1;
-            }
+            });
         }
     } else {
         const int lane_base = (warp % 4) * 32;
         const int h = (warp - 2) / 4;  // the accumulator half this warpgroup drains
+        Stager st{stg + static_cast<std::uint32_t>(warp - 2) * kStgWarp, 0};
         std::uint32_t tphase = 0;
         const int ob = p.out_dtype == BF16 ? 2 : 4;
         const bool vec_ok = (p.N % 32 == 0) && ((p.ldc * ob) % 16 == 0) && ((p.sc * ob) % 16 == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
-        for (int t = pair; t < tiles; t += npairs) {
-            int b, mb, nb;
-            decode(p, t, b, mb, nb);
-            if (skipped(mb, nb)) continue;
+        for_each_tile([&](int b, int mb, int nb, int k, int sl) {
+            const int w = BN / sl;
             mbar_wait(tfull, tphase);
             tc_fence_after();
             const int row = mb * BMW + h * 256 + static_cast<int>(rank) * HALF + lane_base + lane;
             const bool row_ok = row < p.M;
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + h * 256;
+            const int row0 = row - lane;
             if (p.epi == 1) {
-                epilogue_swiglu<BN>(p, tbase, off, nb, row_ok);
+                if (p.tma_c) epilogue_swiglu_tma(p, &tc, st, tbase, row0, w / 2, nb * (BN / 2) + k * (w / 2), b);
+                else epilogue_swiglu(p, tbase, off, w / 2, nb * (BN / 2) + k * (w / 2), row_ok);
             } else if (p.epi == 2) {
-                epilogue_qkv_rope(p, tbase, row, nb * BN, BN, row_ok);
+                epilogue_qkv_rope(p, tbase, row, nb * BN + k * w, w, row_ok);
+            } else if (p.tma_c) {
+                epilogue_plain_tma(p, &tc, st, tbase, off, row0, nb * BN + k * w, w, b, row_ok);
             } else {
-                epilogue_plain<BN>(p, tbase, off, nb * BN, row_ok, vec_ok);
+                epilogue_plain(p, tbase, off, nb * BN + k * w, w, row_ok, vec_ok);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + 8 * h);
             tphase ^= 1;
-        }
+        });
+        if (lane == 0) bulk_wait_all();
     }
 
     tc_fence_before();
@@ -997,6 +1172,13 @@ bool encode(CUtensorMap* map, const void* base, int esize, std::int64_t K, std::
 
 bool encode_tma_3d(CUtensorMap* map, const void* base, int esize, std::int64_t inner, std::int64_t rows,
                    std::int64_t ld, int batch, std::int64_t bstride, int box_inner, int box_rows) {
+    return encode_tma_3d_swz(map, base, esize, inner, rows, ld, batch, bstride, box_inner, box_rows,
+                             CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+bool encode_tma_3d_swz(CUtensorMap* map, const void* base, int esize, std::int64_t inner, std::int64_t rows,
+                       std::int64_t ld, int batch, std::int64_t bstride, int box_inner, int box_rows,
+                       CUtensorMapSwizzle swz) {
     EncodeFn fn = get_encode();
     if (!fn) return false;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
@@ -1006,7 +1188,7 @@ bool encode_tma_3d(CUtensorMap* map, const void* base, int esize, std::int64_t i
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(map, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                     const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -1016,8 +1198,8 @@ template <int BN>
 int smem_bytes() {
     return kStages * (kBM + BN) * kAtom + 256 + 1024;
 }
-int smem_bytes_2sm() { return kStages2 * 2 * 128 * kAtom + 256 + 1024; }
-int smem_bytes_2sm_w() { return kStagesW * 3 * 128 * kAtom + 256 + 1024; }
+int smem_bytes_2sm() { return kStages2 * 2 * 128 * kAtom + 4 * kStgWarp + 256 + 1024; }
+int smem_bytes_2sm_w() { return kStagesW * 3 * 128 * kAtom + 8 * kStgWarp + 256 + 1024; }
 
 }  // namespace
 
@@ -1041,7 +1223,17 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         const bool ab = a.batch > 1 && a.sa != 0, bb = a.batch > 1 && a.sb != 0;
         ok = encode(&plan->ta, a.A, es, a.K, a.M, a.lda, ab ? a.batch : 1, a.sa, kBM) &&
              encode(&plan->tb, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, two_sm ? 128 : bn);
-        plan->tbh_ok = ok && two_sm && encode(&plan->tbh, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, 64);
+        plan->tbh_ok = ok && two_sm && encode(&plan->tbh, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, 64) &&
+                       encode(&plan->tbq, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, 32);
+        // C for the TMA-store epilogue: {64 B x 32 rows} boxes, SWIZZLE_64B
+        const int oes = dtype_size(a.out_dtype);
+        const int n_out = a.epi == 1 ? a.N / 2 : a.N;
+        const bool cb = a.batch > 1;
+        plan->tc_ok = ok && two_sm && (a.epi == 0 || a.epi == 1) && (a.out_dtype == BF16 || a.out_dtype == F32) &&
+                      al16(a.C) && (a.ldc * oes) % 16 == 0 && (!cb || (a.sc * oes) % 16 == 0) &&
+                      (a.R == nullptr || al16(a.R)) && n_out % 32 == 0 &&
+                      encode_tma_3d_swz(&plan->tc, a.C, oes, n_out, a.M, a.ldc, cb ? a.batch : 1, a.sc, 64 / oes, 32,
+                                        CU_TENSOR_MAP_SWIZZLE_64B);
     }
     plan->path = ok ? (two_sm ? 2 : 0) : 1;
     plan->bn = bn;
@@ -1052,39 +1244,62 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         if (env && std::strcmp(env, "wide") == 0) tile = 2;
     }
     if (plan->path == 2 && tile == 2) plan->path = 3;
+    // Tail of the last, partial wave of pairs: its tiles are split into
+    // sl in {1, 2, 4} N-slices (slice_brow) so that the tail costs
+    // ceil(rem * sl / P) / sl tile-times. SwiGLU slices keep gate/up pairs;
+    // the QKV+RoPE epilogue needs whole heads (sl <= 2).
+    const int P = std::max(1, num_sms / 2);
+    // Wide tiles slice at most 2 ways: a 512x64 slice still stages both
+    // 256-row A halves, so it is operand-bound at ~3/4 of a full tile-time.
+    auto tail_plan = [&](long long T, int* split, bool wide) {
+        const long long rem = T >= P ? T % P : T;
+        double best = rem == 0 ? 0.0 : 1.0;
+        *split = 1;
+        if (rem > 0 && a.causal == 0 && plan->tbh_ok) {
+            for (int sl = 2; sl <= (a.epi == 2 || wide ? 2 : 4); sl *= 2) {
+                const double t = static_cast<double>((rem * sl + P - 1) / P) / sl;
+                if (t < best - 1e-9) {
+                    best = t;
+                    *split = sl;
+                }
+            }
+        }
+        return static_cast<double>(T / P) + best;  // whole waves + the tail, in tile-times
+    };
     if (plan->path == 2 && a.M > 256 && tile == 0) {
-        // Wide 512x256 pair tiles do fewer operand bytes per FLOP but leave
-        // the epilogue exposed (no second accumulator): measured slower than
-        // narrow tiles on every 7B shape, so they are only picked when the
-        // narrow tiles quantise much worse (narrow tail: half a tile-time
-        // when the last wave fits in half-width tiles, else a full one).
-        const int P = std::max(1, num_sms / 2);
+        // Wide 512x256 pair tiles stage 25% fewer operand bytes per FLOP
+        // (lower power, so higher clocks under the power cap) but have no
+        // second accumulator: each tile boundary exposes the drain of its
+        // two halves (short with the TMA-store epilogue). Measured in the
+        // 7B step (power-capped, per GEMM class): wide wins ~6.5% at
+        // K = 11008 despite worse wave quantisation (4 vs 3.5 narrow
+        // tile-times) and loses at K = 4096; the QKV+RoPE epilogue does not
+        // stage through TMA, so it stays narrow. Hence: compare wave
+        // quantisation (a wide tile = two narrow tile-times) with a bias of
+        // 1.2 for long K loops (>= 128 K blocks) and 0.9 otherwise.
         const long long tn = (a.N + 255) / 256;
         const long long narrow = a.batch * ((a.M + 255) / 256) * tn, wide = a.batch * ((a.M + 511) / 512) * tn;
-        const long long rem = narrow % P;
-        const double t_narrow = static_cast<double>(narrow / P) + (rem == 0 ? 0.0 : 2 * rem <= P ? 0.5 : 1.0);
-        const double t_wide = static_cast<double>((wide + P - 1) / P) * 2.0 / 0.9;
-        if (t_wide < t_narrow) plan->path = 3;
+        int s1, s2;
+        const double t_narrow = tail_plan(narrow, &s1, false), t_wide = 2.0 * tail_plan(wide, &s2, true);
+        const long long nkb = (static_cast<long long>(a.K) * es + kAtom - 1) / kAtom;
+        static const char* wenv = std::getenv("TN_GEMM_WIDE_BIAS");  // tuning override
+        const double bias = wenv ? std::atof(wenv) : (nkb >= 128 ? 1.2 : 0.9);
+        if (a.epi != 2 && t_wide <= t_narrow * bias + 1e-9 && (a.M % 512 == 0 || a.M > 2048)) plan->path = 3;
     }
     const int bm = plan->path == 2 ? 256 : plan->path == 3 ? 512 : kBM;
     const int tm = (a.M + bm - 1) / bm, tn = (a.N + bn - 1) / bn;
     plan->tiles = a.batch * tm * tn;
     plan->grid = std::min(plan->tiles, std::max(1, num_sms));
-    if (plan->path == 3) plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
-    if (plan->path == 2) {
+    if (plan->path == 2 || plan->path == 3) {
         plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
         const int npairs = plan->grid / 2, T = plan->tiles;
         const int nk = static_cast<int>((a.K * es + kAtom - 1) / kAtom);
-        // Tail of the last wave of pairs. Default: split its tiles into
-        // 256x128 halves when they fit in half the pairs (half a tile-time
-        // instead of a whole one). TN_GEMM_SK=1 selects the stream-K tail
-        // instead (last partial wave + one full wave split by K blocks);
-        // measured on B200 it never beat the plain or half-width tail
-        // (fix-up traffic + serialised finishers), so it is off by default.
+        // TN_GEMM_SK=1 (or tile "streamk") selects a stream-K tail instead
+        // (narrow tiles; last partial wave + one full wave split by K
+        // blocks). Measured on B200 it never beat the sliced tail (fix-up
+        // traffic + serialised finishers), so it is off by default.
         static const char* sk_env = std::getenv("TN_GEMM_SK");
-        const bool sk_on = tile == 3 || (sk_env && std::strcmp(sk_env, "1") == 0);
-        const int P = std::max(1, num_sms / 2);
-        const int rem = T >= P ? T % P : T;
+        const bool sk_on = plan->path == 2 && (tile == 3 || (sk_env && std::strcmp(sk_env, "1") == 0));
         if (sk_on) {
             if (a.causal == 0 && T >= npairs && T % npairs != 0) {
                 const int sk = T / npairs >= 2 ? T % npairs + npairs : T;
@@ -1094,9 +1309,15 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
                     plan->ws_bytes = static_cast<std::size_t>(npairs) * 2 * 128 * 256 * 4 + static_cast<std::size_t>(npairs) * 2 * 4;
                 }
             }
-        } else if (a.causal == 0 && a.epi != 1 && rem > 0 && 2 * rem <= P && plan->tbh_ok) {
-            plan->half_tiles = 2 * rem;
-            plan->grid = 2 * std::min(P, T >= P ? P : 2 * rem);
+        } else {
+            int sl = 1;
+            tail_plan(T, &sl, plan->path == 3);
+            if (sl > 1) {
+                const int rem = T >= P ? T % P : T;
+                plan->tail_split = sl;
+                plan->tail_units = rem * sl;
+                plan->grid = 2 * std::min(P, T >= P ? P : rem * sl);
+            }
         }
     }
     if (ok) {
@@ -1146,8 +1367,10 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
     p.epi = a.epi;
     p.rope = static_cast<const float*>(a.rope);
     p.heads = a.heads;
-    p.dp_tiles = plan.tiles - plan.half_tiles / 2;
-    p.half_tiles = plan.half_tiles;
+    p.tail_split = std::max(1, plan.tail_split);
+    p.tail_units = plan.tail_units;
+    p.dp_tiles = plan.tiles - plan.tail_units / p.tail_split;
+    p.tma_c = plan.tc_ok && (plan.path == 2 || plan.path == 3) && (a.epi == 0 || a.epi == 1) ? 1 : 0;
     p.sk_nk = 0;
     p.sk_total = 0;
     p.ws = nullptr;
@@ -1164,9 +1387,9 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
         p.epoch = ws->epoch;
     }
     if (plan.path == 3)
-        gemm_kernel_2sm_w<<<plan.grid, kThreadsW, smem_bytes_2sm_w(), s>>>(plan.ta, plan.tb, p);
+        gemm_kernel_2sm_w<<<plan.grid, kThreadsW, smem_bytes_2sm_w(), s>>>(plan.ta, plan.tb, plan.tbh, plan.tbq, plan.tc, p);
     else if (plan.path == 2)
-        gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, plan.tbh, p);
+        gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, plan.tbh, plan.tbq, plan.tc, p);
     else if (plan.bn == 128)
         gemm_kernel<128><<<plan.grid, kThreads, smem_bytes<128>(), s>>>(plan.ta, plan.tb, p);
     else if (plan.bn == 64)

@@ -44,7 +44,9 @@ struct GemmArgs {
 struct alignas(64) GemmPlan {
     CUtensorMap ta;  // A: (K, M, batch)
     CUtensorMap tb;  // B: (K, N, batch)
-    CUtensorMap tbh; // B with 64-row boxes (half-width tail tiles of the CTA-pair path)
+    CUtensorMap tbh; // B with 64-row boxes (2-way sliced tail tiles of the CTA-pair paths)
+    CUtensorMap tbq; // B with 32-row boxes (4-way sliced tail tiles)
+    CUtensorMap tc;  // C: {64 B x 32 rows} SWIZZLE_64B boxes for the TMA-store epilogue
     GemmArgs args;
     int path = 0;    // 0 tcgen05 1-CTA, 2 tcgen05 CTA pair (cta_group::2), 1 SIMT fallback
     int bn = 256;    // N tile of the tcgen05 path
@@ -53,8 +55,10 @@ struct alignas(64) GemmPlan {
     int sk_tiles = 0;          // path 2: trailing tiles split by K blocks across all pairs (stream-K)
     int sk_nk = 0;             // K blocks per stream-K tile
     std::size_t ws_bytes = 0;  // workspace the stream-K tail needs (0: none)
-    int half_tiles = 0;        // path 2: trailing tiles run as 2 x 256x128 halves (count of halves)
+    int tail_split = 1;        // paths 2/3: tiles of the last partial wave split into this many N-slices
+    int tail_units = 0;        // number of such slices
     bool tbh_ok = false;
+    bool tc_ok = false;
 };
 
 // Stream-K scratch: per-pair fp32 partial slots + publication flags. One per
@@ -69,6 +73,9 @@ struct GemmWorkspace {
 // 3-D tiled TMA descriptor (inner, rows, batch), 128-byte swizzle.
 bool encode_tma_3d(CUtensorMap* map, const void* base, int esize, std::int64_t inner, std::int64_t rows,
                    std::int64_t ld, int batch, std::int64_t bstride, int box_inner, int box_rows);
+bool encode_tma_3d_swz(CUtensorMap* map, const void* base, int esize, std::int64_t inner, std::int64_t rows,
+                       std::int64_t ld, int batch, std::int64_t bstride, int box_inner, int box_rows,
+                       CUtensorMapSwizzle swz);
 
 // Encodes TMA descriptors (needs a CUDA context on the target device).
 cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms);
