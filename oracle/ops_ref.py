@@ -98,6 +98,8 @@ def op_gemm(op, args, out):
     Bm = strided(args[1], ind, op.get("b_off", 0), B, op.get("sb", 0), N, ldb, K)
     causal = op.get("causal", 0)
     C = np.matmul(A, np.transpose(Bm, (0, 2, 1))) * np.float32(op.get("alpha", 1.0))
+    if op.get("rs_arg", -1) >= 0:  # fused RMSNorm consumer: row m *= rsqrt(sum_c P[c][row0+m] / dim + eps)
+        C = C * row_scale(op, args)[None, :, None]
     if op.get("epilogue", "none") == "qkv_rope":
         # packed [rope(q) (H,M,128) | rope(k) | vT (H,128,M)] from C = x W^T
         H, Mm = op["heads"], op["M"]
@@ -120,12 +122,49 @@ def op_gemm(op, args, out):
         g, u = blk[:, :, :, 0, :], blk[:, :, :, 1, :]
         C = (g / (1.0 + np.exp(-g)) * u).reshape(Bn, Mm, Nn // 2)
         ldc = op.get("ldc") or Nn // 2
-    if len(args) == 3:
+    if len(args) >= 3:
         C = C + strided(args[2], outd, op.get("r_off", 0), B, op.get("sc", 0), M, ldc, N)
+    if op.get("norm_out", 0):  # fused RMSNorm producer: [x | h = x*gamma | P]
+        store_norm_out(out, C[0], load(args[3], "bf16", N))
+        return
     mask = None
     if causal == 1:
         mask = np.broadcast_to((np.arange(N)[None, :] <= np.arange(M)[:, None])[None], C.shape)
     scatter(out, outd, op.get("c_off", 0), op.get("sc", 0), ldc, C.astype(np.float32), mask)
+
+
+def chunk_sumsq(x: np.ndarray) -> np.ndarray:
+    """P[m][c] = sum over the 32 columns of chunk c of x[m]^2, accumulated in
+    column order in fp32 (the fused-norm producers' partial sums, [rows, cols/32])."""
+    R, Cc = x.shape
+    xc = x.reshape(R, Cc // 32, 32)
+    ss = np.zeros((R, Cc // 32), dtype=np.float32)
+    for j in range(32):
+        ss += xc[:, :, j] * xc[:, :, j]
+    return ss
+
+
+def store_norm_out(out, C2d, g):
+    """Writes the fused-RMSNorm producer output [x | h | P] for fp32 values
+    C2d [rows, cols]: x = bf16(C2d), h = bf16(x * g), P = chunk_sumsq(x)."""
+    R, Cc = C2d.shape
+    x = bf16_to_f32(f32_to_bf16(C2d))
+    store(out, "bf16", x)
+    store(out, "bf16", x * g[None, :], R * Cc)
+    store(out, "f32", chunk_sumsq(x), R * Cc)  # f32 element offset R*Cc == byte offset 2*R*Cc*2
+
+
+def row_scale(op, args) -> np.ndarray:
+    """Per-row factor of a fused-RMSNorm consumer: rsqrt(sum_c P[row0+m][c] /
+    dim + eps), c summed in order (P [rows, ld] fp32 read from args[rs_arg]
+    at byte rs_off)."""
+    M, dim, ld, row0 = op["M"], op["rs_dim"], op["rs_ld"], op.get("rs_row0", 0)
+    buf = args[op["rs_arg"]][op.get("rs_off", 0):]
+    P = buf[: (row0 + M) * ld * 4].view(np.float32).reshape(row0 + M, ld)[row0:row0 + M, : dim // 32]
+    ss = np.zeros(M, dtype=np.float32)
+    for c in range(dim // 32):
+        ss += P[:, c]
+    return (np.float32(1.0) / np.sqrt(ss / np.float32(dim) + np.float32(op.get("eps", 1e-5)))).astype(np.float32)
 
 
 def op_rmsnorm(op, args, out):
@@ -342,6 +381,9 @@ def op_embedding(op, args, out):
     S, Dm, V = op["seq"], op["dim"], op["vocab"]
     tok = np.clip(load(args[0], "i32", S), 0, V - 1)
     tab = args[1][: V * Dm * 2].view(np.uint16).reshape(V, Dm)
+    if op.get("norm_out", 0):  # fused RMSNorm producer: [x | h = x*gamma | P]
+        store_norm_out(out, bf16_to_f32(tab[tok]), load(args[2], "bf16", Dm))
+        return
     out[: S * Dm * 2] = tab[tok].reshape(-1).view(np.uint8)
 
 

@@ -380,7 +380,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
     auto es = [](int dt) { return static_cast<std::int64_t>(k::dtype_size(dt)); };
     switch (op.type) {
         case OpType::Gemm: {
-            need_args(2, 3);
+            need_args(2, op.norm_out ? 4 : 3);
             k::GemmArgs g;
             g.M = static_cast<int>(op.M);
             g.N = static_cast<int>(op.N);
@@ -418,12 +418,35 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
                 fits(op.M * 64 * 2 * 4, arg_bytes[2], "rope_table");
                 g.rope = in.argp[2];
                 g.heads = static_cast<int>(op.heads);
-            } else if (op.args.size() == 3) {
+            } else if (op.args.size() >= 3) {
                 fits(extent(op.r_off, g.batch, g.sc, g.M, g.ldc, g.N) * eo, arg_bytes[2], "R");
                 g.R = in.argp[2] + op.r_off * eo;
             }
+            if (op.norm_out) {  // [x | h | P] output, gamma = last argument
+                if (op.args.size() != 4 || op.epilogue != 0 || op.batch != 1 || op.out_dtype != k::BF16 ||
+                    g.ldc != op.N || op.N % 32 != 0)
+                    throw Error("gemm norm_out needs args [A, B, R, gamma], bf16 out, batch 1, dense C, N % 32 == 0");
+                fits(op.N * 2, arg_bytes[3], "gamma");
+                fits(op.c_off * eo + 2 * op.M * op.N * 2 + (op.N / 32) * op.M * 4, out_bytes, "C (x | h | P)");
+                g.no_g = in.argp[3];
+                g.no_P = reinterpret_cast<float*>(in.dst + op.c_off * eo + 2 * op.M * op.N * 2);
+            }
+            if (op.rs_arg >= 0) {
+                if (op.rs_arg >= static_cast<int>(op.args.size()) || op.rs_dim <= 0 || op.rs_dim % 32 != 0 || op.rs_ld <= 0)
+                    throw Error("gemm row scale needs rs_arg < #args, rs_dim % 32 == 0, rs_ld > 0");
+                if (op.rs_ld < op.rs_dim / 32) throw Error("gemm row scale: rs_ld < rs_dim / 32");
+                fits(op.rs_off + ((op.rs_row0 + op.M - 1) * op.rs_ld + op.rs_dim / 32) * 4, arg_bytes[op.rs_arg],
+                     "row-scale sums P");
+                g.rs_P = reinterpret_cast<const float*>(in.argp[op.rs_arg] + op.rs_off);
+                g.rs_ld = static_cast<int>(op.rs_ld);
+                g.rs_row0 = static_cast<int>(op.rs_row0);
+                g.rs_chunks = static_cast<int>(op.rs_dim / 32);
+                g.rs_inv_dim = 1.0f / static_cast<float>(op.rs_dim);
+                g.rs_eps = static_cast<float>(op.eps);
+            }
             in.gemm = std::make_unique<k::GemmPlan>();
-            TN_CUDA(k::gemm_prepare(g, in.gemm.get(), num_sms[v.device]));
+            if (k::gemm_prepare(g, in.gemm.get(), num_sms[v.device]) == cudaErrorNotSupported)
+                throw Error("gemm norm_out needs the CTA-pair tcgen05 path with 16-byte aligned operands");
             if (op.epilogue == 2 && in.gemm->path == 1)
                 throw Error("gemm qkv_rope epilogue needs a tcgen05-eligible shape (M >= 128, aligned operands)");
             break;
@@ -509,10 +532,15 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             fits(static_cast<std::int64_t>(op.args.size()) * op.count * es(op.out_dtype), out_bytes, "out");
             break;
         case OpType::Embedding:
-            need_args(2, 2);
+            need_args(op.norm_out ? 3 : 2, op.norm_out ? 3 : 2);
             fits(op.seq * 4, arg_bytes[0], "tokens");
             fits(op.vocab * op.dim * 2, arg_bytes[1], "table");
-            fits(op.seq * op.dim * 2, out_bytes, "out");
+            fits(op.seq * op.dim * 2 * (op.norm_out ? 2 : 1) + (op.norm_out ? op.seq * (op.dim / 32) * 4 : 0), out_bytes,
+                 "out");
+            if (op.norm_out) {
+                if (op.dim % 32 != 0) throw Error("embedding norm_out needs dim % 32 == 0");
+                fits(op.dim * 2, arg_bytes[2], "gamma");
+            }
             break;
         case OpType::Cast:
             need_args(1, 1);
@@ -684,8 +712,12 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
                     break;
                 }
                 case OpType::Embedding:
-                    TN_CUDA(k::embedding(a[0], a[1], in.dst, static_cast<int>(op.seq), static_cast<int>(op.dim),
-                                         static_cast<int>(op.vocab), s));
+                    if (op.norm_out)
+                        TN_CUDA(k::embedding_norm(a[0], a[1], a[2], in.dst, static_cast<int>(op.seq),
+                                                  static_cast<int>(op.dim), static_cast<int>(op.vocab), s));
+                    else
+                        TN_CUDA(k::embedding(a[0], a[1], in.dst, static_cast<int>(op.seq), static_cast<int>(op.dim),
+                                             static_cast<int>(op.vocab), s));
                     break;
                 case OpType::Cast:
                     TN_CUDA(k::cast(a[0], op.in_dtype, in.dst, op.out_dtype, op.count, s));

@@ -116,6 +116,12 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
             d.k_off = I("k_off", 0);
             d.v_off = I("v_off", 0);
             d.causal = static_cast<int>(I("causal", 0));
+            d.norm_out = static_cast<int>(I("norm_out", 0));
+            d.rs_arg = static_cast<int>(I("rs_arg", -1));
+            d.rs_off = I("rs_off", 0);
+            d.rs_ld = I("rs_ld", 0);
+            d.rs_row0 = I("rs_row0", 0);
+            d.rs_dim = I("rs_dim", 0);
             {
                 const std::string ep = o.value("epilogue", std::string("none"));
                 if (ep == "none") d.epilogue = 0;

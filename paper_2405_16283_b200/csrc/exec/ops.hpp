@@ -71,6 +71,14 @@ struct OpDesc {
     double alpha = 1.0, eps = 1e-5, scale = 1.0;
     std::vector<std::int64_t> offs;  // sum: per-argument element offsets
     std::int64_t q_off = 0, k_off = 0, v_off = 0;  // attention on a packed qkv tensor
+    // Fused RMSNorm. Producer (gemm with residual, embedding): "norm_out": 1
+    // plus a trailing gamma argument; the output holds [x | h = x*gamma | P],
+    // P[m][c] = sum of x[m, 32c..32c+31]^2 (fp32, [rows, dim/32]). Consumer
+    // (gemm): row m scaled by rsqrt(sum_c P[rs_row0 + m][c] / rs_dim + eps),
+    // P read from argument rs_arg at byte offset rs_off with leading dim rs_ld.
+    int norm_out = 0;
+    int rs_arg = -1;
+    std::int64_t rs_off = 0, rs_ld = 0, rs_row0 = 0, rs_dim = 0;
 };
 
 // Parses the "op" payloads of a taskgraph JSON document (vertices without an

@@ -213,6 +213,41 @@ __global__ void embedding_kernel(const int* __restrict__ tok, const __nv_bfloat1
     }
 }
 
+// Embedding gather fused with the first RMSNorm's producer side: x = table
+// row, h = bf16(x * g) in the seq*dim elements after x, and per 32-column
+// chunk c the sum of x^2 (column order) to P[t * dim/32 + c]. One thread per
+// chunk (dim % 32 == 0, 16-byte aligned).
+__global__ void embedding_norm_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
+                                      const __nv_bfloat16* __restrict__ g, __nv_bfloat16* __restrict__ out, int seq,
+                                      int dim, int vocab) {
+    const int t = blockIdx.x;
+    int id = tok[t];
+    id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
+    const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<std::int64_t>(id) * dim);
+    uint4* x = reinterpret_cast<uint4*>(out + static_cast<std::int64_t>(t) * dim);
+    uint4* h = reinterpret_cast<uint4*>(out + static_cast<std::int64_t>(seq) * dim + static_cast<std::int64_t>(t) * dim);
+    float* P = reinterpret_cast<float*>(out + 2 * static_cast<std::int64_t>(seq) * dim);
+    const uint4* gv = reinterpret_cast<const uint4*>(g);
+    for (int c = threadIdx.x; c < dim / 32; c += blockDim.x) {
+        float ss = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 u = src[4 * c + q];
+            float f[8], w[8];
+            unpack8(u, f);
+            unpack8(gv[4 * c + q], w);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                ss = fmaf(f[j], f[j], ss);
+                w[j] *= f[j];
+            }
+            x[4 * c + q] = u;
+            h[4 * c + q] = pack8(w);
+        }
+        P[static_cast<std::int64_t>(t) * (dim / 32) + c] = ss;
+    }
+}
+
 __global__ void cast_kernel(const void* __restrict__ in, int in_dt, void* __restrict__ out, int out_dt,
                             std::int64_t count) {
     for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
@@ -291,6 +326,15 @@ cudaError_t concat(const void* const* parts, int n, std::int64_t part_bytes, voi
         concat_kernel<<<grid_for(part_bytes / 16 * n), kThreads, 0, s>>>(a, static_cast<uint4*>(out), part_bytes / 16);
     else
         concat_bytes_kernel<<<grid_for(part_bytes * n), kThreads, 0, s>>>(a, static_cast<std::uint8_t*>(out), part_bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t embedding_norm(const void* tokens, const void* table, const void* g, void* out, int seq, int dim, int vocab,
+                           cudaStream_t s) {
+    if (dim % 32 != 0 || !al16(table) || !al16(out) || !al16(g)) return cudaErrorNotSupported;
+    embedding_norm_kernel<<<seq, 128, 0, s>>>(static_cast<const int*>(tokens), static_cast<const __nv_bfloat16*>(table),
+                                              static_cast<const __nv_bfloat16*>(g), static_cast<__nv_bfloat16*>(out), seq,
+                                              dim, vocab);
     return cudaGetLastError();
 }
 

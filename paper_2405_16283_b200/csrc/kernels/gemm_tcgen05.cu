@@ -61,10 +61,42 @@ struct Params {
     // [dp_tiles, dp_tiles + tail_units / tail_split).
     int tail_split, tail_units;
     int tma_c;  // 1: plain/SwiGLU epilogues store through smem staging + TMA (tensor map `tc`)
+    // Fused RMSNorm (consumer side): row m of the product is scaled by
+    // rsqrt(sum_c rs_P[(rs_row0 + m)*rs_ld + c] / dim + eps), c in [0, rs_chunks),
+    // summed in c order — the per-32-column sums of squares its producer wrote.
+    const float* rs_P;
+    int rs_ld, rs_row0, rs_chunks;
+    float rs_inv_dim, rs_eps;
+    // Fused RMSNorm (producer side, plain epilogue + residual, bf16, TMA
+    // path): x = bf16(alpha*acc + R) goes to C (box batch 0), h = bf16(x * g)
+    // to the rows after it (box batch 1), and per 32-column chunk c the sum of
+    // x^2 (in column order) to no_P[row*(N/32) + c].
+    const __nv_bfloat16* no_g;
+    float* no_P;
     float* ws;
     unsigned* flags;  // per CTA of each pair: epoch of its last published partial
     unsigned epoch;
 };
+
+__device__ __forceinline__ float row_alpha(const Params& p, int row, bool row_ok) {
+    if (!p.rs_P || !row_ok) return p.alpha;
+    const float* P = p.rs_P + static_cast<std::int64_t>(p.rs_row0 + row) * p.rs_ld;  // row-major [rows, chunks]
+    float ss = 0.f;
+    if ((p.rs_chunks & 3) == 0 && (reinterpret_cast<std::uintptr_t>(P) & 15) == 0) {
+        const float4* P4 = reinterpret_cast<const float4*>(P);
+#pragma unroll 8
+        for (int c = 0; c < p.rs_chunks / 4; ++c) {
+            const float4 x = __ldg(P4 + c);
+            ss += x.x;
+            ss += x.y;
+            ss += x.z;
+            ss += x.w;
+        }
+    } else {
+        for (int c = 0; c < p.rs_chunks; ++c) ss += __ldg(P + c);
+    }
+    return p.alpha * rsqrtf(ss * p.rs_inv_dim + p.rs_eps);
+}
 
 __device__ __forceinline__ bool tile_skipped(const Params& p, int mb, int nb, int bn) {
     return p.causal == 1 && nb * bn > mb * kBM + kBM - 1;
@@ -100,11 +132,11 @@ __device__ __forceinline__ std::uint32_t pack_bf16(float a, float b) {
 
 // Stores one 32-column chunk of an accumulator row (alpha, residual, dtype).
 __device__ __forceinline__ void store_chunk(const Params& p, const std::uint32_t* r, std::int64_t off, int n0,
-                                            bool row_ok, bool vec_ok) {
+                                            bool row_ok, bool vec_ok, float alpha) {
     if (!row_ok || n0 >= p.N) return;
     float v[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * alpha;
     if (vec_ok) {
         if (p.out_dtype == BF16) {
             __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + off + n0;
@@ -189,9 +221,9 @@ struct Stager {
 
 // Alpha and residual of one 32-column chunk of this lane's row (vector path).
 __device__ __forceinline__ void chunk_values(const Params& p, const std::uint32_t* r, std::int64_t off, int n0,
-                                             bool row_ok, float* v) {
+                                             bool row_ok, float* v, float alpha) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * alpha;
     if (!p.R || !row_ok || n0 >= p.N) return;
     if (p.out_dtype == BF16) {
         const uint4* rr = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.R) + off + n0);
@@ -256,15 +288,38 @@ __device__ __forceinline__ void stage_chunk(const Params& p, const CUtensorMap* 
 // Plain epilogue through the stager: 128-row x width accumulator slab.
 __device__ __forceinline__ void epilogue_plain_tma(const Params& p, const CUtensorMap* tc, Stager& st,
                                                    std::uint32_t tbase, std::int64_t off, int row0, int n0, int width,
-                                                   int b, bool row_ok) {
+                                                   int b, bool row_ok, float alpha) {
 #pragma unroll 1
     for (int c0 = 0; c0 < width; c0 += 32) {
         std::uint32_t r[32];
         TN_LD32(tbase + c0, r);
         tc_wait_ld();
         float v[32];
-        chunk_values(p, r, off, n0 + c0, row_ok, v);
-        stage_chunk(p, tc, st, v, row0, n0 + c0, b);
+        chunk_values(p, r, off, n0 + c0, row_ok, v, alpha);
+        if (p.no_P) {  // fused RMSNorm producer: x, h = x * g, per-chunk sum of x^2
+            float ss = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));  // x as stored
+                ss = fmaf(v[j], v[j], ss);
+            }
+            stage_chunk(p, tc, st, v, row0, n0 + c0, 0);
+            if (row_ok) p.no_P[static_cast<std::int64_t>(row0 + threadIdx.x % 32) * (p.N / 32) + (n0 + c0) / 32] = ss;
+            const uint4* gv = reinterpret_cast<const uint4*>(p.no_g + n0 + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float g[8];
+                const uint4 u = __ldg(gv + q);
+                const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) g[j] = __bfloat162float(hb[j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[q * 8 + j] *= g[j];
+            }
+            stage_chunk(p, tc, st, v, row0, n0 + c0, 1);
+        } else {
+            stage_chunk(p, tc, st, v, row0, n0 + c0, b);
+        }
     }
 }
 
@@ -272,7 +327,7 @@ __device__ __forceinline__ void epilogue_plain_tma(const Params& p, const CUtens
 // weight rows are interleaved that way), so each output column needs two
 // TMEM columns of the same row: out = silu(alpha*g) * (alpha*u).
 __device__ __forceinline__ void epilogue_swiglu(const Params& p, std::uint32_t tbase, std::int64_t off, int H,
-                                                int out0, bool row_ok) {
+                                                int out0, bool row_ok, float alpha) {
     Params q = p;
     q.N = p.N / 2;
     q.alpha = 1.0f;
@@ -287,16 +342,16 @@ __device__ __forceinline__ void epilogue_swiglu(const Params& p, std::uint32_t t
         tc_wait_ld();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            const float x = __uint_as_float(g[j]) * p.alpha, y = __uint_as_float(u[j]) * p.alpha;
+            const float x = __uint_as_float(g[j]) * alpha, y = __uint_as_float(u[j]) * alpha;
             g[j] = __float_as_uint(x / (1.0f + __expf(-x)) * y);
         }
-        store_chunk(q, g, off, out0 + c0, row_ok, vec_ok);
+        store_chunk(q, g, off, out0 + c0, row_ok, vec_ok, 1.0f);
     }
 }
 
 // H: gate (= up) columns in the accumulator ([gate | up]); out0: first output column.
 __device__ __forceinline__ void epilogue_swiglu_tma(const Params& p, const CUtensorMap* tc, Stager& st,
-                                                    std::uint32_t tbase, int row0, int H, int out0, int b) {
+                                                    std::uint32_t tbase, int row0, int H, int out0, int b, float alpha) {
 #pragma unroll 1
     for (int c0 = 0; c0 < H; c0 += 32) {
         std::uint32_t g[32], u[32];
@@ -306,7 +361,7 @@ __device__ __forceinline__ void epilogue_swiglu_tma(const Params& p, const CUten
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            const float x = __uint_as_float(g[j]) * p.alpha, y = __uint_as_float(u[j]) * p.alpha;
+            const float x = __uint_as_float(g[j]) * alpha, y = __uint_as_float(u[j]) * alpha;
             v[j] = x / (1.0f + __expf(-x)) * y;
         }
         stage_chunk(p, tc, st, v, row0, out0 + c0, b);
@@ -319,7 +374,7 @@ __device__ __forceinline__ void epilogue_swiglu_tma(const Params& p, const CUten
 // the transposed stores coalesce across the warp). Output = packed
 // [q | k | vᵀ], each H*seq*128 elements.
 __device__ __forceinline__ void epilogue_qkv_rope(const Params& p, std::uint32_t tbase, int row, int n0, int width,
-                                                  bool row_ok) {
+                                                  bool row_ok, float alpha) {
     constexpr int HD = 128;
     const std::int64_t sec = static_cast<std::int64_t>(p.heads) * p.M * HD;
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.C);
@@ -341,8 +396,8 @@ __device__ __forceinline__ void epilogue_qkv_rope(const Params& p, std::uint32_t
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const float4 q = cs[j];  // (cos_2j, sin_2j, cos_2j+1, sin_2j+1)
-                    const float x0 = __uint_as_float(lo[2 * j]), y0 = __uint_as_float(hi[2 * j]);
-                    const float x1 = __uint_as_float(lo[2 * j + 1]), y1 = __uint_as_float(hi[2 * j + 1]);
+                    const float x0 = __uint_as_float(lo[2 * j]) * alpha, y0 = __uint_as_float(hi[2 * j]) * alpha;
+                    const float x1 = __uint_as_float(lo[2 * j + 1]) * alpha, y1 = __uint_as_float(hi[2 * j + 1]) * alpha;
                     a[2 * j] = x0 * q.x - y0 * q.y;
                     b[2 * j] = y0 * q.x + x0 * q.y;
                     a[2 * j + 1] = x1 * q.z - y1 * q.w;
@@ -368,7 +423,7 @@ __device__ __forceinline__ void epilogue_qkv_rope(const Params& p, std::uint32_t
                 if (!row_ok) continue;
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    dst[static_cast<std::int64_t>(c0 + j) * p.M] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                    dst[static_cast<std::int64_t>(c0 + j) * p.M] = __float2bfloat16_rn(__uint_as_float(v[j]) * alpha);
             }
         }
     }
@@ -494,23 +549,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             int b, mb, nb;
             decode(p, t, b, mb, nb);
             if (tile_skipped(p, mb, nb, BN)) continue;
-            mbar_wait(tfull + 8 * acc, acc_phase);
-            tc_fence_after();
             const int row = mb * kBM + lane_base + lane;
             const bool row_ok = row < p.M;
+            const float alpha = row_alpha(p, row, row_ok);  // before the wait: overlaps this tile's MMAs
+            mbar_wait(tfull + 8 * acc, acc_phase);
+            tc_fence_after();
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
             if (p.epi == 1) {
-                epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok);
+                epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok, alpha);
             } else if (p.epi == 2) {
-                epilogue_qkv_rope(p, tbase, row, nb * BN, BN, row_ok);
+                epilogue_qkv_rope(p, tbase, row, nb * BN, BN, row_ok, alpha);
             } else {
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
                     std::uint32_t r[32];
                     TN_LD32(tbase + c0, r);
                     tc_wait_ld();
-                    store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                    store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok, alpha);
                 }
             }
             tc_fence_before();
@@ -771,11 +827,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int w = BN / sl;      // accumulator columns of this segment
             const int n0 = nb * BN + k * w;  // first GEMM column (plain / qkv)
             const int row0 = mb * BM2 + static_cast<int>(rank) * HALF + lane_base;
+            const int row = row0 + lane;
+            const bool row_ok = row < p.M;
+            const float alpha = row_alpha(p, row, row_ok);  // before the wait: overlaps this tile's MMAs
+            const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
             mbar_wait(tfull + 8 * acc, acc_phase);
             tc_fence_after();
-            const int row = mb * BM2 + static_cast<int>(rank) * HALF + lane_base + lane;
-            const bool row_ok = row < p.M;
-            const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
             if (kb0 > 0) {
                 // Stream-K contributor (the first segment of this pair's
@@ -833,28 +890,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             r[4 * j + 3] = __float_as_uint(__uint_as_float(r[4 * j + 3]) + x.w);
                         }
                     }
-                    if (p.epi == 0) store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok);
+                    if (p.epi == 0) store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok, alpha);
                     else TN_ST32(tbase + c0, r);  // summed tile back to TMEM for the fused epilogue
                 }
                 if (p.epi != 0) {
                     tc_wait_st();
-                    if (p.epi == 1) epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok);
-                    else epilogue_qkv_rope(p, tbase, row, n0, BN, row_ok);
+                    if (p.epi == 1) epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok, alpha);
+                    else epilogue_qkv_rope(p, tbase, row, n0, BN, row_ok, alpha);
                 }
             } else if (p.epi == 1) {  // [gate | up] halves of w/2 columns -> output columns nb*128 + k*w/2
-                if (p.tma_c) epilogue_swiglu_tma(p, &tc, st, tbase, row0, w / 2, nb * (BN / 2) + k * (w / 2), b);
-                else epilogue_swiglu(p, tbase, off, w / 2, nb * (BN / 2) + k * (w / 2), row_ok);
+                if (p.tma_c) epilogue_swiglu_tma(p, &tc, st, tbase, row0, w / 2, nb * (BN / 2) + k * (w / 2), b, alpha);
+                else epilogue_swiglu(p, tbase, off, w / 2, nb * (BN / 2) + k * (w / 2), row_ok, alpha);
             } else if (p.epi == 2) {
-                epilogue_qkv_rope(p, tbase, row, n0, w, row_ok);
+                epilogue_qkv_rope(p, tbase, row, n0, w, row_ok, alpha);
             } else if (p.tma_c) {
-                epilogue_plain_tma(p, &tc, st, tbase, off, row0, n0, w, b, row_ok);
+                epilogue_plain_tma(p, &tc, st, tbase, off, row0, n0, w, b, row_ok, alpha);
             } else {
 #pragma unroll 1
                 for (int c0 = 0; c0 < w; c0 += 32) {
                     std::uint32_t r[32];
                     TN_LD32(tbase + c0, r);
                     tc_wait_ld();
-                    store_chunk(p, r, off, n0 + c0, row_ok, vec_ok);
+                    store_chunk(p, r, off, n0 + c0, row_ok, vec_ok, alpha);
                 }
             }
             tc_fence_before();
@@ -893,15 +950,15 @@ constexpr int kThreadsW = 32 * 10;
 // Plain epilogue of one 128-row x BN accumulator slab: two 32-column TMEM
 // loads in flight per wait.
 __device__ __forceinline__ void epilogue_plain(const Params& p, std::uint32_t tbase, std::int64_t off, int n0, int width,
-                                               bool row_ok, bool vec_ok) {
+                                               bool row_ok, bool vec_ok, float alpha) {
 #pragma unroll 1
     for (int c0 = 0; c0 < width; c0 += 64) {
         std::uint32_t r0[32], r1[32];
         TN_LD32(tbase + c0, r0);
         TN_LD32(tbase + c0 + 32, r1);
         tc_wait_ld();
-        store_chunk(p, r0, off, n0 + c0, row_ok, vec_ok);
-        store_chunk(p, r1, off, n0 + c0 + 32, row_ok, vec_ok);
+        store_chunk(p, r0, off, n0 + c0, row_ok, vec_ok, alpha);
+        store_chunk(p, r1, off, n0 + c0 + 32, row_ok, vec_ok, alpha);
     }
 }
 
@@ -1068,22 +1125,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                             ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
         for_each_tile([&](int b, int mb, int nb, int k, int sl) {
             const int w = BN / sl;
-            mbar_wait(tfull, tphase);
-            tc_fence_after();
             const int row = mb * BMW + h * 256 + static_cast<int>(rank) * HALF + lane_base + lane;
             const bool row_ok = row < p.M;
+            const float alpha = row_alpha(p, row, row_ok);  // before the wait: overlaps this tile's MMAs
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+            mbar_wait(tfull, tphase);
+            tc_fence_after();
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + h * 256;
             const int row0 = row - lane;
             if (p.epi == 1) {
-                if (p.tma_c) epilogue_swiglu_tma(p, &tc, st, tbase, row0, w / 2, nb * (BN / 2) + k * (w / 2), b);
-                else epilogue_swiglu(p, tbase, off, w / 2, nb * (BN / 2) + k * (w / 2), row_ok);
+                if (p.tma_c) epilogue_swiglu_tma(p, &tc, st, tbase, row0, w / 2, nb * (BN / 2) + k * (w / 2), b, alpha);
+                else epilogue_swiglu(p, tbase, off, w / 2, nb * (BN / 2) + k * (w / 2), row_ok, alpha);
             } else if (p.epi == 2) {
-                epilogue_qkv_rope(p, tbase, row, nb * BN + k * w, w, row_ok);
+                epilogue_qkv_rope(p, tbase, row, nb * BN + k * w, w, row_ok, alpha);
             } else if (p.tma_c) {
-                epilogue_plain_tma(p, &tc, st, tbase, off, row0, nb * BN + k * w, w, b, row_ok);
+                epilogue_plain_tma(p, &tc, st, tbase, off, row0, nb * BN + k * w, w, b, row_ok, alpha);
             } else {
-                epilogue_plain(p, tbase, off, nb * BN + k * w, w, row_ok, vec_ok);
+                epilogue_plain(p, tbase, off, nb * BN + k * w, w, row_ok, vec_ok, alpha);
             }
             tc_fence_before();
             __syncwarp();
@@ -1116,6 +1174,12 @@ __global__ void gemm_simt_kernel(GemmArgs a) {
     if (a.causal == 1 && n > m) return;
     int kend = a.K;
     if (a.causal == 2) kend = min(kend, m + 1);
+    float alpha = a.alpha;
+    if (a.rs_P) {
+        float ss = 0.f;
+        for (int c = 0; c < a.rs_chunks; ++c) ss += a.rs_P[static_cast<std::int64_t>(a.rs_row0 + m) * a.rs_ld + c];
+        alpha *= rsqrtf(ss * a.rs_inv_dim + a.rs_eps);
+    }
     auto dot = [&](int col) {
         float acc = 0.f;
         if (a.in_dtype == BF16) {
@@ -1129,7 +1193,7 @@ __global__ void gemm_simt_kernel(GemmArgs a) {
         }
 #pragma unroll
         for (int o = 16; o > 0; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        return acc * a.alpha;
+        return acc * alpha;
     };
     float acc = dot(n);
     if (a.epi == 1) {
@@ -1229,10 +1293,13 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         const int oes = dtype_size(a.out_dtype);
         const int n_out = a.epi == 1 ? a.N / 2 : a.N;
         const bool cb = a.batch > 1;
+        // (fused-norm producers: batch index 1 of the map is the h block after C)
+        const bool no = a.no_P != nullptr;
         plan->tc_ok = ok && two_sm && (a.epi == 0 || a.epi == 1) && (a.out_dtype == BF16 || a.out_dtype == F32) &&
                       al16(a.C) && (a.ldc * oes) % 16 == 0 && (!cb || (a.sc * oes) % 16 == 0) &&
                       (a.R == nullptr || al16(a.R)) && n_out % 32 == 0 &&
-                      encode_tma_3d_swz(&plan->tc, a.C, oes, n_out, a.M, a.ldc, cb ? a.batch : 1, a.sc, 64 / oes, 32,
+                      encode_tma_3d_swz(&plan->tc, a.C, oes, n_out, a.M, a.ldc, no ? 2 : cb ? a.batch : 1,
+                                        no ? static_cast<std::int64_t>(a.M) * a.ldc : a.sc, 64 / oes, 32,
                                         CU_TENSOR_MAP_SWIZZLE_64B);
     }
     plan->path = ok ? (two_sm ? 2 : 0) : 1;
@@ -1244,6 +1311,11 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         if (env && std::strcmp(env, "wide") == 0) tile = 2;
     }
     if (plan->path == 2 && tile == 2) plan->path = 3;
+    if (a.no_P) {  // fused-norm producer: only the TMA-store epilogue of the CTA-pair kernels writes x | h | P
+        if (!(plan->path == 2 || plan->path == 3) || !plan->tc_ok || a.epi != 0 || a.R == nullptr ||
+            a.out_dtype != BF16 || a.batch != 1 || a.causal != 0 || a.N % 32 != 0 || !al16(a.no_g) || tile == 3)
+            return cudaErrorNotSupported;
+    }
     // Tail of the last, partial wave of pairs: its tiles are split into
     // sl in {1, 2, 4} N-slices (slice_brow) so that the tail costs
     // ceil(rem * sl / P) / sl tile-times. SwiGLU slices keep gate/up pairs;
@@ -1284,7 +1356,9 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         const long long nkb = (static_cast<long long>(a.K) * es + kAtom - 1) / kAtom;
         static const char* wenv = std::getenv("TN_GEMM_WIDE_BIAS");  // tuning override
         const double bias = wenv ? std::atof(wenv) : (nkb >= 128 ? 1.2 : 0.9);
-        if (a.epi != 2 && t_wide <= t_narrow * bias + 1e-9 && (a.M % 512 == 0 || a.M > 2048)) plan->path = 3;
+        // fused-norm producers stage two outputs per chunk: their drain would
+        // double the wide tiles' exposed accumulator hand-off, so they stay narrow
+        if (a.epi != 2 && !a.no_P && t_wide <= t_narrow * bias + 1e-9 && (a.M % 512 == 0 || a.M > 2048)) plan->path = 3;
     }
     const int bm = plan->path == 2 ? 256 : plan->path == 3 ? 512 : kBM;
     const int tm = (a.M + bm - 1) / bm, tn = (a.N + bn - 1) / bn;
@@ -1299,7 +1373,7 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         // blocks). Measured on B200 it never beat the sliced tail (fix-up
         // traffic + serialised finishers), so it is off by default.
         static const char* sk_env = std::getenv("TN_GEMM_SK");
-        const bool sk_on = plan->path == 2 && (tile == 3 || (sk_env && std::strcmp(sk_env, "1") == 0));
+        const bool sk_on = plan->path == 2 && !a.no_P && (tile == 3 || (sk_env && std::strcmp(sk_env, "1") == 0));
         if (sk_on) {
             if (a.causal == 0 && T >= npairs && T % npairs != 0) {
                 const int sk = T / npairs >= 2 ? T % npairs + npairs : T;
@@ -1371,6 +1445,14 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
     p.tail_units = plan.tail_units;
     p.dp_tiles = plan.tiles - plan.tail_units / p.tail_split;
     p.tma_c = plan.tc_ok && (plan.path == 2 || plan.path == 3) && (a.epi == 0 || a.epi == 1) ? 1 : 0;
+    p.rs_P = a.rs_P;
+    p.rs_ld = a.rs_ld;
+    p.rs_row0 = a.rs_row0;
+    p.rs_chunks = a.rs_chunks;
+    p.rs_inv_dim = a.rs_inv_dim;
+    p.rs_eps = a.rs_eps;
+    p.no_g = static_cast<const __nv_bfloat16*>(a.no_g);
+    p.no_P = a.no_P;
     p.sk_nk = 0;
     p.sk_total = 0;
     p.ws = nullptr;

@@ -37,6 +37,16 @@ struct GemmArgs {
                   // 2: QKV + RoPE epilogue (hd 128): out = [rope(q) (H,M,128) | rope(k) | vᵀ (H,128,M)]
     const void* rope = nullptr;  // epi 2: fp32 [M, 64, 2] (cos, sin)
     int heads = 0;               // epi 2: heads per section, N = 3 * heads * 128
+    // Fused RMSNorm, consumer side: row m is scaled by
+    // rsqrt(sum_{c < rs_chunks} rs_P[(rs_row0 + m) * rs_ld + c] / dim + eps).
+    const float* rs_P = nullptr;
+    int rs_ld = 0, rs_row0 = 0, rs_chunks = 0;
+    float rs_inv_dim = 0.f, rs_eps = 0.f;
+    // Fused RMSNorm, producer side (plain epilogue with residual R, bf16 out,
+    // batch 1): C = x = bf16(alpha*A·Bᵀ + R), then h = bf16(x * no_g) in the
+    // M*ldc elements after C, and no_P[m * (N/32) + c] = sum of x[m, 32c..32c+31]^2.
+    const void* no_g = nullptr;
+    float* no_P = nullptr;
     int tile = 0;                // CTA-pair tile: 0 auto, 1 narrow (256x256), 2 wide (512x256),
                                  // 3 narrow with a stream-K tail (instead of half-width tail tiles)
 };
@@ -141,6 +151,9 @@ cudaError_t concat(const void* const* parts, int n, std::int64_t part_bytes, voi
 // out[t][:] = table[tokens[t]][:]   (tokens int32, table bf16 [vocab, dim])
 cudaError_t embedding(const void* tokens, const void* table, void* out, int seq, int dim, int vocab,
                       cudaStream_t s);
+// Embedding + fused-RMSNorm producer outputs: [x | h = x*g | P] (see GemmArgs::no_P).
+cudaError_t embedding_norm(const void* tokens, const void* table, const void* g, void* out, int seq, int dim, int vocab,
+                           cudaStream_t s);
 
 // --- training (LoRA step) tasks ---------------------------------------------
 // out[b][c][r] = in[b][r][c], esize 2 or 4 bytes.

@@ -187,7 +187,7 @@ LLAMA_65B = LlamaConfig(dim=8192, layers=80, heads=64, ffn=22016)
 
 def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device: int = 0,
                   std: float = 0.02, fused_attention: bool = True, fused_swiglu: bool = True,
-                  fused_qkv: bool = True) -> GraphBuilder:
+                  fused_qkv: bool = True, fused_norm: bool = False) -> GraphBuilder:
     """One forward prefill over `seq` tokens (causal), single device.
 
     Per layer: rmsnorm -> QKV gemm -> rope(q), rope(k), Vᵀ -> attention ->
@@ -203,11 +203,23 @@ def llama_prefill(cfg: LlamaConfig, seq: int, layers: int | None = None, device:
     `fused_qkv` (hd 128, fused attention) the QKV GEMM's epilogue applies RoPE
     to q/k and transposes v, writing one packed [q | k | vᵀ] tensor that the
     attention vertex reads by offset.
+    With `fused_norm` (on top of fused_qkv and fused_swiglu) there are no
+    RMSNorm vertices: every producer of the residual stream (the embedding,
+    each attn_out / ffn_out GEMM) writes [x | h = x*gamma | P] where gamma is
+    the next norm's weight and P the per-32-column sums of x^2; the consuming
+    GEMM reads h and scales its output rows by rsqrt(sum P / dim + eps) in
+    the epilogue (see _llama_fused_norm). Off by default: it removes the 65
+    RMSNorm launches (1.5 ms of the 7B step) but the extra h / P stores and
+    row-scale loads in the GEMM epilogues cost more — paired A/B on one B200
+    (tools/ab_fused_norm.py): 51.24 ms unfused vs 52.62 ms fused per step.
     Head: final rmsnorm -> last-token logits (fp32). Weights are graph inputs
     (cold in host RAM, materialised by H2D at dispatch).
     """
     L = cfg.layers if layers is None else layers
     d, H, hd, f, V, S = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, cfg.vocab, seq
+    if (fused_norm and fused_qkv and fused_swiglu and fused_attention and hd == 128 and f % 128 == 0
+            and d % 256 == 0 and S >= 256):  # norm_out producers need the CTA-pair GEMM path (M >= 256)
+        return _llama_fused_norm(cfg, S, L, device, std)
     g = GraphBuilder(device_count=1)
     dev = device
     tok = g.input("tokens", (S,), "i32", dev, init=("tokens", V))
@@ -275,6 +287,58 @@ def _ffn(g, p, h2, w13, w2, x, S, d, f, dev, fused_swiglu):
         gu = g.gemm(p + "gate_up", h2, w13, S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
         a = g.kernel(p + "act", {"type": "silu_mul", "args": [gu], "rows": S, "cols": f}, (S, f), "bf16", dev)
     return g.gemm(p + "ffn_out", a, w2, S, d, f, r=x, out_shape=(S, d), device=dev)
+
+
+def _llama_fused_norm(cfg: LlamaConfig, S: int, L: int, dev: int, std: float) -> GraphBuilder:
+    """llama_prefill with every RMSNorm fused into its producer / consumer
+    (same inputs and names as the unfused graph). Residual-stream vertices
+    hold [x (S x d bf16) | h = bf16(x * gamma) | P (S x d/32 fp32)]:
+      embed:    x = table rows                 (gamma: layer 0 attention_norm)
+      attn_out: x = o·woᵀ + x_prev             (gamma: ffn_norm)
+      ffn_out:  x = act·w2ᵀ + x_prev           (gamma: next attention_norm / final norm)
+    and the consumers (qkv_rope, swiglu, the last-token head) read h and
+    scale row m by rsqrt(sum_c P[c][m] / d + eps) — RMSNorm(x) W^T =
+    diag(r) (x * gamma) W^T."""
+    d, H, hd, f, V = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, cfg.vocab
+    g = GraphBuilder(device_count=1)
+    xn_shape = (2 * S * d + 2 * S * (d // 32),)  # [x | h | P] in bf16-sized units
+    p_off = 2 * S * d * 2                          # byte offset of P
+    rs = {"rs_arg": 0, "rs_off": p_off, "rs_ld": d // 32, "rs_dim": d, "eps": cfg.eps}
+    tok = g.input("tokens", (S,), "i32", dev, init=("tokens", V))
+    emb = g.input("tok_embeddings", (V, d), "bf16", dev, init=("normal", std))
+    rope_tab = g.input("rope_table", (S, hd // 2, 2), "f32", dev, init=("rope", cfg.theta))
+    wn1 = g.input("layers.0.attention_norm", (d,), "bf16", dev, init=("normal", 1.0))
+    x = g.kernel("embed", {"type": "embedding", "args": [tok, emb, wn1], "seq": S, "dim": d, "vocab": V,
+                           "norm_out": 1}, xn_shape, "bf16", dev)
+    for l in range(L):
+        p = f"layers.{l}."
+        wqkv = g.input(p + "wqkv", (3 * d, d), "bf16", dev, init=("normal", std))
+        wo = g.input(p + "wo", (d, d), "bf16", dev, init=("normal", std))
+        wn2 = g.input(p + "ffn_norm", (d,), "bf16", dev, init=("normal", 1.0))
+        w13 = g.input(p + "w13", (2 * f, d), "bf16", dev, init=("normal", std))
+        w2 = g.input(p + "w2", (d, f), "bf16", dev, init=("normal", std))
+        qkv = g.gemm(p + "qkv_rope", x, wqkv, S, 3 * d, d, r=rope_tab, epilogue="qkv_rope", heads=H,
+                     a_off=S * d, out_shape=(3, H, S, hd), device=dev, **rs)
+        sec = H * S * hd
+        op = {"type": "attention", "args": [qkv], "q_off": 0, "k_off": sec, "v_off": 2 * sec, "heads": H,
+              "seq": S, "hd": hd, "ldo": d, "scale": 1.0 / math.sqrt(hd), "causal": 1}
+        o = g.kernel(p + "attn", op, (S, d), "bf16", dev, cost=2.0 * S * S * hd * H / _PEAK_FLOPS)
+        g.flops += 2.0 * S * S * hd * H * (1 + 1 / S)
+        x = g.kernel(p + "attn_out", {"type": "gemm", "args": [o, wo, x, wn2], "M": S, "N": d, "K": d,
+                                      "in_dtype": "bf16", "out_dtype": "bf16", "norm_out": 1},
+                     xn_shape, "bf16", dev, cost=2.0 * S * d * d / _PEAK_FLOPS)
+        g.flops += 2.0 * S * d * d
+        a = g.gemm(p + "act", x, w13, S, 2 * f, d, epilogue="swiglu", a_off=S * d, out_shape=(S, f), device=dev, **rs)
+        gn = (g.input(f"layers.{l + 1}.attention_norm", (d,), "bf16", dev, init=("normal", 1.0)) if l + 1 < L
+              else g.input("norm", (d,), "bf16", dev, init=("normal", 1.0)))
+        x = g.kernel(p + "ffn_out", {"type": "gemm", "args": [a, w2, x, gn], "M": S, "N": d, "K": f,
+                                     "in_dtype": "bf16", "out_dtype": "bf16", "norm_out": 1},
+                     xn_shape, "bf16", dev, cost=2.0 * S * d * f / _PEAK_FLOPS)
+        g.flops += 2.0 * S * d * f
+    wout = g.input("output", (V, d), "bf16", dev, init=("normal", std))
+    g.gemm("logits", x, wout, 1, V, d, a_off=S * d + (S - 1) * d, out_dtype="f32", out_shape=(1, V), device=dev,
+           rs_row0=S - 1, **rs)
+    return g
 
 
 def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = None,

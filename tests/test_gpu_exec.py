@@ -14,7 +14,7 @@ import json
 import numpy as np
 import pytest
 
-from helpers import inputs_of, oracle_outputs, out_values, rel_err, replay_capacity, small_llama
+from helpers import SMALL, inputs_of, oracle_outputs, out_values, rel_err, replay_capacity, small_llama
 from paper_2405_16283_b200 import workloads as W
 from paper_2405_16283_b200.executor import Executor, execute
 
@@ -216,6 +216,22 @@ def test_llama_small_parity_with_offloads():
     (o,) = g.outputs()
     assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 3e-2
     assert trace["host_bytes_transferred"] > 0
+
+
+def test_llama_fused_norm_parity_with_offloads():
+    """The fused-RMSNorm graph option (producers write [x | x*gamma | sum x^2],
+    consumers scale rows in the epilogue; no rmsnorm vertices) on the GPU vs
+    the oracle of the same graph, under an offloading plan."""
+    g = W.llama_prefill(SMALL, 256, layers=2, fused_norm=True)
+    assert not any((v.get("op") or {}).get("type") == "rmsnorm" for v in g.vertices)
+    cap = int(W.working_set_floor(g)[0] * 1.5) // 1024 * 1024
+    mg, stats = W.plan(g, cap, alloc_horizon="lazy")
+    assert stats["offloads"] > 0
+    inp = inputs_of(g, seed=5)
+    _, got = run_gpu(g, mg, inp)
+    want = oracle_outputs(g, mg, inp)
+    (o,) = g.outputs()
+    assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 3e-2
 
 
 @pytest.mark.parametrize("cfg", [{"lookahead": 1}, {"lookahead": 0}, {"lookahead": 0, "completion": "callback"},

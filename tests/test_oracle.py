@@ -229,7 +229,7 @@ def test_llama_graph_matches_hf_transformers():
     torch = pytest.importorskip("torch")
     tr = pytest.importorskip("transformers")
     from oracle import ops_ref as R
-    cfg, S, L = W.LlamaConfig(dim=256, layers=2, heads=2, ffn=512, vocab=300), 64, 2
+    cfg, S, L = W.LlamaConfig(dim=256, layers=2, heads=2, ffn=512, vocab=300), 256, 2
     g = W.llama_prefill(cfg, S, layers=L)
     mg, _ = W.plan(g, 1 << 30)
     inp = inputs_of(g, seed=7)
@@ -274,3 +274,24 @@ def test_llama_graph_matches_hf_transformers():
     print("oracle vs HF transformers fp32, last-token logits: rel err", err)
     assert err < 2e-2
     assert int(np.argmax(ours)) == int(np.argmax(ref))
+
+
+def test_fused_norm_graph_equals_unfused():
+    """The fused-RMSNorm graph (norms folded into the residual producers'
+    [x | x*gamma | sum x^2] outputs and the consumers' row scales) computes
+    the same logits as the graph with RMSNorm vertices, up to where bf16
+    rounding happens (x*gamma rounded before the GEMM instead of x*r*gamma)."""
+    cfg, S = W.LlamaConfig(dim=256, layers=2, heads=2, ffn=512, vocab=300), 256
+    gf = W.llama_prefill(cfg, S, layers=2, fused_norm=True)
+    gu = W.llama_prefill(cfg, S, layers=2)
+    assert not any((v.get("op") or {}).get("type") == "rmsnorm" for v in gf.vertices)
+    assert sum((v.get("op") or {}).get("type") == "rmsnorm" for v in gu.vertices) == 5
+    mgf, _ = W.plan(gf, 1 << 30)
+    mgu, _ = W.plan(gu, 1 << 30)
+    inu = inputs_of(gu, seed=7)
+    byname = {gu.tensors[v].name: a for v, a in inu.items()}
+    inf = {t.id: byname[t.name] for t in gf.inputs()}
+    (of,), (ou,) = gf.outputs(), gu.outputs()
+    a = out_values(gf, of, oracle_outputs(gf, mgf, inf)[of])
+    b = out_values(gu, ou, oracle_outputs(gu, mgu, inu)[ou])
+    assert rel_err(a, b) < 1.5e-2
