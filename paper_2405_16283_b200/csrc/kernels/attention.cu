@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 #include "tc_common.cuh"
@@ -28,6 +29,28 @@ constexpr int kB = 128;          // query rows per CTA
 constexpr int kN = 64;           // keys per KV block
 constexpr int kHd = 128;         // head dim of the fused path
 constexpr int kThreads = 192;
+
+// 2^x for a pair on the FMA pipe (packed FFMA2/FADD2): x = j + f with
+// j = round(x), degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (max rel.
+// error 7.6e-5, far below the bf16 rounding P gets), j added into the
+// exponent bits. x < -126 clamps to 2^-126 * 2^f (a denormal: a masked key
+// contributes < 1.7e-38); -127 would let 2^f < 1 borrow into the sign bit.
+__device__ __forceinline__ void ex2_poly2(float& a, float& b) {
+    a = fmaxf(a, -126.0f);
+    b = fmaxf(b, -126.0f);
+    float ta = a, tb = b;
+    add2(ta, tb, 12582912.0f, 12582912.0f);  // 1.5 * 2^23: low mantissa bits hold round(x)
+    float ja = ta, jb = tb;
+    add2(ja, jb, -12582912.0f, -12582912.0f);
+    float fa = a, fb = b;
+    add2(fa, fb, -ja, -jb);
+    float pa = 0.05517027f, pb = 0.05517027f;
+    fma2v(pa, pb, fa, fb, 0.24260795f);
+    fma2v(pa, pb, fa, fb, 0.6932609f);
+    fma2v(pa, pb, fa, fb, 0.9999283f);
+    a = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
+    b = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
+}
 // smem (bytes): Q 128x128 (2 atoms of 16 KB), K 2 stages x 64x128 (2 atoms of
 // 8 KB each), V 2 stages x 128(hd)x64(keys) (1 atom, 16 KB): 96 KB, so two
 // CTAs share an SM and interleave their MMA and softmax phases (the softmax
@@ -47,9 +70,16 @@ struct AttnParams {
     int causal;
 };
 
+// EMU of every 4 column pairs take 2^x on the FMA pipe (ex2_poly2), the rest
+// on MUFU.EX2: MUFU does 16 ex2/clk/SM, the same rate the two MMAs consume
+// scores at hd 128, so a quarter on the FMA pipe relieves it (measured:
+// EMU=1 131.9 us, 0 134.5, 2 133.3, 3 143.0 per 7B layer). Splitting each row
+// over two softmax threads (8 softmax warps) was measured slower (138-141 us).
+template <int EMU>
 __global__ void __launch_bounds__(kThreads, 2)
     attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                      const __grid_constant__ CUtensorMap tv, const AttnParams p) {
+    constexpr int CW = kN;  // score columns per softmax thread
     extern __shared__ std::uint8_t smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     if (raw & 1023u) __trap();  // SW128 tiles need 1 KB alignment
@@ -152,9 +182,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int j = 0; j < nkv; ++j) {
             mbar_wait(s_full, j & 1);
             tc_fence_after();
-            float s[kN];
+            float s[CW];
 #pragma unroll
-            for (int c = 0; c < kN; c += 32) {
+            for (int c = 0; c < CW; c += 32) {
                 std::uint32_t u[32];
                 TN_LD32(tS + trow + c, u);
 #pragma unroll
@@ -166,19 +196,19 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (lane == 0) mbar_arrive(s_free);
 
             // masked keys: key index j*kN + c > query row (causal)
-            const int lim = p.causal ? qrow - j * kN : kN;  // keys c <= lim are valid
+            const int lim = p.causal ? qrow - j * kN : CW;  // columns c <= lim are valid
             float pm[kW];
 #pragma unroll
             for (int w = 0; w < kW; ++w) pm[w] = -INFINITY;
-            if (lim < kN - 1) {
+            if (lim < CW - 1) {
 #pragma unroll
-                for (int c = 0; c < kN; ++c) {
+                for (int c = 0; c < CW; ++c) {
                     if (c > lim) s[c] = -INFINITY;
                     pm[c % kW] = fmaxf(pm[c % kW], s[c]);
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < kN; ++c) pm[c % kW] = fmaxf(pm[c % kW], s[c]);
+                for (int c = 0; c < CW; ++c) pm[c % kW] = fmaxf(pm[c % kW], s[c]);
             }
 #pragma unroll
             for (int w = kW / 2; w > 0; w /= 2)
@@ -198,10 +228,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             // x = s*scale - mx, 2^x, per-column-class partial sums: packed
             // FFMA2/FADD2 (bitwise the same as the scalar fmaf / += chain)
 #pragma unroll
-            for (int c = 0; c < kN; c += 2) {
+            for (int c = 0; c < CW; c += 2) {
                 fma2(s[c], s[c + 1], p.scale_log2, -mx);
-                s[c] = ex2(s[c]);
-                s[c + 1] = ex2(s[c + 1]);
+                if ((c % 8) < 2 * EMU) {
+                    ex2_poly2(s[c], s[c + 1]);
+                } else {
+                    s[c] = ex2(s[c]);
+                    s[c + 1] = ex2(s[c + 1]);
+                }
                 add2(ps[c % kW], ps[c % kW + 1], s[c], s[c + 1]);
             }
 #pragma unroll
@@ -228,9 +262,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
             }
             {
-                std::uint32_t pw[kN / 2];
+                std::uint32_t pw[CW / 2];
 #pragma unroll
-                for (int i = 0; i < kN / 2; ++i) {
+                for (int i = 0; i < CW / 2; ++i) {
                     __nv_bfloat162 v2 = __floats2bfloat162_rn(s[2 * i], s[2 * i + 1]);
                     pw[i] = *reinterpret_cast<std::uint32_t*>(&v2);
                 }
@@ -326,7 +360,8 @@ cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (!((attr_set >> dev) & 1ULL)) {
-            cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            cudaFuncSetAttribute(attention_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            cudaFuncSetAttribute(attention_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
             attr_set |= 1ULL << dev;
         }
     }
@@ -352,7 +387,12 @@ cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s) {
     p.ldo = a.ldo;
     p.scale_log2 = sl2;
     p.causal = a.causal;
-    attention_kernel<<<p.heads * p.nblk, kThreads, kSmem, s>>>(plan.tq, plan.tk, plan.tv, p);
+    static const char* emu_env = std::getenv("TN_ATTN_EMU");  // A/B: "0" keeps every 2^x on MUFU
+    const unsigned grid = p.heads * p.nblk;
+    if (emu_env && std::atoi(emu_env) == 0)
+        attention_kernel<0><<<grid, kThreads, kSmem, s>>>(plan.tq, plan.tk, plan.tv, p);
+    else
+        attention_kernel<1><<<grid, kThreads, kSmem, s>>>(plan.tq, plan.tk, plan.tv, p);
     return cudaGetLastError();
 }
 

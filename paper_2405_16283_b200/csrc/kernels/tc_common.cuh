@@ -142,6 +142,12 @@ __device__ __forceinline__ void fma2(float& a, float& b, float m, float c) {  //
         : "+f"(a), "+f"(b)
         : "f"(m), "f"(c));
 }
+__device__ __forceinline__ void fma2v(float& a, float& b, float x, float y, float c) {  // a = a*x + c, b = b*y + c
+    asm("{\n\t.reg .b64 t, u, v;\n\tmov.b64 t, {%0, %1};\n\tmov.b64 u, {%2, %3};\n\tmov.b64 v, {%4, %4};\n\t"
+        "fma.rn.f32x2 t, t, u, v;\n\tmov.b64 {%0, %1}, t;\n\t}"
+        : "+f"(a), "+f"(b)
+        : "f"(x), "f"(y), "f"(c));
+}
 __device__ __forceinline__ void add2(float& a, float& b, float x, float y) {  // a += x, b += y
     asm("{\n\t.reg .b64 t, u;\n\tmov.b64 t, {%0, %1};\n\tmov.b64 u, {%2, %3};\n\t"
         "add.rn.f32x2 t, t, u;\n\tmov.b64 {%0, %1}, t;\n\t}"
