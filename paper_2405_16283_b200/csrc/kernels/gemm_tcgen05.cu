@@ -1185,7 +1185,25 @@ __global__ void gemm_simt_kernel(GemmArgs a) {
         if (a.in_dtype == BF16) {
             const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
             const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B) + b * a.sb + static_cast<std::int64_t>(col) * a.ldb;
-            for (int k = lane; k < kend; k += 32) acc += __bfloat162float(A[k]) * __bfloat162float(B[k]);
+            const bool vec = ((reinterpret_cast<std::uintptr_t>(A) | reinterpret_cast<std::uintptr_t>(B)) & 15) == 0;
+            int k0 = 0;
+            if (vec) {  // 16-byte loads: lane covers 8 consecutive k per 256-wide step (GEMV heads are HBM-bound)
+                const int kv = kend / 256 * 256;
+                for (int k = lane * 8; k < kv; k += 256) {
+                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + k));
+                    const uint4 y = __ldcs(reinterpret_cast<const uint4*>(B + k));  // streamed once
+                    const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&x);
+                    const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 xf = __bfloat1622float2(xh[i]), yf = __bfloat1622float2(yh[i]);
+                        acc = fmaf(xf.x, yf.x, acc);
+                        acc = fmaf(xf.y, yf.y, acc);
+                    }
+                }
+                k0 = kv;
+            }
+            for (int k = k0 + lane; k < kend; k += 32) acc += __bfloat162float(A[k]) * __bfloat162float(B[k]);
         } else {
             const float* A = static_cast<const float*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
             const float* B = static_cast<const float*>(a.B) + b * a.sb + static_cast<std::int64_t>(col) * a.ldb;
