@@ -5,7 +5,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.hpp"
 
@@ -81,6 +84,60 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_vec(const __nv_bfloat16* 
             for (int j = 0; j < 8; ++j) v[i][j] = v[i][j] * inv * g[j];
             yr[c] = pack8(v[i]);
         }
+    }
+}
+
+// Persistent variant: grid = a few CTAs per SM, each CTA walks rows with a
+// stride and loads row i+1 into registers before reducing row i, so HBM/L2
+// latency overlaps the reduction and there is no tail wave.
+template <int kMaxVec>
+__global__ void __launch_bounds__(kRowThreads) rmsnorm_persist(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ w,
+                                                               __nv_bfloat16* __restrict__ y, int rows, int cols,
+                                                               float eps) {
+    __shared__ float red[kRowThreads / 32];
+    const int nv = cols / 8;
+    uint4 cur[kMaxVec], nxt[kMaxVec];
+    auto load = [&](std::int64_t row, uint4* dst) {
+        const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+#pragma unroll
+        for (int i = 0; i < kMaxVec; ++i) {
+            const int c = threadIdx.x + i * kRowThreads;
+            dst[i] = c < nv ? xr[c] : make_uint4(0, 0, 0, 0);
+        }
+    };
+    std::int64_t row = blockIdx.x;
+    if (row >= rows) return;
+    load(row, cur);
+    const uint4* wr = reinterpret_cast<const uint4*>(w);
+    for (; row < rows; row += gridDim.x) {
+        const std::int64_t next = row + gridDim.x;
+        if (next < rows) load(next, nxt);
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxVec; ++i) {
+            float v[8];
+            unpack8(cur[i], v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ss += v[j] * v[j];
+        }
+        ss = block_reduce<false>(ss, red);
+        const float inv = rsqrtf(ss / static_cast<float>(cols) + eps);
+        uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+#pragma unroll
+        for (int i = 0; i < kMaxVec; ++i) {
+            const int c = threadIdx.x + i * kRowThreads;
+            if (c < nv) {
+                float v[8], g[8];
+                unpack8(cur[i], v);
+                unpack8(wr[c], g);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = v[j] * inv * g[j];
+                yr[c] = pack8(v);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxVec; ++i) cur[i] = nxt[i];
     }
 }
 
@@ -279,7 +336,18 @@ cudaError_t rmsnorm(const void* x, const void* w, void* y, int rows, int cols, f
     auto X = static_cast<const __nv_bfloat16*>(x);
     auto W = static_cast<const __nv_bfloat16*>(w);
     auto Y = static_cast<__nv_bfloat16*>(y);
-    if (cols % 8 == 0 && al16(x) && al16(w) && al16(y) && cols <= kRowThreads * 8 * 8) {
+    static const char* env = std::getenv("TN_RMSNORM");  // A/B: "vec" = one CTA per row
+    const bool persist = !(env && std::strcmp(env, "vec") == 0);
+    if (persist && cols % 8 == 0 && al16(x) && al16(w) && al16(y) && cols <= kRowThreads * 8 * 4) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        static const char* cps_env = std::getenv("TN_RMSNORM_CPS");  // tuning: CTAs per SM
+        const int cps = cps_env ? std::atoi(cps_env) : 4;
+        const int grid = std::min(rows, sms * cps);
+        if (cols <= kRowThreads * 8 * 2) rmsnorm_persist<2><<<grid, kRowThreads, 0, s>>>(X, W, Y, rows, cols, eps);
+        else rmsnorm_persist<4><<<grid, kRowThreads, 0, s>>>(X, W, Y, rows, cols, eps);
+    } else if (cols % 8 == 0 && al16(x) && al16(w) && al16(y) && cols <= kRowThreads * 8 * 8) {
         if (cols <= kRowThreads * 8 * 2) rmsnorm_vec<2><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
         else if (cols <= kRowThreads * 8 * 4) rmsnorm_vec<4><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
         else rmsnorm_vec<8><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
