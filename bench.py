@@ -284,6 +284,36 @@ def cpu_sample(cfg, seq, layers_full):
 
 
 # ------------------------------------------------------------------- arms ---
+def reference_planner_leg(g, cap, horizon):
+    """The unmodified reference (oracle/_ref, built from /root/reference by
+    oracle/Makefile) on the same taskgraph: build_memgraph + simulate, timed on
+    one host core, and its memgraph byte-compared with ours (live parity)."""
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(ref_dir):
+        return {"unavailable": "oracle/_ref not built (needs /root/reference at build time)"}
+    sys.path.insert(0, ref_dir)
+    try:
+        import _memplan
+    except ImportError as e:
+        return {"unavailable": f"oracle/_ref/_memplan not importable: {e}"}
+    from paper_2405_16283_b200 import memplan
+
+    tg = g.to_json()
+    t0 = time.perf_counter()
+    ref_mg, ref_stats = _memplan.build_memgraph(tg, [cap], mode="byte", alloc_horizon=horizon)
+    t1 = time.perf_counter()
+    ref_trace = _memplan.simulate(ref_mg)
+    t2 = time.perf_counter()
+    ours_mg, _ = memplan.build_memgraph(tg, [cap], mode="byte", alloc_horizon=horizon)
+    t3 = time.perf_counter()
+    ours_trace = memplan.simulate(ours_mg)
+    t4 = time.perf_counter()
+    return {"build_memgraph_s": round(t1 - t0, 4), "simulate_s": round(t2 - t1, 4),
+            "ours_build_memgraph_s": round(t3 - t2, 4), "ours_simulate_s": round(t4 - t3, 4),
+            "vertices": len(json.loads(ref_mg)["vertices"]), "memgraph_bytes_identical": ref_mg == ours_mg,
+            "simulate_trace_identical": ref_trace == ours_trace, "cores": 1}
+
+
 def run_reference(args, world, rank):
     """The reference arm: the reference has no tensor executor (its run API is
     an abstract-time simulator), so the CPU implementation timed
@@ -303,6 +333,8 @@ def run_reference(args, world, rank):
         vals.append(s["value"])
         samples.append(s["sample_s"])
     v = statistics.mean(vals)
+    g7 = W.llama_prefill(cfg, args.seq, layers=args.layers)
+    planner = reference_planner_leg(g7, int(args.cap_gib * (1 << 30)), args.horizon)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(args.seq / v * 1e3, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -311,7 +343,8 @@ def run_reference(args, world, rank):
             "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": "per step: 1 of 32 decoder layers at seq 4096, extrapolated x32; "
                                        f"layer times {samples}"},
-            "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_planner": planner}
     print(json.dumps(line), flush=True)
 
 
