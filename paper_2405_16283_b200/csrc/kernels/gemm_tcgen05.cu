@@ -1,18 +1,26 @@
 // Contraction tasks: C = alpha * A·Bᵀ (+ R), batched, on
-// the 5th-gen tensor cores.
+// the 5th-gen tensor cores. Three persistent warp-specialised kernels:
 //
-// Persistent warp-specialised kernel, one CTA per SM:
-//   warp 0   TMA producer   — 4-stage ring of 128-byte-swizzled K-major A/B
-//                             tiles (cp.async.bulk.tensor + mbarrier tx count)
-//   warp 1   MMA issuer     — one thread issues tcgen05.mma (M=128, N=BN,
-//                             K=32 bytes per instruction) into a TMEM
-//                             accumulator, double-buffered (2*BN columns) so
-//                             the epilogue of tile i overlaps the MMAs of i+1
-//   warps 2-5 epilogue      — tcgen05.ld 32x32b → fp32 regs → alpha,
-//                             residual add, bf16/fp32 pack → 16-byte stores
+//   gemm_kernel<BN>     1 CTA per SM, M=128 x N=BN tiles (small shapes):
+//     warp 0 TMA producer (4-stage ring of 128-byte-swizzled K-major A/B
+//     tiles, cp.async.bulk.tensor + mbarrier tx counts), warp 1 MMA issuer
+//     (tcgen05.mma into a double-buffered TMEM accumulator, one elected lane
+//     of a converged warp), warps 2-5 epilogue (tcgen05.ld -> registers).
+//   gemm_kernel_2sm     CTA pairs (cta_group::2, cluster 2), 256x256 tiles:
+//     the leader issues M=256 MMAs, each CTA stages half of A and half of B,
+//     multicast commits; double-buffered 2x256-column accumulators.
+//   gemm_kernel_2sm_w   CTA pairs, 512x256 "wide" tiles: each CTA owns two
+//     128-row halves (all 512 TMEM columns), two drain warpgroups; 25 % fewer
+//     operand bytes per FLOP, used for long K.
+// Tails: the last partial wave of pair tiles is split into 2 or 4 N-slices
+// (slice_brow); stream-K is available as tile "streamk". Epilogues: alpha,
+// residual, SwiGLU, QKV+RoPE+Vᵀ, fused-RMSNorm producer/consumer; plain /
+// residual / SwiGLU outputs of the pair kernels go through per-warp
+// SWIZZLE_64B smem boxes and cp.async.bulk.tensor stores.
 // bf16 inputs use kind::f16, fp32 inputs kind::tf32 (same byte geometry:
 // a K block is always one 128-byte swizzle atom).
-// Deterministic: each output element is accumulated by one CTA in K order.
+// Deterministic: each output element is accumulated by one CTA in K order
+// (stream-K partials are summed in ascending pair order).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
