@@ -342,7 +342,7 @@ def _llama_fused_norm(cfg: LlamaConfig, S: int, L: int, dev: int, std: float) ->
 
 
 def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = None,
-                     std: float = 0.02) -> GraphBuilder:
+                     std: float = 0.02, fused_qkv: bool = True) -> GraphBuilder:
     """Config 3: tensor-parallel prefill over `tp` memgraph devices (Megatron
     layout). QKV / gate-up are column-parallel (each device owns
     heads / ffn columns), O / down are row-parallel and produce per-device
@@ -354,7 +354,9 @@ def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = N
         (Transfer) and concatenates them (`concat`) into its replica of x.
     The residual stream x is replicated; weights are per-device inputs
     (host-resident, sliced exactly like a TP checkpoint shard). The final norm
-    and last-token logits run on device 0."""
+    and last-token logits run on device 0. With `fused_qkv` (hd 128) each
+    device's QKV GEMM applies RoPE and transposes V in its epilogue (packed
+    [q | k | vᵀ] read by offset in attention), as in llama_prefill."""
     L = cfg.layers if layers is None else layers
     d, H, hd, f, V, S = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, cfg.vocab, seq
     assert H % tp == 0 and f % tp == 0 and S % tp == 0
@@ -395,6 +397,16 @@ def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = N
             wqkv = g.input(p + f"wqkv@{r}", (3 * dl, d), "bf16", r, init=("normal", std))
             h = g.kernel(p + f"attn_norm_out@{r}", {"type": "rmsnorm", "args": [x[r], wn1], "rows": S, "cols": d,
                                                      "eps": cfg.eps}, (S, d), "bf16", r)
+            if fused_qkv and hd == 128:
+                qkv = g.gemm(p + f"qkv_rope@{r}", h, wqkv, S, 3 * dl, d, r=tab[r], epilogue="qkv_rope", heads=Hl,
+                             out_shape=(3, Hl, S, hd), device=r)
+                sec = Hl * S * hd
+                o[r] = g.kernel(p + f"attn@{r}", {"type": "attention", "args": [qkv], "q_off": 0, "k_off": sec,
+                                                  "v_off": 2 * sec, "heads": Hl, "seq": S, "hd": hd, "ldo": dl,
+                                                  "scale": 1.0 / math.sqrt(hd), "causal": 1}, (S, dl), "bf16", r,
+                                cost=2.0 * S * S * hd * Hl / _PEAK_FLOPS)
+                g.flops += 2.0 * S * S * hd * Hl * (1 + 1 / S)
+                continue
             qkv = g.gemm(p + f"qkv@{r}", h, wqkv, S, 3 * dl, d, out_shape=(S, 3 * dl), device=r)
             q = g.kernel(p + f"q_rope@{r}", {"type": "rope", "args": [qkv, tab[r]], "seq": S, "ld": 3 * dl, "col_off": 0,
                                              "heads": Hl, "hd": hd}, (Hl, S, hd), "bf16", r)

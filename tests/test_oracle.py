@@ -140,6 +140,26 @@ def test_tensor_parallel_graph_equals_single_device():
     assert rel_err(got, want) < 2e-2
 
 
+def test_tensor_parallel_fused_qkv_equals_unfused():
+    """The TP graph with the fused QKV+RoPE+Vᵀ epilogue per device (hd 128)
+    computes the same logits as the TP graph with separate rope/transpose
+    vertices, from the same shards."""
+    cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=512, vocab=300)
+    ga = W.llama_prefill_tp(cfg, 128, tp=2)
+    gb = W.llama_prefill_tp(cfg, 128, tp=2, fused_qkv=False)
+    assert any((v.get("op") or {}).get("epilogue") == "qkv_rope" for v in ga.vertices)
+    assert not any((v.get("op") or {}).get("type") == "rope" for v in ga.vertices)
+    inb = inputs_of(gb, seed=9)
+    byname = {gb.tensors[v].name: a for v, a in inb.items()}
+    ina = {t.id: byname[t.name] for t in ga.inputs()}
+    outs = []
+    for g, inp in ((ga, ina), (gb, inb)):
+        mg, _ = W.plan(g, [1 << 30] * 2)
+        (o,) = g.outputs()
+        outs.append(out_values(g, o, oracle_outputs(g, mg, inp)[o]))
+    assert rel_err(outs[0], outs[1]) < 1e-2
+
+
 def _lora_torch_reference(g, inp, cfg, seq, rank_pad=64, rank=16, lora_alpha=16.0):
     """fp32 torch autograd of the same LoRA step (weights from the graph inputs)."""
     import torch

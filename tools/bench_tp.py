@@ -45,6 +45,12 @@ ts = []
 for s in range(a.steps):
     tr = json.loads(ex.run())
     ts.append(tr["makespan"])
+ids = {v["id"]: v for v in json.loads(g.to_json())["vertices"]}
+by_op = {}
+for r_ in tr["rows"]:
+    v = ids.get(r_["vertex"])
+    key = ((v.get("op") or {}).get("type") or v["kind"]) if v else "offload/reload"
+    by_op[key] = by_op.get(key, 0.0) + r_["end"] - r_["start"]
 stt = ex.stats()
 pk = bench.peaks()
 pcie = bench.measure_pcie(torch.device("cuda", 0))
@@ -63,4 +69,5 @@ print(json.dumps({"workload": f"llama_{a.model}_tp{a.tp}_seq{a.seq}_layers{a.lay
                   "exposed_transfer_gpu_s": round(stt["exposed_transfer_gpu_s"], 4), "pcie_h2d_gbs": round(pcie, 1),
                   "roofline": {"compute_s": round(compute_s, 4), "pcie_h2d_s": round(pcie_s, 4),
                                "bound": "pcie" if pcie_s > compute_s else "tensor",
-                               "frac": round(bound / step, 4)}}))
+                               "frac": round(bound / step, 4)},
+                  "device_time_by_op_s": {k: round(v, 4) for k, v in sorted(by_op.items(), key=lambda kv: -kv[1])}}))
