@@ -87,6 +87,7 @@ struct Executor::Impl {
     std::unordered_map<VertexId, HostBuf> inputs;  // taskgraph input id -> pinned bytes
     std::unordered_map<VertexId, HostBuf> staged;  // input id -> HBM staging copy (device residency)
     std::unordered_map<VertexId, HostBuf> slots;   // evicted root id -> pinned slot
+    std::unordered_map<VertexId, char*> zero_copy;  // input id -> device view of its mapped pinned buffer
     std::unordered_map<VertexId, char*> alias;     // Input mem id -> its staging copy (aliased inputs)
     bool aliased_inputs() const { return cfg.inputs_on_device && cfg.alias_device_inputs; }
 
@@ -253,6 +254,34 @@ void Executor::Impl::build() {
         }
     }
 
+    // Zero-copy gather tables (host residency): an input whose only readers
+    // are embedding kernels (as their table) keeps its bytes in mapped pinned
+    // memory sized to its placement; its Input vertices complete at dispatch
+    // and readers resolve to the device view, so only the gathered rows cross
+    // PCIe (seq * dim * 2 bytes instead of the whole vocab table).
+    if (!cfg.inputs_on_device && cfg.zero_copy_gathers) {
+        std::unordered_map<VertexId, int> table_uses, other_uses;
+        for (const auto& [kid, op] : ops)
+            for (size_t k = 0; k < op.args.size(); ++k)
+                (op.type == OpType::Embedding && k == 1 ? table_uses : other_uses)[op.args[k]]++;
+        for (const auto& v : m.vertices) {
+            if (v.op != MemOpKind::Input) continue;
+            const VertexId r = v.origin.ref;
+            if (!table_uses.count(r) || other_uses.count(r)) continue;
+            auto zc = zero_copy.find(r);
+            if (zc == zero_copy.end()) {
+                HostBuf& b = inputs[r];
+                b.bytes = static_cast<std::size_t>(std::max<std::int64_t>(size_of(v.id), 1));
+                TN_CUDA(cudaHostAlloc(&b.p, b.bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+                std::memset(b.p, 0, b.bytes);
+                void* dp = nullptr;
+                TN_CUDA(cudaHostGetDevicePointer(&dp, b.p, 0));
+                zc = zero_copy.emplace(r, static_cast<char*>(dp)).first;
+            }
+            alias[v.id] = zc->second;
+        }
+    }
+
     const size_t V = m.vertices.size();
     prog.resize(V);
     cb.resize(V);
@@ -274,7 +303,7 @@ void Executor::Impl::build() {
                 in.dst = ptr_of(v.id);
                 in.bytes = static_cast<std::size_t>(size_of(v.id));
                 in.input_id = v.origin.ref;
-                in.instant = aliased_inputs();
+                in.instant = aliased_inputs() || zero_copy.count(v.origin.ref) > 0;
                 in.timeless = in.instant && !has_in_edge[v.id];
                 break;
             }
@@ -712,6 +741,10 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
                     break;
                 }
                 case OpType::Embedding:
+                    if (op.args.size() > 1) {
+                        auto zc = zero_copy.find(op.args[1]);
+                        if (zc != zero_copy.end() && a[1] == zc->second) last.zero_copy_bytes += op.seq * op.dim * 2;
+                    }
                     if (op.norm_out)
                         TN_CUDA(k::embedding_norm(a[0], a[1], a[2], in.dst, static_cast<int>(op.seq),
                                                   static_cast<int>(op.dim), static_cast<int>(op.vocab), s));
@@ -1028,7 +1061,9 @@ void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool 
         return;
     }
     HostBuf& b = impl_->inputs[id];
-    if (!b.p || b.bytes != bytes) {
+    if (impl_->zero_copy.count(id)) {  // fixed mapped buffer: kernels hold its device view
+        if (bytes > b.bytes) throw Error("input " + std::to_string(id) + " exceeds its placement");
+    } else if (!b.p || b.bytes != bytes) {
         if (b.p) cudaFreeHost(b.p);
         b.p = pinned_alloc(bytes);
         b.bytes = bytes;
@@ -1078,6 +1113,7 @@ std::string RunStats::to_json() const {
     j["copy_time_s"] = copy_time_s;
     j["exposed_transfer_s"] = exposed_transfer_s;
     j["exposed_transfer_gpu_s"] = exposed_transfer_gpu_s;
+    j["zero_copy_bytes"] = zero_copy_bytes;
     return j.dump();
 }
 
@@ -1097,6 +1133,7 @@ ExecConfig parse_exec_config(const std::string& text) {
         const std::string comp = j.value("completion", std::string("poll"));
         if (comp != "poll" && comp != "callback") throw ParseError("completion must be poll or callback");
         c.poll = comp == "poll";
+        c.zero_copy_gathers = j.value("zero_copy_gathers", c.zero_copy_gathers);
         const std::string res = j.value("input_residency", std::string("host"));
         if (res != "host" && res != "device") throw ParseError("input_residency must be host or device");
         c.inputs_on_device = res == "device";

@@ -29,6 +29,10 @@ struct ExecConfig {
                                       // Input vertex is zero-cost (reference: simulator.cpp:66-67):
                                       // generation-0 readers use the HBM staging copy in place;
                                       // "copy" -> a D2D copy into the placement at dispatch
+    bool zero_copy_gathers = true;    // "zero_copy_gathers": host-resident inputs read only as the
+                                      // table of embedding kernels stay in mapped pinned memory and
+                                      // the kernel gathers its rows over PCIe (the Input vertex
+                                      // copies nothing; a reload of such an input still copies)
 };
 ExecConfig parse_exec_config(const std::string& text);
 
@@ -38,6 +42,7 @@ struct RunStats {
     double flops = 0, makespan_s = 0, wall_s = 0;
     double kernel_time_s = 0, kernel_busy_s = 0, copy_time_s = 0, exposed_transfer_s = 0;
     double exposed_transfer_gpu_s = 0;  // same, per physical GPU (devices sharing a GPU cover each other)
+    std::int64_t zero_copy_bytes = 0;     // bytes kernels read over PCIe from mapped host inputs
     std::string to_json() const;
 };
 

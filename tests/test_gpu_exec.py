@@ -218,6 +218,27 @@ def test_llama_small_parity_with_offloads():
     assert trace["host_bytes_transferred"] > 0
 
 
+def test_zero_copy_gather_tables_bitwise():
+    """With host residency the embedding table (read only by the gather)
+    stays in mapped pinned memory: the Input vertex copies nothing, the kernel
+    reads seq rows over PCIe; outputs are bitwise those of the full H2D copy."""
+    g, mg, _ = small_llama(seq=256, layers=1)
+    inp = inputs_of(g, seed=8)
+    (o,) = g.outputs()
+    res, st = {}, {}
+    for zc in (True, False):
+        with Executor(mg, g.to_json(), {"zero_copy_gathers": zc}) as ex:
+            for vid, a in inp.items():
+                ex.set_input(vid, a)
+            check_trace(mg, json.loads(ex.run()))
+            res[zc] = ex.get_output(o, g.tensors[o].nbytes)
+            st[zc] = ex.stats()
+    assert res[True] == res[False]
+    table = next(t for t in g.inputs() if t.name == "tok_embeddings")
+    assert st[True]["zero_copy_bytes"] == 256 * SMALL.dim * 2 and st[False]["zero_copy_bytes"] == 0
+    assert st[False]["h2d_bytes"] - st[True]["h2d_bytes"] >= table.nbytes
+
+
 def test_llama_fused_norm_parity_with_offloads():
     """The fused-RMSNorm graph option (producers write [x | x*gamma | sum x^2],
     consumers scale rows in the epilogue; no rmsnorm vertices) on the GPU vs
@@ -373,7 +394,11 @@ def test_tight_cap_offload_reload_bytes():
         (o,) = g.outputs()
         got = ex.get_output(o, g.tensors[o].nbytes)
     assert st["d2h_bytes"] + st["d2h_elided_bytes"] == off  # evicted inputs are not copied out again
-    assert st["h2d_bytes"] == rel + sum(t.nbytes for t in g.inputs())
+    # inputs are copied in full, except the embedding table, which stays in mapped
+    # pinned memory and is gathered over PCIe (zero_copy_bytes = seq * dim * 2)
+    table = next(t for t in g.inputs() if t.name == "tok_embeddings")
+    assert st["h2d_bytes"] == rel + sum(t.nbytes for t in g.inputs()) - table.nbytes
+    assert st["zero_copy_bytes"] == 512 * 1024 * 2
     assert trace["host_bytes_transferred"] == off + rel
     want = oracle_outputs(g, mg, inp)
     assert rel_err(out_values(g, o, got), out_values(g, o, want[o])) < 3e-2
