@@ -110,20 +110,73 @@ __global__ void transpose_heads_kernel(const __nv_bfloat16* __restrict__ src, __
     }
 }
 
+// 64x64 tile per CTA (256 threads) with 16-byte accesses on both sides:
+// src[t][col_off + h*hd + d] -> out[h][d][t]. Loads: a thread reads 8
+// consecutive d of one t; stores: 8 consecutive t of one d (gathered from the
+// padded smem tile). Needs hd % 8 == 0, seq % 8 == 0, 16-byte alignment.
+__global__ void __launch_bounds__(256) transpose_heads_vec(const __nv_bfloat16* __restrict__ src,
+                                                           __nv_bfloat16* __restrict__ out, int seq, std::int64_t ld,
+                                                           std::int64_t col_off, int heads, int hd) {
+    __shared__ __nv_bfloat16 tile[64][64 + 8];
+    const int h = blockIdx.z;
+    const int t0 = blockIdx.x * 64, d0 = blockIdx.y * 64;
+    const __nv_bfloat16* base = src + col_off + static_cast<std::int64_t>(h) * hd;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int idx = threadIdx.x + k * 256;  // 512 vectors: 64 rows (t) x 8 vectors (d)
+        const int r = idx / 8, c = (idx % 8) * 8;
+        const int t = t0 + r, d = d0 + c;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (t < seq && d < hd) v = *reinterpret_cast<const uint4*>(base + static_cast<std::int64_t>(t) * ld + d);
+        *reinterpret_cast<uint4*>(&tile[r][c]) = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        // 64 rows (d) x 8 vectors (t); lanes of a warp take consecutive d so the
+        // smem column reads tile[c + j][r] hit consecutive banks
+        const int idx = threadIdx.x + k * 256;
+        const int r = idx % 64, c = (idx / 64) * 8;
+        const int d = d0 + r, t = t0 + c;
+        if (d >= hd || t >= seq) continue;
+        uint4 v;
+        __nv_bfloat16* e = reinterpret_cast<__nv_bfloat16*>(&v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = tile[c + j][r];
+        *reinterpret_cast<uint4*>(out + (static_cast<std::int64_t>(h) * hd + d) * seq + t) = v;
+    }
+}
+
 __global__ void silu_mul_vec(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int rows,
                              int cols) {
     const int nv = cols / 8;
     const std::int64_t total = static_cast<std::int64_t>(rows) * nv;
-    for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
-         w += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-        const std::int64_t r = w / nv, c = w % nv;
+    const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+    // two independent vectors in flight per thread (loads issued before any math)
+    for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total; w += 2 * stride) {
+        const std::int64_t w2 = w + stride;
+        const std::int64_t r = w / nv, c = w % nv, r2 = w2 / nv, c2 = w2 % nv;
         const uint4* row = reinterpret_cast<const uint4*>(gu + r * 2 * cols);
+        const uint4 gv = __ldcs(row + c), uv = __ldcs(row + nv + c);
+        uint4 gv2 = make_uint4(0, 0, 0, 0), uv2 = gv2;
+        if (w2 < total) {
+            const uint4* row2 = reinterpret_cast<const uint4*>(gu + r2 * 2 * cols);
+            gv2 = __ldcs(row2 + c2);
+            uv2 = __ldcs(row2 + nv + c2);
+        }
         float g[8], u[8];
-        unpack8(row[c], g);
-        unpack8(row[nv + c], u);
+        unpack8(gv, g);
+        unpack8(uv, u);
 #pragma unroll
         for (int j = 0; j < 8; ++j) g[j] = g[j] / (1.0f + __expf(-g[j])) * u[j];
         reinterpret_cast<uint4*>(out + r * cols)[c] = pack8(g);
+        if (w2 < total) {
+            unpack8(gv2, g);
+            unpack8(uv2, u);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) g[j] = g[j] / (1.0f + __expf(-g[j])) * u[j];
+            reinterpret_cast<uint4*>(out + r2 * cols)[c2] = pack8(g);
+        }
     }
 }
 
@@ -179,6 +232,36 @@ __global__ void sum_kernel(SumArgs a, int in_dt, void* __restrict__ out, int out
         for (int k = 1; k < a.n; ++k) acc += ld_as_float(a.in[k], i, in_dt);
         if (out_dt == BF16) static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(acc);
         else static_cast<float*>(out)[i] = acc;
+    }
+}
+
+// bf16 (or fp32) inputs, 8 elements per thread with 16-byte loads; each
+// element is still summed over the arguments in argument order.
+__global__ void sum_vec8(SumArgs a, int in_dt, void* __restrict__ out, int out_dt, std::int64_t count8) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count8;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        float acc[8], x[8];
+        auto load8 = [&](const void* p, float* f) {
+            if (in_dt == BF16) {
+                unpack8(static_cast<const uint4*>(p)[i], f);
+            } else {
+                const float4 lo = static_cast<const float4*>(p)[2 * i], hi = static_cast<const float4*>(p)[2 * i + 1];
+                f[0] = lo.x; f[1] = lo.y; f[2] = lo.z; f[3] = lo.w; f[4] = hi.x; f[5] = hi.y; f[6] = hi.z; f[7] = hi.w;
+            }
+        };
+        load8(a.in[0], acc);
+        for (int k = 1; k < a.n; ++k) {
+            load8(a.in[k], x);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += x[j];
+        }
+        if (out_dt == BF16) {
+            static_cast<uint4*>(out)[i] = pack8(acc);
+        } else {
+            float4* o = static_cast<float4*>(out);
+            o[2 * i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            o[2 * i + 1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        }
     }
 }
 
@@ -258,6 +341,16 @@ __global__ void cast_kernel(const void* __restrict__ in, int in_dt, void* __rest
     }
 }
 
+// f32 -> bf16, 8 elements per thread (two 16-byte loads, one 16-byte store).
+__global__ void cast_f32_bf16_vec(const float4* __restrict__ in, uint4* __restrict__ out, std::int64_t count8) {
+    for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count8;
+         i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const float4 lo = __ldcs(in + 2 * i), hi = __ldcs(in + 2 * i + 1);
+        const float f[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        out[i] = pack8(f);
+    }
+}
+
 bool al16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -280,6 +373,12 @@ cudaError_t rope(const void* src, const void* table, void* out, int seq, std::in
 
 cudaError_t transpose_heads(const void* src, void* out, int seq, std::int64_t ld, std::int64_t col_off, int heads,
                             int hd, cudaStream_t s) {
+    if (hd % 8 == 0 && seq % 8 == 0 && ld % 8 == 0 && col_off % 8 == 0 && al16(src) && al16(out)) {
+        dim3 grid((seq + 63) / 64, (hd + 63) / 64, heads);
+        transpose_heads_vec<<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src),
+                                                 static_cast<__nv_bfloat16*>(out), seq, ld, col_off, heads, hd);
+        return cudaGetLastError();
+    }
     dim3 grid((seq + 31) / 32, (hd + 31) / 32, heads), block(32, 8);
     transpose_heads_kernel<<<grid, block, 0, s>>>(static_cast<const __nv_bfloat16*>(src),
                                                   static_cast<__nv_bfloat16*>(out), seq, ld, col_off, heads, hd);
@@ -308,6 +407,8 @@ cudaError_t sum_n(const void* const* ins, int n, int in_dtype, void* out, int ou
     }
     if (in_dtype == F32 && out_dtype == F32 && count % 4 == 0 && aligned)
         sum_f32_vec<<<grid_for(count / 4), kThreads, 0, s>>>(a, static_cast<float*>(out), count / 4);
+    else if (count % 8 == 0 && aligned)
+        sum_vec8<<<grid_for(count / 8), kThreads, 0, s>>>(a, in_dtype, out, out_dtype, count / 8);
     else
         sum_kernel<<<grid_for(count), kThreads, 0, s>>>(a, in_dtype, out, out_dtype, count);
     return cudaGetLastError();
@@ -346,6 +447,11 @@ cudaError_t embedding(const void* tokens, const void* table, void* out, int seq,
 }
 
 cudaError_t cast(const void* in, int in_dtype, void* out, int out_dtype, std::int64_t count, cudaStream_t s) {
+    if (in_dtype == F32 && out_dtype == BF16 && count % 8 == 0 && al16(in) && al16(out)) {
+        cast_f32_bf16_vec<<<grid_for(count / 8), kThreads, 0, s>>>(static_cast<const float4*>(in),
+                                                                   static_cast<uint4*>(out), count / 8);
+        return cudaGetLastError();
+    }
     cast_kernel<<<grid_for(count), kThreads, 0, s>>>(in, in_dtype, out, out_dtype, count);
     return cudaGetLastError();
 }
