@@ -1,13 +1,16 @@
 """Summarises an ncu --metrics gpu__time_duration.sum launch list (CSV).
 
     python tools/launches.py launches.csv [--last N] [--dump out.csv]
---last N keeps only the last N tn:: launches (e.g. one step); --dump writes
+--last N keeps only the last N tn:: launches (e.g. one step), --first I --count N
+a window (bench.py runs value steps, then arena-copy steps, then e2e steps); --dump writes
 those rows (tn:: kernels only) as a compact CSV for profiles/."""
 import argparse, collections, csv, re
 
 ap = argparse.ArgumentParser()
 ap.add_argument("csv")
 ap.add_argument("--last", type=int, default=0)
+ap.add_argument("--first", type=int, default=-1, help="start index (tn:: launches) of the window, instead of --last")
+ap.add_argument("--count", type=int, default=0)
 ap.add_argument("--dump", default=None)
 a = ap.parse_args()
 rows = list(csv.reader(open(a.csv)))
@@ -17,7 +20,9 @@ for i, r in enumerate(rows):
         break
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
 ours = [r for r in rows[start:] if len(r) > vi and r[ki].startswith(("tn::", "void tn::"))]
-if a.last:
+if a.first >= 0:
+    ours = ours[a.first:a.first + a.count]
+elif a.last:
     ours = ours[-a.last:]  # torch kernels of the input generator run before the step
 if a.dump:
     with open(a.dump, "w", newline="") as f:
