@@ -1,0 +1,35 @@
+"""bench.py helpers that do not need a GPU: the roofline bookkeeping over a
+trace, and the reference arm's live planner leg (oracle/_ref)."""
+import json
+import os
+
+import pytest
+
+import bench
+from paper_2405_16283_b200 import workloads as W
+
+
+def test_roofline_from_trace_counts_gemm_flops_and_bytes():
+    cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=1024, vocab=1000)
+    g = W.llama_prefill(cfg, 256)
+    rows = [{"vertex": v["id"], "start": 0.0, "end": 1e-3} for v in g.vertices]
+    roof, by_type = bench.roofline_from_trace(g, {"rows": rows}, 1000.0)
+    gemms = [v for v in g.vertices if (v.get("op") or {}).get("type") == "gemm"]
+    assert roof["launches_per_step"] == len(gemms)
+    assert roof["algorithmic_flops_per_step"] == pytest.approx(sum(bench.gemm_flops(v["op"]) for v in gemms))
+    assert roof["unit"] == "TFLOP/s" and roof["bound"] == "tensor"
+    assert sum(c["n"] for c in roof["gemm_classes"].values()) == len(gemms)
+    assert roof["algorithmic_bytes_per_launch"] > 0
+    assert by_type["gemm"] == pytest.approx(1e-3 * len(gemms))
+
+
+def test_reference_planner_leg_is_byte_identical():
+    if not os.path.isdir(os.path.join(bench.ROOT, "oracle", "_ref")):
+        pytest.skip("oracle/_ref not built")
+    cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=1024, vocab=1000)
+    g = W.llama_prefill(cfg, 256)
+    leg = bench.reference_planner_leg(g, 64 << 20, "greedy")
+    if "unavailable" in leg:
+        pytest.skip(leg["unavailable"])
+    assert leg["memgraph_bytes_identical"] and leg["simulate_trace_identical"]
+    assert leg["vertices"] == len(json.loads(W.plan(g, 64 << 20)[0])["vertices"])
