@@ -232,8 +232,10 @@ def roofline_from_trace(g, trace, peak_tflops):
     alg_bytes = sum(gemm_bytes(g, ids[r["vertex"]]) for r in trace["rows"]
                     if r["vertex"] in ids and (ids[r["vertex"]].get("op") or {}).get("type") == "gemm")
     traffic, src = gemm_traffic()
+    burst = peaks().get("bf16_tflops")
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
-            "frac": round(ach / peak_tflops, 4), "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
+            "frac": round(ach / peak_tflops, 4), "peak_kind": "sustained (MEASURED_PEAKS bf16_tflops_sustained)",
+            "frac_of_burst_peak": round(ach / burst, 4) if burst else None, "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
             "traffic_source": src, "algorithmic_bytes_per_launch": round(alg_bytes / max(1, launches)),
             "kernel": "gemm_tcgen05 (all GEMM tasks)",
             "launches_per_step": launches, "algorithmic_flops_per_step": fl,
