@@ -75,7 +75,35 @@ def cast(g):
     return outs, S * d * 6
 
 
-for name, b in (("rope q (7B)", rope), ("transpose_heads v (7B)", vt), ("silu_mul (7B)", silu),
+def rmsnorm(g):
+    x = g.input("x", (S, d), "bf16", init=("normal", 1.0))
+    w = g.input("w", (d,), "bf16", init=("normal", 1.0))
+    outs = [g.kernel(f"n{i}", {"type": "rmsnorm", "args": [x, w], "rows": S, "cols": d, "eps": 1e-5}, (S, d), "bf16")
+            for i in range(R)]
+    return outs, 2 * S * d * 2
+
+
+def softmax_causal(g):  # fp32 scores of 8 heads x 2048 x 2048 -> bf16 probabilities (unfused attention path)
+    B, T = 8, 2048
+    sc = g.input("s", (B, T, T), "f32", init=("normal", 1.0))
+    outs = [g.kernel(f"sm{i}", {"type": "softmax", "args": [sc], "batch": B, "rows": T, "cols": T, "scale": 0.088,
+                                "causal": 1}, (B, T, T), "bf16") for i in range(R)]
+    return outs, B * T * T * (4 + 2) // 2 + B * T * T * 2 // 2  # read the lower triangle, write P (zeros above)
+
+
+def tile_softmax(g):  # config-5 score tile 4096 x 4096 bf16: rowstats, then softmax_apply
+    T = 4096
+    st = g.input("S", (T, T), "bf16", init=("normal", 1.0))
+    ml = g.input("ml", (T, 2), "f32", init=("normal", 1.0))
+    outs = [g.kernel(f"rs{i}", {"type": "rowstats", "args": [st], "rows": T, "cols": T, "causal": 0}, (T, 2), "f32")
+            for i in range(R)]
+    outs += [g.kernel(f"sa{i}", {"type": "softmax_apply", "args": [st, ml], "rows": T, "cols": T, "causal": 0},
+                      (T, T), "bf16") for i in range(R)]
+    return outs, T * T * 2 * 3 // 2  # mean of rowstats (read) and softmax_apply (read + write)
+
+
+for name, b in (("rmsnorm (7B)", rmsnorm), ("softmax causal fp32->bf16", softmax_causal),
+                ("rowstats + softmax_apply (4096^2 tile)", tile_softmax), ("rope q (7B)", rope), ("transpose_heads v (7B)", vt), ("silu_mul (7B)", silu),
                 ("sum of 8 partials + residual (65B TP8 block)", sum8), ("concat 8 blocks (65B TP8)", concat8),
                 ("cast f32->bf16", cast)):
     run(name, b)
