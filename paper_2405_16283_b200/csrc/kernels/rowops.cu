@@ -278,6 +278,43 @@ __global__ void __launch_bounds__(kRowThreads) rowstats_kernel(const __nv_bfloat
     if (threadIdx.x == 0) st[r] = make_float2(mx, sum);
 }
 
+// Single pass: the row segment stays in registers between the max and the
+// sum (cols % 8 == 0, 16-byte aligned, cols <= kRowThreads * 8 * kMaxVec).
+template <int kMaxVec>
+__global__ void __launch_bounds__(kRowThreads) rowstats_vec(const __nv_bfloat16* __restrict__ S,
+                                                            float2* __restrict__ st, int cols, int causal) {
+    __shared__ float red[kRowThreads / 32];
+    const std::int64_t r = blockIdx.x;
+    const int valid = causal ? min(cols, static_cast<int>(r) + 1) : cols;
+    const uint4* s = reinterpret_cast<const uint4*>(S + r * cols);
+    constexpr float L2E = 1.4426950408889634f;
+    float v[kMaxVec][8];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+        const int c = (threadIdx.x + i * kRowThreads) * 8;
+        if (c < valid) {
+            unpack8(__ldcs(s + c / 8), v[i]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c + j < valid) mx = fmaxf(mx, v[i][j]);
+        }
+    }
+    mx = block_reduce<true>(mx, red);
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i) {
+        const int c = (threadIdx.x + i * kRowThreads) * 8;
+        if (c < valid) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c + j < valid) sum += exp2f((v[i][j] - mx) * L2E);
+        }
+    }
+    sum = block_reduce<false>(sum, red);
+    if (threadIdx.x == 0) st[r] = make_float2(mx, sum);
+}
+
 constexpr int kMaxParts = 64;
 struct Parts {
     const float2* p[kMaxParts];
@@ -375,8 +412,14 @@ cudaError_t softmax(const void* S, void* P, int batch, int rows, int cols, float
 
 cudaError_t rowstats(const void* S, void* st, int rows, int cols, int causal, cudaStream_t s) {
     if (rows <= 0) return cudaSuccess;
-    rowstats_kernel<<<rows, kRowThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(S), static_cast<float2*>(st), cols,
-                                                 causal);
+    auto Sp = static_cast<const __nv_bfloat16*>(S);
+    auto Tp = static_cast<float2*>(st);
+    if (cols % 8 == 0 && al16(S) && cols <= kRowThreads * 8 * 4) {
+        if (cols <= kRowThreads * 8 * 2) rowstats_vec<2><<<rows, kRowThreads, 0, s>>>(Sp, Tp, cols, causal);
+        else rowstats_vec<4><<<rows, kRowThreads, 0, s>>>(Sp, Tp, cols, causal);
+        return cudaGetLastError();
+    }
+    rowstats_kernel<<<rows, kRowThreads, 0, s>>>(Sp, Tp, cols, causal);
     return cudaGetLastError();
 }
 
