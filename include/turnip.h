@@ -93,8 +93,17 @@ int tn_make_fixed_order(const char* memgraph_json, char** memgraph_out, char** e
  * taskgraph_json: the taskgraph the memgraph was built from, whose vertices
  *   carry an extra "op" payload (ignored by the reference parser,
  *   taskgraph.cpp:375-389) naming the kernel and its argument producers.
- * config_json: {"devices":[cuda ordinals], "streams_per_device":5,
- *   "compute_tokens":1, "materialize_inputs":true, ...} (all optional). */
+ * config_json (all keys optional, defaults shown):
+ *   "devices": [0, 1, ...]          memgraph device d -> CUDA ordinal (default d % #GPUs)
+ *   "streams_per_device": 5         simulator.hpp:23
+ *   "compute_tokens": 1             kernels running at once per device (reference: 1)
+ *   "lookahead": 1                  kernels queued behind the running kernel (0 = exact contract)
+ *   "completion": "poll"            "poll" (cudaEventQuery) | "callback" (cudaLaunchHostFunc)
+ *   "input_residency": "host"       "host" (pinned pool, H2D at dispatch) | "device" (HBM staging)
+ *   "device_inputs": "alias"        with device residency: "alias" (read in place) | "copy" (D2D)
+ *   "zero_copy_gathers": true       host inputs read only by embedding gathers stay in mapped memory
+ *   "elide_input_offloads": true    an evicted input is reloaded from its own copy, never offloaded
+ *   "materialize_inputs": true, "timeout_s": 600 */
 int tn_exec_create(const char* memgraph_json, const char* taskgraph_json, const char* config_json,
                    tn_exec** out, char** err);
 
