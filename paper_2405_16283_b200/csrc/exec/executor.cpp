@@ -81,7 +81,10 @@ struct Executor::Impl {
                                         // lookahead chain is plain stream order (no cross-stream event wait)
     std::vector<std::vector<k::GemmWorkspace>> gws;  // per device x stream: stream-K GEMM scratch
     std::vector<cudaEvent_t> t0;    // per logical device
-    std::vector<cudaEvent_t> ev_start, ev_end;  // per memgraph vertex index
+    std::vector<cudaEvent_t> ev_start, ev_end;  // per memgraph vertex index (timing events)
+    std::vector<cudaEvent_t> ev_done;           // timing-free completion events (untimed runs)
+    bool timed = true;                          // this run records ev_start / ev_end
+    cudaEvent_t done_event(std::int32_t v) const { return timed ? ev_end[v] : ev_done[v]; }
 
     // --- host pool ---------------------------------------------------------------
     std::unordered_map<VertexId, HostBuf> inputs;  // taskgraph input id -> pinned bytes
@@ -287,6 +290,7 @@ void Executor::Impl::build() {
     cb.resize(V);
     ev_start.resize(V);
     ev_end.resize(V);
+    ev_done.resize(V);
     for (size_t i = 0; i < V; ++i) {
         const MemVertex& v = m.vertices[i];
         Instr& in = prog[i];
@@ -297,6 +301,7 @@ void Executor::Impl::build() {
         set_device(v.device);
         TN_CUDA(cudaEventCreate(&ev_start[i]));
         TN_CUDA(cudaEventCreate(&ev_end[i]));
+        TN_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
         const auto& din = data_in[v.id];
         switch (v.op) {
             case MemOpKind::Input: {
@@ -631,8 +636,8 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
                                   : streams[in.dev][stream < 0 ? 0 : stream];  // inputs hold no stream when not materialised
     // lookahead: run behind `after` (same stream when both are on the compute stream)
     if (after >= 0 && !(on_compute && prog[after].op == MemOpKind::Kernel && prog[after].dev == in.dev))
-        TN_CUDA(cudaStreamWaitEvent(s, ev_end[after], 0));
-    TN_CUDA(cudaEventRecord(ev_start[vidx], s));
+        TN_CUDA(cudaStreamWaitEvent(s, done_event(after), 0));
+    if (timed) TN_CUDA(cudaEventRecord(ev_start[vidx], s));
     switch (in.op) {
         case MemOpKind::Input: {
             if (in.instant) break;  // readers use the staging copy in place
@@ -687,6 +692,10 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
         case MemOpKind::Kernel: {
             const OpDesc& op = *in.op_desc;
             const auto& a = in.argp;
+            struct PdlScope {  // PDL for this launch only (untimed runs, compute stream)
+                explicit PdlScope(bool on) { k::set_pdl(on); }
+                ~PdlScope() { k::set_pdl(false); }
+            } pdl_scope(!timed && cfg.pdl && on_compute);
             switch (op.type) {
                 case OpType::Gemm:
                     TN_CUDA(k::gemm_launch(*in.gemm, s, &gws[in.dev][stream < 0 ? 0 : stream]));
@@ -782,7 +791,7 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
             break;
         }
     }
-    TN_CUDA(cudaEventRecord(ev_end[vidx], s));
+    TN_CUDA(cudaEventRecord(done_event(vidx), s));
     if (!cfg.poll) TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
 }
 
@@ -841,7 +850,7 @@ class CudaBackend {
                 const std::int32_t v = flying_[i];
                 const int dev = x_.prog[v].dev;
                 if (x_.ordinal[dev] != x_.cur_dev) x_.set_device(dev);
-                cudaError_t e = cudaEventQuery(x_.ev_end[v]);
+                cudaError_t e = cudaEventQuery(x_.done_event(v));
                 if (e == cudaErrorNotReady) continue;
                 if (e != cudaSuccess) throw CudaError(std::string("vertex failed on the device: ") + cudaGetErrorString(e));
                 flying_.erase(flying_.begin() + static_cast<std::ptrdiff_t>(i));
@@ -873,6 +882,7 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
         g = &fixed;
     }
     last = RunStats{};
+    timed = trace != nullptr || cfg.all_timestamps;
     dispatched.clear();
     dispatched.reserve(g->vertices.size());
     stream_of.assign(g->vertices.size(), -1);
@@ -914,6 +924,9 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
 // Trace of the most recent run from its device timestamps (seconds since the
 // device's t0 event), plus the derived timing stats.
 ExecutionTrace Executor::Impl::build_trace() {
+    if (!timed)
+        throw Error("the last run recorded no timestamps (untimed run): run with a trace or config "
+                    "\"timestamps\": \"all\"");
     const MemGraph* g = last_graph ? last_graph.get() : &m;
     ExecutionTrace t;
     t.rows.reserve(dispatched.size());
@@ -991,6 +1004,7 @@ Executor::Impl::~Impl() {
     for (size_t i = 0; i < ev_start.size(); ++i) {
         if (ev_start[i]) cudaEventDestroy(ev_start[i]);
         if (ev_end[i]) cudaEventDestroy(ev_end[i]);
+        if (ev_done[i]) cudaEventDestroy(ev_done[i]);
     }
     for (int d = 0; d < static_cast<int>(t0.size()); ++d) {
         bool owner = true;
@@ -1134,6 +1148,10 @@ ExecConfig parse_exec_config(const std::string& text) {
         if (comp != "poll" && comp != "callback") throw ParseError("completion must be poll or callback");
         c.poll = comp == "poll";
         c.zero_copy_gathers = j.value("zero_copy_gathers", c.zero_copy_gathers);
+        c.pdl = j.value("pdl", c.pdl);
+        const std::string ts = j.value("timestamps", std::string("traced"));
+        if (ts != "traced" && ts != "all") throw ParseError("timestamps must be traced or all");
+        c.all_timestamps = ts == "all";
         const std::string res = j.value("input_residency", std::string("host"));
         if (res != "host" && res != "device") throw ParseError("input_residency must be host or device");
         c.inputs_on_device = res == "device";

@@ -29,6 +29,13 @@ struct ExecConfig {
                                       // Input vertex is zero-cost (reference: simulator.cpp:66-67):
                                       // generation-0 readers use the HBM staging copy in place;
                                       // "copy" -> a D2D copy into the placement at dispatch
+    bool all_timestamps = false;      // "timestamps": "traced" -> runs without a trace use timing-free
+                                      // completion events and programmatic dependent launch (a
+                                      // timing event between two kernels costs ~3 us and blocks PDL);
+                                      // "all" -> every run records per-vertex timestamps
+    bool pdl = false;                 // "pdl": programmatic dependent launch in untimed runs (no
+                                      // measurable gain on the 7B step: the persistent kernels hold
+                                      // every SM until they exit; tools/diag_run_overhead.py)
     bool zero_copy_gathers = true;    // "zero_copy_gathers": host-resident inputs read only as the
                                       // table of embedding kernels stay in mapped pinned memory and
                                       // the kernel gathers its rows over PCIe (the Input vertex

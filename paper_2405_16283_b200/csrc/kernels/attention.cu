@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         s_full = b0 + 72, s_free = b0 + 80, p_full = b0 + 88, o_done = b0 + 96;
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 13);
 
+    pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int h = blockIdx.x % p.heads;
     const int qb = p.nblk - 1 - static_cast<int>(blockIdx.x / p.heads);  // heavy blocks first
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();  // the previous kernel's outputs (q, k, vT) are complete and visible
     const std::uint32_t tmem = *tmem_slot;
     const std::uint32_t tS = tmem, tP = tmem + 64, tO = tmem + 128;
 
@@ -390,10 +392,8 @@ cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s) {
     static const char* emu_env = std::getenv("TN_ATTN_EMU");  // A/B: "0" keeps every 2^x on MUFU
     const unsigned grid = p.heads * p.nblk;
     if (emu_env && std::atoi(emu_env) == 0)
-        attention_kernel<0><<<grid, kThreads, kSmem, s>>>(plan.tq, plan.tk, plan.tv, p);
-    else
-        attention_kernel<1><<<grid, kThreads, kSmem, s>>>(plan.tq, plan.tk, plan.tv, p);
-    return cudaGetLastError();
+        return launch_pdl(attention_kernel<0>, dim3(grid), dim3(kThreads), kSmem, s, plan.tq, plan.tk, plan.tv, p);
+    return launch_pdl(attention_kernel<1>, dim3(grid), dim3(kThreads), kSmem, s, plan.tq, plan.tk, plan.tv, p);
 }
 
 double attention_flops(const AttnArgs& a) {

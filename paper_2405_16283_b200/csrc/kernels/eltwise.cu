@@ -8,8 +8,16 @@
 #include <cstdint>
 
 #include "kernels.hpp"
+#include "tc_common.cuh"
 
 namespace tn::k {
+
+namespace {
+thread_local bool g_pdl = false;
+}
+void set_pdl(bool on) { g_pdl = on; }
+bool pdl_enabled() { return g_pdl; }
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -283,6 +291,8 @@ __global__ void sum_f32_vec(SumArgs a, float* __restrict__ out, std::int64_t cou
 
 __global__ void embedding_kernel(const int* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
                                  __nv_bfloat16* __restrict__ out, int dim, int vocab, int vec) {
+    pdl_trigger();
+    pdl_wait();
     const int t = blockIdx.x;
     int id = tok[t];
     id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
@@ -441,8 +451,8 @@ cudaError_t embedding_norm(const void* tokens, const void* table, const void* g,
 
 cudaError_t embedding(const void* tokens, const void* table, void* out, int seq, int dim, int vocab, cudaStream_t s) {
     int vec = dim % 8 == 0 && al16(table) && al16(out);
-    embedding_kernel<<<seq, 128, 0, s>>>(static_cast<const int*>(tokens), static_cast<const __nv_bfloat16*>(table),
-                                        static_cast<__nv_bfloat16*>(out), dim, vocab, vec);
+    return launch_pdl(embedding_kernel, dim3(seq), dim3(128), 0, s, static_cast<const int*>(tokens),
+                      static_cast<const __nv_bfloat16*>(table), static_cast<__nv_bfloat16*>(out), dim, vocab, vec);
     return cudaGetLastError();
 }
 

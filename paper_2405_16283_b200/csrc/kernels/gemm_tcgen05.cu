@@ -455,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const std::uint32_t tfull = empty + 8 * kStages, tempty = tfull + 16;
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 4);
 
+    pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int bk = kAtom / p.in_bytes;
     const bool tf32 = p.in_bytes == 4;
@@ -482,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();  // previous kernel complete: its outputs are visible, its inputs may be overwritten
     const std::uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
@@ -732,6 +734,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const std::uint32_t tfull = empty + 8 * kStages2, tempty = tfull + 16;
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages2 + 4);
 
+    pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const std::uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
@@ -765,6 +768,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
+    pdl_wait();  // previous kernel complete: its outputs are visible, its inputs may be overwritten
     const std::uint32_t tmem = *tmem_slot;
     const std::uint32_t full_leader0 = mapa(full, 0);
     const std::uint32_t tempty_leader0 = mapa(tempty, 0);
@@ -991,6 +995,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     const std::uint32_t tfull = empty + 8 * kStagesW, tempty = tfull + 8;  // tempty[2]
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStagesW + 3);
 
+    pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const std::uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
@@ -1043,6 +1048,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
+    pdl_wait();  // previous kernel complete: its outputs are visible, its inputs may be overwritten
     const std::uint32_t tmem = *tmem_slot;
     const std::uint32_t full_leader0 = mapa(full, 0);
     const std::uint32_t tempty_leader0 = mapa(tempty, 0);
@@ -1169,6 +1175,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
 // --- SIMT fallback: one warp per output element, fp32 accumulate in K order.
 // Used for tiny M (GEMV-like last-token heads) or shapes TMA cannot describe.
 __global__ void gemm_simt_kernel(GemmArgs a) {
+    pdl_trigger();
+    pdl_wait();
     const std::int64_t gw = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
     const int lane = threadIdx.x % 32;
     const int Nout = a.epi == 1 ? a.N / 2 : a.N;
@@ -1443,8 +1451,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
         const std::int64_t warps = static_cast<std::int64_t>(a.batch) * a.M * (a.epi == 1 ? a.N / 2 : a.N);
         const int threads = 256;
         const std::int64_t blocks = (warps * 32 + threads - 1) / threads;
-        gemm_simt_kernel<<<static_cast<unsigned>(blocks), threads, 0, s>>>(a);
-        return cudaGetLastError();
+        return launch_pdl(gemm_simt_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0, s, a);
     }
     Params p;
     p.C = a.C;
@@ -1495,16 +1502,16 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
         p.epoch = ws->epoch;
     }
     if (plan.path == 3)
-        gemm_kernel_2sm_w<<<plan.grid, kThreadsW, smem_bytes_2sm_w(), s>>>(plan.ta, plan.tb, plan.tbh, plan.tbq, plan.tc, p);
-    else if (plan.path == 2)
-        gemm_kernel_2sm<<<plan.grid, kThreads, smem_bytes_2sm(), s>>>(plan.ta, plan.tb, plan.tbh, plan.tbq, plan.tc, p);
-    else if (plan.bn == 128)
-        gemm_kernel<128><<<plan.grid, kThreads, smem_bytes<128>(), s>>>(plan.ta, plan.tb, p);
-    else if (plan.bn == 64)
-        gemm_kernel<64><<<plan.grid, kThreads, smem_bytes<64>(), s>>>(plan.ta, plan.tb, p);
-    else
-        gemm_kernel<256><<<plan.grid, kThreads, smem_bytes<256>(), s>>>(plan.ta, plan.tb, p);
-    return cudaGetLastError();
+        return launch_pdl(gemm_kernel_2sm_w, dim3(plan.grid), dim3(kThreadsW), smem_bytes_2sm_w(), s, plan.ta, plan.tb,
+                          plan.tbh, plan.tbq, plan.tc, p);
+    if (plan.path == 2)
+        return launch_pdl(gemm_kernel_2sm, dim3(plan.grid), dim3(kThreads), smem_bytes_2sm(), s, plan.ta, plan.tb,
+                          plan.tbh, plan.tbq, plan.tc, p);
+    if (plan.bn == 128)
+        return launch_pdl(gemm_kernel<128>, dim3(plan.grid), dim3(kThreads), smem_bytes<128>(), s, plan.ta, plan.tb, p);
+    if (plan.bn == 64)
+        return launch_pdl(gemm_kernel<64>, dim3(plan.grid), dim3(kThreads), smem_bytes<64>(), s, plan.ta, plan.tb, p);
+    return launch_pdl(gemm_kernel<256>, dim3(plan.grid), dim3(kThreads), smem_bytes<256>(), s, plan.ta, plan.tb, p);
 }
 
 }  // namespace tn::k

@@ -13,6 +13,13 @@ namespace tn::k {
 
 enum DType : int { BF16 = 0, F32 = 1, I32 = 2 };
 
+// Programmatic dependent launch for the next kernel launches of this host
+// thread (the executor's dispatcher): the kernel may be scheduled while the
+// previous kernel on its stream drains; every PDL-aware kernel calls
+// griddepcontrol.wait before its first global-memory access.
+void set_pdl(bool on);
+bool pdl_enabled();
+
 inline int dtype_size(int dt) { return dt == BF16 ? 2 : 4; }
 
 // C[b][m][n] = alpha * sum_k A[b][m][k] * B[b][n][k] (+ R[b][m][n])

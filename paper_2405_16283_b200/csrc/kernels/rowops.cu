@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "kernels.hpp"
+#include "tc_common.cuh"
 
 namespace tn::k {
 namespace {
@@ -106,6 +107,8 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_persist(const __nv_bfloat
             dst[i] = c < nv ? xr[c] : make_uint4(0, 0, 0, 0);
         }
     };
+    pdl_trigger();
+    pdl_wait();
     std::int64_t row = blockIdx.x;
     if (row >= rows) return;
     load(row, cur);
@@ -382,8 +385,8 @@ cudaError_t rmsnorm(const void* x, const void* w, void* y, int rows, int cols, f
         static const char* cps_env = std::getenv("TN_RMSNORM_CPS");  // tuning: CTAs per SM
         const int cps = cps_env ? std::atoi(cps_env) : 4;
         const int grid = std::min(rows, sms * cps);
-        if (cols <= kRowThreads * 8 * 2) rmsnorm_persist<2><<<grid, kRowThreads, 0, s>>>(X, W, Y, rows, cols, eps);
-        else rmsnorm_persist<4><<<grid, kRowThreads, 0, s>>>(X, W, Y, rows, cols, eps);
+        if (cols <= kRowThreads * 8 * 2) return launch_pdl(rmsnorm_persist<2>, dim3(grid), dim3(kRowThreads), 0, s, X, W, Y, rows, cols, eps);
+        return launch_pdl(rmsnorm_persist<4>, dim3(grid), dim3(kRowThreads), 0, s, X, W, Y, rows, cols, eps);
     } else if (cols % 8 == 0 && al16(x) && al16(w) && al16(y) && cols <= kRowThreads * 8 * 8) {
         if (cols <= kRowThreads * 8 * 2) rmsnorm_vec<2><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);
         else if (cols <= kRowThreads * 8 * 4) rmsnorm_vec<4><<<rows, kRowThreads, 0, s>>>(X, W, Y, cols, eps);

@@ -4,10 +4,21 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
+#include "kernels.hpp"
+
 namespace tn::k {
+
+// PDL: let the next kernel on the stream launch once every CTA of this one
+// has started (pdl_trigger at entry), and wait for the previous kernel's
+// completion + memory visibility before touching global memory (pdl_wait).
+// Both are no-ops when the launch carries no PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -170,6 +181,23 @@ __device__ __forceinline__ void tmem_free(std::uint32_t taddr, std::uint32_t col
 __host__ __device__ constexpr std::uint32_t make_idesc(std::uint32_t fmt, int M, int N) {
     return (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<std::uint32_t>(N >> 3) << 17) |
            (static_cast<std::uint32_t>(M >> 4) << 24);
+}
+
+// Kernel launch with the PDL attribute when the dispatcher enabled it.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 }  // namespace tn::k

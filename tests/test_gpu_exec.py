@@ -14,6 +14,8 @@ import json
 import numpy as np
 import pytest
 
+from paper_2405_16283_b200.memplan import MemplanError
+
 from helpers import SMALL, inputs_of, oracle_outputs, out_values, rel_err, replay_capacity, small_llama
 from paper_2405_16283_b200 import workloads as W
 from paper_2405_16283_b200.executor import Executor, execute
@@ -216,6 +218,25 @@ def test_llama_small_parity_with_offloads():
     (o,) = g.outputs()
     assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 3e-2
     assert trace["host_bytes_transferred"] > 0
+
+
+def test_untimed_runs_with_pdl_are_bitwise_equal_to_traced_runs():
+    """Untimed runs (timing-free completion events, programmatic dependent
+    launch between consecutive kernels) give the bytes of traced runs."""
+    g, mg, _ = small_llama(seq=256, layers=2)
+    inp = inputs_of(g, seed=12)
+    (o,) = g.outputs()
+    n = g.tensors[o].nbytes
+    for cfg in ({"input_residency": "device"}, {"input_residency": "device", "pdl": True}, {"pdl": True}):
+        with Executor(mg, g.to_json(), cfg) as ex:
+            for vid, a in inp.items():
+                ex.set_input(vid, a)
+            traced = [ex.run() and ex.get_output(o, n) for _ in range(2)]
+            fast = []
+            for _ in range(4):
+                ex.run(trace=False)
+                fast.append(ex.get_output(o, n))
+        assert all(x == traced[0] for x in traced + fast)
 
 
 def test_zero_copy_gather_tables_bitwise():
@@ -606,5 +627,8 @@ def test_executor_reuse_many_runs_and_inputs_update():
                 ex.set_input(vid, arr)
             ex.run(trace=False)
             outs.append(ex.get_output(c, 256 * 256 * 2))
+        with pytest.raises(MemplanError, match="no timestamps"):
+            ex.last_trace()  # untimed runs record timing-free events only
+        ex.run()
         assert json.loads(ex.last_trace())["rows"]
     assert outs[0] == outs[2] and outs[0] != outs[1]
