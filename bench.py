@@ -48,6 +48,8 @@ class Clocks:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
+    PERIOD_MS = 100
+
     def __init__(self, index: int):
         self.index = index
         self.proc = None
@@ -56,7 +58,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -386,14 +388,15 @@ def run_ours(args, world, rank, local):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         for _ in range(args.steps):
-            exv.run(trace=False)  # per-vertex CUDA events are recorded; no host trace work in the loop
+            exv.run(trace=False)  # timing-free completion events, no host trace work in the loop
         e.record()
+        # one more step, back to back with the timed ones (same power/clock state; an idle gap
+        # first would let the GPU boost), with per-vertex timestamps for the roofline and the
+        # per-op breakdown — not part of the timed region
+        last = json.loads(exv.run())
         torch.cuda.synchronize()
     barrier(world)
     t_value = max_over_ranks(s.elapsed_time(e) * 1e-3, world)
-    # one more (untimed-by-us) step with per-vertex timestamps for the roofline and the
-    # per-op breakdown: timed runs record timing-free completion events and use PDL
-    last = json.loads(exv.run())
     st_v = exv.stats()
     makespans.append(last["makespan"])
     exv.close()
