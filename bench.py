@@ -196,6 +196,23 @@ def measure_pcie(device) -> float:
     return best
 
 
+def untimed_steps(ex, steps: int, policy: str = "event-driven", tie_break: str = "fifo") -> list[float]:
+    """Per-step device time (s) of `steps` untimed executor runs (timing-free
+    completion events), each bracketed by CUDA events on the current stream;
+    run back to back so the GPU stays in its sustained power state."""
+    import torch
+
+    out = []
+    for i in range(steps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        ex.run(policy, tie_break, i, trace=False)
+        e.record()
+        torch.cuda.synchronize()
+        out.append(s.elapsed_time(e) * 1e-3)
+    return out
+
+
 # ----------------------------------------------------------------- roofline ---
 def gemm_flops(op) -> float:
     f = 2.0 * op["M"] * op["N"] * op["K"] * op.get("batch", 1)
