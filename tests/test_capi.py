@@ -41,3 +41,21 @@ def test_executor_without_gpu_fails_loudly():
     with pytest.raises(memplan.MemplanError) as e:
         Executor(mg, g.to_json())
     assert e.value.code == 3
+
+
+def test_executor_config_keys_are_validated_before_any_cuda_call():
+    """Bad executor configuration is a usage error (code 2) with the key named,
+    raised before the CUDA runtime is touched (so it reproduces on CPU)."""
+    import pytest
+    from paper_2405_16283_b200 import memplan, workloads as W
+    from paper_2405_16283_b200.executor import Executor
+    g = W.GraphBuilder()
+    a = g.input("A", (128, 128), "bf16")
+    b = g.input("B", (128, 128), "bf16")
+    g.gemm("C", a, b, 128, 128, 128, out_shape=(128, 128))
+    mg, _ = W.plan(g, 1 << 24)
+    for cfg, key in (({"timestamps": "bogus"}, "timestamps"), ({"input_residency": "gpu"}, "input_residency"),
+                     ({"completion": "spin"}, "completion"), ({"device_inputs": "move"}, "device_inputs")):
+        with pytest.raises(memplan.MemplanError) as e:
+            Executor(mg, g.to_json(), cfg)
+        assert e.value.code == 2 and key in str(e.value)
