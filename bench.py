@@ -508,7 +508,12 @@ def run_ours(args, world, rank, local):
         "device_time_by_op_s": {k: round(v, 5) for k, v in sorted(by_type.items(), key=lambda kv: -kv[1])},
         "value_run": {"last_step_makespan_s": [round(x, 5) for x in makespans], "exposed_transfer_s":
                       round(st_v["exposed_transfer_s"], 5), "d2d_input_bytes": st_v["d2d_bytes"],
-                      "inputs": "aliased in place (HBM staging copies outside the arena)"},
+                      "inputs": "aliased in place (HBM staging copies outside the arena)",
+                      # host event loop of the traced step (A7): dispatch work vs waiting on completions
+                      "host_dispatch_ms": round(st_v.get("host_dispatch_s", 0) * 1e3, 3),
+                      "host_wait_ms": round(st_v.get("host_wait_s", 0) * 1e3, 3),
+                      "host_dispatch_us_per_vertex": round(st_v.get("host_dispatch_s", 0) * 1e6 /
+                                                           max(1, st_v["vertices"]), 2)},
         "value_inputs_copied_into_arena": {"value": round(tokens / t_copy, 1), "unit": UNIT,
                                            "ms_per_step": round(t_copy / args.steps * 1e3, 2),
                                            "d2d_input_bytes_per_step": st_c["d2d_bytes"]},

@@ -817,7 +817,16 @@ class CudaBackend {
         if (x_.cfg.poll) flying_.push_back(vidx);
     }
     bool idle() const { return in_flight_ == 0; }
+    double wait_s() const { return wait_s_; }
     std::int32_t wait_next(double& now) {
+        const auto t_in = std::chrono::steady_clock::now();
+        const std::int32_t v = wait_next_(now);
+        wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_in).count();
+        return v;
+    }
+
+  private:
+    std::int32_t wait_next_(double& now) {
         if (!instant_.empty()) {  // aliased inputs complete at dispatch
             const std::int32_t v = instant_.front();
             instant_.pop_front();
@@ -840,7 +849,6 @@ class CudaBackend {
         return v;
     }
 
-  private:
     // Spins over the in-flight vertices' end events (oldest first) until one
     // has completed; lower latency than a host-function round trip.
     std::int32_t poll_next(double& now) {
@@ -867,6 +875,7 @@ class CudaBackend {
     Executor::Impl& x_;
     std::chrono::steady_clock::time_point start_;
     int in_flight_ = 0;
+    double wait_s_ = 0;
     std::vector<std::int32_t> flying_;
     std::deque<std::int32_t> instant_;
 };
@@ -903,6 +912,9 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
     try {
         if (chain) dispatch_loop_lookahead(*g, res, ready, be, cfg.lookahead);
         else dispatch_loop(*g, res, ready, be);
+        last.host_wait_s = be.wait_s();
+        last.host_dispatch_s =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count() - last.host_wait_s;
     } catch (...) {
         for (int d = 0; d < D; ++d) {
             cudaSetDevice(ordinal[d]);
@@ -1128,6 +1140,8 @@ std::string RunStats::to_json() const {
     j["exposed_transfer_s"] = exposed_transfer_s;
     j["exposed_transfer_gpu_s"] = exposed_transfer_gpu_s;
     j["zero_copy_bytes"] = zero_copy_bytes;
+    j["host_dispatch_s"] = host_dispatch_s;
+    j["host_wait_s"] = host_wait_s;
     return j.dump();
 }
 

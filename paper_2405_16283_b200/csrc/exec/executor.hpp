@@ -50,6 +50,9 @@ struct RunStats {
     double kernel_time_s = 0, kernel_busy_s = 0, copy_time_s = 0, exposed_transfer_s = 0;
     double exposed_transfer_gpu_s = 0;  // same, per physical GPU (devices sharing a GPU cover each other)
     std::int64_t zero_copy_bytes = 0;     // bytes kernels read over PCIe from mapped host inputs
+    // host event loop: time spent dispatching (ready-list ordering, resource
+    // accounting, launch/copy API calls) vs waiting for the next completion
+    double host_dispatch_s = 0, host_wait_s = 0;
     std::string to_json() const;
 };
 

@@ -296,6 +296,9 @@ def test_dispatch_order_independence_bitwise(cfg):
         st = ex.stats()
     assert all(r == results[0] for r in results)
     assert st["kernel_launches"] > 0 and st["d2h_bytes"] + st["d2h_elided_bytes"] > 0
+    # host event loop accounting: dispatch work + completion waits fit inside the run's wall time
+    assert st["host_dispatch_s"] > 0 and st["host_wait_s"] >= 0
+    assert st["host_dispatch_s"] + st["host_wait_s"] <= st["wall_s"] * 1.05 + 1e-4
     want = oracle_outputs(g, mg, inp)
     assert rel_err(out_values(g, o, results[0]), out_values(g, o, want[o])) < 3e-2
 

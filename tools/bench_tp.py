@@ -66,6 +66,7 @@ print(json.dumps({"workload": f"llama_{a.model}_tp{a.tp}_seq{a.seq}_layers{a.lay
                   "d2h_bytes": stt["d2h_bytes"], "kernel_launches": stt["kernel_launches"],
                   "exposed_transfer_s": round(stt["exposed_transfer_s"], 4),
                   "exposed_transfer_gpu_s": round(stt["exposed_transfer_gpu_s"], 4), "pcie_h2d_gbs": round(pcie, 1),
+                  "host_dispatch_s": round(stt["host_dispatch_s"], 4), "host_wait_s": round(stt["host_wait_s"], 4),
                   "roofline": {"compute_s": round(compute_s, 4), "pcie_h2d_s": round(pcie_s, 4),
                                "bound": "pcie" if pcie_s > compute_s else "tensor",
                                "frac": round(bound / step, 4)},
