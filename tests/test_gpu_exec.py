@@ -367,6 +367,23 @@ def test_input_residency_modes_bitwise():
     assert res["host"] == res["copy"] == res["alias"]
 
 
+def test_full_width_llama7b_layer_matches_oracle_with_offloads():
+    """One LLaMA-7B layer at BASELINE config 2's full width and sequence
+    (d 4096, 32 heads, ffn 11008, vocab 32000, seq 4096) under a lazy plan at
+    1.25x the working-set floor (weights and activations offloaded and
+    reloaded), against the CPU oracle on the same inputs (bf16 tolerance)."""
+    g = W.llama_prefill(W.LLAMA_7B, 4096, layers=1)
+    mg, stats = W.plan(g, int(W.working_set_floor(g)[0] * 1.25), alloc_horizon="lazy")
+    assert stats["offloads"] > 0 and stats["reloads"] > 0
+    inp = inputs_of(g, seed=3)
+    trace, got = run_gpu(g, mg, inp)
+    assert trace["host_bytes_transferred"] > 0
+    check_trace(mg, trace)
+    want = oracle_outputs(g, mg, inp)
+    (o,) = g.outputs()
+    assert rel_err(out_values(g, o, got[o]), out_values(g, o, want[o])) < 3e-2
+
+
 def test_full_size_llama7b_properties():
     """BASELINE config 2 at full size (LLaMA-7B, seq 4096, 16 GiB cap), checked
     through size-independent properties: bitwise-identical logits under
