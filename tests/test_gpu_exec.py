@@ -77,6 +77,8 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=1024, N=512, K=1024, batch=2, causal=2, tile="wide"),
     dict(M=1536, N=1024, K=256, epilogue="swiglu", tile="wide"),  # wide + fused SwiGLU
     dict(M=512, N=256, K=4096, tile="wide"),         # long K: deferred half-1 MMAs cycle the ring
+    dict(M=4096, N=12288, K=256, tile="wide"),       # 5+ short tiles per pair: split-drain hand-off per tile
+    dict(M=2048, N=8192, K=256, epilogue="swiglu", tile="wide"),  # split drain of gate/up column halves
     dict(M=2304, N=2304, K=256, epilogue="swiglu", tile="streamk"),  # stream-K + fused SwiGLU
     dict(M=2304, N=2304, K=256, epilogue="swiglu", tile="narrow"),  # SwiGLU never takes half tiles
 ])
