@@ -51,3 +51,33 @@ def test_two_rank_gloo():
     import json
     res = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
     assert all(r["max"] == 1.5 and r["same_plan"] for r in res)
+
+
+def test_reference_arm_two_ranks_rank0_only():
+    """`bench.py --impl reference` under a 2-rank launch: rank 0 alone times the
+    CPU arm and prints the JSON line, rank 1 exits 0 without work (gloo here,
+    NCCL on the GPU box)."""
+    import json
+    ref_so = os.path.join(ROOT, "oracle", "_ref")
+    if not (os.path.isdir(ref_so) and any(f.startswith("_memplan") for f in os.listdir(ref_so))):
+        import pytest
+        pytest.skip("oracle/_ref (the reference planner) is not built")
+    port = free_port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, WORLD_SIZE="2", RANK=str(r), LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), CUDA_VISIBLE_DEVICES="")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                                       "--gpus", "2", "--steps", "1", "--warmup", "0", "--seq", "256",
+                                       "--layers", "1"], env=env, cwd=ROOT, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-2000:]
+    lines0 = [l for l in outs[0][0].splitlines() if l.startswith("{")]
+    assert len(lines0) == 1 and not [l for l in outs[1][0].splitlines() if l.startswith("{")]
+    d = json.loads(lines0[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+    rp = d["reference_planner"]
+    assert rp["memgraph_bytes_identical"] is True and rp["simulate_trace_identical"] is True
