@@ -105,7 +105,7 @@ int tn_make_fixed_order(const char* memgraph_json, char** memgraph_out, char** e
  *   "timestamps": "traced"          "traced": runs without a trace record timing-free completion
  *                                   events only (a timing event between kernels costs ~3 us);
  *                                   "all": every run is timestamped (last_trace() after any run)
- *   "pdl": false                    programmatic dependent launch between kernels of untimed runs
+ *   "pdl": true                     programmatic dependent launch between kernels of untimed runs
  *   "elide_input_offloads": true    an evicted input is reloaded from its own copy, never offloaded
  *   "materialize_inputs": true, "timeout_s": 600 */
 int tn_exec_create(const char* memgraph_json, const char* taskgraph_json, const char* config_json,

@@ -33,9 +33,10 @@ struct ExecConfig {
                                       // completion events and programmatic dependent launch (a
                                       // timing event between two kernels costs ~3 us and blocks PDL);
                                       // "all" -> every run records per-vertex timestamps
-    bool pdl = false;                 // "pdl": programmatic dependent launch in untimed runs (no
-                                      // measurable gain on the 7B step: the persistent kernels hold
-                                      // every SM until they exit; tools/diag_run_overhead.py)
+    bool pdl = true;                  // "pdl": programmatic dependent launch between consecutive
+                                      // compute-stream kernels of untimed runs (each kernel's
+                                      // prologue overlaps its predecessor's tail; paired A/B on the
+                                      // 7B step: 49.72 vs 50.00 ms, tools/ab_exec_cfg.py)
     bool zero_copy_gathers = true;    // "zero_copy_gathers": host-resident inputs read only as the
                                       // table of embedding kernels stay in mapped pinned memory and
                                       // the kernel gathers its rows over PCIe (the Input vertex

@@ -233,7 +233,8 @@ def test_untimed_runs_with_pdl_are_bitwise_equal_to_traced_runs():
     inp = inputs_of(g, seed=12)
     (o,) = g.outputs()
     n = g.tensors[o].nbytes
-    for cfg in ({"input_residency": "device"}, {"input_residency": "device", "pdl": True}, {"pdl": True}):
+    for cfg in ({"input_residency": "device", "pdl": False}, {"input_residency": "device"}, {"pdl": True},
+                {"pdl": False}):
         with Executor(mg, g.to_json(), cfg) as ex:
             for vid, a in inp.items():
                 ex.set_input(vid, a)
