@@ -1379,17 +1379,17 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         // two halves (short with the TMA-store epilogue). Measured in the
         // 7B step (power-capped, per GEMM class): wide wins ~6.5% at
         // K = 11008 despite worse wave quantisation (4 vs 3.5 narrow
-        // tile-times) and loses at K = 4096; the QKV+RoPE epilogue does not
-        // stage through TMA, so it stays narrow. Hence: compare wave
-        // quantisation (a wide tile = two narrow tile-times) with a bias of
-        // 1.2 for long K loops (>= 128 K blocks) and 0.9 otherwise.
+        // tile-times); the QKV+RoPE epilogue does not stage through TMA, so
+        // it stays narrow. Hence: compare wave quantisation (a wide tile =
+        // two narrow tile-times) with a bias of 1.2 in favour of wide tiles
+        // (with PDL on, wide attn_out / gate_up tiles at K = 4096 too: 7B
+        // step 49.60-49.65 vs 49.91-50.07 ms, alternating runs).
         const long long tn = (a.N + 255) / 256;
         const long long narrow = a.batch * ((a.M + 255) / 256) * tn, wide = a.batch * ((a.M + 511) / 512) * tn;
         int s1, s2;
         const double t_narrow = tail_plan(narrow, &s1, false), t_wide = 2.0 * tail_plan(wide, &s2, true);
-        const long long nkb = (static_cast<long long>(a.K) * es + kAtom - 1) / kAtom;
         static const char* wenv = std::getenv("TN_GEMM_WIDE_BIAS");  // tuning override
-        const double bias = wenv ? std::atof(wenv) : (nkb >= 128 ? 1.2 : 0.9);
+        const double bias = wenv ? std::atof(wenv) : 1.2;
         // fused-norm producers stage two outputs per chunk: their drain would
         // double the wide tiles' exposed accumulator hand-off, so they stay narrow
         if (a.epi != 2 && !a.no_P && t_wide <= t_narrow * bias + 1e-9 && (a.M % 512 == 0 || a.M > 2048)) plan->path = 3;
