@@ -38,10 +38,9 @@ int tn_validate_taskgraph(const char* graph_json, char** violations_json, char**
 int tn_topological_order(const char* graph_json, const char* policy, uint64_t seed, char** order_json,
                          char** err);
 
-/* replaces bindings.cpp:53-59 gen_matmul / gen_layered / gen_random_dag. */
-int tn_gen_matmul(int parts, char** graph_json, char** err);
-int tn_gen_layered(int layers, int width, int devices, uint64_t seed, char** graph_json, char** err);
-int tn_gen_random_dag(int n, double edge_density, int devices, uint64_t seed, char** graph_json, char** err);
+/* bindings.cpp:53-59 gen_matmul / gen_layered / gen_random_dag (toy
+ * generators, SURVEY §2 out of scope) are not part of this library; the tests
+ * read the reference generators' outputs from tests/golden/taskgraphs.json. */
 
 /* replaces bindings.cpp:118-124 taskgraph_to_dot / memgraph_to_dot. */
 int tn_taskgraph_to_dot(const char* graph_json, char** dot, char** err);

@@ -41,9 +41,6 @@ def lib():
             "tn_free": (None, [c_void_p]),
             "tn_validate_taskgraph": (c_int, [c_char_p, P, P]),
             "tn_topological_order": (c_int, [c_char_p, c_char_p, c_uint64, P, P]),
-            "tn_gen_matmul": (c_int, [c_int, P, P]),
-            "tn_gen_layered": (c_int, [c_int, c_int, c_int, c_uint64, P, P]),
-            "tn_gen_random_dag": (c_int, [c_int, c_double, c_int, c_uint64, P, P]),
             "tn_taskgraph_to_dot": (c_int, [c_char_p, P, P]),
             "tn_memgraph_to_dot": (c_int, [c_char_p, P, P]),
             "tn_build_memgraph": (

@@ -64,16 +64,6 @@ int tn_topological_order(const char* graph_json, const char* policy, uint64_t se
     });
 }
 
-int tn_gen_matmul(int parts, char** out, char** err) {
-    return guarded(err, [&] { *out = dup(serialize_taskgraph(gen_matmul(parts))); });
-}
-int tn_gen_layered(int layers, int width, int devices, uint64_t seed, char** out, char** err) {
-    return guarded(err, [&] { *out = dup(serialize_taskgraph(gen_layered(layers, width, devices, seed))); });
-}
-int tn_gen_random_dag(int n, double density, int devices, uint64_t seed, char** out, char** err) {
-    return guarded(err, [&] { *out = dup(serialize_taskgraph(gen_random_dag(n, density, devices, seed))); });
-}
-
 int tn_taskgraph_to_dot(const char* graph_json, char** out, char** err) {
     return guarded(err, [&] { *out = dup(taskgraph_to_dot(parse_taskgraph(str(graph_json)))); });
 }

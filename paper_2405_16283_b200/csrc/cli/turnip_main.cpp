@@ -14,8 +14,6 @@
 //                     [--out F] [--format json|csv]
 //   turnip bench      --memgraph M [--profile P] [--trials N] [--seed N] [--out F]
 //   turnip export-dot (--graph G | --memgraph M) [--out F]
-//   turnip gen        [--kind matmul|layered|random] [--parts N] [--layers N] [--width N]
-//                     [--devices N] [--n N] [--density X] [--seed N] [--out F]
 //   turnip execute    --memgraph M --graph G [--config JSON] [--policy ..] [--tie-break ..]
 //                     [--seed N] [--input ID=FILE]... [--output ID=FILE]... [--out TRACE]
 #include <cstdio>
@@ -247,25 +245,6 @@ int cmd_export_dot(const Args& a) {
     return kOk;
 }
 
-int cmd_gen(const Args& a) {
-    auto i = [&](const char* k, int d) { return a.has(k) ? std::stoi(a.get(k)) : d; };
-    const std::string kind = a.get("kind", "matmul");
-    const std::uint64_t seed = seed_of(a);
-    TaskGraph g;
-    if (kind == "matmul") g = gen_matmul(i("parts", 3));
-    else if (kind == "layered") g = gen_layered(i("layers", 2), i("width", 2), i("devices", 2), seed);
-    else if (kind == "random")
-        g = gen_random_dag(i("n", 16), a.has("density") ? std::stod(a.get("density")) : 0.3, i("devices", 2), seed);
-    else {
-        std::cerr << "unknown generator kind: " << kind << "\n";
-        return kUsage;
-    }
-    std::string out = serialize_taskgraph(g);
-    if (a.has("out")) write_file(a.get("out"), out);
-    else std::cout << out;
-    return kOk;
-}
-
 int cmd_execute(const Args& a) {
     const std::string mg = read_file(a.need("memgraph"));
     const std::string tg = read_file(a.need("graph"));
@@ -297,7 +276,7 @@ int cmd_execute(const Args& a) {
 }
 
 void usage() {
-    std::cerr << "usage: turnip <validate|compile|verify|simulate|bench|export-dot|gen|execute> [options]\n";
+    std::cerr << "usage: turnip <validate|compile|verify|simulate|bench|export-dot|execute> [options]\n";
 }
 
 }  // namespace
@@ -326,9 +305,6 @@ int main(int argc, char** argv) {
         if (cmd == "bench")
             return cmd_bench(parse_args(argc, argv, 2, {"memgraph", "profile", "trials", "seed", "out"}, {}));
         if (cmd == "export-dot") return cmd_export_dot(parse_args(argc, argv, 2, {"graph", "memgraph", "out"}, {}));
-        if (cmd == "gen")
-            return cmd_gen(parse_args(argc, argv, 2,
-                                      {"kind", "parts", "layers", "width", "devices", "n", "density", "seed", "out"}, {}));
         if (cmd == "execute")
             return cmd_execute(parse_args(argc, argv, 2,
                                           {"memgraph", "graph", "config", "policy", "tie-break", "seed", "input",

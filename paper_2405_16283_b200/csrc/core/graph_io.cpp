@@ -16,6 +16,12 @@
 
 #include <nlohmann/json.hpp>
 
+// Byte-identical serialisation with the reference depends on the exact
+// nlohmann/json release it links (number formatting, dump(2) layout).
+#if NLOHMANN_JSON_VERSION_MAJOR != 3 || NLOHMANN_JSON_VERSION_MINOR != 11 || NLOHMANN_JSON_VERSION_PATCH != 3
+#error "memgraph JSON must be serialised with nlohmann/json 3.11.3 (set JSONINC)"
+#endif
+
 #include "planner.hpp"
 
 namespace tn {
@@ -412,180 +418,6 @@ void prune_superfluous_edges(MemGraph& m, bool drop) {
             if (!flag[e]) kept.push_back(m.edges[e]);
         m.edges = std::move(kept);
     }
-}
-
-// -------------------------------------------------------------- generators --
-// Restatements of taskgraph.cpp:418-616 (identical RNG draw sequences).
-TaskGraph gen_matmul(int parts) {
-    if (parts < 1) throw Error("gen_matmul: parts must be >= 1");
-    TaskGraph g;
-    g.device_count = parts;
-    VertexId next = 0;
-    auto add = [&](VertexKind kind, DeviceId dev, DeviceId src = -1) {
-        TaskVertex v;
-        v.id = next++;
-        v.kind = kind;
-        v.device = dev;
-        v.src_device = src;
-        g.vertices.push_back(v);
-        return v.id;
-    };
-    auto edge = [&](VertexId p, VertexId c) { g.edges.emplace_back(p, c); };
-    VertexId x0 = add(VertexKind::Input, 0), y0 = add(VertexKind::Input, 0), p0 = add(VertexKind::Kernel, 0);
-    edge(x0, p0);
-    edge(y0, p0);
-    if (parts == 1) {
-        g.reindex();
-        return g;
-    }
-    std::vector<VertexId> partial(parts);
-    partial[0] = p0;
-    for (int d = 1; d < parts; ++d) {
-        VertexId x = add(VertexKind::Input, d), y = add(VertexKind::Input, d), p = add(VertexKind::Kernel, d);
-        edge(x, p);
-        edge(y, p);
-        partial[d] = p;
-    }
-    VertexId tail = partial[parts - 1];
-    for (int d = parts - 1; d >= 2; --d) {
-        VertexId t = add(VertexKind::Transfer, d - 1, d);
-        edge(tail, t);
-        VertexId combine = add(VertexKind::Kernel, d - 1);
-        edge(partial[d - 1], combine);
-        edge(t, combine);
-        tail = combine;
-    }
-    VertexId ship = add(VertexKind::Transfer, 0, 1);
-    edge(tail, ship);
-    VertexId reshape;
-    if (parts >= 3) {
-        VertexId raw = add(VertexKind::Transfer, 0, 1);
-        edge(partial[1], raw);
-        reshape = add(VertexKind::Kernel, 0);
-        edge(ship, reshape);
-        edge(raw, reshape);
-    } else {
-        reshape = add(VertexKind::Kernel, 0);
-        edge(ship, reshape);
-    }
-    VertexId result = add(VertexKind::Kernel, 0);
-    edge(p0, result);
-    edge(reshape, result);
-    g.reindex();
-    return g;
-}
-
-TaskGraph gen_layered(int layers, int width, int devices, std::uint64_t seed) {
-    if (layers < 1 || width < 1 || devices < 1) throw Error("gen_layered: parameters must be positive");
-    std::mt19937_64 rng(seed);
-    std::uniform_int_distribution<std::int64_t> size_dist(1, 4);
-    std::uniform_real_distribution<double> cost_dist(0.5, 2.0);
-    TaskGraph g;
-    g.device_count = devices;
-    VertexId next = 0;
-    auto add = [&](VertexKind kind, DeviceId dev, DeviceId src = -1) {
-        TaskVertex v;
-        v.id = next++;
-        v.kind = kind;
-        v.device = dev;
-        v.src_device = src;
-        v.output_size = size_dist(rng);
-        v.cost_hint = cost_dist(rng);
-        g.vertices.push_back(v);
-        return v.id;
-    };
-    auto edge = [&](VertexId p, VertexId c) { g.edges.emplace_back(p, c); };
-    std::vector<VertexId> head(devices);
-    std::vector<std::vector<VertexId>> boundaries(devices);
-    for (int d = 0; d < devices; ++d) head[d] = add(VertexKind::Input, d);
-    for (int layer = 0; layer < layers; ++layer) {
-        std::vector<VertexId> out(devices);
-        for (int d = 0; d < devices; ++d) {
-            VertexId cur = head[d];
-            for (int k = 0; k < width; ++k) {
-                VertexId ker = add(VertexKind::Kernel, d);
-                edge(cur, ker);
-                if (k == width - 1 && width > 1) edge(head[d], ker);
-                cur = ker;
-            }
-            out[d] = cur;
-            boundaries[d].push_back(cur);
-        }
-        if (devices > 1) {
-            for (int d = 0; d < devices; ++d) {
-                int dst = (d + 1) % devices;
-                VertexId t = add(VertexKind::Transfer, dst, d);
-                edge(out[d], t);
-                head[dst] = t;
-            }
-        } else {
-            head[0] = out[0];
-        }
-    }
-    for (int d = 0; d < devices; ++d) {
-        VertexId prev = -1;
-        for (int layer = layers - 1; layer >= 0; --layer) {
-            VertexId tail = add(VertexKind::Kernel, d);
-            edge(boundaries[d][layer], tail);
-            if (prev != -1) edge(prev, tail);
-            prev = tail;
-        }
-    }
-    g.reindex();
-    return g;
-}
-
-TaskGraph gen_random_dag(int n, double edge_density, int devices, std::uint64_t seed) {
-    if (n < 1 || devices < 1) throw Error("gen_random_dag: parameters must be positive");
-    if (!(edge_density > 0.0 && edge_density <= 1.0)) throw Error("gen_random_dag: edge_density must be in (0, 1]");
-    std::mt19937_64 rng(seed);
-    std::uniform_int_distribution<int> dev_dist(0, devices - 1);
-    std::uniform_int_distribution<std::int64_t> size_dist(1, 8);
-    std::uniform_real_distribution<double> coin(0.0, 1.0);
-    struct Node {
-        DeviceId device;
-        std::int64_t size;
-        std::vector<int> parents;
-    };
-    std::vector<Node> nodes(n);
-    for (int i = 0; i < n; ++i) {
-        nodes[i].device = dev_dist(rng);
-        nodes[i].size = size_dist(rng);
-        for (int p = 0; p < i; ++p)
-            if (coin(rng) < edge_density) nodes[i].parents.push_back(p);
-    }
-    TaskGraph g;
-    g.device_count = devices;
-    VertexId next = 0;
-    auto add = [&](VertexKind kind, DeviceId dev, std::int64_t size, DeviceId src = -1) {
-        TaskVertex v;
-        v.id = next++;
-        v.kind = kind;
-        v.device = dev;
-        v.src_device = src;
-        v.output_size = size;
-        g.vertices.push_back(v);
-        return v.id;
-    };
-    std::vector<VertexId> node_id(n);
-    for (int i = 0; i < n; ++i) {
-        if (nodes[i].parents.empty()) {
-            node_id[i] = add(VertexKind::Input, nodes[i].device, nodes[i].size);
-            continue;
-        }
-        node_id[i] = add(VertexKind::Kernel, nodes[i].device, nodes[i].size);
-        for (int p : nodes[i].parents) {
-            if (nodes[p].device == nodes[i].device) {
-                g.edges.emplace_back(node_id[p], node_id[i]);
-            } else {
-                VertexId t = add(VertexKind::Transfer, nodes[i].device, nodes[p].size, nodes[p].device);
-                g.edges.emplace_back(node_id[p], t);
-                g.edges.emplace_back(t, node_id[i]);
-            }
-        }
-    }
-    g.reindex();
-    return g;
 }
 
 // -------------------------------------------------------------- taskgraph IO --

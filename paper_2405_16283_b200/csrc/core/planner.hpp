@@ -57,9 +57,6 @@ std::vector<std::string> validate_taskgraph(const TaskGraph& g);
 VertexOrder topological_order(const TaskGraph& g, OrderPolicy policy, std::uint64_t seed = 0);
 bool is_linear_extension(const TaskGraph& g, const VertexOrder& order);
 
-TaskGraph gen_matmul(int parts);
-TaskGraph gen_layered(int layers, int width, int devices, std::uint64_t seed);
-TaskGraph gen_random_dag(int n, double edge_density, int devices, std::uint64_t seed);
 
 // --- wire formats -------------------------------------------------------------
 std::string serialize_taskgraph(const TaskGraph& g);

@@ -599,6 +599,9 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             break;
         case OpType::Attention: {
             need_args(1, 3);
+            if (op.args.size() == 2)
+                throw Error("kernel " + std::to_string(v.id) +
+                            " (attention): takes one packed tensor (q_off/k_off/v_off) or three arguments [q, k, vT]");
             if (op.hd <= 0 || op.hd > 256 || op.seq <= 0 || op.heads <= 0) throw Error("attention: bad shape");
             const std::int64_t ldo = op.ldo ? op.ldo : op.heads * op.hd;
             const std::int64_t sec = op.heads * op.seq * op.hd;
@@ -792,7 +795,9 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
         }
     }
     TN_CUDA(cudaEventRecord(done_event(vidx), s));
-    if (!cfg.poll) TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
+    // instant vertices complete through the backend's instant queue at
+    // dispatch; a host callback as well would complete them twice
+    if (!cfg.poll && !in.instant) TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
 }
 
 // -------------------------------------------------------------------- run ---
@@ -1046,8 +1051,27 @@ Executor::Impl::~Impl() {
 }
 
 // ------------------------------------------------------------- public API ---
+namespace {
+// Every public entry point starts from the thread's real current device (the
+// caller may have switched devices since the last call) and hands it back
+// unchanged on exit.
+struct DeviceGuard {
+    int& cached;
+    int saved = -1;
+    explicit DeviceGuard(int& cur) : cached(cur) {
+        if (cudaGetDevice(&saved) != cudaSuccess) saved = -1;
+        cached = -1;
+    }
+    ~DeviceGuard() {
+        if (saved >= 0) cudaSetDevice(saved);
+        cached = -1;
+    }
+};
+}  // namespace
+
 Executor::Executor(const std::string& memgraph_json, const std::string& taskgraph_json, const ExecConfig& cfg)
     : impl_(std::make_unique<Impl>()) {
+    DeviceGuard dg(impl_->cur_dev);
     auto [m, map] = parse_memgraph(memgraph_json);
     impl_->m = std::move(m);
     impl_->map = std::move(map);
@@ -1059,9 +1083,15 @@ Executor::Executor(const std::string& memgraph_json, const std::string& taskgrap
     impl_->build();
 }
 
-Executor::~Executor() = default;
+Executor::~Executor() {
+    if (impl_) {
+        DeviceGuard dg(impl_->cur_dev);
+        impl_.reset();
+    }
+}
 
 void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool from_device) {
+    DeviceGuard dg(impl_->cur_dev);
     const TaskVertex* v = impl_->tg.find(id);
     if (!v || v->kind != VertexKind::Input) throw Error("vertex " + std::to_string(id) + " is not a taskgraph input");
     if (bytes > static_cast<std::size_t>(v->output_size))
@@ -1099,6 +1129,7 @@ void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool 
 }
 
 ExecutionTrace Executor::run(const SchedulerPolicy& pol, std::uint64_t seed, bool want_trace) {
+    DeviceGuard dg(impl_->cur_dev);
     ExecutionTrace t;
     impl_->run(pol, seed, want_trace ? &t : nullptr);
     return t;
@@ -1106,6 +1137,7 @@ ExecutionTrace Executor::run(const SchedulerPolicy& pol, std::uint64_t seed, boo
 
 ExecutionTrace Executor::last_trace() {
     if (impl_->dispatched.empty()) throw Error("no run to trace yet");
+    DeviceGuard dg(impl_->cur_dev);
     return impl_->build_trace();
 }
 
@@ -1114,6 +1146,7 @@ void Executor::get_output(VertexId id, void* host, std::size_t bytes) {
     if (it == impl_->map.placements.end()) throw Error("vertex " + std::to_string(id) + " has no placement");
     if (bytes > static_cast<std::size_t>(it->second.size))
         throw Error("requested " + std::to_string(bytes) + " bytes from a region of " + std::to_string(it->second.size));
+    DeviceGuard dg(impl_->cur_dev);
     impl_->set_device(it->second.device);
     TN_CUDA(cudaMemcpy(host, impl_->ptr_of(id), bytes, cudaMemcpyDeviceToHost));
 }

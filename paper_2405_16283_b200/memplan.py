@@ -17,9 +17,6 @@ __all__ = [
     "MemplanError",
     "build_memgraph",
     "compare_policies",
-    "gen_layered",
-    "gen_matmul",
-    "gen_random_dag",
     "make_fixed_order",
     "memgraph_to_dot",
     "simulate",
@@ -39,18 +36,6 @@ def validate_taskgraph(graph_json: str) -> list[str]:
 def topological_order(graph_json: str, policy: str = "as-listed", seed: int = 0) -> list[int]:
     """bindings.cpp:47-51."""
     return json.loads(call("tn_topological_order", enc(graph_json), enc(policy), seed))
-
-
-def gen_matmul(parts: int) -> str:
-    return call("tn_gen_matmul", parts)
-
-
-def gen_layered(layers: int, width: int, devices: int, seed: int = 0) -> str:
-    return call("tn_gen_layered", layers, width, devices, seed)
-
-
-def gen_random_dag(n: int, edge_density: float, devices: int, seed: int = 0) -> str:
-    return call("tn_gen_random_dag", n, float(edge_density), devices, seed)
 
 
 def build_memgraph(

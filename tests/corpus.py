@@ -52,14 +52,25 @@ def gen_args(seed):
     return "gen_matmul", [1 + seed % 5]
 
 
-def corpus_cases(n_seeds=90, gen_fn=None):
-    """Yields build cases; `gen_fn(name, args) -> taskgraph json` (defaults to
-    the reference-compatible generators of whichever module the caller uses)."""
-    from paper_2405_16283_b200 import memplan as mine
+_GRAPHS = None
 
+
+def taskgraph(name, args):
+    """A toy taskgraph emitted by the reference generator `name(*args)`
+    (tests/golden/taskgraphs.json, written by make_taskgraphs.py from oracle/_ref)."""
+    global _GRAPHS
+    if _GRAPHS is None:
+        import os
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "taskgraphs.json")) as f:
+            _GRAPHS = json.load(f)["graphs"]
+    return _GRAPHS[f"{name}{json.dumps(list(args))}"]
+
+
+def corpus_cases(n_seeds=90):
+    """Yields build cases over the reference-generated toy taskgraphs."""
     for seed in range(n_seeds):
         name, args = gen_args(seed)
-        gj = json.loads(getattr(mine, name)(*args))
+        gj = json.loads(taskgraph(name, args))
         for mode in ("slot", "byte"):
             fl, tot = _floor(gj, mode), _total(gj, mode)
             for rung in range(4):

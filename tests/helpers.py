@@ -111,3 +111,11 @@ def tp_inputs_from_full(g_tp, g_full, full_inputs, cfg, tp):
             a = a.reshape(d, f)[:, r * fl:(r + 1) * fl]
         out[t.id] = np.ascontiguousarray(a).reshape(-1)
     return out
+
+
+def inputs_with_in_edges(mg_json) -> int:
+    """Input vertices that must wait for earlier vertices (memory edges into
+    an input reusing a freed region; SURVEY hard part 3)."""
+    m = json.loads(mg_json)
+    ins = {v["id"] for v in m["vertices"] if v["op"] == "input"}
+    return len({e["to"] for e in m["edges"] if e["to"] in ins})

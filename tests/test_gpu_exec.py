@@ -16,7 +16,7 @@ import pytest
 
 from paper_2405_16283_b200.memplan import MemplanError
 
-from helpers import SMALL, inputs_of, oracle_outputs, out_values, rel_err, replay_capacity, small_llama
+from helpers import SMALL, inputs_of, inputs_with_in_edges, oracle_outputs, out_values, rel_err, replay_capacity, small_llama
 from paper_2405_16283_b200 import workloads as W
 from paper_2405_16283_b200.executor import Executor, execute
 
@@ -284,9 +284,14 @@ def test_llama_fused_norm_parity_with_offloads():
 
 
 @pytest.mark.parametrize("cfg", [{"lookahead": 1}, {"lookahead": 0}, {"lookahead": 0, "completion": "callback"},
-                                 {"lookahead": 2, "streams_per_device": 3}])
+                                 {"lookahead": 2, "streams_per_device": 3},
+                                 # aliased device inputs with in-edges complete at dispatch: the host
+                                 # callback path must not complete them a second time
+                                 {"lookahead": 0, "completion": "callback", "input_residency": "device"},
+                                 {"lookahead": 1, "completion": "callback", "input_residency": "device"}])
 def test_dispatch_order_independence_bitwise(cfg):
     g, mg, _ = small_llama(seq=256, layers=2)
+    assert inputs_with_in_edges(mg) > 0  # inputs that reuse freed regions wait on memory edges
     inp = inputs_of(g, seed=2)
     (o,) = g.outputs()
     results = []
@@ -620,6 +625,15 @@ def test_executor_rejects_bad_payloads_without_crashing():
     del bad["vertices"][2]["op"]
     with pytest.raises(MemplanError, match="no op payload"):
         Executor(mg, json.dumps(bad))
+    # attention takes one packed tensor or [q, k, vT]; two arguments are ambiguous
+    g2 = W.GraphBuilder()
+    q = g2.input("q", (1, 128, 128), "bf16")
+    k = g2.input("k", (1, 128, 128), "bf16")
+    g2.kernel("o", {"type": "attention", "args": [q, k], "heads": 1, "seq": 128, "hd": 128, "scale": 0.1,
+                    "causal": 1}, (128, 128), "bf16")
+    mg2, _ = W.plan(g2, 1 << 24)
+    with pytest.raises(MemplanError, match="packed tensor"):
+        Executor(mg2, g2.to_json())
     slot_mg, _ = memplan_build_slot(g)
     with pytest.raises(MemplanError, match="byte-mode"):
         Executor(slot_mg, g.to_json())

@@ -2,6 +2,7 @@
 (proj/tests/test_simulator.cpp restated through the memplan-compatible API)."""
 import json
 
+from corpus import taskgraph
 from paper_2405_16283_b200 import memplan
 
 
@@ -47,7 +48,7 @@ def test_overlap_on_two_devices():
 
 def test_fixed_order_never_faster_without_noise():
     for seed in range(12):
-        g = memplan.gen_random_dag(14, 0.3, 2, seed)
+        g = taskgraph("gen_random_dag", [14, 0.3, 2, seed])
         try:
             mg, _ = memplan.build_memgraph(g, [6, 6])
         except memplan.MemplanError:
@@ -64,7 +65,7 @@ def test_compare_policies_chain_zero():
 
 
 def test_fixed_order_chains_each_device():
-    mg, _ = memplan.build_memgraph(memplan.gen_matmul(1), [4])
+    mg, _ = memplan.build_memgraph(taskgraph("gen_matmul", [1]), [4])
     fixed = json.loads(memplan.make_fixed_order(mg))
     m = json.loads(mg)
     op = {v["id"]: v["op"] for v in m["vertices"]}
@@ -74,7 +75,7 @@ def test_fixed_order_chains_each_device():
 
 
 def test_noisy_traces_deterministic_and_csv():
-    g = memplan.gen_layered(2, 2, 2, 3)
+    g = taskgraph("gen_layered", [2, 2, 2, 3])
     mg, _ = memplan.build_memgraph(g, [6, 6])
     prof = json.dumps({"noise": {"kind": "uniform", "param": 0.2}})
     a = memplan.simulate(mg, prof, tie_break="seeded-random", seed=99)
