@@ -141,6 +141,14 @@ int tn_exec_placement_ptr(tn_exec* h, int64_t vertex_id, void** device_ptr, char
  * transfer time, per-op-type device time). */
 int tn_exec_stats(tn_exec* h, char** stats_json, char** err);
 
+/* replaces bindings.cpp:109-116 compare_policies(memgraph_json, profile_json,
+ * trials, seed) with measured makespans: `trials` paired runs of this
+ * executor's memgraph, event-driven vs make_fixed_order (simulator.cpp:86-104),
+ * alternating which goes first, each makespan device-timed (CUDA events around
+ * the whole run); summary JSON in the schema of tn_compare_policies with the
+ * same 2000-resample bootstrap (simulator.cpp:365-417). */
+int tn_exec_compare_policies(tn_exec* h, int64_t trials, uint64_t seed, char** summary_json, char** err);
+
 void tn_exec_destroy(tn_exec* h);
 
 #ifdef __cplusplus

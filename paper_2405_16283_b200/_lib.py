@@ -63,6 +63,7 @@ def lib():
             "tn_exec_last_trace": (c_int, [c_void_p, P, P]),
             "tn_exec_placement_ptr": (c_int, [c_void_p, c_int64, POINTER(c_void_p), P]),
             "tn_exec_stats": (c_int, [c_void_p, P, P]),
+            "tn_exec_compare_policies": (c_int, [c_void_p, c_int64, c_uint64, P, P]),
             "tn_exec_destroy": (None, [c_void_p]),
         }
         for name, (res, args) in {**sig, **exec_sig}.items():

@@ -106,6 +106,13 @@ int tn_exec_stats(tn_exec* h, char** out, char** err) {
     });
 }
 
+int tn_exec_compare_policies(tn_exec* h, int64_t trials, uint64_t seed, char** summary_json, char** err) {
+    return guarded(err, [&] {
+        if (!h) throw Error("null executor handle");
+        *summary_json = dup(h->x->compare_policies(trials, seed).to_json());
+    });
+}
+
 void tn_exec_destroy(tn_exec* h) {
     try {
         delete h;

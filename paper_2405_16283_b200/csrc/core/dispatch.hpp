@@ -399,6 +399,9 @@ struct ComparisonSummary {
 PolicyStats bootstrap_stats(const std::vector<double>& samples, std::uint64_t seed);
 ComparisonSummary compare_policies(const MemGraph& m, const MemoryMap& map, const DeviceProfile& p,
                                    std::int64_t trials, std::uint64_t seed);
+// The summary of paired makespans (event-driven ev[t], fixed-order fx[t]):
+// speedup (f - e) / f per pair, each series bootstrapped as in compare_policies.
+ComparisonSummary summarize_pairs(const std::vector<double>& ev, const std::vector<double>& fx, std::uint64_t seed);
 
 std::string serialize_profile(const DeviceProfile& p);
 DeviceProfile parse_profile(const std::string& text);

@@ -81,6 +81,7 @@ struct Executor::Impl {
                                         // lookahead chain is plain stream order (no cross-stream event wait)
     std::vector<std::vector<k::GemmWorkspace>> gws;  // per device x stream: stream-K GEMM scratch
     std::vector<cudaEvent_t> t0;    // per logical device
+    std::vector<cudaEvent_t> tend;  // per logical device (owner of its GPU): end of the run
     std::vector<cudaEvent_t> ev_start, ev_end;  // per memgraph vertex index (timing events)
     std::vector<cudaEvent_t> ev_done;           // timing-free completion events (untimed runs)
     bool timed = true;                          // this run records ev_start / ev_end
@@ -191,6 +192,7 @@ void Executor::Impl::build() {
     marker.assign(D, nullptr);
     compute.assign(D, nullptr);
     t0.resize(D);
+    tend.resize(D);
     for (int d = 0; d < D; ++d) {
         set_device(d);
         TN_CUDA(cudaDeviceGetAttribute(&num_sms[d], cudaDevAttrMultiProcessorCount, ordinal[d]));
@@ -207,8 +209,13 @@ void Executor::Impl::build() {
                 first = e;
                 break;
             }
-        if (first == d) TN_CUDA(cudaEventCreate(&t0[d]));
-        else t0[d] = t0[first];
+        if (first == d) {
+            TN_CUDA(cudaEventCreate(&t0[d]));
+            TN_CUDA(cudaEventCreate(&tend[d]));
+        } else {
+            t0[d] = t0[first];
+            tend[d] = tend[first];
+        }
     }
     // Peer access for every pair of distinct GPUs a transfer connects.
     for (const auto& v : m.vertices) {
@@ -932,6 +939,17 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
         set_device(d);
         TN_CUDA(cudaDeviceSynchronize());
     }
+    last.device_makespan_s = 0;
+    for (int d = 0; d < D; ++d) {
+        if (t0[d] == nullptr || (d > 0 && std::find(ordinal.begin(), ordinal.begin() + d, ordinal[d]) != ordinal.begin() + d))
+            continue;  // one clock per physical GPU
+        set_device(d);
+        TN_CUDA(cudaEventRecord(tend[d], streams[d][0]));
+        TN_CUDA(cudaEventSynchronize(tend[d]));
+        float ms = 0;
+        TN_CUDA(cudaEventElapsedTime(&ms, t0[d], tend[d]));
+        last.device_makespan_s = std::max(last.device_makespan_s, ms * 1e-3);
+    }
     last.wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     last.vertices = static_cast<std::int64_t>(dispatched.size());
     last_graph = g == &m ? nullptr : std::make_unique<MemGraph>(std::move(fixed));
@@ -1027,6 +1045,7 @@ Executor::Impl::~Impl() {
         bool owner = true;
         for (int e = 0; e < d; ++e) owner = owner && t0[e] != t0[d];
         if (t0[d] && owner) cudaEventDestroy(t0[d]);
+        if (d < static_cast<int>(tend.size()) && tend[d] && owner) cudaEventDestroy(tend[d]);
     }
     for (auto& ss : streams)
         for (auto s : ss)
@@ -1155,6 +1174,26 @@ void* Executor::placement_ptr(VertexId id) { return impl_->ptr_of(id); }
 
 const RunStats& Executor::stats() const { return impl_->last; }
 
+ComparisonSummary Executor::compare_policies(std::int64_t trials, std::uint64_t seed) {
+    if (trials < 1) throw Error("compare_policies: trials must be >= 1");
+    DeviceGuard dg(impl_->cur_dev);
+    const SchedulerPolicy ev{SchedulerKind::EventDriven, TieBreak::Fifo};
+    const SchedulerPolicy fx{SchedulerKind::FixedOrder, TieBreak::Fifo};
+    impl_->run(ev, seed, nullptr);  // warm both paths (fixed-order graph, caches, clocks)
+    impl_->run(fx, seed, nullptr);
+    std::vector<double> e(trials), f(trials);
+    for (std::int64_t t = 0; t < trials; ++t) {
+        const std::uint64_t ts = mix64(seed + static_cast<std::uint64_t>(t));
+        const bool ev_first = (t % 2) == 0;  // alternate to cancel drift (clocks, power)
+        for (int k = 0; k < 2; ++k) {
+            const bool is_ev = (k == 0) == ev_first;
+            impl_->run(is_ev ? ev : fx, ts, nullptr);
+            (is_ev ? e : f)[t] = impl_->last.device_makespan_s;
+        }
+    }
+    return summarize_pairs(e, f, seed);
+}
+
 std::string RunStats::to_json() const {
     json j;
     j["vertices"] = vertices;
@@ -1175,6 +1214,7 @@ std::string RunStats::to_json() const {
     j["zero_copy_bytes"] = zero_copy_bytes;
     j["host_dispatch_s"] = host_dispatch_s;
     j["host_wait_s"] = host_wait_s;
+    j["device_makespan_s"] = device_makespan_s;
     return j.dump();
 }
 

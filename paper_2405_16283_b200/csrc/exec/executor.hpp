@@ -54,6 +54,10 @@ struct RunStats {
     // host event loop: time spent dispatching (ready-list ordering, resource
     // accounting, launch/copy API calls) vs waiting for the next completion
     double host_dispatch_s = 0, host_wait_s = 0;
+    // device-timed span of the run: max over GPUs of (t0 event recorded after the
+    // pre-run synchronize -> end event recorded after the last vertex), no
+    // per-vertex timestamps needed
+    double device_makespan_s = 0;
     std::string to_json() const;
 };
 
@@ -67,6 +71,12 @@ class Executor {
     void get_output(VertexId id, void* host, std::size_t bytes);
     void* placement_ptr(VertexId id);
     const RunStats& stats() const;
+    // The reference's compare_policies (simulator.cpp:391-417) on hardware:
+    // `trials` paired runs of this memgraph, event-driven vs make_fixed_order,
+    // alternating which policy goes first; makespan = device_makespan_s; trial t
+    // uses seed mix64(seed + t); same summary schema and bootstrap (2000
+    // resamples) as the simulator's.
+    ComparisonSummary compare_policies(std::int64_t trials, std::uint64_t seed);
     struct Impl;
 
   private:

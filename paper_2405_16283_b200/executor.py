@@ -83,6 +83,14 @@ class Executor:
         check(lib().tn_exec_stats(self._ptr(), out.ref, err.ref), err)
         return json.loads(out.take())
 
+    def compare_policies(self, trials: int = 10, seed: int = 0) -> str:
+        """Hardware counterpart of memplan.compare_policies (bindings.cpp:109-116):
+        paired event-driven / fixed-order runs of this memgraph with
+        device-timed makespans; the reference's summary JSON schema."""
+        out, err = Out(), Out()
+        check(lib().tn_exec_compare_policies(self._ptr(), trials, seed, out.ref, err.ref), err)
+        return out.take()
+
     def close(self) -> None:
         if self._h:
             lib().tn_exec_destroy(self._h)
