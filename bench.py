@@ -1,19 +1,41 @@
 """Benchmark: LLaMA-7B forward prefill (seq 4096, bf16) executed as a memgraph
-on B200 with the HBM arena capped at 16 GiB (BASELINE.json configs[1]).
+on B200 with the HBM arena capped at 16 GiB per GPU (BASELINE.json configs[1]).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One "step" = one full execution of the memgraph (every input materialised,
-every kernel, every copy) over one batch of 4096 synthetic tokens.
-  value  tokens/s with inputs already resident in HBM when the timed region
-         starts (Input vertices copy from an HBM staging buffer, D2D);
+One "step" = one full execution of the memgraph (every Input vertex
+materialised into its arena placement, every kernel, every copy) over one
+batch of 4096 synthetic tokens.
+
+  value  tokens/s with the weights already resident in HBM when the timed
+         region starts: they sit in HBM staging buffers and every Input vertex
+         D2D-copies its tensor into its placement inside the capped arena, so
+         the whole step runs under the 16 GiB cap;
   e2e    tokens/s through the public executor API with the weights cold in
-         pinned HOST memory: every step H2D-materialises all 13.5 GB of
-         inputs and reads the logits back to host (the headline).
-Multi-GPU (torchrun): every rank runs its own replica of the single-device
-memgraph (weak scaling, no collective on the data path); the time is the max
-over ranks. --impl reference times the CPU oracle executor (oracle/) on a
-bounded sample, see DESIGN.md §Measurement.
+         pinned HOST memory: every step H2D-materialises all inputs and reads
+         the logits back to host (the headline against the reference arm);
+  compute_ceiling  the same step with Input vertices aliased to the staging
+         buffers (zero-cost inputs, as the reference simulator models them,
+         simulator.cpp:66-67): weights outside the cap, not a capped number;
+  offload  config 4 (LLaMA-7B LoRA step, activation offload under 16 GiB):
+         offload/reload bytes and PCIe GB/s, plus the paper's event-driven vs
+         fixed-order comparison measured on hardware (paired trials, bootstrap
+         CI; reference compare_policies, simulator.cpp:391-417) on config 4
+         and on a config-5 blockwise-attention plan.
+
+N GPUs (`--gpus N`, or torchrun with N ranks): ONE memgraph, the tensor-parallel
+prefill (llama_prefill_tp), partitioned over the N GPUs and driven by one host
+process (rank 0); its Transfer vertices are NVLink peer copies (no NCCL on the
+data path). Under torchrun the other ranks only join the barriers. Same total
+work at every N ("scaling": "strong"). `--mode replicas` instead runs one
+single-GPU memgraph per rank (weak scaling).
+
+--impl reference: the reference has no tensor executor (its run API is an
+abstract-time simulator), so the CPU implementation timed is the
+oracle port (oracle/, numpy + BLAS on all host cores) executing a memgraph
+planned by the UNMODIFIED reference planner (oracle/_ref/_memplan), one
+decoder layer per step (the actually-timed sample; full-depth projection in a
+named field). See DESIGN.md §6.
 """
 from __future__ import annotations
 
@@ -42,7 +64,7 @@ def peaks():
 
 
 class Clocks:
-    """Samples nvidia-smi clocks + throttle reasons during the timed region."""
+    """Samples nvidia-smi clocks + throttle reasons of `indices` during the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -50,15 +72,15 @@ class Clocks:
 
     PERIOD_MS = 100
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, indices):
+        self.indices = {int(i) for i in (indices if isinstance(indices, (list, tuple, set)) else [indices])}
         self.proc = None
         self.lines = []
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", str(self.PERIOD_MS)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -86,6 +108,8 @@ class Clocks:
             if len(f) < 8:
                 continue
             try:
+                if int(f[0]) not in self.indices:
+                    continue
                 sm.append(float(f[1]))
                 mx = max(mx, float(f[2]))
             except ValueError:
@@ -94,10 +118,14 @@ class Clocks:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "gpus": sorted(self.indices)}
 
 
-def dist_setup():
+def dist_setup(mode):
+    """torchrun env -> (world, rank, local). The data path has no collective:
+    in tp mode (one process drives every GPU) the process group only carries
+    barriers and the max-over-ranks timing, so it uses gloo and the idle ranks
+    never touch a GPU."""
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -106,7 +134,7 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
 
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = "nccl" if (torch.cuda.is_available() and mode == "replicas") else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend, init_method="env://")
@@ -128,7 +156,8 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    on_gpu = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -162,55 +191,107 @@ def device_inputs_one(t, seed: int, device):
     elif kind == "normal":
         x = torch.randn(n, generator=gen, device=device, dtype=torch.float32).mul_(float(t.init[1]))
         x = x.to(torch.bfloat16) if t.dtype == "bf16" else x
+    elif kind == "ones":
+        x = torch.ones(n, device=device, dtype=torch.float32)
+        x = x.to(torch.bfloat16) if t.dtype == "bf16" else x
     else:
         x = torch.empty(n, device=device, dtype=torch.float32).uniform_(t.init[1], t.init[2], generator=gen)
         x = x.to(torch.bfloat16) if t.dtype == "bf16" else x
     return {t.id: x}
 
 
-def device_inputs(g, seed: int, device):
-    """Synthetic inputs generated on the GPU (random-init weights ~N(0, 0.02),
-    token ids U[0, vocab), RoPE table) — torch is only the data source."""
+def device_inputs(g, seed: int, device=None, devs=None):
+    """Synthetic inputs generated on the GPU of their memgraph device (random-init
+    weights ~N(0, 0.02), token ids U[0, vocab), RoPE table) — torch is only the
+    data source. `devs[d]` = CUDA ordinal of memgraph device d."""
+    import torch
+
     out = {}
     for t in g.inputs():
-        out.update(device_inputs_one(t, seed, device))
+        dv = device if devs is None else torch.device("cuda", devs[t.device])
+        out.update(device_inputs_one(t, seed, dv))
     return out
 
 
-def measure_pcie(device) -> float:
-    """Pinned H2D bandwidth (GB/s) of this GPU, 1 GiB copies, best of 5."""
+def load_inputs(ex, g, seed, devs):
+    """Generates each input on its GPU, hands it to the executor, drops it
+    (the device never holds more than the arenas + staging + one tensor)."""
+    import torch
+
+    for t in g.inputs():
+        for k, v in device_inputs_one(t, seed, torch.device("cuda", devs[t.device])).items():
+            ex.set_input(k, v)
+
+
+def measure_pcie(device, direction="h2d") -> float:
+    """Pinned H2D (or D2H) bandwidth (GB/s) of this GPU, 1 GiB copies, best of 5."""
     import torch
 
     n = 1 << 30
     h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(n, dtype=torch.uint8, device=device)
     best = 0.0
-    for _ in range(5):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        d.copy_(h, non_blocking=True)
-        e.record()
-        e.synchronize()
-        best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
+    with torch.cuda.device(device):
+        for _ in range(5):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            if direction == "h2d":
+                d.copy_(h, non_blocking=True)
+            else:
+                h.copy_(d, non_blocking=True)
+            e.record()
+            e.synchronize()
+            best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
     del h, d
     return best
 
 
-def untimed_steps(ex, steps: int, policy: str = "event-driven", tie_break: str = "fifo") -> list[float]:
-    """Per-step device time (s) of `steps` untimed executor runs (timing-free
-    completion events), each bracketed by CUDA events on the current stream;
-    run back to back so the GPU stays in its sustained power state."""
+def measure_p2p(a: int, b: int) -> float | None:
+    """Peer copy bandwidth GPU a -> GPU b (GB/s), 1 GiB, best of 3."""
     import torch
 
-    out = []
-    for i in range(steps):
+    if a == b:
+        return None
+    n = 1 << 30
+    x = torch.empty(n, dtype=torch.uint8, device=f"cuda:{a}")
+    y = torch.empty(n, dtype=torch.uint8, device=f"cuda:{b}")
+    best = 0.0
+    with torch.cuda.device(b):
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            y.copy_(x, non_blocking=True)
+            e.record()
+            e.synchronize()
+            best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)
+    return best
+
+
+def sync_all(devs):
+    import torch
+
+    for d in sorted(set(devs)):
+        torch.cuda.synchronize(d)
+
+
+def timed_runs(ex, steps, devs, after=None):
+    """`steps` back-to-back untimed executor runs (timing-free completion
+    events) bracketed by CUDA events on the first GPU's current stream, with a
+    synchronize of every GPU on both sides (run() itself returns only after
+    every device drained). Returns seconds."""
+    import torch
+
+    sync_all(devs)
+    with torch.cuda.device(devs[0]):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        ex.run(policy, tie_break, i, trace=False)
+        for _ in range(steps):
+            ex.run(trace=False)
+            if after:
+                after()
         e.record()
-        torch.cuda.synchronize()
-        out.append(s.elapsed_time(e) * 1e-3)
-    return out
+    sync_all(devs)
+    return s.elapsed_time(e) * 1e-3
 
 
 # ----------------------------------------------------------------- roofline ---
@@ -254,8 +335,9 @@ def roofline_from_trace(g, trace, peak_tflops):
     burst = peaks().get("bf16_tflops")
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": round(ach / peak_tflops, 4), "peak_kind": "sustained (MEASURED_PEAKS bf16_tflops_sustained)",
-            "frac_of_burst_peak": round(ach / burst, 4) if burst else None, "traffic": traffic, "traffic_unit": "bytes/launch (DRAM read+write)",
-            "traffic_source": src, "algorithmic_bytes_per_launch": round(alg_bytes / max(1, launches)),
+            "frac_of_burst_peak": round(ach / burst, 4) if burst else None, "traffic": traffic,
+            "traffic_unit": "bytes/launch (DRAM read+write)", "traffic_source": src,
+            "algorithmic_bytes_per_launch": round(alg_bytes / max(1, launches)),
             "kernel": "gemm_tcgen05 (all GEMM tasks)",
             "launches_per_step": launches, "algorithmic_flops_per_step": fl,
             "gemm_device_s_per_step": round(dur, 6), "gemm_classes": by_class}, by_type
@@ -272,256 +354,366 @@ def gemm_traffic():
     """DRAM bytes per GEMM launch from the committed `ncu --set full` capture
     of one layer's four GEMM classes (each class is 1/4 of the step's GEMM
     launches, so the plain mean is the per-launch average)."""
-    p = os.path.join(ROOT, "profiles", "r1_ncu_gemm.json")
-    try:
-        ls = json.load(open(p))["launches"]
-        return round(sum(x["dram_bytes"] for x in ls) / len(ls)), "profiles/r1_ncu_gemm.json"
-    except Exception:
-        return None, None
+    for name in ("r2_ncu_gemm.json", "r1_ncu_gemm.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        try:
+            ls = json.load(open(p))["launches"]
+            return round(sum(x["dram_bytes"] for x in ls) / len(ls)), f"profiles/{name}"
+        except Exception:
+            continue
+    return None, None
+
+
+def input_h2d_bytes_per_device(g, mg_json, D):
+    """Per memgraph device: bytes an e2e step moves host->device (inputs, minus
+    embedding tables gathered zero-copy, plus the rows gathered, plus reloads)."""
+    m = json.loads(mg_json)
+    zc = {op_args[1] for v in g.vertices if (op := v.get("op")) and op["type"] == "embedding"
+          for op_args in [op["args"]]}
+    other = {a for v in g.vertices if (op := v.get("op")) and op["type"] != "embedding" for a in op["args"]}
+    zc -= other
+    out = [0] * D
+    for t in g.inputs():
+        out[t.device] += t.nbytes if t.id not in zc else 0
+    for v in g.vertices:
+        if (op := v.get("op")) and op["type"] == "embedding" and op["args"][1] in zc:
+            out[v["device"]] += op["seq"] * op["dim"] * 2
+    for v in m["vertices"]:
+        if v["op"] == "reload":
+            out[v["device"]] += v["size"]
+    return out
+
+
+# ------------------------------------------------------------------ config ---
+def bench_config(args, n_gpus):
+    """The workload, identical in both arms' JSON lines."""
+    layers = args.layers or 32
+    tp = n_gpus > 1 and args.mode == "tp"
+    return {"workload": "llama7b_prefill_seq4096_cap16GiB" + (f"_tp{n_gpus}" if tp else ""),
+            "model": "LLaMA-7B (random init)", "global_batch": 1 if tp else n_gpus, "seq_len": args.seq,
+            "layers": layers, "hbm_cap_bytes_per_gpu": int(args.cap_gib * (1 << 30)), "alloc_horizon": args.horizon,
+            "parallelism": (f"tp{n_gpus}: one memgraph partitioned over {n_gpus} GPUs (Transfer vertices = NVLink "
+                            "peer copies), one host process" if tp else
+                            ("1 GPU" if n_gpus == 1 else f"replicas x{n_gpus} (one memgraph per GPU)")),
+            "inputs": "value: weights in HBM staging buffers, D2D-copied into their capped-arena placements by "
+                      "the Input vertices every step; e2e: weights in pinned host memory, H2D every step",
+            "l2": "inputs larger than L2 (13.5 GB of weights stream through every step)"}
+
+
+def make_graph(args, n_gpus, layers=None):
+    from paper_2405_16283_b200 import workloads as W
+
+    cfg = W.LLAMA_7B if not args.quick else W.LlamaConfig(dim=1024, layers=4, heads=8, ffn=2816, vocab=4000)
+    L = layers if layers is not None else args.layers
+    if n_gpus > 1 and args.mode == "tp":
+        return cfg, W.llama_prefill_tp(cfg, args.seq, n_gpus, layers=L)
+    return cfg, W.llama_prefill(cfg, args.seq, layers=L)
 
 
 # --------------------------------------------------------------- CPU sample ---
-def cpu_sample(cfg, seq, layers_full):
+def cpu_sample(args, n_gpus, plan_with_reference: bool):
     """The CPU oracle executor (oracle/, numpy + BLAS on all host cores) on a
-    bounded sample: one decoder layer of the same model at the same seq
-    (+ embedding and head), extrapolated to the full depth."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    bounded sample: one decoder layer of the same graph (+ embedding and head),
+    planned at the same cap (by the reference planner in the reference arm).
+    Returns (seconds actually timed, layers of the full model)."""
     from oracle.cpu_executor import CpuExecutor
     from paper_2405_16283_b200 import workloads as W
 
-    g = W.llama_prefill(cfg, seq, layers=1)
-    mg, _ = W.plan(g, 16 << 30)  # the bench cap; numpy arenas are calloc-backed (lazy)
-    ex = CpuExecutor(mg, g.to_json())
+    cfg, g = make_graph(args, n_gpus, layers=1)
+    caps = [int(args.cap_gib * (1 << 30))] * g.device_count
+    if plan_with_reference:
+        mg, _ = reference_memplan().build_memgraph(g.to_json(), caps, mode="byte", alloc_horizon=args.horizon)
+    else:
+        mg, _ = W.plan(g, caps, alloc_horizon=args.horizon)
+    ex = CpuExecutor(mg, g.to_json())  # numpy arenas are calloc-backed (lazy)
     for t in g.inputs():
         ex.set_input(t.id, W.make_input(t, 0))
     t0 = time.perf_counter()
     ex.run(outputs=g.outputs())
-    dt = time.perf_counter() - t0
-    est_step = dt * layers_full  # embedding/head are negligible next to a layer
-    return {"value": round(seq / est_step, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"1 of {layers_full} decoder layers (+embed/head) of LLaMA-7B at seq {seq} on the numpy "
-                      f"oracle executor ({dt:.1f}s), step time extrapolated x{layers_full}",
-            "sample_s": round(dt, 2)}
+    return time.perf_counter() - t0, (args.layers or cfg.layers)
 
 
-# ------------------------------------------------------------------- arms ---
-def reference_planner_leg(g, cap, horizon):
-    """The unmodified reference (oracle/_ref, built from /root/reference by
-    oracle/Makefile) on the same taskgraph: build_memgraph + simulate, timed on
-    one host core, and its memgraph byte-compared with ours (live parity)."""
+def reference_memplan():
     ref_dir = os.path.join(ROOT, "oracle", "_ref")
-    if not os.path.isdir(ref_dir):
-        return {"unavailable": "oracle/_ref not built (needs /root/reference at build time)"}
     sys.path.insert(0, ref_dir)
+    import _memplan  # the unmodified reference build (oracle/Makefile)
+
+    return _memplan
+
+
+def planner_parity(g, caps, horizon):
+    """Live check inside our arm's cpu_baseline leg: our memgraph is
+    byte-identical to the unmodified reference planner's on the bench graph."""
     try:
-        import _memplan
+        ref = reference_memplan()
     except ImportError as e:
-        return {"unavailable": f"oracle/_ref/_memplan not importable: {e}"}
+        return {"unavailable": f"oracle/_ref not importable: {e}"}
     from paper_2405_16283_b200 import memplan
 
     tg = g.to_json()
     t0 = time.perf_counter()
-    ref_mg, ref_stats = _memplan.build_memgraph(tg, [cap], mode="byte", alloc_horizon=horizon)
+    a = ref.build_memgraph(tg, caps, mode="byte", alloc_horizon=horizon)
     t1 = time.perf_counter()
-    ref_trace = _memplan.simulate(ref_mg)
+    b = memplan.build_memgraph(tg, caps, mode="byte", alloc_horizon=horizon)
     t2 = time.perf_counter()
-    ours_mg, _ = memplan.build_memgraph(tg, [cap], mode="byte", alloc_horizon=horizon)
-    t3 = time.perf_counter()
-    ours_trace = memplan.simulate(ours_mg)
-    t4 = time.perf_counter()
-    return {"build_memgraph_s": round(t1 - t0, 4), "simulate_s": round(t2 - t1, 4),
-            "ours_build_memgraph_s": round(t3 - t2, 4), "ours_simulate_s": round(t4 - t3, 4),
-            "vertices": len(json.loads(ref_mg)["vertices"]), "memgraph_bytes_identical": ref_mg == ours_mg,
-            "simulate_trace_identical": ref_trace == ours_trace, "cores": 1}
+    return {"memgraph_bytes_identical": a == b, "reference_build_memgraph_s": round(t1 - t0, 4),
+            "ours_build_memgraph_s": round(t2 - t1, 4), "vertices": len(json.loads(a[0])["vertices"])}
 
 
+# ------------------------------------------------------------- reference arm ---
 def run_reference(args, world, rank):
-    """The reference arm: the reference has no tensor executor (its run API is
-    an abstract-time simulator), so the CPU implementation timed
-    is our oracle port executing the same memgraph semantics on host cores."""
+    """The reference arm on host cores: the oracle port executing a memgraph
+    planned by the unmodified reference planner; one decoder layer per step."""
     if rank != 0:
         return
+    n = max(world, args.gpus) if args.mode == "tp" else world
     from paper_2405_16283_b200 import workloads as W
 
-    cfg = W.LLAMA_7B
-    for _ in range(args.warmup):  # warm-up: small sample (numpy/BLAS init)
-        small = W.LlamaConfig(dim=512, layers=1, heads=4, ffn=1024, vocab=1000)
-        cpu_sample(small, 256, 1)
-    vals = []
+    small = argparse.Namespace(**{**vars(args), "quick": True, "seq": 256, "layers": 1})
+    for _ in range(args.warmup):  # warm-up: a small sample (numpy/BLAS init)
+        cpu_sample(small, 1, True)
     samples = []
     for _ in range(args.steps):
-        s = cpu_sample(cfg, args.seq, cfg.layers)
-        vals.append(s["value"])
-        samples.append(s["sample_s"])
-    v = statistics.mean(vals)
-    g7 = W.llama_prefill(cfg, args.seq, layers=args.layers)
-    planner = reference_planner_leg(g7, int(args.cap_gib * (1 << 30)), args.horizon)
-    line = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(args.seq / v * 1e3, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": "llama7b_prefill_seq4096_cap16GiB", "seq_len": args.seq,
-                                            "global_batch": 1, "cpu_sample": "1 decoder layer per step"},
-            "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                             "sample": "per step: 1 of 32 decoder layers at seq 4096, extrapolated x32; "
-                                       f"layer times {samples}"},
-            "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "reference_planner": planner}
+        dt, L = cpu_sample(args, n, True)
+        samples.append(dt)
+    step_s = statistics.mean(samples)
+    value = args.seq / (step_s * L)  # tokens/s of the full model at this per-layer rate
+    # the reference planner itself on the full bench graph (single host core)
+    ref = reference_memplan()
+    _, g = make_graph(args, n)
+    caps = [int(args.cap_gib * (1 << 30))] * g.device_count
+    t0 = time.perf_counter()
+    mg, _ = ref.build_memgraph(g.to_json(), caps, mode="byte", alloc_horizon=args.horizon)
+    t1 = time.perf_counter()
+    ref.simulate(mg)
+    t2 = time.perf_counter()
+    sample = (f"per step: 1 of {L} decoder layers (+embedding, head) of the bench graph at seq {args.seq}, planned "
+              "by oracle/_ref, executed by the numpy oracle port")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
+            "higher_is_better": True, "scaling": "strong" if (n > 1 and args.mode == "tp") else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": bench_config(args, n),
+            "step_unit": f"1 of {L} decoder layers (value = seq / (ms_per_step x {L}))",
+            "projected_full_step_s": round(step_s * L, 2),
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": sample, "layer_s": [round(x, 2) for x in samples]},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_planner": {"build_memgraph_s": round(t1 - t0, 4), "simulate_s": round(t2 - t1, 4),
+                                  "vertices": len(json.loads(mg)["vertices"]), "cores": 1}}
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------ offload leg ---
+def offload_leg(args, dev):
+    """Config 4 (LLaMA-7B LoRA step, seq 4096, activation offload under the
+    16 GiB cap, frozen weights cold in host RAM) executed on one GPU, plus the
+    hardware event-driven vs fixed-order comparison on config 4 and on a
+    config-5 blockwise-attention plan."""
+    import torch
+
+    from paper_2405_16283_b200 import workloads as W
+    from paper_2405_16283_b200.executor import Executor
+
+    pk = peaks()
+    out = {}
+    g = W.llama_lora_step(W.LLAMA_7B, args.seq)
+    mg, st = W.plan(g, int(args.cap_gib * (1 << 30)), alloc_horizon="lazy")
+    m = json.loads(mg)
+    off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
+    rel = sum(v["size"] for v in m["vertices"] if v["op"] == "reload")
+    with Executor(mg, g.to_json(), {"devices": [dev], "input_residency": "host"}) as ex:
+        load_inputs(ex, g, 0, [dev])
+        ex.run(trace=False)
+        steps = max(1, args.offload_steps)
+        t = timed_runs(ex, steps, [dev]) / steps
+        ex.run()  # one traced step: exposed transfer
+        s = ex.stats()
+        pcie_h2d, pcie_d2h = measure_pcie(torch.device("cuda", dev)), measure_pcie(torch.device("cuda", dev), "d2h")
+        roof = max(s["flops"] / (pk["bf16_tflops_sustained"] * 1e12), s["h2d_bytes"] / (pcie_h2d * 1e9),
+                   s["d2h_bytes"] / (pcie_d2h * 1e9))
+        out["config4_lora_step"] = {
+            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy", "memgraph_vertices": len(m["vertices"]),
+            "offloads": st["offloads"], "reloads": st["reloads"], "offload_bytes_planned": off,
+            "reload_bytes_planned": rel, "step_s": round(t, 4), "tokens_per_s": round(args.seq / t, 1),
+            "h2d_bytes": s["h2d_bytes"], "d2h_bytes": s["d2h_bytes"],
+            "d2h_elided_bytes": s["d2h_elided_bytes"],
+            "achieved_h2d_gbs": round(s["h2d_bytes"] / t / 1e9, 1), "achieved_d2h_gbs": round(s["d2h_bytes"] / t / 1e9, 1),
+            "pcie_h2d_gbs_measured": round(pcie_h2d, 1), "pcie_d2h_gbs_measured": round(pcie_d2h, 1),
+            "exposed_transfer_s": round(s["exposed_transfer_s"], 4), "flops": s["flops"],
+            "roofline_s": round(roof, 4), "frac_of_roofline": round(roof / t, 4),
+            "roofline": "max(FLOP / sustained bf16 peak, H2D bytes / PCIe H2D, D2H bytes / PCIe D2H)"}
+        if args.policy_trials > 0:
+            out["config4_lora_step"]["compare_policies"] = json.loads(ex.compare_policies(args.policy_trials, 0))
+    if args.policy_trials > 0:
+        g5 = W.blockwise_attention(65536, 8, 128, 4096, lag=2)
+        mg5, st5 = W.plan(g5, 4 << 30, alloc_horizon="lazy")
+        with Executor(mg5, g5.to_json(), {"devices": [dev], "input_residency": "host"}) as ex:
+            load_inputs(ex, g5, 0, [dev])
+            cmp5 = json.loads(ex.compare_policies(args.policy_trials, 0))
+        out["config5_blockwise_compare_policies"] = {
+            "workload": "blockwise_attention_seq65536_h8_tile4096_lag2_cap4GiB_lazy",
+            "memgraph_vertices": len(json.loads(mg5)["vertices"]), "offloads": st5["offloads"], **cmp5}
+    return out
+
+
+# ------------------------------------------------------------------ our arm ---
 def run_ours(args, world, rank, local):
     import torch
 
     from paper_2405_16283_b200 import workloads as W
     from paper_2405_16283_b200.executor import Executor
 
-    dev = torch.device("cuda", local)
-    cfg = W.LLAMA_7B if not args.quick else W.LlamaConfig(dim=1024, layers=4, heads=8, ffn=2816, vocab=4000)
+    tp = args.mode == "tp"
+    n = max(world, args.gpus) if tp else world
+    if tp and world > 1:  # rank 0 drives every GPU; the others wait for it at one barrier
+        if rank == 0:
+            try:
+                run_ours_on(args, 1, 0, local, n, tp)
+            finally:
+                barrier(world)
+        else:
+            barrier(world)
+        return
+    run_ours_on(args, world, rank, local, n, tp)
+
+
+def run_ours_on(args, world, rank, local, n, tp):
+    """`world` here counts the ranks that run executors (1 in tp mode)."""
+    import torch
+
+    from paper_2405_16283_b200 import workloads as W
+    from paper_2405_16283_b200.executor import Executor
+
+    ngpu = torch.cuda.device_count()
+    if tp and n > ngpu and not args.emulate:
+        raise SystemExit(f"--gpus {n} needs {n} visible GPUs, found {ngpu} (use --emulate to map them onto GPU 0)")
+    devs = ([0] * n if args.emulate else list(range(n))) if tp else [local]
+    dev0 = torch.device("cuda", devs[0])
     t0 = time.perf_counter()
-    g = W.llama_prefill(cfg, args.seq, layers=args.layers)
-    cap = int(args.cap_gib * (1 << 30))
-    mg, stats = W.plan(g, cap, alloc_horizon=args.horizon)
+    cfg, g = make_graph(args, n)
+    caps = [int(args.cap_gib * (1 << 30))] * g.device_count
+    mg, stats = W.plan(g, caps, alloc_horizon=args.horizon)
     plan_s = time.perf_counter() - t0
     tg = g.to_json()
     (logits,) = g.outputs()
     logits_bytes = g.tensors[logits].nbytes
-    in_bytes = sum(t.nbytes for t in g.inputs())
     pk = peaks()
+    exec_cfg = {"devices": devs, "streams_per_device": args.streams, "compute_tokens": args.compute_tokens}
 
-    inputs = device_inputs(g, seed=0, device=dev)
-    exec_cfg = {"devices": [local], "streams_per_device": args.streams, "compute_tokens": args.compute_tokens}
-
-    # ---- value: inputs resident in HBM (D2D materialisation) ----
-    exv = Executor(mg, tg, {**exec_cfg, "input_residency": "device"})
-    for vid, t in inputs.items():
-        exv.set_input(vid, t)
+    # ---- value: weights resident in HBM, materialised into the capped arena each step ----
+    exv = Executor(mg, tg, {**exec_cfg, "input_residency": "device", "device_inputs": "copy"})
+    load_inputs(exv, g, 0, devs)
     for _ in range(args.warmup):
         exv.run(trace=False)
-    torch.cuda.synchronize()
+    sync_all(devs)
     barrier(world)
-    torch.cuda.synchronize()
-    makespans = []
-    with Clocks(local) as clk:
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for _ in range(args.steps):
-            exv.run(trace=False)  # timing-free completion events, no host trace work in the loop
-        e.record()
-        # one more step, back to back with the timed ones (same power/clock state; an idle gap
-        # first would let the GPU boost), with per-vertex timestamps for the roofline and the
-        # per-op breakdown — not part of the timed region
+    with Clocks(sorted(set(devs))) as clk:
+        t_value = timed_runs(exv, args.steps, devs)
+        # one more step, back to back with the timed ones (same power/clock state), with
+        # per-vertex timestamps for the roofline and the per-op breakdown — not timed
         last = json.loads(exv.run())
-        torch.cuda.synchronize()
+        sync_all(devs)
     barrier(world)
-    t_value = max_over_ranks(s.elapsed_time(e) * 1e-3, world)
+    t_value = max_over_ranks(t_value, world)
     st_v = exv.stats()
-    makespans.append(last["makespan"])
+    exv.run(trace=False)
+    launches = exv.stats()["kernel_launches"]
     exv.close()
     del exv
 
-    # ---- the same, but every Input vertex D2D-copied into its arena placement ----
-    # (weights resident in HBM outside the cap, materialised into the capped
-    # arena each step instead of being read in place)
-    exc = Executor(mg, tg, {**exec_cfg, "input_residency": "device", "device_inputs": "copy"})
-    for vid, t in inputs.items():
-        exc.set_input(vid, t)
+    # ---- compute ceiling: Input vertices aliased to the staging buffers (weights outside the cap) ----
+    exa = Executor(mg, tg, {**exec_cfg, "input_residency": "device"})
+    load_inputs(exa, g, 0, devs)
     for _ in range(args.warmup):
-        exc.run(trace=False)
-    torch.cuda.synchronize()
-    barrier(world)
-    torch.cuda.synchronize()
-    s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s3.record()
-    for _ in range(args.steps):
-        exc.run(trace=False)
-    e3.record()
-    torch.cuda.synchronize()
-    barrier(world)
-    t_copy = max_over_ranks(s3.elapsed_time(e3) * 1e-3, world)
-    st_c = exc.stats()
-    exc.close()
-    del exc
+        exa.run(trace=False)
+    t_alias = timed_runs(exa, args.steps, devs)
+    exa.run()
+    st_a = exa.stats()
+    exa.close()
+    del exa
+    torch.cuda.empty_cache()
 
     # ---- e2e: weights cold in pinned host memory, logits read back ----
     exe = Executor(mg, tg, {**exec_cfg, "input_residency": "host"})
-    for vid, t in inputs.items():
-        exe.set_input(vid, t)
-    del inputs
-    torch.cuda.empty_cache()
+    load_inputs(exe, g, 0, devs)
+    fetch = lambda: exe.get_output(logits, logits_bytes)  # noqa: E731
     for _ in range(max(1, args.warmup)):
         exe.run(trace=False)
-        exe.get_output(logits, logits_bytes)
-    torch.cuda.synchronize()
+        fetch()
+    sync_all(devs)
     barrier(world)
-    torch.cuda.synchronize()
-    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s2.record()
-    for _ in range(args.steps):
-        exe.run(trace=False)
-        exe.get_output(logits, logits_bytes)
-    e2.record()
-    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(timed_runs(exe, args.steps, devs, after=fetch), world)
     barrier(world)
-    t_e2e = max_over_ranks(s2.elapsed_time(e2) * 1e-3, world)
     exe.run()  # one traced step fills the exposed-transfer stats (timing events)
-    exe.get_output(logits, logits_bytes)
+    fetch()
     st_e = exe.stats()
     exe.close()
 
     if rank != 0:
         return
-    pcie = measure_pcie(dev)
-    tokens = args.seq * world * args.steps
+    pcie = measure_pcie(dev0)
+    nvlink = measure_p2p(devs[0], devs[1]) if len(set(devs)) > 1 else None
+    tokens = args.seq * (1 if tp else world) * args.steps
     value = tokens / t_value
     e2e = tokens / t_e2e
     roof, by_type = roofline_from_trace(g, last, pk["bf16_tflops_sustained"])
-    flops = W.prefill_flops(cfg, args.seq, args.layers)
-    step_compute = flops / (pk["bf16_tflops_sustained"] * 1e12)
-    h2d_step = st_e["h2d_bytes"] + st_e.get("zero_copy_bytes", 0)  # copies + rows gathered over PCIe
-    step_pcie = h2d_step / (pcie * 1e9)
+    flops = (W.prefill_flops(cfg, args.seq, args.layers) if not tp else st_v["flops"])
+    gpus = len(set(devs))
+    step_compute = flops / (gpus * pk["bf16_tflops_sustained"] * 1e12)
+    h2d_dev = input_h2d_bytes_per_device(g, mg, g.device_count)
+    step_pcie = max(h2d_dev) / (pcie * 1e9) if gpus == g.device_count else sum(h2d_dev) / (pcie * 1e9)
+    step_nvlink = (st_e["p2p_bytes"] / gpus / (nvlink * 1e9)) if nvlink else 0.0
     e2e_step = t_e2e / args.steps
+    h2d_step = st_e["h2d_bytes"] + st_e.get("zero_copy_bytes", 0)  # copies + rows gathered over PCIe
     line = {
-        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_value / args.steps * 1e3, 2), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "llama7b_prefill_seq4096_cap16GiB" if not args.quick else "llama_quick",
-                   "model": "LLaMA-7B (random init)" if not args.quick else "quick", "global_batch": world,
-                   "seq_len": args.seq, "layers": args.layers or cfg.layers, "hbm_cap_bytes": cap,
-                   "alloc_horizon": args.horizon, "parallelism": f"replicas x{world} (memgraph per GPU)",
-                   "l2": "inputs larger than L2 (13.5 GB of weights stream through every step)",
-                   "memgraph": {"vertices": len(json.loads(mg)["vertices"]), **stats}, "plan_s": round(plan_s, 2),
-                   "streams_per_device": args.streams, "compute_tokens": args.compute_tokens},
+        "scaling": "strong" if (tp and n > 1) else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": bench_config(args, n),
+        "plan": {"memgraph_vertices": len(json.loads(mg)["vertices"]), **stats, "plan_s": round(plan_s, 2),
+                 "devices": devs, "streams_per_device": args.streams, "compute_tokens": args.compute_tokens},
         "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d_step,
                 "zero_copy_gather_bytes_per_step": st_e.get("zero_copy_bytes", 0),
-                "d2h_bytes_per_step": logits_bytes + st_e["d2h_bytes"], "ms_per_step": round(e2e_step * 1e3, 2),
+                "d2h_bytes_per_step": logits_bytes + st_e["d2h_bytes"], "p2p_bytes_per_step": st_e["p2p_bytes"],
+                "ms_per_step": round(e2e_step * 1e3, 2),
                 "exposed_transfer_s": round(st_e["exposed_transfer_s"], 4),
                 "exposed_transfer_gpu_s": round(st_e.get("exposed_transfer_gpu_s", st_e["exposed_transfer_s"]), 4),
                 "pcie_h2d_gbs_measured": round(pcie, 1),
                 "achieved_h2d_gbs": round(h2d_step / e2e_step / 1e9, 1)},
-        "gpu_launches": st_v["kernel_launches"] * args.steps,
+        "gpu_launches": launches * args.steps,
         "roofline": roof,
         "step_roofline": {
-            "compute_s": round(step_compute, 5), "pcie_h2d_s": round(step_pcie, 5),
-            "bound": "pcie" if step_pcie > step_compute else "tensor",
+            "compute_s": round(step_compute, 5), "pcie_h2d_s": round(step_pcie, 5), "nvlink_s": round(step_nvlink, 5),
+            "bound": max((("tensor", step_compute), ("pcie", step_pcie), ("nvlink", step_nvlink)), key=lambda x: x[1])[0],
             "value_frac_of_compute_roofline": round(step_compute / (t_value / args.steps), 4),
-            "e2e_frac_of_step_roofline": round(max(step_compute, step_pcie) / e2e_step, 4)},
+            "e2e_frac_of_step_roofline": round(max(step_compute, step_pcie, step_nvlink) / e2e_step, 4),
+            "nvlink_gbs_measured": round(nvlink, 1) if nvlink else None},
         "device_time_by_op_s": {k: round(v, 5) for k, v in sorted(by_type.items(), key=lambda kv: -kv[1])},
-        "value_run": {"last_step_makespan_s": [round(x, 5) for x in makespans], "exposed_transfer_s":
-                      round(st_v["exposed_transfer_s"], 5), "d2d_input_bytes": st_v["d2d_bytes"],
-                      "inputs": "aliased in place (HBM staging copies outside the arena)",
+        "value_run": {"last_step_makespan_s": round(last["makespan"], 5), "d2d_input_bytes_per_step": st_v["d2d_bytes"],
+                      "p2p_bytes_per_step": st_v["p2p_bytes"], "exposed_transfer_s": round(st_v["exposed_transfer_s"], 5),
                       # host event loop of the traced step (A7): dispatch work vs waiting on completions
                       "host_dispatch_ms": round(st_v.get("host_dispatch_s", 0) * 1e3, 3),
                       "host_wait_ms": round(st_v.get("host_wait_s", 0) * 1e3, 3),
                       "host_dispatch_us_per_vertex": round(st_v.get("host_dispatch_s", 0) * 1e6 /
                                                            max(1, st_v["vertices"]), 2)},
-        "value_inputs_copied_into_arena": {"value": round(tokens / t_copy, 1), "unit": UNIT,
-                                           "ms_per_step": round(t_copy / args.steps * 1e3, 2),
-                                           "d2d_input_bytes_per_step": st_c["d2d_bytes"]},
+        "compute_ceiling": {"value": round(tokens / t_alias, 1), "unit": UNIT,
+                            "ms_per_step": round(t_alias / args.steps * 1e3, 2),
+                            "inputs": "aliased in place: weights read from HBM staging buffers OUTSIDE the capped "
+                                      "arena (zero-cost Input vertices, simulator.cpp:66-67); not a capped number",
+                            "host_dispatch_us_per_vertex": round(st_a.get("host_dispatch_s", 0) * 1e6 /
+                                                                 max(1, st_a["vertices"]), 2)},
         "clocks": clk.summary(),
         "peaks": {k: pk.get(k) for k in ("bf16_tflops", "bf16_tflops_sustained", "hbm_gbs")},
     }
-    if world == 1 and not args.no_cpu_baseline and not args.quick:
-        line["cpu_baseline"] = cpu_sample(cfg, args.seq, cfg.layers)
+    if not args.no_offload_leg and not args.quick:
+        line["offload"] = offload_leg(args, devs[0])
+    if n == 1 and not args.no_cpu_baseline and not args.quick:
+        dt, L = cpu_sample(args, 1, False)
+        line["cpu_baseline"] = {"value": round(args.seq / (dt * L), 2), "unit": UNIT, "cores": os.cpu_count(),
+                                "kind": "port", "sample": f"1 of {L} decoder layers (+embed/head) of LLaMA-7B at seq "
+                                f"{args.seq} on the numpy oracle executor ({dt:.1f}s), tokens/s at that per-layer rate",
+                                "sample_s": round(dt, 2)}
+        line["planner_parity"] = planner_parity(g, caps, args.horizon)
     print(json.dumps(line), flush=True)
 
 
@@ -531,16 +723,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="tp", choices=["tp", "replicas"],
+                    help="N>1: one TP memgraph over N GPUs (default) or one replica per rank")
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--cap-gib", type=float, default=16.0)
     ap.add_argument("--horizon", default="greedy", choices=["greedy", "lazy"])
     ap.add_argument("--streams", type=int, default=5)
     ap.add_argument("--compute-tokens", type=int, default=1)
+    ap.add_argument("--offload-steps", type=int, default=3)
+    ap.add_argument("--policy-trials", type=int, default=10)
+    ap.add_argument("--no-offload-leg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate", action="store_true", help="map every memgraph device onto GPU 0 (harness test)")
     ap.add_argument("--quick", action="store_true", help="small model for smoke-testing the harness")
     args = ap.parse_args()
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args.mode)
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

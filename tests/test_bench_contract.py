@@ -23,13 +23,32 @@ def test_roofline_from_trace_counts_gemm_flops_and_bytes():
     assert by_type["gemm"] == pytest.approx(1e-3 * len(gemms))
 
 
-def test_reference_planner_leg_is_byte_identical():
+def test_planner_parity_leg_is_byte_identical():
     if not os.path.isdir(os.path.join(bench.ROOT, "oracle", "_ref")):
         pytest.skip("oracle/_ref not built")
     cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=1024, vocab=1000)
     g = W.llama_prefill(cfg, 256)
-    leg = bench.reference_planner_leg(g, 64 << 20, "greedy")
+    leg = bench.planner_parity(g, [64 << 20], "greedy")
     if "unavailable" in leg:
         pytest.skip(leg["unavailable"])
-    assert leg["memgraph_bytes_identical"] and leg["simulate_trace_identical"]
+    assert leg["memgraph_bytes_identical"]
     assert leg["vertices"] == len(json.loads(W.plan(g, 64 << 20)[0])["vertices"])
+
+
+def test_both_arms_share_the_config():
+    import argparse
+    a = argparse.Namespace(layers=None, seq=4096, cap_gib=16.0, horizon="greedy", mode="tp", quick=False)
+    c1, c8 = bench.bench_config(a, 1), bench.bench_config(a, 8)
+    assert c1["workload"] == "llama7b_prefill_seq4096_cap16GiB" and c1["layers"] == 32
+    assert c8["workload"].endswith("_tp8") and c8["global_batch"] == 1
+    _, g = bench.make_graph(argparse.Namespace(**{**vars(a), "seq": 256, "layers": 1}), 2)
+    assert g.device_count == 2  # N > 1: the partitioned (TP) memgraph
+
+
+def test_input_h2d_bytes_per_device():
+    cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=1024, vocab=1000)
+    g = W.llama_prefill_tp(cfg, 256, 2)
+    mg, _ = W.plan(g, [64 << 20] * 2)
+    per = bench.input_h2d_bytes_per_device(g, mg, 2)
+    tables = sum(t.nbytes for t in g.inputs() if t.name.startswith("tok_embeddings"))
+    assert sum(per) == sum(t.nbytes for t in g.inputs()) - tables + 2 * 256 * 512 * 2

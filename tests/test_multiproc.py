@@ -12,7 +12,7 @@ import os, sys, json
 sys.path.insert(0, %r)
 import torch.distributed as dist
 import bench
-world, rank, local = bench.dist_setup()
+world, rank, local = bench.dist_setup("replicas")
 t = bench.max_over_ranks(0.5 + rank, world)
 bench.barrier(world)
 # each rank plans its own replica of a small memgraph: identical plans
@@ -79,5 +79,46 @@ def test_reference_arm_two_ranks_rank0_only():
     d = json.loads(lines0[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
-    rp = d["reference_planner"]
-    assert rp["memgraph_bytes_identical"] is True and rp["simulate_trace_identical"] is True
+    # the arm's config is the one our arm prints (same workload: the TP graph over 2 GPUs)
+    assert d["config"]["workload"] == "llama7b_prefill_seq4096_cap16GiB_tp2" and d["scaling"] == "strong"
+    assert abs(d["ms_per_step"] - d["cpu_baseline"]["layer_s"][0] * 1e3) < 6  # the actually-timed sample
+    assert d["reference_planner"]["vertices"] > 0
+
+
+TP_WORKER = r"""
+import os, sys, json, time
+sys.path.insert(0, %r)
+import bench
+calls = []
+def fake(args, world, rank, local, n, tp):  # stands in for the GPU work of rank 0
+    time.sleep(1.0)
+    calls.append((world, rank, n, tp))
+bench.run_ours_on = fake
+args = bench.argparse.Namespace(mode="tp", gpus=2)
+world, rank, local = bench.dist_setup("tp")
+import torch.distributed as dist
+assert dist.get_backend() == "gloo"  # no NCCL: the idle rank never touches a GPU
+t0 = time.time()
+bench.run_ours(args, world, rank, local)
+print(json.dumps({"rank": rank, "calls": calls, "waited": time.time() - t0}))
+dist.destroy_process_group()
+"""
+
+
+def test_tp_mode_rank0_drives_all_gpus():
+    """tp mode under a 2-rank launch: rank 0 alone runs the partitioned memgraph
+    over both GPUs (one host process), rank 1 waits for it at one barrier."""
+    import json
+    port = free_port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, WORLD_SIZE="2", RANK=str(r), LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), CUDA_VISIBLE_DEVICES="")
+        procs.append(subprocess.Popen([sys.executable, "-c", TP_WORKER % ROOT], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=240) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e[-2000:]
+    res = {d["rank"]: d for d in (json.loads(o.strip().splitlines()[-1]) for o, _ in outs)}
+    assert res[0]["calls"] == [[1, 0, 2, True]] and res[1]["calls"] == []
+    assert res[1]["waited"] >= 0.9  # rank 1 left only after rank 0 finished
