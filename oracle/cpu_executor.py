@@ -96,10 +96,23 @@ class CpuExecutor:
         d, off, sz = self.place[mid]
         return arenas[d][off:off + sz]
 
-    def run(self, schedule: list[int] | None = None, outputs: list[int] | None = None) -> dict[int, bytes]:
+    def run(self, schedule: list[int] | None = None, outputs: list[int] | None = None,
+            record_reads: bool = False) -> dict[int, bytes]:
+        """Executes `schedule` (default: the build's total order). With
+        `record_reads`, self.reads[(reader, producer)] = digest of the bytes the
+        reader found in the producer's region when it ran: the byte-level
+        counterpart of TokenMachine's "reads region of P but finds ..."
+        check (verifier.cpp:316-349)."""
+        import hashlib
+
         arenas = [np.zeros(c, dtype=np.uint8) for c in self.caps]
         host: dict[int, np.ndarray] = {}
+        self.reads = {}
         for vid in schedule or self.mg["total_order"]:
+            if record_reads:
+                for src in self.data_in.get(vid, []):
+                    if src in self.place:
+                        self.reads[(vid, src)] = hashlib.sha1(self.region(arenas, src).tobytes()).hexdigest()
             v = self.verts[vid]
             if v.op == "input":
                 r = self.region(arenas, vid)

@@ -125,12 +125,41 @@ def input_key(t: Tensor) -> int:
     return zlib.crc32(t.name.encode())
 
 
+_CHUNK = 1 << 22  # elements per independently seeded chunk of a large input
+
+
+def _to_bf16(x: np.ndarray) -> np.ndarray:
+    u = x.view(np.uint32)
+    return ((u + (((u >> 16) & 1) + 0x7FFF)) >> 16).astype(np.uint16)
+
+
 def make_input(t: Tensor, seed: int) -> np.ndarray:
     """Deterministic synthetic bytes for an input tensor (host numpy), keyed by
-    the tensor name so equal-named inputs of different graphs agree."""
-    rng = np.random.default_rng([seed, input_key(t)])
+    the tensor name so equal-named inputs of different graphs agree. Random
+    tensors larger than one chunk are drawn chunk by chunk from independent
+    streams (seed, name key, chunk index) on a thread pool, so multi-GB weight
+    sets generate at memory speed; the values do not depend on the thread count."""
     n = int(np.prod(t.shape))
     kind = t.init[0]
+    if kind in ("normal", "uniform") and n > _CHUNK:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+
+        out = np.empty(n, dtype=np.uint16 if t.dtype == "bf16" else np.float32)
+
+        def fill(c):
+            lo, hi = c * _CHUNK, min(n, (c + 1) * _CHUNK)
+            rng = np.random.default_rng([seed, input_key(t), c])
+            if kind == "normal":
+                x = rng.standard_normal(hi - lo, dtype=np.float32) * np.float32(t.init[1])
+            else:
+                x = rng.uniform(t.init[1], t.init[2], size=hi - lo).astype(np.float32)
+            out[lo:hi] = _to_bf16(x) if t.dtype == "bf16" else x
+
+        with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as pool:
+            list(pool.map(fill, range((n + _CHUNK - 1) // _CHUNK)))
+        return out
+    rng = np.random.default_rng([seed, input_key(t)])
     if kind == "tokens":
         return rng.integers(0, t.init[1], size=n, dtype=np.int32)
     if kind == "rope":
@@ -160,8 +189,7 @@ def make_input(t: Tensor, seed: int) -> np.ndarray:
     else:
         raise ValueError(kind)
     if t.dtype == "bf16":
-        u = x.view(np.uint32)
-        return (((u + (((u >> 16) & 1) + 0x7FFF)) >> 16).astype(np.uint16))
+        return _to_bf16(x)
     return x
 
 
