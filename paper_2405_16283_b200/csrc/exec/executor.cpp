@@ -433,6 +433,8 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             g.ldc = op.ldc ? op.ldc : n_out;
             g.epi = op.epilogue;
             g.tile = op.tile;
+            g.split = op.split;
+            if (op.split && op.in_dtype != k::F32) throw Error("gemm precision 3xtf32 needs f32 inputs");
             if (op.epilogue == 1 && (op.N % 256 != 0 || op.args.size() != 2))
                 throw Error("gemm swiglu epilogue needs N % 256 == 0 and no residual");
             if (op.epilogue == 2 && (op.N != 3 * op.heads * 128 || op.args.size() != 3 || op.batch != 1))

@@ -134,6 +134,10 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
                 else if (tl == "wide") d.tile = 2;
                 else if (tl == "streamk") d.tile = 3;
                 else throw ParseError("gemm tile must be auto, narrow, wide or streamk");
+                const std::string pr = o.value("precision", std::string("tf32"));
+                if (pr == "tf32") d.split = 0;
+                else if (pr == "3xtf32") d.split = 1;
+                else throw ParseError("gemm precision must be tf32 or 3xtf32");
             }
             d.in_dtype = dtype_of(o.value("in_dtype", std::string("bf16")));
             d.out_dtype = dtype_of(o.value("out_dtype", std::string("bf16")));

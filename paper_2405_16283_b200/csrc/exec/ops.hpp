@@ -6,7 +6,9 @@
 //   {"type": "gemm", "args": [A, B (, R)], "M":..,"N":..,"K":.., "batch":1,
 //    "lda","ldb","ldc","sa","sb","sc", "a_off","b_off","c_off","r_off",
 //    "alpha":1.0, "in_dtype":"bf16"|"f32", "out_dtype":"bf16"|"f32",
-//    "causal":0|1|2, "epilogue": "none"|"swiglu", "tile": "auto"|"narrow"|"wide"}   swiglu: out [M, N/2] with
+//    "causal":0|1|2, "epilogue": "none"|"swiglu", "tile": "auto"|"narrow"|"wide",
+//    "precision": "tf32"|"3xtf32" (f32 inputs: one tf32 MMA, or the fp32-accurate
+//    3xTF32 split)}   swiglu: out [M, N/2] with
 //    out[:, 128b+j] = silu(C[:, 256b+j]) * C[:, 256b+128+j] (gate/up rows interleaved in 128-row blocks)
 //    "qkv_rope": args [x, wqkv, rope_table], "heads", hd 128, N = 3*heads*128 -> out packed
 //    [rope(q) (H,M,128) | rope(k) (H,M,128) | vᵀ (H,128,M)]
@@ -66,6 +68,7 @@ struct OpDesc {
     int causal = 0;
     int epilogue = 0;  // gemm: 0 none, 1 swiglu, 2 qkv_rope
     int tile = 0;      // gemm: CTA-pair tile choice, 0 auto, 1 narrow 256x256, 2 wide 512x256
+    int split = 0;     // gemm, f32 inputs: 0 tf32, 1 3xTF32
     int inverse = 0, tokens_out = 0;  // rope
     int in_dtype = 0, out_dtype = 0;  // k::DType
     double alpha = 1.0, eps = 1e-5, scale = 1.0;

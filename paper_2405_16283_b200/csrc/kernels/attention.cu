@@ -16,6 +16,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 
@@ -358,13 +359,13 @@ cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan) {
                            kHd);
     plan->path = ok ? 0 : 1;
     if (ok) {
-        static unsigned long long attr_set = 0;
+        static std::atomic<unsigned long long> attr_set{0};  // per CUDA device, any thread
         int dev = 0;
         cudaGetDevice(&dev);
-        if (!((attr_set >> dev) & 1ULL)) {
+        if (!((attr_set.load(std::memory_order_acquire) >> dev) & 1ULL)) {
             cudaFuncSetAttribute(attention_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
             cudaFuncSetAttribute(attention_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-            attr_set |= 1ULL << dev;
+            attr_set.fetch_or(1ULL << dev, std::memory_order_release);
         }
     }
     return cudaSuccess;

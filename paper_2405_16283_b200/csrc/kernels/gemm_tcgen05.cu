@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -69,6 +70,7 @@ struct Params {
     // [dp_tiles, dp_tiles + tail_units / tail_split).
     int tail_split, tail_units;
     int tma_c;  // 1: plain/SwiGLU epilogues store through smem staging + TMA (tensor map `tc`)
+    int split;  // 3xTF32 (1-CTA kernel, SPLIT = true)
     // Fused RMSNorm (consumer side): row m of the product is scaled by
     // rsqrt(sum_c rs_P[(rs_row0 + m)*rs_ld + c] / dim + eps), c in [0, rs_chunks),
     // summed in c order — the per-32-column sums of squares its producer wrote.
@@ -437,12 +439,48 @@ __device__ __forceinline__ void epilogue_qkv_rope(const Params& p, std::uint32_t
     }
 }
 
-template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+// 3xTF32 operand split (SPLIT kernels): x = hi + lo with hi = tf32(x)
+// (round to nearest, low 13 mantissa bits zero) and lo = tf32(x - hi); the
+// subtraction is exact, so hi·hi + hi·lo + lo·hi misses only lo·lo
+// (|lo| <= 2^-11 |x|) and fp32-input products come out fp32-accurate.
+__device__ __forceinline__ float tf32_rna(float x) {
+    std::uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+// Splits `bytes` of fp32 operands in place (hi) and into `lo` (same offsets,
+// so the same 128-byte swizzle applies to both buffers).
+__device__ __forceinline__ void split_operands(std::uint8_t* hi, std::uint8_t* lo, int bytes, int tid, int nthr) {
+#pragma unroll 4
+    for (int off = tid * 16; off < bytes; off += nthr * 16) {
+        float4 x = *reinterpret_cast<const float4*>(hi + off);
+        float4 h, l;
+        h.x = tf32_rna(x.x), l.x = tf32_rna(x.x - h.x);
+        h.y = tf32_rna(x.y), l.y = tf32_rna(x.y - h.y);
+        h.z = tf32_rna(x.z), l.z = tf32_rna(x.z - h.z);
+        h.w = tf32_rna(x.w), l.w = tf32_rna(x.w - h.w);
+        *reinterpret_cast<float4*>(hi + off) = h;
+        *reinterpret_cast<float4*>(lo + off) = l;
+    }
+}
+
+template <int BN, bool SPLIT>
+constexpr int stages_1cta() {
+    return SPLIT ? (BN >= 128 ? 3 : 4) : kStages;
+}
+template <int BN, bool SPLIT>
+constexpr int threads_1cta() {
+    return SPLIT ? kThreads + 128 : kThreads;  // + 4 splitter warps (6-9)
+}
+
+template <int BN, bool SPLIT>
+__global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Params p) {
     constexpr int A_BYTES = kBM * kAtom;
     constexpr int B_BYTES = BN * kAtom;
-    constexpr int STAGE = A_BYTES + B_BYTES;
+    constexpr int LOADED = A_BYTES + B_BYTES;               // TMA bytes per stage
+    constexpr int STAGE = SPLIT ? 2 * LOADED : LOADED;       // SPLIT: [A_hi | B_hi | A_lo | B_lo]
+    constexpr int kStages = stages_1cta<BN, SPLIT>();
     constexpr std::uint32_t TMEM_COLS = 2 * BN;
 
     extern __shared__ std::uint8_t smem_raw[];
@@ -453,7 +491,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + kStages * STAGE);
     const std::uint32_t full = smem_u32(bars), empty = full + 8 * kStages;
     const std::uint32_t tfull = empty + 8 * kStages, tempty = tfull + 16;
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 4);
+    const std::uint32_t splitb = tempty + 16;  // SPLIT: stage s operands split (4 splitter warps)
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + (SPLIT ? 3 : 2) * kStages + 4);
 
     pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -467,6 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             mbar_init(full + 8 * s, 1);
             mbar_init(empty + 8 * s, 1);
+            if (SPLIT) mbar_init(splitb + 8 * s, 4);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + 8 * a, 1);
@@ -498,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(empty + 8 * stage, phase ^ 1);
                     const std::uint32_t fb = full + 8 * stage;
-                    mbar_expect_tx(fb, STAGE);
+                    mbar_expect_tx(fb, LOADED);
                     const std::uint32_t sa = sbase + stage * STAGE;
                     tma_load_3d(sa, &ta, kb * bk, mb * kBM, p.a_batched ? b : 0, fb);
                     tma_load_3d(sa + A_BYTES, &tb, kb * bk, nb * BN, p.b_batched ? b : 0, fb);
@@ -526,13 +566,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const std::uint32_t d = tmem + acc * BN;
                 for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(full + 8 * stage, phase);
+                    mbar_wait((SPLIT ? splitb : full) + 8 * stage, phase);
                     tc_fence_after();
                     const std::uint32_t sa = sbase + stage * STAGE;
                     const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + A_BYTES);
+                    if (SPLIT) {
+                        const std::uint64_t al = sdesc(sa + LOADED), bl = sdesc(sa + LOADED + A_BYTES);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)  // 4 x 32 bytes of K per 128-byte block
-                        tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                        for (int k = 0; k < 4; ++k) {  // small terms first, then hi·hi
+                            tc_mma(d, al + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, true);
+                            tc_mma(d, ad + 2 * k, bl + 2 * k, idesc, 1u, true);
+                            tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, 1u, true);
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)  // 4 x 32 bytes of K per 128-byte block
+                            tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                    }
                     tc_commit(empty + 8 * stage);
                     if (++stage == kStages) {
                         stage = 0;
@@ -543,6 +593,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (SPLIT && warp >= 6) {
+        // Splitter warps: per stage, fp32 operands -> (hi in place, lo beside),
+        // then a generic->async proxy fence so the MMAs see the new bytes.
+        const int tid = threadIdx.x - 6 * 32;
+        int stage = 0;
+        std::uint32_t phase = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            int b, mb, nb;
+            decode(p, t, b, mb, nb);
+            if (tile_skipped(p, mb, nb, BN)) continue;
+            const int nk = kblocks(p, mb, bk);
+            for (int kb = 0; kb < nk; ++kb) {
+                mbar_wait(full + 8 * stage, phase);
+                std::uint8_t* st = smem + stage * STAGE;
+                split_operands(st, st + LOADED, LOADED, tid, 128);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(splitb + 8 * stage);
+                if (++stage == kStages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
@@ -1292,9 +1366,9 @@ bool encode_tma_3d_swz(CUtensorMap* map, const void* base, int esize, std::int64
 
 namespace {
 
-template <int BN>
+template <int BN, bool SPLIT = false>
 int smem_bytes() {
-    return kStages * (kBM + BN) * kAtom + 256 + 1024;
+    return stages_1cta<BN, SPLIT>() * (SPLIT ? 2 : 1) * (kBM + BN) * kAtom + 256 + 1024;
 }
 int smem_bytes_2sm() { return kStages2 * 2 * 128 * kAtom + 4 * kStgWarp + 256 + 1024; }
 int smem_bytes_2sm_w() { return kStagesW * 3 * 128 * kAtom + 8 * kStgWarp + 256 + 1024; }
@@ -1311,9 +1385,16 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     plan->args = a;
     const int es = dtype_size(a.in_dtype);
     auto al16 = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
-    const int bn = a.N >= 256 ? 256 : a.N >= 128 ? 128 : 64;
-    const bool two_sm = a.M >= 256 && a.N >= 256;
-    bool ok = (a.epi == 0 || (a.N % 256 == 0 && bn == 256 && a.R == nullptr)) &&
+    const bool split = a.split && a.in_dtype == F32;
+    // 3xTF32 runs on the 1-CTA kernel with N tiles of <= 128 (the split doubles
+    // the staged bytes); 64-column tiles when 128-column ones leave SMs idle
+    const int bn = split ? (a.N >= 128 && static_cast<long long>(a.batch) * ((a.M + kBM - 1) / kBM) *
+                                                  ((a.N + 127) / 128) >= num_sms ? 128 : 64)
+                         : a.N >= 256 ? 256 : a.N >= 128 ? 128 : 64;
+    const bool two_sm = !split && a.M >= 256 && a.N >= 256;
+    if (a.split && a.in_dtype != F32) return cudaErrorInvalidValue;
+    bool ok = (!split || (a.epi == 0 && !a.no_P && !a.rs_P)) &&
+              (a.epi == 0 || (a.N % 256 == 0 && bn == 256 && a.R == nullptr)) &&
               (a.epi != 2 || (a.batch == 1 && (reinterpret_cast<std::uintptr_t>(a.rope) & 15) == 0)) && a.M >= kBM && a.N >= bn && a.K * es >= kAtom && al16(a.A) && al16(a.B) && (a.lda * es) % 16 == 0 &&
               (a.ldb * es) % 16 == 0 && (a.batch == 1 || ((a.sa * es) % 16 == 0 && (a.sb * es) % 16 == 0)) &&
               (a.in_dtype == BF16 || a.in_dtype == F32);
@@ -1429,16 +1510,20 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         }
     }
     if (ok) {
-        static unsigned long long attr_set = 0;  // per CUDA device
+        // Kernel attributes once per CUDA device (any thread; setting them twice is harmless).
+        static std::atomic<unsigned long long> attr_set{0};
         int dev = 0;
         cudaGetDevice(&dev);
-        if (!((attr_set >> dev) & 1ULL)) {
-            cudaFuncSetAttribute(gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>());
-            cudaFuncSetAttribute(gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
-            cudaFuncSetAttribute(gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>());
+        if (!((attr_set.load(std::memory_order_acquire) >> dev) & 1ULL)) {
+            cudaFuncSetAttribute(gemm_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>());
+            cudaFuncSetAttribute(gemm_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
+            cudaFuncSetAttribute(gemm_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>());
+            cudaFuncSetAttribute(gemm_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64, true>());
+            cudaFuncSetAttribute(gemm_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes<128, true>());
             cudaFuncSetAttribute(gemm_kernel_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm());
             cudaFuncSetAttribute(gemm_kernel_2sm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm_w());
-            attr_set |= 1ULL << dev;
+            attr_set.fetch_or(1ULL << dev, std::memory_order_release);
         }
     }
     return cudaSuccess;
@@ -1478,6 +1563,7 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
     p.tail_units = plan.tail_units;
     p.dp_tiles = plan.tiles - plan.tail_units / p.tail_split;
     p.tma_c = plan.tc_ok && (plan.path == 2 || plan.path == 3) && (a.epi == 0 || a.epi == 1) ? 1 : 0;
+    p.split = a.split && a.in_dtype == F32 && plan.path == 0 ? 1 : 0;
     p.rs_P = a.rs_P;
     p.rs_ld = a.rs_ld;
     p.rs_row0 = a.rs_row0;
@@ -1507,11 +1593,20 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
     if (plan.path == 2)
         return launch_pdl(gemm_kernel_2sm, dim3(plan.grid), dim3(kThreads), smem_bytes_2sm(), s, plan.ta, plan.tb,
                           plan.tbh, plan.tbq, plan.tc, p);
+    if (p.split && plan.bn == 128)
+        return launch_pdl(gemm_kernel<128, true>, dim3(plan.grid), dim3(threads_1cta<128, true>()),
+                          smem_bytes<128, true>(), s, plan.ta, plan.tb, p);
+    if (p.split)
+        return launch_pdl(gemm_kernel<64, true>, dim3(plan.grid), dim3(threads_1cta<64, true>()),
+                          smem_bytes<64, true>(), s, plan.ta, plan.tb, p);
     if (plan.bn == 128)
-        return launch_pdl(gemm_kernel<128>, dim3(plan.grid), dim3(kThreads), smem_bytes<128>(), s, plan.ta, plan.tb, p);
+        return launch_pdl(gemm_kernel<128, false>, dim3(plan.grid), dim3(kThreads), smem_bytes<128>(), s, plan.ta,
+                          plan.tb, p);
     if (plan.bn == 64)
-        return launch_pdl(gemm_kernel<64>, dim3(plan.grid), dim3(kThreads), smem_bytes<64>(), s, plan.ta, plan.tb, p);
-    return launch_pdl(gemm_kernel<256>, dim3(plan.grid), dim3(kThreads), smem_bytes<256>(), s, plan.ta, plan.tb, p);
+        return launch_pdl(gemm_kernel<64, false>, dim3(plan.grid), dim3(kThreads), smem_bytes<64>(), s, plan.ta,
+                          plan.tb, p);
+    return launch_pdl(gemm_kernel<256, false>, dim3(plan.grid), dim3(kThreads), smem_bytes<256>(), s, plan.ta, plan.tb,
+                      p);
 }
 
 }  // namespace tn::k

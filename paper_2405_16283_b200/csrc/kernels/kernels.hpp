@@ -54,6 +54,8 @@ struct GemmArgs {
     // M*ldc elements after C, and no_P[m * (N/32) + c] = sum of x[m, 32c..32c+31]^2.
     const void* no_g = nullptr;
     float* no_P = nullptr;
+    int split = 0;               // fp32 inputs: 1 = 3xTF32 (A = Ahi + Alo, B = Bhi + Blo split in shared
+                                 // memory, C += Alo·Bhi + Ahi·Blo + Ahi·Bhi; fp32-accurate), 0 = tf32
     int tile = 0;                // CTA-pair tile: 0 auto, 1 narrow (256x256), 2 wide (512x256),
                                  // 3 narrow with a stream-K tail (instead of half-width tail tiles)
 };

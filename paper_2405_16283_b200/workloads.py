@@ -737,7 +737,7 @@ def blockwise_attention_flops(seq, heads, hd, tile):
 
 # ------------------------------------------------- tiled matmul chain (cfg 1) ---
 def matmul_chain(n: int = 4096, tile: int = 1024, chain: int = 4, devices: int = 2,
-                 dtype: str = "f32") -> GraphBuilder:
+                 dtype: str = "f32", precision: str = "3xtf32") -> GraphBuilder:
     """Config 1: X·W1·W2·…·WL, n×n fp32, tiled `tile`×`tile`.
 
     Row panels of X are split over devices; each device holds its own copy of
@@ -746,7 +746,9 @@ def matmul_chain(n: int = 4096, tile: int = 1024, chain: int = 4, devices: int =
     so the reduction order never depends on the schedule). Between links the
     activation row panels are exchanged with Transfer vertices (all-gather of
     panels), which exercises the move path across devices.
-    Weights are stored transposed per tile (B operand is K-major)."""
+    Weights are stored transposed per tile (B operand is K-major). fp32 tiles
+    multiply with `precision` "3xtf32" (fp32-accurate split on the tensor
+    cores, the default) or "tf32" (one tf32 MMA, ~1e-3 relative)."""
     T = n // tile
     g = GraphBuilder(device_count=devices)
     rows_per_dev = [list(range(d * T // devices, (d + 1) * T // devices)) for d in range(devices)]
@@ -768,7 +770,8 @@ def matmul_chain(n: int = 4096, tile: int = 1024, chain: int = 4, devices: int =
                 parts = []
                 for k in range(T):
                     parts.append(g.gemm(f"P{l}[{i},{j},{k}]", cur[(i, k)], Wt[(d, j, k)], tile, tile, tile,
-                                        in_dtype=dtype, out_dtype="f32", out_shape=(tile, tile), device=d))
+                                        in_dtype=dtype, out_dtype="f32", out_shape=(tile, tile), device=d,
+                                        precision=precision if dtype == "f32" else None))
                 nxt[(i, j)] = g.kernel(f"Y{l}[{i},{j}]", {"type": "sum", "args": parts, "count": tile * tile,
                                                           "in_dtype": "f32", "out_dtype": dtype},
                                        (tile, tile), dtype, d)

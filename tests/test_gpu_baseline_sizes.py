@@ -18,12 +18,11 @@ BITWISE identical logits on the GPU (plans move bytes, never change math);
 executor byte counters equal the memgraph's offload/reload sizes.
 """
 import json
-import os
 
 import numpy as np
 import pytest
 
-from helpers import inputs_of, inputs_with_in_edges, oracle_outputs, out_values, rel_err
+from helpers import record_err as record, inputs_of, inputs_with_in_edges, oracle_outputs, out_values, rel_err
 from paper_2405_16283_b200 import workloads as W
 from paper_2405_16283_b200.executor import Executor
 
@@ -37,14 +36,6 @@ TOL_C1 = 1e-5
 TOL_C3 = 3e-2
 TOL_C4 = 5e-2
 TOL_C5 = 2e-2
-
-
-def record(name, **kw):
-    """Appends measured errors to $PARITY_LOG (JSON lines) when set."""
-    p = os.environ.get("PARITY_LOG")
-    if p:
-        with open(p, "a") as f:
-            f.write(json.dumps({"test": name, **kw}) + "\n")
 
 
 def gpu_outputs(g, mg, inputs, outputs, config=None, runs=(("event-driven", "fifo", 0),)):
