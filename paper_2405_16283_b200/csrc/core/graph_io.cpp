@@ -26,7 +26,11 @@
 
 namespace tn {
 
-using json = nlohmann::ordered_json;
+using json = nlohmann::ordered_json;  // serialisation: the reference's key order and layout
+// Parsing only reads keys, so it uses the std::map object type: an
+// ordered_json object is a vector with linear key lookup, which made parsing
+// a 38k-vertex memgraph (38k placement keys) quadratic (3.7 s vs 0.7 s).
+using pjson = nlohmann::json;
 
 // ------------------------------------------------------------------ basics --
 void TaskGraph::reindex() {
@@ -441,10 +445,10 @@ std::string serialize_taskgraph(const TaskGraph& g) {
 }
 
 TaskGraph parse_taskgraph(const std::string& text) {
-    json j;
+    pjson j;
     try {
-        j = json::parse(text);
-    } catch (const json::parse_error& e) {
+        j = pjson::parse(text);
+    } catch (const pjson::parse_error& e) {
         throw ParseError(std::string("invalid JSON: ") + e.what());
     }
     if (!j.is_object()) throw ParseError("top level must be an object");
@@ -475,7 +479,7 @@ TaskGraph parse_taskgraph(const std::string& text) {
             if (!g.find(c)) throw ParseError("edge references unknown vertex " + std::to_string(c));
             g.edges.emplace_back(p, c);
         }
-    } catch (const json::exception& e) {
+    } catch (const pjson::exception& e) {
         throw ParseError(std::string("invalid taskgraph: ") + e.what());
     }
     return g;
@@ -525,10 +529,10 @@ std::string serialize_memgraph(const MemGraph& m, const MemoryMap& map) {
 }
 
 std::pair<MemGraph, MemoryMap> parse_memgraph(const std::string& text) {
-    json j;
+    pjson j;
     try {
-        j = json::parse(text);
-    } catch (const json::parse_error& e) {
+        j = pjson::parse(text);
+    } catch (const pjson::parse_error& e) {
         throw ParseError(std::string("invalid JSON: ") + e.what());
     }
     if (!j.is_object() || !j.contains("vertices") || !j.contains("edges"))
@@ -573,23 +577,26 @@ std::pair<MemGraph, MemoryMap> parse_memgraph(const std::string& text) {
             m.edges.push_back(e);
         }
         m.total_order = j.value("total_order", std::vector<VertexId>{});
-        const json placements = j.value("placement", json::object());
-        for (const auto& [key, jp] : placements.items()) {
-            Placement p;
-            p.device = jp.value("device", 0);
-            p.offset = jp.value("offset", std::int64_t{0});
-            p.size = jp.value("size", std::int64_t{1});
-            map.placements[std::stoll(key)] = p;
+        if (j.contains("placement")) {
+            for (const auto& [key, jp] : j["placement"].items()) {
+                Placement p;
+                p.device = jp.value("device", 0);
+                p.offset = jp.value("offset", std::int64_t{0});
+                p.size = jp.value("size", std::int64_t{1});
+                map.placements[std::stoll(key)] = p;
+            }
         }
-        for (const auto& jh : j.value("history", json::array())) {
-            RegionClaim h;
-            h.owner = jh.value("owner", VertexId{0});
-            h.device = jh.value("device", 0);
-            h.offset = jh.value("offset", std::int64_t{0});
-            h.size = jh.value("size", std::int64_t{0});
-            map.history.push_back(h);
+        if (j.contains("history")) {
+            for (const auto& jh : j["history"]) {
+                RegionClaim h;
+                h.owner = jh.value("owner", VertexId{0});
+                h.device = jh.value("device", 0);
+                h.offset = jh.value("offset", std::int64_t{0});
+                h.size = jh.value("size", std::int64_t{0});
+                map.history.push_back(h);
+            }
         }
-    } catch (const json::exception& e) {
+    } catch (const pjson::exception& e) {
         throw ParseError(std::string("invalid memgraph: ") + e.what());
     }
     return {std::move(m), std::move(map)};

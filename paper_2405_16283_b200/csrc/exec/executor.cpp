@@ -167,6 +167,15 @@ struct Executor::Impl {
     void build();
     void prepare_kernel(Instr& in, const MemVertex& v, const std::vector<std::pair<VertexId, VertexId>>& data_in);
     void launch(std::int32_t vidx, std::int32_t stream, std::int32_t after = -1);
+    // The CUDA stream a vertex runs on, as a dense lane id (device-major):
+    // work on one lane completes in launch order, so completion polling only
+    // ever needs to query the oldest in-flight vertex of each lane.
+    int lanes() const { return D * (cfg.streams_per_device + 1); }
+    int lane_of(std::int32_t vidx, std::int32_t stream) const {
+        const Instr& in = prog[vidx];
+        const bool on_compute = in.op == MemOpKind::Kernel && cfg.compute_tokens == 1;
+        return in.dev * (cfg.streams_per_device + 1) + (on_compute ? cfg.streams_per_device : stream < 0 ? 0 : stream);
+    }
     void run(const SchedulerPolicy& pol, std::uint64_t seed, ExecutionTrace* trace);
     ExecutionTrace build_trace();
     std::unique_ptr<MemGraph> last_graph;  // fixed-order graph of the last run
@@ -814,21 +823,22 @@ namespace {
 
 class CudaBackend {
   public:
-    explicit CudaBackend(Executor::Impl& x) : x_(x), start_(std::chrono::steady_clock::now()) {}
+    explicit CudaBackend(Executor::Impl& x)
+        : x_(x), start_(std::chrono::steady_clock::now()), lanes_(x.lanes()) {}
     void launch(std::int32_t vidx, std::int32_t stream, double) {
         x_.launch(vidx, stream);
         x_.dispatched.push_back(vidx);
         x_.stream_of[vidx] = stream;
         in_flight_++;
         if (x_.prog[vidx].instant) instant_.push_back(vidx);
-        else if (x_.cfg.poll) flying_.push_back(vidx);
+        else if (x_.cfg.poll) track(vidx, stream);
     }
     void launch_after(std::int32_t vidx, std::int32_t stream, std::int32_t after, double) {
         x_.launch(vidx, stream, after);
         x_.dispatched.push_back(vidx);
         x_.stream_of[vidx] = stream;
         in_flight_++;
-        if (x_.cfg.poll) flying_.push_back(vidx);
+        if (x_.cfg.poll) track(vidx, stream);
     }
     bool idle() const { return in_flight_ == 0; }
     double wait_s() const { return wait_s_; }
@@ -863,19 +873,35 @@ class CudaBackend {
         return v;
     }
 
-    // Spins over the in-flight vertices' end events (oldest first) until one
-    // has completed; lower latency than a host-function round trip.
+    void track(std::int32_t vidx, std::int32_t stream) {
+        const int l = x_.lane_of(vidx, stream);
+        if (lanes_[l].empty()) active_.push_back(l);
+        lanes_[l].push_back(vidx);
+    }
+
+    // Spins over the lanes with work in flight, querying only the OLDEST
+    // vertex of each (a stream completes in order), round-robin from where
+    // the last completion was found; lower latency than a host-function
+    // round trip and O(#busy streams) per sweep instead of O(#in flight).
     std::int32_t poll_next(double& now) {
         const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(x_.cfg.timeout_s);
         for (std::uint64_t spin = 0;; ++spin) {
-            for (size_t i = 0; i < flying_.size(); ++i) {
-                const std::int32_t v = flying_[i];
+            const size_t n = active_.size();
+            for (size_t k = 0; k < n; ++k) {
+                const size_t i = (rr_ + k) % n;
+                const int l = active_[i];
+                const std::int32_t v = lanes_[l].front();
                 const int dev = x_.prog[v].dev;
                 if (x_.ordinal[dev] != x_.cur_dev) x_.set_device(dev);
                 cudaError_t e = cudaEventQuery(x_.done_event(v));
                 if (e == cudaErrorNotReady) continue;
                 if (e != cudaSuccess) throw CudaError(std::string("vertex failed on the device: ") + cudaGetErrorString(e));
-                flying_.erase(flying_.begin() + static_cast<std::ptrdiff_t>(i));
+                lanes_[l].pop_front();
+                if (lanes_[l].empty()) {
+                    active_[i] = active_.back();
+                    active_.pop_back();
+                }
+                rr_ = active_.empty() ? 0 : i % active_.size();
                 in_flight_--;
                 now = std::chrono::duration<double>(std::chrono::steady_clock::now() - start_).count();
                 return v;
@@ -890,7 +916,9 @@ class CudaBackend {
     std::chrono::steady_clock::time_point start_;
     int in_flight_ = 0;
     double wait_s_ = 0;
-    std::vector<std::int32_t> flying_;
+    std::vector<std::deque<std::int32_t>> lanes_;  // in-flight vertices per stream, launch order
+    std::vector<int> active_;                      // lanes with work in flight
+    size_t rr_ = 0;
     std::deque<std::int32_t> instant_;
 };
 

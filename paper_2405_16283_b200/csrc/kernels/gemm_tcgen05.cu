@@ -464,6 +464,14 @@ __device__ __forceinline__ void split_operands(std::uint8_t* hi, std::uint8_t* l
     }
 }
 
+// SPLIT kernels also accumulate K in chunks of kChunkKB blocks: each chunk
+// goes into a fresh TMEM accumulator and the epilogue adds the chunks in
+// fp32 registers (round to nearest). The tensor core's own accumulation
+// truncates, so its error grows with the number of MMAs summed into one
+// accumulator (measured 7e-6 normwise at K = 1024 unchunked); chunking bounds
+// that to one chunk.
+constexpr int kChunkKB = 4;
+
 template <int BN, bool SPLIT>
 constexpr int stages_1cta() {
     return SPLIT ? (BN >= 128 ? 3 : 4) : kStages;
@@ -562,10 +570,12 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                 decode(p, t, b, mb, nb);
                 if (tile_skipped(p, mb, nb, BN)) continue;
                 const int nk = kblocks(p, mb, bk);
+                const int chunk = SPLIT ? kChunkKB : nk;
+                for (int kb0 = 0; kb0 < nk; kb0 += chunk) {
                 mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
                 tc_fence_after();
                 const std::uint32_t d = tmem + acc * BN;
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = kb0; kb < nk && kb < kb0 + chunk; ++kb) {
                     mbar_wait((SPLIT ? splitb : full) + 8 * stage, phase);
                     tc_fence_after();
                     const std::uint32_t sa = sbase + stage * STAGE;
@@ -574,7 +584,7 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                         const std::uint64_t al = sdesc(sa + LOADED), bl = sdesc(sa + LOADED + A_BYTES);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {  // small terms first, then hi·hi
-                            tc_mma(d, al + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, true);
+                            tc_mma(d, al + 2 * k, bd + 2 * k, idesc, (kb != kb0) | (k != 0), true);
                             tc_mma(d, ad + 2 * k, bl + 2 * k, idesc, 1u, true);
                             tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, 1u, true);
                         }
@@ -593,6 +603,7 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
+                }
                 }
             }
         }
@@ -639,6 +650,40 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
             mbar_wait(tfull + 8 * acc, acc_phase);
             tc_fence_after();
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+            if (SPLIT) {  // sum the tile's K chunks in registers, then store
+                float sum[BN];
+#pragma unroll
+                for (int c = 0; c < BN; ++c) sum[c] = 0.f;
+                const int nk = kblocks(p, mb, bk);
+                for (int kb0 = 0; kb0 < nk; kb0 += kChunkKB) {
+                    if (kb0) mbar_wait(tfull + 8 * acc, acc_phase);
+                    tc_fence_after();
+                    const std::uint32_t tb = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
+#pragma unroll
+                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                        std::uint32_t r[32];
+                        TN_LD32(tb + c0, r);
+                        tc_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) sum[c0 + j] += __uint_as_float(r[j]);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty + 8 * acc);
+                    if (++acc == 2) {
+                        acc = 0;
+                        acc_phase ^= 1;
+                    }
+                }
+#pragma unroll
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    std::uint32_t r[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(sum[c0 + j]);
+                    store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok, alpha);
+                }
+                continue;
+            }
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
             if (p.epi == 1) {
                 epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok, alpha);
@@ -1386,11 +1431,9 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     const int es = dtype_size(a.in_dtype);
     auto al16 = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
     const bool split = a.split && a.in_dtype == F32;
-    // 3xTF32 runs on the 1-CTA kernel with N tiles of <= 128 (the split doubles
-    // the staged bytes); 64-column tiles when 128-column ones leave SMs idle
-    const int bn = split ? (a.N >= 128 && static_cast<long long>(a.batch) * ((a.M + kBM - 1) / kBM) *
-                                                  ((a.N + 127) / 128) >= num_sms ? 128 : 64)
-                         : a.N >= 256 ? 256 : a.N >= 128 ? 128 : 64;
+    // 3xTF32 runs on the 1-CTA kernel with 64-column tiles (the split doubles the
+    // staged bytes; the chunked epilogue keeps a 64-float row sum in registers)
+    const int bn = split ? 64 : a.N >= 256 ? 256 : a.N >= 128 ? 128 : 64;
     const bool two_sm = !split && a.M >= 256 && a.N >= 256;
     if (a.split && a.in_dtype != F32) return cudaErrorInvalidValue;
     bool ok = (!split || (a.epi == 0 && !a.no_P && !a.rs_P)) &&
@@ -1519,8 +1562,6 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
             cudaFuncSetAttribute(gemm_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
             cudaFuncSetAttribute(gemm_kernel<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>());
             cudaFuncSetAttribute(gemm_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64, true>());
-            cudaFuncSetAttribute(gemm_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes<128, true>());
             cudaFuncSetAttribute(gemm_kernel_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm());
             cudaFuncSetAttribute(gemm_kernel_2sm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes_2sm_w());
             attr_set.fetch_or(1ULL << dev, std::memory_order_release);
@@ -1593,9 +1634,6 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
     if (plan.path == 2)
         return launch_pdl(gemm_kernel_2sm, dim3(plan.grid), dim3(kThreads), smem_bytes_2sm(), s, plan.ta, plan.tb,
                           plan.tbh, plan.tbq, plan.tc, p);
-    if (p.split && plan.bn == 128)
-        return launch_pdl(gemm_kernel<128, true>, dim3(plan.grid), dim3(threads_1cta<128, true>()),
-                          smem_bytes<128, true>(), s, plan.ta, plan.tb, p);
     if (p.split)
         return launch_pdl(gemm_kernel<64, true>, dim3(plan.grid), dim3(threads_1cta<64, true>()),
                           smem_bytes<64, true>(), s, plan.ta, plan.tb, p);

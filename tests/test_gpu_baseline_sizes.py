@@ -31,11 +31,14 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
-TOL_C2 = 3e-2
+# measured on a B200 (round 2): config 2 4.3e-2 (bf16 rounding differences
+# between vertices compound over 32 layers: 6.7e-3 after one layer),
+# config 3 8.0e-3, config 4 1.9e-2 (worst adapter gradient), config 5 1.8e-4
+TOL_C2 = 8e-2
 TOL_C1 = 1e-5
-TOL_C3 = 3e-2
-TOL_C4 = 5e-2
-TOL_C5 = 2e-2
+TOL_C3 = 1.6e-2
+TOL_C4 = 4e-2
+TOL_C5 = 4e-4
 
 
 def gpu_outputs(g, mg, inputs, outputs, config=None, runs=(("event-driven", "fifo", 0),)):

@@ -1,11 +1,12 @@
 """GPU parity: the CUDA executor (through the C ABI) against the CPU oracle.
 
-Tolerances (normwise relative error vs the fp32 oracle):
-  * bf16 outputs of a single op: 1e-2 (one bf16 rounding, 2^-8 relative);
-  * fp32 outputs of bf16 GEMMs: 1e-4 (products exact, only the accumulation
-    order differs);
-  * tf32 GEMMs (fp32 inputs, config-1 path): 5e-3 (10-bit mantissa inputs);
-  * end-to-end LLaMA logits (bf16 pipeline, 2 layers): 3e-2.
+Tolerances (normwise relative error vs the fp32 oracle) are about 2x the
+error measured on a B200 for each case (the measured values are logged to
+$PARITY_LOG and summarised in profiles/r2_parity_errors.md), e.g.:
+  * bf16 GEMM outputs 3e-4, fp32 outputs of bf16 GEMMs 1e-6 (products exact,
+    only the accumulation order differs), tf32 1.6e-3, 3xTF32 2e-6;
+  * fused attention 5e-3; end-to-end small LLaMA logits 1.3e-2 (bf16
+    activations rounded between vertices, like the oracle).
 GPU results must be BITWISE identical across dispatch orders: every kernel
 reduces in a fixed order and no task uses atomics.
 """
@@ -108,8 +109,10 @@ def test_gemm_parity(shape):
         x, y = x[keep], y[keep]
     if shape.get("precision") == "3xtf32":
         tol = 2e-6
-    else:
-        tol = 5e-3 if shape.get("in_dtype") == "f32" else (1e-4 if shape.get("out_dtype") == "f32" else 1e-2)
+    elif shape.get("in_dtype") == "f32":
+        tol = 1.6e-3  # tf32 inputs (10-bit mantissa): measured 7.7e-4
+    else:  # bf16 inputs, products exact, fp32 accumulation order differs
+        tol = 1e-6 if shape.get("out_dtype") == "f32" else 3e-4  # measured 4.9e-7 / 1.5e-4
     err = rel_err(x, y)
     record_err("gemm_parity", shape=str(shape), rel_err=err)
     assert err < tol, err
@@ -134,7 +137,7 @@ def test_gemm_qkv_rope_epilogue_tiles(tile, S, H):
     want = oracle_outputs(g, mg, inp)
     _e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
     record_err("gpu_exec", line=1, rel_err=_e)
-    assert _e < 1e-2
+    assert _e < 1.2e-4
 
 
 def test_gemm_stream_k_deterministic():
@@ -192,7 +195,9 @@ def test_rowops_and_eltwise_parity():
     for o in outs:
         x_, y_ = out_values(g, o, got[o]), out_values(g, o, want[o])
         exact = g.tensors[o].name in ("vt", "emb", "sum32", "cast")
-        assert rel_err(x_, y_) <= (0 if exact else 1e-2), g.tensors[o].name
+        e = rel_err(x_, y_)
+        record_err("rowops", name=g.tensors[o].name, rel_err=e)
+        assert e <= (0 if exact else 2e-3), g.tensors[o].name
 
 
 @pytest.mark.parametrize("seq,hd,causal,sigma", [(256, 128, 1, 1.0), (512, 128, 1, 1.0), (256, 128, 0, 1.0),
@@ -214,7 +219,7 @@ def test_fused_attention_parity(seq, hd, causal, sigma):
     want = oracle_outputs(g, mg, inp)
     _e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
     record_err("gpu_exec", line=2, rel_err=_e)
-    assert _e < 1e-2
+    assert _e < 5e-3
 
 
 def test_unfused_attention_pipeline_matches_fused():
@@ -229,7 +234,7 @@ def test_unfused_attention_pipeline_matches_fused():
         outs.append(out_values(g, o, got[o]))
     _e = rel_err(outs[0], outs[1])
     record_err("gpu_exec", line=3, rel_err=_e)
-    assert _e < 3e-2
+    assert _e < 1.3e-2
 
 
 def test_llama_small_parity_with_offloads():
@@ -241,7 +246,7 @@ def test_llama_small_parity_with_offloads():
     (o,) = g.outputs()
     _e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
     record_err("gpu_exec", line=4, rel_err=_e)
-    assert _e < 3e-2
+    assert _e < 1.3e-2
     assert trace["host_bytes_transferred"] > 0
 
 
@@ -301,7 +306,7 @@ def test_llama_fused_norm_parity_with_offloads():
     (o,) = g.outputs()
     _e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
     record_err("gpu_exec", line=5, rel_err=_e)
-    assert _e < 3e-2
+    assert _e < 1.3e-2
 
 
 @pytest.mark.parametrize("cfg", [{"lookahead": 1}, {"lookahead": 0}, {"lookahead": 0, "completion": "callback"},
@@ -335,7 +340,7 @@ def test_dispatch_order_independence_bitwise(cfg):
     want = oracle_outputs(g, mg, inp)
     _e = rel_err(out_values(g, o, results[0]), out_values(g, o, want[o]))
     record_err("gpu_exec", line=6, rel_err=_e)
-    assert _e < 3e-2
+    assert _e < 1.3e-2
 
 
 def check_trace(mg, trace):
@@ -367,7 +372,7 @@ def test_multi_device_graph_on_one_gpu_tf32():
     for o in g.outputs():
         _e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
         record_err("gpu_exec", line=7, rel_err=_e)
-        assert _e < 5e-3
+        assert _e < 1e-5
     check_trace(mg, trace)
 
 
@@ -420,7 +425,7 @@ def test_full_width_llama7b_layer_matches_oracle_with_offloads():
     (o,) = g.outputs()
     _e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
     record_err("gpu_exec", line=8, rel_err=_e)
-    assert _e < 3e-2
+    assert _e < 1.3e-2
 
 
 def test_full_size_llama7b_properties():
@@ -483,7 +488,7 @@ def test_tight_cap_offload_reload_bytes():
     want = oracle_outputs(g, mg, inp)
     _e = rel_err(out_values(g, o, got), out_values(g, o, want[o]))
     record_err("gpu_exec", line=9, rel_err=_e)
-    assert _e < 3e-2
+    assert _e < 1.4e-2
     check_trace(mg, trace)
 
 
@@ -509,7 +514,7 @@ def test_blockwise_attention_offloaded_tiles_parity():
     for o in outs:
         _e = rel_err(out_values(g, o, res[0][o]), out_values(g, o, want[o]))
         record_err("gpu_exec", line=10, rel_err=_e)
-        assert _e < 2e-2
+        assert _e < 5e-4
     assert st["d2h_bytes"] > 0 and trace["host_bytes_transferred"] > 0
 
 
@@ -537,7 +542,7 @@ def test_tensor_parallel_on_one_gpu_four_memgraph_devices():
     assert st["d2d_bytes"] > 0
     _e = rel_err(out_values(g, o, res[0]), out_values(g, o, want[o]))
     record_err("gpu_exec", line=11, rel_err=_e)
-    assert _e < 3e-2
+    assert _e < 1.5e-2
 
 
 @pytest.mark.parametrize("shape", [dict(batch=1, rows=200, cols=72, dt="bf16"), dict(batch=3, rows=256, cols=128, dt="bf16"),
@@ -590,7 +595,7 @@ def test_training_rowops_parity():
     for o in outs:
         _e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
         record_err("gpu_exec", line=12, rel_err=_e, name=g.tensors[o].name)
-        assert _e < 1e-2, g.tensors[o].name
+        assert _e < 2e-5, g.tensors[o].name
 
 
 def test_input_offload_elision_is_exact():
@@ -636,7 +641,7 @@ def test_lora_step_parity_with_activation_offload():
     for o in g.outputs():
         _e = rel_err(out_values(g, o, res[0][o]), out_values(g, o, want[o]))
         record_err("gpu_exec", line=13, rel_err=_e, name=g.tensors[o].name)
-        assert _e < 5e-2, g.tensors[o].name
+        assert _e < 1.5e-2, g.tensors[o].name
 
 
 def test_executor_rejects_bad_payloads_without_crashing():
@@ -710,3 +715,30 @@ def test_executor_reuse_many_runs_and_inputs_update():
         ex.run()
         assert json.loads(ex.last_trace())["rows"]
     assert outs[0] == outs[2] and outs[0] != outs[1]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 visible GPUs")
+def test_tensor_parallel_over_two_distinct_gpus_peer_copies():
+    """A TP memgraph over 2 DISTINCT GPUs: Transfer vertices are NVLink peer
+    copies (cudaMemcpyPeerAsync, p2p_bytes > 0), outputs match the oracle and
+    are bitwise identical to the same memgraph mapped onto one GPU."""
+    cfg = W.LlamaConfig(dim=1024, layers=2, heads=8, ffn=1024, vocab=1000)
+    g = W.llama_prefill_tp(cfg, 512, tp=2)
+    caps = [int(c * 1.5) // 1024 * 1024 for c in W.working_set_floor(g)]
+    mg, _ = W.plan(g, caps, alloc_horizon="lazy")
+    inp = inputs_of(g, seed=41)
+    (o,) = g.outputs()
+    res, stats = {}, {}
+    for name, devs in (("two", [0, 1]), ("one", [0, 0])):
+        with Executor(mg, g.to_json(), {"devices": devs}) as ex:
+            for vid, a in inp.items():
+                ex.set_input(vid, a)
+            trace = json.loads(ex.run("event-driven", "seeded-random", 3))
+            check_trace(mg, trace)
+            res[name] = ex.get_output(o, g.tensors[o].nbytes)
+            stats[name] = ex.stats()
+    assert stats["two"]["p2p_bytes"] > 0 and stats["one"]["p2p_bytes"] == 0
+    assert stats["two"]["p2p_bytes"] == stats["one"]["d2d_bytes"]
+    assert res["two"] == res["one"]
+    want = oracle_outputs(g, mg, inp)
+    assert rel_err(out_values(g, o, res["two"]), out_values(g, o, want[o])) < 3e-2
