@@ -294,6 +294,17 @@ def timed_runs(ex, steps, devs, after=None):
     return s.elapsed_time(e) * 1e-3
 
 
+def untimed_steps(ex, steps: int, policy: str = "event-driven", tie_break: str = "fifo") -> list[float]:
+    """Per-step device time (s) of `steps` untimed executor runs (used by the
+    tools/ harnesses): each run's device-timed makespan (CUDA events around
+    the whole run), back to back so the GPU stays in its sustained state."""
+    out = []
+    for i in range(steps):
+        ex.run(policy, tie_break, i, trace=False)
+        out.append(ex.stats()["device_makespan_s"])
+    return out
+
+
 # ----------------------------------------------------------------- roofline ---
 def gemm_flops(op) -> float:
     f = 2.0 * op["M"] * op["N"] * op["K"] * op.get("batch", 1)

@@ -35,7 +35,7 @@ if not torch.cuda.is_available():
 # between vertices compound over 32 layers: 6.7e-3 after one layer),
 # config 3 8.0e-3, config 4 1.9e-2 (worst adapter gradient), config 5 1.8e-4
 TOL_C2 = 8e-2
-TOL_C1 = 1e-5
+TOL_C1 = 7e-6  # measured 3.3e-6 (3xTF32, chunked accumulation)
 TOL_C3 = 1.6e-2
 TOL_C4 = 4e-2
 TOL_C5 = 4e-4
