@@ -515,11 +515,14 @@ def run_reference(args, world, rank):
 
 
 # ------------------------------------------------------------ offload leg ---
-def offload_leg(args, dev):
+def offload_leg(args, devs):
     """Config 4 (LLaMA-7B LoRA step, seq 4096, activation offload under the
-    16 GiB cap, frozen weights cold in host RAM) executed on one GPU, plus the
+    16 GiB cap per GPU, frozen weights cold in host RAM) — on one GPU, or data
+    parallel over the N GPUs of the run (one sequence per GPU, adapter
+    gradients all-reduced by Transfer + fixed-order sum vertices) — plus the
     hardware event-driven vs fixed-order comparison on config 4 and on a
-    config-5 blockwise-attention plan."""
+    config-5 blockwise-attention plan (first GPU)."""
+    dev = devs[0]
     import torch
 
     from paper_2405_16283_b200 import workloads as W
@@ -527,32 +530,36 @@ def offload_leg(args, dev):
 
     pk = peaks()
     out = {}
-    g = W.llama_lora_step(W.LLAMA_7B, args.seq)
-    mg, st = W.plan(g, int(args.cap_gib * (1 << 30)), alloc_horizon="lazy")
+    dp = len(devs)
+    g = W.llama_lora_step(W.LLAMA_7B, args.seq) if dp == 1 else W.llama_lora_step_dp(W.LLAMA_7B, args.seq, dp)
+    mg, st = W.plan(g, [int(args.cap_gib * (1 << 30))] * dp, alloc_horizon="lazy")
     m = json.loads(mg)
     off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
     rel = sum(v["size"] for v in m["vertices"] if v["op"] == "reload")
-    with Executor(mg, g.to_json(), {"devices": [dev], "input_residency": "host"}) as ex:
-        load_inputs(ex, g, 0, [dev])
+    with Executor(mg, g.to_json(), {"devices": devs, "input_residency": "host"}) as ex:
+        load_inputs(ex, g, 0, devs)
         ex.run(trace=False)
         steps = max(1, args.offload_steps)
-        t = timed_runs(ex, steps, [dev]) / steps
+        t = timed_runs(ex, steps, devs) / steps
         ex.run()  # one traced step: exposed transfer
         s = ex.stats()
         pcie_h2d, pcie_d2h = measure_pcie(torch.device("cuda", dev)), measure_pcie(torch.device("cuda", dev), "d2h")
-        roof = max(s["flops"] / (pk["bf16_tflops_sustained"] * 1e12), s["h2d_bytes"] / (pcie_h2d * 1e9),
-                   s["d2h_bytes"] / (pcie_d2h * 1e9))
+        gpus = len(set(devs))
+        roof = max(s["flops"] / (gpus * pk["bf16_tflops_sustained"] * 1e12), s["h2d_bytes"] / (gpus * pcie_h2d * 1e9),
+                   s["d2h_bytes"] / (gpus * pcie_d2h * 1e9))
         out["config4_lora_step"] = {
-            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy", "memgraph_vertices": len(m["vertices"]),
+            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy" + (f"_dp{dp}" if dp > 1 else ""),
+            "gpus": gpus, "global_batch": dp, "memgraph_vertices": len(m["vertices"]),
             "offloads": st["offloads"], "reloads": st["reloads"], "offload_bytes_planned": off,
-            "reload_bytes_planned": rel, "step_s": round(t, 4), "tokens_per_s": round(args.seq / t, 1),
+            "reload_bytes_planned": rel, "step_s": round(t, 4), "tokens_per_s": round(dp * args.seq / t, 1),
+            "p2p_bytes": s["p2p_bytes"],
             "h2d_bytes": s["h2d_bytes"], "d2h_bytes": s["d2h_bytes"],
             "d2h_elided_bytes": s["d2h_elided_bytes"],
             "achieved_h2d_gbs": round(s["h2d_bytes"] / t / 1e9, 1), "achieved_d2h_gbs": round(s["d2h_bytes"] / t / 1e9, 1),
             "pcie_h2d_gbs_measured": round(pcie_h2d, 1), "pcie_d2h_gbs_measured": round(pcie_d2h, 1),
             "exposed_transfer_s": round(s["exposed_transfer_s"], 4), "flops": s["flops"],
             "roofline_s": round(roof, 4), "frac_of_roofline": round(roof / t, 4),
-            "roofline": "max(FLOP / sustained bf16 peak, H2D bytes / PCIe H2D, D2H bytes / PCIe D2H)"}
+            "roofline": "max(FLOP / sustained bf16 peak, H2D bytes / PCIe H2D, D2H bytes / PCIe D2H), per GPU"}
         if args.policy_trials > 0:
             out["config4_lora_step"]["compare_policies"] = json.loads(ex.compare_policies(args.policy_trials, 0))
     if args.policy_trials > 0:
@@ -717,7 +724,7 @@ def run_ours_on(args, world, rank, local, n, tp):
         "peaks": {k: pk.get(k) for k in ("bf16_tflops", "bf16_tflops_sustained", "hbm_gbs")},
     }
     if not args.no_offload_leg and not args.quick:
-        line["offload"] = offload_leg(args, devs[0])
+        line["offload"] = offload_leg(args, devs)
     if n == 1 and not args.no_cpu_baseline and not args.quick:
         dt, L = cpu_sample(args, 1, False)
         line["cpu_baseline"] = {"value": round(args.seq / (dt * L), 2), "unit": UNIT, "cores": os.cpu_count(),

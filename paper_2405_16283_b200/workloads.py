@@ -490,12 +490,43 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     are expressed as explicit `transpose` vertices feeding the K-major GEMM
     task, and the attention backward as dP = dO·Vᵀ -> softmax_bwd ->
     dQ = dS·K, dK = dSᵀ·Q, dV = Pᵀ·dO (materialised n² tiles)."""
+    g = GraphBuilder(device_count=1)
+    _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "")
+    return g
+
+
+def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None = None, rank: int = 16,
+                       rank_pad: int = 64, lora_alpha: float = 16.0, std: float = 0.02) -> GraphBuilder:
+    """Config 4 over `dp` devices (data parallel): every memgraph
+    device runs the full LoRA step on its own sequence (tokens/targets
+    `@r`; the frozen weights and adapters are the same tensors on every device,
+    each device materialising its copy from host), then the per-device loss
+    and adapter gradients are summed on device 0 in fixed device order — the
+    gradient all-reduce as explicit Transfer vertices (NVLink peer copies)
+    into `sum` combines, no NCCL. Outputs: the summed loss and gradients
+    (same names as llama_lora_step's). Global batch = dp sequences."""
+    g = GraphBuilder(device_count=dp)
+    outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "")
+            for r in range(dp)]
+    for name, v0 in outs[0].items():
+        t = g.tensors[v0]
+        n = int(np.prod(t.shape))
+        args = [v0] + [g.transfer(outs[r][name], 0, f"{name}@{r}->0") for r in range(1, dp)]
+        g.kernel(f"{name}.sum", {"type": "sum", "args": args, "count": n, "in_dtype": t.dtype,
+                                 "out_dtype": t.dtype}, t.shape, t.dtype, 0)
+    return g
+
+
+def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, rank_pad, lora_alpha, std, device,
+                    data_sfx) -> dict:
+    """Appends one LoRA step on `device` to `g`; returns {output name: vid}
+    (the loss and every adapter gradient)."""
     L = cfg.layers if layers is None else layers
     d, H, hd, f, V, S = cfg.dim, cfg.heads, cfg.hd, cfg.ffn, cfg.vocab, seq
     R, sc = rank_pad, lora_alpha / rank
     scale = 1.0 / math.sqrt(hd)
-    g = GraphBuilder(device_count=1)
     dev = device
+    results = {}
 
     def tr(name, x, rows, cols, batch=1, dt="bf16"):
         return g.kernel(name, {"type": "transpose", "args": [x], "batch": batch, "rows": rows, "cols": cols,
@@ -513,8 +544,8 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
         return g.kernel(name, {"type": "sum", "args": [a, b], "count": S * d, "in_dtype": "bf16",
                                "out_dtype": "bf16"}, (S, d), "bf16", dev)
 
-    tok = g.input("tokens", (S,), "i32", dev, init=("tokens", V))
-    tgt = g.input("targets", (S,), "i32", dev, init=("tokens", V))
+    tok = g.input("tokens" + data_sfx, (S,), "i32", dev, init=("tokens", V))
+    tgt = g.input("targets" + data_sfx, (S,), "i32", dev, init=("tokens", V))
     emb = g.input("tok_embeddings", (V, d), "bf16", dev, init=("normal", std))
     rope_tab = g.input("rope_table", (S, hd // 2, 2), "f32", dev, init=("rope", cfg.theta))
     x = g.kernel("embed", {"type": "embedding", "args": [tok, emb], "seq": S, "dim": d, "vocab": V}, (S, d), "bf16", dev)
@@ -568,8 +599,8 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     xL = x
     hn = rms("final_norm", xL, wn)
     logits = g.gemm("logits", hn, wout, S, V, d, out_shape=(S, V), device=dev)
-    g.kernel("loss", {"type": "xent_loss", "args": [logits, tgt], "rows": S, "vocab": V, "scale": 1.0 / S,
-                      "in_dtype": "bf16"}, (1,), "f32", dev)
+    results["loss"] = g.kernel("loss", {"type": "xent_loss", "args": [logits, tgt], "rows": S, "vocab": V,
+                                        "scale": 1.0 / S, "in_dtype": "bf16"}, (1,), "f32", dev)
     dlog = g.kernel("dlogits", {"type": "xent_grad", "args": [logits, tgt], "rows": S, "vocab": V, "scale": 1.0 / S,
                                 "in_dtype": "bf16", "out_dtype": "bf16"}, (S, V), "bf16", dev)
     woutT = tr("output.T", wout, V, d)
@@ -583,12 +614,13 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
         Vv = g.gemm(p + nm + ".V", dY, BT, S, R, n_out, out_shape=(S, R), device=dev)
         dYT = tr(p + nm + ".dY.T", dY, S, n_out)
         UT = tr(p + nm + ".U.T", U, S, R)
-        g.gemm(p + nm + ".dB", dYT, UT, n_out, R, S, alpha=sc, out_shape=(n_out, R), device=dev)
+        results[p + nm + ".dB"] = g.gemm(p + nm + ".dB", dYT, UT, n_out, R, S, alpha=sc, out_shape=(n_out, R),
+                                         device=dev)
         VT = tr(p + nm + ".V.T", Vv, S, R)
         XT = tr(p + nm + ".X.T", X, S, k_in)
         # dAᵀ = s·Xᵀ·V keeps M = k_in on the tensor cores (R rows would be a GEMV)
         dAT = g.gemm(p + nm + ".dA.T", XT, VT, k_in, R, S, alpha=sc, out_shape=(k_in, R), device=dev)
-        tr(p + nm + ".dA", dAT, k_in, R)
+        results[p + nm + ".dA"] = tr(p + nm + ".dA", dAT, k_in, R)
         return Vv
 
     for l in reversed(range(L)):
@@ -641,12 +673,12 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
                         out_shape=(S, R), device=dev)
             dT = tr(p + f"lora_qkv.dY{j}.T", dpart, S, d)
             dBs.append(g.gemm(p + f"lora_qkv.dB{j}", dT, U1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev))
-        g.kernel(p + "lora_qkv.dB", {"type": "concat", "args": dBs, "count": d * R, "out_dtype": "bf16"},
-                 (3 * d, R), "bf16", dev)
+        results[p + "lora_qkv.dB"] = g.kernel(p + "lora_qkv.dB", {"type": "concat", "args": dBs, "count": d * R,
+                                                                  "out_dtype": "bf16"}, (3 * d, R), "bf16", dev)
         V1T = tr(p + "lora_qkv.V.T", V1, S, R)
         hT = tr(p + "lora_qkv.X.T", a["h"], S, d)
         dA1T = g.gemm(p + "lora_qkv.dA.T", hT, V1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev)
-        tr(p + "lora_qkv.dA", dA1T, d, R)
+        results[p + "lora_qkv.dA"] = tr(p + "lora_qkv.dA", dA1T, d, R)
         if l == 0:
             break  # no gradient is needed below the first layer
         wqkvT = tr(p + "wqkv.T", w["wqkv"], 3 * d, d)
@@ -657,7 +689,7 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
                         out_shape=(S, d), device=dev)
         dh = g.gemm(p + "d_attn_norm_out", V1, A1T, S, d, R, r=dh, alpha=sc, out_shape=(S, d), device=dev)
         dx = add(p + "d_x", dx1, rms_bwd(p + "d_x_norm", a["x"], w["wn1"], dh))
-    return g
+    return results
 
 
 def prefill_flops(cfg: LlamaConfig, seq: int, layers: int | None = None) -> float:

@@ -374,3 +374,34 @@ def test_oracle_executor_pinned_to_reference_token_machine(ref_memplan):
             assert got[(reader, producer)] != base[(reader, producer)], (i, w[:120])
     print("checked", checked, "races", races)
     assert checked > 100 and races > 20
+
+
+def test_lora_dp_graph_sums_replica_gradients():
+    """Config 4 over 2 memgraph devices (data parallel): the DP graph's loss
+    and adapter gradients are the fixed-order sums of the single-device
+    step's outputs on each replica's sequence (bitwise, fp32 sum -> bf16)."""
+    from oracle import ops_ref
+    from paper_2405_16283_b200 import workloads as W
+    from helpers import inputs_of, oracle_outputs
+
+    cfg = W.LlamaConfig(dim=256, layers=1, heads=2, ffn=256, vocab=300)
+    gd = W.llama_lora_step_dp(cfg, 128, 2)
+    mgd, _ = W.plan(gd, [1 << 30, 1 << 30])
+    inp = inputs_of(gd, seed=5)
+    got = oracle_outputs(gd, mgd, inp)
+    name_of = {o: gd.tensors[o].name[:-len(".sum")] for o in gd.outputs()}
+    per_rep = []
+    for r in range(2):
+        g1 = W.llama_lora_step(cfg, 128)
+        by = {t.name: t.id for t in gd.inputs()}
+        inp1 = {t.id: inp[by[t.name + ("@1" if r and t.name in ("tokens", "targets") else "")]] for t in g1.inputs()}
+        mg1, _ = W.plan(g1, 1 << 30)
+        o1 = oracle_outputs(g1, mg1, inp1)
+        per_rep.append({g1.tensors[o].name: o1[o] for o in g1.outputs()})
+    for o, name in name_of.items():
+        dt = gd.tensors[o].dtype
+        n = int(np.prod(gd.tensors[o].shape))
+        vals = [ops_ref.load(np.frombuffer(p[name], np.uint8), dt, n) for p in per_rep]
+        want = np.zeros(n * ops_ref.DT[dt], np.uint8)
+        ops_ref.store(want, dt, (vals[0].astype(np.float32) + vals[1].astype(np.float32)).astype(np.float32))
+        assert got[o][: want.size] == want.tobytes(), name
