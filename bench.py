@@ -616,7 +616,8 @@ def run_ours_on(args, world, rank, local, n, tp):
     (logits,) = g.outputs()
     logits_bytes = g.tensors[logits].nbytes
     pk = peaks()
-    exec_cfg = {"devices": devs, "streams_per_device": args.streams, "compute_tokens": args.compute_tokens}
+    exec_cfg = {"devices": devs, "streams_per_device": args.streams, "compute_tokens": args.compute_tokens,
+                "execution": args.execution}
 
     # ---- value: weights resident in HBM, materialised into the capped arena each step ----
     exv = Executor(mg, tg, {**exec_cfg, "input_residency": "device", "device_inputs": "copy"})
@@ -750,6 +751,8 @@ def main():
     ap.add_argument("--streams", type=int, default=5)
     ap.add_argument("--compute-tokens", type=int, default=1)
     ap.add_argument("--offload-steps", type=int, default=3)
+    ap.add_argument("--execution", default="events", choices=["events", "graph"],
+                    help="untimed runs through the host event loop, or replayed as one CUDA graph")
     ap.add_argument("--policy-trials", type=int, default=10)
     ap.add_argument("--no-offload-leg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -167,6 +167,29 @@ struct Executor::Impl {
     void build();
     void prepare_kernel(Instr& in, const MemVertex& v, const std::vector<std::pair<VertexId, VertexId>>& data_in);
     void launch(std::int32_t vidx, std::int32_t stream, std::int32_t after = -1);
+    void issue(std::int32_t vidx, cudaStream_t s, std::int32_t stream);
+
+    // --- graph mode ("execution": "graph") ------------------------------------------
+    // The memgraph as ONE CUDA graph: a node per vertex (its copy / kernel
+    // launches captured in isolation on the device's capture stream, added as
+    // a child-graph node) whose dependencies are exactly the vertex's memgraph
+    // in-edges. The GPU then resolves the dependencies itself: every vertex
+    // starts when its predecessors have finished (the event-driven contract,
+    // without a host round trip or a host API call per vertex). Built on the
+    // first untimed run of each policy, replayed afterwards.
+    struct GraphCache {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t x = nullptr;
+        RunStats counters;  // per-run launch / byte counters (static for a graph)
+        std::int64_t nodes = 0;
+    };
+    GraphCache graphs[2];           // [0] the memgraph, [1] its make_fixed_order form
+    std::vector<cudaStream_t> cap;  // per logical device: capture stream
+    bool capturing = false;
+    std::string graph_error;        // why graph mode fell back to the host loop (empty: it did not)
+    void drop_graphs();
+    void build_graph(const MemGraph& g, GraphCache& gc);
+    bool run_graph(const SchedulerPolicy& pol);
     // The CUDA stream a vertex runs on, as a dense lane id (device-major):
     // work on one lane completes in launch order, so completion polling only
     // ever needs to query the oldest in-flight vertex of each lane.
@@ -200,6 +223,7 @@ void Executor::Impl::build() {
     streams.resize(D);
     marker.assign(D, nullptr);
     compute.assign(D, nullptr);
+    cap.assign(D, nullptr);
     t0.resize(D);
     tend.resize(D);
     for (int d = 0; d < D; ++d) {
@@ -210,6 +234,7 @@ void Executor::Impl::build() {
         for (auto& s : streams[d]) TN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         TN_CUDA(cudaStreamCreateWithFlags(&marker[d], cudaStreamNonBlocking));
         TN_CUDA(cudaStreamCreateWithFlags(&compute[d], cudaStreamNonBlocking));
+        TN_CUDA(cudaStreamCreateWithFlags(&cap[d], cudaStreamNonBlocking));
         // One time origin per physical GPU: memgraph devices that share a GPU
         // share t0, so cross-device edges compare on one clock.
         int first = d;
@@ -659,6 +684,19 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
     if (after >= 0 && !(on_compute && prog[after].op == MemOpKind::Kernel && prog[after].dev == in.dev))
         TN_CUDA(cudaStreamWaitEvent(s, done_event(after), 0));
     if (timed) TN_CUDA(cudaEventRecord(ev_start[vidx], s));
+    issue(vidx, s, stream);
+    TN_CUDA(cudaEventRecord(done_event(vidx), s));
+    // instant vertices complete through the backend's instant queue at
+    // dispatch; a host callback as well would complete them twice
+    if (!cfg.poll && !in.instant) TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
+}
+
+// The vertex's own work on stream `s` (no timing / completion events): the
+// copy or kernel launch(es) of one memgraph vertex. Also what graph mode
+// captures, one vertex at a time.
+void Executor::Impl::issue(std::int32_t vidx, cudaStream_t s, std::int32_t stream) {
+    Instr& in = prog[vidx];
+    const bool on_compute = in.op == MemOpKind::Kernel && cfg.compute_tokens == 1;
     switch (in.op) {
         case MemOpKind::Input: {
             if (in.instant) break;  // readers use the staging copy in place
@@ -716,7 +754,7 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
             struct PdlScope {  // PDL for this launch only (untimed runs, compute stream)
                 explicit PdlScope(bool on) { k::set_pdl(on); }
                 ~PdlScope() { k::set_pdl(false); }
-            } pdl_scope(!timed && cfg.pdl && on_compute);
+            } pdl_scope(!timed && cfg.pdl && on_compute && !capturing);
             switch (op.type) {
                 case OpType::Gemm:
                     TN_CUDA(k::gemm_launch(*in.gemm, s, &gws[in.dev][stream < 0 ? 0 : stream]));
@@ -812,10 +850,6 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
             break;
         }
     }
-    TN_CUDA(cudaEventRecord(done_event(vidx), s));
-    // instant vertices complete through the backend's instant queue at
-    // dispatch; a host callback as well would complete them twice
-    if (!cfg.poll && !in.instant) TN_CUDA(cudaLaunchHostFunc(s, &Impl::on_done, &cb[vidx]));
 }
 
 // -------------------------------------------------------------------- run ---
@@ -932,8 +966,9 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
         fixed.reindex();
         g = &fixed;
     }
-    last = RunStats{};
     timed = trace != nullptr || cfg.all_timestamps;
+    if (cfg.graph && !timed && run_graph(pol)) return;
+    last = RunStats{};
     dispatched.clear();
     dispatched.reserve(g->vertices.size());
     stream_of.assign(g->vertices.size(), -1);
@@ -1080,7 +1115,10 @@ Executor::Impl::~Impl() {
     for (auto& ss : streams)
         for (auto s : ss)
             if (s) cudaStreamDestroy(s);
+    drop_graphs();
     for (auto s : marker)
+        if (s) cudaStreamDestroy(s);
+    for (auto s : cap)
         if (s) cudaStreamDestroy(s);
     for (auto s : compute)
         if (s) cudaStreamDestroy(s);
@@ -1097,6 +1135,136 @@ Executor::Impl::~Impl() {
         if (in.scratch) cudaFree(in.scratch);
     for (auto& [id, b] : slots)
         if (b.p) cudaFreeHost(b.p);
+}
+
+// -------------------------------------------------------------- graph mode ---
+void Executor::Impl::drop_graphs() {
+    for (auto& gc : graphs) {
+        if (gc.x) cudaGraphExecDestroy(gc.x);
+        if (gc.g) cudaGraphDestroy(gc.g);
+        gc = GraphCache{};
+    }
+}
+
+void Executor::Impl::build_graph(const MemGraph& g, GraphCache& gc) {
+    for (const auto& in : prog)
+        if (in.gemm && in.gemm->sk_tiles > 0)  // its partial-sum epochs advance per launch
+            throw Error("graph execution does not support stream-K GEMM tiles");
+    const size_t V = g.vertices.size();
+    GraphIndex gi(g);
+    std::vector<std::vector<std::int32_t>> preds(V);
+    for (size_t u = 0; u < V; ++u)
+        for (std::int32_t a = gi.succ_start[u]; a < gi.succ_start[u + 1]; ++a)
+            preds[gi.succ[a]].push_back(static_cast<std::int32_t>(u));
+    // a topological order: the build's total order (every edge points forward)
+    std::vector<std::int32_t> order;
+    if (g.total_order.size() == V) {
+        for (VertexId id : g.total_order) order.push_back(g.idx(id));
+    } else {
+        std::vector<std::int32_t> deg = gi.indeg;
+        for (size_t i = 0; i < V; ++i)
+            if (!deg[i]) order.push_back(static_cast<std::int32_t>(i));
+        for (size_t k = 0; k < order.size(); ++k)
+            for (std::int32_t a = gi.succ_start[order[k]]; a < gi.succ_start[order[k] + 1]; ++a)
+                if (--deg[gi.succ[a]] == 0) order.push_back(gi.succ[a]);
+    }
+    if (order.size() != V) throw Error("graph execution needs an acyclic memgraph");
+    TN_CUDA(cudaGraphCreate(&gc.g, 0));
+    std::vector<cudaGraphNode_t> node(V, nullptr);
+    const RunStats saved = last;
+    last = RunStats{};
+    capturing = true;
+    try {
+        std::vector<cudaGraphNode_t> deps;
+        for (std::int32_t v : order) {
+            deps.clear();
+            for (std::int32_t p : preds[v])
+                if (node[p]) deps.push_back(node[p]);
+            std::sort(deps.begin(), deps.end());
+            deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+            const Instr& in = prog[v];
+            if (in.instant) {  // no device work: a join point for its in-edges, if any
+                if (!deps.empty()) TN_CUDA(cudaGraphAddEmptyNode(&node[v], gc.g, deps.data(), deps.size()));
+                continue;
+            }
+            set_device(in.dev);
+            cudaGraph_t child = nullptr;
+            TN_CUDA(cudaStreamBeginCapture(cap[in.dev], cudaStreamCaptureModeThreadLocal));
+            try {
+                issue(v, cap[in.dev], 0);
+            } catch (...) {
+                cudaStreamEndCapture(cap[in.dev], &child);
+                if (child) cudaGraphDestroy(child);
+                throw;
+            }
+            TN_CUDA(cudaStreamEndCapture(cap[in.dev], &child));
+            size_t nn = 0;
+            TN_CUDA(cudaGraphGetNodes(child, nullptr, &nn));
+            if (nn == 0) TN_CUDA(cudaGraphAddEmptyNode(&node[v], gc.g, deps.data(), deps.size()));
+            else TN_CUDA(cudaGraphAddChildGraphNode(&node[v], gc.g, deps.data(), deps.size(), child));
+            cudaGraphDestroy(child);
+            gc.nodes++;
+        }
+        set_device(0);
+        TN_CUDA(cudaGraphInstantiate(&gc.x, gc.g, 0));
+    } catch (...) {
+        capturing = false;
+        last = saved;
+        if (gc.g) cudaGraphDestroy(gc.g);
+        gc = GraphCache{};
+        throw;
+    }
+    capturing = false;
+    gc.counters = last;
+    gc.counters.vertices = static_cast<std::int64_t>(V);
+    last = saved;
+}
+
+// One untimed run as a graph launch; false (host loop instead) when the
+// graph cannot be built for this memgraph (the reason is kept in graph_error).
+bool Executor::Impl::run_graph(const SchedulerPolicy& pol) {
+    if (!graph_error.empty()) return false;
+    GraphCache& gc = graphs[pol.kind == SchedulerKind::FixedOrder ? 1 : 0];
+    const auto w0 = std::chrono::steady_clock::now();
+    if (!gc.x) {
+        try {
+            if (pol.kind == SchedulerKind::FixedOrder) {
+                MemGraph fixed = make_fixed_order(m);
+                fixed.reindex();
+                build_graph(fixed, gc);
+            } else {
+                build_graph(m, gc);
+            }
+        } catch (const CudaError& e) {
+            graph_error = e.what();
+            cudaGetLastError();
+            cur_dev = -1;
+            return false;
+        }
+    }
+    for (int d = 0; d < D; ++d) {
+        set_device(d);
+        TN_CUDA(cudaDeviceSynchronize());
+    }
+    set_device(0);
+    cudaStream_t o = streams[0][0];
+    const auto w1 = std::chrono::steady_clock::now();
+    TN_CUDA(cudaEventRecord(t0[0], o));
+    TN_CUDA(cudaGraphLaunch(gc.x, o));
+    TN_CUDA(cudaEventRecord(tend[0], o));
+    const auto w2 = std::chrono::steady_clock::now();
+    TN_CUDA(cudaEventSynchronize(tend[0]));
+    const auto w3 = std::chrono::steady_clock::now();
+    float ms = 0;
+    TN_CUDA(cudaEventElapsedTime(&ms, t0[0], tend[0]));
+    last = gc.counters;
+    last.device_makespan_s = ms * 1e-3;
+    last.host_dispatch_s = std::chrono::duration<double>(w2 - w1).count();
+    last.host_wait_s = std::chrono::duration<double>(w3 - w2).count();
+    last.wall_s = std::chrono::duration<double>(w3 - w0).count();
+    last.graph_nodes = gc.nodes;
+    last_graph.reset();
+    return true;
 }
 
 // ------------------------------------------------------------- public API ---
@@ -1161,6 +1329,7 @@ void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool 
             b.p = nullptr;
             TN_CUDA(cudaMalloc(&b.p, std::max<std::size_t>(bytes, 1)));
             b.bytes = bytes;
+            impl_->drop_graphs();
         }
         TN_CUDA(cudaMemcpy(b.p, host, bytes, from_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
         return;
@@ -1172,6 +1341,7 @@ void Executor::set_input(VertexId id, const void* host, std::size_t bytes, bool 
         if (b.p) cudaFreeHost(b.p);
         b.p = pinned_alloc(bytes);
         b.bytes = bytes;
+        impl_->drop_graphs();  // captured copies hold the old buffer's address
     }
     if (from_device) TN_CUDA(cudaMemcpy(b.p, host, bytes, cudaMemcpyDeviceToHost));
     else std::memcpy(b.p, host, bytes);
@@ -1245,6 +1415,7 @@ std::string RunStats::to_json() const {
     j["host_dispatch_s"] = host_dispatch_s;
     j["host_wait_s"] = host_wait_s;
     j["device_makespan_s"] = device_makespan_s;
+    j["graph_nodes"] = graph_nodes;
     return j.dump();
 }
 
@@ -1266,6 +1437,9 @@ ExecConfig parse_exec_config(const std::string& text) {
         c.poll = comp == "poll";
         c.zero_copy_gathers = j.value("zero_copy_gathers", c.zero_copy_gathers);
         c.pdl = j.value("pdl", c.pdl);
+        const std::string ex = j.value("execution", std::string("events"));
+        if (ex != "events" && ex != "graph") throw ParseError("execution must be events or graph");
+        c.graph = ex == "graph";
         const std::string ts = j.value("timestamps", std::string("traced"));
         if (ts != "traced" && ts != "all") throw ParseError("timestamps must be traced or all");
         c.all_timestamps = ts == "all";

@@ -37,6 +37,10 @@ struct ExecConfig {
                                       // compute-stream kernels of untimed runs (each kernel's
                                       // prologue overlaps its predecessor's tail; paired A/B on the
                                       // 7B step: 49.72 vs 50.00 ms, tools/ab_exec_cfg.py)
+    bool graph = false;               // "execution": "events" (the host event loop) | "graph" (untimed
+                                      // runs replay the memgraph as one CUDA graph whose node
+                                      // dependencies are the memgraph edges; traced runs stay on the
+                                      // host loop)
     bool zero_copy_gathers = true;    // "zero_copy_gathers": host-resident inputs read only as the
                                       // table of embedding kernels stay in mapped pinned memory and
                                       // the kernel gathers its rows over PCIe (the Input vertex
@@ -58,6 +62,7 @@ struct RunStats {
     // pre-run synchronize -> end event recorded after the last vertex), no
     // per-vertex timestamps needed
     double device_makespan_s = 0;
+    std::int64_t graph_nodes = 0;  // > 0: the run was a CUDA graph launch of this many vertex nodes
     std::string to_json() const;
 };
 

@@ -772,3 +772,44 @@ def test_lora_data_parallel_two_devices_parity():
         _e = rel_err(out_values(g, o, res[0][o]), out_values(g, o, want[o]))
         record_err("gpu_exec", line=14, rel_err=_e, name=g.tensors[o].name)
         assert _e < 1.5e-2, g.tensors[o].name
+
+
+@pytest.mark.parametrize("which", ["llama_offload", "tp4_one_gpu", "lora"])
+def test_graph_mode_bitwise_equals_event_loop(which):
+    """"execution": "graph" replays the memgraph as one CUDA graph whose node
+    dependencies are exactly the memgraph edges (device-side event-driven
+    dispatch): outputs are bitwise those of the host event loop, for the
+    memgraph and for its fixed-order form, with offloads, reloads and
+    cross-device transfers; byte counters match the host loop's."""
+    if which == "llama_offload":
+        g, mg, _ = small_llama(seq=256, layers=2)
+        cfgs = {}
+    elif which == "tp4_one_gpu":
+        cfg = W.LlamaConfig(dim=1024, layers=2, heads=8, ffn=1024, vocab=1000)
+        g = W.llama_prefill_tp(cfg, 512, tp=4)
+        mg, _ = W.plan(g, [int(c * 1.5) // 1024 * 1024 for c in W.working_set_floor(g)], alloc_horizon="lazy")
+        cfgs = {"devices": [0, 0, 0, 0]}
+    else:
+        cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=512, vocab=1000)
+        g = W.llama_lora_step(cfg, 256)
+        mg, _ = W.plan(g, int(W.working_set_floor(g)[0] * 2.0), alloc_horizon="lazy")
+        cfgs = {}
+    inp = inputs_of(g, seed=71)
+    outs = g.outputs()
+    res = {}
+    for mode in ("events", "graph"):
+        with Executor(mg, g.to_json(), {**cfgs, "execution": mode}) as ex:
+            for vid, a in inp.items():
+                ex.set_input(vid, a)
+            for pol in ("event-driven", "fixed-order"):
+                for rep in range(2):
+                    ex.run(pol, "fifo", 0, trace=False)
+                    st = ex.stats()
+                    assert (st["graph_nodes"] > 0) == (mode == "graph"), st
+                    res[(mode, pol, rep)] = ({o: ex.get_output(o, g.tensors[o].nbytes) for o in outs},
+                                             {k: st[k] for k in ("h2d_bytes", "d2h_bytes", "d2d_bytes", "p2p_bytes",
+                                                                 "kernel_launches")})
+    base = res[("events", "event-driven", 0)]
+    for k, v in res.items():
+        assert v[0] == base[0], k
+        assert v[1] == base[1], (k, v[1], base[1])

@@ -24,6 +24,7 @@ ap.add_argument("--tp", type=int, default=8)
 ap.add_argument("--cap-gib", type=float, default=8)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--residency", default="host")
+ap.add_argument("--execution", default="events")
 a = ap.parse_args()
 cfg = W.LLAMA_65B if a.model == "65b" else W.LLAMA_7B
 t0 = time.time()
@@ -31,7 +32,8 @@ g = W.llama_prefill_tp(cfg, a.seq, a.tp, layers=a.layers)
 mg, st = W.plan(g, [int(a.cap_gib * (1 << 30))] * a.tp, alloc_horizon="lazy")
 plan_s = time.time() - t0
 ngpu = torch.cuda.device_count()
-ex = Executor(mg, g.to_json(), {"input_residency": a.residency, "devices": [d % ngpu for d in range(a.tp)]})
+ex = Executor(mg, g.to_json(), {"input_residency": a.residency, "devices": [d % ngpu for d in range(a.tp)],
+                                "execution": a.execution})
 t1 = time.time()
 in_bytes = 0
 for t in g.inputs():  # generate each input on its GPU, hand it over, drop it
@@ -42,6 +44,7 @@ for t in g.inputs():  # generate each input on its GPU, hand it over, drop it
 torch.cuda.empty_cache()
 load_s = time.time() - t1
 ts = bench.untimed_steps(ex, a.steps)  # timing-free completion events
+st_untimed = ex.stats()
 tr = json.loads(ex.run())  # one traced step (per-vertex timestamps) for the breakdown
 ids = {v["id"]: v for v in json.loads(g.to_json())["vertices"]}
 by_op = {}
@@ -67,6 +70,9 @@ print(json.dumps({"workload": f"llama_{a.model}_tp{a.tp}_seq{a.seq}_layers{a.lay
                   "exposed_transfer_s": round(stt["exposed_transfer_s"], 4),
                   "exposed_transfer_gpu_s": round(stt["exposed_transfer_gpu_s"], 4), "pcie_h2d_gbs": round(pcie, 1),
                   "host_dispatch_s": round(stt["host_dispatch_s"], 4), "host_wait_s": round(stt["host_wait_s"], 4),
+                  "untimed_host_dispatch_s": round(st_untimed["host_dispatch_s"], 4),
+                  "untimed_host_dispatch_us_per_vertex": round(st_untimed["host_dispatch_s"] * 1e6 / len(json.loads(mg)["vertices"]), 2),
+                  "execution": a.execution, "graph_nodes": st_untimed.get("graph_nodes", 0),
                   "roofline": {"compute_s": round(compute_s, 4), "pcie_h2d_s": round(pcie_s, 4),
                                "bound": "pcie" if pcie_s > compute_s else "tensor",
                                "frac": round(bound / step, 4)},
