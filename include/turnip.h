@@ -105,6 +105,10 @@ int tn_make_fixed_order(const char* memgraph_json, char** memgraph_out, char** e
  *                                   events only (a timing event between kernels costs ~3 us);
  *                                   "all": every run is timestamped (last_trace() after any run)
  *   "pdl": true                     programmatic dependent launch between kernels of untimed runs
+ *   "execution": "events"           "events": the host event loop; "graph": untimed runs replay the
+ *                                   memgraph as one CUDA graph (a node per vertex, dependencies =
+ *                                   memgraph edges: the GPU dispatches each vertex when its
+ *                                   predecessors finished); traced runs use the host loop
  *   "elide_input_offloads": true    an evicted input is reloaded from its own copy, never offloaded
  *   "materialize_inputs": true, "timeout_s": 600 */
 int tn_exec_create(const char* memgraph_json, const char* taskgraph_json, const char* config_json,

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(gen_base + kQ + 2 * kKst + 2 * kV);
     const std::uint32_t b0 = smem_u32(bars);
     const std::uint32_t q_full = b0, k_full = b0 + 8, k_empty = b0 + 24, v_full = b0 + 40, v_empty = b0 + 56,
-                        s_full = b0 + 72, s_free = b0 + 80, p_full = b0 + 88, o_done = b0 + 96;
+                        s_full = b0 + 72, p_full = b0 + 88, o_done = b0 + 96;  // s_full[2]
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 13);
 
     pdl_trigger();
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(v_empty, 1);
         mbar_init(v_empty + 8, 1);
         mbar_init(s_full, 1);
-        mbar_init(s_free, 4);
+        mbar_init(s_full + 8, 1);
         mbar_init(p_full, 4);
         mbar_init(o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -124,7 +124,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_after();
     pdl_wait();  // the previous kernel's outputs (q, k, vT) are complete and visible
     const std::uint32_t tmem = *tmem_slot;
-    const std::uint32_t tS = tmem, tP = tmem + 64, tO = tmem + 128;
+    // S double-buffered: S_j in columns [64*(j%2), +64), and P_j (bf16, 32
+    // columns) written over S_j once the softmax has it in registers. S_{j+1}
+    // is computed while the softmax works on S_j; S_{j+2} reuses buffer j%2
+    // after P_j·V (MMAs of one issuer execute in order).
+    const std::uint32_t tS = tmem, tO = tmem + 128;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -147,32 +151,33 @@ __global__ void __launch_bounds__(kThreads, 2)
         {  // whole warp: one elected lane issues (tc_mma)
             const std::uint32_t idesc_s = make_idesc(1u, kB, kN);
             const std::uint32_t idesc_o = make_idesc(1u, kB, kHd);
-            auto issue_s = [&](int j) {
+            auto issue_s = [&](int j) {  // K stage and S buffer are both j % 2
                 const int st = j & 1;
                 mbar_wait(k_full + 8 * st, (j >> 1) & 1);
-                if (j > 0) mbar_wait(s_free, (j - 1) & 1);  // softmax pulled S_{j-1} into registers
                 tc_fence_after();
                 const std::uint32_t dk = sK0 + st * kKst;
 #pragma unroll
                 for (int kk = 0; kk < kHd / 16; ++kk)
-                    tc_mma(tS, sdesc(sQ + (kk >> 2) * (kQ / 2) + (kk & 3) * 32),
+                    tc_mma(tS + 64 * st, sdesc(sQ + (kk >> 2) * (kQ / 2) + (kk & 3) * 32),
                            sdesc(dk + (kk >> 2) * (kKst / 2) + (kk & 3) * 32), idesc_s, kk != 0, false);
-                tc_commit(s_full);
+                tc_commit(s_full + 8 * st);
                 tc_commit(k_empty + 8 * st);
             };
             mbar_wait(q_full, 0);
             issue_s(0);
+            if (nkv > 1) issue_s(1);
             for (int j = 0; j < nkv; ++j) {
-                if (j + 1 < nkv) issue_s(j + 1);
                 mbar_wait(p_full, j & 1);
                 mbar_wait(v_full + 8 * (j & 1), (j >> 1) & 1);
                 tc_fence_after();
                 const std::uint32_t dv = sV + (j & 1) * kV;
+                const std::uint32_t tPj = tS + 64 * (j & 1);
 #pragma unroll
                 for (int kk = 0; kk < kN / 16; ++kk)
-                    tc_mma_ts(tO, tP + kk * 8, sdesc(dv + kk * 32), idesc_o, (j | kk) != 0);
+                    tc_mma_ts(tO, tPj + kk * 8, sdesc(dv + kk * 32), idesc_o, (j | kk) != 0);
                 tc_commit(o_done);
                 tc_commit(v_empty + 8 * (j & 1));
+                if (j + 2 < nkv) issue_s(j + 2);  // into buffer j%2, after P_j·V
             }
         }
     } else {
@@ -183,20 +188,18 @@ __global__ void __launch_bounds__(kThreads, 2)
         float m = -INFINITY, l = 0.f;
         constexpr int kW = 8;
         for (int j = 0; j < nkv; ++j) {
-            mbar_wait(s_full, j & 1);
+            const std::uint32_t tSj = tS + 64 * (j & 1);
+            mbar_wait(s_full + 8 * (j & 1), (j >> 1) & 1);
             tc_fence_after();
             float s[CW];
 #pragma unroll
             for (int c = 0; c < CW; c += 32) {
                 std::uint32_t u[32];
-                TN_LD32(tS + trow + c, u);
+                TN_LD32(tSj + trow + c, u);
 #pragma unroll
                 for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(u[i]);
             }
             tc_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(s_free);
 
             // masked keys: key index j*kN + c > query row (causal)
             const int lim = p.causal ? qrow - j * kN : CW;  // columns c <= lim are valid
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     __nv_bfloat162 v2 = __floats2bfloat162_rn(s[2 * i], s[2 * i + 1]);
                     pw[i] = *reinterpret_cast<std::uint32_t*>(&v2);
                 }
-                TN_ST32(tP + trow, pw);
+                TN_ST32(tSj + trow, pw);  // P_j over S_j (already in registers)
                 tc_wait_st();
             }
             tc_fence_before();
