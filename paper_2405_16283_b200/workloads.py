@@ -475,7 +475,8 @@ def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = N
 
 
 def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank: int = 16, rank_pad: int = 64,
-                    lora_alpha: float = 16.0, std: float = 0.02, device: int = 0) -> GraphBuilder:
+                    lora_alpha: float = 16.0, std: float = 0.02, device: int = 0,
+                    recompute_attention: bool = True) -> GraphBuilder:
     """Config 4: one LoRA fine-tuning step (forward + backward) of a LLaMA
     model over `seq` tokens, rank-`rank` adapters on the fused QKV projection
     and on both FFN projections ("rank 16 on Q,K,V,FFN"), frozen
@@ -489,14 +490,22 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     Backward GEMMs need transposed operands (dX = dY·W, dW = dYᵀ·X); they
     are expressed as explicit `transpose` vertices feeding the K-major GEMM
     task, and the attention backward as dP = dO·Vᵀ -> softmax_bwd ->
-    dQ = dS·K, dK = dSᵀ·Q, dV = Pᵀ·dO (materialised n² tiles)."""
+    dQ = dS·K, dK = dSᵀ·Q, dV = Pᵀ·dO (materialised n² tiles).
+
+    With `recompute_attention` (default; SURVEY §8d "fwd + bwd with
+    recompute") the backward recomputes P = softmax(scale·QKᵀ) from the saved
+    q and k instead of keeping the forward's P (H·S² bf16 = 1 GB per 7B layer)
+    live across the step: the planner then never offloads the n² tensor, at the
+    cost of one more causal scores GEMM + softmax per layer. The recomputed P
+    is bitwise the forward's (same kernels, same inputs)."""
     g = GraphBuilder(device_count=1)
-    _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "")
+    _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "", recompute_attention)
     return g
 
 
 def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None = None, rank: int = 16,
-                       rank_pad: int = 64, lora_alpha: float = 16.0, std: float = 0.02) -> GraphBuilder:
+                       rank_pad: int = 64, lora_alpha: float = 16.0, std: float = 0.02,
+                       recompute_attention: bool = True) -> GraphBuilder:
     """Config 4 over `dp` devices (data parallel): every memgraph
     device runs the full LoRA step on its own sequence (tokens/targets
     `@r`; the frozen weights and adapters are the same tensors on every device,
@@ -506,8 +515,8 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
     into `sum` combines, no NCCL. Outputs: the summed loss and gradients
     (same names as llama_lora_step's). Global batch = dp sequences."""
     g = GraphBuilder(device_count=dp)
-    outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "")
-            for r in range(dp)]
+    outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "",
+                            recompute_attention) for r in range(dp)]
     for name, v0 in outs[0].items():
         t = g.tensors[v0]
         n = int(np.prod(t.shape))
@@ -518,7 +527,7 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
 
 
 def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, rank_pad, lora_alpha, std, device,
-                    data_sfx) -> dict:
+                    data_sfx, recompute_attention=True) -> dict:
     """Appends one LoRA step on `device` to `g`; returns {output name: vid}
     (the loss and every adapter gradient)."""
     L = cfg.layers if layers is None else layers
@@ -645,7 +654,14 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
         do = g.gemm(p + "d_attn", dx1, woT, S, d, d, out_shape=(S, d), device=dev)
         dP = g.gemm(p + "d_probs", do, a["qkv"], S, S, hd, batch=H, lda=d, sa=hd, ldb=3 * d, b_off=2 * d, sb=hd,
                     sc=S * S, out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
-        dS = g.kernel(p + "d_scores", {"type": "softmax_bwd", "args": [a["P"], dP], "batch": H, "rows": S, "cols": S,
+        if recompute_attention:  # P again from the saved q, k (bitwise the forward's)
+            scr_b = g.gemm(p + "scores.re", a["q"], a["k"], S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S,
+                           out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
+            P = g.kernel(p + "probs.re", {"type": "softmax", "args": [scr_b], "batch": H, "rows": S, "cols": S,
+                                          "scale": scale, "causal": 1}, (H, S, S), "bf16", dev)
+        else:
+            P = a["P"]
+        dS = g.kernel(p + "d_scores", {"type": "softmax_bwd", "args": [P, dP], "batch": H, "rows": S, "cols": S,
                                        "causal": 1, "in_dtype": "f32"}, (H, S, S), "bf16", dev)
         kT = tr(p + "k.T", a["k"], S, hd, batch=H)
         dq_r = g.gemm(p + "d_q_rot", dS, kT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
@@ -654,7 +670,7 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
         qT = tr(p + "q.T", a["q"], S, hd, batch=H)
         dk_r = g.gemm(p + "d_k_rot", dST, qT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
                       alpha=scale, out_shape=(S, d), device=dev)
-        PT = tr(p + "probs.T", a["P"], S, S, batch=H)
+        PT = tr(p + "probs.T", P, S, S, batch=H)
         doT = g.kernel(p + "d_attn.T", {"type": "transpose_heads", "args": [do], "seq": S, "ld": d, "col_off": 0,
                                         "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
         dv = g.gemm(p + "d_v", PT, doT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,

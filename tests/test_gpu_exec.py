@@ -813,3 +813,54 @@ def test_graph_mode_bitwise_equals_event_loop(which):
     for k, v in res.items():
         assert v[0] == base[0], k
         assert v[1] == base[1], (k, v[1], base[1])
+
+
+def test_unaligned_placements_take_gpu_fallback_paths():
+    """A graph whose sizes are padded only to 4 bytes (not the generators'
+    1 KiB): placements land on 4-byte but not 16-byte boundaries, so TMA and
+    128-bit paths are illegal and every op must take its SIMT / scalar GPU
+    path — never a CPU path — and still match the oracle."""
+    S, H, hd = 128, 2, 64
+    d = H * hd
+    g = W.GraphBuilder()
+    x = g.input("x", (S, d), "bf16", init=("normal", 1.0))
+    w = g.input("w", (d,), "bf16", init=("normal", 1.0))
+    wq = g.input("wq", (d, d), "bf16", init=("normal", 0.1))
+    x32 = g.input("x32", (S, d), "f32", init=("normal", 1.0))
+    qkv = g.input("qkv", (S, 3 * d), "bf16", init=("normal", 1.0))
+    tab = g.input("tab", (S, hd // 2, 2), "f32", init=("rope", 10000.0))
+    sc = g.input("sc", (H, S, S), "f32", init=("normal", 2.0))
+    gu = g.input("gu", (S, 2 * d), "bf16", init=("normal", 1.0))
+    outs = [
+        g.kernel("rms", {"type": "rmsnorm", "args": [x, w], "rows": S, "cols": d, "eps": 1e-5}, (S, d), "bf16"),
+        g.gemm("mm", x, wq, S, d, d, out_shape=(S, d)),
+        g.gemm("mm32", x32, x32, S, S, d, in_dtype="f32", out_dtype="f32", out_shape=(S, S)),
+        g.kernel("q", {"type": "rope", "args": [qkv, tab], "seq": S, "ld": 3 * d, "col_off": 0, "heads": H,
+                       "hd": hd}, (H, S, hd), "bf16"),
+        g.kernel("vt", {"type": "transpose_heads", "args": [qkv], "seq": S, "ld": 3 * d, "col_off": 2 * d,
+                        "heads": H, "hd": hd}, (H, hd, S), "bf16"),
+        g.kernel("p", {"type": "softmax", "args": [sc], "batch": H, "rows": S, "cols": S, "scale": 0.2,
+                       "causal": 1}, (H, S, S), "bf16"),
+        g.kernel("act", {"type": "silu_mul", "args": [gu], "rows": S, "cols": d}, (S, d), "bf16"),
+        g.kernel("sum", {"type": "sum", "args": [x, x], "count": S * d, "in_dtype": "bf16", "out_dtype": "f32"},
+                 (S, d), "f32"),
+        g.kernel("cast", {"type": "cast", "args": [x32], "count": S * d, "in_dtype": "f32", "out_dtype": "bf16"},
+                 (S, d), "bf16"),
+    ]
+    q, vt = outs[3], outs[4]
+    k = g.kernel("k", {"type": "rope", "args": [qkv, tab], "seq": S, "ld": 3 * d, "col_off": d, "heads": H,
+                       "hd": hd}, (H, S, hd), "bf16")
+    outs.append(g.kernel("o", {"type": "attention", "args": [q, k, vt], "heads": H, "seq": S, "hd": hd, "ldo": d,
+                               "scale": hd ** -0.5, "causal": 1}, (S, d), "bf16"))
+    for v in g.vertices:  # 4-byte granularity instead of 1 KiB
+        v["output_size"] = g.tensors[v["id"]].nbytes + 4
+    mg, _ = W.plan(g, 1 << 26)
+    pl = json.loads(mg)["placement"]
+    assert any(p["offset"] % 16 for p in pl.values())
+    inp = inputs_of(g, seed=77)
+    _, got = run_gpu(g, mg, inp)
+    want = oracle_outputs(g, mg, inp)
+    for o in outs:
+        e = rel_err(out_values(g, o, got[o]), out_values(g, o, want[o]))
+        record_err("unaligned", name=g.tensors[o].name, rel_err=e)
+        assert e < 1e-2, (g.tensors[o].name, e)
