@@ -246,6 +246,38 @@ def measure_pcie(device, direction="h2d") -> float:
     return best
 
 
+def measure_pcie_duplex(device) -> float:
+    """Aggregate GB/s of a concurrent pinned H2D + D2H pair (1 GiB each, two
+    streams), best of 4: the duplex link bound for plans that overlap them."""
+    import torch
+
+    n = 1 << 30
+    h1, h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True), torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    best = 0.0
+    with torch.cuda.device(device):
+        d1, d2 = torch.empty(n, dtype=torch.uint8, device=device), torch.empty(n, dtype=torch.uint8, device=device)
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        cur = torch.cuda.current_stream()
+        for _ in range(4):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            s1.wait_stream(cur)
+            s2.wait_stream(cur)
+            with torch.cuda.stream(s1):
+                d1.copy_(h1, non_blocking=True)
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+            cur.wait_stream(s1)
+            cur.wait_stream(s2)
+            e1.record()
+            e1.synchronize()
+            best = max(best, 2 * n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        del d1, d2
+    del h1, h2
+    return best
+
+
 def measure_p2p(a: int, b: int) -> float | None:
     """Peer copy bandwidth GPU a -> GPU b (GB/s), 1 GiB, best of 3."""
     import torch

@@ -108,6 +108,9 @@ struct Executor::Impl {
         bool elided = false;      // offload of an unmodified input: no copy
         bool instant = false;     // aliased Input: completes at dispatch, no stream, no copy
         bool timeless = false;    // instant with no in-edges: no device timestamps (trace time 0)
+        // instant (non-timeless) predecessors: their marker event is waited on
+        // device, so the trace's start >= each predecessor's end on every edge
+        std::vector<std::int32_t> instant_preds;
         const OpDesc* op_desc = nullptr;
         std::vector<const char*> argp;  // resolved argument pointers
         std::unique_ptr<k::GemmPlan> gemm;
@@ -377,6 +380,14 @@ void Executor::Impl::build() {
                 break;
             }
             case MemOpKind::Kernel: prepare_kernel(in, v, din); break;
+        }
+    }
+    {
+        std::unordered_map<VertexId, std::int32_t> vidx;
+        for (size_t i = 0; i < V; ++i) vidx[m.vertices[i].id] = static_cast<std::int32_t>(i);
+        for (const auto& e : m.edges) {
+            const std::int32_t f = vidx.at(e.from), t = vidx.at(e.to);
+            if (prog[f].instant && !prog[f].timeless && !prog[t].instant) prog[t].instant_preds.push_back(f);
         }
     }
     // Pinned offload slots (one per evicted root, reused across generations:
@@ -683,6 +694,9 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
     // lookahead: run behind `after` (same stream when both are on the compute stream)
     if (after >= 0 && !(on_compute && prog[after].op == MemOpKind::Kernel && prog[after].dev == in.dev))
         TN_CUDA(cudaStreamWaitEvent(s, done_event(after), 0));
+    // An instant predecessor completed at dispatch on the host, but its marker
+    // timestamp is recorded on another stream: order this vertex behind it.
+    for (std::int32_t p : in.instant_preds) TN_CUDA(cudaStreamWaitEvent(s, done_event(p), 0));
     if (timed) TN_CUDA(cudaEventRecord(ev_start[vidx], s));
     issue(vidx, s, stream);
     TN_CUDA(cudaEventRecord(done_event(vidx), s));

@@ -729,43 +729,6 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
 //   tempty[a] leader only: 8 arrivals (4 epilogue warps x 2 CTAs)
 constexpr int kStages2 = 6;
 
-__device__ __forceinline__ std::uint32_t cluster_rank() {
-    std::uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ std::uint32_t mapa(std::uint32_t addr, std::uint32_t rank) {
-    std::uint32_t out;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
-    return out;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_3d_2sm(std::uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                                std::uint32_t leader_bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-        "%4}], [%5];" ::"r"(dst),
-        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
-        : "memory");
-}
-__device__ __forceinline__ void tc_mma_2sm(std::uint32_t d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
-                                           std::uint32_t accum, bool tf32) {
-    if (tf32) {
-        asm volatile(
-            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-            "l"(a), "l"(b), "r"(idesc), "r"(accum)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-            "l"(a), "l"(b), "r"(idesc), "r"(accum)
-            : "memory");
-    }
-}
 __device__ __forceinline__ long long sk_begin(const Params& p, int q, int npairs) {
     return p.sk_total * q / npairs;
 }
@@ -820,17 +783,6 @@ __device__ __forceinline__ void for_each_segment(const Params& p, int pair, int 
     }
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_commit_2sm(std::uint32_t bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
-        "h"(static_cast<unsigned short>(3))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(std::uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_kernel_2sm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,

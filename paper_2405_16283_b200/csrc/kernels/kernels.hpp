@@ -115,9 +115,9 @@ struct AttnArgs {
     int causal = 1;
 };
 struct alignas(64) AttnPlan {
-    CUtensorMap tq, tk, tv;
+    CUtensorMap tq, tk, tv, tv2;
     AttnArgs args;
-    int path = 0;  // 0 tcgen05 fused, 1 SIMT fallback
+    int path = 0;  // 0 tcgen05 fused (1 CTA per 128 rows), 1 SIMT fallback, 2 tcgen05 CTA pairs (seq % 256 == 0)
 };
 cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan);
 cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s);

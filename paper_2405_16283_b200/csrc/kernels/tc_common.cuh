@@ -138,6 +138,20 @@ __device__ __forceinline__ std::uint64_t sdesc(std::uint32_t saddr) {
         "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])                   \
         : "memory")
 
+#define TN_ST16(taddr, r)                                                                                     \
+    asm volatile(                                                                                             \
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])           \
+        : "memory")
+
+// max(a, b, c) in one instruction (FMNMX3, sm_100).
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 // 2^x on the SFU (MUFU.EX2), flushing denormal results to zero.
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -181,6 +195,71 @@ __device__ __forceinline__ void tmem_free(std::uint32_t taddr, std::uint32_t col
 __host__ __device__ constexpr std::uint32_t make_idesc(std::uint32_t fmt, int M, int N) {
     return (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<std::uint32_t>(N >> 3) << 17) |
            (static_cast<std::uint32_t>(M >> 4) << 24);
+}
+
+// CTA-pair (cta_group::2) helpers: cluster rank, peer smem addresses, TMA
+// loads that signal the leader CTA's barrier, pair MMAs and multicast commits.
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+    std::uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ std::uint32_t mapa(std::uint32_t addr, std::uint32_t rank) {
+    std::uint32_t out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+    return out;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(std::uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                std::uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_2sm(std::uint32_t d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                           std::uint32_t accum, bool tf32) {
+    if (tf32) {
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accum)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accum)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tc_commit_2sm(std::uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+        "h"(static_cast<unsigned short>(3))
+        : "memory");
+}
+// Arrive on a barrier in a peer CTA's shared memory (mapa address). Default
+// .release.cta semantics: the arrivals here only publish tensor-memory
+// accesses, which the tcgen05 fences order; .release.cluster would add a
+// MEMBAR.ALL.GPU to every arrive.
+__device__ __forceinline__ void mbar_arrive_remote(std::uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// Pair MMA with the A operand from tensor memory (each CTA's TMEM holds its
+// 128 rows of A at the same address), B from shared memory.
+__device__ __forceinline__ void tc_mma_ts_2sm(std::uint32_t d, std::uint32_t a_tmem, std::uint64_t b,
+                                              std::uint32_t idesc, std::uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum)
+        : "memory");
 }
 
 // Kernel launch with the PDL attribute when the dispatcher enabled it.

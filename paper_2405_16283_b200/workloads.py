@@ -719,7 +719,7 @@ def prefill_flops(cfg: LlamaConfig, seq: int, layers: int | None = None) -> floa
 
 # ------------------------------------------ long-context blockwise attention (cfg 5) ---
 def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: int = 4096,
-                        device: int = 0, lag: int | None = None) -> GraphBuilder:
+                        device: int = 0, lag: int | None = None, interleave: str = "head") -> GraphBuilder:
     """Config 5: causal attention over `seq` tokens with the n^2 score tiles
     materialised as vertices and kept live across a two-pass softmax, so a
     capped plan must offload them to host RAM.
@@ -736,7 +736,10 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
     and its pass 2: pass 2 of head h is listed right after pass 1 of head
     h + lag, so `lag` heads of score tiles are live at once — enough to force
     offloads under a cap while letting the D2H of new tiles overlap the H2D of
-    old ones (duplex PCIe)."""
+    old ones (duplex PCIe). `interleave="block"` lists the two passes query
+    block by query block (pass 1 of (h + lag, i), then pass 2 of (h, i)), so
+    the tiles being produced (offloaded) and the tiles being consumed
+    (reloaded) alternate at tile granularity instead of head granularity."""
     assert seq % tile == 0
     nb = seq // tile
     T = tile
@@ -749,8 +752,8 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
     S, ml = {}, {}
     lag = heads if lag is None else max(0, min(lag, heads))
 
-    def pass1(h):
-        for i in range(nb):
+    def pass1(h, blocks=None):
+        for i in (range(nb) if blocks is None else blocks):
             parts = []
             for j in range(i + 1):
                 S[(h, i, j)] = g.gemm(f"S[{h},{i},{j}]", q[(h, i)], k[(h, j)], T, T, hd, alpha=scale,
@@ -759,8 +762,8 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
                                                             "cols": T, "causal": int(i == j)}, (T, 2), "f32", dev))
             ml[(h, i)] = g.kernel(f"ml[{h},{i}]", {"type": "stats_combine", "args": parts, "rows": T}, (T, 2), "f32", dev)
 
-    def pass2(h):
-        for i in range(nb):
+    def pass2(h, blocks=None):
+        for i in (range(nb) if blocks is None else blocks):
             acc = None
             for j in range(i + 1):
                 P = g.kernel(f"P[{h},{i},{j}]", {"type": "softmax_apply", "args": [S[(h, i, j)], ml[(h, i)]], "rows": T,
@@ -770,7 +773,13 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
             g.kernel(f"out[{h},{i}]", {"type": "cast", "args": [acc], "count": T * hd, "in_dtype": "f32",
                                        "out_dtype": "bf16"}, (T, hd), "bf16", dev)
 
+    assert interleave in ("head", "block")
     for step in range(heads + lag):
+        if interleave == "block" and step < heads and step - lag >= 0:
+            for i in range(nb):
+                pass1(step, [i])
+                pass2(step - lag, [i])
+            continue
         if step < heads:
             pass1(step)
         if step - lag >= 0:

@@ -202,6 +202,8 @@ def test_rowops_and_eltwise_parity():
 
 @pytest.mark.parametrize("seq,hd,causal,sigma", [(256, 128, 1, 1.0), (512, 128, 1, 1.0), (256, 128, 0, 1.0),
                                                  (200, 64, 1, 1.0),
+                                                 # seq % 256 != 0: the 1-CTA kernel (pairs need 256-row blocks)
+                                                 (384, 128, 1, 1.0), (384, 128, 0, 4.0),
                                                  # scores with std ~16: the running max moves by > 2^8
                                                  # (lazy O rescale), most exp2 underflow (poly clamp)
                                                  (1024, 128, 1, 4.0), (512, 128, 0, 4.0)])

@@ -18,10 +18,12 @@ ap.add_argument("--cap-gib", type=float, default=16)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--policy", default="event-driven")
 ap.add_argument("--lag", type=int, default=None)
+ap.add_argument("--horizon", default="lazy")
+ap.add_argument("--interleave", default="head")
 a = ap.parse_args()
 t0 = time.time()
-g = W.blockwise_attention(a.seq, a.heads, 128, a.tile, lag=a.lag)
-mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon="lazy")
+g = W.blockwise_attention(a.seq, a.heads, 128, a.tile, lag=a.lag, interleave=a.interleave)
+mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon=a.horizon)
 m = json.loads(mg)
 off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
 rel = sum(v["size"] for v in m["vertices"] if v["op"] == "reload")
@@ -36,6 +38,7 @@ for k, v in inputs.items():
 del inputs
 setup_s = time.time() - t1
 pcie = bench.measure_pcie(dev)
+duplex = bench.measure_pcie_duplex(dev)
 pk = bench.peaks()
 times = bench.untimed_steps(ex, a.steps, a.policy)  # timing-free completion events
 tr = json.loads(ex.run(a.policy, "fifo", 0))  # one traced step: exposed transfer / kernel busy
@@ -43,7 +46,9 @@ stt = ex.stats()
 flops = W.blockwise_attention_flops(a.seq, a.heads, 128, a.tile)
 roof = max(stt["h2d_bytes"] / (pcie * 1e9), stt["d2h_bytes"] / (pcie * 1e9), flops / (pk["bf16_tflops_sustained"] * 1e12))
 best = min(times)
-print(json.dumps({"workload": f"blockwise_attention_seq{a.seq}_h{a.heads}_tile{a.tile}_lag{a.lag}_cap{a.cap_gib}GiB",
+dup_s = max((stt["h2d_bytes"] + stt["d2h_bytes"]) / (duplex * 1e9), stt["h2d_bytes"] / (pcie * 1e9))
+plan_ideal = bench.plan_ideal_s(mg, pcie)
+print(json.dumps({"workload": f"blockwise_attention_seq{a.seq}_h{a.heads}_tile{a.tile}_lag{a.lag}_cap{a.cap_gib}GiB_{a.horizon}_{a.interleave}",
                   "memgraph_vertices": len(m["vertices"]), "plan": st, "plan_s": round(plan_s, 2),
                   "setup_s": round(setup_s, 1), "offload_gb": round(off / 1e9, 2), "reload_gb": round(rel / 1e9, 2),
                   "input_gb": round(inb / 1e9, 2), "step_s": [round(x, 4) for x in times],
@@ -52,4 +57,6 @@ print(json.dumps({"workload": f"blockwise_attention_seq{a.seq}_h{a.heads}_tile{a
                   "d2h_gbs": round(stt["d2h_bytes"] / best / 1e9, 1), "pcie_h2d_measured_gbs": round(pcie, 1),
                   "roofline_s": round(roof, 4), "frac_of_roofline": round(roof / best, 4),
                   "exposed_transfer_s": round(stt["exposed_transfer_s"], 3), "kernel_busy_s": round(stt["kernel_busy_s"], 4),
+                  "pcie_duplex_measured_gbs": round(duplex, 1), "duplex_bound_s": round(dup_s, 4),
+                  "frac_of_duplex_bound": round(dup_s / best, 4), "plan_ideal_s": round(plan_ideal, 4),
                   "flops": flops, "wall_s": round(stt["wall_s"], 3)}), flush=True)
