@@ -406,4 +406,98 @@ ComparisonSummary summarize_pairs(const std::vector<double>& ev, const std::vect
 std::string serialize_profile(const DeviceProfile& p);
 DeviceProfile parse_profile(const std::string& text);
 
+
+// Device-dependency variant (executor config "dependencies": "device"): a
+// vertex becomes a candidate as soon as every predecessor has been
+// DISPATCHED; the backend makes it wait on the device for the predecessors
+// that have not completed (CUDA events; kernel -> kernel on one device is
+// ordered by the compute stream), so the host round trip between a copy and
+// the kernel that consumes it (or the offload of a freshly produced tile)
+// leaves the critical path. Resources are the reference's (stream slots,
+// host_in / host_out per device, held from dispatch to completion); kernels
+// of a device run in order on its compute stream, at most 1 + `lookahead`
+// in flight. Each sweep first dispatches candidates whose predecessors have
+// all completed (tie-break order), then the early ones. Outputs are
+// unchanged: every memgraph edge is enforced on the GPU.
+// Backend additionally provides:
+//   void launch_waits(std::int32_t vidx, std::int32_t stream, const std::int32_t* waits, int n, double now);
+template <class Backend>
+void dispatch_loop_device_deps(const MemGraph& m, Resources& res, ReadyList& ready, Backend& be, int lookahead) {
+    GraphIndex gi(m);
+    const size_t V = m.vertices.size();
+    const int D = m.device_count;
+    std::vector<std::int32_t> npc = gi.indeg, npd = gi.indeg;
+    std::vector<std::int32_t> held(V, -1), kq(D, 0);
+    std::vector<char> done(V, 0);
+    std::vector<std::int32_t> pstart(V + 1, 0), preds;
+    for (size_t u = 0; u < V; ++u)
+        for (std::int32_t a = gi.succ_start[u]; a < gi.succ_start[u + 1]; ++a) pstart[gi.succ[a] + 1]++;
+    for (size_t i = 0; i < V; ++i) pstart[i + 1] += pstart[i];
+    preds.resize(gi.succ.size());
+    {
+        std::vector<std::int32_t> fill(pstart.begin(), pstart.end() - 1);
+        for (size_t u = 0; u < V; ++u)
+            for (std::int32_t a = gi.succ_start[u]; a < gi.succ_start[u + 1]; ++a)
+                preds[fill[gi.succ[a]]++] = static_cast<std::int32_t>(u);
+    }
+    const int kmax = 1 + std::max(0, lookahead);
+    std::vector<std::int32_t> waits;
+    for (size_t i = 0; i < V; ++i)
+        if (npd[i] == 0) ready.push(m.vertices[i].id, static_cast<std::int32_t>(i), 0.0);
+    double now = 0.0;
+    size_t ndone = 0;
+    while (ndone < V) {
+        bool restart = ready.sort();
+        for (int pass = 0; pass < 2; ++pass) {
+            size_t i = 0;
+            while (i < ready.size()) {
+                const std::int32_t v = ready.entries()[i].vidx;
+                const MemVertex& x = m.vertices[v];
+                const bool early = npc[v] > 0;
+                // Inputs (aliased ones complete at dispatch on a shared marker
+                // stream) are never dispatched early.
+                bool go = early == (pass == 1) && !(early && x.op == MemOpKind::Input) && res.free(x);
+                if (go && x.op == MemOpKind::Kernel) go = kq[x.device] < kmax;
+                if (!go) {
+                    ++i;
+                    continue;
+                }
+                held[v] = res.acquire(x);
+                ready.erase(i);
+                if (x.op == MemOpKind::Kernel) kq[x.device]++;
+                waits.clear();
+                for (std::int32_t k = pstart[v]; k < pstart[v + 1]; ++k) {
+                    const std::int32_t p = preds[k];
+                    if (done[p]) continue;
+                    const MemVertex& y = m.vertices[p];
+                    if (x.op == MemOpKind::Kernel && y.op == MemOpKind::Kernel && y.device == x.device) continue;
+                    waits.push_back(p);
+                }
+                be.launch_waits(v, held[v], waits.data(), static_cast<int>(waits.size()), now);
+                for (std::int32_t a = gi.succ_start[v]; a < gi.succ_start[v + 1]; ++a) {
+                    const std::int32_t w = gi.succ[a];
+                    if (--npd[w] == 0) ready.push(m.vertices[w].id, w, now);
+                }
+                if (restart) {
+                    ready.sort();
+                    i = 0;
+                }
+            }
+        }
+        if (be.idle()) {
+            std::string msg = "simulation deadlock: " + std::to_string(ready.size()) +
+                              " vertices ready but blocked, none in flight; frontier:";
+            for (const auto& r : ready.entries()) msg += " " + std::to_string(r.vertex);
+            throw DeadlockError(msg);
+        }
+        const std::int32_t u = be.wait_next(now);
+        const MemVertex& y = m.vertices[u];
+        res.release(y, held[u]);
+        if (y.op == MemOpKind::Kernel) kq[y.device]--;
+        done[u] = 1;
+        ndone++;
+        for (std::int32_t a = gi.succ_start[u]; a < gi.succ_start[u + 1]; ++a) --npc[gi.succ[a]];
+    }
+}
+
 }  // namespace tn

@@ -169,7 +169,8 @@ struct Executor::Impl {
 
     void build();
     void prepare_kernel(Instr& in, const MemVertex& v, const std::vector<std::pair<VertexId, VertexId>>& data_in);
-    void launch(std::int32_t vidx, std::int32_t stream, std::int32_t after = -1);
+    void launch(std::int32_t vidx, std::int32_t stream, std::int32_t after = -1, const std::int32_t* waits = nullptr,
+                int nwaits = 0);
     void issue(std::int32_t vidx, cudaStream_t s, std::int32_t stream);
 
     // --- graph mode ("execution": "graph") ------------------------------------------
@@ -421,6 +422,9 @@ void Executor::Impl::build() {
             TN_CUDA(cudaMalloc(&w.p, need));
             TN_CUDA(cudaMemset(w.p, 0, need));
             w.bytes = need;
+            w.counter_count = 4096;  // split-K tile counters (zero between launches: the reducer resets them)
+            TN_CUDA(cudaMalloc(&w.counters, w.counter_count * sizeof(unsigned)));
+            TN_CUDA(cudaMemset(w.counters, 0, w.counter_count * sizeof(unsigned)));
         }
     }
     for (size_t i = 0; i < V; ++i) {
@@ -478,6 +482,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             g.ldc = op.ldc ? op.ldc : n_out;
             g.epi = op.epilogue;
             g.tile = op.tile;
+            g.ksplit = op.ksplit > 1 ? op.ksplit : -1;
             g.split = op.split;
             if (op.split && op.in_dtype != k::F32) throw Error("gemm precision 3xtf32 needs f32 inputs");
             if (op.epilogue == 1 && (op.N % 256 != 0 || op.args.size() != 2))
@@ -683,7 +688,8 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
 }
 
 // ----------------------------------------------------------------- launch ---
-void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t after) {
+void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t after, const std::int32_t* waits,
+                            int nwaits) {
     Instr& in = prog[vidx];
     set_device(in.dev);
     if (in.timeless) return;  // zero-cost input with nothing to wait for: trace time 0
@@ -697,6 +703,9 @@ void Executor::Impl::launch(std::int32_t vidx, std::int32_t stream, std::int32_t
     // An instant predecessor completed at dispatch on the host, but its marker
     // timestamp is recorded on another stream: order this vertex behind it.
     for (std::int32_t p : in.instant_preds) TN_CUDA(cudaStreamWaitEvent(s, done_event(p), 0));
+    // device-dependency dispatch: predecessors still running elsewhere
+    for (int k = 0; k < nwaits; ++k)
+        if (!prog[waits[k]].timeless) TN_CUDA(cudaStreamWaitEvent(s, done_event(waits[k]), 0));
     if (timed) TN_CUDA(cudaEventRecord(ev_start[vidx], s));
     issue(vidx, s, stream);
     TN_CUDA(cudaEventRecord(done_event(vidx), s));
@@ -874,7 +883,19 @@ class CudaBackend {
     explicit CudaBackend(Executor::Impl& x)
         : x_(x), start_(std::chrono::steady_clock::now()), lanes_(x.lanes()) {}
     void launch(std::int32_t vidx, std::int32_t stream, double) {
+        const auto t_in = std::chrono::steady_clock::now();
         x_.launch(vidx, stream);
+        launch_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_in).count();
+        x_.dispatched.push_back(vidx);
+        x_.stream_of[vidx] = stream;
+        in_flight_++;
+        if (x_.prog[vidx].instant) instant_.push_back(vidx);
+        else if (x_.cfg.poll) track(vidx, stream);
+    }
+    void launch_waits(std::int32_t vidx, std::int32_t stream, const std::int32_t* waits, int n, double) {
+        const auto t_in = std::chrono::steady_clock::now();
+        x_.launch(vidx, stream, -1, waits, n);
+        launch_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_in).count();
         x_.dispatched.push_back(vidx);
         x_.stream_of[vidx] = stream;
         in_flight_++;
@@ -882,7 +903,9 @@ class CudaBackend {
         else if (x_.cfg.poll) track(vidx, stream);
     }
     void launch_after(std::int32_t vidx, std::int32_t stream, std::int32_t after, double) {
+        const auto t_in = std::chrono::steady_clock::now();
         x_.launch(vidx, stream, after);
+        launch_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_in).count();
         x_.dispatched.push_back(vidx);
         x_.stream_of[vidx] = stream;
         in_flight_++;
@@ -890,6 +913,7 @@ class CudaBackend {
     }
     bool idle() const { return in_flight_ == 0; }
     double wait_s() const { return wait_s_; }
+    double launch_s() const { return launch_s_; }
     std::int32_t wait_next(double& now) {
         const auto t_in = std::chrono::steady_clock::now();
         const std::int32_t v = wait_next_(now);
@@ -963,7 +987,7 @@ class CudaBackend {
     Executor::Impl& x_;
     std::chrono::steady_clock::time_point start_;
     int in_flight_ = 0;
-    double wait_s_ = 0;
+    double wait_s_ = 0, launch_s_ = 0;
     std::vector<std::deque<std::int32_t>> lanes_;  // in-flight vertices per stream, launch order
     std::vector<int> active_;                      // lanes with work in flight
     size_t rr_ = 0;
@@ -996,14 +1020,16 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
     }
     auto wall0 = std::chrono::steady_clock::now();
     const bool chain = cfg.lookahead > 0 && cfg.compute_tokens == 1;
-    Resources res(D, cfg.streams_per_device, chain ? (1 << 30) : cfg.compute_tokens,
+    Resources res(D, cfg.streams_per_device, chain || cfg.device_deps ? (1 << 30) : cfg.compute_tokens,
                   cfg.materialize_inputs && !aliased_inputs(), !cfg.inputs_on_device);
     ReadyList ready(pol.tie_break, seed);
     CudaBackend be(*this);
     try {
-        if (chain) dispatch_loop_lookahead(*g, res, ready, be, cfg.lookahead);
+        if (cfg.device_deps) dispatch_loop_device_deps(*g, res, ready, be, cfg.lookahead);
+        else if (chain) dispatch_loop_lookahead(*g, res, ready, be, cfg.lookahead);
         else dispatch_loop(*g, res, ready, be);
         last.host_wait_s = be.wait_s();
+        last.host_launch_s = be.launch_s();
         last.host_dispatch_s =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count() - last.host_wait_s;
     } catch (...) {
@@ -1137,8 +1163,10 @@ Executor::Impl::~Impl() {
     for (auto s : compute)
         if (s) cudaStreamDestroy(s);
     for (auto& ws : gws)
-        for (auto& w : ws)
+        for (auto& w : ws) {
             if (w.p) cudaFree(w.p);
+            if (w.counters) cudaFree(w.counters);
+        }
     for (auto p : arena)
         if (p) cudaFree(p);
     for (auto& [id, b] : inputs)
@@ -1162,8 +1190,8 @@ void Executor::Impl::drop_graphs() {
 
 void Executor::Impl::build_graph(const MemGraph& g, GraphCache& gc) {
     for (const auto& in : prog)
-        if (in.gemm && in.gemm->sk_tiles > 0)  // its partial-sum epochs advance per launch
-            throw Error("graph execution does not support stream-K GEMM tiles");
+        if (in.gemm && (in.gemm->sk_tiles > 0 || in.gemm->ksplit > 1))  // per-stream partial-sum workspaces
+            throw Error("graph execution does not support stream-K / split-K GEMM tiles");
     const size_t V = g.vertices.size();
     GraphIndex gi(g);
     std::vector<std::vector<std::int32_t>> preds(V);
@@ -1428,6 +1456,7 @@ std::string RunStats::to_json() const {
     j["zero_copy_bytes"] = zero_copy_bytes;
     j["host_dispatch_s"] = host_dispatch_s;
     j["host_wait_s"] = host_wait_s;
+    j["host_launch_s"] = host_launch_s;
     j["device_makespan_s"] = device_makespan_s;
     j["graph_nodes"] = graph_nodes;
     return j.dump();
@@ -1443,6 +1472,9 @@ ExecConfig parse_exec_config(const std::string& text) {
         c.streams_per_device = j.value("streams_per_device", c.streams_per_device);
         c.compute_tokens = j.value("compute_tokens", c.compute_tokens);
         c.lookahead = j.value("lookahead", c.lookahead);
+        const std::string deps = j.value("dependencies", std::string("host"));
+        if (deps != "host" && deps != "device") throw ParseError("dependencies must be host or device");
+        c.device_deps = deps == "device";
         c.elide_input_offloads = j.value("elide_input_offloads", c.elide_input_offloads);
         c.materialize_inputs = j.value("materialize_inputs", c.materialize_inputs);
         c.timeout_s = j.value("timeout_s", c.timeout_s);

@@ -14,6 +14,10 @@ struct ExecConfig {
     std::vector<int> devices;        // memgraph device -> CUDA ordinal (default d % gpus)
     int streams_per_device = 5;      // simulator.hpp:23
     int compute_tokens = 1;          // concurrent kernels per device (reference: 1)
+    bool device_deps = false;        // "dependencies": "host" (a vertex is dispatched once the host saw
+                                     // its predecessors complete; kernels may chain, see lookahead) |
+                                     // "device" (dispatched once its predecessors are dispatched,
+                                     // waiting on the GPU for them: dispatch_loop_device_deps)
     int lookahead = 1;               // kernels queued behind the running one on the GPU
                                      // (0 = reference dispatch: only after host-observed completion)
     bool materialize_inputs = true;  // Input = a copy into its placement at dispatch
@@ -58,6 +62,7 @@ struct RunStats {
     // host event loop: time spent dispatching (ready-list ordering, resource
     // accounting, launch/copy API calls) vs waiting for the next completion
     double host_dispatch_s = 0, host_wait_s = 0;
+    double host_launch_s = 0;  // part of host_dispatch_s inside the CUDA launch / copy / event calls
     // device-timed span of the run: max over GPUs of (t0 event recorded after the
     // pre-run synchronize -> end event recorded after the last vertex), no
     // per-vertex timestamps needed

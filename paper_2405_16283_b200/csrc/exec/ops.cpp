@@ -134,6 +134,8 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
                 else if (tl == "wide") d.tile = 2;
                 else if (tl == "streamk") d.tile = 3;
                 else throw ParseError("gemm tile must be auto, narrow, wide or streamk");
+                d.ksplit = o.value("ksplit", 0);
+                if (d.ksplit < 0 || d.ksplit > 16) throw ParseError("gemm ksplit must be in [0, 16]");
                 const std::string pr = o.value("precision", std::string("tf32"));
                 if (pr == "tf32") d.split = 0;
                 else if (pr == "3xtf32") d.split = 1;

@@ -86,6 +86,13 @@ struct Params {
     float* ws;
     unsigned* flags;  // per CTA of each pair: epoch of its last published partial
     unsigned epoch;
+    // Split-K (1-CTA kernel, plain epilogue): each tile's K blocks are split
+    // into `ksplit` ranges (work unit = tile x split); every unit writes its
+    // fp32 partial to ws, and the unit that completes a tile's count sums the
+    // partials in split order 0..ksplit-1 (the order never depends on which
+    // unit arrives last), then runs the epilogue. The counter only elects the
+    // reducer and is reset by it.
+    int ksplit;
 };
 
 __device__ __forceinline__ float row_alpha(const Params& p, int row, bool row_ok) {
@@ -133,6 +140,15 @@ __device__ __forceinline__ int kblocks(const Params& p, int mb, int bk) {
     int kb = (p.K + bk - 1) / bk;
     if (p.causal == 2) kb = min(kb, ((mb + 1) * kBM + bk - 1) / bk);
     return kb;
+}
+
+// Work unit u of the 1-CTA kernel -> (tile, split, K-block range).
+__device__ __forceinline__ void unit_range(const Params& p, int u, int nk, int& t, int& k, int& kb0, int& kb1) {
+    const int ks = p.ksplit;
+    t = u / ks;
+    k = u - t * ks;
+    kb0 = static_cast<int>(static_cast<long long>(nk) * k / ks);
+    kb1 = static_cast<int>(static_cast<long long>(nk) * (k + 1) / ks);
 }
 
 __device__ __forceinline__ std::uint32_t pack_bf16(float a, float b) {
@@ -507,6 +523,7 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
     const int bk = kAtom / p.in_bytes;
     const bool tf32 = p.in_bytes == 4;
     const int tiles = p.batch * p.tiles_m * p.tiles_n;
+    const int units = tiles * p.ksplit;  // ksplit == 1 unless split-K (never with SPLIT)
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&ta)) : "memory");
@@ -538,12 +555,13 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
         if (lane == 0) {
             int stage = 0;
             std::uint32_t phase = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                int b, mb, nb;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int t, ks, kb0, kb1, b, mb, nb;
+                unit_range(p, u, 0, t, ks, kb0, kb1);
                 decode(p, t, b, mb, nb);
                 if (tile_skipped(p, mb, nb, BN)) continue;
-                const int nk = kblocks(p, mb, bk);
-                for (int kb = 0; kb < nk; ++kb) {
+                unit_range(p, u, kblocks(p, mb, bk), t, ks, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty + 8 * stage, phase ^ 1);
                     const std::uint32_t fb = full + 8 * stage;
                     mbar_expect_tx(fb, LOADED);
@@ -565,13 +583,14 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                                         (static_cast<std::uint32_t>(kBM >> 4) << 24);
             int stage = 0, acc = 0;
             std::uint32_t phase = 0, acc_phase = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                int b, mb, nb;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int t, ks, ulo, nk, b, mb, nb;
+                unit_range(p, u, 0, t, ks, ulo, nk);
                 decode(p, t, b, mb, nb);
                 if (tile_skipped(p, mb, nb, BN)) continue;
-                const int nk = kblocks(p, mb, bk);
-                const int chunk = SPLIT ? kChunkKB : nk;
-                for (int kb0 = 0; kb0 < nk; kb0 += chunk) {
+                unit_range(p, u, kblocks(p, mb, bk), t, ks, ulo, nk);  // K blocks [ulo, nk)
+                const int chunk = SPLIT ? kChunkKB : nk - ulo;
+                for (int kb0 = ulo; kb0 < nk; kb0 += chunk) {
                 mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
                 tc_fence_after();
                 const std::uint32_t d = tmem + acc * BN;
@@ -591,7 +610,7 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                     } else {
 #pragma unroll
                         for (int k = 0; k < 4; ++k)  // 4 x 32 bytes of K per 128-byte block
-                            tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                            tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0) | (k != 0), tf32);
                     }
                     tc_commit(empty + 8 * stage);
                     if (++stage == kStages) {
@@ -640,8 +659,10 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
         const bool vec_ok = (p.N % 32 == 0) && ((p.ldc * ob) % 16 == 0) && ((p.sc * ob) % 16 == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.C) & 15) == 0) &&
                             ((reinterpret_cast<std::uintptr_t>(p.R) & 15) == 0);
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-            int b, mb, nb;
+        __shared__ int s_reducer;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            int t, ks, kb0, kb1, b, mb, nb;
+            unit_range(p, u, 0, t, ks, kb0, kb1);
             decode(p, t, b, mb, nb);
             if (tile_skipped(p, mb, nb, BN)) continue;
             const int row = mb * kBM + lane_base + lane;
@@ -685,6 +706,62 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                 continue;
             }
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
+            if (!SPLIT && p.ksplit > 1) {
+                // publish this split's partial, free the accumulator, elect the reducer
+                const int r_local = lane_base + lane;
+                float* slot = p.ws + (static_cast<std::int64_t>(t) * p.ksplit + ks) * (kBM * BN) +
+                              static_cast<std::int64_t>(r_local) * BN;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    std::uint32_t r[32];
+                    TN_LD32(tbase + c0, r);
+                    tc_wait_ld();
+                    float4* dst = reinterpret_cast<float4*>(slot + c0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        __stcg(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                    __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + 8 * acc);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (threadIdx.x == 64) s_reducer = atomicAdd(p.flags + t, 1u) == static_cast<unsigned>(p.ksplit - 1);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (s_reducer) {
+                    __threadfence();
+                    const float* base = p.ws + static_cast<std::int64_t>(t) * p.ksplit * (kBM * BN) +
+                                        static_cast<std::int64_t>(r_local) * BN;
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                        float a[32];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 x = __ldcg(reinterpret_cast<const float4*>(base + c0) + q);
+                            a[4 * q] = x.x, a[4 * q + 1] = x.y, a[4 * q + 2] = x.z, a[4 * q + 3] = x.w;
+                        }
+                        for (int sp = 1; sp < p.ksplit; ++sp) {  // split order: deterministic
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 x =
+                                    __ldcg(reinterpret_cast<const float4*>(base + sp * (kBM * BN) + c0) + q);
+                                a[4 * q] += x.x, a[4 * q + 1] += x.y, a[4 * q + 2] += x.z, a[4 * q + 3] += x.w;
+                            }
+                        }
+                        std::uint32_t r[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(a[j]);
+                        store_chunk(p, r, off, nb * BN + c0, row_ok, vec_ok, alpha);
+                    }
+                    if (threadIdx.x == 64) p.flags[t] = 0u;  // ready for the next launch
+                }
+                continue;
+            }
             if (p.epi == 1) {
                 epilogue_swiglu(p, tbase, off, BN / 2, nb * (BN / 2), row_ok, alpha);
             } else if (p.epi == 2) {
@@ -1474,6 +1551,19 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     const int tm = (a.M + bm - 1) / bm, tn = (a.N + bn - 1) / bn;
     plan->tiles = a.batch * tm * tn;
     plan->grid = std::min(plan->tiles, std::max(1, num_sms));
+    plan->ksplit = 1;
+    if (plan->path == 0 && !split && a.epi == 0 && a.causal == 0 && !a.no_P && a.ksplit > 1) {
+        // Requested split-K (tiles that fill few SMs with a long K, e.g. the
+        // config-5 P·V accumulation M 4096 x N 128 x K 4096 = 32 tiles): ksplit
+        // units per tile, fp32 partials in the workspace, reduced in split order.
+        const int nk = static_cast<int>((a.K * es + kAtom - 1) / kAtom);
+        const int ks = std::min(a.ksplit, nk);
+        if (ks >= 2) {
+            plan->ksplit = ks;
+            plan->grid = std::min(plan->tiles * ks, std::max(1, num_sms));
+            plan->ws_bytes = static_cast<std::size_t>(plan->tiles) * ks * kBM * bn * 4;
+        }
+    }
     if (plan->path == 2 || plan->path == 3) {
         plan->grid = std::max(2, std::min(2 * plan->tiles, num_sms) / 2 * 2);
         const int npairs = plan->grid / 2, T = plan->tiles;
@@ -1580,6 +1670,18 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
         if (++ws->epoch == 0) ws->epoch = 1;  // 0 = never published
         p.epoch = ws->epoch;
     }
+    p.ksplit = 1;
+    unsigned grid = static_cast<unsigned>(plan.grid);
+    if (plan.path == 0 && plan.ksplit > 1) {
+        if (ws && ws->p && ws->bytes >= plan.ws_bytes && ws->counters &&
+            ws->counter_count >= static_cast<std::size_t>(plan.tiles)) {
+            p.ksplit = plan.ksplit;
+            p.ws = static_cast<float*>(ws->p);
+            p.flags = ws->counters;
+        } else {
+            grid = static_cast<unsigned>(std::min(plan.tiles, plan.grid));  // no workspace: unsplit
+        }
+    }
     if (plan.path == 3)
         return launch_pdl(gemm_kernel_2sm_w, dim3(plan.grid), dim3(kThreadsW), smem_bytes_2sm_w(), s, plan.ta, plan.tb,
                           plan.tbh, plan.tbq, plan.tc, p);
@@ -1587,15 +1689,15 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
         return launch_pdl(gemm_kernel_2sm, dim3(plan.grid), dim3(kThreads), smem_bytes_2sm(), s, plan.ta, plan.tb,
                           plan.tbh, plan.tbq, plan.tc, p);
     if (p.split)
-        return launch_pdl(gemm_kernel<64, true>, dim3(plan.grid), dim3(threads_1cta<64, true>()),
+        return launch_pdl(gemm_kernel<64, true>, dim3(grid), dim3(threads_1cta<64, true>()),
                           smem_bytes<64, true>(), s, plan.ta, plan.tb, p);
     if (plan.bn == 128)
-        return launch_pdl(gemm_kernel<128, false>, dim3(plan.grid), dim3(kThreads), smem_bytes<128>(), s, plan.ta,
+        return launch_pdl(gemm_kernel<128, false>, dim3(grid), dim3(kThreads), smem_bytes<128>(), s, plan.ta,
                           plan.tb, p);
     if (plan.bn == 64)
-        return launch_pdl(gemm_kernel<64, false>, dim3(plan.grid), dim3(kThreads), smem_bytes<64>(), s, plan.ta,
+        return launch_pdl(gemm_kernel<64, false>, dim3(grid), dim3(kThreads), smem_bytes<64>(), s, plan.ta,
                           plan.tb, p);
-    return launch_pdl(gemm_kernel<256, false>, dim3(plan.grid), dim3(kThreads), smem_bytes<256>(), s, plan.ta, plan.tb,
+    return launch_pdl(gemm_kernel<256, false>, dim3(grid), dim3(kThreads), smem_bytes<256>(), s, plan.ta, plan.tb,
                       p);
 }
 

@@ -58,6 +58,8 @@ struct GemmArgs {
                                  // memory, C += Alo·Bhi + Ahi·Blo + Ahi·Bhi; fp32-accurate), 0 = tf32
     int tile = 0;                // CTA-pair tile: 0 auto, 1 narrow (256x256), 2 wide (512x256),
                                  // 3 narrow with a stream-K tail (instead of half-width tail tiles)
+    int ksplit = 0;              // 1-CTA split-K units per tile: n > 1 requested (needs a GemmWorkspace with
+                                 // counters; plain epilogue, causal 0), otherwise none
 };
 
 struct alignas(64) GemmPlan {
@@ -76,6 +78,7 @@ struct alignas(64) GemmPlan {
     std::size_t ws_bytes = 0;  // workspace the stream-K tail needs (0: none)
     int tail_split = 1;        // paths 2/3: tiles of the last partial wave split into this many N-slices
     int tail_units = 0;        // number of such slices
+    int ksplit = 1;            // path 0: split-K units per tile (ws_bytes of partials + per-tile counters)
     bool tbh_ok = false;
     bool tc_ok = false;
 };
@@ -87,6 +90,8 @@ struct GemmWorkspace {
     void* p = nullptr;
     std::size_t bytes = 0;
     unsigned epoch = 0;
+    unsigned* counters = nullptr;  // split-K per-tile arrival counters (zero-initialised, reset by each reducer)
+    std::size_t counter_count = 0;
 };
 
 // 3-D tiled TMA descriptor (inner, rows, batch), 128-byte swizzle.

@@ -318,6 +318,98 @@ __global__ void __launch_bounds__(kRowThreads) rowstats_vec(const __nv_bfloat16*
     if (threadIdx.x == 0) st[r] = make_float2(mx, sum);
 }
 
+// Warp-per-row variants for long bf16 rows (cols % 256 == 0, 16-byte
+// aligned): 8 rows per 256-thread CTA, no block barriers; lane l reads the
+// 16-byte chunks l, l+32, ... (coalesced), four in flight per lane per pass.
+// rowstats: pass 1 the row max (warp shuffles), pass 2 re-reads the row (an
+// L2 hit: 8 KB per row was just read) for sum exp(s - m). Each lane sums its
+// columns in chunk order, then a fixed xor-shuffle tree: deterministic.
+constexpr int kWarpRows = kRowThreads / 32;
+__global__ void __launch_bounds__(kRowThreads) rowstats_warp(const __nv_bfloat16* __restrict__ S,
+                                                             float2* __restrict__ st, int rows, int cols,
+                                                             int causal) {
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const std::int64_t r = static_cast<std::int64_t>(blockIdx.x) * kWarpRows + warp;
+    if (r >= rows) return;
+    const int valid = causal ? min(cols, static_cast<int>(r) + 1) : cols;
+    const uint4* s = reinterpret_cast<const uint4*>(S + r * cols);
+    const int nch = cols / 8;  // 16-byte chunks per row
+    constexpr float L2E = 1.4426950408889634f;
+    float mx = -INFINITY;
+    for (int c0 = lane; c0 < nch; c0 += 32 * 4) {
+        uint4 u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (c0 + 32 * i < nch) u[i] = __ldg(s + c0 + 32 * i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = (c0 + 32 * i) * 8;
+            if (c0 + 32 * i >= nch || c >= valid) continue;
+            float f[8];
+            unpack8(u[i], f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c + j < valid) mx = fmaxf(mx, f[j]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o /= 2) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float moff = mx * L2E;
+    float sum = 0.f;
+    for (int c0 = lane; c0 < nch; c0 += 32 * 4) {
+        uint4 u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (c0 + 32 * i < nch) u[i] = __ldcs(s + c0 + 32 * i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = (c0 + 32 * i) * 8;
+            if (c0 + 32 * i >= nch || c >= valid) continue;
+            float f[8];
+            unpack8(u[i], f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c + j < valid) sum += exp2f(fmaf(f[j], L2E, -moff));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o /= 2) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) st[r] = make_float2(mx, sum);
+}
+
+// P = exp(S - m) / l, warp per row (same layout as rowstats_warp).
+__global__ void __launch_bounds__(kRowThreads) softmax_apply_warp(const __nv_bfloat16* __restrict__ S,
+                                                                  const float2* __restrict__ st,
+                                                                  __nv_bfloat16* __restrict__ P, int rows, int cols,
+                                                                  int causal) {
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const std::int64_t r = static_cast<std::int64_t>(blockIdx.x) * kWarpRows + warp;
+    if (r >= rows) return;
+    const int valid = causal ? min(cols, static_cast<int>(r) + 1) : cols;
+    constexpr float L2E = 1.4426950408889634f;
+    const float2 ml = st[r];
+    const float inv = 1.0f / ml.y, moff = ml.x * L2E;
+    const uint4* s = reinterpret_cast<const uint4*>(S + r * cols);
+    uint4* p = reinterpret_cast<uint4*>(P + r * cols);
+    const int nch = cols / 8;
+    for (int c0 = lane; c0 < nch; c0 += 32 * 4) {
+        uint4 u[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (c0 + 32 * i < nch) u[i] = __ldcs(s + c0 + 32 * i);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (c0 + 32 * i >= nch) continue;
+            const int c = (c0 + 32 * i) * 8;
+            float f[8];
+            unpack8(u[i], f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = (c + j < valid) ? exp2f(fmaf(f[j], L2E, -moff)) * inv : 0.f;
+            __stcs(p + c0 + 32 * i, pack8(f));
+        }
+    }
+}
+
 constexpr int kMaxParts = 64;
 struct Parts {
     const float2* p[kMaxParts];
@@ -417,6 +509,12 @@ cudaError_t rowstats(const void* S, void* st, int rows, int cols, int causal, cu
     if (rows <= 0) return cudaSuccess;
     auto Sp = static_cast<const __nv_bfloat16*>(S);
     auto Tp = static_cast<float2*>(st);
+    static const char* env = std::getenv("TN_ROWOPS");  // A/B: "block" = one CTA per row
+    const bool warp_rows = !(env && std::strcmp(env, "block") == 0);
+    if (warp_rows && cols % 256 == 0 && al16(S)) {
+        rowstats_warp<<<(rows + kWarpRows - 1) / kWarpRows, kRowThreads, 0, s>>>(Sp, Tp, rows, cols, causal);
+        return cudaGetLastError();
+    }
     if (cols % 8 == 0 && al16(S) && cols <= kRowThreads * 8 * 4) {
         if (cols <= kRowThreads * 8 * 2) rowstats_vec<2><<<rows, kRowThreads, 0, s>>>(Sp, Tp, cols, causal);
         else rowstats_vec<4><<<rows, kRowThreads, 0, s>>>(Sp, Tp, cols, causal);
@@ -437,6 +535,14 @@ cudaError_t stats_combine(const void* const* parts, int n, void* out, int rows, 
 
 cudaError_t softmax_apply(const void* S, const void* st, void* P, int rows, int cols, int causal, cudaStream_t s) {
     if (rows <= 0) return cudaSuccess;
+    static const char* env = std::getenv("TN_ROWOPS");
+    const bool warp_rows = !(env && std::strcmp(env, "block") == 0);
+    if (warp_rows && cols % 256 == 0 && al16(S) && al16(P)) {
+        softmax_apply_warp<<<(rows + kWarpRows - 1) / kWarpRows, kRowThreads, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(S), static_cast<const float2*>(st), static_cast<__nv_bfloat16*>(P), rows,
+            cols, causal);
+        return cudaGetLastError();
+    }
     softmax_apply_kernel<<<rows, kRowThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(S),
                                                       static_cast<const float2*>(st), static_cast<__nv_bfloat16*>(P),
                                                       cols, causal);

@@ -20,6 +20,8 @@ ap.add_argument("--policy", default="event-driven")
 ap.add_argument("--lag", type=int, default=None)
 ap.add_argument("--horizon", default="lazy")
 ap.add_argument("--interleave", default="head")
+ap.add_argument("--exec-cfg", default="{}", help="extra executor config keys (JSON)")
+ap.add_argument("--dump", default="", help="write the memgraph + one traced step here (JSON)")
 a = ap.parse_args()
 t0 = time.time()
 g = W.blockwise_attention(a.seq, a.heads, 128, a.tile, lag=a.lag, interleave=a.interleave)
@@ -32,7 +34,7 @@ plan_s = time.time() - t0
 dev = torch.device("cuda", 0)
 inputs = bench.device_inputs(g, 0, dev)
 t1 = time.time()
-ex = Executor(mg, g.to_json(), {"input_residency": "host"})
+ex = Executor(mg, g.to_json(), {"input_residency": "host", **json.loads(a.exec_cfg)})
 for k, v in inputs.items():
     ex.set_input(k, v)
 del inputs
@@ -40,9 +42,13 @@ setup_s = time.time() - t1
 pcie = bench.measure_pcie(dev)
 duplex = bench.measure_pcie_duplex(dev)
 pk = bench.peaks()
-times = bench.untimed_steps(ex, a.steps, a.policy)  # timing-free completion events
+with bench.Clocks([0]) as ck:
+    times = bench.untimed_steps(ex, a.steps, a.policy)  # timing-free completion events
 tr = json.loads(ex.run(a.policy, "fifo", 0))  # one traced step: exposed transfer / kernel busy
 stt = ex.stats()
+if a.dump:
+    with open(a.dump, "w") as f:
+        json.dump({"memgraph": m, "trace": tr}, f)
 flops = W.blockwise_attention_flops(a.seq, a.heads, 128, a.tile)
 roof = max(stt["h2d_bytes"] / (pcie * 1e9), stt["d2h_bytes"] / (pcie * 1e9), flops / (pk["bf16_tflops_sustained"] * 1e12))
 best = min(times)
@@ -59,4 +65,6 @@ print(json.dumps({"workload": f"blockwise_attention_seq{a.seq}_h{a.heads}_tile{a
                   "exposed_transfer_s": round(stt["exposed_transfer_s"], 3), "kernel_busy_s": round(stt["kernel_busy_s"], 4),
                   "pcie_duplex_measured_gbs": round(duplex, 1), "duplex_bound_s": round(dup_s, 4),
                   "frac_of_duplex_bound": round(dup_s / best, 4), "plan_ideal_s": round(plan_ideal, 4),
-                  "flops": flops, "wall_s": round(stt["wall_s"], 3)}), flush=True)
+                  "flops": flops, "wall_s": round(stt["wall_s"], 3),
+                  "host": {k: round(stt[k], 4) for k in ("host_dispatch_s", "host_wait_s", "host_launch_s")},
+                  "clocks": ck.summary()}), flush=True)

@@ -17,16 +17,18 @@ ap.add_argument("--cap-gib", type=float, default=16)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--residency", default="host")
 ap.add_argument("--compare", action="store_true")
+ap.add_argument("--exec-cfg", default="{}", help="extra executor config keys (JSON)")
+ap.add_argument("--horizon", default="lazy")
 a = ap.parse_args()
 t0 = time.time()
 g = W.llama_lora_step(W.LLAMA_7B, a.seq, layers=a.layers)
-mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon="lazy")
+mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon=a.horizon)
 m = json.loads(mg)
 off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
 plan_s = time.time() - t0
 dev = torch.device("cuda", 0)
 inputs = bench.device_inputs(g, 0, dev)
-ex = Executor(mg, g.to_json(), {"input_residency": a.residency})
+ex = Executor(mg, g.to_json(), {"input_residency": a.residency, **json.loads(a.exec_cfg)})
 for k, v in inputs.items():
     ex.set_input(k, v)
 del inputs
@@ -38,7 +40,7 @@ stt = ex.stats()
 loss_id = next(o for o in g.outputs() if g.tensors[o].name == "loss")
 import struct
 loss = struct.unpack("<f", ex.get_output(loss_id, 4))[0]
-res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency}", "memgraph_vertices": len(m["vertices"]),
+res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency}_{a.horizon}", "exec_cfg": a.exec_cfg, "memgraph_vertices": len(m["vertices"]),
        "plan": st, "plan_s": round(plan_s, 2), "offload_gb": round(off / 1e9, 1), "step_s": [round(x, 4) for x in ts], "traced_step_makespan_s": round(traced, 4),
        "loss": loss, "tokens_per_s": round(a.seq / min(ts), 1), "flops": stt["flops"],
        "h2d_gb": round(stt["h2d_bytes"] / 1e9, 2), "d2h_gb": round(stt["d2h_bytes"] / 1e9, 2),
@@ -47,6 +49,7 @@ res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency
 roof = max(stt["flops"] / (pk["bf16_tflops_sustained"] * 1e12), stt["h2d_bytes"] / (pcie * 1e9),
            stt["d2h_bytes"] / (pcie * 1e9))
 res["roofline_s"] = round(roof, 4)
+res["plan_ideal_s"] = round(bench.plan_ideal_s(mg, pcie), 4)
 res["frac_of_roofline"] = round(roof / min(ts), 4)
 if a.compare:
     fx = bench.untimed_steps(ex, a.steps, "fixed-order")

@@ -106,4 +106,6 @@ for name, b in (("rmsnorm (7B)", rmsnorm), ("softmax causal fp32->bf16", softmax
                 ("rowstats + softmax_apply (4096^2 tile)", tile_softmax), ("rope q (7B)", rope), ("transpose_heads v (7B)", vt), ("silu_mul (7B)", silu),
                 ("sum of 8 partials + residual (65B TP8 block)", sum8), ("concat 8 blocks (65B TP8)", concat8),
                 ("cast f32->bf16", cast)):
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] not in name:
+        continue
     run(name, b)
