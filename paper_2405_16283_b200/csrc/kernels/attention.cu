@@ -16,6 +16,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -52,18 +53,6 @@ __device__ __forceinline__ void ex2_poly2(float& a, float& b) {
     fma2v(pa, pb, fa, fb, 0.9999283f);
     a = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
     b = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
-}
-// 2^x for a pair on MUFU in half precision (MUFU.EX2 on f16x2: two results
-// per lane per instruction, twice the f32 rate): x rounded to f16 (|x| < 1:
-// abs. error <= 2^-11, rel. error of 2^x <= 3.4e-4; P is then rounded to bf16,
-// 2^-9), results widened back to f32 for the row sum and the bf16 pack.
-__device__ __forceinline__ void ex2_h2(float& a, float& b) {
-    std::uint32_t h;
-    asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(a), "f"(b));  // a -> low half, b -> high half
-    asm("ex2.approx.f16x2 %0, %0;" : "+r"(h));
-    asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
-        : "=f"(a), "=f"(b)
-        : "r"(h));
 }
 // smem (bytes): Q 128x128 (2 atoms of 16 KB), K 2 stages x 64x128 (2 atoms of
 // 8 KB each), V 2 stages x 128(hd)x64(keys) (1 atom, 16 KB): 96 KB, so two
@@ -327,9 +316,12 @@ constexpr int kSmem = kQ + 2 * kKst + 2 * kV + 128;
 
 // ---------------------------------------------------------------------------
 // CTA-pair kernel (cta_group::2, a cluster of two CTAs on one TPC), the fast
-// path for seq % 256 == 0. The pair owns 512 consecutive query rows of one
-// head as TWO Q tiles of 256 rows (each tile = M 256 MMAs issued by the
-// leader; a CTA holds 128 rows of each tile) and walks 128-key blocks.
+// path for seq % 256 == 0. A work item is 512 consecutive query rows of one
+// head, as TWO Q tiles of 256 rows (each tile = M 256 MMAs issued by the
+// leader; a CTA holds 128 rows of each tile), walking 128-key blocks.
+// Persistent: one cluster per TPC walks its items (heaviest first, snake
+// order over the clusters for balance); the next item's Q load and first
+// S MMAs overlap the current item's last blocks and O epilogue.
 // Each CTA stages HALF of every K block (64 keys) and HALF of every Vᵀ block
 // (64 of the 128 head-dim rows), so per 128x128 score tile an SM moves 80 KB
 // through shared memory (vs 192 KB in the 1-CTA kernel) and the tensor pipe,
@@ -337,18 +329,23 @@ constexpr int kSmem = kQ + 2 * kKst + 2 * kV + 128;
 // TMEM (512 columns per CTA): S0/P0 [0,128), S1/P1 [128,256), O0 [256,384),
 // O1 [384,512). smem: Q0, Q1 (32 KB each), 3 stages of K and Vᵀ halves.
 //   warp 0     TMA (both CTAs; .cta_group::2 loads signal the leader's barriers)
-//   warp 1     leader only, one in-order issuer: S0_0, S1_0, then per block j
-//              P0_j·V_j, S0_{j+1}, P1_j·V_j, S1_{j+1}. The single issuer
-//              staggers the two tiles: tile 0's softmax runs while the pipe
-//              executes tile 1's MMAs and vice versa. Each P·V is issued in
-//              two halves (keys [0,64) as soon as the softmax stored them).
+//   warp 1     leader only, one in-order issuer: per item S0_0, S1_0, then per
+//              block j P0_j·V_j, S0_{j+1}, P1_j·V_j, S1_{j+1}. The single
+//              issuer staggers the two tiles: tile 0's softmax runs while the
+//              pipe executes tile 1's MMAs and vice versa. Each P·V is issued
+//              in two halves (keys [0,64) as soon as the softmax stored them).
 //              In-order execution makes S_t,j+1 overwrite P_t,j only after
 //              P_t,j·V read it, and S_t,j+1 complete implies P_t,j·V complete
-//              (O_t stable for the softmax warps' rare rescale).
+//              (O_t stable for the softmax warps' rare rescale). An item's
+//              first P_t·V (which overwrites O_t) waits until the previous
+//              item's epilogue has read O_t (o_empty).
 //   warps 2-5  softmax of tile 0, warps 6-9 tile 1: one query row per thread,
 //              128 scores in registers, P (bf16) over S in TMEM, final O / l.
-// Causal: tile t of pair i covers rows [512i + 256t, +256) and walks blocks
+// Causal: tile t of item i covers rows [512i + 256t, +256) and walks blocks
 // 0..4i+2t+1; in the diagonal blocks the rows above the key range are masked.
+// Measured alternatives (7B layer, causal): one pair per item without the
+// overlap 138-140 us (1-CTA kernel 132.5); two softmax threads per row with a
+// shared-memory max exchange (16 softmax warps, setmaxnreg) 154.8 us.
 constexpr int kN2 = 128;                  // keys per block
 constexpr int kKh = 64 * kHd * 2;         // per CTA per stage: 64 keys x hd 128 = 16 KB (2 SW128 atoms of 8 KB)
 constexpr int kVh = (kHd / 2) * kN2 * 2;  // per CTA per stage: 64 Vᵀ rows x 128 keys = 16 KB (2 atoms)
@@ -356,24 +353,24 @@ constexpr int kStg2 = 3;
 constexpr int kThreads2 = 320;
 constexpr int kSmem2 = 2 * kQ + kStg2 * (kKh + kVh) + 256;
 
-#ifdef TN_ATTN_PROF
-__device__ long long g_aprof[2][64][10];  // diagnostics build only: per block clocks of the heaviest pair's leader
-__device__ unsigned long long g_acl[4096][5];
-__device__ unsigned long long g_agt[3][64];  // cluster 0, tile 0: globaltimer of softmax p0 arrive (rank 0, rank 1), MMA p0 seen  // per cluster: smid, globaltimer at entry / first S / last S issued / exit
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
+struct PairItem {
+    int h, qi, nkv_t[2], nkv;
+};
+// Item `n` of cluster `c` (snake order: even rounds ascend, odd rounds
+// descend over the clusters); items are numbered heaviest first.
+__device__ __forceinline__ bool pair_item(const AttnParams& p, int c, int nc, int n, PairItem& it) {
+    const int idx = n * nc + ((n & 1) ? nc - 1 - c : c);
+    if (idx >= p.heads * p.nblk) return false;
+    it.h = idx % p.heads;
+    it.qi = p.nblk - 1 - idx / p.heads;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int row0 = it.qi * 512 + t * 256;
+        it.nkv_t[t] = row0 >= p.seq ? 0 : p.causal ? (row0 + 256) / kN2 : p.seq / kN2;
+    }
+    it.nkv = max(it.nkv_t[0], it.nkv_t[1]);
+    return true;
 }
-__device__ __forceinline__ unsigned smid() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
-    return r;
-}
-#define APROF(t, j, k) do { if (blockIdx.x == 0 && lane == 0 && (j) < 64) g_aprof[(t)][(j)][(k)] = clock64(); } while (0)
-#else
-#define APROF(t, j, k) do { } while (0)
-#endif
 
 template <int EMU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
@@ -387,30 +384,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw + 2 * kQ + kStg2 * (kKh + kVh));
     const std::uint32_t b0 = smem_u32(bars);
     // q_full | k_full[3] | k_empty[3] | v_full[3] | v_empty[3] | s_full[2] | p_full[2][2] | o_full[2]
+    // | o_empty[2] | q_empty
     const std::uint32_t q_full = b0, k_full = b0 + 8, k_empty = b0 + 32, v_full = b0 + 56, v_empty = b0 + 80,
-                        s_full = b0 + 104, p_full = b0 + 120, o_full = b0 + 152;
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 21);
+                        s_full = b0 + 104, p_full = b0 + 120, o_full = b0 + 152, o_empty = b0 + 168,
+                        q_empty = b0 + 184;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 24);
 
     pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const std::uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
-    const int cl = blockIdx.x / 2;
-    const int h = cl % p.heads;
-    const int qi = p.nblk - 1 - cl / p.heads;  // heavy pairs first (p.nblk = ceil(seq / 512))
-    int nkv_t[2];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        const int row0 = qi * 512 + t * 256;
-        nkv_t[t] = row0 >= p.seq ? 0 : p.causal ? (row0 + 256) / kN2 : p.seq / kN2;
-    }
-    const int nkv = max(nkv_t[0], nkv_t[1]);
-#ifdef TN_ATTN_PROF
-    if (leader && threadIdx.x == 0) {
-        g_acl[cl][0] = smid();
-        g_acl[cl][1] = gtimer();
-    }
-#endif
+    const int cl = blockIdx.x / 2, ncl = gridDim.x / 2;
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tq)) : "memory");
@@ -420,6 +404,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         for (int i = 0; i < 4; ++i) mbar_init(p_full + 8 * i, 8);  // 4 softmax warps x 2 CTAs
         mbar_init(o_full, 1);
         mbar_init(o_full + 8, 1);
+        mbar_init(o_empty, 8);
+        mbar_init(o_empty + 8, 8);
+        mbar_init(q_empty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -436,32 +423,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            const int ntiles = nkv_t[1] > 0 ? 2 : 1;
-            if (leader) mbar_expect_tx(q_full, 2 * kQ * ntiles);
-            const std::uint32_t qf = mapa(q_full, 0);
-            for (int t = 0; t < ntiles; ++t) {
-                const int qrow0 = qi * 512 + t * 256 + static_cast<int>(rank) * kB;
-                tma_load_3d_2sm(sQ + t * kQ, &tq, 0, qrow0, h, qf);
-                tma_load_3d_2sm(sQ + t * kQ + kQ / 2, &tq, 64, qrow0, h, qf);
-            }
             int st = 0;
             std::uint32_t ph = 0;
-            for (int j = 0; j < nkv; ++j) {
-                mbar_wait(k_empty + 8 * st, ph ^ 1);
-                if (leader) mbar_expect_tx(k_full + 8 * st, 2 * kKh);
-                const std::uint32_t kf = mapa(k_full + 8 * st, 0), dk = sK0 + st * kKh;
-                const int key0 = j * kN2 + static_cast<int>(rank) * 64;
-                tma_load_3d_2sm(dk, &tk, 0, key0, h, kf);
-                tma_load_3d_2sm(dk + kKh / 2, &tk, 64, key0, h, kf);
-                mbar_wait(v_empty + 8 * st, ph ^ 1);
-                if (leader) mbar_expect_tx(v_full + 8 * st, 2 * kVh);
-                const std::uint32_t vf = mapa(v_full + 8 * st, 0), dv = sV0 + st * kVh;
-                const int vrow = static_cast<int>(rank) * (kHd / 2);
-                tma_load_3d_2sm(dv, &tv, j * kN2, vrow, h, vf);
-                tma_load_3d_2sm(dv + kVh / 2, &tv, j * kN2 + 64, vrow, h, vf);
-                if (++st == kStg2) {
-                    st = 0;
-                    ph ^= 1;
+            PairItem it;
+            for (int n = 0; pair_item(p, cl, ncl, n, it); ++n) {
+                const int ntiles = it.nkv_t[1] > 0 ? 2 : 1;
+                if (n > 0) mbar_wait(q_empty, (n - 1) & 1);  // the previous item's S MMAs have read Q
+                if (leader) mbar_expect_tx(q_full, 2 * kQ * ntiles);
+                const std::uint32_t qf = mapa(q_full, 0);
+                for (int t = 0; t < ntiles; ++t) {
+                    const int qrow0 = it.qi * 512 + t * 256 + static_cast<int>(rank) * kB;
+                    tma_load_3d_2sm(sQ + t * kQ, &tq, 0, qrow0, it.h, qf);
+                    tma_load_3d_2sm(sQ + t * kQ + kQ / 2, &tq, 64, qrow0, it.h, qf);
+                }
+                for (int j = 0; j < it.nkv; ++j) {
+                    mbar_wait(k_empty + 8 * st, ph ^ 1);
+                    if (leader) mbar_expect_tx(k_full + 8 * st, 2 * kKh);
+                    const std::uint32_t kf = mapa(k_full + 8 * st, 0), dk = sK0 + st * kKh;
+                    const int key0 = j * kN2 + static_cast<int>(rank) * 64;
+                    tma_load_3d_2sm(dk, &tk, 0, key0, it.h, kf);
+                    tma_load_3d_2sm(dk + kKh / 2, &tk, 64, key0, it.h, kf);
+                    mbar_wait(v_empty + 8 * st, ph ^ 1);
+                    if (leader) mbar_expect_tx(v_full + 8 * st, 2 * kVh);
+                    const std::uint32_t vf = mapa(v_full + 8 * st, 0), dv = sV0 + st * kVh;
+                    const int vrow = static_cast<int>(rank) * (kHd / 2);
+                    tma_load_3d_2sm(dv, &tv, j * kN2, vrow, it.h, vf);
+                    tma_load_3d_2sm(dv + kVh / 2, &tv, j * kN2 + 64, vrow, it.h, vf);
+                    if (++st == kStg2) {
+                        st = 0;
+                        ph ^= 1;
+                    }
                 }
             }
         }
@@ -477,174 +468,170 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                                sdesc(dk + (kk >> 2) * (kKh / 2) + (kk & 3) * 32), idesc_s, kk != 0, false);
                 tc_commit_2sm(s_full + 8 * t);
             };
-            mbar_wait(q_full, 0);
-            mbar_wait(k_full, 0);
-            tc_fence_after();
-#ifdef TN_ATTN_PROF
-            if (lane == 0) g_acl[cl][2] = gtimer();
-#endif
-            issue_s(0, 0);
-            if (nkv_t[1] > 0) issue_s(1, 0);
-            tc_commit_2sm(k_empty);
             int st = 0;
             std::uint32_t ph = 0;
-            for (int j = 0; j < nkv; ++j) {
-                const int st1 = st + 1 == kStg2 ? 0 : st + 1;
-                const std::uint32_t ph1 = st1 == 0 ? ph ^ 1 : ph;
-                const bool knext = j + 1 < nkv;
-                bool kwaited = false;
-                APROF(0, j, 8);
-                mbar_wait(v_full + 8 * st, ph);
-                APROF(0, j, 9);
-                const std::uint32_t dv = sV0 + st * kVh;
+            int bt[2] = {0, 0}, itc[2] = {0, 0};  // per tile: blocks and items processed before this item
+            PairItem it;
+            for (int n = 0; pair_item(p, cl, ncl, n, it); ++n) {
+                mbar_wait(q_full, n & 1);
+                mbar_wait(k_full + 8 * st, ph);
+                tc_fence_after();
+                issue_s(0, st);
+                if (it.nkv_t[1] > 0) issue_s(1, st);
+                tc_commit_2sm(k_empty + 8 * st);
+                if (it.nkv == 1) tc_commit_2sm(q_empty);
+                for (int j = 0; j < it.nkv; ++j) {
+                    const int st1 = st + 1 == kStg2 ? 0 : st + 1;
+                    const std::uint32_t ph1 = st1 == 0 ? ph ^ 1 : ph;
+                    const bool knext = j + 1 < it.nkv;
+                    bool kwaited = false;
+                    mbar_wait(v_full + 8 * st, ph);
+                    const std::uint32_t dv = sV0 + st * kVh;
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    if (j >= nkv_t[t]) continue;
-                    const std::uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
-                    mbar_wait(p_full + 16 * t, j & 1);
-                    APROF(t, j, 4);
-#ifdef TN_ATTN_PROF
-                    if (cl == 0 && t == 0 && lane == 0 && j < 64) g_agt[2][j] = gtimer();
-#endif
-                    tc_fence_after();
+                    for (int t = 0; t < 2; ++t) {
+                        if (j >= it.nkv_t[t]) continue;
+                        const std::uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
+                        if (j == 0 && itc[t] > 0) mbar_wait(o_empty + 8 * t, (itc[t] - 1) & 1);
+                        const std::uint32_t pph = static_cast<std::uint32_t>(bt[t] + j) & 1;
+                        mbar_wait(p_full + 16 * t, pph);
+                        tc_fence_after();
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        tc_mma_ts_2sm(tO, tS + kk * 8, sdesc(dv + kk * 32), idesc_o, (j | kk) != 0);
-                    mbar_wait(p_full + 16 * t + 8, j & 1);
-                    APROF(t, j, 5);
-                    tc_fence_after();
+                        for (int kk = 0; kk < 4; ++kk)
+                            tc_mma_ts_2sm(tO, tS + kk * 8, sdesc(dv + kk * 32), idesc_o, (j | kk) != 0);
+                        mbar_wait(p_full + 16 * t + 8, pph);
+                        tc_fence_after();
 #pragma unroll
-                    for (int kk = 4; kk < 8; ++kk)
-                        tc_mma_ts_2sm(tO, tS + kk * 8, sdesc(dv + kVh / 2 + (kk & 3) * 32), idesc_o, 1);
-                    if (j + 1 == nkv_t[t]) tc_commit_2sm(o_full + 8 * t);
-                    APROF(t, j, 6);
-                    if (j + 1 < nkv_t[t]) {
-                        if (!kwaited) {
-                            mbar_wait(k_full + 8 * st1, ph1);
-                            tc_fence_after();
-                            kwaited = true;
+                        for (int kk = 4; kk < 8; ++kk)
+                            tc_mma_ts_2sm(tO, tS + kk * 8, sdesc(dv + kVh / 2 + (kk & 3) * 32), idesc_o, 1);
+                        if (j + 1 == it.nkv_t[t]) tc_commit_2sm(o_full + 8 * t);
+                        if (j + 1 < it.nkv_t[t]) {
+                            if (!kwaited) {
+                                mbar_wait(k_full + 8 * st1, ph1);
+                                tc_fence_after();
+                                kwaited = true;
+                            }
+                            issue_s(t, st1);
                         }
-                        issue_s(t, st1);
                     }
-                    APROF(t, j, 7);
+                    tc_commit_2sm(v_empty + 8 * st);
+                    if (knext) tc_commit_2sm(k_empty + 8 * st1);
+                    if (j + 2 == it.nkv) tc_commit_2sm(q_empty);  // the item's last S MMAs were just issued
+                    st = st1;
+                    ph = ph1;
                 }
-                tc_commit_2sm(v_empty + 8 * st);
-                if (knext) tc_commit_2sm(k_empty + 8 * st1);
-#ifdef TN_ATTN_PROF
-                if (lane == 0 && !knext) g_acl[cl][3] = gtimer();
-#endif
-                st = st1;
-                ph = ph1;
+#pragma unroll
+                for (int t = 0; t < 2; ++t)
+                    if (it.nkv_t[t] > 0) {
+                        bt[t] += it.nkv_t[t];
+                        itc[t]++;
+                    }
             }
         }
     } else {
         const int t = (warp - 2) / 4;
-        const int nk = t == 0 ? nkv_t[0] : nkv_t[1];
         const int lane_base = (warp % 4) * 32;
         const int r = lane_base + lane;
-        const int qrow = qi * 512 + t * 256 + static_cast<int>(rank) * kB + r;
         const std::uint32_t trow = static_cast<std::uint32_t>(lane_base) << 16;
         const std::uint32_t tS = tmem + t * 128 + trow, tO = tmem + 256 + t * 128 + trow;
         const std::uint32_t pf0 = mapa(p_full + 16 * t, 0), pf1 = pf0 + 8;
+        const std::uint32_t oe = mapa(o_empty + 8 * t, 0);
         const std::uint32_t sf = s_full + 8 * t;
-        float m = -INFINITY, l = 0.f;
-        constexpr int kW = 8;
-        for (int j = 0; j < nk; ++j) {
-            mbar_wait(sf, j & 1);
-            if (warp % 4 == 2) APROF(t, j, 0);
-            tc_fence_after();
-            float s[CW];
+        int bt = 0, itc = 0;
+        PairItem it;
+        for (int n = 0; pair_item(p, cl, ncl, n, it); ++n) {
+            const int nk = t == 0 ? it.nkv_t[0] : it.nkv_t[1];
+            if (nk == 0) continue;
+            const int qrow = it.qi * 512 + t * 256 + static_cast<int>(rank) * kB + r;
+            float m = -INFINITY, l = 0.f;
+            constexpr int kW = 8;
+            for (int j = 0; j < nk; ++j) {
+                mbar_wait(sf, (bt + j) & 1);
+                tc_fence_after();
+                float s[CW];
 #pragma unroll
-            for (int c = 0; c < CW; c += 32) {
-                std::uint32_t u[32];
-                TN_LD32(tS + c, u);
+                for (int c = 0; c < CW; c += 32) {
+                    std::uint32_t u[32];
+                    TN_LD32(tS + c, u);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(u[i]);
-            }
-            tc_wait_ld();
-            const int lim = p.causal ? qrow - j * kN2 : CW;  // columns c <= lim are valid
-            float pm[kW];
-#pragma unroll
-            for (int w = 0; w < kW; ++w) pm[w] = -INFINITY;
-            if (lim < CW - 1) {
-#pragma unroll
-                for (int c = 0; c < CW; ++c)
-                    if (c > lim) s[c] = -INFINITY;
-            }
-#pragma unroll
-            for (int c = 0; c < CW; c += 2) pm[(c / 2) % kW] = fmax3(pm[(c / 2) % kW], s[c], s[c + 1]);
-#pragma unroll
-            for (int w = kW / 2; w > 0; w /= 2)
-#pragma unroll
-                for (int i = 0; i < w; ++i) pm[i] = fmaxf(pm[i], pm[i + w]);
-            if (warp % 4 == 2) APROF(t, j, 1);
-            const float cand = fmaxf(m, pm[0] * p.scale_log2);  // a fully masked block keeps m
-            const bool grew = cand > m + 8.0f;
-            const float mx = grew ? cand : m;
-            const float corr = ex2(m - mx);
-            float ps[kW];
-#pragma unroll
-            for (int w = 0; w < kW; ++w) ps[w] = 0.f;
-#pragma unroll
-            for (int c0 = 0; c0 < CW; c0 += 32) {
-                std::uint32_t pw[16];
-#pragma unroll
-                for (int c = c0; c < c0 + 32; c += 2) {
-                    fma2(s[c], s[c + 1], p.scale_log2, -mx);
-                    if (EMU == 3) {
-                        ex2_h2(s[c], s[c + 1]);
-                    } else if ((c % 8) < 2 * EMU) {
-                        ex2_poly2(s[c], s[c + 1]);
-                    } else {
-                        s[c] = ex2(s[c]);
-                        s[c + 1] = ex2(s[c + 1]);
-                    }
-                    add2(ps[c % kW], ps[c % kW + 1], s[c], s[c + 1]);
-                    __nv_bfloat162 v2 = __floats2bfloat162_rn(s[c], s[c + 1]);
-                    pw[(c - c0) / 2] = *reinterpret_cast<std::uint32_t*>(&v2);
+                    for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(u[i]);
                 }
-                TN_ST16(tS + c0 / 2, pw);  // P (bf16 pairs) over S
-                if (c0 == 32) {
-                    // S_t,j complete => P_t,j-1·V complete: O_t is stable for the
-                    // rare rescale, which must precede the first P_t,j·V MMA.
-                    if (j > 0 && __any_sync(0xffffffffu, grew)) {
-#pragma unroll 1
-                        for (int c = 0; c < kHd; c += 32) {
-                            std::uint32_t u[32];
-                            TN_LD32(tO + c, u);
-                            tc_wait_ld();
+                tc_wait_ld();
+                const int lim = p.causal ? qrow - j * kN2 : CW;  // columns c <= lim are valid
+                float pm[kW];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * corr);
-                            TN_ST32(tO + c, u);
+                for (int w = 0; w < kW; ++w) pm[w] = -INFINITY;
+                if (lim < CW - 1) {
+#pragma unroll
+                    for (int c = 0; c < CW; ++c)
+                        if (c > lim) s[c] = -INFINITY;
+                }
+#pragma unroll
+                for (int c = 0; c < CW; c += 2) pm[(c / 2) % kW] = fmax3(pm[(c / 2) % kW], s[c], s[c + 1]);
+#pragma unroll
+                for (int w = kW / 2; w > 0; w /= 2)
+#pragma unroll
+                    for (int i = 0; i < w; ++i) pm[i] = fmaxf(pm[i], pm[i + w]);
+                const float cand = fmaxf(m, pm[0] * p.scale_log2);  // a fully masked block keeps m
+                const bool grew = cand > m + 8.0f;
+                const float mx = grew ? cand : m;
+                const float corr = ex2(m - mx);
+                float ps[kW];
+#pragma unroll
+                for (int w = 0; w < kW; ++w) ps[w] = 0.f;
+#pragma unroll
+                for (int c0 = 0; c0 < CW; c0 += 32) {
+                    std::uint32_t pw[16];
+#pragma unroll
+                    for (int c = c0; c < c0 + 32; c += 2) {
+                        fma2(s[c], s[c + 1], p.scale_log2, -mx);
+                        if ((c % 8) < 2 * EMU) {
+                            ex2_poly2(s[c], s[c + 1]);
+                        } else {
+                            s[c] = ex2(s[c]);
+                            s[c + 1] = ex2(s[c + 1]);
                         }
+                        add2(ps[c % kW], ps[c % kW + 1], s[c], s[c + 1]);
+                        __nv_bfloat162 v2 = __floats2bfloat162_rn(s[c], s[c + 1]);
+                        pw[(c - c0) / 2] = *reinterpret_cast<std::uint32_t*>(&v2);
                     }
-                    tc_wait_st();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_remote(pf0);
-                    if (warp % 4 == 2) APROF(t, j, 2);
-#ifdef TN_ATTN_PROF
-                    if (cl == 0 && t == 0 && warp == 2 && lane == 0 && j < 64) g_agt[rank][j] = gtimer();
-#endif
+                    TN_ST16(tS + c0 / 2, pw);  // P (bf16 pairs) over S
+                    if (c0 == 32) {
+                        // S_t,j complete => P_t,j-1·V complete: O_t is stable for the
+                        // rare rescale, which must precede the first P_t,j·V MMA.
+                        if (j > 0 && __any_sync(0xffffffffu, grew)) {
+#pragma unroll 1
+                            for (int c = 0; c < kHd; c += 32) {
+                                std::uint32_t u[32];
+                                TN_LD32(tO + c, u);
+                                tc_wait_ld();
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * corr);
+                                TN_ST32(tO + c, u);
+                            }
+                        }
+                        tc_wait_st();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(pf0);
+                    }
                 }
+                tc_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(pf1);
+#pragma unroll
+                for (int w = kW / 2; w > 0; w /= 2)
+#pragma unroll
+                    for (int i = 0; i < w; ++i) ps[i] += ps[i + w];
+                l = l * corr + ps[0];
+                m = mx;
             }
-            tc_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(pf1);
-            if (warp % 4 == 2) APROF(t, j, 3);
-#pragma unroll
-            for (int w = kW / 2; w > 0; w /= 2)
-#pragma unroll
-                for (int i = 0; i < w; ++i) ps[i] += ps[i + w];
-            l = l * corr + ps[0];
-            m = mx;
-        }
-        if (nk > 0) {
-            mbar_wait(o_full + 8 * t, 0);
+            bt += nk;
+            mbar_wait(o_full + 8 * t, itc & 1);
             tc_fence_after();
             const float inv = 1.0f / l;
-            __nv_bfloat16* orow = p.O + static_cast<std::int64_t>(qrow) * p.ldo + static_cast<std::int64_t>(h) * kHd;
+            __nv_bfloat16* orow =
+                p.O + static_cast<std::int64_t>(qrow) * p.ldo + static_cast<std::int64_t>(it.h) * kHd;
 #pragma unroll 1
             for (int c = 0; c < kHd; c += 32) {
                 std::uint32_t u[32];
@@ -662,27 +649,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     dst[q] = v;
                 }
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(oe);  // O_t read: the next item may overwrite it
+            itc++;
         }
     }
     tc_fence_before();
     cluster_sync();
     tc_fence_after();
-#ifdef TN_ATTN_PROF
-    if (leader && threadIdx.x == 0) g_acl[cl][4] = gtimer();
-    if (blockIdx.x == 0 && threadIdx.x == 64)
-        for (int j = 0; j < nkv_t[0]; ++j)
-            printf("AGT j=%d r0_p0=%llu r1_p0=%llu mma_p0=%llu\n", j, g_agt[0][j] - g_agt[0][0], g_agt[1][j] - g_agt[0][0],
-                   g_agt[2][j] - g_agt[0][0]);
-    if (blockIdx.x == 0 && threadIdx.x == 64) {
-        const long long b = g_aprof[0][0][0];
-        for (int t = 0; t < 2; ++t)
-            for (int j = 0; j < nkv_t[t] && j < 64; ++j)
-                printf("APROF t=%d j=%d s_ready=%lld max=%lld p0=%lld p1=%lld | mma p0=%lld p1=%lld pv_issued=%lld s_issued=%lld loop=%lld vfull=%lld\n",
-                       t, j, g_aprof[t][j][0] - b, g_aprof[t][j][1] - b, g_aprof[t][j][2] - b, g_aprof[t][j][3] - b,
-                       g_aprof[t][j][4] - b, g_aprof[t][j][5] - b, g_aprof[t][j][6] - b, g_aprof[t][j][7] - b,
-                       g_aprof[0][j][8] - b, g_aprof[0][j][9] - b);
-    }
-#endif
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
 }
@@ -736,14 +711,14 @@ cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan) {
              encode_tma_3d(&plan->tv, a.vt, 2, a.seq, a.hd, a.seq, a.heads, static_cast<std::int64_t>(a.seq) * a.hd, 64,
                            kHd);
     plan->path = ok ? 0 : 1;
-    // CTA-pair kernel (512-row query pairs, two 256-row tiles; Vᵀ boxes of 64
-    // head-dim rows): measured on the 7B layer (32 heads, seq 4096) at 240.6 vs
-    // 242.9 us non-causal but 138-140 vs 132.5 us causal (one pair per TPC: its
-    // Q load / O store do not overlap another pair), so causal keeps the 1-CTA
-    // kernel. TN_ATTN_PAIR=1 / TN_ATTN_1CTA=1 force either (A/B).
+    // CTA-pair kernel (persistent; 512-row items of two 256-row tiles; Vᵀ boxes
+    // of 64 head-dim rows) whenever seq % 256 == 0: measured on the 7B layer
+    // (32 heads, seq 4096) at 128.4-128.9 vs 133.2 us causal and 236.9 vs
+    // 252.8 us non-causal against the 1-CTA kernel. TN_ATTN_PAIR=0 /
+    // TN_ATTN_1CTA=1 force the 1-CTA kernel (A/B).
     static const char* pair_env = std::getenv("TN_ATTN_PAIR");
     static const bool force_1cta = std::getenv("TN_ATTN_1CTA") != nullptr;
-    const bool want_pair = pair_env ? std::atoi(pair_env) != 0 : !a.causal;
+    const bool want_pair = pair_env ? std::atoi(pair_env) != 0 : true;
     if (ok && a.seq % 256 == 0 && want_pair && !force_1cta)
         if (encode_tma_3d(&plan->tv2, a.vt, 2, a.seq, a.hd, a.seq, a.heads, static_cast<std::int64_t>(a.seq) * a.hd, 64,
                           kHd / 2))
@@ -757,8 +732,6 @@ cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan) {
             cudaFuncSetAttribute(attention_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
             cudaFuncSetAttribute(attention_kernel_2sm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
             cudaFuncSetAttribute(attention_kernel_2sm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
-            cudaFuncSetAttribute(attention_kernel_2sm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
-            cudaFuncSetAttribute(attention_kernel_2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
             attr_set.fetch_or(1ULL << dev, std::memory_order_release);
         }
     }
@@ -788,7 +761,10 @@ cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s) {
     const bool emu0 = emu_env && std::atoi(emu_env) == 0;
     if (plan.path == 2) {
         p.nblk = (a.seq + 511) / 512;
-        const unsigned grid2 = 2u * p.heads * p.nblk;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned grid2 = 2u * static_cast<unsigned>(std::min(p.heads * p.nblk, std::max(1, sms / 2)));
         static const bool occ = std::getenv("TN_ATTN_OCC") != nullptr;  // diagnostics: resident pairs
         if (occ) {
             cudaLaunchConfig_t cfg{};
@@ -811,12 +787,6 @@ cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s) {
         }
         if (emu0)
             return launch_pdl(attention_kernel_2sm<0>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq, plan.tk,
-                              plan.tv2, p);
-        if (emu_env && std::atoi(emu_env) == 2)
-            return launch_pdl(attention_kernel_2sm<2>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq, plan.tk,
-                              plan.tv2, p);
-        if (emu_env && std::atoi(emu_env) == 3)
-            return launch_pdl(attention_kernel_2sm<3>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq, plan.tk,
                               plan.tv2, p);
         return launch_pdl(attention_kernel_2sm<1>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq, plan.tk, plan.tv2,
                           p);
