@@ -719,7 +719,8 @@ def prefill_flops(cfg: LlamaConfig, seq: int, layers: int | None = None) -> floa
 
 # ------------------------------------------ long-context blockwise attention (cfg 5) ---
 def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: int = 4096,
-                        device: int = 0, lag: int | None = None, interleave: str = "head") -> GraphBuilder:
+                        device: int = 0, lag: int | None = None, interleave: str = "head",
+                        pv_ksplit: int = 0) -> GraphBuilder:
     """Config 5: causal attention over `seq` tokens with the n^2 score tiles
     materialised as vertices and kept live across a two-pass softmax, so a
     capped plan must offload them to host RAM.
@@ -739,7 +740,10 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
     old ones (duplex PCIe). `interleave="block"` lists the two passes query
     block by query block (pass 1 of (h + lag, i), then pass 2 of (h, i)), so
     the tiles being produced (offloaded) and the tiles being consumed
-    (reloaded) alternate at tile granularity instead of head granularity."""
+    (reloaded) alternate at tile granularity instead of head granularity.
+    `pv_ksplit` > 1 asks the executor to split the K (= tile keys) of each
+    P·V GEMM into that many ranges (M = tile, N = hd fills only tile/128
+    CTAs); the partials are reduced in split order."""
     assert seq % tile == 0
     nb = seq // tile
     T = tile
@@ -769,7 +773,7 @@ def blockwise_attention(seq: int = 65536, heads: int = 32, hd: int = 128, tile: 
                 P = g.kernel(f"P[{h},{i},{j}]", {"type": "softmax_apply", "args": [S[(h, i, j)], ml[(h, i)]], "rows": T,
                                                  "cols": T, "causal": int(i == j)}, (T, T), "bf16", dev)
                 acc = g.gemm(f"O[{h},{i},{j}]", P, vt[(h, j)], T, hd, T, r=acc, out_dtype="f32", out_shape=(T, hd),
-                             device=dev)
+                             device=dev, ksplit=pv_ksplit or None)
             g.kernel(f"out[{h},{i}]", {"type": "cast", "args": [acc], "count": T * hd, "in_dtype": "f32",
                                        "out_dtype": "bf16"}, (T, hd), "bf16", dev)
 

@@ -21,10 +21,11 @@ ap.add_argument("--lag", type=int, default=None)
 ap.add_argument("--horizon", default="lazy")
 ap.add_argument("--interleave", default="head")
 ap.add_argument("--exec-cfg", default="{}", help="extra executor config keys (JSON)")
+ap.add_argument("--pv-ksplit", type=int, default=0)
 ap.add_argument("--dump", default="", help="write the memgraph + one traced step here (JSON)")
 a = ap.parse_args()
 t0 = time.time()
-g = W.blockwise_attention(a.seq, a.heads, 128, a.tile, lag=a.lag, interleave=a.interleave)
+g = W.blockwise_attention(a.seq, a.heads, 128, a.tile, lag=a.lag, interleave=a.interleave, pv_ksplit=a.pv_ksplit)
 mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon=a.horizon)
 m = json.loads(mg)
 off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
