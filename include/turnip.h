@@ -97,6 +97,9 @@ int tn_make_fixed_order(const char* memgraph_json, char** memgraph_out, char** e
  *   "streams_per_device": 5         simulator.hpp:23
  *   "compute_tokens": 1             kernels running at once per device (reference: 1)
  *   "lookahead": 1                  kernels queued behind the running kernel (0 = exact contract)
+ *   "dependencies": "host"          "host": a vertex dispatches once the host saw its predecessors
+ *                                   complete; "device": once they are dispatched, the GPU waiting
+ *                                   (CUDA events) for the unfinished ones, same resource tokens
  *   "completion": "poll"            "poll" (cudaEventQuery) | "callback" (cudaLaunchHostFunc)
  *   "input_residency": "host"       "host" (pinned pool, H2D at dispatch) | "device" (HBM staging)
  *   "device_inputs": "alias"        with device residency: "alias" (read in place) | "copy" (D2D)
