@@ -19,7 +19,6 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.hpp"
@@ -723,6 +722,12 @@ cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan) {
         if (encode_tma_3d(&plan->tv2, a.vt, 2, a.seq, a.hd, a.seq, a.heads, static_cast<std::int64_t>(a.seq) * a.hd, 64,
                           kHd / 2))
             plan->path = 2;
+    if (plan->path == 2) {  // persistent: one cluster (CTA pair) per TPC, at most one per item
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        plan->grid = 2 * std::min(a.heads * ((a.seq + 511) / 512), std::max(1, sms / 2));
+    }
     if (ok) {
         static std::atomic<unsigned long long> attr_set{0};  // per CUDA device, any thread
         int dev = 0;
@@ -761,30 +766,7 @@ cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s) {
     const bool emu0 = emu_env && std::atoi(emu_env) == 0;
     if (plan.path == 2) {
         p.nblk = (a.seq + 511) / 512;
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const unsigned grid2 = 2u * static_cast<unsigned>(std::min(p.heads * p.nblk, std::max(1, sms / 2)));
-        static const bool occ = std::getenv("TN_ATTN_OCC") != nullptr;  // diagnostics: resident pairs
-        if (occ) {
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(grid2);
-            cfg.blockDim = dim3(kThreads2);
-            cfg.dynamicSmemBytes = kSmem2;
-            cfg.stream = s;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = 2;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            int n = -1, nb = -1;
-            cudaError_t e = cudaOccupancyMaxActiveClusters(&n, attention_kernel_2sm<1>, &cfg);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, attention_kernel_2sm<1>, kThreads2, kSmem2);
-            std::fprintf(stderr, "attention_kernel_2sm: max active clusters %d (%s), blocks/SM %d\n", n,
-                         cudaGetErrorString(e), nb);
-        }
+        const unsigned grid2 = static_cast<unsigned>(plan.grid);
         if (emu0)
             return launch_pdl(attention_kernel_2sm<0>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq, plan.tk,
                               plan.tv2, p);

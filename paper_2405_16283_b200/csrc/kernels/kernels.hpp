@@ -123,6 +123,7 @@ struct alignas(64) AttnPlan {
     CUtensorMap tq, tk, tv, tv2;
     AttnArgs args;
     int path = 0;  // 0 tcgen05 fused (1 CTA per 128 rows), 1 SIMT fallback, 2 tcgen05 CTA pairs (seq % 256 == 0)
+    int grid = 0;  // path 2: CTAs of the persistent launch
 };
 cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan);
 cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s);
