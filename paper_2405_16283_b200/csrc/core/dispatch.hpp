@@ -82,10 +82,13 @@ void finalize_trace(const MemGraph& m, const MemoryMap& map, ExecutionTrace& t);
 // `compute_tokens` (reference: 1) and `inputs_use_host_in`.
 class Resources {
   public:
+    // kernels_take_stream = false (executor: kernels run in order on a per-device
+    // compute stream) keeps the generic stream slots for copies, so a backlog of
+    // ready input copies cannot hold off a ready kernel.
     Resources(int devices, int streams_per_device, int compute_tokens, bool inputs_take_stream,
-              bool inputs_use_host_in = true)
+              bool inputs_use_host_in = true, bool kernels_take_stream = true)
         : streams_(streams_per_device), inputs_(inputs_take_stream), inputs_host_(inputs_use_host_in),
-          devs_(devices) {
+          kernels_(kernels_take_stream), devs_(devices) {
         for (auto& d : devs_) {
             d.free_mask.assign((streams_per_device + 63) / 64, 0);
             for (int i = 0; i < streams_per_device; ++i) d.free_mask[i / 64] |= 1ULL << (i % 64);
@@ -94,11 +97,12 @@ class Resources {
         }
     }
     bool holds_nothing(const MemVertex& v) const { return v.op == MemOpKind::Input && !inputs_; }
+    bool slotless(const MemVertex& v) const { return v.op == MemOpKind::Kernel && !kernels_; }
     bool free(const MemVertex& v) const {
         const Dev& d = devs_[v.device];
         switch (v.op) {
             case MemOpKind::Input: return !inputs_ || (d.nfree > 0 && (!inputs_host_ || d.host_in));
-            case MemOpKind::Kernel: return d.nfree > 0 && d.compute > 0;
+            case MemOpKind::Kernel: return (!kernels_ || d.nfree > 0) && d.compute > 0;
             case MemOpKind::Transfer: return d.nfree > 0;
             case MemOpKind::Offload: return d.nfree > 0 && d.host_out;
             case MemOpKind::Reload: return d.nfree > 0 && d.host_in;
@@ -108,6 +112,10 @@ class Resources {
     std::int32_t acquire(const MemVertex& v) {
         if (holds_nothing(v)) return -1;
         Dev& d = devs_[v.device];
+        if (slotless(v)) {
+            d.compute--;
+            return -1;
+        }
         std::int32_t s = -1;
         for (size_t w = 0; w < d.free_mask.size(); ++w)
             if (d.free_mask[w]) {
@@ -125,6 +133,10 @@ class Resources {
     void release(const MemVertex& v, std::int32_t s) {
         if (holds_nothing(v)) return;
         Dev& d = devs_[v.device];
+        if (slotless(v)) {
+            d.compute++;
+            return;
+        }
         d.free_mask[s / 64] |= 1ULL << (s % 64);
         d.nfree++;
         if (v.op == MemOpKind::Kernel) d.compute++;
@@ -140,7 +152,7 @@ class Resources {
         bool host_out = true, host_in = true;
     };
     int streams_;
-    bool inputs_, inputs_host_;
+    bool inputs_, inputs_host_, kernels_;
     std::vector<Dev> devs_;
 };
 

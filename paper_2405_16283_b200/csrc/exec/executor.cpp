@@ -1021,7 +1021,8 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
     auto wall0 = std::chrono::steady_clock::now();
     const bool chain = cfg.lookahead > 0 && cfg.compute_tokens == 1;
     Resources res(D, cfg.streams_per_device, chain || cfg.device_deps ? (1 << 30) : cfg.compute_tokens,
-                  cfg.materialize_inputs && !aliased_inputs(), !cfg.inputs_on_device);
+                  cfg.materialize_inputs && !aliased_inputs(), !cfg.inputs_on_device,
+                  !((chain || cfg.device_deps) && cfg.compute_tokens == 1 && !cfg.kernel_slots));
     ReadyList ready(pol.tie_break, seed);
     CudaBackend be(*this);
     try {
@@ -1080,7 +1081,9 @@ ExecutionTrace Executor::Impl::build_trace() {
             TN_CUDA(cudaEventElapsedTime(&b, t0[v.device], ev_end[vidx]));
         }
         double s = a * 1e-3, e = std::max(a, b) * 1e-3;
-        t.rows.push_back({v.id, s, e, v.device, stream_of[vidx]});
+        // kernels that hold no generic stream slot run on the compute stream: its id is streams_per_device
+        const std::int32_t st = stream_of[vidx] < 0 && v.op == MemOpKind::Kernel ? cfg.streams_per_device : stream_of[vidx];
+        t.rows.push_back({v.id, s, e, v.device, st});
         if (v.op == MemOpKind::Kernel) {
             kernel_s += e - s;
             kspans[v.device].push_back({s, e});
@@ -1472,6 +1475,7 @@ ExecConfig parse_exec_config(const std::string& text) {
         c.streams_per_device = j.value("streams_per_device", c.streams_per_device);
         c.compute_tokens = j.value("compute_tokens", c.compute_tokens);
         c.lookahead = j.value("lookahead", c.lookahead);
+        c.kernel_slots = j.value("kernel_slots", c.kernel_slots);
         const std::string deps = j.value("dependencies", std::string("host"));
         if (deps != "host" && deps != "device") throw ParseError("dependencies must be host or device");
         c.device_deps = deps == "device";

@@ -18,6 +18,10 @@ struct ExecConfig {
                                      // its predecessors complete; kernels may chain, see lookahead) |
                                      // "device" (dispatched once its predecessors are dispatched,
                                      // waiting on the GPU for them: dispatch_loop_device_deps)
+    bool kernel_slots = false;       // "kernel_slots": true -> kernels also hold one of the generic
+                                     // stream slots (the reference resource model). Default with
+                                     // lookahead (kernels on the compute stream): slots are for copies
+                                     // only, so queued input copies cannot starve a ready kernel
     int lookahead = 1;               // kernels queued behind the running one on the GPU
                                      // (0 = reference dispatch: only after host-observed completion)
     bool materialize_inputs = true;  // Input = a copy into its placement at dispatch
