@@ -641,6 +641,75 @@ def offload_leg(args, devs):
     return out
 
 
+# -------------------------------------------------- configs 1 and 3 leg ---
+def other_configs_leg(args, devs):
+    """Config 1 (fp32 matmul chain 4096², tile 1024, L = 4, 3xTF32, 2 memgraph
+    devices, cap 1.5x the working-set floor: 128 offloads) and config 3
+    (LLaMA-65B prefill, seq 8192, TP8 as 8 memgraph devices, 10 of 80 layers,
+    weights cold in host RAM, 16 GiB per device), each memgraph device on GPU
+    devs[d % N]. Driver-run versions of tools/bench_matmul_chain.py and
+    tools/bench_tp.py (no oracle here: parity is in tests/)."""
+    import torch
+
+    from paper_2405_16283_b200 import workloads as W
+    from paper_2405_16283_b200.executor import Executor
+
+    out = {}
+    n = len(devs)
+    pcie = measure_pcie(torch.device("cuda", devs[0]))
+    # config 1
+    g = W.matmul_chain(4096, 1024, 4, devices=2, precision="3xtf32")
+    caps = [int(f * 1.5) // 1024 * 1024 for f in W.working_set_floor(g)]
+    mg, st = W.plan(g, caps, alloc_horizon="lazy")
+    mdev = [devs[d % n] for d in range(2)]
+    with Executor(mg, g.to_json(), {"devices": mdev, "input_residency": "host"}) as ex:
+        load_inputs(ex, g, 0, mdev)
+        ex.run(trace=False)
+        steps = 5
+        t = timed_runs(ex, steps, sorted(set(mdev))) / steps
+        tr = json.loads(ex.run())
+        s = ex.stats()
+    ids = {v["id"]: v for v in g.vertices}
+    gemm_s = sum(r["end"] - r["start"] for r in tr["rows"]
+                 if r["vertex"] in ids and (ids[r["vertex"]].get("op") or {}).get("type") == "gemm")
+    flops = 2.0 * 4096 ** 3 * 4
+    gpus = len(set(mdev))
+    roof = max(s["h2d_bytes"], s["d2h_bytes"]) / (pcie * 1e9 * gpus)
+    out["config1_matmul_chain"] = {
+        "workload": "matmul_chain_4096_tile1024_L4_fp32_3xtf32_2dev_cap1.5xfloor", "memgraph_devices_on_gpus": mdev,
+        "offloads": st["offloads"], "step_s": round(t, 5), "gemm_tflops": round(flops / gemm_s / 1e12, 1),
+        "h2d_bytes": s["h2d_bytes"], "d2h_bytes": s["d2h_bytes"], "p2p_bytes": s["p2p_bytes"],
+        "d2d_bytes": s["d2d_bytes"], "pcie_bound_s": round(roof, 5), "frac_of_pcie_roofline": round(roof / t, 4),
+        "roofline": "max(H2D, D2H bytes) / PCIe per GPU (the 3xTF32 GEMMs take gemm_tflops)"}
+    # config 3
+    layers = 10
+    g = W.llama_prefill_tp(W.LLAMA_65B, 8192, 8, layers=layers)
+    mg, st = W.plan(g, [16 << 30] * 8, alloc_horizon="lazy")
+    mdev = [devs[d % n] for d in range(8)]
+    nv = len(json.loads(mg)["vertices"])
+    with Executor(mg, g.to_json(), {"devices": mdev, "input_residency": "host"}) as ex:
+        load_inputs(ex, g, 0, mdev)
+        torch.cuda.empty_cache()
+        ex.run(trace=False)
+        steps = 2
+        t = timed_runs(ex, steps, sorted(set(mdev))) / steps
+        s = ex.stats()
+    pk = peaks()
+    gpus = len(set(mdev))
+    compute_s = s["flops"] / (pk["bf16_tflops_sustained"] * 1e12 * gpus)
+    pcie_s = s["h2d_bytes"] / (pcie * 1e9 * gpus)
+    out["config3_llama65b_tp8"] = {
+        "workload": f"llama65b_prefill_seq8192_tp8_{layers}of80_layers_cap16GiB_host", "memgraph_devices_on_gpus": mdev,
+        "memgraph_vertices": nv, "step_s": round(t, 4), "tokens_per_s": round(8192 / t, 1),
+        "h2d_bytes": s["h2d_bytes"], "p2p_bytes": s["p2p_bytes"], "d2d_bytes": s["d2d_bytes"],
+        "achieved_p2p_gbs": round(s["p2p_bytes"] / t / 1e9, 1),
+        "host_dispatch_us_per_vertex": round(s["host_dispatch_s"] * 1e6 / nv, 2),
+        "roofline_s": round(max(compute_s, pcie_s), 4), "bound": "pcie" if pcie_s > compute_s else "tensor",
+        "frac_of_roofline": round(max(compute_s, pcie_s) / t, 4),
+        "roofline": "max(FLOP / sustained bf16 peak, H2D bytes / PCIe), per GPU; peer-copy bytes ride NVLink"}
+    return out
+
+
 # ------------------------------------------------------------------ our arm ---
 def run_ours(args, world, rank, local):
     import torch
@@ -793,6 +862,8 @@ def run_ours_on(args, world, rank, local, n, tp):
     }
     if not args.no_offload_leg and not args.quick:
         line["offload"] = offload_leg(args, devs)
+    if rank == 0 and not args.no_offload_leg and not args.no_other_configs and not args.quick:
+        line["configs_1_3"] = other_configs_leg(args, devs)
     if n == 1 and not args.no_cpu_baseline and not args.quick:
         dt, L = cpu_sample(args, 1, False)
         line["cpu_baseline"] = {"value": round(args.seq / (dt * L), 2), "unit": UNIT, "cores": os.cpu_count(),
@@ -823,6 +894,7 @@ def main():
     ap.add_argument("--policy-trials", type=int, default=10)
     ap.add_argument("--no-offload-leg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the config 1 / config 3 leg")
     ap.add_argument("--emulate", action="store_true", help="map every memgraph device onto GPU 0 (harness test)")
     ap.add_argument("--quick", action="store_true", help="small model for smoke-testing the harness")
     args = ap.parse_args()
