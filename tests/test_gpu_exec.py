@@ -87,7 +87,8 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=256, N=192, K=512, in_dtype="f32", out_dtype="f32", precision="3xtf32"),
     dict(M=300, N=200, K=136, in_dtype="f32", out_dtype="f32", precision="3xtf32", alpha=0.5),
     dict(M=256, N=256, K=256, batch=2, in_dtype="f32", out_dtype="f32", causal=1, precision="3xtf32"),
-    dict(M=2048, N=2048, K=256, in_dtype="f32", out_dtype="f32", residual=True, precision="3xtf32"),
+    dict(M=2048, N=2048, K=256, in_dtype="f32", out_dtype="f32", residual=True, precision="3xtf32"),  # BN=128
+    dict(M=1536, N=1536, K=256, batch=2, in_dtype="f32", out_dtype="f32", causal=1, precision="3xtf32"),
     # 1-CTA split-K (tiles fill < half the SMs, long K): partials reduced in split order
     dict(M=4096, N=128, K=4096, out_dtype="f32", residual=True, ksplit=4),  # config-5 P·V: 32 tiles x 4
     dict(M=640, N=200, K=2048, residual=True, ksplit=8),                    # ragged N, 10 tiles x 8
