@@ -97,6 +97,8 @@ int tn_make_fixed_order(const char* memgraph_json, char** memgraph_out, char** e
  *   "streams_per_device": 5         simulator.hpp:23
  *   "compute_tokens": 1             kernels running at once per device (reference: 1)
  *   "lookahead": 1                  kernels queued behind the running kernel (0 = exact contract)
+ *   "kernel_slots": true            kernels hold a generic stream slot (reference model); false with
+ *                                   lookahead: slots are for copies only (kernels use the compute stream)
  *   "dependencies": "host"          "host": a vertex dispatches once the host saw its predecessors
  *                                   complete; "device": once they are dispatched, the GPU waiting
  *                                   (CUDA events) for the unfinished ones, same resource tokens
