@@ -137,7 +137,10 @@ def dist_setup(mode):
         backend = "nccl" if (torch.cuda.is_available() and mode == "replicas") else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local)
-        dist.init_process_group(backend, init_method="env://")
+        import datetime
+
+        # tp mode: the idle ranks wait at one barrier for the whole bench of rank 0
+        dist.init_process_group(backend, init_method="env://", timeout=datetime.timedelta(hours=2))
     elif torch.cuda.is_available():
         torch.cuda.set_device(local)
     return world, rank, local
