@@ -595,7 +595,7 @@ def offload_leg(args, devs):
         roof = max(s["flops"] / (gpus * pk["bf16_tflops_sustained"] * 1e12), s["h2d_bytes"] / (gpus * pcie_h2d * 1e9),
                    s["d2h_bytes"] / (gpus * pcie_d2h * 1e9))
         out["config4_lora_step"] = {
-            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy" + (f"_dp{dp}" if dp > 1 else ""),
+            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy_recompute_attn_qkv_ffn" + (f"_dp{dp}" if dp > 1 else ""),
             "gpus": gpus, "global_batch": dp, "memgraph_vertices": len(m["vertices"]),
             "offloads": st["offloads"], "reloads": st["reloads"], "offload_bytes_planned": off,
             "reload_bytes_planned": rel, "step_s": round(t, 4), "tokens_per_s": round(dp * args.seq / t, 1),
@@ -610,6 +610,23 @@ def offload_leg(args, devs):
             "roofline": "max(FLOP / sustained bf16 peak, H2D bytes / PCIe H2D, D2H bytes / PCIe D2H), per GPU"}
         if args.policy_trials > 0:
             out["config4_lora_step"]["compare_policies"] = json.loads(ex.compare_policies(args.policy_trials, 0))
+    if dp == 1:
+        # the same step keeping the QKV / FFN activations (attention probabilities
+        # still recomputed): 3x the activation offload, more PCIe-bound
+        g2 = W.llama_lora_step(W.LLAMA_7B, args.seq, recompute_ffn=False, recompute_qkv=False)
+        mg2, st2 = W.plan(g2, [int(args.cap_gib * (1 << 30))], alloc_horizon="lazy")
+        with Executor(mg2, g2.to_json(), {"devices": devs, "input_residency": "host"}) as ex:
+            load_inputs(ex, g2, 0, devs)
+            ex.run(trace=False)
+            t2 = timed_runs(ex, max(1, args.offload_steps), devs) / max(1, args.offload_steps)
+            s2 = ex.stats()
+        pcie_h2d = measure_pcie(torch.device("cuda", dev))
+        roof2 = max(s2["flops"] / (pk["bf16_tflops_sustained"] * 1e12), s2["h2d_bytes"] / (pcie_h2d * 1e9))
+        out["config4_lora_step_saved_activations"] = {
+            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy_recompute_attn", "offloads": st2["offloads"],
+            "step_s": round(t2, 4), "tokens_per_s": round(args.seq / t2, 1), "h2d_bytes": s2["h2d_bytes"],
+            "d2h_bytes": s2["d2h_bytes"], "flops": s2["flops"], "roofline_s": round(roof2, 4),
+            "frac_of_roofline": round(roof2 / t2, 4)}
     if args.policy_trials > 0:
         # greedy horizon (the reference planner's default): allocations run ahead
         # of execution, so offloads of new tiles overlap reloads of old ones

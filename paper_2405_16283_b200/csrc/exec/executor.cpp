@@ -482,7 +482,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             g.ldc = op.ldc ? op.ldc : n_out;
             g.epi = op.epilogue;
             g.tile = op.tile;
-            g.ksplit = op.ksplit > 1 ? op.ksplit : -1;
+            g.ksplit = op.ksplit == 1 ? -1 : op.ksplit;  // op: 0 automatic, 1 off, n > 1 forced
             g.split = op.split;
             if (op.split && op.in_dtype != k::F32) throw Error("gemm precision 3xtf32 needs f32 inputs");
             if (op.epilogue == 1 && (op.N % 256 != 0 || op.args.size() != 2))

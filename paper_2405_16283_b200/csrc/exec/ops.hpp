@@ -68,7 +68,8 @@ struct OpDesc {
     int causal = 0;
     int epilogue = 0;  // gemm: 0 none, 1 swiglu, 2 qkv_rope
     int tile = 0;      // gemm: CTA-pair tile choice, 0 auto, 1 narrow 256x256, 2 wide 512x256
-    int ksplit = 0;    // gemm: 1-CTA split-K units per tile (0 / 1: none); partials reduced in split order
+    int ksplit = 0;    // gemm: 1-CTA split-K units per tile: 0 automatic, 1 none, n > 1 forced (partials reduced
+                       // in split order)
     int split = 0;     // gemm, f32 inputs: 0 tf32, 1 3xTF32
     int inverse = 0, tokens_out = 0;  // rope
     int in_dtype = 0, out_dtype = 0;  // k::DType

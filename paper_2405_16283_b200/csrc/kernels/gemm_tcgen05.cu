@@ -1554,12 +1554,17 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     plan->tiles = a.batch * tm * tn;
     plan->grid = std::min(plan->tiles, std::max(1, num_sms));
     plan->ksplit = 1;
-    if (plan->path == 0 && !split && a.epi == 0 && a.causal == 0 && !a.no_P && a.ksplit > 1) {
-        // Requested split-K (tiles that fill few SMs with a long K, e.g. the
-        // config-5 P·V accumulation M 4096 x N 128 x K 4096 = 32 tiles): ksplit
-        // units per tile, fp32 partials in the workspace, reduced in split order.
+    if (plan->path == 0 && !split && a.epi == 0 && a.causal == 0 && !a.no_P && a.ksplit >= 0) {
+        // Split-K for tiles that fill few SMs with a long K (the LoRA adapter
+        // GEMMs M 4096 x N 64 x K 4096-22016 = 32 tiles; config 5's P·V):
+        // ksplit units per tile, fp32 partials in the workspace, reduced in
+        // split order. Automatic (ksplit 0) when the tiles fill <= 1/4 of the
+        // SMs and K has >= 32 blocks; n > 1 forces n.
         const int nk = static_cast<int>((a.K * es + kAtom - 1) / kAtom);
-        const int ks = std::min(a.ksplit, nk);
+        int ks = a.ksplit;
+        if (ks == 0 && 4 * plan->tiles <= num_sms && nk >= 32)
+            ks = std::min({num_sms / std::max(1, plan->tiles), nk / 8, 8});
+        ks = std::min(ks, nk);
         if (ks >= 2) {
             plan->ksplit = ks;
             plan->grid = std::min(plan->tiles * ks, std::max(1, num_sms));

@@ -63,6 +63,39 @@ __global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, 
     }
 }
 
+// 16-bit transpose with 128-bit global accesses: a 64x64 tile per 256-thread
+// CTA; each thread loads two 8-element row chunks, scatters them transposed
+// into shared memory (row pitch 72 elements: the 8 rows a warp writes per
+// step land 2-way at most on a bank), then stores two 8-element chunks of
+// the transposed tile. rows % 8 == 0, cols % 8 == 0, 16-byte aligned.
+__global__ void __launch_bounds__(256) transpose16_vec(const std::uint16_t* __restrict__ in,
+                                                       std::uint16_t* __restrict__ out, int rows, int cols) {
+    constexpr int TP = 72;
+    __shared__ __align__(16) std::uint16_t tile[64 * TP];
+    const std::int64_t base = static_cast<std::int64_t>(blockIdx.z) * rows * cols;
+    const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int lr = t / 8 + 32 * k, lc = (t % 8) * 8;
+        const int r = r0 + lr, c = c0 + lc;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < rows && c < cols) v = __ldcs(reinterpret_cast<const uint4*>(in + base + static_cast<std::int64_t>(r) * cols + c));
+        const std::uint16_t* e = reinterpret_cast<const std::uint16_t*>(&v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tile[(lc + j) * TP + lr] = e[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int lc = t / 8 + 32 * k, lr = (t % 8) * 8;  // output row = input column
+        const int c = c0 + lc, r = r0 + lr;
+        if (c < cols && r < rows)
+            __stcs(reinterpret_cast<uint4*>(out + base + static_cast<std::int64_t>(c) * rows + r),
+                   *reinterpret_cast<const uint4*>(&tile[lc * TP + lr]));
+    }
+}
+
 // dx = r*(w.dy) - x * r^3 * mean((w.dy).x),  r = rsqrt(mean(x^2) + eps)
 __global__ void __launch_bounds__(kT) rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                          const __nv_bfloat16* __restrict__ w,
@@ -164,6 +197,13 @@ __global__ void __launch_bounds__(kT) row_sum_kernel(const float* __restrict__ v
 }  // namespace
 
 cudaError_t transpose(const void* in, void* out, int batch, int rows, int cols, int esize, cudaStream_t s) {
+    auto al16 = [](const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15) == 0; };
+    if (esize == 2 && rows % 8 == 0 && cols % 8 == 0 && al16(in) && al16(out)) {
+        dim3 g64((cols + 63) / 64, (rows + 63) / 64, batch);
+        transpose16_vec<<<g64, 256, 0, s>>>(static_cast<const std::uint16_t*>(in), static_cast<std::uint16_t*>(out),
+                                             rows, cols);
+        return cudaGetLastError();
+    }
     dim3 grid((cols + 31) / 32, (rows + 31) / 32, batch), block(32, 8);
     if (esize == 2)
         transpose_kernel<std::uint16_t><<<grid, block, 0, s>>>(static_cast<const std::uint16_t*>(in),

@@ -476,7 +476,8 @@ def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = N
 
 def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank: int = 16, rank_pad: int = 64,
                     lora_alpha: float = 16.0, std: float = 0.02, device: int = 0,
-                    recompute_attention: bool = True) -> GraphBuilder:
+                    recompute_attention: bool = True, recompute_ffn: bool = True,
+                    recompute_qkv: bool = True) -> GraphBuilder:
     """Config 4: one LoRA fine-tuning step (forward + backward) of a LLaMA
     model over `seq` tokens, rank-`rank` adapters on the fused QKV projection
     and on both FFN projections ("rank 16 on Q,K,V,FFN"), frozen
@@ -497,15 +498,25 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     q and k instead of keeping the forward's P (H·S² bf16 = 1 GB per 7B layer)
     live across the step: the planner then never offloads the n² tensor, at the
     cost of one more causal scores GEMM + softmax per layer. The recomputed P
-    is bitwise the forward's (same kernels, same inputs)."""
+    is bitwise the forward's (same kernels, same inputs).
+
+    `recompute_ffn` / `recompute_qkv` (defaults) extend the recompute to the
+    gate/up projection + SwiGLU (gu, act from the saved h2 and U2) and to the
+    QKV projection + RoPE (qkv, q, k from the saved h and U1): each layer then
+    keeps only the norm inputs / outputs and the rank-R adapter activations
+    live across the step. On the 7B step under 16 GiB this cuts the planned
+    activation offload from 20.6 to 6.9 GB (simulated step 0.82 -> 0.38 s) for
+    +28 % FLOPs (one more gate/up and QKV GEMM per layer)."""
     g = GraphBuilder(device_count=1)
-    _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "", recompute_attention)
+    _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "", recompute_attention,
+                    recompute_ffn, recompute_qkv)
     return g
 
 
 def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None = None, rank: int = 16,
                        rank_pad: int = 64, lora_alpha: float = 16.0, std: float = 0.02,
-                       recompute_attention: bool = True) -> GraphBuilder:
+                       recompute_attention: bool = True, recompute_ffn: bool = True,
+                       recompute_qkv: bool = True) -> GraphBuilder:
     """Config 4 over `dp` devices (data parallel): every memgraph
     device runs the full LoRA step on its own sequence (tokens/targets
     `@r`; the frozen weights and adapters are the same tensors on every device,
@@ -516,7 +527,7 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
     (same names as llama_lora_step's). Global batch = dp sequences."""
     g = GraphBuilder(device_count=dp)
     outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "",
-                            recompute_attention) for r in range(dp)]
+                            recompute_attention, recompute_ffn, recompute_qkv) for r in range(dp)]
     for name, v0 in outs[0].items():
         t = g.tensors[v0]
         n = int(np.prod(t.shape))
@@ -527,7 +538,7 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
 
 
 def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, rank_pad, lora_alpha, std, device,
-                    data_sfx, recompute_attention=True) -> dict:
+                    data_sfx, recompute_attention=True, recompute_ffn=False, recompute_qkv=False) -> dict:
     """Appends one LoRA step on `device` to `g`; returns {output name: vid}
     (the loss and every adapter gradient)."""
     L = cfg.layers if layers is None else layers
@@ -635,6 +646,21 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
     for l in reversed(range(L)):
         p, w, a = saved[l]
         dy = dx  # gradient of x_{l+1}
+        if recompute_ffn:  # gu and act again from the saved h2, U2 (bitwise the forward's)
+            gub_r = g.gemm(p + "gate_up_base.re", a["h2"], w["w13"], S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
+            gu_r = g.gemm(p + "gate_up.re", a["U2"], w["B2"], S, 2 * f, R, r=gub_r, alpha=sc, out_shape=(S, 2 * f),
+                          device=dev)
+            a = dict(a, gu=gu_r, act=g.kernel(p + "act.re", {"type": "silu_mul", "args": [gu_r], "rows": S, "cols": f},
+                                              (S, f), "bf16", dev))
+        if recompute_qkv:  # qkv, q, k again from the saved h, U1
+            base_r = g.gemm(p + "qkv_base.re", a["h"], w["wqkv"], S, 3 * d, d, out_shape=(S, 3 * d), device=dev)
+            qkv_r = g.gemm(p + "qkv.re", a["U1"], w["B1"], S, 3 * d, R, r=base_r, alpha=sc, out_shape=(S, 3 * d),
+                           device=dev)
+            a = dict(a, qkv=qkv_r,
+                     q=g.kernel(p + "q_rope.re", {"type": "rope", "args": [qkv_r, rope_tab], "seq": S, "ld": 3 * d,
+                                                  "col_off": 0, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev),
+                     k=g.kernel(p + "k_rope.re", {"type": "rope", "args": [qkv_r, rope_tab], "seq": S, "ld": 3 * d,
+                                                  "col_off": d, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev))
         # x_{l+1} = act·W2ᵀ + s·U3·B3ᵀ + x1
         V3 = lora_grads(p, "lora_w2", dy, d, f, a["U3"], a["act"], w["A3"], w["B3"])
         w2T = tr(p + "w2.T", w["w2"], d, f)

@@ -28,10 +28,14 @@ GIB = 1 << 30
 def cases():
     """(name, taskgraph builder, capacities, build kwargs) — shared with the test."""
     return [
-        ("lora7b_seq4096_cap16GiB_lazy", lambda: W.llama_lora_step(W.LLAMA_7B, 4096), [16 * GIB],
+        ("lora7b_seq4096_cap16GiB_lazy", lambda: W.llama_lora_step(W.LLAMA_7B, 4096, recompute_ffn=False,
+                                                                    recompute_qkv=False), [16 * GIB],
          {"alloc_horizon": "lazy"}),
-        ("lora7b_seq4096_cap16GiB_lazy_saveP", lambda: W.llama_lora_step(W.LLAMA_7B, 4096, recompute_attention=False),
+        ("lora7b_seq4096_cap16GiB_lazy_saveP", lambda: W.llama_lora_step(W.LLAMA_7B, 4096, recompute_attention=False,
+                                                                         recompute_ffn=False, recompute_qkv=False),
          [16 * GIB], {"alloc_horizon": "lazy"}),
+        ("lora7b_seq4096_cap16GiB_lazy_recompute", lambda: W.llama_lora_step(W.LLAMA_7B, 4096), [16 * GIB],
+         {"alloc_horizon": "lazy"}),
         ("blockwise_seq65536_h32_tile4096_lag8_cap16GiB_lazy",
          lambda: W.blockwise_attention(65536, 32, 128, 4096, lag=8), [16 * GIB], {"alloc_horizon": "lazy"}),
         ("llama65b_tp8_seq8192_layers10_cap0.9GiB_lazy", lambda: W.llama_prefill_tp(W.LLAMA_65B, 8192, 8, layers=10),
@@ -45,12 +49,20 @@ def h(s: str) -> str:
     return hashlib.sha256(s.encode()).hexdigest()
 
 
-def main():
+def main(only=None):
+    """Rebuilds every case with the reference (or only the named ones, keeping
+    the other entries of the existing corpus)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
     import _memplan as ref
 
     out = []
+    old = {}
+    if only:
+        old = {c["name"]: c for c in json.load(open(os.path.join(HERE, "scale_corpus.json")))["cases"]}
     for name, mk, caps, kw in cases():
+        if only and name not in only:
+            out.append(old[name])
+            continue
         tg = mk().to_json()
         t0 = time.perf_counter()
         mg, stats = ref.build_memgraph(tg, caps, mode="byte", **kw)
@@ -65,4 +77,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

@@ -581,7 +581,9 @@ def test_tensor_parallel_on_one_gpu_four_memgraph_devices():
 
 
 @pytest.mark.parametrize("shape", [dict(batch=1, rows=200, cols=72, dt="bf16"), dict(batch=3, rows=256, cols=128, dt="bf16"),
-                                   dict(batch=2, rows=64, cols=96, dt="f32")])
+                                   dict(batch=2, rows=64, cols=96, dt="f32"),
+                                   dict(batch=2, rows=4096, cols=136, dt="bf16"),   # 64x64 vector tiles, ragged N
+                                   dict(batch=1, rows=100, cols=36, dt="bf16")])    # rows % 8 != 0: scalar tiles
 def test_transpose_parity(shape):
     g = W.GraphBuilder()
     x = g.input("x", (shape["batch"], shape["rows"], shape["cols"]), shape["dt"], init=("normal", 1.0))

@@ -19,6 +19,7 @@ ap.add_argument("--residency", default="host")
 ap.add_argument("--compare", action="store_true")
 ap.add_argument("--exec-cfg", default="{}", help="extra executor config keys (JSON)")
 ap.add_argument("--horizon", default="lazy")
+ap.add_argument("--dump", default="", help="write the memgraph + one traced step here (JSON)")
 a = ap.parse_args()
 t0 = time.time()
 g = W.llama_lora_step(W.LLAMA_7B, a.seq, layers=a.layers)
@@ -35,7 +36,20 @@ del inputs
 pcie = bench.measure_pcie(dev)
 pk = bench.peaks()
 ts = bench.untimed_steps(ex, a.steps)  # timing-free completion events
-traced = json.loads(ex.run("event-driven", "fifo", 0))["makespan"]
+trj = json.loads(ex.run("event-driven", "fifo", 0))
+traced = trj["makespan"]
+if a.dump:
+    with open(a.dump, "w") as f:
+        json.dump({"memgraph": m, "trace": trj}, f)
+ids = {v["id"]: v for v in json.loads(g.to_json())["vertices"]}
+by_op = {}
+for r_ in trj["rows"]:
+    v = ids.get(r_["vertex"])
+    key = ((v.get("op") or {}).get("type") or v["kind"]) if v else "offload/reload"
+    if key == "gemm" and v:
+        o_ = v["op"]
+        key = "gemm_small" if min(o_["M"], o_["N"]) <= 128 else ("gemm_bmm" if o_.get("batch", 1) > 1 else "gemm")
+    by_op[key] = by_op.get(key, 0.0) + r_["end"] - r_["start"]
 stt = ex.stats()
 loss_id = next(o for o in g.outputs() if g.tensors[o].name == "loss")
 import struct
@@ -45,7 +59,8 @@ res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency
        "loss": loss, "tokens_per_s": round(a.seq / min(ts), 1), "flops": stt["flops"],
        "h2d_gb": round(stt["h2d_bytes"] / 1e9, 2), "d2h_gb": round(stt["d2h_bytes"] / 1e9, 2),
        "pcie_h2d_measured_gbs": round(pcie, 1), "kernel_busy_s": round(stt["kernel_busy_s"], 4),
-       "exposed_transfer_s": round(stt["exposed_transfer_s"], 4)}
+       "exposed_transfer_s": round(stt["exposed_transfer_s"], 4),
+       "device_time_by_op_s": {k: round(v, 4) for k, v in sorted(by_op.items(), key=lambda kv: -kv[1])}}
 roof = max(stt["flops"] / (pk["bf16_tflops_sustained"] * 1e12), stt["h2d_bytes"] / (pcie * 1e9),
            stt["d2h_bytes"] / (pcie * 1e9))
 res["roofline_s"] = round(roof, 4)
