@@ -92,10 +92,20 @@ def op_gemm(op, args, out):
     triangular (A[b][i][k>i] == 0, e.g. causal softmax probabilities), which
     lets the kernel skip the all-zero K blocks; the product is the plain one."""
     M, N, K, B = op["M"], op["N"], op["K"], op.get("batch", 1)
-    lda, ldb, ldc = op.get("lda") or K, op.get("ldb") or K, op.get("ldc") or N
+    a_mn, b_mn = op.get("a_major", "k") == "mn", op.get("b_major", "k") == "mn"
+    # MN-major operands: A stored [K, M], B stored [K, N] (row pitch lda / ldb)
+    lda = op.get("lda") or (M if a_mn else K)
+    ldb = op.get("ldb") or (N if b_mn else K)
+    ldc = op.get("ldc") or N
     ind, outd = op.get("in_dtype", "bf16"), op.get("out_dtype", "bf16")
-    A = strided(args[0], ind, op.get("a_off", 0), B, op.get("sa", 0), M, lda, K)
-    Bm = strided(args[1], ind, op.get("b_off", 0), B, op.get("sb", 0), N, ldb, K)
+    if a_mn:
+        A = np.transpose(strided(args[0], ind, op.get("a_off", 0), B, op.get("sa", 0), K, lda, M), (0, 2, 1))
+    else:
+        A = strided(args[0], ind, op.get("a_off", 0), B, op.get("sa", 0), M, lda, K)
+    if b_mn:
+        Bm = np.transpose(strided(args[1], ind, op.get("b_off", 0), B, op.get("sb", 0), K, ldb, N), (0, 2, 1))
+    else:
+        Bm = strided(args[1], ind, op.get("b_off", 0), B, op.get("sb", 0), N, ldb, K)
     causal = op.get("causal", 0)
     C = np.matmul(A, np.transpose(Bm, (0, 2, 1))) * np.float32(op.get("alpha", 1.0))
     if op.get("rs_arg", -1) >= 0:  # fused RMSNorm consumer: row m *= rsqrt(sum_c P[c][row0+m] / dim + eps)

@@ -500,8 +500,16 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             const std::int64_t ei = es(op.in_dtype), eo = es(op.out_dtype);
             auto extent = [](std::int64_t off, int batch, std::int64_t bs, std::int64_t rows, std::int64_t ld,
                              std::int64_t cols) { return off + (batch - 1) * bs + (rows - 1) * ld + cols; };
-            fits(extent(op.a_off, g.batch, g.sa, g.M, g.lda, g.K) * ei, arg_bytes[0], "A");
-            fits(extent(op.b_off, g.batch, g.sb, g.N, g.ldb, g.K) * ei, arg_bytes[1], "B");
+            g.a_mn = op.a_mn;
+            g.b_mn = op.b_mn;
+            if (op.a_mn && !op.lda) g.lda = op.M;  // MN-major: [K, M] / [K, N] row pitch
+            if (op.b_mn && !op.ldb) g.ldb = op.N;
+            if ((op.a_mn || op.b_mn) && (op.in_dtype != k::BF16 || op.epilogue != 0 || op.norm_out))
+                throw Error("gemm MN-major operands need bf16 inputs and the plain epilogue");
+            fits((op.a_mn ? extent(op.a_off, g.batch, g.sa, g.K, g.lda, g.M) : extent(op.a_off, g.batch, g.sa, g.M, g.lda, g.K)) * ei,
+                 arg_bytes[0], "A");
+            fits((op.b_mn ? extent(op.b_off, g.batch, g.sb, g.K, g.ldb, g.N) : extent(op.b_off, g.batch, g.sb, g.N, g.ldb, g.K)) * ei,
+                 arg_bytes[1], "B");
             if (op.epilogue == 2) fits(3 * op.heads * 128 * op.M * 2, out_bytes, "C (packed q|k|vT)");
             else fits(extent(op.c_off, g.batch, g.sc, g.M, g.ldc, n_out) * eo, out_bytes, "C");
             g.A = in.argp[0] + op.a_off * ei;

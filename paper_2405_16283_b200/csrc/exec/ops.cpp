@@ -134,6 +134,13 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
                 else if (tl == "wide") d.tile = 2;
                 else if (tl == "streamk") d.tile = 3;
                 else throw ParseError("gemm tile must be auto, narrow, wide or streamk");
+                auto major = [&](const char* key) {
+                    const std::string v = o.value(key, std::string("k"));
+                    if (v != "k" && v != "mn") throw ParseError(std::string("gemm ") + key + " must be k or mn");
+                    return v == "mn" ? 1 : 0;
+                };
+                d.a_mn = major("a_major");
+                d.b_mn = major("b_major");
                 d.ksplit = o.value("ksplit", 0);
                 if (d.ksplit < 0 || d.ksplit > 16) throw ParseError("gemm ksplit must be in [0, 16]");
                 const std::string pr = o.value("precision", std::string("tf32"));

@@ -68,6 +68,7 @@ struct OpDesc {
     int causal = 0;
     int epilogue = 0;  // gemm: 0 none, 1 swiglu, 2 qkv_rope
     int tile = 0;      // gemm: CTA-pair tile choice, 0 auto, 1 narrow 256x256, 2 wide 512x256
+    int a_mn = 0, b_mn = 0;  // gemm "a_major" / "b_major": "k" (default: A [M, K], B [N, K]) | "mn" (A [K, M], B [K, N])
     int ksplit = 0;    // gemm: 1-CTA split-K units per tile: 0 automatic, 1 none, n > 1 forced (partials reduced
                        // in split order)
     int split = 0;     // gemm, f32 inputs: 0 tf32, 1 3xTF32

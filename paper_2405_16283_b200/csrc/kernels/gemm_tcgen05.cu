@@ -93,7 +93,44 @@ struct Params {
     // unit arrives last), then runs the epilogue. The counter only elects the
     // reducer and is reset by it.
     int ksplit;
+    // MN-major operands (bf16): A stored [K, M] (M contiguous, row pitch lda),
+    // B stored [K, N]; staged as 64x64 boxes (64 M/N elements x 64 K rows, 8 KB,
+    // SWIZZLE_128B) read by MN-major UMMA descriptors (LBO = 8 KB between
+    // 64-element chunks, SBO = 1 KB between 8-row K groups, +2 KB per K = 16).
+    int a_mn, b_mn;
 };
+
+__device__ __forceinline__ std::uint64_t sdesc_mn(std::uint32_t saddr) {
+    std::uint64_t d = 0;
+    d |= static_cast<std::uint64_t>((saddr & 0x3FFFF) >> 4);
+    d |= static_cast<std::uint64_t>(8192 >> 4) << 16;
+    d |= static_cast<std::uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<std::uint64_t>(1) << 46;
+    d |= static_cast<std::uint64_t>(2) << 61;
+    return d;
+}
+// Operand descriptor and its per-K16 increment (descriptor units of 16 B).
+__device__ __forceinline__ std::uint64_t op_desc(std::uint32_t saddr, int mn) { return mn ? sdesc_mn(saddr) : sdesc(saddr); }
+__device__ __forceinline__ int op_kstep(int mn) { return mn ? 2048 >> 4 : 32 >> 4; }
+// Stages `rows` rows (M or N) x one 64-element K block of an operand at
+// smem `dst`: K-major = one box {64 K, rows}; MN-major = rows/64 boxes {64, 64 K}.
+__device__ __forceinline__ void load_operand(std::uint32_t dst, const CUtensorMap* map, int k0, int row0, int rows,
+                                             int batch, std::uint32_t bar, int mn) {
+    if (!mn) {
+        tma_load_3d(dst, map, k0, row0, batch, bar);
+        return;
+    }
+    for (int i = 0; i < rows / 64; ++i) tma_load_3d(dst + i * 8192, map, row0 + i * 64, k0, batch, bar);
+}
+// Same for the CTA-pair kernels (.cta_group::2 loads signalling the leader's barrier).
+__device__ __forceinline__ void load_operand_2sm(std::uint32_t dst, const CUtensorMap* map, int k0, int row0,
+                                                 int rows, int batch, std::uint32_t leader_bar, int mn) {
+    if (!mn) {
+        tma_load_3d_2sm(dst, map, k0, row0, batch, leader_bar);
+        return;
+    }
+    for (int i = 0; i < rows / 64; ++i) tma_load_3d_2sm(dst + i * 8192, map, row0 + i * 64, k0, batch, leader_bar);
+}
 
 __device__ __forceinline__ float row_alpha(const Params& p, int row, bool row_ok) {
     if (!p.rs_P || !row_ok) return p.alpha;
@@ -566,8 +603,8 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                     const std::uint32_t fb = full + 8 * stage;
                     mbar_expect_tx(fb, LOADED);
                     const std::uint32_t sa = sbase + stage * STAGE;
-                    tma_load_3d(sa, &ta, kb * bk, mb * kBM, p.a_batched ? b : 0, fb);
-                    tma_load_3d(sa + A_BYTES, &tb, kb * bk, nb * BN, p.b_batched ? b : 0, fb);
+                    load_operand(sa, &ta, kb * bk, mb * kBM, kBM, p.a_batched ? b : 0, fb, p.a_mn);
+                    load_operand(sa + A_BYTES, &tb, kb * bk, nb * BN, BN, p.b_batched ? b : 0, fb, p.b_mn);
                     if (++stage == kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -579,8 +616,11 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
         {  // whole warp: one elected lane issues (tc_mma)
             const std::uint32_t fmt = tf32 ? 2u : 1u;
             const std::uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
+                                        (static_cast<std::uint32_t>(p.a_mn) << 15) |
+                                        (static_cast<std::uint32_t>(p.b_mn) << 16) |
                                         (static_cast<std::uint32_t>(BN >> 3) << 17) |
                                         (static_cast<std::uint32_t>(kBM >> 4) << 24);
+            const int as = op_kstep(p.a_mn), bs = op_kstep(p.b_mn);
             int stage = 0, acc = 0;
             std::uint32_t phase = 0, acc_phase = 0;
             for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -598,7 +638,7 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                     mbar_wait((SPLIT ? splitb : full) + 8 * stage, phase);
                     tc_fence_after();
                     const std::uint32_t sa = sbase + stage * STAGE;
-                    const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + A_BYTES);
+                    const std::uint64_t ad = op_desc(sa, p.a_mn), bd = op_desc(sa + A_BYTES, p.b_mn);
                     if (SPLIT) {
                         const std::uint64_t al = sdesc(sa + LOADED), bl = sdesc(sa + LOADED + A_BYTES);
 #pragma unroll
@@ -609,8 +649,8 @@ __global__ void __launch_bounds__(threads_1cta<BN, SPLIT>(), 1)
                         }
                     } else {
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)  // 4 x 32 bytes of K per 128-byte block
-                            tc_mma(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0) | (k != 0), tf32);
+                        for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-element K block
+                            tc_mma(d, ad + as * k, bd + bs * k, idesc, (kb != kb0) | (k != 0), tf32);
                     }
                     tc_commit(empty + 8 * stage);
                     if (++stage == kStages) {
@@ -934,8 +974,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const std::uint32_t fb = full_leader0 + 8 * stage;
                     if (leader) mbar_expect_tx(full + 8 * stage, 2 * (A_BYTES + brows * kAtom));
                     const std::uint32_t sa = sbase + stage * STAGE;
-                    tma_load_3d_2sm(sa, &ta, kb * bk, mb * BM2 + rank * HALF, p.a_batched ? b : 0, fb);
-                    tma_load_3d_2sm(sa + A_BYTES, mb_map, kb * bk, brow, p.b_batched ? b : 0, fb);
+                    load_operand_2sm(sa, &ta, kb * bk, mb * BM2 + rank * HALF, HALF, p.a_batched ? b : 0, fb, p.a_mn);
+                    load_operand_2sm(sa + A_BYTES, mb_map, kb * bk, brow, brows, p.b_batched ? b : 0, fb, p.b_mn);
                     if (++stage == kStages2) {
                         stage = 0;
                         phase ^= 1;
@@ -949,7 +989,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0, acc = 0;
             std::uint32_t phase = 0, acc_phase = 0;
             for_each_segment(p, pair, npairs, bk, [&](int, int, int, int, int sl, int kb0, int kb1, int, long long) {
-                const std::uint32_t idesc = make_idesc(fmt, BM2, BN / sl);
+                const std::uint32_t idesc = make_idesc(fmt, BM2, BN / sl) | (static_cast<std::uint32_t>(p.a_mn) << 15) |
+                                            (static_cast<std::uint32_t>(p.b_mn) << 16);
+                const int as = op_kstep(p.a_mn), bs = op_kstep(p.b_mn);
                 mbar_wait(tempty + 8 * acc, acc_phase ^ 1);
                 tc_fence_after();
                 const std::uint32_t d = tmem + acc * BN;
@@ -957,9 +999,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(full + 8 * stage, phase);
                     tc_fence_after();
                     const std::uint32_t sa = sbase + stage * STAGE;
-                    const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + A_BYTES);
+                    const std::uint64_t ad = op_desc(sa, p.a_mn), bd = op_desc(sa + A_BYTES, p.b_mn);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) tc_mma_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0) | (k != 0), tf32);
+                    for (int k = 0; k < 4; ++k)
+                        tc_mma_2sm(d, ad + as * k, bd + bs * k, idesc, (kb != kb0) | (k != 0), tf32);
                     tc_commit_2sm(empty + 8 * stage);
                     if (++stage == kStages2) {
                         stage = 0;
@@ -1209,16 +1252,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                 const int nk = tile_nk(mb);
                 const CUtensorMap* bmap = sl == 1 ? &tb : sl == 2 ? &tbh : &tbq;
                 const int brow = slice_brow(p, nb, k, sl, static_cast<int>(rank));
-                const std::uint32_t tx = 2 * (2 * A_SUB + (BN / 2 / sl) * kAtom);
+                const int brows = BN / 2 / sl;  // B rows staged per CTA
+                const std::uint32_t tx = 2 * (2 * A_SUB + brows * kAtom);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(empty + 8 * stage, phase ^ 1);
                     const std::uint32_t fb = full_leader0 + 8 * stage;
                     if (leader) mbar_expect_tx(full + 8 * stage, tx);
                     const std::uint32_t sa = sbase + stage * STAGE;
                     const int ab = p.a_batched ? b : 0;
-                    tma_load_3d_2sm(sa, &ta, kb * bk, mb * BMW + rank * HALF, ab, fb);
-                    tma_load_3d_2sm(sa + A_SUB, &ta, kb * bk, mb * BMW + 256 + rank * HALF, ab, fb);
-                    tma_load_3d_2sm(sa + 2 * A_SUB, bmap, kb * bk, brow, p.b_batched ? b : 0, fb);
+                    load_operand_2sm(sa, &ta, kb * bk, mb * BMW + rank * HALF, HALF, ab, fb, p.a_mn);
+                    load_operand_2sm(sa + A_SUB, &ta, kb * bk, mb * BMW + 256 + rank * HALF, HALF, ab, fb, p.a_mn);
+                    load_operand_2sm(sa + 2 * A_SUB, bmap, kb * bk, brow, brows, p.b_batched ? b : 0, fb, p.b_mn);
                     if (++stage == kStagesW) {
                         stage = 0;
                         phase ^= 1;
@@ -1234,17 +1278,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             int defer_stage[kStagesW];
             for_each_tile([&](int, int mb, int, int, int sl) {
                 const int nk = tile_nk(mb);
-                const std::uint32_t idesc = make_idesc(fmt, 256, BN / sl);
+                const std::uint32_t idesc = make_idesc(fmt, 256, BN / sl) | (static_cast<std::uint32_t>(p.a_mn) << 15) |
+                                            (static_cast<std::uint32_t>(p.b_mn) << 16);
+                const int as = op_kstep(p.a_mn), bs = op_kstep(p.b_mn);
                 mbar_wait(tempty, tphase ^ 1);  // half 0 drained by the previous tile's epilogue
                 tc_fence_after();
                 bool h1_ready = false;
                 int ndefer = 0, h1_done = 0;  // half-1 K blocks issued so far
                 auto issue_h1 = [&](int st) {
                     const std::uint32_t sa = sbase + st * STAGE;
-                    const std::uint64_t ad = sdesc(sa + A_SUB), bd = sdesc(sa + 2 * A_SUB);
+                    const std::uint64_t ad = op_desc(sa + A_SUB, p.a_mn), bd = op_desc(sa + 2 * A_SUB, p.b_mn);
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        tc_mma_2sm(tmem + 256, ad + 2 * k, bd + 2 * k, idesc, (h1_done | k) != 0, tf32);
+                        tc_mma_2sm(tmem + 256, ad + as * k, bd + bs * k, idesc, (h1_done | k) != 0, tf32);
                     tc_commit_2sm(empty + 8 * st);
                     ++h1_done;
                 };
@@ -1252,9 +1298,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
                     mbar_wait(full + 8 * stage, phase);
                     tc_fence_after();
                     const std::uint32_t sa = sbase + stage * STAGE;
-                    const std::uint64_t ad = sdesc(sa), bd = sdesc(sa + 2 * A_SUB);
+                    const std::uint64_t ad = op_desc(sa, p.a_mn), bd = op_desc(sa + 2 * A_SUB, p.b_mn);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) tc_mma_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0, tf32);
+                    for (int k = 0; k < 4; ++k) tc_mma_2sm(tmem, ad + as * k, bd + bs * k, idesc, (kb | k) != 0, tf32);
                     if (!h1_ready) {
                         defer_stage[ndefer++] = stage;
                         const bool drained = __shfl_sync(0xffffffffu, mbar_test(tempty + 8, tphase ^ 1), 0);
@@ -1346,7 +1392,20 @@ __global__ void gemm_simt_kernel(GemmArgs a) {
     }
     auto dot = [&](int col) {
         float acc = 0.f;
-        if (a.in_dtype == BF16) {
+        if (a.a_mn || a.b_mn) {  // MN-major operand(s): element (m|n, k) at k * ld + m|n
+            const std::int64_t as = a.a_mn ? a.lda : 1, am = a.a_mn ? 1 : a.lda;
+            const std::int64_t bs = a.b_mn ? a.ldb : 1, bn = a.b_mn ? 1 : a.ldb;
+            const std::int64_t a0 = b * a.sa + static_cast<std::int64_t>(m) * am, b0 = b * a.sb + static_cast<std::int64_t>(col) * bn;
+            if (a.in_dtype == BF16) {
+                const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A);
+                const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B);
+                for (int k = lane; k < kend; k += 32) acc += __bfloat162float(A[a0 + k * as]) * __bfloat162float(B[b0 + k * bs]);
+            } else {
+                const float* A = static_cast<const float*>(a.A);
+                const float* B = static_cast<const float*>(a.B);
+                for (int k = lane; k < kend; k += 32) acc += A[a0 + k * as] * B[b0 + k * bs];
+            }
+        } else if (a.in_dtype == BF16) {
             const __nv_bfloat16* A = static_cast<const __nv_bfloat16*>(a.A) + b * a.sa + static_cast<std::int64_t>(m) * a.lda;
             const __nv_bfloat16* B = static_cast<const __nv_bfloat16*>(a.B) + b * a.sb + static_cast<std::int64_t>(col) * a.ldb;
             const bool vec = ((reinterpret_cast<std::uintptr_t>(A) | reinterpret_cast<std::uintptr_t>(B)) & 15) == 0;
@@ -1467,16 +1526,21 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
     const int bn = split ? (a.N >= 128 && tiles128 >= num_sms ? 128 : 64) : a.N >= 256 ? 256 : a.N >= 128 ? 128 : 64;
     const bool two_sm = !split && a.M >= 256 && a.N >= 256;
     if (a.split && a.in_dtype != F32) return cudaErrorInvalidValue;
-    bool ok = (!split || (a.epi == 0 && !a.no_P && !a.rs_P)) &&
+    const bool mn = a.a_mn || a.b_mn;
+    bool ok = (!mn || (a.in_dtype == BF16 && !split && a.epi == 0 && !a.no_P)) &&
+              (!split || (a.epi == 0 && !a.no_P && !a.rs_P)) &&
               (a.epi == 0 || (a.N % 256 == 0 && bn == 256 && a.R == nullptr)) &&
               (a.epi != 2 || (a.batch == 1 && (reinterpret_cast<std::uintptr_t>(a.rope) & 15) == 0)) && a.M >= kBM && a.N >= bn && a.K * es >= kAtom && al16(a.A) && al16(a.B) && (a.lda * es) % 16 == 0 &&
               (a.ldb * es) % 16 == 0 && (a.batch == 1 || ((a.sa * es) % 16 == 0 && (a.sb * es) % 16 == 0)) &&
               (a.in_dtype == BF16 || a.in_dtype == F32);
     if (ok) {
         const bool ab = a.batch > 1 && a.sa != 0, bb = a.batch > 1 && a.sb != 0;
-        ok = encode(&plan->ta, a.A, es, a.K, a.M, a.lda, ab ? a.batch : 1, a.sa, kBM) &&
-             encode(&plan->tb, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, two_sm ? 128 : bn);
-        plan->tbh_ok = ok && two_sm && encode(&plan->tbh, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, 64) &&
+        // MN-major operands: [K rows, M|N contiguous] maps with 64x64 boxes (load_operand)
+        ok = (a.a_mn ? encode_tma_3d(&plan->ta, a.A, es, a.M, a.K, a.lda, ab ? a.batch : 1, a.sa, 64, 64)
+                     : encode(&plan->ta, a.A, es, a.K, a.M, a.lda, ab ? a.batch : 1, a.sa, kBM)) &&
+             (a.b_mn ? encode_tma_3d(&plan->tb, a.B, es, a.N, a.K, a.ldb, bb ? a.batch : 1, a.sb, 64, 64)
+                     : encode(&plan->tb, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, two_sm ? 128 : bn));
+        plan->tbh_ok = ok && two_sm && !a.b_mn && encode(&plan->tbh, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, 64) &&
                        encode(&plan->tbq, a.B, es, a.K, a.N, a.ldb, bb ? a.batch : 1, a.sb, 32);
         // C for the TMA-store epilogue: {64 B x 32 rows} boxes, SWIZZLE_64B
         const int oes = dtype_size(a.out_dtype);
@@ -1580,7 +1644,7 @@ cudaError_t gemm_prepare(const GemmArgs& a, GemmPlan* plan, int num_sms) {
         // blocks). Measured on B200 it never beat the sliced tail (fix-up
         // traffic + serialised finishers), so it is off by default.
         static const char* sk_env = std::getenv("TN_GEMM_SK");
-        const bool sk_on = plan->path == 2 && !a.no_P && (tile == 3 || (sk_env && std::strcmp(sk_env, "1") == 0));
+        const bool sk_on = plan->path == 2 && !a.no_P && !mn && (tile == 3 || (sk_env && std::strcmp(sk_env, "1") == 0));
         if (sk_on) {
             if (a.causal == 0 && T >= npairs && T % npairs != 0) {
                 const int sk = T / npairs >= 2 ? T % npairs + npairs : T;
@@ -1656,6 +1720,8 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t s, GemmWorkspace* ws)
     p.dp_tiles = plan.tiles - plan.tail_units / p.tail_split;
     p.tma_c = plan.tc_ok && (plan.path == 2 || plan.path == 3) && (a.epi == 0 || a.epi == 1) ? 1 : 0;
     p.split = a.split && a.in_dtype == F32 && plan.path == 0 ? 1 : 0;
+    p.a_mn = a.a_mn ? 1 : 0;
+    p.b_mn = a.b_mn ? 1 : 0;
     p.rs_P = a.rs_P;
     p.rs_ld = a.rs_ld;
     p.rs_row0 = a.rs_row0;

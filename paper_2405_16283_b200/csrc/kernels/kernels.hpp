@@ -58,6 +58,8 @@ struct GemmArgs {
                                  // memory, C += Alo·Bhi + Ahi·Blo + Ahi·Bhi; fp32-accurate), 0 = tf32
     int tile = 0;                // CTA-pair tile: 0 auto, 1 narrow (256x256), 2 wide (512x256),
                                  // 3 narrow with a stream-K tail (instead of half-width tail tiles)
+    int a_mn = 0, b_mn = 0;      // MN-major operands (bf16): A stored [K, M] / B stored [K, N], row pitch lda /
+                                 // ldb (>= M / N), batch strides sa / sb
     int ksplit = 0;              // 1-CTA split-K units per tile: 0 automatic, -1 off, n > 1 forced (needs a
                                  // GemmWorkspace with counters; plain epilogue, causal 0)
 };

@@ -477,7 +477,7 @@ def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = N
 def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank: int = 16, rank_pad: int = 64,
                     lora_alpha: float = 16.0, std: float = 0.02, device: int = 0,
                     recompute_attention: bool = True, recompute_ffn: bool = True,
-                    recompute_qkv: bool = True) -> GraphBuilder:
+                    recompute_qkv: bool = True, mn_major: bool = True) -> GraphBuilder:
     """Config 4: one LoRA fine-tuning step (forward + backward) of a LLaMA
     model over `seq` tokens, rank-`rank` adapters on the fused QKV projection
     and on both FFN projections ("rank 16 on Q,K,V,FFN"), frozen
@@ -506,17 +506,22 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     keeps only the norm inputs / outputs and the rank-R adapter activations
     live across the step. On the 7B step under 16 GiB this cuts the planned
     activation offload from 20.6 to 6.9 GB (simulated step 0.82 -> 0.38 s) for
-    +28 % FLOPs (one more gate/up and QKV GEMM per layer)."""
+    +28 % FLOPs (one more gate/up and QKV GEMM per layer).
+
+    `mn_major` (default): the backward GEMMs read transposed operands in place
+    ("a_major" / "b_major": "mn", e.g. dX = dY·W with W stored [out, in]) instead
+    of through explicit transpose vertices (≈1,000 vertices and ~3 GB of
+    transposed copies per layer on the 7B step, n² probability tiles included)."""
     g = GraphBuilder(device_count=1)
     _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "", recompute_attention,
-                    recompute_ffn, recompute_qkv)
+                    recompute_ffn, recompute_qkv, mn_major)
     return g
 
 
 def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None = None, rank: int = 16,
                        rank_pad: int = 64, lora_alpha: float = 16.0, std: float = 0.02,
                        recompute_attention: bool = True, recompute_ffn: bool = True,
-                       recompute_qkv: bool = True) -> GraphBuilder:
+                       recompute_qkv: bool = True, mn_major: bool = True) -> GraphBuilder:
     """Config 4 over `dp` devices (data parallel): every memgraph
     device runs the full LoRA step on its own sequence (tokens/targets
     `@r`; the frozen weights and adapters are the same tensors on every device,
@@ -527,7 +532,7 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
     (same names as llama_lora_step's). Global batch = dp sequences."""
     g = GraphBuilder(device_count=dp)
     outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "",
-                            recompute_attention, recompute_ffn, recompute_qkv) for r in range(dp)]
+                            recompute_attention, recompute_ffn, recompute_qkv, mn_major) for r in range(dp)]
     for name, v0 in outs[0].items():
         t = g.tensors[v0]
         n = int(np.prod(t.shape))
@@ -538,7 +543,8 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
 
 
 def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, rank_pad, lora_alpha, std, device,
-                    data_sfx, recompute_attention=True, recompute_ffn=False, recompute_qkv=False) -> dict:
+                    data_sfx, recompute_attention=True, recompute_ffn=False, recompute_qkv=False,
+                    mn_major=False) -> dict:
     """Appends one LoRA step on `device` to `g`; returns {output name: vid}
     (the loss and every adapter gradient)."""
     L = cfg.layers if layers is None else layers
@@ -623,13 +629,24 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
                                         "scale": 1.0 / S, "in_dtype": "bf16"}, (1,), "f32", dev)
     dlog = g.kernel("dlogits", {"type": "xent_grad", "args": [logits, tgt], "rows": S, "vocab": V, "scale": 1.0 / S,
                                 "in_dtype": "bf16", "out_dtype": "bf16"}, (S, V), "bf16", dev)
-    woutT = tr("output.T", wout, V, d)
-    dhn = g.gemm("d_final_norm_out", dlog, woutT, S, d, V, out_shape=(S, d), device=dev)
+    if mn_major:  # B = wout stored [V = K, d = N]
+        dhn = g.gemm("d_final_norm_out", dlog, wout, S, d, V, b_major="mn", out_shape=(S, d), device=dev)
+    else:
+        woutT = tr("output.T", wout, V, d)
+        dhn = g.gemm("d_final_norm_out", dlog, woutT, S, d, V, out_shape=(S, d), device=dev)
     dx = rms_bwd("d_x_final", xL, wn, dhn)
 
     def lora_grads(p, nm, dY, n_out, k_in, U, X, A, B):
         """dY [S, n_out] of Y = X Wᵀ + s U Bᵀ with U = X Aᵀ: returns V = dY·B and emits
         dB = s dYᵀU [n_out, R], dA = s VᵀX [R, k_in] as graph outputs."""
+        if mn_major:  # B [n_out, R], dY [S, n_out], U [S, R], X [S, k_in], V [S, R] read in place
+            Vv = g.gemm(p + nm + ".V", dY, B, S, R, n_out, b_major="mn", out_shape=(S, R), device=dev)
+            results[p + nm + ".dB"] = g.gemm(p + nm + ".dB", dY, U, n_out, R, S, a_major="mn", b_major="mn",
+                                             alpha=sc, out_shape=(n_out, R), device=dev)
+            dAT = g.gemm(p + nm + ".dA.T", X, Vv, k_in, R, S, a_major="mn", b_major="mn", alpha=sc,
+                         out_shape=(k_in, R), device=dev)
+            results[p + nm + ".dA"] = tr(p + nm + ".dA", dAT, k_in, R)
+            return Vv
         BT = tr(p + nm + ".B.T", B, n_out, R)
         Vv = g.gemm(p + nm + ".V", dY, BT, S, R, n_out, out_shape=(S, R), device=dev)
         dYT = tr(p + nm + ".dY.T", dY, S, n_out)
@@ -663,21 +680,35 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
                                                   "col_off": d, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev))
         # x_{l+1} = act·W2ᵀ + s·U3·B3ᵀ + x1
         V3 = lora_grads(p, "lora_w2", dy, d, f, a["U3"], a["act"], w["A3"], w["B3"])
-        w2T = tr(p + "w2.T", w["w2"], d, f)
-        A3T = tr(p + "lora_w2.A.T", w["A3"], R, f)
-        da0 = g.gemm(p + "d_act_base", dy, w2T, S, f, d, out_shape=(S, f), device=dev)
-        da = g.gemm(p + "d_act", V3, A3T, S, f, R, r=da0, alpha=sc, out_shape=(S, f), device=dev)
+        if mn_major:  # W2 [d, f], A3 [R, f] read MN-major
+            da0 = g.gemm(p + "d_act_base", dy, w["w2"], S, f, d, b_major="mn", out_shape=(S, f), device=dev)
+            da = g.gemm(p + "d_act", V3, w["A3"], S, f, R, r=da0, alpha=sc, b_major="mn", out_shape=(S, f),
+                        device=dev)
+        else:
+            w2T = tr(p + "w2.T", w["w2"], d, f)
+            A3T = tr(p + "lora_w2.A.T", w["A3"], R, f)
+            da0 = g.gemm(p + "d_act_base", dy, w2T, S, f, d, out_shape=(S, f), device=dev)
+            da = g.gemm(p + "d_act", V3, A3T, S, f, R, r=da0, alpha=sc, out_shape=(S, f), device=dev)
         dgu = g.kernel(p + "d_gate_up", {"type": "swiglu_bwd", "args": [a["gu"], da], "rows": S, "cols": f},
                        (S, 2 * f), "bf16", dev)
         V2 = lora_grads(p, "lora_w13", dgu, 2 * f, d, a["U2"], a["h2"], w["A2"], w["B2"])
-        w13T = tr(p + "w13.T", w["w13"], 2 * f, d)
-        A2T = tr(p + "lora_w13.A.T", w["A2"], R, d)
-        dh2_0 = g.gemm(p + "d_ffn_norm_out_base", dgu, w13T, S, d, 2 * f, out_shape=(S, d), device=dev)
-        dh2 = g.gemm(p + "d_ffn_norm_out", V2, A2T, S, d, R, r=dh2_0, alpha=sc, out_shape=(S, d), device=dev)
+        if mn_major:
+            dh2_0 = g.gemm(p + "d_ffn_norm_out_base", dgu, w["w13"], S, d, 2 * f, b_major="mn", out_shape=(S, d),
+                           device=dev)
+            dh2 = g.gemm(p + "d_ffn_norm_out", V2, w["A2"], S, d, R, r=dh2_0, alpha=sc, b_major="mn",
+                         out_shape=(S, d), device=dev)
+        else:
+            w13T = tr(p + "w13.T", w["w13"], 2 * f, d)
+            A2T = tr(p + "lora_w13.A.T", w["A2"], R, d)
+            dh2_0 = g.gemm(p + "d_ffn_norm_out_base", dgu, w13T, S, d, 2 * f, out_shape=(S, d), device=dev)
+            dh2 = g.gemm(p + "d_ffn_norm_out", V2, A2T, S, d, R, r=dh2_0, alpha=sc, out_shape=(S, d), device=dev)
         dx1 = add(p + "d_x1", dy, rms_bwd(p + "d_x1_norm", a["x1"], w["wn2"], dh2))
         # x1 = o·Woᵀ + x ; o[:, head h] = P_h·V_h
-        woT = tr(p + "wo.T", w["wo"], d, d)
-        do = g.gemm(p + "d_attn", dx1, woT, S, d, d, out_shape=(S, d), device=dev)
+        if mn_major:
+            do = g.gemm(p + "d_attn", dx1, w["wo"], S, d, d, b_major="mn", out_shape=(S, d), device=dev)
+        else:
+            woT = tr(p + "wo.T", w["wo"], d, d)
+            do = g.gemm(p + "d_attn", dx1, woT, S, d, d, out_shape=(S, d), device=dev)
         dP = g.gemm(p + "d_probs", do, a["qkv"], S, S, hd, batch=H, lda=d, sa=hd, ldb=3 * d, b_off=2 * d, sb=hd,
                     sc=S * S, out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
         if recompute_attention:  # P again from the saved q, k (bitwise the forward's)
@@ -689,47 +720,73 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
             P = a["P"]
         dS = g.kernel(p + "d_scores", {"type": "softmax_bwd", "args": [P, dP], "batch": H, "rows": S, "cols": S,
                                        "causal": 1, "in_dtype": "f32"}, (H, S, S), "bf16", dev)
-        kT = tr(p + "k.T", a["k"], S, hd, batch=H)
-        dq_r = g.gemm(p + "d_q_rot", dS, kT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
-                      alpha=scale, causal=2, out_shape=(S, d), device=dev)
-        dST = tr(p + "d_scores.T", dS, S, S, batch=H)
-        qT = tr(p + "q.T", a["q"], S, hd, batch=H)
-        dk_r = g.gemm(p + "d_k_rot", dST, qT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
-                      alpha=scale, out_shape=(S, d), device=dev)
-        PT = tr(p + "probs.T", P, S, S, batch=H)
-        doT = g.kernel(p + "d_attn.T", {"type": "transpose_heads", "args": [do], "seq": S, "ld": d, "col_off": 0,
-                                        "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
-        dv = g.gemm(p + "d_v", PT, doT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
-                    out_shape=(S, d), device=dev)
+        if mn_major:  # k, q [H, S, hd], dS / P [H, queries, keys], do [S, d] read in place
+            dq_r = g.gemm(p + "d_q_rot", dS, a["k"], S, hd, S, batch=H, lda=S, ldb=hd, ldc=d, sa=S * S, sb=hd * S,
+                          sc=hd, alpha=scale, causal=2, b_major="mn", out_shape=(S, d), device=dev)
+            dk_r = g.gemm(p + "d_k_rot", dS, a["q"], S, hd, S, batch=H, lda=S, ldb=hd, ldc=d, sa=S * S, sb=hd * S,
+                          sc=hd, alpha=scale, a_major="mn", b_major="mn", out_shape=(S, d), device=dev)
+            dv = g.gemm(p + "d_v", P, do, S, hd, S, batch=H, lda=S, ldb=d, ldc=d, sa=S * S, sb=hd, sc=hd,
+                        a_major="mn", b_major="mn", out_shape=(S, d), device=dev)
+        else:
+            kT = tr(p + "k.T", a["k"], S, hd, batch=H)
+            dq_r = g.gemm(p + "d_q_rot", dS, kT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                          alpha=scale, causal=2, out_shape=(S, d), device=dev)
+            dST = tr(p + "d_scores.T", dS, S, S, batch=H)
+            qT = tr(p + "q.T", a["q"], S, hd, batch=H)
+            dk_r = g.gemm(p + "d_k_rot", dST, qT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S,
+                          sc=hd, alpha=scale, out_shape=(S, d), device=dev)
+            PT = tr(p + "probs.T", P, S, S, batch=H)
+            doT = g.kernel(p + "d_attn.T", {"type": "transpose_heads", "args": [do], "seq": S, "ld": d, "col_off": 0,
+                                            "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
+            dv = g.gemm(p + "d_v", PT, doT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                        out_shape=(S, d), device=dev)
         dq = g.kernel(p + "d_q", {"type": "rope", "args": [dq_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
                                   "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
         dk = g.kernel(p + "d_k", {"type": "rope", "args": [dk_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
                                   "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
         # qkv = h·Wqkvᵀ + s·U1·B1ᵀ with dqkv = [dq | dk | dv]
-        B1T = tr(p + "lora_qkv.B.T", w["B1"], 3 * d, R)
         V1 = None
         dBs = []
-        U1T = tr(p + "lora_qkv.U.T", a["U1"], S, R)
-        for j, dpart in enumerate((dq, dk, dv)):
-            V1 = g.gemm(p + f"lora_qkv.V{j}", dpart, B1T, S, R, d, ldb=3 * d, b_off=j * d, r=V1,
-                        out_shape=(S, R), device=dev)
-            dT = tr(p + f"lora_qkv.dY{j}.T", dpart, S, d)
-            dBs.append(g.gemm(p + f"lora_qkv.dB{j}", dT, U1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev))
-        results[p + "lora_qkv.dB"] = g.kernel(p + "lora_qkv.dB", {"type": "concat", "args": dBs, "count": d * R,
-                                                                  "out_dtype": "bf16"}, (3 * d, R), "bf16", dev)
-        V1T = tr(p + "lora_qkv.V.T", V1, S, R)
-        hT = tr(p + "lora_qkv.X.T", a["h"], S, d)
-        dA1T = g.gemm(p + "lora_qkv.dA.T", hT, V1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev)
+        if mn_major:  # B1 [3d, R] (part j: rows j*d..), U1 [S, R], dq/dk/dv [S, d], h [S, d], V1 [S, R]
+            for j, dpart in enumerate((dq, dk, dv)):
+                V1 = g.gemm(p + f"lora_qkv.V{j}", dpart, w["B1"], S, R, d, ldb=R, b_off=j * d * R, r=V1,
+                            b_major="mn", out_shape=(S, R), device=dev)
+                dBs.append(g.gemm(p + f"lora_qkv.dB{j}", dpart, a["U1"], d, R, S, alpha=sc, a_major="mn",
+                                  b_major="mn", out_shape=(d, R), device=dev))
+            results[p + "lora_qkv.dB"] = g.kernel(p + "lora_qkv.dB", {"type": "concat", "args": dBs, "count": d * R,
+                                                                      "out_dtype": "bf16"}, (3 * d, R), "bf16", dev)
+            dA1T = g.gemm(p + "lora_qkv.dA.T", a["h"], V1, d, R, S, alpha=sc, a_major="mn", b_major="mn",
+                          out_shape=(d, R), device=dev)
+        else:
+            B1T = tr(p + "lora_qkv.B.T", w["B1"], 3 * d, R)
+            U1T = tr(p + "lora_qkv.U.T", a["U1"], S, R)
+            for j, dpart in enumerate((dq, dk, dv)):
+                V1 = g.gemm(p + f"lora_qkv.V{j}", dpart, B1T, S, R, d, ldb=3 * d, b_off=j * d, r=V1,
+                            out_shape=(S, R), device=dev)
+                dT = tr(p + f"lora_qkv.dY{j}.T", dpart, S, d)
+                dBs.append(g.gemm(p + f"lora_qkv.dB{j}", dT, U1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev))
+            results[p + "lora_qkv.dB"] = g.kernel(p + "lora_qkv.dB", {"type": "concat", "args": dBs, "count": d * R,
+                                                                      "out_dtype": "bf16"}, (3 * d, R), "bf16", dev)
+            V1T = tr(p + "lora_qkv.V.T", V1, S, R)
+            hT = tr(p + "lora_qkv.X.T", a["h"], S, d)
+            dA1T = g.gemm(p + "lora_qkv.dA.T", hT, V1T, d, R, S, alpha=sc, out_shape=(d, R), device=dev)
         results[p + "lora_qkv.dA"] = tr(p + "lora_qkv.dA", dA1T, d, R)
         if l == 0:
             break  # no gradient is needed below the first layer
-        wqkvT = tr(p + "wqkv.T", w["wqkv"], 3 * d, d)
-        A1T = tr(p + "lora_qkv.A.T", w["A1"], R, d)
         dh = None
-        for j, dpart in enumerate((dq, dk, dv)):
-            dh = g.gemm(p + f"d_attn_norm_out{j}", dpart, wqkvT, S, d, d, ldb=3 * d, b_off=j * d, r=dh,
+        if mn_major:  # Wqkv [3d, d] (part j: rows j*d..), A1 [R, d]
+            for j, dpart in enumerate((dq, dk, dv)):
+                dh = g.gemm(p + f"d_attn_norm_out{j}", dpart, w["wqkv"], S, d, d, ldb=d, b_off=j * d * d, r=dh,
+                            b_major="mn", out_shape=(S, d), device=dev)
+            dh = g.gemm(p + "d_attn_norm_out", V1, w["A1"], S, d, R, r=dh, alpha=sc, b_major="mn",
                         out_shape=(S, d), device=dev)
-        dh = g.gemm(p + "d_attn_norm_out", V1, A1T, S, d, R, r=dh, alpha=sc, out_shape=(S, d), device=dev)
+        else:
+            wqkvT = tr(p + "wqkv.T", w["wqkv"], 3 * d, d)
+            A1T = tr(p + "lora_qkv.A.T", w["A1"], R, d)
+            for j, dpart in enumerate((dq, dk, dv)):
+                dh = g.gemm(p + f"d_attn_norm_out{j}", dpart, wqkvT, S, d, d, ldb=3 * d, b_off=j * d, r=dh,
+                            out_shape=(S, d), device=dev)
+            dh = g.gemm(p + "d_attn_norm_out", V1, A1T, S, d, R, r=dh, alpha=sc, out_shape=(S, d), device=dev)
         dx = add(p + "d_x", dx1, rms_bwd(p + "d_x_norm", a["x"], w["wn1"], dh))
     return results
 

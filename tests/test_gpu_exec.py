@@ -36,8 +36,9 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     g = W.GraphBuilder()
     sa = kw.pop("sa", M * K if batch > 1 else 0)
     sb = kw.pop("sb", N * K if batch > 1 else 0)
-    a = g.input("A", (batch, M, K), in_dtype, init=("normal", 1.0))
-    b = g.input("B", (batch, N, K), in_dtype, init=("normal", 1.0))
+    a_mn, b_mn = kw.get("a_major") == "mn", kw.get("b_major") == "mn"
+    a = g.input("A", (batch, K, M) if a_mn else (batch, M, K), in_dtype, init=("normal", 1.0))
+    b = g.input("B", (batch, K, N) if b_mn else (batch, N, K), in_dtype, init=("normal", 1.0))
     r = g.input("R", (batch, M, N), out_dtype, init=("normal", 1.0)) if residual else None
     n_out = N // 2 if kw.get("epilogue") == "swiglu" else N
     g.gemm("C", a, b, M, N, K, r=r, batch=batch, sa=sa, sb=sb, sc=M * n_out if batch > 1 else 0, in_dtype=in_dtype,
@@ -93,6 +94,16 @@ def gemm_graph(M, N, K, *, batch=1, in_dtype="bf16", out_dtype="bf16", residual=
     dict(M=4096, N=128, K=4096, out_dtype="f32", residual=True, ksplit=4),  # config-5 P·V: 32 tiles x 4
     dict(M=640, N=200, K=2048, residual=True, ksplit=8),                    # ragged N, 10 tiles x 8
     dict(M=256, N=64, K=4096, out_dtype="f32", alpha=0.5, ksplit=8),       # BN=64, 4 tiles x 8
+    # MN-major operands (A stored [K, M], B stored [K, N]): 64x64 TMA boxes, MN-major UMMA descriptors
+    dict(M=256, N=128, K=256, b_major="mn"),                            # 1-CTA BN=128
+    dict(M=384, N=64, K=512, a_major="mn", b_major="mn", out_dtype="f32"),  # 1-CTA BN=64, both
+    dict(M=200, N=200, K=136, a_major="mn", residual=True),             # ragged, TMA OOB on both dims
+    dict(M=1024, N=1024, K=512, b_major="mn", residual=True, tile="narrow"),   # CTA pairs 256x256
+    dict(M=1024, N=1024, K=512, a_major="mn", b_major="mn", tile="wide"),      # CTA pairs 512x256
+    dict(M=512, N=128, K=512, batch=3, a_major="mn", b_major="mn", out_dtype="f32"),  # batched
+    dict(M=512, N=128, K=512, batch=2, a_major="mn", causal=2),         # causal K-block limit, MN A
+    dict(M=4096, N=64, K=4096, a_major="mn", b_major="mn", out_dtype="f32"),  # automatic split-K, MN
+    dict(M=8, N=256, K=128, a_major="mn", b_major="mn"),                # SIMT path (M < 128)
 ])
 def test_gemm_parity(shape):
     shape = dict(shape)
@@ -101,9 +112,15 @@ def test_gemm_parity(shape):
     inp = inputs_of(g, seed=11)
     if shape.get("causal") == 2:  # A must be lower triangular (causal probabilities)
         a_id = g.inputs()[0].id
-        B, M, K = g.tensors[a_id].shape
-        tri = (np.arange(K)[None, :] <= np.arange(M)[:, None])[None]
-        inp[a_id] = np.where(np.broadcast_to(tri, (B, M, K)).reshape(-1), inp[a_id], 0).astype(inp[a_id].dtype)
+        if shape.get("a_major") == "mn":  # stored [B, K, M]
+            B, K, M = g.tensors[a_id].shape
+            tri = (np.arange(K)[:, None] <= np.arange(M)[None, :])[None]
+            full = (B, K, M)
+        else:
+            B, M, K = g.tensors[a_id].shape
+            tri = (np.arange(K)[None, :] <= np.arange(M)[:, None])[None]
+            full = (B, M, K)
+        inp[a_id] = np.where(np.broadcast_to(tri, full).reshape(-1), inp[a_id], 0).astype(inp[a_id].dtype)
     _, got = run_gpu(g, mg, inp)
     want = oracle_outputs(g, mg, inp)
     (o,) = g.outputs()

@@ -19,10 +19,11 @@ ap.add_argument("--residency", default="host")
 ap.add_argument("--compare", action="store_true")
 ap.add_argument("--exec-cfg", default="{}", help="extra executor config keys (JSON)")
 ap.add_argument("--horizon", default="lazy")
+ap.add_argument("--no-mn-major", action="store_true", help="explicit transpose vertices in the backward")
 ap.add_argument("--dump", default="", help="write the memgraph + one traced step here (JSON)")
 a = ap.parse_args()
 t0 = time.time()
-g = W.llama_lora_step(W.LLAMA_7B, a.seq, layers=a.layers)
+g = W.llama_lora_step(W.LLAMA_7B, a.seq, layers=a.layers, mn_major=not a.no_mn_major)
 mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon=a.horizon)
 m = json.loads(mg)
 off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
@@ -54,7 +55,7 @@ stt = ex.stats()
 loss_id = next(o for o in g.outputs() if g.tensors[o].name == "loss")
 import struct
 loss = struct.unpack("<f", ex.get_output(loss_id, 4))[0]
-res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency}_{a.horizon}", "exec_cfg": a.exec_cfg, "memgraph_vertices": len(m["vertices"]),
+res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency}_{a.horizon}" + ("_transposes" if a.no_mn_major else ""), "exec_cfg": a.exec_cfg, "memgraph_vertices": len(m["vertices"]),
        "plan": st, "plan_s": round(plan_s, 2), "offload_gb": round(off / 1e9, 1), "step_s": [round(x, 4) for x in ts], "traced_step_makespan_s": round(traced, 4),
        "loss": loss, "tokens_per_s": round(a.seq / min(ts), 1), "flops": stt["flops"],
        "h2d_gb": round(stt["h2d_bytes"] / 1e9, 2), "d2h_gb": round(stt["d2h_bytes"] / 1e9, 2),
