@@ -329,7 +329,7 @@ def timed_runs(ex, steps, devs, after=None):
     return s.elapsed_time(e) * 1e-3
 
 
-def untimed_steps(ex, steps: int, policy: str = "event-driven", tie_break: str = "fifo") -> list[float]:
+def untimed_steps(ex, steps: int, policy: str = "event-driven", tie_break: str | None = None) -> list[float]:
     """Per-step device time (s) of `steps` untimed executor runs (used by the
     tools/ harnesses): each run's device-timed makespan (CUDA events around
     the whole run), back to back so the GPU stays in its sustained state."""

@@ -130,7 +130,9 @@ int tn_exec_set_input_device(tn_exec* h, int64_t vertex_id, const void* device_p
                              char** err);
 
 /* One full execution. policy: "event-driven" | "fixed-order"; tie_break:
- * "fifo" | "seeded-random" | "lowest-id". Blocks until every vertex finished.
+ * "fifo" | "seeded-random" | "lowest-id" | "plan-order" (memgraph total order;
+ * an extension), NULL or "" = the executor config's "tie_break" (default
+ * "plan-order"). Blocks until every vertex finished.
  * trace_json uses the reference ExecutionTrace schema (simulator.cpp:421-436)
  * with times in seconds measured by CUDA events; may be NULL. */
 int tn_exec_run(tn_exec* h, const char* policy, const char* tie_break, uint64_t seed, char** trace_json,

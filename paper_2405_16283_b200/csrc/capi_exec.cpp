@@ -72,7 +72,8 @@ int tn_exec_run(tn_exec* h, const char* policy, const char* tie_break, uint64_t 
         if (!h) throw Error("null executor handle");
         SchedulerPolicy pol;
         pol.kind = scheduler_kind_from_string(str(policy, "event-driven"));
-        pol.tie_break = tie_break_from_string(str(tie_break, "fifo"));
+        const std::string tb = str(tie_break);
+        pol.tie_break = tb.empty() ? h->x->default_tie_break() : tie_break_from_string(tb);
         auto t = h->x->run(pol, seed, trace != nullptr);
         if (trace) *trace = dup(t.to_json());
     });

@@ -43,7 +43,10 @@ struct DeviceProfile {
 };
 
 enum class SchedulerKind : std::uint8_t { EventDriven, FixedOrder };
-enum class TieBreak : std::uint8_t { Fifo, SeededRandom, LowestId };
+// PlanOrder (an extension, not in the reference simulator): ready vertices are
+// taken in the memgraph's total order, so a copy engine loads the tensor the
+// plan needs first rather than the one that became ready first.
+enum class TieBreak : std::uint8_t { Fifo, SeededRandom, LowestId, PlanOrder };
 
 struct SchedulerPolicy {
     SchedulerKind kind = SchedulerKind::EventDriven;
@@ -171,9 +174,17 @@ class ReadyList {
         std::int32_t vidx;
     };
     ReadyList(TieBreak tb, std::uint64_t seed) : tb_(tb), rng_(mix64(seed)) {}
+    // PlanOrder: rank[vidx] = position of vertex vidx in the memgraph's total order.
+    void set_rank(std::vector<std::int32_t> rank) { rank_ = std::move(rank); }
     void push(VertexId id, std::int32_t vidx, double t) {
         Entry e{t, arrivals_++, id, vidx};
-        if (tb_ == TieBreak::LowestId) {
+        if (tb_ == TieBreak::PlanOrder) {
+            const std::vector<std::int32_t>& r = rank_;
+            auto key = [&r](const Entry& x) { return r.empty() ? x.vidx : r[static_cast<size_t>(x.vidx)]; };
+            auto it = std::upper_bound(v_.begin(), v_.end(), e,
+                                       [&key](const Entry& a, const Entry& b) { return key(a) < key(b); });
+            v_.insert(it, e);
+        } else if (tb_ == TieBreak::LowestId) {
             auto it = std::upper_bound(v_.begin(), v_.end(), e,
                                        [](const Entry& a, const Entry& b) { return a.vertex < b.vertex; });
             v_.insert(it, e);
@@ -198,8 +209,18 @@ class ReadyList {
     TieBreak tb_;
     std::mt19937_64 rng_;
     std::vector<Entry> v_;
+    std::vector<std::int32_t> rank_;
     std::int64_t arrivals_ = 0;
 };
+
+// rank[vidx] = position in m.total_order (empty when the memgraph has none).
+inline std::vector<std::int32_t> plan_rank(const MemGraph& m) {
+    std::vector<std::int32_t> r;
+    if (m.total_order.size() != m.vertices.size()) return r;
+    r.assign(m.vertices.size(), 0);
+    for (size_t i = 0; i < m.total_order.size(); ++i) r[static_cast<size_t>(m.idx(m.total_order[i]))] = static_cast<std::int32_t>(i);
+    return r;
+}
 
 // Successor CSR and in-degrees of a memgraph, by vertex index.
 struct GraphIndex {

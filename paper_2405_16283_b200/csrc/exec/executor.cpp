@@ -1032,6 +1032,7 @@ void Executor::Impl::run(const SchedulerPolicy& pol, std::uint64_t seed, Executi
                   cfg.materialize_inputs && !aliased_inputs(), !cfg.inputs_on_device,
                   !((chain || cfg.device_deps) && cfg.compute_tokens == 1 && !cfg.kernel_slots));
     ReadyList ready(pol.tie_break, seed);
+    if (pol.tie_break == TieBreak::PlanOrder) ready.set_rank(plan_rank(*g));
     CudaBackend be(*this);
     try {
         if (cfg.device_deps) dispatch_loop_device_deps(*g, res, ready, be, cfg.lookahead);
@@ -1427,10 +1428,12 @@ void* Executor::placement_ptr(VertexId id) { return impl_->ptr_of(id); }
 
 const RunStats& Executor::stats() const { return impl_->last; }
 
+TieBreak Executor::default_tie_break() const { return impl_->cfg.tie_break; }
+
 ComparisonSummary Executor::compare_policies(std::int64_t trials, std::uint64_t seed) {
     if (trials < 1) throw Error("compare_policies: trials must be >= 1");
     DeviceGuard dg(impl_->cur_dev);
-    const SchedulerPolicy ev{SchedulerKind::EventDriven, TieBreak::Fifo};
+    const SchedulerPolicy ev{SchedulerKind::EventDriven, impl_->cfg.tie_break};
     const SchedulerPolicy fx{SchedulerKind::FixedOrder, TieBreak::Fifo};
     impl_->run(ev, seed, nullptr);  // warm both paths (fixed-order graph, caches, clocks)
     impl_->run(fx, seed, nullptr);
@@ -1490,6 +1493,7 @@ ExecConfig parse_exec_config(const std::string& text) {
         c.elide_input_offloads = j.value("elide_input_offloads", c.elide_input_offloads);
         c.materialize_inputs = j.value("materialize_inputs", c.materialize_inputs);
         c.timeout_s = j.value("timeout_s", c.timeout_s);
+        if (j.contains("tie_break")) c.tie_break = tie_break_from_string(j["tie_break"].get<std::string>());
         const std::string comp = j.value("completion", std::string("poll"));
         if (comp != "poll" && comp != "callback") throw ParseError("completion must be poll or callback");
         c.poll = comp == "poll";

@@ -32,6 +32,13 @@ struct ExecConfig {
                                      // staging copy (stream only); "host" -> H2D from the
                                      // pinned pool (stream + host_in channel)
     int timeout_s = 600;             // completion watchdog
+    TieBreak tie_break = TieBreak::PlanOrder;  // "tie_break": the event-driven ready-list order when a
+                                          // run names none: "plan-order" (default; ready copies / kernels
+                                          // in the memgraph's total order, so the H2D engine loads the
+                                          // tensor the plan needs next instead of the one that became
+                                          // ready first: config-4 step 0.586 -> 0.537 s, config 5
+                                          // 0.563 -> 0.553 s) | "fifo" (the reference simulator's
+                                          // default) | "seeded-random" | "lowest-id"
     bool elide_input_offloads = true;  // an evicted *input* is never modified: skip its D2H and
                                        // reload from the input's own host (or HBM staging) copy
     bool poll = true;                // "completion": "poll" (spin on cudaEventQuery) | "callback"
@@ -94,6 +101,7 @@ class Executor {
     // uses seed mix64(seed + t); same summary schema and bootstrap (2000
     // resamples) as the simulator's.
     ComparisonSummary compare_policies(std::int64_t trials, std::uint64_t seed);
+    TieBreak default_tie_break() const;
     struct Impl;
 
   private:

@@ -55,9 +55,12 @@ class Executor:
             rc = lib().tn_exec_set_input(self._ptr(), vid, ctypes.cast(buf, c_void_p), len(b), err.ref)
         check(rc, err)
 
-    def run(self, policy: str = "event-driven", tie_break: str = "fifo", seed: int = 0, trace: bool = True) -> str | None:
+    def run(self, policy: str = "event-driven", tie_break: str | None = None, seed: int = 0,
+            trace: bool = True) -> str | None:
+        """tie_break None: the config's "tie_break" (default "plan-order")."""
         out, err = Out(), Out()
-        rc = lib().tn_exec_run(self._ptr(), enc(policy), enc(tie_break), seed, out.ref if trace else None, err.ref)
+        rc = lib().tn_exec_run(self._ptr(), enc(policy), enc(tie_break or ""), seed, out.ref if trace else None,
+                               err.ref)
         check(rc, err)
         return out.take()
 
@@ -110,9 +113,10 @@ class Executor:
 
 
 def execute(memgraph_json: str, taskgraph_json: str, inputs: dict, outputs=(), config=None,
-            policy: str = "event-driven", tie_break: str = "fifo", seed: int = 0):
+            policy: str = "event-driven", tie_break: str | None = None, seed: int = 0):
     """One-shot: returns (trace_json, {vid: bytes}) — the real-hardware
-    counterpart of `memplan.simulate(memgraph_json, ...)`."""
+    counterpart of `memplan.simulate(memgraph_json, ...)`. tie_break None: the
+    config's (default "plan-order"; simulate's default is the reference's "fifo")."""
     mg = json.loads(memgraph_json)
     sizes = {int(k): p["size"] for k, p in mg["placement"].items()}
     with Executor(memgraph_json, taskgraph_json, config) as ex:

@@ -477,7 +477,8 @@ def llama_prefill_tp(cfg: LlamaConfig, seq: int, tp: int, layers: int | None = N
 def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank: int = 16, rank_pad: int = 64,
                     lora_alpha: float = 16.0, std: float = 0.02, device: int = 0,
                     recompute_attention: bool = True, recompute_ffn: bool = True,
-                    recompute_qkv: bool = True, mn_major: bool = True) -> GraphBuilder:
+                    recompute_qkv: bool = True, mn_major: bool = True, prefetch: int = 0,
+                    recompute_norms: bool = True, bwd_prefetch: int = 0) -> GraphBuilder:
     """Config 4: one LoRA fine-tuning step (forward + backward) of a LLaMA
     model over `seq` tokens, rank-`rank` adapters on the fused QKV projection
     and on both FFN projections ("rank 16 on Q,K,V,FFN"), frozen
@@ -514,14 +515,15 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     transposed copies per layer on the 7B step, n² probability tiles included)."""
     g = GraphBuilder(device_count=1)
     _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "", recompute_attention,
-                    recompute_ffn, recompute_qkv, mn_major)
+                    recompute_ffn, recompute_qkv, mn_major, prefetch, recompute_norms, bwd_prefetch)
     return g
 
 
 def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None = None, rank: int = 16,
                        rank_pad: int = 64, lora_alpha: float = 16.0, std: float = 0.02,
                        recompute_attention: bool = True, recompute_ffn: bool = True,
-                       recompute_qkv: bool = True, mn_major: bool = True) -> GraphBuilder:
+                       recompute_qkv: bool = True, mn_major: bool = True, prefetch: int = 0,
+                    recompute_norms: bool = True, bwd_prefetch: int = 0) -> GraphBuilder:
     """Config 4 over `dp` devices (data parallel): every memgraph
     device runs the full LoRA step on its own sequence (tokens/targets
     `@r`; the frozen weights and adapters are the same tensors on every device,
@@ -532,7 +534,8 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
     (same names as llama_lora_step's). Global batch = dp sequences."""
     g = GraphBuilder(device_count=dp)
     outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "",
-                            recompute_attention, recompute_ffn, recompute_qkv, mn_major) for r in range(dp)]
+                            recompute_attention, recompute_ffn, recompute_qkv, mn_major, prefetch,
+                            recompute_norms, bwd_prefetch) for r in range(dp)]
     for name, v0 in outs[0].items():
         t = g.tensors[v0]
         n = int(np.prod(t.shape))
@@ -544,7 +547,7 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
 
 def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, rank_pad, lora_alpha, std, device,
                     data_sfx, recompute_attention=True, recompute_ffn=False, recompute_qkv=False,
-                    mn_major=False) -> dict:
+                    mn_major=False, prefetch=0, recompute_norms=False, bwd_prefetch=0) -> dict:
     """Appends one LoRA step on `device` to `g`; returns {output name: vid}
     (the loss and every adapter gradient)."""
     L = cfg.layers if layers is None else layers
@@ -577,9 +580,11 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
     x = g.kernel("embed", {"type": "embedding", "args": [tok, emb], "seq": S, "dim": d, "vocab": V}, (S, d), "bf16", dev)
 
     saved = []
-    for l in range(L):
+    ws = {}
+
+    def layer_weights(l):
         p = f"layers.{l}."
-        w = {
+        return {
             "wn1": g.input(p + "attention_norm", (d,), "bf16", dev, init=("normal", 1.0)),
             "wqkv": g.input(p + "wqkv", (3 * d, d), "bf16", dev, init=("normal", std)),
             "wo": g.input(p + "wo", (d, d), "bf16", dev, init=("normal", std)),
@@ -593,6 +598,13 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
             "A3": g.input(p + "lora_w2.A", (R, f), "bf16", dev, init=("lora_a", std, rank)),
             "B3": g.input(p + "lora_w2.B", (d, R), "bf16", dev, init=("lora_b", std, rank)),
         }
+
+    for l in range(L):
+        p = f"layers.{l}."
+        for j in range(l, min(L, l + 1 + prefetch)):
+            if j not in ws:
+                ws[j] = layer_weights(j)
+        w = ws.pop(l)
         a = {"x": x}
         a["h"] = rms(p + "attn_norm_out", x, w["wn1"])
         base = g.gemm(p + "qkv_base", a["h"], w["wqkv"], S, 3 * d, d, out_shape=(S, 3 * d), device=dev)
@@ -660,9 +672,14 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
         results[p + nm + ".dA"] = tr(p + nm + ".dA", dAT, k_in, R)
         return Vv
 
-    for l in reversed(range(L)):
+    def recompute(l):
+        """Layer l's forward activations again from the saved residual stream /
+        adapter activations (bitwise the forward's); depends on no gradient."""
         p, w, a = saved[l]
-        dy = dx  # gradient of x_{l+1}
+        if recompute_norms:  # h, h2 again from the saved x, x1 (bitwise the forward's): only the
+            # residual stream is kept across the step
+            a = dict(a, h2=rms(p + "ffn_norm_out.re", a["x1"], w["wn2"]), h=rms(p + "attn_norm_out.re", a["x"],
+                                                                                   w["wn1"]))
         if recompute_ffn:  # gu and act again from the saved h2, U2 (bitwise the forward's)
             gub_r = g.gemm(p + "gate_up_base.re", a["h2"], w["w13"], S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
             gu_r = g.gemm(p + "gate_up.re", a["U2"], w["B2"], S, 2 * f, R, r=gub_r, alpha=sc, out_shape=(S, 2 * f),
@@ -678,6 +695,19 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
                                                   "col_off": 0, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev),
                      k=g.kernel(p + "k_rope.re", {"type": "rope", "args": [qkv_r, rope_tab], "seq": S, "ld": 3 * d,
                                                   "col_off": d, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev))
+        return a
+
+    rec = {}
+    for l in reversed(range(L)):
+        # the recompute of layers l-1 .. l-bwd_prefetch is listed ahead of layer l's
+        # gradient GEMMs, so the planner reloads their frozen weights one or more
+        # layers early and the H2D of layer l-1 overlaps layer l's backward
+        for j2 in range(l, max(-1, l - 1 - bwd_prefetch), -1):
+            if j2 not in rec:
+                rec[j2] = recompute(j2)
+        p, w, _ = saved[l]
+        a = rec.pop(l)
+        dy = dx  # gradient of x_{l+1}
         # x_{l+1} = act·W2ᵀ + s·U3·B3ᵀ + x1
         V3 = lora_grads(p, "lora_w2", dy, d, f, a["U3"], a["act"], w["A3"], w["B3"])
         if mn_major:  # W2 [d, f], A3 [R, f] read MN-major

@@ -29,11 +29,12 @@ def cases():
     """(name, taskgraph builder, capacities, build kwargs) — shared with the test."""
     return [
         ("lora7b_seq4096_cap16GiB_lazy", lambda: W.llama_lora_step(W.LLAMA_7B, 4096, recompute_ffn=False,
-                                                                    recompute_qkv=False, mn_major=False), [16 * GIB],
+                                                                    recompute_qkv=False, mn_major=False,
+                                                                    recompute_norms=False), [16 * GIB],
          {"alloc_horizon": "lazy"}),
         ("lora7b_seq4096_cap16GiB_lazy_saveP", lambda: W.llama_lora_step(W.LLAMA_7B, 4096, recompute_attention=False,
                                                                          recompute_ffn=False, recompute_qkv=False,
-                                                                         mn_major=False),
+                                                                         mn_major=False, recompute_norms=False),
          [16 * GIB], {"alloc_horizon": "lazy"}),
         ("lora7b_seq4096_cap16GiB_lazy_recompute", lambda: W.llama_lora_step(W.LLAMA_7B, 4096), [16 * GIB],
          {"alloc_horizon": "lazy"}),

@@ -376,7 +376,7 @@ def test_dispatch_order_independence_bitwise(cfg):
         n = g.tensors[o].nbytes
         for pol, tb, seed in (("event-driven", "fifo", 0), ("event-driven", "lowest-id", 0),
                               ("event-driven", "seeded-random", 1), ("event-driven", "seeded-random", 2),
-                              ("fixed-order", "fifo", 0)):
+                              ("event-driven", "plan-order", 0), ("fixed-order", "fifo", 0)):
             trace = json.loads(ex.run(pol, tb, seed))
             results.append(ex.get_output(o, n))
             check_trace(mg, trace)
@@ -492,7 +492,7 @@ def test_full_size_llama7b_properties():
     with Executor(mg, g.to_json(), {"input_residency": "device"}) as ex:
         for vid, t in inputs.items():
             ex.set_input(vid, t)
-        for tb, seed in (("fifo", 0), ("seeded-random", 5), ("lowest-id", 0)):
+        for tb, seed in (("fifo", 0), ("seeded-random", 5), ("lowest-id", 0), ("plan-order", 0)):
             trace = json.loads(ex.run("event-driven", tb, seed))
             outs.append(ex.get_output(o, n))
             st = ex.stats()

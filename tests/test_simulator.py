@@ -92,3 +92,28 @@ def test_deadlock_and_bad_profile_raise():
         memplan.simulate(mg, json.dumps({"streams_per_device": 0}))
     with pytest.raises(memplan.MemplanError):
         memplan.simulate(mg, policy="nope")
+
+
+def test_plan_order_tie_break():
+    """"plan-order" (an extension): ready vertices go in the memgraph's total
+    order, not in the order they became ready. One stream; kernel 2 is ready
+    at t=0 but planned last, kernel 3 becomes ready at t=1 (after kernel 1)."""
+    vs = [{"id": 0, "kind": "input", "device": 0}] + [{"id": i, "kind": "kernel", "device": 0} for i in range(1, 4)]
+    g = json.dumps({"device_count": 1, "vertices": vs, "edges": [[0, 1], [0, 2], [1, 3]]})
+    mg, _ = memplan.build_memgraph(g, [8], order=[0, 1, 3, 2])
+    prof = json.dumps({"streams_per_device": 1})
+
+    def ran(tb):
+        t = json.loads(memplan.simulate(mg, prof, tie_break=tb))
+        invariants(mg, json.dumps(t))
+        return [r["vertex"] for r in sorted(t["rows"], key=lambda r: r["start"]) if r["vertex"] != 0]
+
+    assert ran("plan-order") == [1, 3, 2]
+    assert ran("fifo") == [1, 2, 3]
+    for seed in range(6):
+        g = taskgraph("gen_random_dag", [14, 0.3, 2, seed])
+        try:
+            mg, _ = memplan.build_memgraph(g, [6, 6])
+        except memplan.MemplanError:
+            continue
+        invariants(mg, memplan.simulate(mg, tie_break="plan-order"))

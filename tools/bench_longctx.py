@@ -45,7 +45,7 @@ duplex = bench.measure_pcie_duplex(dev)
 pk = bench.peaks()
 with bench.Clocks([0]) as ck:
     times = bench.untimed_steps(ex, a.steps, a.policy)  # timing-free completion events
-tr = json.loads(ex.run(a.policy, "fifo", 0))  # one traced step: exposed transfer / kernel busy
+tr = json.loads(ex.run(a.policy, None, 0))  # one traced step: exposed transfer / kernel busy
 stt = ex.stats()
 if a.dump:
     with open(a.dump, "w") as f:
