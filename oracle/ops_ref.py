@@ -231,18 +231,59 @@ def op_attention(op, args, out):
     vt = load(av, "bf16", n, op.get("v_off", 0)).reshape(H, hd, S)
     keep = (np.arange(S)[None, :] <= np.arange(S)[:, None]) if causal else None
     O = np.empty((S, H, hd), dtype=np.float32)
+    lse = np.empty((H, S), dtype=np.float32)
 
     def one(h):
         s = (q[h] @ k[h].T) * np.float32(scale)
         if keep is not None:
             np.copyto(s, np.float32(-np.inf), where=~keep)
-        s -= s.max(axis=1, keepdims=True)
+        mx = s.max(axis=1, keepdims=True)
+        s -= mx
         np.exp(s, out=s)
-        s /= s.sum(axis=1, keepdims=True, dtype=np.float32)
+        tot = s.sum(axis=1, keepdims=True, dtype=np.float32)
+        lse[h] = (mx + np.log(tot))[:, 0]
+        s /= tot
         O[:, h, :] = s @ vt[h].T
 
     list(_pool().map(one, range(H)))
     scatter(out, "bf16", 0, 0, ldo, O.reshape(1, S, H * hd))
+    if op.get("lse", 0):  # natural-log logsumexp of each scaled score row, after the [S, ldo] output
+        store(out, "f32", lse, S * ldo // 2)
+
+
+def op_attention_bwd(op, args, out):
+    """Attention gradient (attention_bwd.cu): P = exp(scale q k^T - lse) from the
+    forward's lse, D = rowsum(dO * O), dS = P * (dP - D), dP = dO v^T;
+    out = [dq | dk | dv] rows of 3*H*hd (dq = scale dS k, dk = scale dS^T q,
+    dv = P^T dO), then D (f32 [H, S]). fp32 throughout (the kernel rounds P and
+    dS to bf16 for its MMAs)."""
+    H, S, hd, scale, causal = op["heads"], op["seq"], op["hd"], op.get("scale", 1.0), op.get("causal", 1)
+    w = H * hd
+    ldo, vld, dld = op.get("ldo") or w, op.get("v_ld") or w, op.get("do_ld") or w
+    n = H * S * hd
+    q = load(args[0], "bf16", n, op.get("q_off", 0)).reshape(H, S, hd)
+    k = load(args[1], "bf16", n, op.get("k_off", 0)).reshape(H, S, hd)
+    v = strided(args[2], "bf16", op.get("v_off", 0), 1, 0, S, vld, w)[0].reshape(S, H, hd)
+    o = strided(args[3], "bf16", 0, 1, 0, S, ldo, w)[0].reshape(S, H, hd)
+    lse = load(args[3], "f32", H * S, S * ldo // 2).reshape(H, S)
+    do = strided(args[4], "bf16", 0, 1, 0, S, dld, w)[0].reshape(S, H, hd)
+    keep = (np.arange(S)[None, :] <= np.arange(S)[:, None]) if causal else np.ones((S, S), bool)
+    G = np.empty((S, 3, H, hd), dtype=np.float32)
+    D = np.empty((H, S), dtype=np.float32)
+
+    def one(h):
+        s = (q[h] @ k[h].T) * np.float32(scale)
+        P = np.where(keep, np.exp(s - lse[h][:, None]), np.float32(0.0)).astype(np.float32)
+        dOh = do[:, h, :]
+        D[h] = np.sum(dOh * o[:, h, :], axis=1, dtype=np.float32)
+        dS = P * (dOh @ v[:, h, :].T - D[h][:, None])
+        G[:, 0, h, :] = np.float32(scale) * (dS @ k[h])
+        G[:, 1, h, :] = np.float32(scale) * (dS.T @ q[h])
+        G[:, 2, h, :] = P.T @ dOh
+
+    list(_pool().map(one, range(H)))
+    store(out, "bf16", G.reshape(-1))
+    store(out, "f32", D, S * 3 * w // 2)
 
 
 def _valid_mask(rows, cols, causal):
@@ -413,6 +454,7 @@ OPS = {
     "embedding": op_embedding,
     "cast": op_cast,
     "attention": op_attention,
+    "attention_bwd": op_attention_bwd,
     "rowstats": op_rowstats,
     "stats_combine": op_stats_combine,
     "softmax_apply": op_softmax_apply,

@@ -115,6 +115,7 @@ struct Executor::Impl {
         std::vector<const char*> argp;  // resolved argument pointers
         std::unique_ptr<k::GemmPlan> gemm;
         std::unique_ptr<k::AttnPlan> attn;
+        std::unique_ptr<k::AttnBwdPlan> attn_bwd;
         void* scratch = nullptr;  // per-vertex device scratch (xent_loss row losses), outside the arena
     };
     std::vector<Instr> prog;
@@ -677,6 +678,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             fits((op.k_off + sec) * 2, arg_bytes[ik], "k");
             fits((op.v_off + sec) * 2, arg_bytes[iv], "vt");
             fits(((op.seq - 1) * ldo + op.heads * op.hd) * 2, out_bytes, "out");
+            if (op.lse) fits(op.seq * ldo * 2 + op.heads * op.seq * 4, out_bytes, "out (o + lse)");
             k::AttnArgs aa;
             aa.q = in.argp[iq] + op.q_off * 2;
             aa.k = in.argp[ik] + op.k_off * 2;
@@ -688,8 +690,46 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             aa.ldo = ldo;
             aa.scale = static_cast<float>(op.scale);
             aa.causal = op.causal;
+            if (op.lse) aa.lse = reinterpret_cast<float*>(in.dst + op.seq * ldo * 2);
             in.attn = std::make_unique<k::AttnPlan>();
             TN_CUDA(k::attention_prepare(aa, in.attn.get()));
+            break;
+        }
+        case OpType::AttentionBwd: {
+            need_args(5, 5);
+            if (op.hd != 128 || op.seq <= 0 || op.seq % 128 != 0 || op.heads <= 0)
+                throw Error("kernel " + std::to_string(v.id) + " (attention_bwd): needs hd 128 and seq % 128 == 0");
+            const std::int64_t sec = op.heads * op.seq * op.hd, w = op.heads * op.hd;
+            const std::int64_t ldo = op.ldo ? op.ldo : w, vld = op.v_ld ? op.v_ld : w, dld = op.do_ld ? op.do_ld : w;
+            fits((op.q_off + sec) * 2, arg_bytes[0], "q");
+            fits((op.k_off + sec) * 2, arg_bytes[1], "k");
+            fits((op.v_off + (op.seq - 1) * vld + w) * 2, arg_bytes[2], "v");
+            fits(op.seq * ldo * 2 + op.heads * op.seq * 4, arg_bytes[3], "o_lse");
+            fits(((op.seq - 1) * dld + w) * 2, arg_bytes[4], "dO");
+            fits(op.seq * 3 * w * 2 + op.heads * op.seq * 4, out_bytes, "out (dq|dk|dv + D)");
+            k::AttnBwdArgs ab;
+            ab.q = in.argp[0] + op.q_off * 2;
+            ab.k = in.argp[1] + op.k_off * 2;
+            ab.v = in.argp[2] + op.v_off * 2;
+            ab.ldv = vld;
+            ab.o = in.argp[3];
+            ab.ldo = ldo;
+            ab.lse = reinterpret_cast<const float*>(in.argp[3] + op.seq * ldo * 2);
+            ab.dout = in.argp[4];
+            ab.lddo = dld;
+            ab.dq = in.dst;
+            ab.dk = in.dst + w * 2;
+            ab.dv = in.dst + 2 * w * 2;
+            ab.ldg = 3 * w;
+            ab.D = reinterpret_cast<float*>(in.dst + op.seq * 3 * w * 2);
+            ab.heads = static_cast<int>(op.heads);
+            ab.seq = static_cast<int>(op.seq);
+            ab.hd = static_cast<int>(op.hd);
+            ab.scale = static_cast<float>(op.scale);
+            ab.causal = op.causal;
+            in.attn_bwd = std::make_unique<k::AttnBwdPlan>();
+            if (k::attention_bwd_prepare(ab, in.attn_bwd.get()) != cudaSuccess)
+                throw Error("kernel " + std::to_string(v.id) + " (attention_bwd): operands not 16-byte aligned");
             break;
         }
     }
@@ -875,6 +915,11 @@ void Executor::Impl::issue(std::int32_t vidx, cudaStream_t s, std::int32_t strea
                 case OpType::Attention:
                     TN_CUDA(k::attention_launch(*in.attn, s));
                     last.flops += k::attention_flops(in.attn->args);
+                    break;
+                case OpType::AttentionBwd:
+                    TN_CUDA(k::attention_bwd_launch(*in.attn_bwd, s));
+                    last.flops += k::attention_bwd_flops(in.attn_bwd->args);
+                    last.kernel_launches++;  // attn_bwd_prep + attention_bwd_kernel
                     break;
             }
             last.kernel_launches++;

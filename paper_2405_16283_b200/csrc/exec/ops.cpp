@@ -29,6 +29,7 @@ const char* to_string(OpType t) {
         case OpType::SoftmaxBwd: return "softmax_bwd";
         case OpType::XentGrad: return "xent_grad";
         case OpType::XentLoss: return "xent_loss";
+        case OpType::AttentionBwd: return "attention_bwd";
     }
     return "?";
 }
@@ -63,6 +64,7 @@ OpType type_of(const std::string& s) {
     if (s == "softmax_bwd") return OpType::SoftmaxBwd;
     if (s == "xent_grad") return OpType::XentGrad;
     if (s == "xent_loss") return OpType::XentLoss;
+    if (s == "attention_bwd") return OpType::AttentionBwd;
     throw ParseError("unknown op type '" + s + "'");
 }
 
@@ -115,6 +117,9 @@ std::unordered_map<VertexId, OpDesc> parse_ops(const std::string& text) {
             d.q_off = I("q_off", 0);
             d.k_off = I("k_off", 0);
             d.v_off = I("v_off", 0);
+            d.lse = static_cast<int>(I("lse", 0));
+            d.v_ld = I("v_ld", 0);
+            d.do_ld = I("do_ld", 0);
             d.causal = static_cast<int>(I("causal", 0));
             d.norm_out = static_cast<int>(I("norm_out", 0));
             d.rs_arg = static_cast<int>(I("rs_arg", -1));

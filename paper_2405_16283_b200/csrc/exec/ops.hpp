@@ -32,7 +32,13 @@
 //   {"type": "embedding", "args": [tokens, table], "seq", "dim", "vocab"}
 //   {"type": "cast", "args": [x], "count", "in_dtype", "out_dtype"}
 //   {"type": "attention", "args": [q, k, vt], "heads", "seq", "hd", "ldo", "scale",
-//    "causal"}   q,k [H,seq,hd], vt [H,hd,seq] -> out [seq, ldo] (head h at col h*hd)
+//    "causal", "lse": 0|1}   q,k [H,seq,hd], vt [H,hd,seq] -> out [seq, ldo] (head h at col h*hd);
+//    lse 1: followed (byte offset seq*ldo*2) by the f32 [H, seq] natural-log logsumexp of each
+//    scaled score row
+//   {"type": "attention_bwd", "args": [q, k, v, o_lse, dO], "heads", "seq", "hd", "scale", "causal",
+//    "q_off", "k_off", "v_off", "v_ld", "ldo", "do_ld"}   q,k [H,seq,hd]; v [seq, v_ld] from v_off
+//    (head h at col h*hd); o_lse = an attention output with lse 1 (pitch ldo); dO [seq, do_ld] ->
+//    out [seq, 3*H*hd] = [dq | dk | dv] (bf16), then f32 [H, seq] D = rowsum(dO*O) (scratch)
 //   {"type": "rowstats", "args": [S], "rows", "cols", "causal"}      bf16 S -> f32 (m,l) rows
 //   {"type": "stats_combine", "args": [st0, st1, ...], "rows"}        fold (m,l) in arg order
 //   {"type": "softmax_apply", "args": [S, st], "rows", "cols", "causal"}  P = exp(S-m)/l, bf16
@@ -53,7 +59,7 @@ namespace tn {
 enum class OpType : std::uint8_t {
     Gemm, RmsNorm, Softmax, Rope, TransposeHeads, SiluMul, Sum, Embedding, Cast, Attention,
     RowStats, StatsCombine, SoftmaxApply, Concat,
-    Transpose, RmsNormBwd, SwigluBwd, SoftmaxBwd, XentGrad, XentLoss
+    Transpose, RmsNormBwd, SwigluBwd, SoftmaxBwd, XentGrad, XentLoss, AttentionBwd
 };
 
 struct OpDesc {
@@ -77,6 +83,8 @@ struct OpDesc {
     double alpha = 1.0, eps = 1e-5, scale = 1.0;
     std::vector<std::int64_t> offs;  // sum: per-argument element offsets
     std::int64_t q_off = 0, k_off = 0, v_off = 0;  // attention on a packed qkv tensor
+    int lse = 0;                                   // attention: also write the row logsumexp
+    std::int64_t v_ld = 0, do_ld = 0;              // attention_bwd: v / dO row pitch
     // Fused RMSNorm. Producer (gemm with residual, embedding): "norm_out": 1
     // plus a trailing gamma argument; the output holds [x | h = x*gamma | P],
     // P[m][c] = sum of x[m, 32c..32c+31]^2 (fp32, [rows, dim/32]). Consumer

@@ -66,6 +66,7 @@ constexpr int kQ = 32768, kKst = 16384, kV = 16384;
 
 struct AttnParams {
     __nv_bfloat16* O;
+    float* lse;  // optional [heads][seq]: (m + log2 l) * ln 2 of each row
     int heads, seq, nblk;
     std::int64_t ldo;
     float scale_log2;
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(o_done, (nkv - 1) & 1);
         tc_fence_after();
         const float inv = 1.0f / l;
+        if (p.lse) p.lse[static_cast<std::int64_t>(h) * p.seq + qrow] = (m + __log2f(l)) * 0.6931471805599453f;
         __nv_bfloat16* orow = p.O + static_cast<std::int64_t>(qrow) * p.ldo + static_cast<std::int64_t>(h) * kHd;
 #pragma unroll 1
         for (int c = 0; c < kHd; c += 32) {
@@ -629,6 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             mbar_wait(o_full + 8 * t, itc & 1);
             tc_fence_after();
             const float inv = 1.0f / l;
+            if (p.lse) p.lse[static_cast<std::int64_t>(it.h) * p.seq + qrow] = (m + __log2f(l)) * 0.6931471805599453f;
             __nv_bfloat16* orow =
                 p.O + static_cast<std::int64_t>(qrow) * p.ldo + static_cast<std::int64_t>(it.h) * kHd;
 #pragma unroll 1
@@ -665,7 +668,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
 // softmax over all keys in order. Slow; only for shapes the fused path rejects.
 __global__ void attention_simt(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
                                const __nv_bfloat16* __restrict__ vt, __nv_bfloat16* __restrict__ O, int heads, int seq,
-                               int hd, std::int64_t ldo, float scale_log2, int causal) {
+                               int hd, std::int64_t ldo, float scale_log2, int causal, float* lse) {
     const std::int64_t w = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
     const int lane = threadIdx.x % 32;
     if (w >= static_cast<std::int64_t>(heads) * seq) return;
@@ -689,6 +692,7 @@ __global__ void attention_simt(const __nv_bfloat16* __restrict__ q, const __nv_b
         }
         m = mx;
     }
+    if (lse && lane == 0) lse[static_cast<std::int64_t>(h) * seq + i] = (m + log2f(l)) * 0.6931471805599453f;
     for (int c = 0; c < 8; ++c) {
         const int col = lane + 32 * c;
         if (col < hd) O[static_cast<std::int64_t>(i) * ldo + static_cast<std::int64_t>(h) * hd + col] = __float2bfloat16_rn(acc[c] / l);
@@ -751,11 +755,12 @@ cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s) {
         attention_simt<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(
             static_cast<const __nv_bfloat16*>(a.q), static_cast<const __nv_bfloat16*>(a.k),
             static_cast<const __nv_bfloat16*>(a.vt), static_cast<__nv_bfloat16*>(a.out), a.heads, a.seq, a.hd, a.ldo,
-            sl2, a.causal);
+            sl2, a.causal, a.lse);
         return cudaGetLastError();
     }
     AttnParams p;
     p.O = static_cast<__nv_bfloat16*>(a.out);
+    p.lse = a.lse;
     p.heads = a.heads;
     p.seq = a.seq;
     p.nblk = a.seq / kB;

@@ -120,6 +120,7 @@ struct AttnArgs {
     std::int64_t ldo = 0;
     float scale = 1.0f;
     int causal = 1;
+    float* lse = nullptr;  // optional [heads][seq]: natural-log logsumexp of each scaled score row
 };
 struct alignas(64) AttnPlan {
     CUtensorMap tq, tk, tv, tv2;
@@ -128,6 +129,30 @@ struct alignas(64) AttnPlan {
     int grid = 0;  // path 2: CTAs of the persistent launch
 };
 cudaError_t attention_prepare(const AttnArgs& a, AttnPlan* plan);
+
+// Fused attention backward (attention_bwd.cu): q, k [heads][seq][hd]; v, o, dO
+// row-major [seq][ld] with head h at columns h*hd (v may point into a packed
+// qkv); lse [heads][seq] (natural log, written by the forward with
+// AttnArgs::lse); D [heads][seq] fp32 scratch. Writes dq, dk, dv [seq][ldg]
+// (head h at columns h*hd). hd 128, seq % 128 == 0.
+struct AttnBwdArgs {
+    const void *q = nullptr, *k = nullptr, *v = nullptr, *o = nullptr, *dout = nullptr;
+    std::int64_t ldv = 0, ldo = 0, lddo = 0;
+    const float* lse = nullptr;
+    float* D = nullptr;
+    void *dq = nullptr, *dk = nullptr, *dv = nullptr;
+    std::int64_t ldg = 0;
+    int heads = 0, seq = 0, hd = 0;
+    float scale = 1.0f;
+    int causal = 1;
+};
+struct alignas(64) AttnBwdPlan {
+    CUtensorMap tq, tk, tv, tdo;
+    AttnBwdArgs args;
+};
+cudaError_t attention_bwd_prepare(const AttnBwdArgs& a, AttnBwdPlan* plan);
+cudaError_t attention_bwd_launch(const AttnBwdPlan& plan, cudaStream_t s);
+double attention_bwd_flops(const AttnBwdArgs& a);
 cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s);
 double attention_flops(const AttnArgs& a);
 

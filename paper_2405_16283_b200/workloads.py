@@ -478,7 +478,8 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
                     lora_alpha: float = 16.0, std: float = 0.02, device: int = 0,
                     recompute_attention: bool = True, recompute_ffn: bool = True,
                     recompute_qkv: bool = True, mn_major: bool = True, prefetch: int = 0,
-                    recompute_norms: bool = True, bwd_prefetch: int = 0) -> GraphBuilder:
+                    recompute_norms: bool = True, bwd_prefetch: int = 0,
+                    fused_attention: bool = False) -> GraphBuilder:
     """Config 4: one LoRA fine-tuning step (forward + backward) of a LLaMA
     model over `seq` tokens, rank-`rank` adapters on the fused QKV projection
     and on both FFN projections ("rank 16 on Q,K,V,FFN"), frozen
@@ -515,7 +516,8 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     transposed copies per layer on the 7B step, n² probability tiles included)."""
     g = GraphBuilder(device_count=1)
     _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "", recompute_attention,
-                    recompute_ffn, recompute_qkv, mn_major, prefetch, recompute_norms, bwd_prefetch)
+                    recompute_ffn, recompute_qkv, mn_major, prefetch, recompute_norms, bwd_prefetch,
+                    fused_attention)
     return g
 
 
@@ -523,7 +525,8 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
                        rank_pad: int = 64, lora_alpha: float = 16.0, std: float = 0.02,
                        recompute_attention: bool = True, recompute_ffn: bool = True,
                        recompute_qkv: bool = True, mn_major: bool = True, prefetch: int = 0,
-                    recompute_norms: bool = True, bwd_prefetch: int = 0) -> GraphBuilder:
+                    recompute_norms: bool = True, bwd_prefetch: int = 0,
+                    fused_attention: bool = False) -> GraphBuilder:
     """Config 4 over `dp` devices (data parallel): every memgraph
     device runs the full LoRA step on its own sequence (tokens/targets
     `@r`; the frozen weights and adapters are the same tensors on every device,
@@ -535,7 +538,7 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
     g = GraphBuilder(device_count=dp)
     outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "",
                             recompute_attention, recompute_ffn, recompute_qkv, mn_major, prefetch,
-                            recompute_norms, bwd_prefetch) for r in range(dp)]
+                            recompute_norms, bwd_prefetch, fused_attention) for r in range(dp)]
     for name, v0 in outs[0].items():
         t = g.tensors[v0]
         n = int(np.prod(t.shape))
@@ -547,7 +550,8 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
 
 def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, rank_pad, lora_alpha, std, device,
                     data_sfx, recompute_attention=True, recompute_ffn=False, recompute_qkv=False,
-                    mn_major=False, prefetch=0, recompute_norms=False, bwd_prefetch=0) -> dict:
+                    mn_major=False, prefetch=0, recompute_norms=False, bwd_prefetch=0,
+                    fused_attention=False) -> dict:
     """Appends one LoRA step on `device` to `g`; returns {output name: vid}
     (the loss and every adapter gradient)."""
     L = cfg.layers if layers is None else layers
@@ -556,6 +560,9 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
     scale = 1.0 / math.sqrt(hd)
     dev = device
     results = {}
+    if fused_attention and not (mn_major and hd == 128 and S % 128 == 0):
+        raise ValueError("fused_attention needs mn_major, hd 128 and seq % 128 == 0")
+    attn_flops = 2.0 * S * S * hd * H * (1 + 1 / S)  # causal: QKᵀ and PV, half each
 
     def tr(name, x, rows, cols, batch=1, dt="bf16"):
         return g.kernel(name, {"type": "transpose", "args": [x], "batch": batch, "rows": rows, "cols": cols,
@@ -616,12 +623,18 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
                                          "col_off": d, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev)
         vt = g.kernel(p + "v_t", {"type": "transpose_heads", "args": [a["qkv"]], "seq": S, "ld": 3 * d,
                                   "col_off": 2 * d, "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
-        scr = g.gemm(p + "scores", a["q"], a["k"], S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S,
-                     out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
-        a["P"] = g.kernel(p + "probs", {"type": "softmax", "args": [scr], "batch": H, "rows": S, "cols": S,
-                                        "scale": scale, "causal": 1}, (H, S, S), "bf16", dev)
-        o = g.gemm(p + "attn", a["P"], vt, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
-                   causal=2, out_shape=(S, d), device=dev)
+        if fused_attention:  # the fused kernel; the backward recomputes it with the row logsumexp
+            o = g.kernel(p + "attn", {"type": "attention", "args": [a["q"], a["k"], vt], "heads": H, "seq": S,
+                                      "hd": hd, "ldo": d, "scale": scale, "causal": 1}, (S, d), "bf16", dev,
+                         cost=attn_flops / _PEAK_FLOPS)
+            g.flops += attn_flops
+        else:
+            scr = g.gemm(p + "scores", a["q"], a["k"], S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S,
+                         out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
+            a["P"] = g.kernel(p + "probs", {"type": "softmax", "args": [scr], "batch": H, "rows": S, "cols": S,
+                                            "scale": scale, "causal": 1}, (H, S, S), "bf16", dev)
+            o = g.gemm(p + "attn", a["P"], vt, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                       causal=2, out_shape=(S, d), device=dev)
         a["x1"] = g.gemm(p + "attn_out", o, w["wo"], S, d, d, r=x, out_shape=(S, d), device=dev)
         a["h2"] = rms(p + "ffn_norm_out", a["x1"], w["wn2"])
         gub = g.gemm(p + "gate_up_base", a["h2"], w["w13"], S, 2 * f, d, out_shape=(S, 2 * f), device=dev)
@@ -697,6 +710,45 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
                                                   "col_off": d, "heads": H, "hd": hd}, (H, S, hd), "bf16", dev))
         return a
 
+    def attention_grads(p, a, do):
+        """dq, dk, dv of the materialised attention (scores / probs / softmax_bwd)."""
+        dP = g.gemm(p + "d_probs", do, a["qkv"], S, S, hd, batch=H, lda=d, sa=hd, ldb=3 * d, b_off=2 * d, sb=hd,
+                    sc=S * S, out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
+        if recompute_attention:  # P again from the saved q, k (bitwise the forward's)
+            scr_b = g.gemm(p + "scores.re", a["q"], a["k"], S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S,
+                           out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
+            P = g.kernel(p + "probs.re", {"type": "softmax", "args": [scr_b], "batch": H, "rows": S, "cols": S,
+                                          "scale": scale, "causal": 1}, (H, S, S), "bf16", dev)
+        else:
+            P = a["P"]
+        dS = g.kernel(p + "d_scores", {"type": "softmax_bwd", "args": [P, dP], "batch": H, "rows": S, "cols": S,
+                                       "causal": 1, "in_dtype": "f32"}, (H, S, S), "bf16", dev)
+        if mn_major:  # k, q [H, S, hd], dS / P [H, queries, keys], do [S, d] read in place
+            dq_r = g.gemm(p + "d_q_rot", dS, a["k"], S, hd, S, batch=H, lda=S, ldb=hd, ldc=d, sa=S * S, sb=hd * S,
+                          sc=hd, alpha=scale, causal=2, b_major="mn", out_shape=(S, d), device=dev)
+            dk_r = g.gemm(p + "d_k_rot", dS, a["q"], S, hd, S, batch=H, lda=S, ldb=hd, ldc=d, sa=S * S, sb=hd * S,
+                          sc=hd, alpha=scale, a_major="mn", b_major="mn", out_shape=(S, d), device=dev)
+            dv = g.gemm(p + "d_v", P, do, S, hd, S, batch=H, lda=S, ldb=d, ldc=d, sa=S * S, sb=hd, sc=hd,
+                        a_major="mn", b_major="mn", out_shape=(S, d), device=dev)
+        else:
+            kT = tr(p + "k.T", a["k"], S, hd, batch=H)
+            dq_r = g.gemm(p + "d_q_rot", dS, kT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                          alpha=scale, causal=2, out_shape=(S, d), device=dev)
+            dST = tr(p + "d_scores.T", dS, S, S, batch=H)
+            qT = tr(p + "q.T", a["q"], S, hd, batch=H)
+            dk_r = g.gemm(p + "d_k_rot", dST, qT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S,
+                          sc=hd, alpha=scale, out_shape=(S, d), device=dev)
+            PT = tr(p + "probs.T", P, S, S, batch=H)
+            doT = g.kernel(p + "d_attn.T", {"type": "transpose_heads", "args": [do], "seq": S, "ld": d, "col_off": 0,
+                                            "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
+            dv = g.gemm(p + "d_v", PT, doT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
+                        out_shape=(S, d), device=dev)
+        dq = g.kernel(p + "d_q", {"type": "rope", "args": [dq_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
+                                  "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
+        dk = g.kernel(p + "d_k", {"type": "rope", "args": [dk_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
+                                  "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
+        return dq, dk, ((dq, None, None), (dk, None, None), (dv, None, None))
+
     rec = {}
     for l in reversed(range(L)):
         # the recompute of layers l-1 .. l-bwd_prefetch is listed ahead of layer l's
@@ -739,50 +791,36 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
         else:
             woT = tr(p + "wo.T", w["wo"], d, d)
             do = g.gemm(p + "d_attn", dx1, woT, S, d, d, out_shape=(S, d), device=dev)
-        dP = g.gemm(p + "d_probs", do, a["qkv"], S, S, hd, batch=H, lda=d, sa=hd, ldb=3 * d, b_off=2 * d, sb=hd,
-                    sc=S * S, out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
-        if recompute_attention:  # P again from the saved q, k (bitwise the forward's)
-            scr_b = g.gemm(p + "scores.re", a["q"], a["k"], S, S, hd, batch=H, sa=S * hd, sb=S * hd, sc=S * S,
-                           out_dtype="f32", causal=1, out_shape=(H, S, S), device=dev)
-            P = g.kernel(p + "probs.re", {"type": "softmax", "args": [scr_b], "batch": H, "rows": S, "cols": S,
-                                          "scale": scale, "causal": 1}, (H, S, S), "bf16", dev)
+        if fused_attention:
+            # O and the row logsumexp again (fused forward), then dq|dk|dv in one fused kernel
+            vt_r = g.kernel(p + "v_t.re", {"type": "transpose_heads", "args": [a["qkv"]], "seq": S, "ld": 3 * d,
+                                           "col_off": 2 * d, "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
+            o_lse = g.kernel(p + "attn.re", {"type": "attention", "args": [a["q"], a["k"], vt_r], "heads": H,
+                                             "seq": S, "hd": hd, "ldo": d, "scale": scale, "causal": 1, "lse": 1},
+                             (S * d + 2 * H * S,), "bf16", dev, cost=attn_flops / _PEAK_FLOPS)
+            g.flops += attn_flops
+            dqkv = g.kernel(p + "d_attn_qkv", {"type": "attention_bwd", "args": [a["q"], a["k"], a["qkv"], o_lse, do],
+                                                "heads": H, "seq": S, "hd": hd, "scale": scale, "causal": 1,
+                                                "v_off": 2 * d, "v_ld": 3 * d, "ldo": d, "do_ld": d},
+                            (S * 3 * d + 2 * H * S,), "bf16", dev, cost=2.5 * attn_flops / _PEAK_FLOPS)
+            g.flops += 2.5 * attn_flops
+            dq = g.kernel(p + "d_q", {"type": "rope", "args": [dqkv, rope_tab], "seq": S, "ld": 3 * d, "col_off": 0,
+                                      "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
+            dk = g.kernel(p + "d_k", {"type": "rope", "args": [dqkv, rope_tab], "seq": S, "ld": 3 * d,
+                                      "col_off": d, "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d),
+                          "bf16", dev)
+            parts = ((dq, None, None), (dk, None, None), (dqkv, 2 * d, 3 * d))  # (tensor, a_off, lda)
         else:
-            P = a["P"]
-        dS = g.kernel(p + "d_scores", {"type": "softmax_bwd", "args": [P, dP], "batch": H, "rows": S, "cols": S,
-                                       "causal": 1, "in_dtype": "f32"}, (H, S, S), "bf16", dev)
-        if mn_major:  # k, q [H, S, hd], dS / P [H, queries, keys], do [S, d] read in place
-            dq_r = g.gemm(p + "d_q_rot", dS, a["k"], S, hd, S, batch=H, lda=S, ldb=hd, ldc=d, sa=S * S, sb=hd * S,
-                          sc=hd, alpha=scale, causal=2, b_major="mn", out_shape=(S, d), device=dev)
-            dk_r = g.gemm(p + "d_k_rot", dS, a["q"], S, hd, S, batch=H, lda=S, ldb=hd, ldc=d, sa=S * S, sb=hd * S,
-                          sc=hd, alpha=scale, a_major="mn", b_major="mn", out_shape=(S, d), device=dev)
-            dv = g.gemm(p + "d_v", P, do, S, hd, S, batch=H, lda=S, ldb=d, ldc=d, sa=S * S, sb=hd, sc=hd,
-                        a_major="mn", b_major="mn", out_shape=(S, d), device=dev)
-        else:
-            kT = tr(p + "k.T", a["k"], S, hd, batch=H)
-            dq_r = g.gemm(p + "d_q_rot", dS, kT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
-                          alpha=scale, causal=2, out_shape=(S, d), device=dev)
-            dST = tr(p + "d_scores.T", dS, S, S, batch=H)
-            qT = tr(p + "q.T", a["q"], S, hd, batch=H)
-            dk_r = g.gemm(p + "d_k_rot", dST, qT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S,
-                          sc=hd, alpha=scale, out_shape=(S, d), device=dev)
-            PT = tr(p + "probs.T", P, S, S, batch=H)
-            doT = g.kernel(p + "d_attn.T", {"type": "transpose_heads", "args": [do], "seq": S, "ld": d, "col_off": 0,
-                                            "heads": H, "hd": hd}, (H, hd, S), "bf16", dev)
-            dv = g.gemm(p + "d_v", PT, doT, S, hd, S, batch=H, lda=S, ldb=S, ldc=d, sa=S * S, sb=hd * S, sc=hd,
-                        out_shape=(S, d), device=dev)
-        dq = g.kernel(p + "d_q", {"type": "rope", "args": [dq_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
-                                  "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
-        dk = g.kernel(p + "d_k", {"type": "rope", "args": [dk_r, rope_tab], "seq": S, "ld": d, "col_off": 0,
-                                  "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
+            dq, dk, parts = attention_grads(p, a, do)
         # qkv = h·Wqkvᵀ + s·U1·B1ᵀ with dqkv = [dq | dk | dv]
         V1 = None
         dBs = []
         if mn_major:  # B1 [3d, R] (part j: rows j*d..), U1 [S, R], dq/dk/dv [S, d], h [S, d], V1 [S, R]
-            for j, dpart in enumerate((dq, dk, dv)):
+            for j, (dpart, off, ld) in enumerate(parts):
                 V1 = g.gemm(p + f"lora_qkv.V{j}", dpart, w["B1"], S, R, d, ldb=R, b_off=j * d * R, r=V1,
-                            b_major="mn", out_shape=(S, R), device=dev)
+                            b_major="mn", a_off=off, lda=ld, out_shape=(S, R), device=dev)
                 dBs.append(g.gemm(p + f"lora_qkv.dB{j}", dpart, a["U1"], d, R, S, alpha=sc, a_major="mn",
-                                  b_major="mn", out_shape=(d, R), device=dev))
+                                  b_major="mn", a_off=off, lda=ld, out_shape=(d, R), device=dev))
             results[p + "lora_qkv.dB"] = g.kernel(p + "lora_qkv.dB", {"type": "concat", "args": dBs, "count": d * R,
                                                                       "out_dtype": "bf16"}, (3 * d, R), "bf16", dev)
             dA1T = g.gemm(p + "lora_qkv.dA.T", a["h"], V1, d, R, S, alpha=sc, a_major="mn", b_major="mn",
@@ -790,7 +828,7 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
         else:
             B1T = tr(p + "lora_qkv.B.T", w["B1"], 3 * d, R)
             U1T = tr(p + "lora_qkv.U.T", a["U1"], S, R)
-            for j, dpart in enumerate((dq, dk, dv)):
+            for j, (dpart, _, _) in enumerate(parts):
                 V1 = g.gemm(p + f"lora_qkv.V{j}", dpart, B1T, S, R, d, ldb=3 * d, b_off=j * d, r=V1,
                             out_shape=(S, R), device=dev)
                 dT = tr(p + f"lora_qkv.dY{j}.T", dpart, S, d)
@@ -805,15 +843,15 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
             break  # no gradient is needed below the first layer
         dh = None
         if mn_major:  # Wqkv [3d, d] (part j: rows j*d..), A1 [R, d]
-            for j, dpart in enumerate((dq, dk, dv)):
+            for j, (dpart, off, ld) in enumerate(parts):
                 dh = g.gemm(p + f"d_attn_norm_out{j}", dpart, w["wqkv"], S, d, d, ldb=d, b_off=j * d * d, r=dh,
-                            b_major="mn", out_shape=(S, d), device=dev)
+                            b_major="mn", a_off=off, lda=ld, out_shape=(S, d), device=dev)
             dh = g.gemm(p + "d_attn_norm_out", V1, w["A1"], S, d, R, r=dh, alpha=sc, b_major="mn",
                         out_shape=(S, d), device=dev)
         else:
             wqkvT = tr(p + "wqkv.T", w["wqkv"], 3 * d, d)
             A1T = tr(p + "lora_qkv.A.T", w["A1"], R, d)
-            for j, dpart in enumerate((dq, dk, dv)):
+            for j, (dpart, _, _) in enumerate(parts):
                 dh = g.gemm(p + f"d_attn_norm_out{j}", dpart, wqkvT, S, d, d, ldb=3 * d, b_off=j * d, r=dh,
                             out_shape=(S, d), device=dev)
             dh = g.gemm(p + "d_attn_norm_out", V1, A1T, S, d, R, r=dh, alpha=sc, out_shape=(S, d), device=dev)

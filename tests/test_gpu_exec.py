@@ -267,6 +267,61 @@ def test_fused_attention_parity(seq, hd, causal, sigma):
     assert _e < 5e-3
 
 
+def _attn_bwd_graph(seq, causal, sigma, H=2, hd=128):
+    """q, k, qkv (v in its last third), dO -> fused forward with the row
+    logsumexp -> fused backward; both vertices are graph outputs."""
+    w = H * hd
+    g = W.GraphBuilder()
+    q = g.input("q", (H, seq, hd), "bf16", init=("normal", sigma))
+    k = g.input("k", (H, seq, hd), "bf16", init=("normal", sigma))
+    qkv = g.input("qkv", (seq, 3 * w), "bf16", init=("normal", 1.0))
+    dout = g.input("dout", (seq, w), "bf16", init=("normal", 1.0))
+    vt = g.kernel("vt", {"type": "transpose_heads", "args": [qkv], "seq": seq, "ld": 3 * w, "col_off": 2 * w,
+                         "heads": H, "hd": hd}, (H, hd, seq), "bf16")
+    o = g.kernel("o", {"type": "attention", "args": [q, k, vt], "heads": H, "seq": seq, "hd": hd, "ldo": w,
+                       "scale": hd ** -0.5, "causal": causal, "lse": 1}, (seq * w + 2 * H * seq,), "bf16")
+    gr = g.kernel("grad", {"type": "attention_bwd", "args": [q, k, qkv, o, dout], "heads": H, "seq": seq, "hd": hd,
+                           "scale": hd ** -0.5, "causal": causal, "v_off": 2 * w, "v_ld": 3 * w, "ldo": w,
+                           "do_ld": w}, (seq * 3 * w + 2 * H * seq,), "bf16")
+    g.kernel("o_copy", dict(g.vertices[o]["op"]), (seq * w + 2 * H * seq,), "bf16")  # O + lse as an output
+    return g, o, gr
+
+
+@pytest.mark.parametrize("seq,causal,sigma", [(256, 1, 1.0), (384, 1, 1.0), (512, 0, 1.0), (1024, 1, 2.0),
+                                              (256, 0, 4.0)])
+def test_fused_attention_bwd_parity(seq, causal, sigma):
+    """attention_bwd (tcgen05, both CTA roles) and the forward's logsumexp
+    output against the fp32 oracle; deterministic (bitwise equal reruns)."""
+    H, hd = 2, 128
+    w = H * hd
+    g, o, gr = _attn_bwd_graph(seq, causal, sigma, H, hd)
+    mg, _ = W.plan(g, 1 << 30)
+    inp = inputs_of(g, seed=17)
+    _, got = run_gpu(g, mg, inp)
+    _, got2 = run_gpu(g, mg, inp)
+    want = oracle_outputs(g, mg, inp)
+    (oc,) = [v for v in g.outputs() if g.tensors[v].name == "o_copy"]
+    assert got[gr] == got2[gr]
+    n = seq * 3 * w
+    G = np.frombuffer(got[gr], np.uint16)[:n]
+    Gw = np.frombuffer(want[gr], np.uint16)[:n]
+    from helpers import as_f32
+    gg = as_f32(G.tobytes(), "bf16", n).reshape(seq, 3, w)
+    gw = as_f32(Gw.tobytes(), "bf16", n).reshape(seq, 3, w)
+    for j, nm in enumerate(("dq", "dk", "dv")):
+        e = rel_err(gg[:, j], gw[:, j])
+        record_err("attention_bwd", seq=seq, causal=causal, sigma=sigma, part=nm, rel_err=e)
+        assert e < 2e-2, nm
+    D = np.frombuffer(got[gr], np.float32, count=H * seq, offset=n * 2)
+    Dw = np.frombuffer(want[gr], np.float32, count=H * seq, offset=n * 2)
+    assert rel_err(D, Dw) < 2e-3
+    lse = np.frombuffer(got[oc], np.float32, count=H * seq, offset=seq * w * 2)
+    lsew = np.frombuffer(want[oc], np.float32, count=H * seq, offset=seq * w * 2)
+    e = float(np.max(np.abs(lse - lsew)))
+    record_err("attention_lse", seq=seq, causal=causal, sigma=sigma, max_abs=e)
+    assert e < 2e-3
+
+
 def test_unfused_attention_pipeline_matches_fused():
     """Materialised S/P (scores gemm -> softmax -> P·V gemm) vs the fused vertex."""
     from helpers import SMALL

@@ -3,6 +3,7 @@ semantics, verifier.cpp:316-349) and agreement with a memgraph-free forward."""
 import json
 
 import numpy as np
+import pytest
 
 from helpers import direct_forward, inputs_of, oracle_outputs, out_values, rel_err, small_llama
 from oracle import ops_ref
@@ -216,14 +217,16 @@ def _lora_torch_reference(g, inp, cfg, seq, rank_pad=64, rank=16, lora_alpha=16.
     return float(loss), {k: v.grad.numpy() for k, v in params.items()}
 
 
-def test_lora_step_gradients_match_torch_autograd():
+@pytest.mark.parametrize("fused_attention", [False, True])
+def test_lora_step_gradients_match_torch_autograd(fused_attention):
     """Config-4 semantics: the LoRA fwd+bwd memgraph (transposes, rmsnorm/
-    swiglu/softmax backward, inverse RoPE, cross entropy), executed by the
-    oracle under an offloading plan, reproduces fp32 autograd's loss and
-    adapter gradients (bf16 activations: 5e-2 normwise)."""
+    swiglu/softmax backward, inverse RoPE, cross entropy; or the fused
+    attention forward with logsumexp + attention_bwd), executed by the oracle
+    under an offloading plan, reproduces fp32 autograd's loss and adapter
+    gradients (bf16 activations: 5e-2 normwise)."""
     cfg = W.LlamaConfig(dim=256, layers=2, heads=2, ffn=256, vocab=300)
     S = 128
-    g = W.llama_lora_step(cfg, S)
+    g = W.llama_lora_step(cfg, S, fused_attention=fused_attention)
     fl = W.working_set_floor(g)[0]
     mg, st = W.plan(g, int(fl * 2.0), alloc_horizon="lazy")
     assert st["offloads"] > 0  # activations are offloaded between forward and backward

@@ -20,13 +20,15 @@ ap.add_argument("--compare", action="store_true")
 ap.add_argument("--exec-cfg", default="{}", help="extra executor config keys (JSON)")
 ap.add_argument("--horizon", default="lazy")
 ap.add_argument("--bwd-prefetch", type=int, default=0)
+ap.add_argument("--fused-attention", type=int, default=None, help="1/0: override the builder default")
 ap.add_argument("--no-recompute-norms", action="store_true")
 ap.add_argument("--no-mn-major", action="store_true", help="explicit transpose vertices in the backward")
 ap.add_argument("--dump", default="", help="write the memgraph + one traced step here (JSON)")
 a = ap.parse_args()
 t0 = time.time()
 g = W.llama_lora_step(W.LLAMA_7B, a.seq, layers=a.layers, mn_major=not a.no_mn_major, bwd_prefetch=a.bwd_prefetch,
-                      recompute_norms=not a.no_recompute_norms)
+                      recompute_norms=not a.no_recompute_norms,
+                      **({} if a.fused_attention is None else {"fused_attention": bool(a.fused_attention)}))
 mg, st = W.plan(g, int(a.cap_gib * (1 << 30)), alloc_horizon=a.horizon)
 m = json.loads(mg)
 off = sum(v["size"] for v in m["vertices"] if v["op"] == "offload")
@@ -58,7 +60,7 @@ stt = ex.stats()
 loss_id = next(o for o in g.outputs() if g.tensors[o].name == "loss")
 import struct
 loss = struct.unpack("<f", ex.get_output(loss_id, 4))[0]
-res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency}_{a.horizon}" + ("_transposes" if a.no_mn_major else "") + (f"_bwdpf{a.bwd_prefetch}" if a.bwd_prefetch else "") + ("_savednorms" if a.no_recompute_norms else ""), "exec_cfg": a.exec_cfg, "memgraph_vertices": len(m["vertices"]),
+res = {"workload": f"llama7b_lora_step_seq{a.seq}_cap{a.cap_gib}GiB_{a.residency}_{a.horizon}" + ("_transposes" if a.no_mn_major else "") + (f"_bwdpf{a.bwd_prefetch}" if a.bwd_prefetch else "") + ("_savednorms" if a.no_recompute_norms else "") + ("" if a.fused_attention is None else f"_fusedattn{a.fused_attention}"), "exec_cfg": a.exec_cfg, "memgraph_vertices": len(m["vertices"]),
        "plan": st, "plan_s": round(plan_s, 2), "offload_gb": round(off / 1e9, 1), "step_s": [round(x, 4) for x in ts], "traced_step_makespan_s": round(traced, 4),
        "loss": loss, "tokens_per_s": round(a.seq / min(ts), 1), "flops": stt["flops"],
        "h2d_gb": round(stt["h2d_bytes"] / 1e9, 2), "d2h_gb": round(stt["d2h_bytes"] / 1e9, 2),
