@@ -588,14 +588,33 @@ def offload_leg(args, devs):
         ex.run(trace=False)
         steps = max(1, args.offload_steps)
         t = timed_runs(ex, steps, devs) / steps
-        ex.run()  # one traced step: exposed transfer
+        tr4 = json.loads(ex.run())  # one traced step: exposed transfer, backward kernel time
         s = ex.stats()
         pcie_h2d, pcie_d2h = measure_pcie(torch.device("cuda", dev)), measure_pcie(torch.device("cuda", dev), "d2h")
+        # dependency bound: the loss needs every layer's weights (all cold in host RAM), and the
+        # backward needs the loss -> step >= weight bytes / PCIe + the backward's kernel time
+        kinds = {v["id"]: v for v in json.loads(g.to_json())["vertices"]}
+        mk = {v["id"]: v for v in m["vertices"]}
+        loss_ids = {v for v in g.outputs() if g.tensors[v].name.startswith("loss")}
+        loss_end = max(r["end"] for r in tr4["rows"] if mk[r["vertex"]]["origin"]["ref"] in loss_ids)
+        bwd_iv = sorted((max(r["start"], loss_end), r["end"]) for r in tr4["rows"]
+                        if mk[r["vertex"]]["op"] == "kernel" and r["end"] > loss_end)
+        bwd_busy, cur = 0.0, None
+        for a_, b_ in bwd_iv:
+            if cur is None or a_ > cur[1]:
+                bwd_busy += (cur[1] - cur[0]) if cur else 0.0
+                cur = [a_, b_]
+            else:
+                cur[1] = max(cur[1], b_)
+        bwd_busy += (cur[1] - cur[0]) if cur else 0.0
+        wbytes = sum(g.tensors[v["id"]].nbytes for v in kinds.values() if v["kind"] == "input")
+        dep_bound = wbytes / (len(set(devs)) * pcie_h2d * 1e9) + bwd_busy
         gpus = len(set(devs))
         roof = max(s["flops"] / (gpus * pk["bf16_tflops_sustained"] * 1e12), s["h2d_bytes"] / (gpus * pcie_h2d * 1e9),
                    s["d2h_bytes"] / (gpus * pcie_d2h * 1e9))
         out["config4_lora_step"] = {
-            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy_recompute_attn_qkv_ffn" + (f"_dp{dp}" if dp > 1 else ""),
+            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy_fused_attn_bwd_recompute_qkv_ffn_norms"
+                        + (f"_dp{dp}" if dp > 1 else ""),
             "gpus": gpus, "global_batch": dp, "memgraph_vertices": len(m["vertices"]),
             "offloads": st["offloads"], "reloads": st["reloads"], "offload_bytes_planned": off,
             "reload_bytes_planned": rel, "step_s": round(t, 4), "tokens_per_s": round(dp * args.seq / t, 1),
@@ -607,12 +626,16 @@ def offload_leg(args, devs):
             "exposed_transfer_s": round(s["exposed_transfer_s"], 4), "flops": s["flops"],
             "roofline_s": round(roof, 4), "frac_of_roofline": round(roof / t, 4),
             "plan_ideal_s": round(plan_ideal_s(mg, pcie_h2d), 4),
-            "roofline": "max(FLOP / sustained bf16 peak, H2D bytes / PCIe H2D, D2H bytes / PCIe D2H), per GPU"}
+            "roofline": "max(FLOP / sustained bf16 peak, H2D bytes / PCIe H2D, D2H bytes / PCIe D2H), per GPU",
+            "dependency_bound_s": round(dep_bound, 4), "frac_of_dependency_bound": round(dep_bound / t, 4),
+            "backward_kernel_busy_s": round(bwd_busy, 4),
+            "dependency_bound": "input (weight) bytes / PCIe H2D + the traced backward's kernel busy time: the "
+                                "loss needs every cold weight, the backward needs the loss"}
         if args.policy_trials > 0:
             out["config4_lora_step"]["compare_policies"] = json.loads(ex.compare_policies(args.policy_trials, 0))
     if dp == 1:
-        # the same step keeping the QKV / FFN activations (attention probabilities
-        # still recomputed): 3x the activation offload, more PCIe-bound
+        # the same step keeping the QKV / FFN activations (the attention forward
+        # still recomputed for its logsumexp): more activation offload, more PCIe-bound
         g2 = W.llama_lora_step(W.LLAMA_7B, args.seq, recompute_ffn=False, recompute_qkv=False)
         mg2, st2 = W.plan(g2, [int(args.cap_gib * (1 << 30))], alloc_horizon="lazy")
         with Executor(mg2, g2.to_json(), {"devices": devs, "input_residency": "host"}) as ex:
@@ -623,7 +646,7 @@ def offload_leg(args, devs):
         pcie_h2d = measure_pcie(torch.device("cuda", dev))
         roof2 = max(s2["flops"] / (pk["bf16_tflops_sustained"] * 1e12), s2["h2d_bytes"] / (pcie_h2d * 1e9))
         out["config4_lora_step_saved_activations"] = {
-            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy_recompute_attn", "offloads": st2["offloads"],
+            "workload": "llama7b_lora_step_seq4096_cap16GiB_lazy_fused_attn_bwd_saved_qkv_ffn", "offloads": st2["offloads"],
             "step_s": round(t2, 4), "tokens_per_s": round(args.seq / t2, 1), "h2d_bytes": s2["h2d_bytes"],
             "d2h_bytes": s2["d2h_bytes"], "flops": s2["flops"], "roofline_s": round(roof2, 4),
             "frac_of_roofline": round(roof2 / t2, 4)}

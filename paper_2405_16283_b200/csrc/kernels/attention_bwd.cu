@@ -24,7 +24,7 @@
 //   warp 0     TMA: the CTA's fixed tiles once, then a 2-stage ring of the
 //              walked tiles (+ the 128 lse / D values of a query block)
 //   warp 1     MMA issue (one elected lane)
-//   warps 2-5  one TMEM lane (row) per thread: P, dS, epilogue
+//   warps 2-9  P, dS, epilogue: one TMEM lane (row) and 64 of its columns per thread
 // TMEM (512 columns): S / P [0,128), dP / dS [128,256), dV or dQ [256,384),
 // dK [384,512). smem: 2 fixed 32 KB tiles + 1 KB, 2 stages of 65 KB.
 #include <cuda_bf16.h>
@@ -45,7 +45,7 @@ constexpr int kTile = kT * kHdB * 2;      // 32 KB: two SW128 atoms of [128 rows
 constexpr int kAtomB = kTile / 2;         // 16 KB
 constexpr int kVec = kT * 4;              // 512 B: the lse or D values of one query block
 constexpr int kStage = 2 * kTile + 2 * kVec;  // 65 KB (a multiple of 1 KB)
-constexpr int kThreadsB = 192;
+constexpr int kThreadsB = 320;
 constexpr int kSmemB = 3 * kStage + 256;  // fixed (2 tiles + vecs) + 2 stages + barriers
 
 struct BwdParams {
@@ -86,10 +86,10 @@ __device__ __forceinline__ float2 unpack2(std::uint32_t u) {
     __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
     return __bfloat1622float2(v);
 }
-// One 128-column fp32 TMEM row (this thread's lane) -> bf16 at dst, times mul.
+// 64 fp32 TMEM columns of this thread's lane -> bf16 at dst, times mul.
 __device__ __forceinline__ void store_row(std::uint32_t taddr, __nv_bfloat16* dst, float mul) {
 #pragma unroll 1
-    for (int c = 0; c < kHdB; c += 32) {
+    for (int c = 0; c < 64; c += 32) {
         std::uint32_t u[32];
         TN_LD32(taddr + c, u);
         tc_wait_ld();
@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tv)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tdo)) : "memory");
         for (int i = 0; i < 6; ++i) mbar_init(b0 + 8 * i, 1);  // fix, stg full/empty, s_full
-        mbar_init(p_full, 4);
-        mbar_init(ds_full, 4);
+        mbar_init(p_full, 8);
+        mbar_init(ds_full, 8);
         mbar_init(o_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -217,13 +217,14 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 // dV += Pᵀ dO_i (A = Pᵀ in TMEM, K = queries; B = dO_i MN-major)
 #pragma unroll
                 for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA0, tS + kk * 8, sdesc_mn16(sb + kTile + kk * 2048), id_mn, (it | kk) != 0);
+                    tc_mma_ts(tA0, tS + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kTile + kk * 2048), id_mn,
+                              (it | kk) != 0);
                 mbar_wait(ds_full, it & 1);
                 tc_fence_after();
                 // dK += dSᵀ Q_i (A = dSᵀ in TMEM; B = Q_i MN-major)
 #pragma unroll
                 for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA1, tdP + kk * 8, sdesc_mn16(sb + kk * 2048), id_mn, (it | kk) != 0);
+                    tc_mma_ts(tA1, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn, (it | kk) != 0);
             } else {
                 // S = Q_i K_jᵀ, dP = dO_i V_jᵀ (M = queries, N = keys)
 #pragma unroll
@@ -238,28 +239,33 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 // dQ += dS K_j (A = dS in TMEM, K = keys; B = K_j MN-major)
 #pragma unroll
                 for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA0, tdP + kk * 8, sdesc_mn16(sb + kk * 2048), id_mn, (it | kk) != 0);
+                    tc_mma_ts(tA0, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn, (it | kk) != 0);
             }
             tc_commit(stg_empty + 8 * st);
         }
         tc_commit(o_done);
     } else {
-        const int lane_base = (warp % 4) * 32;
+        // two warps per TMEM lane quadrant: warp w owns rows 32*(w%4).. and
+        // the 64 columns [64*hf, +64) of them; its bf16 P / dS pairs go to the
+        // first 32 of those columns (the MMA A operand reads columns
+        // 64*(kk/4) + 8*(kk%4) for K16 step kk), never over a column another
+        // warp has still to read
+        const int lane_base = (warp % 4) * 32, hf = (warp - 2) / 4, c_lo = 64 * hf;
         const int r = lane_base + lane;  // this thread's TMEM lane = tile row
-        const std::uint32_t trow = static_cast<std::uint32_t>(lane_base) << 16;
+        const std::uint32_t trow = (static_cast<std::uint32_t>(lane_base) << 16) + static_cast<std::uint32_t>(c_lo);
         constexpr float kLog2e = 1.4426950408889634f;
         const float sl2 = p.scale_log2;
-        std::uint32_t pk[64];
+        std::uint32_t pk[32];
         if (!role_q) {
             for (int it = 0; it < n; ++it) {
                 const int st = it & 1, i = first + it;
-                const float* lse = reinterpret_cast<const float*>(smem_raw + kStage * (1 + st) + 2 * kTile);
+                const float* lse = reinterpret_cast<const float*>(smem_raw + kStage * (1 + st) + 2 * kTile) + c_lo;
                 const float* Dv = lse + kT;
                 const bool diag = p.causal && i == tb;  // key r > query c is masked
                 mbar_wait(s_full, it & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int c0 = 0; c0 < kT; c0 += 32) {
+                for (int c0 = 0; c0 < 64; c0 += 32) {
                     std::uint32_t u[32];
                     TN_LD32(tS + trow + c0, u);
                     tc_wait_ld();
@@ -270,20 +276,19 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                         float x1 = fmaf(__uint_as_float(u[cc + 1]), sl2, -lse[c + 1] * kLog2e);
                         float p0 = ex2(x0), p1 = ex2(x1);
                         if (diag) {
-                            if (r > c) p0 = 0.f;
-                            if (r > c + 1) p1 = 0.f;
+                            if (r > c_lo + c) p0 = 0.f;
+                            if (r > c_lo + c + 1) p1 = 0.f;
                         }
                         pk[c / 2] = pack2(p0, p1);
                     }
                 }
                 TN_ST32(tS + trow, pk);  // Pᵀ (bf16 pairs) over Sᵀ
-                TN_ST32(tS + trow + 32, (pk + 32));
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full);
 #pragma unroll
-                for (int c0 = 0; c0 < kT; c0 += 32) {
+                for (int c0 = 0; c0 < 64; c0 += 32) {
                     std::uint32_t u[32];
                     TN_LD32(tdP + trow + c0, u);
                     tc_wait_ld();
@@ -296,7 +301,6 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                     }
                 }
                 TN_ST32(tdP + trow, pk);  // dSᵀ over dPᵀ
-                TN_ST32(tdP + trow + 32, (pk + 32));
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -305,8 +309,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             mbar_wait(o_done, 0);
             tc_fence_after();
             const std::int64_t row = static_cast<std::int64_t>(tb) * kT + r;
-            store_row(tA0 + trow, p.dv + row * p.ldg + static_cast<std::int64_t>(h) * kHdB, 1.0f);
-            store_row(tA1 + trow, p.dk + row * p.ldg + static_cast<std::int64_t>(h) * kHdB, p.scale);
+            const std::int64_t col = static_cast<std::int64_t>(h) * kHdB + c_lo;
+            store_row(tA0 + trow, p.dv + row * p.ldg + col, 1.0f);
+            store_row(tA1 + trow, p.dk + row * p.ldg + col, p.scale);
         } else {
             mbar_wait(fix_full, 0);  // lse_i, D_i staged with Q_i
             const float lse2 = fixv[r] * kLog2e, Dr = fixv[kT + r];
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(s_full, it & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int c0 = 0; c0 < kT; c0 += 32) {
+                for (int c0 = 0; c0 < 64; c0 += 32) {
                     std::uint32_t us[32], ud[32];
                     TN_LD32(tS + trow + c0, us);
                     TN_LD32(tdP + trow + c0, ud);
@@ -327,15 +332,14 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                         float p0 = ex2(fmaf(__uint_as_float(us[cc]), sl2, -lse2));
                         float p1 = ex2(fmaf(__uint_as_float(us[cc + 1]), sl2, -lse2));
                         if (diag) {
-                            if (c > r) p0 = 0.f;
-                            if (c + 1 > r) p1 = 0.f;
+                            if (c_lo + c > r) p0 = 0.f;
+                            if (c_lo + c + 1 > r) p1 = 0.f;
                         }
                         const float2 pp = unpack2(pack2(p0, p1));  // the bf16 P the KV role multiplies
                         pk[c / 2] = pack2(pp.x * (__uint_as_float(ud[cc]) - Dr), pp.y * (__uint_as_float(ud[cc + 1]) - Dr));
                     }
                 }
                 TN_ST32(tdP + trow, pk);  // dS over dP
-                TN_ST32(tdP + trow + 32, (pk + 32));
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
             mbar_wait(o_done, 0);
             tc_fence_after();
             const std::int64_t row = static_cast<std::int64_t>(tb) * kT + r;
-            store_row(tA0 + trow, p.dq + row * p.ldg + static_cast<std::int64_t>(h) * kHdB, p.scale);
+            store_row(tA0 + trow, p.dq + row * p.ldg + static_cast<std::int64_t>(h) * kHdB + c_lo, p.scale);
         }
     }
     tc_fence_before();

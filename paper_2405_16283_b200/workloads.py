@@ -479,7 +479,7 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
                     recompute_attention: bool = True, recompute_ffn: bool = True,
                     recompute_qkv: bool = True, mn_major: bool = True, prefetch: int = 0,
                     recompute_norms: bool = True, bwd_prefetch: int = 0,
-                    fused_attention: bool = False) -> GraphBuilder:
+                    fused_attention: bool | None = None) -> GraphBuilder:
     """Config 4: one LoRA fine-tuning step (forward + backward) of a LLaMA
     model over `seq` tokens, rank-`rank` adapters on the fused QKV projection
     and on both FFN projections ("rank 16 on Q,K,V,FFN"), frozen
@@ -513,7 +513,24 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     `mn_major` (default): the backward GEMMs read transposed operands in place
     ("a_major" / "b_major": "mn", e.g. dX = dY·W with W stored [out, in]) instead
     of through explicit transpose vertices (≈1,000 vertices and ~3 GB of
-    transposed copies per layer on the 7B step, n² probability tiles included)."""
+    transposed copies per layer on the 7B step, n² probability tiles included).
+
+    `recompute_norms` (default): the backward recomputes both RMSNorm outputs
+    from the saved residual stream (x, x1), so only x, x1 and the rank-R
+    adapter activations stay live across the step. `prefetch` /
+    `bwd_prefetch`: list the next layers' weight inputs / recompute GEMMs
+    that many layers early in the taskgraph order (planner-visible prefetch;
+    measured neutral on the 7B step, default 0).
+
+    `fused_attention` (default when hd == 128 and seq % 128 == 0): the
+    forward runs the fused attention kernel, and the backward recomputes it
+    with the per-row logsumexp ("lse": 1) and takes dq|dk|dv from ONE fused
+    `attention_bwd` vertex (csrc/kernels/attention_bwd.cu) instead of the
+    materialised scores / probs / dP / dS chain: no n² tensor exists at all,
+    so the 7B step under 16 GiB needs no activation offload (step 0.52 ->
+    0.39 s)."""
+    if fused_attention is None:
+        fused_attention = mn_major and cfg.hd == 128 and seq % 128 == 0
     g = GraphBuilder(device_count=1)
     _lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, device, "", recompute_attention,
                     recompute_ffn, recompute_qkv, mn_major, prefetch, recompute_norms, bwd_prefetch,
@@ -526,7 +543,7 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
                        recompute_attention: bool = True, recompute_ffn: bool = True,
                        recompute_qkv: bool = True, mn_major: bool = True, prefetch: int = 0,
                     recompute_norms: bool = True, bwd_prefetch: int = 0,
-                    fused_attention: bool = False) -> GraphBuilder:
+                    fused_attention: bool | None = None) -> GraphBuilder:
     """Config 4 over `dp` devices (data parallel): every memgraph
     device runs the full LoRA step on its own sequence (tokens/targets
     `@r`; the frozen weights and adapters are the same tensors on every device,
@@ -535,6 +552,8 @@ def llama_lora_step_dp(cfg: LlamaConfig, seq: int, dp: int, layers: int | None =
     gradient all-reduce as explicit Transfer vertices (NVLink peer copies)
     into `sum` combines, no NCCL. Outputs: the summed loss and gradients
     (same names as llama_lora_step's). Global batch = dp sequences."""
+    if fused_attention is None:
+        fused_attention = mn_major and cfg.hd == 128 and seq % 128 == 0
     g = GraphBuilder(device_count=dp)
     outs = [_lora_step_into(g, cfg, seq, layers, rank, rank_pad, lora_alpha, std, r, f"@{r}" if r else "",
                             recompute_attention, recompute_ffn, recompute_qkv, mn_major, prefetch,

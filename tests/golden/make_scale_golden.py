@@ -38,6 +38,8 @@ def cases():
          [16 * GIB], {"alloc_horizon": "lazy"}),
         ("lora7b_seq4096_cap16GiB_lazy_recompute", lambda: W.llama_lora_step(W.LLAMA_7B, 4096), [16 * GIB],
          {"alloc_horizon": "lazy"}),
+        ("lora7b_seq4096_cap12GiB_lazy_fused", lambda: W.llama_lora_step(W.LLAMA_7B, 4096), [12 * GIB],
+         {"alloc_horizon": "lazy"}),
         ("blockwise_seq65536_h32_tile4096_lag8_cap16GiB_lazy",
          lambda: W.blockwise_attention(65536, 32, 128, 4096, lag=8), [16 * GIB], {"alloc_horizon": "lazy"}),
         ("llama65b_tp8_seq8192_layers10_cap0.9GiB_lazy", lambda: W.llama_prefill_tp(W.LLAMA_65B, 8192, 8, layers=10),

@@ -311,15 +311,15 @@ def test_fused_attention_bwd_parity(seq, causal, sigma):
     for j, nm in enumerate(("dq", "dk", "dv")):
         e = rel_err(gg[:, j], gw[:, j])
         record_err("attention_bwd", seq=seq, causal=causal, sigma=sigma, part=nm, rel_err=e)
-        assert e < 2e-2, nm
+        assert e < 1.2e-2, nm  # measured <= 5.5e-3 (sigma 4), bf16 P / dS operands
     D = np.frombuffer(got[gr], np.float32, count=H * seq, offset=n * 2)
     Dw = np.frombuffer(want[gr], np.float32, count=H * seq, offset=n * 2)
-    assert rel_err(D, Dw) < 2e-3
+    assert rel_err(D, Dw) < 4e-3  # D = rowsum(dO*O): the GPU O and the oracle O differ by their bf16 rounding
     lse = np.frombuffer(got[oc], np.float32, count=H * seq, offset=seq * w * 2)
     lsew = np.frombuffer(want[oc], np.float32, count=H * seq, offset=seq * w * 2)
     e = float(np.max(np.abs(lse - lsew)))
     record_err("attention_lse", seq=seq, causal=causal, sigma=sigma, max_abs=e)
-    assert e < 2e-3
+    assert e < 2e-4  # measured <= 9.5e-5
 
 
 def test_unfused_attention_pipeline_matches_fused():
