@@ -118,10 +118,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const float* fixv = reinterpret_cast<const float*>(smem_raw + 2 * kTile);
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw + 3 * kStage);
     const std::uint32_t b0 = smem_u32(bars);
-    // fix_full | stg_full[2] | stg_empty[2] | s_full | p_full | ds_full | o_done
+    // fix_full | stg_full[2] | stg_empty[2] | s_full | p_full | ds_full | o_done | dp_full
     const std::uint32_t fix_full = b0, stg_full = b0 + 8, stg_empty = b0 + 24, s_full = b0 + 40, p_full = b0 + 48,
-                        ds_full = b0 + 56, o_done = b0 + 64;
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 9);
+                        ds_full = b0 + 56, o_done = b0 + 64, dp_full = b0 + 72;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 10);
 
     pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         mbar_init(p_full, 8);
         mbar_init(ds_full, 8);
         mbar_init(o_done, 1);
+        mbar_init(dp_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -197,51 +198,68 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     } else if (warp == 1) {  // whole warp: one elected lane issues
         const std::uint32_t id_kk = make_idesc(1u, kT, kT);              // both operands K-major
         const std::uint32_t id_mn = make_idesc(1u, kT, kHdB) | (1u << 16);  // B MN-major
+        // Issue order (KV role): S(0) dP(0) | dV(i) S(i+1) | dK(i) dP(i+1) | ...:
+        // S(i+1) overwrites Pᵀ(i) only after dV(i) read it (in-order pipe) and
+        // runs while the compute warps turn dP(i) into dS(i); dP(i+1) follows
+        // dK(i), which reads dSᵀ(i) from the same columns. The Q role keeps P
+        // in registers, so S(i+1) is issued once the warps consumed S(i).
+        auto stage_of = [&](int it) { return sStg + (it & 1) * kStage; };
+        auto wait_stage = [&](int it) {
+            mbar_wait(stg_full + 8 * (it & 1), (it >> 1) & 1);
+            tc_fence_after();
+        };
+        auto issue_s = [&](int it) {  // KV: Sᵀ = K_j Q_iᵀ; Q: S = Q_i K_jᵀ (fixed tile is A)
+            const std::uint32_t sb = stage_of(it);
+#pragma unroll
+            for (int kk = 0; kk < kHdB / 16; ++kk)
+                tc_mma(tS, sdesc(kmaj(sFix0, kk)), sdesc(kmaj(sb, kk)), id_kk, kk != 0, false);
+            tc_commit(s_full);
+        };
+        auto issue_dp = [&](int it) {  // KV: dPᵀ = V_j dO_iᵀ; Q: dP = dO_i V_jᵀ
+            const std::uint32_t sb = stage_of(it);
+#pragma unroll
+            for (int kk = 0; kk < kHdB / 16; ++kk)
+                tc_mma(tdP, sdesc(kmaj(sFix1, kk)), sdesc(kmaj(sb + kTile, kk)), id_kk, kk != 0, false);
+            tc_commit(dp_full);
+        };
         mbar_wait(fix_full, 0);
+        wait_stage(0);
+        issue_s(0);
+        issue_dp(0);
         for (int it = 0; it < n; ++it) {
             const int st = it & 1;
-            const std::uint32_t sb = sStg + st * kStage;
-            mbar_wait(stg_full + 8 * st, (it >> 1) & 1);
+            const std::uint32_t sb = stage_of(it);
+            const bool more = it + 1 < n;
+            mbar_wait(p_full, it & 1);  // KV: Pᵀ(i) in TMEM; Q: S(i) consumed
             tc_fence_after();
             if (!role_q) {
-                // Sᵀ = K_j Q_iᵀ, dPᵀ = V_j dO_iᵀ (M = keys, N = queries, K = hd)
-#pragma unroll
-                for (int kk = 0; kk < kHdB / 16; ++kk)
-                    tc_mma(tS, sdesc(kmaj(sFix0, kk)), sdesc(kmaj(sb, kk)), id_kk, kk != 0, false);
-#pragma unroll
-                for (int kk = 0; kk < kHdB / 16; ++kk)
-                    tc_mma(tdP, sdesc(kmaj(sFix1, kk)), sdesc(kmaj(sb + kTile, kk)), id_kk, kk != 0, false);
-                tc_commit(s_full);
-                mbar_wait(p_full, it & 1);
-                tc_fence_after();
                 // dV += Pᵀ dO_i (A = Pᵀ in TMEM, K = queries; B = dO_i MN-major)
 #pragma unroll
                 for (int kk = 0; kk < kT / 16; ++kk)
                     tc_mma_ts(tA0, tS + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kTile + kk * 2048), id_mn,
                               (it | kk) != 0);
-                mbar_wait(ds_full, it & 1);
-                tc_fence_after();
+            }
+            if (more) {
+                wait_stage(it + 1);
+                issue_s(it + 1);
+            }
+            mbar_wait(ds_full, it & 1);
+            tc_fence_after();
+            if (!role_q) {
                 // dK += dSᵀ Q_i (A = dSᵀ in TMEM; B = Q_i MN-major)
 #pragma unroll
                 for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA1, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn, (it | kk) != 0);
+                    tc_mma_ts(tA1, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn,
+                              (it | kk) != 0);
             } else {
-                // S = Q_i K_jᵀ, dP = dO_i V_jᵀ (M = queries, N = keys)
-#pragma unroll
-                for (int kk = 0; kk < kHdB / 16; ++kk)
-                    tc_mma(tS, sdesc(kmaj(sFix0, kk)), sdesc(kmaj(sb, kk)), id_kk, kk != 0, false);
-#pragma unroll
-                for (int kk = 0; kk < kHdB / 16; ++kk)
-                    tc_mma(tdP, sdesc(kmaj(sFix1, kk)), sdesc(kmaj(sb + kTile, kk)), id_kk, kk != 0, false);
-                tc_commit(s_full);
-                mbar_wait(ds_full, it & 1);
-                tc_fence_after();
                 // dQ += dS K_j (A = dS in TMEM, K = keys; B = K_j MN-major)
 #pragma unroll
                 for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA0, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn, (it | kk) != 0);
+                    tc_mma_ts(tA0, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn,
+                              (it | kk) != 0);
             }
             tc_commit(stg_empty + 8 * st);
+            if (more) issue_dp(it + 1);
         }
         tc_commit(o_done);
     } else {
@@ -287,6 +305,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full);
+                mbar_wait(dp_full, it & 1);
+                tc_fence_after();
 #pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 32) {
                     std::uint32_t u[32];
@@ -322,9 +342,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 tc_fence_after();
 #pragma unroll
                 for (int c0 = 0; c0 < 64; c0 += 32) {
-                    std::uint32_t us[32], ud[32];
+                    std::uint32_t us[32];
                     TN_LD32(tS + trow + c0, us);
-                    TN_LD32(tdP + trow + c0, ud);
                     tc_wait_ld();
 #pragma unroll
                     for (int cc = 0; cc < 32; cc += 2) {
@@ -335,7 +354,23 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                             if (c_lo + c > r) p0 = 0.f;
                             if (c_lo + c + 1 > r) p1 = 0.f;
                         }
-                        const float2 pp = unpack2(pack2(p0, p1));  // the bf16 P the KV role multiplies
+                        pk[c / 2] = pack2(p0, p1);  // the bf16 P the KV role multiplies
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full);  // S(i) consumed: S(i+1) may overwrite it
+                mbar_wait(dp_full, it & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 32) {
+                    std::uint32_t ud[32];
+                    TN_LD32(tdP + trow + c0, ud);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int cc = 0; cc < 32; cc += 2) {
+                        const int c = c0 + cc;
+                        const float2 pp = unpack2(pk[c / 2]);
                         pk[c / 2] = pack2(pp.x * (__uint_as_float(ud[cc]) - Dr), pp.y * (__uint_as_float(ud[cc + 1]) - Dr));
                     }
                 }
