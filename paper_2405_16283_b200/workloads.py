@@ -490,10 +490,12 @@ def llama_lora_step(cfg: LlamaConfig, seq: int, layers: int | None = None, rank:
     adapter. Adapters are stored zero-padded to `rank_pad` (the tensor-core
     K atom); padding rows/columns are exactly zero.
 
-    Backward GEMMs need transposed operands (dX = dY·W, dW = dYᵀ·X); they
-    are expressed as explicit `transpose` vertices feeding the K-major GEMM
-    task, and the attention backward as dP = dO·Vᵀ -> softmax_bwd ->
-    dQ = dS·K, dK = dSᵀ·Q, dV = Pᵀ·dO (materialised n² tiles).
+    Backward GEMMs need transposed operands (dX = dY·W, dW = dYᵀ·X): read in
+    place MN-major (`mn_major`, default) or, with mn_major=False, through
+    explicit `transpose` vertices. The attention backward is one fused
+    `attention_bwd` vertex (`fused_attention`, default) or, with
+    fused_attention=False, dP = dO·Vᵀ -> softmax_bwd -> dQ = dS·K,
+    dK = dSᵀ·Q, dV = Pᵀ·dO over materialised n² tiles.
 
     With `recompute_attention` (default; SURVEY §8d "fwd + bwd with
     recompute") the backward recomputes P = softmax(scale·QKᵀ) from the saved
