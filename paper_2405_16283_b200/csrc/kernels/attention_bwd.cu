@@ -9,7 +9,9 @@
 //   dP = dO Vᵀ,  dS = P ⊙ (dP − D),  D = rowsum(dO ⊙ O)     (D: attn_bwd_prep)
 //   dV = Pᵀ dO,  dK = scale · dSᵀ Q,  dQ = scale · dS K
 //
-// One launch, two CTA roles interleaved heaviest-first (blockIdx even / odd):
+// One launch, two CTA roles (blockIdx even / odd); a CTA runs two items of
+// its role and head, blocks b and nblk-1-b, so every CTA walks nblk+1 blocks
+// (causal), and CTAs go head-major for L2 reuse:
 //   role KV, per (head, 128-key block j): walks the query blocks i >= j with
 //     Sᵀ = K_j Q_iᵀ and dPᵀ = V_j dO_iᵀ (M = keys), writes Pᵀ / dSᵀ (bf16) over
 //     them in TMEM and accumulates dV += Pᵀ dO_i, dK += dSᵀ Q_i with the A
@@ -106,6 +108,25 @@ __device__ __forceinline__ void store_row(std::uint32_t taddr, __nv_bfloat16* ds
     }
 }
 
+// Work of one CTA: up to two items of its role and head, key (KV) or query
+// (Q) blocks tb and nblk-1-tb, so every CTA walks nblk+1 blocks (causal).
+struct Items {
+    int n_items, tb0, tb1;
+    __device__ __forceinline__ int tb(int k) const { return k == 0 ? tb0 : tb1; }
+};
+__device__ __forceinline__ Items cta_items(const BwdParams& p, int pr) {
+    Items it;
+    it.tb0 = pr;
+    it.tb1 = p.nblk - 1 - pr;
+    it.n_items = it.tb1 == it.tb0 ? 1 : 2;
+    return it;
+}
+// (first block walked, blocks walked) of item tb
+__device__ __forceinline__ void item_range(const BwdParams& p, bool role_q, int tb, int& first, int& n) {
+    first = role_q ? 0 : (p.causal ? tb : 0);
+    n = role_q ? (p.causal ? tb + 1 : p.nblk) : p.nblk - first;
+}
+
 __global__ void __launch_bounds__(kThreadsB, 1)
     attention_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                          const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
@@ -118,21 +139,21 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const float* fixv = reinterpret_cast<const float*>(smem_raw + 2 * kTile);
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem_raw + 3 * kStage);
     const std::uint32_t b0 = smem_u32(bars);
-    // fix_full | stg_full[2] | stg_empty[2] | s_full | p_full | ds_full | o_done | dp_full
+    // fix_full | stg_full[2] | stg_empty[2] | s_full | p_full | ds_full | o_done | dp_full | fix_empty | acc_empty
     const std::uint32_t fix_full = b0, stg_full = b0 + 8, stg_empty = b0 + 24, s_full = b0 + 40, p_full = b0 + 48,
-                        ds_full = b0 + 56, o_done = b0 + 64, dp_full = b0 + 72;
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 10);
+                        ds_full = b0 + 56, o_done = b0 + 64, dp_full = b0 + 72, fix_empty = b0 + 80,
+                        acc_empty = b0 + 88;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 12);
 
     pdl_trigger();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    // head-major order (all CTAs are equal work): the ~2 heads in flight keep
+    // their q, k, v, dO tiles (5 MB per head) L2-resident while every CTA of
+    // the head streams them
     const bool role_q = blockIdx.x & 1;
-    const int idx = blockIdx.x >> 1;
-    const int h = idx % p.heads, blk = idx / p.heads;
-    // role KV: key block j = blk (j = 0 walks the most query blocks);
-    // role Q: query block i = nblk-1-blk (the last walks the most key blocks)
-    const int tb = role_q ? p.nblk - 1 - blk : blk;
-    const int first = role_q ? 0 : (p.causal ? tb : 0);
-    const int n = role_q ? (p.causal ? tb + 1 : p.nblk) : p.nblk - first;
+    const int idx = blockIdx.x >> 1, npairs = (p.nblk + 1) / 2;
+    const int h = idx / npairs;
+    const Items items = cta_items(p, idx % npairs);
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&tq)) : "memory");
@@ -144,6 +165,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         mbar_init(ds_full, 8);
         mbar_init(o_done, 1);
         mbar_init(dp_full, 1);
+        mbar_init(fix_empty, 1);
+        mbar_init(acc_empty, 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
@@ -157,42 +180,48 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     if (warp == 0) {
         if (lane == 0) {
             const std::int64_t hs = static_cast<std::int64_t>(h) * p.seq;
-            if (!role_q) {  // fixed K_j, V_j; walked Q_i, dO_i, lse_i, D_i
-                mbar_expect_tx(fix_full, 2 * kTile);
-                tma_load_3d(sFix0, &tk, 0, tb * kT, h, fix_full);
-                tma_load_3d(sFix0 + kAtomB, &tk, 64, tb * kT, h, fix_full);
-                tma_load_3d(sFix1, &tv, 0, tb * kT, h, fix_full);
-                tma_load_3d(sFix1 + kAtomB, &tv, 64, tb * kT, h, fix_full);
-                for (int it = 0; it < n; ++it) {
-                    const int st = it & 1, i = first + it;
-                    mbar_wait(stg_empty + 8 * st, ((it >> 1) & 1) ^ 1);
-                    const std::uint32_t sb = sStg + st * kStage, fb = stg_full + 8 * st;
-                    mbar_expect_tx(fb, kStage);
-                    tma_load_3d(sb, &tq, 0, i * kT, h, fb);
-                    tma_load_3d(sb + kAtomB, &tq, 64, i * kT, h, fb);
-                    tma_load_3d(sb + kTile, &tdo, 0, i * kT, h, fb);
-                    tma_load_3d(sb + kTile + kAtomB, &tdo, 64, i * kT, h, fb);
-                    bulk_load(sb + 2 * kTile, p.lse + hs + i * kT, kVec, fb);
-                    bulk_load(sb + 2 * kTile + kVec, p.D + hs + i * kT, kVec, fb);
+            int g = 0;  // blocks walked by the previous items (stage ring position)
+            for (int k = 0; k < items.n_items; ++k) {
+                const int tb = items.tb(k);
+                int first, n;
+                item_range(p, role_q, tb, first, n);
+                if (k > 0) mbar_wait(fix_empty, (k - 1) & 1);  // the previous item's last MMAs are done
+                if (!role_q) {  // fixed K_j, V_j; walked Q_i, dO_i, lse_i, D_i
+                    mbar_expect_tx(fix_full, 2 * kTile);
+                    tma_load_3d(sFix0, &tk, 0, tb * kT, h, fix_full);
+                    tma_load_3d(sFix0 + kAtomB, &tk, 64, tb * kT, h, fix_full);
+                    tma_load_3d(sFix1, &tv, 0, tb * kT, h, fix_full);
+                    tma_load_3d(sFix1 + kAtomB, &tv, 64, tb * kT, h, fix_full);
+                } else {  // fixed Q_i, dO_i, lse_i, D_i; walked K_j, V_j
+                    mbar_expect_tx(fix_full, 2 * kTile + 2 * kVec);
+                    tma_load_3d(sFix0, &tq, 0, tb * kT, h, fix_full);
+                    tma_load_3d(sFix0 + kAtomB, &tq, 64, tb * kT, h, fix_full);
+                    tma_load_3d(sFix1, &tdo, 0, tb * kT, h, fix_full);
+                    tma_load_3d(sFix1 + kAtomB, &tdo, 64, tb * kT, h, fix_full);
+                    bulk_load(sFixV, p.lse + hs + tb * kT, kVec, fix_full);
+                    bulk_load(sFixV + kVec, p.D + hs + tb * kT, kVec, fix_full);
                 }
-            } else {  // fixed Q_i, dO_i, lse_i, D_i; walked K_j, V_j
-                mbar_expect_tx(fix_full, 2 * kTile + 2 * kVec);
-                tma_load_3d(sFix0, &tq, 0, tb * kT, h, fix_full);
-                tma_load_3d(sFix0 + kAtomB, &tq, 64, tb * kT, h, fix_full);
-                tma_load_3d(sFix1, &tdo, 0, tb * kT, h, fix_full);
-                tma_load_3d(sFix1 + kAtomB, &tdo, 64, tb * kT, h, fix_full);
-                bulk_load(sFixV, p.lse + hs + tb * kT, kVec, fix_full);
-                bulk_load(sFixV + kVec, p.D + hs + tb * kT, kVec, fix_full);
                 for (int it = 0; it < n; ++it) {
-                    const int st = it & 1, j = first + it;
-                    mbar_wait(stg_empty + 8 * st, ((it >> 1) & 1) ^ 1);
+                    const int gi = g + it, st = gi & 1, blk = first + it;
+                    mbar_wait(stg_empty + 8 * st, ((gi >> 1) & 1) ^ 1);
                     const std::uint32_t sb = sStg + st * kStage, fb = stg_full + 8 * st;
-                    mbar_expect_tx(fb, 2 * kTile);
-                    tma_load_3d(sb, &tk, 0, j * kT, h, fb);
-                    tma_load_3d(sb + kAtomB, &tk, 64, j * kT, h, fb);
-                    tma_load_3d(sb + kTile, &tv, 0, j * kT, h, fb);
-                    tma_load_3d(sb + kTile + kAtomB, &tv, 64, j * kT, h, fb);
+                    if (!role_q) {
+                        mbar_expect_tx(fb, kStage);
+                        tma_load_3d(sb, &tq, 0, blk * kT, h, fb);
+                        tma_load_3d(sb + kAtomB, &tq, 64, blk * kT, h, fb);
+                        tma_load_3d(sb + kTile, &tdo, 0, blk * kT, h, fb);
+                        tma_load_3d(sb + kTile + kAtomB, &tdo, 64, blk * kT, h, fb);
+                        bulk_load(sb + 2 * kTile, p.lse + hs + blk * kT, kVec, fb);
+                        bulk_load(sb + 2 * kTile + kVec, p.D + hs + blk * kT, kVec, fb);
+                    } else {
+                        mbar_expect_tx(fb, 2 * kTile);
+                        tma_load_3d(sb, &tk, 0, blk * kT, h, fb);
+                        tma_load_3d(sb + kAtomB, &tk, 64, blk * kT, h, fb);
+                        tma_load_3d(sb + kTile, &tv, 0, blk * kT, h, fb);
+                        tma_load_3d(sb + kTile + kAtomB, &tv, 64, blk * kT, h, fb);
+                    }
                 }
+                g += n;
             }
         }
     } else if (warp == 1) {  // whole warp: one elected lane issues
@@ -203,65 +232,76 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         // runs while the compute warps turn dP(i) into dS(i); dP(i+1) follows
         // dK(i), which reads dSᵀ(i) from the same columns. The Q role keeps P
         // in registers, so S(i+1) is issued once the warps consumed S(i).
-        auto stage_of = [&](int it) { return sStg + (it & 1) * kStage; };
-        auto wait_stage = [&](int it) {
-            mbar_wait(stg_full + 8 * (it & 1), (it >> 1) & 1);
+        auto stage_of = [&](int gi) { return sStg + (gi & 1) * kStage; };
+        auto wait_stage = [&](int gi) {
+            mbar_wait(stg_full + 8 * (gi & 1), (gi >> 1) & 1);
             tc_fence_after();
         };
-        auto issue_s = [&](int it) {  // KV: Sᵀ = K_j Q_iᵀ; Q: S = Q_i K_jᵀ (fixed tile is A)
-            const std::uint32_t sb = stage_of(it);
+        auto issue_s = [&](int gi) {  // KV: Sᵀ = K_j Q_iᵀ; Q: S = Q_i K_jᵀ (fixed tile is A)
+            const std::uint32_t sb = stage_of(gi);
 #pragma unroll
             for (int kk = 0; kk < kHdB / 16; ++kk)
                 tc_mma(tS, sdesc(kmaj(sFix0, kk)), sdesc(kmaj(sb, kk)), id_kk, kk != 0, false);
             tc_commit(s_full);
         };
-        auto issue_dp = [&](int it) {  // KV: dPᵀ = V_j dO_iᵀ; Q: dP = dO_i V_jᵀ
-            const std::uint32_t sb = stage_of(it);
+        auto issue_dp = [&](int gi) {  // KV: dPᵀ = V_j dO_iᵀ; Q: dP = dO_i V_jᵀ
+            const std::uint32_t sb = stage_of(gi);
 #pragma unroll
             for (int kk = 0; kk < kHdB / 16; ++kk)
                 tc_mma(tdP, sdesc(kmaj(sFix1, kk)), sdesc(kmaj(sb + kTile, kk)), id_kk, kk != 0, false);
             tc_commit(dp_full);
         };
-        mbar_wait(fix_full, 0);
-        wait_stage(0);
-        issue_s(0);
-        issue_dp(0);
-        for (int it = 0; it < n; ++it) {
-            const int st = it & 1;
-            const std::uint32_t sb = stage_of(it);
-            const bool more = it + 1 < n;
-            mbar_wait(p_full, it & 1);  // KV: Pᵀ(i) in TMEM; Q: S(i) consumed
-            tc_fence_after();
-            if (!role_q) {
-                // dV += Pᵀ dO_i (A = Pᵀ in TMEM, K = queries; B = dO_i MN-major)
+        int g = 0;
+        for (int k = 0; k < items.n_items; ++k) {
+            int first, n;
+            item_range(p, role_q, items.tb(k), first, n);
+            mbar_wait(fix_full, k & 1);
+            wait_stage(g);
+            issue_s(g);
+            issue_dp(g);
+            for (int it = 0; it < n; ++it) {
+                const int gi = g + it;
+                const std::uint32_t sb = stage_of(gi);
+                const bool more = it + 1 < n;
+                mbar_wait(p_full, gi & 1);  // KV: Pᵀ(i) in TMEM; Q: S(i) consumed
+                tc_fence_after();
+                if (it == 0 && k > 0) {  // the previous item's accumulators were read out
+                    mbar_wait(acc_empty, (k - 1) & 1);
+                    tc_fence_after();
+                }
+                if (!role_q) {
+                    // dV += Pᵀ dO_i (A = Pᵀ in TMEM, K = queries; B = dO_i MN-major)
 #pragma unroll
-                for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA0, tS + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kTile + kk * 2048), id_mn,
-                              (it | kk) != 0);
-            }
-            if (more) {
-                wait_stage(it + 1);
-                issue_s(it + 1);
-            }
-            mbar_wait(ds_full, it & 1);
-            tc_fence_after();
-            if (!role_q) {
-                // dK += dSᵀ Q_i (A = dSᵀ in TMEM; B = Q_i MN-major)
+                    for (int kk = 0; kk < kT / 16; ++kk)
+                        tc_mma_ts(tA0, tS + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kTile + kk * 2048),
+                                  id_mn, (it | kk) != 0);
+                }
+                if (more) {
+                    wait_stage(gi + 1);
+                    issue_s(gi + 1);
+                }
+                mbar_wait(ds_full, gi & 1);
+                tc_fence_after();
+                if (!role_q) {
+                    // dK += dSᵀ Q_i (A = dSᵀ in TMEM; B = Q_i MN-major)
 #pragma unroll
-                for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA1, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn,
-                              (it | kk) != 0);
-            } else {
-                // dQ += dS K_j (A = dS in TMEM, K = keys; B = K_j MN-major)
+                    for (int kk = 0; kk < kT / 16; ++kk)
+                        tc_mma_ts(tA1, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn,
+                                  (it | kk) != 0);
+                } else {
+                    // dQ += dS K_j (A = dS in TMEM, K = keys; B = K_j MN-major)
 #pragma unroll
-                for (int kk = 0; kk < kT / 16; ++kk)
-                    tc_mma_ts(tA0, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn,
-                              (it | kk) != 0);
+                    for (int kk = 0; kk < kT / 16; ++kk)
+                        tc_mma_ts(tA0, tdP + (kk >> 2) * 64 + (kk & 3) * 8, sdesc_mn16(sb + kk * 2048), id_mn,
+                                  (it | kk) != 0);
+                }
+                tc_commit(stg_empty + 8 * (gi & 1));
+                if (more) issue_dp(gi + 1);
             }
-            tc_commit(stg_empty + 8 * st);
-            if (more) issue_dp(it + 1);
+            tc_commit(fix_empty);
+            tc_commit(o_done);
+            g += n;
         }
-        tc_commit(o_done);
     } else {
         // two warps per TMEM lane quadrant: warp w owns rows 32*(w%4).. and
         // the 64 columns [64*hf, +64) of them; its bf16 P / dS pairs go to the
@@ -274,116 +314,127 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         constexpr float kLog2e = 1.4426950408889634f;
         const float sl2 = p.scale_log2;
         std::uint32_t pk[32];
-        if (!role_q) {
-            for (int it = 0; it < n; ++it) {
-                const int st = it & 1, i = first + it;
-                const float* lse = reinterpret_cast<const float*>(smem_raw + kStage * (1 + st) + 2 * kTile) + c_lo;
-                const float* Dv = lse + kT;
-                const bool diag = p.causal && i == tb;  // key r > query c is masked
-                mbar_wait(s_full, it & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 32) {
-                    std::uint32_t u[32];
-                    TN_LD32(tS + trow + c0, u);
-                    tc_wait_ld();
-#pragma unroll
-                    for (int cc = 0; cc < 32; cc += 2) {
-                        const int c = c0 + cc;
-                        float x0 = fmaf(__uint_as_float(u[cc]), sl2, -lse[c] * kLog2e);
-                        float x1 = fmaf(__uint_as_float(u[cc + 1]), sl2, -lse[c + 1] * kLog2e);
-                        float p0 = ex2(x0), p1 = ex2(x1);
-                        if (diag) {
-                            if (r > c_lo + c) p0 = 0.f;
-                            if (r > c_lo + c + 1) p1 = 0.f;
-                        }
-                        pk[c / 2] = pack2(p0, p1);
-                    }
-                }
-                TN_ST32(tS + trow, pk);  // Pᵀ (bf16 pairs) over Sᵀ
-                tc_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(p_full);
-                mbar_wait(dp_full, it & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 32) {
-                    std::uint32_t u[32];
-                    TN_LD32(tdP + trow + c0, u);
-                    tc_wait_ld();
-#pragma unroll
-                    for (int cc = 0; cc < 32; cc += 2) {
-                        const int c = c0 + cc;
-                        const float2 pp = unpack2(pk[c / 2]);
-                        pk[c / 2] = pack2(pp.x * (__uint_as_float(u[cc]) - Dv[c]),
-                                          pp.y * (__uint_as_float(u[cc + 1]) - Dv[c + 1]));
-                    }
-                }
-                TN_ST32(tdP + trow, pk);  // dSᵀ over dPᵀ
-                tc_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(ds_full);
-            }
-            mbar_wait(o_done, 0);
-            tc_fence_after();
+        int g = 0;
+        for (int k = 0; k < items.n_items; ++k) {
+            const int tb = items.tb(k);
+            int first, n;
+            item_range(p, role_q, tb, first, n);
             const std::int64_t row = static_cast<std::int64_t>(tb) * kT + r;
             const std::int64_t col = static_cast<std::int64_t>(h) * kHdB + c_lo;
-            store_row(tA0 + trow, p.dv + row * p.ldg + col, 1.0f);
-            store_row(tA1 + trow, p.dk + row * p.ldg + col, p.scale);
-        } else {
-            mbar_wait(fix_full, 0);  // lse_i, D_i staged with Q_i
-            const float lse2 = fixv[r] * kLog2e, Dr = fixv[kT + r];
-            for (int it = 0; it < n; ++it) {
-                const int j = first + it;
-                const bool diag = p.causal && j == tb;  // key c > query r is masked
-                mbar_wait(s_full, it & 1);
-                tc_fence_after();
+            if (!role_q) {
+                for (int it = 0; it < n; ++it) {
+                    const int gi = g + it, i = first + it;
+                    const float* lse =
+                        reinterpret_cast<const float*>(smem_raw + kStage * (1 + (gi & 1)) + 2 * kTile) + c_lo;
+                    const float* Dv = lse + kT;
+                    const bool diag = p.causal && i == tb;  // key r > query c is masked
+                    mbar_wait(s_full, gi & 1);
+                    tc_fence_after();
 #pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 32) {
-                    std::uint32_t us[32];
-                    TN_LD32(tS + trow + c0, us);
-                    tc_wait_ld();
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        std::uint32_t u[32];
+                        TN_LD32(tS + trow + c0, u);
+                        tc_wait_ld();
 #pragma unroll
-                    for (int cc = 0; cc < 32; cc += 2) {
-                        const int c = c0 + cc;
-                        float p0 = ex2(fmaf(__uint_as_float(us[cc]), sl2, -lse2));
-                        float p1 = ex2(fmaf(__uint_as_float(us[cc + 1]), sl2, -lse2));
-                        if (diag) {
-                            if (c_lo + c > r) p0 = 0.f;
-                            if (c_lo + c + 1 > r) p1 = 0.f;
+                        for (int cc = 0; cc < 32; cc += 2) {
+                            const int c = c0 + cc;
+                            float x0 = fmaf(__uint_as_float(u[cc]), sl2, -lse[c] * kLog2e);
+                            float x1 = fmaf(__uint_as_float(u[cc + 1]), sl2, -lse[c + 1] * kLog2e);
+                            float p0 = ex2(x0), p1 = ex2(x1);
+                            if (diag) {
+                                if (r > c_lo + c) p0 = 0.f;
+                                if (r > c_lo + c + 1) p1 = 0.f;
+                            }
+                            pk[c / 2] = pack2(p0, p1);
                         }
-                        pk[c / 2] = pack2(p0, p1);  // the bf16 P the KV role multiplies
                     }
+                    TN_ST32(tS + trow, pk);  // Pᵀ (bf16 pairs) over Sᵀ
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(p_full);
+                    mbar_wait(dp_full, gi & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        std::uint32_t u[32];
+                        TN_LD32(tdP + trow + c0, u);
+                        tc_wait_ld();
+#pragma unroll
+                        for (int cc = 0; cc < 32; cc += 2) {
+                            const int c = c0 + cc;
+                            const float2 pp = unpack2(pk[c / 2]);
+                            pk[c / 2] = pack2(pp.x * (__uint_as_float(u[cc]) - Dv[c]),
+                                              pp.y * (__uint_as_float(u[cc + 1]) - Dv[c + 1]));
+                        }
+                    }
+                    TN_ST32(tdP + trow, pk);  // dSᵀ over dPᵀ
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(ds_full);
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(p_full);  // S(i) consumed: S(i+1) may overwrite it
-                mbar_wait(dp_full, it & 1);
+                mbar_wait(o_done, k & 1);
                 tc_fence_after();
+                store_row(tA0 + trow, p.dv + row * p.ldg + col, 1.0f);
+                store_row(tA1 + trow, p.dk + row * p.ldg + col, p.scale);
+            } else {
+                mbar_wait(fix_full, k & 1);  // lse_i, D_i staged with Q_i
+                const float lse2 = fixv[r] * kLog2e, Dr = fixv[kT + r];
+                for (int it = 0; it < n; ++it) {
+                    const int gi = g + it, j = first + it;
+                    const bool diag = p.causal && j == tb;  // key c > query r is masked
+                    mbar_wait(s_full, gi & 1);
+                    tc_fence_after();
 #pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 32) {
-                    std::uint32_t ud[32];
-                    TN_LD32(tdP + trow + c0, ud);
-                    tc_wait_ld();
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        std::uint32_t us[32];
+                        TN_LD32(tS + trow + c0, us);
+                        tc_wait_ld();
 #pragma unroll
-                    for (int cc = 0; cc < 32; cc += 2) {
-                        const int c = c0 + cc;
-                        const float2 pp = unpack2(pk[c / 2]);
-                        pk[c / 2] = pack2(pp.x * (__uint_as_float(ud[cc]) - Dr), pp.y * (__uint_as_float(ud[cc + 1]) - Dr));
+                        for (int cc = 0; cc < 32; cc += 2) {
+                            const int c = c0 + cc;
+                            float p0 = ex2(fmaf(__uint_as_float(us[cc]), sl2, -lse2));
+                            float p1 = ex2(fmaf(__uint_as_float(us[cc + 1]), sl2, -lse2));
+                            if (diag) {
+                                if (c_lo + c > r) p0 = 0.f;
+                                if (c_lo + c + 1 > r) p1 = 0.f;
+                            }
+                            pk[c / 2] = pack2(p0, p1);  // the bf16 P the KV role multiplies
+                        }
                     }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(p_full);  // S(i) consumed: S(i+1) may overwrite it
+                    mbar_wait(dp_full, gi & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        std::uint32_t ud[32];
+                        TN_LD32(tdP + trow + c0, ud);
+                        tc_wait_ld();
+#pragma unroll
+                        for (int cc = 0; cc < 32; cc += 2) {
+                            const int c = c0 + cc;
+                            const float2 pp = unpack2(pk[c / 2]);
+                            pk[c / 2] = pack2(pp.x * (__uint_as_float(ud[cc]) - Dr),
+                                              pp.y * (__uint_as_float(ud[cc + 1]) - Dr));
+                        }
+                    }
+                    TN_ST32(tdP + trow, pk);  // dS over dP
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(ds_full);
                 }
-                TN_ST32(tdP + trow, pk);  // dS over dP
-                tc_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(ds_full);
+                mbar_wait(o_done, k & 1);
+                tc_fence_after();
+                store_row(tA0 + trow, p.dq + row * p.ldg + col, p.scale);
             }
-            mbar_wait(o_done, 0);
-            tc_fence_after();
-            const std::int64_t row = static_cast<std::int64_t>(tb) * kT + r;
-            store_row(tA0 + trow, p.dq + row * p.ldg + static_cast<std::int64_t>(h) * kHdB + c_lo, p.scale);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);  // accumulators read: the next item may overwrite
+            g += n;
         }
     }
     tc_fence_before();
@@ -459,7 +510,7 @@ cudaError_t attention_bwd_launch(const AttnBwdPlan& plan, cudaStream_t s) {
     p.causal = a.causal;
     p.scale = a.scale;
     p.scale_log2 = a.scale * 1.4426950408889634f;
-    const unsigned grid = static_cast<unsigned>(2 * a.heads * p.nblk);
+    const unsigned grid = static_cast<unsigned>(2 * a.heads * ((p.nblk + 1) / 2));
     return launch_pdl(attention_bwd_kernel, dim3(grid), dim3(kThreadsB), kSmemB, s, plan.tq, plan.tk, plan.tv,
                       plan.tdo, p);
 }
