@@ -114,6 +114,10 @@ int tn_make_fixed_order(const char* memgraph_json, char** memgraph_out, char** e
  *                                   memgraph as one CUDA graph (a node per vertex, dependencies =
  *                                   memgraph edges: the GPU dispatches each vertex when its
  *                                   predecessors finished); traced runs use the host loop
+ *   "tie_break": "plan-order"       ready-list order when tn_exec_run names none: "plan-order" (the
+ *                                   memgraph's total order: each copy engine takes the tensor the plan
+ *                                   needs soonest) | "fifo" (reference default) | "lowest-id" |
+ *                                   "seeded-random"
  *   "elide_input_offloads": true    an evicted input is reloaded from its own copy, never offloaded
  *   "materialize_inputs": true, "timeout_s": 600 */
 int tn_exec_create(const char* memgraph_json, const char* taskgraph_json, const char* config_json,
