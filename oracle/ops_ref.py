@@ -282,6 +282,11 @@ def op_attention_bwd(op, args, out):
         G[:, 2, h, :] = P.T @ dOh
 
     list(_pool().map(one, range(H)))
+    if len(args) == 6:  # pre-RoPE dq, dk: rotate-half by -theta at each position (op_rope "inverse")
+        tab = load(args[5], "f32", S * (hd // 2) * 2).reshape(S, hd // 2, 2)
+        c, sn = tab[:, None, None, :, 0], tab[:, None, None, :, 1]
+        a, b = G[:, :2, :, : hd // 2], G[:, :2, :, hd // 2:]
+        G[:, :2] = np.concatenate([a * c + b * sn, b * c - a * sn], axis=-1)
     store(out, "bf16", G.reshape(-1))
     store(out, "f32", D, S * 3 * w // 2)
 

@@ -696,7 +696,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             break;
         }
         case OpType::AttentionBwd: {
-            need_args(5, 5);
+            need_args(5, 6);
             if (op.hd != 128 || op.seq <= 0 || op.seq % 128 != 0 || op.heads <= 0)
                 throw Error("kernel " + std::to_string(v.id) + " (attention_bwd): needs hd 128 and seq % 128 == 0");
             const std::int64_t sec = op.heads * op.seq * op.hd, w = op.heads * op.hd;
@@ -707,6 +707,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             fits(op.seq * ldo * 2 + op.heads * op.seq * 4, arg_bytes[3], "o_lse");
             fits(((op.seq - 1) * dld + w) * 2, arg_bytes[4], "dO");
             fits(op.seq * 3 * w * 2 + op.heads * op.seq * 4, out_bytes, "out (dq|dk|dv + D)");
+            if (op.args.size() == 6) fits(op.seq * op.hd * 4, arg_bytes[5], "rope table");
             k::AttnBwdArgs ab;
             ab.q = in.argp[0] + op.q_off * 2;
             ab.k = in.argp[1] + op.k_off * 2;
@@ -722,6 +723,7 @@ void Executor::Impl::prepare_kernel(Instr& in, const MemVertex& v,
             ab.dv = in.dst + 2 * w * 2;
             ab.ldg = 3 * w;
             ab.D = reinterpret_cast<float*>(in.dst + op.seq * 3 * w * 2);
+            if (op.args.size() == 6) ab.rope = reinterpret_cast<const float*>(in.argp[5]);
             ab.heads = static_cast<int>(op.heads);
             ab.seq = static_cast<int>(op.seq);
             ab.hd = static_cast<int>(op.hd);

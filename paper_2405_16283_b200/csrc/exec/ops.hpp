@@ -35,10 +35,12 @@
 //    "causal", "lse": 0|1}   q,k [H,seq,hd], vt [H,hd,seq] -> out [seq, ldo] (head h at col h*hd);
 //    lse 1: followed (byte offset seq*ldo*2) by the f32 [H, seq] natural-log logsumexp of each
 //    scaled score row
-//   {"type": "attention_bwd", "args": [q, k, v, o_lse, dO], "heads", "seq", "hd", "scale", "causal",
+//   {"type": "attention_bwd", "args": [q, k, v, o_lse, dO (, rope_table)], "heads", "seq", "hd", "scale", "causal",
 //    "q_off", "k_off", "v_off", "v_ld", "ldo", "do_ld"}   q,k [H,seq,hd]; v [seq, v_ld] from v_off
 //    (head h at col h*hd); o_lse = an attention output with lse 1 (pitch ldo); dO [seq, do_ld] ->
-//    out [seq, 3*H*hd] = [dq | dk | dv] (bf16), then f32 [H, seq] D = rowsum(dO*O) (scratch)
+//    out [seq, 3*H*hd] = [dq | dk | dv] (bf16), then f32 [H, seq] D = rowsum(dO*O) (scratch);
+//    with a rope_table [seq, hd/2, (cos, sin)] dq and dk are the pre-RoPE gradients (rotate-half,
+//    rotation by -theta, like rope "inverse": 1)
 //   {"type": "rowstats", "args": [S], "rows", "cols", "causal"}      bf16 S -> f32 (m,l) rows
 //   {"type": "stats_combine", "args": [st0, st1, ...], "rows"}        fold (m,l) in arg order
 //   {"type": "softmax_apply", "args": [S, st], "rows", "cols", "causal"}  P = exp(S-m)/l, bf16

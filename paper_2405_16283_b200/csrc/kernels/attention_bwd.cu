@@ -55,6 +55,7 @@ struct BwdParams {
     std::int64_t ldg;  // row pitch (elements) of dq / dk / dv
     const float* lse;  // [heads][seq], natural log
     const float* D;    // [heads][seq]
+    const float* rope; // optional [seq][hd/2][cos, sin]: dq, dk leave inverse-rotated (pre-RoPE gradients)
     int heads, seq, nblk, causal;
     float scale, scale_log2;
 };
@@ -87,6 +88,33 @@ __device__ __forceinline__ std::uint32_t pack2(float a, float b) {
 __device__ __forceinline__ float2 unpack2(std::uint32_t u) {
     __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
     return __bfloat1622float2(v);
+}
+// The pre-RoPE gradient of one row (rotate-half RoPE, rotation by -theta):
+// pairs i in [i0, i0+32) of the 128-column accumulator at taddr (lane = row),
+// a = col i, b = col 64+i: dst[i] = (a cos + b sin) * mul, dst[64+i] = (b cos - a sin) * mul.
+__device__ __forceinline__ void store_row_rope(std::uint32_t taddr, __nv_bfloat16* dst, float mul,
+                                               const float* tab_row, int i0) {
+    std::uint32_t ua[32], ub[32];
+    TN_LD32(taddr + i0, ua);
+    TN_LD32(taddr + 64 + i0, ub);
+    tc_wait_ld();
+    const float4* cs = reinterpret_cast<const float4*>(tab_row + 2 * i0);  // (cos, sin) pairs
+    std::uint32_t ya[16], yb[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const float4 t = __ldg(cs + q);  // pairs i0+2q, i0+2q+1
+        const float a0 = __uint_as_float(ua[2 * q]), a1 = __uint_as_float(ua[2 * q + 1]);
+        const float b0 = __uint_as_float(ub[2 * q]), b1 = __uint_as_float(ub[2 * q + 1]);
+        ya[q] = pack2((a0 * t.x + b0 * t.y) * mul, (a1 * t.z + b1 * t.w) * mul);
+        yb[q] = pack2((b0 * t.x - a0 * t.y) * mul, (b1 * t.z - a1 * t.w) * mul);
+    }
+    uint4* da = reinterpret_cast<uint4*>(dst + i0);
+    uint4* db = reinterpret_cast<uint4*>(dst + 64 + i0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        da[q] = make_uint4(ya[4 * q], ya[4 * q + 1], ya[4 * q + 2], ya[4 * q + 3]);
+        db[q] = make_uint4(yb[4 * q], yb[4 * q + 1], yb[4 * q + 2], yb[4 * q + 3]);
+    }
 }
 // 64 fp32 TMEM columns of this thread's lane -> bf16 at dst, times mul.
 __device__ __forceinline__ void store_row(std::uint32_t taddr, __nv_bfloat16* dst, float mul) {
@@ -377,7 +405,11 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 mbar_wait(o_done, k & 1);
                 tc_fence_after();
                 store_row(tA0 + trow, p.dv + row * p.ldg + col, 1.0f);
-                store_row(tA1 + trow, p.dk + row * p.ldg + col, p.scale);
+                if (p.rope)  // warp half hf takes RoPE pairs [32 hf, +32) of the whole row
+                    store_row_rope(tA1 + trow - c_lo, p.dk + row * p.ldg + static_cast<std::int64_t>(h) * kHdB,
+                                   p.scale, p.rope + row * kHdB, 32 * hf);
+                else
+                    store_row(tA1 + trow, p.dk + row * p.ldg + col, p.scale);
             } else {
                 mbar_wait(fix_full, k & 1);  // lse_i, D_i staged with Q_i
                 const float lse2 = fixv[r] * kLog2e, Dr = fixv[kT + r];
@@ -429,7 +461,11 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                 }
                 mbar_wait(o_done, k & 1);
                 tc_fence_after();
-                store_row(tA0 + trow, p.dq + row * p.ldg + col, p.scale);
+                if (p.rope)
+                    store_row_rope(tA0 + trow - c_lo, p.dq + row * p.ldg + static_cast<std::int64_t>(h) * kHdB,
+                                   p.scale, p.rope + row * kHdB, 32 * hf);
+                else
+                    store_row(tA0 + trow, p.dq + row * p.ldg + col, p.scale);
             }
             tc_fence_before();
             __syncwarp();
@@ -470,7 +506,7 @@ cudaError_t attention_bwd_prepare(const AttnBwdArgs& a, AttnBwdPlan* plan) {
     plan->args = a;
     auto al16 = [](const void* x) { return (reinterpret_cast<std::uintptr_t>(x) & 15) == 0; };
     const bool ok = a.hd == kHdB && a.seq % kT == 0 && a.seq >= kT && al16(a.q) && al16(a.k) && al16(a.v) &&
-                    al16(a.dout) && al16(a.dq) && al16(a.dk) && al16(a.dv) && al16(a.lse) && al16(a.D) &&
+                    al16(a.dout) && al16(a.dq) && al16(a.dk) && al16(a.dv) && al16(a.lse) && al16(a.D) && al16(a.rope) &&
                     (a.ldv * 2) % 16 == 0 && (a.lddo * 2) % 16 == 0 && (a.ldg * 2) % 16 == 0 && a.o && a.lse;
     if (!ok) return cudaErrorInvalidValue;
     const std::int64_t shd = static_cast<std::int64_t>(a.seq) * a.hd;
@@ -504,6 +540,7 @@ cudaError_t attention_bwd_launch(const AttnBwdPlan& plan, cudaStream_t s) {
     p.ldg = a.ldg;
     p.lse = a.lse;
     p.D = a.D;
+    p.rope = a.rope;
     p.heads = a.heads;
     p.seq = a.seq;
     p.nblk = a.seq / kT;

@@ -140,6 +140,7 @@ struct AttnBwdArgs {
     std::int64_t ldv = 0, ldo = 0, lddo = 0;
     const float* lse = nullptr;
     float* D = nullptr;
+    const float* rope = nullptr;  // optional [seq][hd/2][cos, sin]: dq, dk inverse-rotated in the epilogue
     void *dq = nullptr, *dk = nullptr, *dv = nullptr;
     std::int64_t ldg = 0;
     int heads = 0, seq = 0, hd = 0;

@@ -138,6 +138,37 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
     }
 }
 
+// Same, 8 columns per thread with 16-byte loads / stores (cols % 8 == 0,
+// 16-byte aligned rows): per element the scalar kernel's arithmetic.
+__global__ void swiglu_bwd_vec(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ da,
+                               __nv_bfloat16* __restrict__ dgu, int rows, int cols) {
+    const int nv = cols / 8;
+    const std::int64_t total = static_cast<std::int64_t>(rows) * nv;
+    for (std::int64_t w = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+        const std::int64_t r = w / nv, c = w % nv;
+        const uint4* row = reinterpret_cast<const uint4*>(gu + r * 2 * cols);
+        const uint4 gv = __ldcs(row + c), uv = __ldcs(row + nv + c), dv = __ldcs(reinterpret_cast<const uint4*>(da) + w);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+        const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+        uint4 og, ou;
+        __nv_bfloat162* og2 = reinterpret_cast<__nv_bfloat162*>(&og);
+        __nv_bfloat162* ou2 = reinterpret_cast<__nv_bfloat162*>(&ou);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 g = __bfloat1622float2(g2[j]), u = __bfloat1622float2(u2[j]), d = __bfloat1622float2(d2[j]);
+            const float s0 = 1.0f / (1.0f + __expf(-g.x)), s1 = 1.0f / (1.0f + __expf(-g.y));
+            og2[j] = __floats2bfloat162_rn(d.x * u.x * s0 * (1.0f + g.x * (1.0f - s0)),
+                                           d.y * u.y * s1 * (1.0f + g.y * (1.0f - s1)));
+            ou2[j] = __floats2bfloat162_rn(d.x * g.x * s0, d.y * g.y * s1);
+        }
+        uint4* orow = reinterpret_cast<uint4*>(dgu + r * 2 * cols);
+        orow[c] = og;
+        orow[nv + c] = ou;
+    }
+}
+
 // dS = P * (dP - sum_j P_j dP_j) per row; masked (causal) entries are 0.
 __global__ void __launch_bounds__(kT) softmax_bwd_kernel(const __nv_bfloat16* __restrict__ P, const void* __restrict__ dP,
                                                          int dp_dt, __nv_bfloat16* __restrict__ dS, int rows, int cols,
@@ -223,6 +254,13 @@ cudaError_t rmsnorm_bwd(const void* x, const void* w, const void* dy, void* dx, 
 }
 
 cudaError_t swiglu_bwd(const void* gu, const void* da, void* dgu, int rows, int cols, cudaStream_t s) {
+    auto al16 = [](const void* x) { return (reinterpret_cast<std::uintptr_t>(x) & 15) == 0; };
+    if (cols % 8 == 0 && al16(gu) && al16(da) && al16(dgu)) {
+        swiglu_bwd_vec<<<grid_for(static_cast<std::int64_t>(rows) * (cols / 8)), kT, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(gu), static_cast<const __nv_bfloat16*>(da),
+            static_cast<__nv_bfloat16*>(dgu), rows, cols);
+        return cudaGetLastError();
+    }
     swiglu_bwd_kernel<<<grid_for(static_cast<std::int64_t>(rows) * cols), kT, 0, s>>>(
         static_cast<const __nv_bfloat16*>(gu), static_cast<const __nv_bfloat16*>(da), static_cast<__nv_bfloat16*>(dgu),
         rows, cols);

@@ -820,23 +820,28 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
                                              "seq": S, "hd": hd, "ldo": d, "scale": scale, "causal": 1, "lse": 1},
                              (S * d + 2 * H * S,), "bf16", dev, cost=attn_flops / _PEAK_FLOPS)
             g.flops += attn_flops
-            dqkv = g.kernel(p + "d_attn_qkv", {"type": "attention_bwd", "args": [a["q"], a["k"], a["qkv"], o_lse, do],
+            # dqkv = [dq | dk | dv] rows of 3d, dq and dk already rotated back (pre-RoPE)
+            dqkv = g.kernel(p + "d_attn_qkv", {"type": "attention_bwd",
+                                                "args": [a["q"], a["k"], a["qkv"], o_lse, do, rope_tab],
                                                 "heads": H, "seq": S, "hd": hd, "scale": scale, "causal": 1,
                                                 "v_off": 2 * d, "v_ld": 3 * d, "ldo": d, "do_ld": d},
                             (S * 3 * d + 2 * H * S,), "bf16", dev, cost=2.5 * attn_flops / _PEAK_FLOPS)
             g.flops += 2.5 * attn_flops
-            dq = g.kernel(p + "d_q", {"type": "rope", "args": [dqkv, rope_tab], "seq": S, "ld": 3 * d, "col_off": 0,
-                                      "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d), "bf16", dev)
-            dk = g.kernel(p + "d_k", {"type": "rope", "args": [dqkv, rope_tab], "seq": S, "ld": 3 * d,
-                                      "col_off": d, "heads": H, "hd": hd, "inverse": 1, "tokens_out": 1}, (S, d),
-                          "bf16", dev)
-            parts = ((dq, None, None), (dk, None, None), (dqkv, 2 * d, 3 * d))  # (tensor, a_off, lda)
+            parts = None
         else:
             dq, dk, parts = attention_grads(p, a, do)
         # qkv = h·Wqkvᵀ + s·U1·B1ᵀ with dqkv = [dq | dk | dv]
         V1 = None
         dBs = []
-        if mn_major:  # B1 [3d, R] (part j: rows j*d..), U1 [S, R], dq/dk/dv [S, d], h [S, d], V1 [S, R]
+        if parts is None:  # one [S, 3d] gradient: each product over all of q|k|v at once
+            V1 = g.gemm(p + "lora_qkv.V", dqkv, w["B1"], S, R, 3 * d, ldb=R, b_major="mn", out_shape=(S, R),
+                        device=dev)
+            results[p + "lora_qkv.dB"] = g.gemm(p + "lora_qkv.dB", dqkv, a["U1"], 3 * d, R, S, alpha=sc,
+                                                a_major="mn", lda=3 * d, b_major="mn", out_shape=(3 * d, R),
+                                                device=dev)
+            dA1T = g.gemm(p + "lora_qkv.dA.T", a["h"], V1, d, R, S, alpha=sc, a_major="mn", b_major="mn",
+                          out_shape=(d, R), device=dev)
+        elif mn_major:  # B1 [3d, R] (part j: rows j*d..), U1 [S, R], dq/dk/dv [S, d], h [S, d], V1 [S, R]
             for j, (dpart, off, ld) in enumerate(parts):
                 V1 = g.gemm(p + f"lora_qkv.V{j}", dpart, w["B1"], S, R, d, ldb=R, b_off=j * d * R, r=V1,
                             b_major="mn", a_off=off, lda=ld, out_shape=(S, R), device=dev)
@@ -863,7 +868,12 @@ def _lora_step_into(g: GraphBuilder, cfg: LlamaConfig, seq: int, layers, rank, r
         if l == 0:
             break  # no gradient is needed below the first layer
         dh = None
-        if mn_major:  # Wqkv [3d, d] (part j: rows j*d..), A1 [R, d]
+        if parts is None:
+            dh = g.gemm(p + "d_attn_norm_out_base", dqkv, w["wqkv"], S, d, 3 * d, ldb=d, b_major="mn",
+                        out_shape=(S, d), device=dev)
+            dh = g.gemm(p + "d_attn_norm_out", V1, w["A1"], S, d, R, r=dh, alpha=sc, b_major="mn",
+                        out_shape=(S, d), device=dev)
+        elif mn_major:  # Wqkv [3d, d] (part j: rows j*d..), A1 [R, d]
             for j, (dpart, off, ld) in enumerate(parts):
                 dh = g.gemm(p + f"d_attn_norm_out{j}", dpart, w["wqkv"], S, d, d, ldb=d, b_off=j * d * d, r=dh,
                             b_major="mn", a_off=off, lda=ld, out_shape=(S, d), device=dev)

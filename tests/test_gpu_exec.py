@@ -267,7 +267,7 @@ def test_fused_attention_parity(seq, hd, causal, sigma):
     assert _e < 5e-3
 
 
-def _attn_bwd_graph(seq, causal, sigma, H=2, hd=128):
+def _attn_bwd_graph(seq, causal, sigma, H=2, hd=128, rope=False):
     """q, k, qkv (v in its last third), dO -> fused forward with the row
     logsumexp -> fused backward; both vertices are graph outputs."""
     w = H * hd
@@ -280,21 +280,25 @@ def _attn_bwd_graph(seq, causal, sigma, H=2, hd=128):
                          "heads": H, "hd": hd}, (H, hd, seq), "bf16")
     o = g.kernel("o", {"type": "attention", "args": [q, k, vt], "heads": H, "seq": seq, "hd": hd, "ldo": w,
                        "scale": hd ** -0.5, "causal": causal, "lse": 1}, (seq * w + 2 * H * seq,), "bf16")
-    gr = g.kernel("grad", {"type": "attention_bwd", "args": [q, k, qkv, o, dout], "heads": H, "seq": seq, "hd": hd,
+    extra = [g.input("rope_table", (seq, hd // 2, 2), "f32", init=("rope", 10000.0))] if rope else []
+    gr = g.kernel("grad", {"type": "attention_bwd", "args": [q, k, qkv, o, dout] + extra, "heads": H, "seq": seq, "hd": hd,
                            "scale": hd ** -0.5, "causal": causal, "v_off": 2 * w, "v_ld": 3 * w, "ldo": w,
                            "do_ld": w}, (seq * 3 * w + 2 * H * seq,), "bf16")
     g.kernel("o_copy", dict(g.vertices[o]["op"]), (seq * w + 2 * H * seq,), "bf16")  # O + lse as an output
     return g, o, gr
 
 
-@pytest.mark.parametrize("seq,causal,sigma", [(256, 1, 1.0), (384, 1, 1.0), (512, 0, 1.0), (1024, 1, 2.0),
-                                              (256, 0, 4.0)])
-def test_fused_attention_bwd_parity(seq, causal, sigma):
-    """attention_bwd (tcgen05, both CTA roles) and the forward's logsumexp
-    output against the fp32 oracle; deterministic (bitwise equal reruns)."""
+@pytest.mark.parametrize("seq,causal,sigma,rope", [(256, 1, 1.0, False), (384, 1, 1.0, False), (512, 0, 1.0, False),
+                                                   (1024, 1, 2.0, False), (256, 0, 4.0, False), (384, 1, 1.0, True),
+                                                   (512, 0, 2.0, True)])
+def test_fused_attention_bwd_parity(seq, causal, sigma, rope):
+    """attention_bwd (tcgen05, both CTA roles; with a rope table dq / dk leave
+    the epilogue rotated back to pre-RoPE gradients) and the forward's
+    logsumexp output against the fp32 oracle; deterministic (bitwise equal
+    reruns)."""
     H, hd = 2, 128
     w = H * hd
-    g, o, gr = _attn_bwd_graph(seq, causal, sigma, H, hd)
+    g, o, gr = _attn_bwd_graph(seq, causal, sigma, H, hd, rope)
     mg, _ = W.plan(g, 1 << 30)
     inp = inputs_of(g, seed=17)
     _, got = run_gpu(g, mg, inp)
@@ -310,7 +314,7 @@ def test_fused_attention_bwd_parity(seq, causal, sigma):
     gw = as_f32(Gw.tobytes(), "bf16", n).reshape(seq, 3, w)
     for j, nm in enumerate(("dq", "dk", "dv")):
         e = rel_err(gg[:, j], gw[:, j])
-        record_err("attention_bwd", seq=seq, causal=causal, sigma=sigma, part=nm, rel_err=e)
+        record_err("attention_bwd", seq=seq, causal=causal, sigma=sigma, rope=rope, part=nm, rel_err=e)
         assert e < 1.2e-2, nm  # measured <= 5.5e-3 (sigma 4), bf16 P / dS operands
     D = np.frombuffer(got[gr], np.float32, count=H * seq, offset=n * 2)
     Dw = np.frombuffer(want[gr], np.float32, count=H * seq, offset=n * 2)
