@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.hpp"
@@ -71,6 +72,7 @@ struct AttnParams {
     std::int64_t ldo;
     float scale_log2;
     int causal;
+    long long* dbg;  // TN_ATTN_DBG timeline (pair kernel: cluster 0, its first item), else nullptr
 };
 
 // EMU of every 4 column pairs take 2^x on the FMA pipe (ex2_poly2), the rest
@@ -494,12 +496,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         const std::uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
                         if (j == 0 && itc[t] > 0) mbar_wait(o_empty + 8 * t, (itc[t] - 1) & 1);
                         const std::uint32_t pph = static_cast<std::uint32_t>(bt[t] + j) & 1;
+                        const bool dbgi = p.dbg && cl == 0 && n == 0 && j < 64;
+                        if (dbgi) p.dbg[(t * 64 + j) * 4 + 0] = clock64();
                         mbar_wait(p_full + 16 * t, pph);
+                        if (dbgi) p.dbg[(t * 64 + j) * 4 + 1] = clock64();
                         tc_fence_after();
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
                             tc_mma_ts_2sm(tO, tS + kk * 8, sdesc(dv + kk * 32), idesc_o, (j | kk) != 0);
                         mbar_wait(p_full + 16 * t + 8, pph);
+                        if (dbgi) p.dbg[(t * 64 + j) * 4 + 2] = clock64();
                         tc_fence_after();
 #pragma unroll
                         for (int kk = 4; kk < 8; ++kk)
@@ -546,7 +552,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             float m = -INFINITY, l = 0.f;
             constexpr int kW = 8;
             for (int j = 0; j < nk; ++j) {
+                const bool dbgs = p.dbg && cl == 0 && n == 0 && j < 64 && rank == 0 && (warp == 2 || warp == 6) && lane == 0;
+                long long* dp = dbgs ? p.dbg + 512 + (t * 64 + j) * 8 : nullptr;
+                if (dbgs) dp[0] = clock64();
                 mbar_wait(sf, (bt + j) & 1);
+                if (dbgs) dp[1] = clock64();
                 tc_fence_after();
                 float s[CW];
 #pragma unroll
@@ -557,6 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(u[i]);
                 }
                 tc_wait_ld();
+                if (dbgs) dp[2] = clock64();
                 const int lim = p.causal ? qrow - j * kN2 : CW;  // columns c <= lim are valid
                 float pm[kW];
 #pragma unroll
@@ -576,6 +587,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 const bool grew = cand > m + 8.0f;
                 const float mx = grew ? cand : m;
                 const float corr = ex2(m - mx);
+                if (dbgs) dp[3] = clock64();
                 float ps[kW];
 #pragma unroll
                 for (int w = 0; w < kW; ++w) ps[w] = 0.f;
@@ -614,12 +626,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_remote(pf0);
+                        if (dbgs) dp[4] = clock64();
                     }
                 }
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_remote(pf1);
+                if (dbgs) dp[5] = clock64();
 #pragma unroll
                 for (int w = kW / 2; w > 0; w /= 2)
 #pragma unroll
@@ -767,16 +781,36 @@ cudaError_t attention_launch(const AttnPlan& plan, cudaStream_t s) {
     p.ldo = a.ldo;
     p.scale_log2 = sl2;
     p.causal = a.causal;
+    p.dbg = nullptr;
+    // TN_ATTN_DBG=<file>: per-block clock64 timeline of the pair kernel (cluster 0,
+    // first item) appended to <file>; synchronises after the launch (diagnostics
+    // only; tools/attn_timeline.py reads it)
+    static const char* dbg_env = std::getenv("TN_ATTN_DBG");
+    static long long* dbg_buf = nullptr;
+    if (dbg_env && plan.path == 2) {
+        if (!dbg_buf) cudaMalloc(&dbg_buf, 4096 * sizeof(long long));
+        cudaMemsetAsync(dbg_buf, 0, 4096 * sizeof(long long), s);
+        p.dbg = dbg_buf;
+    }
     static const char* emu_env = std::getenv("TN_ATTN_EMU");  // A/B: "0" keeps every 2^x on MUFU
     const bool emu0 = emu_env && std::atoi(emu_env) == 0;
     if (plan.path == 2) {
         p.nblk = (a.seq + 511) / 512;
         const unsigned grid2 = static_cast<unsigned>(plan.grid);
-        if (emu0)
-            return launch_pdl(attention_kernel_2sm<0>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq, plan.tk,
-                              plan.tv2, p);
-        return launch_pdl(attention_kernel_2sm<1>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq, plan.tk, plan.tv2,
-                          p);
+        cudaError_t e = emu0 ? launch_pdl(attention_kernel_2sm<0>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq,
+                                          plan.tk, plan.tv2, p)
+                             : launch_pdl(attention_kernel_2sm<1>, dim3(grid2), dim3(kThreads2), kSmem2, s, plan.tq,
+                                          plan.tk, plan.tv2, p);
+        if (p.dbg && e == cudaSuccess) {
+            static long long host[4096];
+            cudaMemcpyAsync(host, p.dbg, sizeof(host), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            if (FILE* f = std::fopen(dbg_env, "a")) {
+                for (int i = 0; i < 4096; ++i) std::fprintf(f, "%lld%c", host[i], i == 4095 ? '\n' : ' ');
+                std::fclose(f);
+            }
+        }
+        return e;
     }
     const unsigned grid = p.heads * p.nblk;
     if (emu0)
