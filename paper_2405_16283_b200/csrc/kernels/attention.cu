@@ -375,6 +375,44 @@ __device__ __forceinline__ bool pair_item(const AttnParams& p, int c, int nc, in
     return true;
 }
 
+// Four K=16 pair MMAs from one elected lane: D (+)= A_k·B_k for k = 0..3,
+// the smem descriptors advanced by 32 bytes (2 units) per k; A from smem (SS)
+// or from TMEM (TS: 8 columns of packed bf16 per k). One elect per group
+// instead of one per MMA: the issuer warp shares its sub-partition with two
+// softmax warps, and the per-MMA elect / vote / uniform-register setup (~12
+// issue slots each, ~470 per block) made those two the last to hand P over,
+// ~400 clk after the others (TN_ATTN_DBG, profiles/r2d_attention_timeline.md).
+__device__ __forceinline__ void mma4_ss_2sm(std::uint32_t d, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                            std::uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b32 r;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, t;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc0)
+        : "memory");
+}
+__device__ __forceinline__ void mma4_ts_2sm(std::uint32_t d, std::uint32_t a, std::uint64_t b, std::uint32_t idesc,
+                                            std::uint32_t acc0) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b32 r, a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, %4, %4;\n\t"
+        "add.s32 a1, %1, 8;\n\tadd.s32 a2, %1, 16;\n\tadd.s32 a3, %1, 24;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, t;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, t;\n\t}" ::"r"(d),
+        "r"(a), "l"(b), "r"(idesc), "r"(acc0)
+        : "memory");
+}
+
 template <int EMU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     attention_kernel_2sm(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -464,11 +502,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             const std::uint32_t idesc_s = make_idesc(1u, 2 * kB, kN2);
             const std::uint32_t idesc_o = make_idesc(1u, 2 * kB, kHd);
             auto issue_s = [&](int t, int st) {
-                const std::uint32_t dk = sK0 + st * kKh, q = sQ + t * kQ;
-#pragma unroll
-                for (int kk = 0; kk < kHd / 16; ++kk)
-                    tc_mma_2sm(tmem + t * 128, sdesc(q + (kk >> 2) * (kQ / 2) + (kk & 3) * 32),
-                               sdesc(dk + (kk >> 2) * (kKh / 2) + (kk & 3) * 32), idesc_s, kk != 0, false);
+                const std::uint64_t qa = sdesc(sQ + t * kQ), kb = sdesc(sK0 + st * kKh);
+                mma4_ss_2sm(tmem + t * 128, qa, kb, idesc_s, 0);  // head dims [0, 64)
+                mma4_ss_2sm(tmem + t * 128, qa + (kQ / 2 >> 4), kb + (kKh / 2 >> 4), idesc_s, 1);  // [64, 128)
                 tc_commit_2sm(s_full + 8 * t);
             };
             int st = 0;
@@ -501,15 +537,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         mbar_wait(p_full + 16 * t, pph);
                         if (dbgi) p.dbg[(t * 64 + j) * 4 + 1] = clock64();
                         tc_fence_after();
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            tc_mma_ts_2sm(tO, tS + kk * 8, sdesc(dv + kk * 32), idesc_o, (j | kk) != 0);
+                        const std::uint64_t vb = sdesc(dv);
+                        mma4_ts_2sm(tO, tS, vb, idesc_o, j != 0);  // keys [0, 64)
                         mbar_wait(p_full + 16 * t + 8, pph);
-                        if (dbgi) p.dbg[(t * 64 + j) * 4 + 2] = clock64();
+                        if (dbgi) {
+                            p.dbg[(t * 64 + j) * 4 + 2] = clock64();
+                            long long gt;
+                            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+                            p.dbg[(t * 64 + j) * 4 + 3] = gt;
+                        }
                         tc_fence_after();
-#pragma unroll
-                        for (int kk = 4; kk < 8; ++kk)
-                            tc_mma_ts_2sm(tO, tS + kk * 8, sdesc(dv + kVh / 2 + (kk & 3) * 32), idesc_o, 1);
+                        mma4_ts_2sm(tO, tS + 32, vb + (kVh / 2 >> 4), idesc_o, 1);  // keys [64, 128)
                         if (j + 1 == it.nkv_t[t]) tc_commit_2sm(o_full + 8 * t);
                         if (j + 1 < it.nkv_t[t]) {
                             if (!kwaited) {
@@ -634,6 +672,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive_remote(pf1);
                 if (dbgs) dp[5] = clock64();
+                if (p.dbg && cl == 0 && n == 0 && j < 64 && lane == 0) {  // every softmax warp: P_B hand-off
+                    long long gt;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+                    const int w = (warp - 2) % 4, slot = (t * 64 + j) * 8 + static_cast<int>(rank) * 4 + w;
+                    p.dbg[1536 + slot] = gt;                      // ns, comparable across the pair
+                    if (rank == 0) p.dbg[2560 + (t * 64 + j) * 4 + w] = clock64();  // leader SM clock
+                }
 #pragma unroll
                 for (int w = kW / 2; w > 0; w /= 2)
 #pragma unroll
