@@ -348,6 +348,21 @@ __device__ __forceinline__ void stage_chunk(const Params& p, const CUtensorMap* 
     }
 }
 
+// Residual epilogues read R in 64-byte pieces of each lane's row, one
+// 32-column chunk at a time: 32 rows x 64 B per warp load, each piece in a
+// different DRAM page, each row's page reopened once per chunk. Pulling the
+// lane's whole row segment (w columns, contiguous) into L2 before the tile's
+// accumulator is ready turns that into one burst per row and overlaps it
+// with the tile's MMAs (C = U·Bᵀ + base at K = 64, 4096 x 22016: 136 -> 111 us
+// with the prefetch at the start of the epilogue; no residual 53 us).
+__device__ __forceinline__ void prefetch_residual(const Params& p, std::int64_t off, int n0, int w, bool row_ok) {
+    if (!p.R || p.epi != 0 || !row_ok || n0 >= p.N) return;
+    const int es = p.out_dtype == BF16 ? 2 : 4;
+    const char* rb = static_cast<const char*>(p.R) + (off + n0) * es;
+    const int nb = min(w, p.N - n0) * es;
+    for (int b = 0; b < nb; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + b));
+}
+
 // Plain epilogue through the stager: 128-row x width accumulator slab.
 __device__ __forceinline__ void epilogue_plain_tma(const Params& p, const CUtensorMap* tc, Stager& st,
                                                    std::uint32_t tbase, std::int64_t off, int row0, int n0, int width,
@@ -1034,6 +1049,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const bool row_ok = row < p.M;
             const float alpha = row_alpha(p, row, row_ok);  // before the wait: overlaps this tile's MMAs
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+            if (kb0 == 0) prefetch_residual(p, off, n0, w, row_ok);
             mbar_wait(tfull + 8 * acc, acc_phase);
             tc_fence_after();
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + acc * BN;
@@ -1337,6 +1353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsW, 1)
             const bool row_ok = row < p.M;
             const float alpha = row_alpha(p, row, row_ok);  // before the wait: overlaps this tile's MMAs
             const std::int64_t off = static_cast<std::int64_t>(b) * p.sc + static_cast<std::int64_t>(row) * p.ldc;
+            prefetch_residual(p, off, nb * BN + k * w, w, row_ok);
             mbar_wait(tfull, tphase);
             tc_fence_after();
             const std::uint32_t tbase = tmem + (static_cast<std::uint32_t>(lane_base) << 16) + h * 256;
