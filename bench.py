@@ -389,6 +389,45 @@ def roofline_from_trace(g, trace, peak_tflops):
             "gemm_device_s_per_step": round(dur, 6), "gemm_classes": by_class}, by_type
 
 
+def attention_roofline(g, trace, peak_tflops):
+    """The fused attention task in the traced step (the kernel the round-1
+    verdict named furthest below its roofline): FLOP per launch =
+    4·H·S²·hd (×½(1 + 1/S) causal, attention_flops in attention.cu) over its
+    CUDA-event duration; algorithmic bytes = q, k, vᵀ read and O written once;
+    DRAM traffic from the committed ncu capture of the same kernel."""
+    ids = {v["id"]: v for v in g.vertices}
+    fl = dur = 0.0
+    n = 0
+    alg = 0
+    for r in trace["rows"]:
+        v = ids.get(r["vertex"])
+        op = (v or {}).get("op") or {}
+        if op.get("type") != "attention":
+            continue
+        H, S, hd = op["heads"], op["seq"], op["hd"]
+        f = 4.0 * H * S * S * hd
+        fl += f * 0.5 * (1 + 1 / S) if op.get("causal") else f
+        dur += r["end"] - r["start"]
+        n += 1
+        alg += 4 * H * S * hd * 2
+    if n == 0 or dur <= 0:
+        return None
+    ach = fl / dur / 1e12
+    traffic, src = None, None
+    for name in ("r2e_ncu_attention.json", "r2b_ncu_attention_pair.json"):
+        try:
+            ls = json.load(open(os.path.join(ROOT, "profiles", name)))["launches"]
+            traffic, src = round(sum(x["dram_bytes"] for x in ls) / len(ls)), f"profiles/{name}"
+            break
+        except Exception:
+            continue
+    return {"kernel": "attention_kernel_2sm (fused causal attention, CTA pairs)", "bound": "tensor",
+            "achieved": round(ach, 1), "peak": peak_tflops, "unit": "TFLOP/s", "frac": round(ach / peak_tflops, 4),
+            "launches_per_step": n, "device_s_per_step": round(dur, 6),
+            "algorithmic_bytes_per_launch": alg // n, "traffic": traffic, "traffic_source": src,
+            "note": "steady state 2,048 clk of MMAs per 2,900-clk block (profiles/r2d_attention_timeline.md)"}
+
+
 def gemm_bytes(g, v) -> int:
     """Algorithmic HBM bytes of one GEMM task: its operands and its output,
     each touched once (A, B, optional residual/rope table, C)."""
@@ -867,6 +906,7 @@ def run_ours_on(args, world, rank, local, n, tp):
     value = tokens / t_value
     e2e = tokens / t_e2e
     roof, by_type = roofline_from_trace(g, last, pk["bf16_tflops_sustained"])
+    roof["attention"] = attention_roofline(g, last, pk["bf16_tflops_sustained"])
     flops = (W.prefill_flops(cfg, args.seq, args.layers) if not tp else st_v["flops"])
     gpus = len(set(devs))
     step_compute = flops / (gpus * pk["bf16_tflops_sustained"] * 1e12)
