@@ -1,2 +1,2 @@
-for e in 1 2 0 1 2; do TN_ATTN_EMU=$e timeout 120 python tools/attn_bench.py --reps 8 --runs 3 2>&1 | tail -1; done
-TN_ATTN_EMU=2 timeout 300 python -m pytest tests/test_gpu_exec.py -m gpu -q -x -k "fused_attention_parity" 2>&1 | tail -1
+for r in 1 2; do for e in 1 2 3 0; do TN_ATTN_EMU=$e python tools/attn_bench.py | sed "s/^/emu$e /"; done; done > gpurun_out/attn_emu.txt 2>&1
+for e in 1 2; do TN_ATTN_EMU=$e python tools/attn_bench.py --causal 0 | sed "s/^/nc emu$e /"; done >> gpurun_out/attn_emu.txt 2>&1
