@@ -23,6 +23,23 @@ def test_roofline_from_trace_counts_gemm_flops_and_bytes():
     assert by_type["gemm"] == pytest.approx(1e-3 * len(gemms))
 
 
+def test_attention_roofline_flops_and_bytes():
+    cfg = W.LlamaConfig(dim=512, layers=2, heads=4, ffn=1024, vocab=1000)
+    S = 256
+    g = W.llama_prefill(cfg, S)
+    rows = [{"vertex": v["id"], "start": 0.0, "end": 1e-9} for v in g.vertices]  # TF/s rounded to 0.1
+    att = bench.attention_roofline(g, {"rows": rows}, 1000.0)
+    assert att["launches_per_step"] == cfg.layers
+    hd = cfg.dim // cfg.heads
+    per = 4.0 * cfg.heads * S * S * hd * 0.5 * (1 + 1 / S)  # causal
+    assert att["achieved"] == pytest.approx(per / 1e-9 / 1e12, rel=1e-3)
+    assert att["frac"] == pytest.approx(att["achieved"] / 1000.0, rel=1e-3)
+    assert att["algorithmic_bytes_per_launch"] == 4 * cfg.heads * S * hd * 2  # q, k, vT in; O out
+    no_attn = W.GraphBuilder()
+    no_attn.input("x", (4, 4), "bf16")
+    assert bench.attention_roofline(no_attn, {"rows": []}, 1000.0) is None
+
+
 def test_planner_parity_leg_is_byte_identical():
     if not os.path.isdir(os.path.join(bench.ROOT, "oracle", "_ref")):
         pytest.skip("oracle/_ref not built")
