@@ -439,7 +439,7 @@ def gemm_traffic():
     """DRAM bytes per GEMM launch from the committed `ncu --set full` capture
     of one layer's four GEMM classes (each class is 1/4 of the step's GEMM
     launches, so the plain mean is the per-launch average)."""
-    for name in ("r2_ncu_gemm.json", "r1_ncu_gemm.json"):
+    for name in ("r2g_ncu_gemm.json", "r2_ncu_gemm.json", "r1_ncu_gemm.json"):
         p = os.path.join(ROOT, "profiles", name)
         try:
             ls = json.load(open(p))["launches"]

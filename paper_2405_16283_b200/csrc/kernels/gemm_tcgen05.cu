@@ -356,7 +356,11 @@ __device__ __forceinline__ void stage_chunk(const Params& p, const CUtensorMap* 
 // with the tile's MMAs (C = U·Bᵀ + base at K = 64, 4096 x 22016: 136 -> 111 us
 // with the prefetch at the start of the epilogue; no residual 53 us).
 __device__ __forceinline__ void prefetch_residual(const Params& p, std::int64_t off, int n0, int w, bool row_ok) {
-    if (!p.R || p.epi != 0 || !row_ok || n0 >= p.N) return;
+    // Only short-K GEMMs, whose tiles are epilogue-bound: with a long K the
+    // residual read overlaps the next tile's main loop anyway, and the early
+    // lines crowd A/B out of L2 (ncu DRAM per launch: ffn_out 333 -> 365 MB,
+    // attn_out 146 -> 167 MB with the prefetch on every residual GEMM).
+    if (!p.R || p.epi != 0 || !row_ok || n0 >= p.N || p.K > 1024) return;
     const int es = p.out_dtype == BF16 ? 2 : 4;
     const char* rb = static_cast<const char*>(p.R) + (off + n0) * es;
     const int nb = min(w, p.N - n0) * es;
